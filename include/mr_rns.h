@@ -1,0 +1,137 @@
+/*
+ * mr_rns.h — C ABI of the B200-native MR-MOD / MR-RSA hot path of Chauvet & Mahé,
+ * "Secrets from the GPU" (arXiv:1305.3699).  Citations: PAPER.md line numbers (P:n), section in
+ * brackets; readings (R#) where the paper is silent.
+ *
+ * What the library computes (the paper's MR-MOD layer, §3.1, and the MR-RSA kernels,
+ * P:50-56 §3.2-§3.3): batched modular exponentiation x^E mod N where every bignum lives in the
+ * Residue Number System over two 32-bit prime bases B, B' plus the extra modulus m_r = 2^32,
+ * and every multiply is an RNS Montgomery multiplication with R = M = prod(B) ([Bajard2001])
+ * whose two base extensions B -> B' ∪ {m_r} and B' -> B carry all cross-channel work.  The results
+ * are exact integers: bit-identical to x^E mod N computed any other way.
+ *
+ * Conventions shared by every entry point
+ *  - Big integers are little-endian arrays of uint32_t limbs, fixed width per call (R16).
+ *  - Batch buffers (d_*) are DEVICE pointers owned by the caller (e.g. torch tensors), row-major
+ *    [count][limbs], 4-byte aligned (16-byte alignment is faster).  Host pointers are marked HOST.
+ *  - Every batch call is asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *    default stream) and returns after enqueuing.  The return code reports host-detectable problems
+ *    only (arguments, capacity, launch failure) and never synchronises the device.
+ *  - Per-message data errors go to d_status[i] (nullable): MR_OK, or MR_ERR_RANGE when the input is
+ *    >= its bound, in which case that output is zero-filled.
+ *  - count = 0 is MR_OK and launches nothing.
+ *  - Contexts are immutable after creation and may be used concurrently from any host thread or
+ *    stream.  Scratch memory is allocated stream-ordered (cudaMallocAsync) inside each call.
+ *  - There is no CPU fallback: on a machine without a usable CUDA device every call returns
+ *    MR_ERR_CUDA.
+ */
+#ifndef MR_RNS_H
+#define MR_RNS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mr_rns_ctx mr_rns_ctx;   /* modulus N + base pair (B, B', m_r) + device constants */
+typedef struct mr_rsa_priv mr_rsa_priv; /* RSA private key for CRT decryption (two half contexts) */
+
+enum {
+    MR_OK = 0,
+    MR_ERR_ARG = 1,          /* null pointer, bad size, unsupported k, exponent/limb count invalid */
+    MR_ERR_EVEN_MODULUS = 2, /* N even or N < 3: R = M is odd, so Montgomery needs N odd */
+    MR_ERR_NOT_COPRIME = 3,  /* N shares a prime with B ∪ B' (gcd(N, M M') != 1)                  */
+    MR_ERR_CAPACITY = 4,     /* N too large for the requested k (bound of DESIGN.md §3, R5)        */
+    MR_ERR_RANGE = 5,        /* per-message: input >= bound                                        */
+    MR_ERR_CUDA = 6,         /* CUDA runtime error or no device                                    */
+    MR_ERR_NOMEM = 7         /* host or device allocation failed                                   */
+};
+
+enum { MR_COMPOSITE = 0, MR_PROBABLY_PRIME = 1, MR_FACTOR = 2 }; /* Miller-Rabin verdicts */
+
+/* ------------------------------------------------------------------------------------------
+ * mr_rns_ctx_create — precompute and install the RNS/Montgomery constants for modulus N.
+ *   "these constants are pre-computed and installed permanently in GPU memory at initialization
+ *    time" (§3.1).
+ * modulus: HOST, `limbs` limbs, odd, N >= 3.
+ * k: channels per base.  0 = auto = the smallest compiled k with 4(k+3)^2 N < M and
+ *    4(k+3) N < M' (e.g. 33 for 1024-bit, 65 for 2048-bit N).  A nonzero k is rounded up to the
+ *    next compiled k (see mr_rns_supported_k); below the bound -> MR_ERR_CAPACITY.
+ * device: CUDA ordinal that will run every batch call on this context.
+ * On success *out owns host and device memory until mr_rns_ctx_destroy.
+ * Errors: MR_ERR_ARG, MR_ERR_EVEN_MODULUS, MR_ERR_NOT_COPRIME, MR_ERR_CAPACITY, MR_ERR_CUDA,
+ *         MR_ERR_NOMEM.  *out is NULL on error.
+ * ------------------------------------------------------------------------------------------ */
+int mr_rns_ctx_create(mr_rns_ctx **out, const uint32_t *modulus, size_t limbs, int k, int device);
+void mr_rns_ctx_destroy(mr_rns_ctx *ctx);
+
+/* k actually used, limbs of N, bits(N), and the paper's nominal key-size cap k*31 bits for k
+ * 32-bit primes ("128 32-bit prime integers, sufficient for RSA keys up to 3,968-bit"; R4).
+ * Any out pointer may be NULL. */
+int mr_rns_ctx_info(const mr_rns_ctx *ctx, int *k, size_t *limbs, int *modulus_bits, int *paper_cap_bits);
+
+/* Writes up to `cap` compiled channel counts k (ascending) into ks (HOST); returns how many exist. */
+int mr_rns_supported_k(int *ks, int cap);
+
+/* ------------------------------------------------------------------------------------------
+ * mr_modexp_batch — d_y[i] = d_x[i]^E mod N for i < count (§3.1: "exponentiation,
+ * implemented with traditional square-and-multiply algorithms ... chaining Montgomery modular
+ * multiplications"; here a sliding window, reading R6).
+ * d_x, d_y: DEVICE [count][limbs(N)].  d_x[i] must be < N, else d_status[i] = MR_ERR_RANGE and
+ *           d_y[i] = 0.  d_y may alias d_x.
+ * exp: HOST, exp_limbs limbs, shared by the whole batch; any length (R7: exponents longer than N
+ *      are computed literally); E = 0 gives 1.
+ * d_status: DEVICE int32 [count] or NULL.
+ * ------------------------------------------------------------------------------------------ */
+int mr_modexp_batch(const mr_rns_ctx *ctx, const uint32_t *d_x, uint32_t *d_y, size_t count,
+                    const uint32_t *exp, size_t exp_limbs, int32_t *d_status, void *stream);
+
+/* mr_rsa_encrypt_batch — c = m^e mod N (§3.3 "two GPU kernels respectively for encryption
+ * and decryption of messages, applying modular exponentiation").  Same contract as
+ * mr_modexp_batch with E = e. */
+int mr_rsa_encrypt_batch(const mr_rns_ctx *n_ctx, const uint32_t *e, size_t e_limbs, const uint32_t *d_m,
+                         uint32_t *d_c, size_t count, int32_t *d_status, void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * mr_rsa_priv_create — private key for CRT decryption (north_star; Garner recombination, HAC 14.71;
+ * the paper mentions p/q splitting only in related work).
+ * p, q, d_p = d mod (p-1), d_q = d mod (q-1), q_inv = q^-1 mod p: HOST, half_limbs limbs each.
+ * The two half contexts share one base pair; k_half = 0 picks it automatically.
+ * Ciphertexts and plaintexts of mr_rsa_decrypt_batch have 2*half_limbs limbs and must be < p*q.
+ * Errors as mr_rns_ctx_create, plus MR_ERR_ARG if p == q or q_inv*q != 1 mod p.
+ * ------------------------------------------------------------------------------------------ */
+int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, size_t half_limbs,
+                       const uint32_t *d_p, const uint32_t *d_q, const uint32_t *q_inv, int k_half, int device);
+void mr_rsa_priv_destroy(mr_rsa_priv *priv);
+
+/* mr_rsa_decrypt_batch — d_m[i] = d_c[i]^d mod pq by CRT: m_p = c^d_p mod p, m_q = c^d_q mod q
+ * (two half-size RNS ladders in one launch), h = q_inv (m_p - m_q) mod p, m = m_q + q h.
+ * d_c, d_m: DEVICE [count][2*half_limbs]; d_c[i] >= pq -> MR_ERR_RANGE.  d_m may alias d_c. */
+int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t *d_m, size_t count,
+                         int32_t *d_status, void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * mr_miller_rabin_batch — Miller-Rabin in the Montgomery domain, one candidate per message
+ * ("primality testing in the Montgomery domain has been implemented as a dedicated GPU kernel ...
+ *  a Miller-Rabin test with a user-parameterized number of iterations", §3.2; HAC 4.24).
+ * d_n: DEVICE [count][limbs] candidates; d_bases: DEVICE [count][rounds][limbs], each in [2, n-2]
+ *      (bases are inputs, reading R13).
+ * k: channels (0 = auto from limbs).  d_verdict: DEVICE uint8 [count] = MR_COMPOSITE |
+ * MR_PROBABLY_PRIME | MR_FACTOR (n > 2^32 divisible by a prime of B ∪ B', R14).
+ * d_witness_round: DEVICE int16 [count] or NULL: first round that proved compositeness, else -1.
+ * d_status: DEVICE int32 [count] or NULL: MR_ERR_RANGE if n even, n < 5 or a base outside
+ *           [2, n-2]; MR_ERR_NOT_COPRIME if n < 2^32 is itself a base prime.
+ * ------------------------------------------------------------------------------------------ */
+int mr_miller_rabin_batch(const uint32_t *d_n, size_t limbs, size_t count, const uint32_t *d_bases, int rounds,
+                          int k, uint8_t *d_verdict, int16_t *d_witness_round, int32_t *d_status, int device,
+                          void *stream);
+
+/* Human-readable name of an MR_* code (static storage). */
+const char *mr_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MR_RNS_H */

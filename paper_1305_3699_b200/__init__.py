@@ -1,0 +1,261 @@
+"""B200-native batched RNS-Montgomery RSA (arXiv:1305.3699, MR-MOD / MR-RSA hot path).
+
+Thin ctypes binding of ``libmr_rns.so`` (C ABI: ``include/mr_rns.h``).  Same entry-point names as
+the C header; argument marshalling only — every step of the path runs in the CUDA kernels of
+``csrc/``.  There is no CPU fallback: if the shared library is missing or no CUDA device is usable,
+calls raise.
+
+Device buffers are ``torch`` CUDA tensors of dtype int32 whose bits are the uint32 limbs
+(little-endian, row-major ``[count][limbs]``); the current torch stream of the tensor's device is
+used unless ``stream`` is given.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "lib", "MrError", "MR_OK", "MR_ERR_RANGE", "MR_COMPOSITE", "MR_PROBABLY_PRIME", "MR_FACTOR",
+    "mr_rns_ctx_create", "mr_rns_ctx_destroy", "mr_rns_ctx_info", "mr_rns_supported_k",
+    "mr_modexp_batch", "mr_rsa_encrypt_batch", "mr_rsa_priv_create", "mr_rsa_priv_destroy",
+    "mr_rsa_decrypt_batch", "mr_miller_rabin_batch", "mr_strerror",
+    "RnsContext", "RsaPrivateKey", "limbs_of", "ints_to_limbs", "limbs_to_ints",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmr_rns.so")
+
+MR_OK, MR_ERR_ARG, MR_ERR_EVEN_MODULUS, MR_ERR_NOT_COPRIME = 0, 1, 2, 3
+MR_ERR_CAPACITY, MR_ERR_RANGE, MR_ERR_CUDA, MR_ERR_NOMEM = 4, 5, 6, 7
+MR_COMPOSITE, MR_PROBABLY_PRIME, MR_FACTOR = 0, 1, 2
+
+EXPORTS = (
+    "mr_rns_ctx_create", "mr_rns_ctx_destroy", "mr_rns_ctx_info", "mr_rns_supported_k", "mr_modexp_batch",
+    "mr_rsa_encrypt_batch", "mr_rsa_priv_create", "mr_rsa_priv_destroy", "mr_rsa_decrypt_batch",
+    "mr_miller_rabin_batch", "mr_strerror",
+)
+
+
+class MrError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        super().__init__(f"{what}: {mr_strerror(code)} (code {code})" if what else mr_strerror(code))
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libmr_rns.so (raises if it has not been built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1305_3699_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+        ip = ctypes.POINTER(ctypes.c_int)
+        up = ctypes.POINTER(ctypes.c_uint32)
+        L.mr_rns_ctx_create.argtypes = [ctypes.POINTER(vp), up, sz, i32, i32]
+        L.mr_rns_ctx_destroy.argtypes = [vp]
+        L.mr_rns_ctx_destroy.restype = None
+        L.mr_rns_ctx_info.argtypes = [vp, ip, ctypes.POINTER(sz), ip, ip]
+        L.mr_rns_supported_k.argtypes = [ip, i32]
+        L.mr_modexp_batch.argtypes = [vp, vp, vp, sz, up, sz, vp, vp]
+        L.mr_rsa_encrypt_batch.argtypes = [vp, up, sz, vp, vp, sz, vp, vp]
+        L.mr_rsa_priv_create.argtypes = [ctypes.POINTER(vp), up, up, sz, up, up, up, i32, i32]
+        L.mr_rsa_priv_destroy.argtypes = [vp]
+        L.mr_rsa_priv_destroy.restype = None
+        L.mr_rsa_decrypt_batch.argtypes = [vp, vp, vp, sz, vp, vp]
+        L.mr_miller_rabin_batch.argtypes = [vp, sz, sz, vp, i32, i32, vp, vp, vp, i32, vp]
+        L.mr_strerror.argtypes = [i32]
+        L.mr_strerror.restype = ctypes.c_char_p
+        for name in EXPORTS:
+            if name not in ("mr_rns_ctx_destroy", "mr_rsa_priv_destroy", "mr_strerror"):
+                getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+# ------------------------------------------------------------------ marshalling helpers (I/O only)
+
+def limbs_of(x: int, n: int) -> np.ndarray:
+    """little-endian uint32 limbs of a non-negative int, fixed width n."""
+    if x < 0 or x >> (32 * n):
+        raise ValueError("value does not fit in %d limbs" % n)
+    return np.frombuffer(x.to_bytes(4 * n, "little"), dtype=np.uint32).copy()
+
+
+def ints_to_limbs(values: Sequence[int], n: int) -> np.ndarray:
+    out = np.zeros((len(values), n), dtype=np.uint32)
+    for i, v in enumerate(values):
+        out[i] = limbs_of(int(v), n)
+    return out
+
+
+def limbs_to_ints(a) -> list[int]:
+    a = np.ascontiguousarray(_to_numpy(a), dtype=np.uint32)
+    return [int.from_bytes(row.tobytes(), "little") for row in a]
+
+
+def _to_numpy(a):
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            return a.detach().cpu().numpy().view(np.uint32)
+    except ImportError:
+        pass
+    return np.asarray(a)
+
+
+def _hp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+def _dptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise MrError(MR_ERR_ARG, "device buffers must be CUDA tensors (no CPU fallback)")
+    if not t.is_contiguous():
+        raise MrError(MR_ERR_ARG, "device buffers must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(t, stream) -> Optional[int]:
+    if stream is not None:
+        return getattr(stream, "cuda_stream", stream)
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != MR_OK:
+        raise MrError(rc, what)
+
+
+# ------------------------------------------------------------------ C ABI, same names
+
+def mr_strerror(code: int) -> str:
+    return lib().mr_strerror(code).decode()
+
+
+def mr_rns_supported_k() -> list[int]:
+    buf = (ctypes.c_int * 64)()
+    n = lib().mr_rns_supported_k(buf, 64)
+    return list(buf[:n])
+
+
+def mr_rns_ctx_create(modulus: int, limbs: int, k: int = 0, device: int = 0) -> ctypes.c_void_p:
+    m = limbs_of(modulus, limbs)
+    h = ctypes.c_void_p()
+    _check(lib().mr_rns_ctx_create(ctypes.byref(h), _hp(m), limbs, k, device), "mr_rns_ctx_create")
+    return h
+
+
+def mr_rns_ctx_destroy(ctx) -> None:
+    lib().mr_rns_ctx_destroy(ctx)
+
+
+def mr_rns_ctx_info(ctx) -> dict:
+    k, bits, cap = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    limbs = ctypes.c_size_t()
+    _check(lib().mr_rns_ctx_info(ctx, ctypes.byref(k), ctypes.byref(limbs), ctypes.byref(bits), ctypes.byref(cap)),
+           "mr_rns_ctx_info")
+    return {"k": k.value, "limbs": limbs.value, "modulus_bits": bits.value, "paper_cap_bits": cap.value}
+
+
+def mr_modexp_batch(ctx, d_x, d_y, count: int, exp: int, d_status=None, stream=None) -> None:
+    e = limbs_of(exp, max(1, (exp.bit_length() + 31) // 32))
+    _check(lib().mr_modexp_batch(ctx, _dptr(d_x), _dptr(d_y), count, _hp(e), len(e) if exp else 0,
+                                 _dptr(d_status), _stream(d_x, stream)), "mr_modexp_batch")
+
+
+def mr_rsa_encrypt_batch(ctx, e: int, d_m, d_c, count: int, d_status=None, stream=None) -> None:
+    el = limbs_of(e, max(1, (e.bit_length() + 31) // 32))
+    _check(lib().mr_rsa_encrypt_batch(ctx, _hp(el), len(el) if e else 0, _dptr(d_m), _dptr(d_c), count,
+                                      _dptr(d_status), _stream(d_m, stream)), "mr_rsa_encrypt_batch")
+
+
+def mr_rsa_priv_create(p: int, q: int, half_limbs: int, d_p: int, d_q: int, q_inv: int, k_half: int = 0,
+                       device: int = 0) -> ctypes.c_void_p:
+    arrs = [limbs_of(v, half_limbs) for v in (p, q, d_p, d_q, q_inv)]
+    h = ctypes.c_void_p()
+    _check(lib().mr_rsa_priv_create(ctypes.byref(h), *[_hp(a) for a in arrs[:2]], half_limbs,
+                                    *[_hp(a) for a in arrs[2:]], k_half, device), "mr_rsa_priv_create")
+    return h
+
+
+def mr_rsa_priv_destroy(priv) -> None:
+    lib().mr_rsa_priv_destroy(priv)
+
+
+def mr_rsa_decrypt_batch(priv, d_c, d_m, count: int, d_status=None, stream=None) -> None:
+    _check(lib().mr_rsa_decrypt_batch(priv, _dptr(d_c), _dptr(d_m), count, _dptr(d_status), _stream(d_c, stream)),
+           "mr_rsa_decrypt_batch")
+
+
+def mr_miller_rabin_batch(d_n, limbs: int, count: int, d_bases, rounds: int, d_verdict, d_witness=None,
+                          d_status=None, k: int = 0, device: int = 0, stream=None) -> None:
+    _check(lib().mr_miller_rabin_batch(_dptr(d_n), limbs, count, _dptr(d_bases), rounds, k, _dptr(d_verdict),
+                                       _dptr(d_witness), _dptr(d_status), device, _stream(d_n, stream)),
+           "mr_miller_rabin_batch")
+
+
+# ------------------------------------------------------------------ RAII conveniences
+
+class RnsContext:
+    """Modulus N with its device-resident RNS constants (mr_rns_ctx)."""
+
+    def __init__(self, modulus: int, limbs: Optional[int] = None, k: int = 0, device: int = 0):
+        self.modulus = modulus
+        self.limbs = limbs or max(1, (modulus.bit_length() + 31) // 32)
+        self.device = device
+        self.handle = mr_rns_ctx_create(modulus, self.limbs, k, device)
+        self.info = mr_rns_ctx_info(self.handle)
+        self.k = self.info["k"]
+
+    def modexp(self, d_x, d_y, exp: int, d_status=None, stream=None, count: Optional[int] = None) -> None:
+        mr_modexp_batch(self.handle, d_x, d_y, d_x.shape[0] if count is None else count, exp, d_status, stream)
+
+    def encrypt(self, d_m, d_c, e: int, d_status=None, stream=None) -> None:
+        mr_rsa_encrypt_batch(self.handle, e, d_m, d_c, d_m.shape[0], d_status, stream)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            mr_rns_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RsaPrivateKey:
+    """RSA private key held for CRT decryption (mr_rsa_priv)."""
+
+    def __init__(self, p: int, q: int, dp: int, dq: int, qinv: int, half_limbs: Optional[int] = None,
+                 k_half: int = 0, device: int = 0):
+        """(p, q, dp = d mod (p-1), dq = d mod (q-1), qinv = q^-1 mod p): the PKCS#1 CRT key fields."""
+        self.half = half_limbs or max((p.bit_length() + 31) // 32, (q.bit_length() + 31) // 32)
+        self.limbs = 2 * self.half
+        self.device = device
+        self.handle = mr_rsa_priv_create(p, q, self.half, dp, dq, qinv, k_half, device)
+
+    def decrypt(self, d_c, d_m, d_status=None, stream=None) -> None:
+        mr_rsa_decrypt_batch(self.handle, d_c, d_m, d_c.shape[0], d_status, stream)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            mr_rsa_priv_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

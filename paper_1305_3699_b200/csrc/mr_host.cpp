@@ -1,0 +1,835 @@
+// mr_host.cpp — host runtime of the C ABI (include/mr_rns.h): base construction, constant
+// precomputation ("pre-computed and installed permanently in GPU memory at initialization time",
+// P:48 §3.1), exponent recoding into kernel programs (sliding window, reading R6), scratch
+// management and launches.  All bignum work here is library-internal positional helpers used only
+// for precomputation; it shares no code with oracle/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/mr_rns.h"
+#include "mr_internal.h"
+
+namespace mr {
+#define MR_DECLARE_K(k) KernelSet kernels_k##k();
+MR_DECLARE_K(1)
+MR_DECLARE_K(2)
+MR_DECLARE_K(3)
+MR_DECLARE_K(5)
+MR_DECLARE_K(9)
+MR_DECLARE_K(17)
+MR_DECLARE_K(33)
+MR_DECLARE_K(49)
+MR_DECLARE_K(65)
+
+static const KernelSet &kernel_set_for(int k) {
+    static std::vector<KernelSet> sets = {kernels_k1(),  kernels_k2(),  kernels_k3(),  kernels_k5(), kernels_k9(),
+                                          kernels_k17(), kernels_k33(), kernels_k49(), kernels_k65()};
+    for (const auto &s : sets)
+        if (s.k == k) return s;
+    return sets[0];
+}
+static const int kSupportedK[] = {1, 2, 3, 5, 9, 17, 33, 49, 65};
+static const int kNumK = sizeof(kSupportedK) / sizeof(kSupportedK[0]);
+
+// ------------------------------------------------------------------ host positional helpers
+typedef std::vector<u32> Big;  // little-endian limbs, trimmed (no high zero limbs)
+
+static void trim(Big &a) {
+    while (!a.empty() && a.back() == 0) a.pop_back();
+}
+static Big big_of(const u32 *p, size_t n) {
+    Big a(p, p + n);
+    trim(a);
+    return a;
+}
+static int cmp(const Big &a, const Big &b) {
+    if (a.size() != b.size()) return a.size() < b.size() ? -1 : 1;
+    for (size_t i = a.size(); i-- > 0;)
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    return 0;
+}
+static Big add(const Big &a, const Big &b) {
+    Big r(std::max(a.size(), b.size()) + 1, 0);
+    u64 c = 0;
+    for (size_t i = 0; i + 1 < r.size(); i++) {
+        u64 s = c + (i < a.size() ? a[i] : 0) + (i < b.size() ? b[i] : 0);
+        r[i] = (u32)s;
+        c = s >> 32;
+    }
+    r.back() = (u32)c;
+    trim(r);
+    return r;
+}
+static Big sub(const Big &a, const Big &b) {  // a >= b
+    Big r(a.size(), 0);
+    u64 br = 0;
+    for (size_t i = 0; i < a.size(); i++) {
+        u64 bi = (i < b.size() ? b[i] : 0) + br;
+        r[i] = (u32)((u64)a[i] - bi);
+        br = (u64)a[i] < bi;
+    }
+    trim(r);
+    return r;
+}
+static Big mul(const Big &a, const Big &b) {
+    if (a.empty() || b.empty()) return Big();
+    Big r(a.size() + b.size(), 0);
+    for (size_t i = 0; i < a.size(); i++) {
+        u64 c = 0;
+        for (size_t j = 0; j < b.size(); j++) {
+            u64 t = (u64)a[i] * b[j] + r[i + j] + c;
+            r[i + j] = (u32)t;
+            c = t >> 32;
+        }
+        r[i + b.size()] = (u32)c;
+    }
+    trim(r);
+    return r;
+}
+static Big mul_word(const Big &a, u32 w) { return mul(a, Big{w}); }
+static int bits(const Big &a) { return a.empty() ? 0 : 32 * (int)(a.size() - 1) + (32 - __builtin_clz(a.back())); }
+static int bit(const Big &a, int i) { return (a[i / 32] >> (i % 32)) & 1; }
+static Big mod(const Big &a, const Big &n) {  // bit-serial restoring reduction
+    Big r;
+    for (int i = bits(a) - 1; i >= 0; i--) {
+        r = add(r, r);
+        if (bit(a, i)) r = add(r, Big{1});
+        if (cmp(r, n) >= 0) r = sub(r, n);
+    }
+    return r;
+}
+static u32 mod_word(const Big &a, u32 m) {
+    u64 r = 0;
+    for (size_t i = a.size(); i-- > 0;) r = ((r << 32) | a[i]) % m;
+    return (u32)r;
+}
+static Big pow2(int e) {
+    Big r(e / 32 + 1, 0);
+    r[e / 32] = 1u << (e % 32);
+    return r;
+}
+
+// ------------------------------------------------------------------ word arithmetic
+static u32 mulm(u32 a, u32 b, u32 m) { return (u32)((u64)a * b % m); }
+static u32 powm(u32 a, u64 e, u32 m) {
+    u64 r = 1 % m, x = a % m;
+    while (e) {
+        if (e & 1) r = r * x % m;
+        x = x * x % m;
+        e >>= 1;
+    }
+    return (u32)r;
+}
+static u32 invp(u32 a, u32 p) { return powm(a % p, p - 2, p); }  // p prime (Fermat)
+static u32 inv32(u32 a) {                                        // a odd: a^-1 mod 2^32 (Newton)
+    u32 x = a;                                                   // correct to 3 bits
+    for (int i = 0; i < 5; i++) x *= 2 - a * x;
+    return x;
+}
+static bool is_prime32(u32 n) {  // deterministic Miller-Rabin for n < 2^32: bases 2, 7, 61
+    if (n < 2) return false;
+    for (u32 p : {2u, 3u, 5u, 7u, 11u, 13u, 61u})
+        if (n % p == 0) return n == p;
+    u32 d = n - 1;
+    int s = 0;
+    while (!(d & 1)) d >>= 1, s++;
+    for (u32 a : {2u, 7u, 61u}) {
+        u64 x = powm(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int r = 1; r < s; r++) {
+            x = x * x % n;
+            if (x == n - 1) { comp = false; break; }
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+// reading R1: B = the k largest primes below 2^32 (descending), B' = the next k
+static std::mutex g_mu;
+static std::vector<u32> g_primes;
+static const std::vector<u32> &primes_desc(size_t n) {
+    if (g_primes.size() < n) {
+        u32 w = g_primes.empty() ? 0xFFFFFFFFu : g_primes.back() - 1;
+        while (g_primes.size() < n) {
+            if (is_prime32(w)) g_primes.push_back(w);
+            w--;
+        }
+    }
+    return g_primes;
+}
+
+// ------------------------------------------------------------------ per-k base data
+struct Base {
+    int k = 0;
+    std::vector<u32> B, Bp;        // moduli
+    std::vector<u32> lambda;       // |M'_j^-1|_{m'_j}
+    std::vector<u32> mu;           // |M^-1|_{m'_j}
+    std::vector<u32> Mi_self;      // |M_i|_{m_i}
+    u32 M_r = 0, Mp_r = 0;         // M, M' mod 2^32
+    Big M, Mp;                     // products
+    std::vector<u32> flat;         // constant-bank image (BaseLayout)
+    std::vector<u32> pow;          // to_rns powers [k][2k]
+};
+static std::map<int, Base> g_bases;
+
+static const Base &base_for(int k) {
+    auto it = g_bases.find(k);
+    if (it != g_bases.end()) return it->second;
+    Base b;
+    b.k = k;
+    const std::vector<u32> &pr = primes_desc(2 * k);
+    b.B.assign(pr.begin(), pr.begin() + k);
+    b.Bp.assign(pr.begin() + k, pr.begin() + 2 * k);
+    b.M = Big{1};
+    b.Mp = Big{1};
+    for (u32 m : b.B) b.M = mul_word(b.M, m);
+    for (u32 m : b.Bp) b.Mp = mul_word(b.Mp, m);
+    b.M_r = b.M.empty() ? 0 : b.M[0];
+    b.Mp_r = b.Mp[0];
+    const BaseLayout L = base_layout(k);
+    b.flat.assign(L.words, 0);
+    u32 *f = b.flat.data();
+    for (int i = 0; i < k; i++) {
+        f[L.c + i] = 0u - b.B[i];
+        f[L.c + k + i] = 0u - b.Bp[i];
+    }
+    for (int ch = 0; ch < 2 * k; ch++) f[L.c2 + ch] = f[L.c + ch] * f[L.c + ch];
+    std::vector<u32> M_bp(k), Mp_b(k);
+    for (int j = 0; j < k; j++) M_bp[j] = mod_word(b.M, b.Bp[j]);
+    for (int i = 0; i < k; i++) Mp_b[i] = mod_word(b.Mp, b.B[i]);
+    b.lambda.resize(k);
+    b.mu.resize(k);
+    b.Mi_self.resize(k);
+    for (int j = 0; j < k; j++) {
+        u32 Mpj = 1;
+        for (int l = 0; l < k; l++)
+            if (l != j) Mpj = mulm(Mpj, b.Bp[l] % b.Bp[j], b.Bp[j]);
+        b.lambda[j] = invp(Mpj, b.Bp[j]);
+        b.mu[j] = invp(M_bp[j], b.Bp[j]);
+    }
+    for (int i = 0; i < k; i++) {
+        u32 Mi = 1;
+        for (int l = 0; l < k; l++)
+            if (l != i) Mi = mulm(Mi, b.B[l] % b.B[i], b.B[i]);
+        b.Mi_self[i] = Mi;
+    }
+    for (int i = 0; i < k; i++) {
+        for (int j = 0; j < k; j++) f[L.A1 + i * k + j] = mulm(M_bp[j], invp(b.B[i] % b.Bp[j], b.Bp[j]), b.Bp[j]);
+        f[L.A1r + i] = b.M_r * inv32(b.B[i]);
+    }
+    for (int j = 0; j < k; j++) {
+        for (int i = 0; i < k; i++) f[L.A2 + j * k + i] = mulm(Mp_b[i], invp(b.Bp[j] % b.B[i], b.B[i]), b.B[i]);
+        f[L.A2r + j] = b.Mp_r * inv32(b.Bp[j]);
+    }
+    for (int j = 0; j < k; j++) f[L.C1 + j] = mulm(b.mu[j], invp(b.lambda[j], b.Bp[j]), b.Bp[j]);
+    for (int i = 0; i < k; i++) f[L.pin + i] = (b.B[i] - Mp_b[i]) % b.B[i];
+    f[L.misc + 0] = inv32(b.M_r);
+    f[L.misc + 1] = inv32(b.Mp_r);
+    for (int j = 0; j < k; j++) {
+        Big Mpj{1};
+        for (int l = 0; l < k; l++)
+            if (l != j) Mpj = mul_word(Mpj, b.Bp[l]);
+        for (int l = 0; l <= k; l++) f[L.MpL + j * (k + 1) + l] = l < (int)Mpj.size() ? Mpj[l] : 0;
+    }
+    {
+        Big NMp = sub(pow2(32 * (k + 1)), b.Mp);
+        for (int l = 0; l <= k; l++) f[L.NMp + l] = l < (int)NMp.size() ? NMp[l] : 0;
+    }
+    b.pow.assign((size_t)k * 2 * k, 0);
+    for (int l = 0; l < k; l++) {
+        Big p2 = pow2(32 * l);
+        for (int i = 0; i < k; i++) b.pow[(size_t)l * 2 * k + i] = mod_word(p2, b.B[i]);
+        for (int j = 0; j < k; j++)
+            b.pow[(size_t)l * 2 * k + k + j] = mulm(mod_word(p2, b.Bp[j]), b.lambda[j], b.Bp[j]);
+    }
+    return g_bases.emplace(k, std::move(b)).first->second;
+}
+
+// RNS image of a positional value x (B, B' in ξ-form, m_r)
+static void to_rns_host(const Base &b, const Big &x, u32 *out) {
+    const int k = b.k;
+    for (int i = 0; i < k; i++) out[i] = mod_word(x, b.B[i]);
+    for (int j = 0; j < k; j++) out[k + j] = mulm(mod_word(x, b.Bp[j]), b.lambda[j], b.Bp[j]);
+    out[2 * k] = x.empty() ? 0 : x[0];
+}
+
+// device residency of per-k tables
+struct DevBase {
+    u32 *d_pow = nullptr;
+};
+static std::map<std::pair<int, int>, DevBase> g_devbases;
+
+static int ensure_device_base(int k, int device, const u32 **d_pow) {
+    auto key = std::make_pair(device, k);
+    auto it = g_devbases.find(key);
+    if (it != g_devbases.end()) {
+        *d_pow = it->second.d_pow;
+        return MR_OK;
+    }
+    const Base &b = base_for(k);
+    if (cudaSetDevice(device) != cudaSuccess) return MR_ERR_CUDA;
+    const KernelSet &ks = kernel_set_for(k);
+    if (ks.upload_base(b.flat.data(), device) != 0) return MR_ERR_CUDA;
+    DevBase db;
+    if (cudaMalloc(&db.d_pow, b.pow.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
+    if (cudaMemcpy(db.d_pow, b.pow.data(), b.pow.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        return MR_ERR_CUDA;
+    g_devbases[key] = db;
+    *d_pow = db.d_pow;
+    return MR_OK;
+}
+
+// capacity: 4 (k+3)^2 N < M and 4 (k+3) N < M'
+static bool fits(const Base &b, const Big &N) {
+    const u32 kk = (u32)b.k + 3;
+    Big lhs = mul_word(mul_word(N, 4 * kk), kk);
+    Big lhs2 = mul_word(N, 4 * kk);
+    return cmp(lhs, b.M) < 0 && cmp(lhs2, b.Mp) < 0;
+}
+
+static int auto_k(const Big &N, int min_k) {
+    for (int i = 0; i < kNumK; i++) {
+        int k = kSupportedK[i];
+        if (k < min_k) continue;
+        if (fits(base_for(k), N)) return k;
+    }
+    return -1;
+}
+
+}  // namespace mr
+
+using namespace mr;
+
+struct DevProg {
+    u64 *d_ops = nullptr;
+    u32 nops = 0;
+    int w = 1;
+};
+
+struct mr_rns_ctx {
+    int k = 0, device = 0;
+    size_t limbs = 0;
+    int bits = 0;
+    Big N;
+    u32 *d_cx = nullptr;       // device context block
+    const u32 *d_pow = nullptr;
+    std::vector<u32> h_cx;
+    std::mutex mu;             // guards the program cache
+    std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program
+};
+
+struct mr_rsa_priv {
+    mr_rns_ctx *cp = nullptr, *cq = nullptr;
+    size_t half = 0;
+    Big dp, dq;
+    u32 *d_q = nullptr;        // q limbs on device
+};
+
+// the per-context constant block of DESIGN.md §3 (layout cx_* in mr_internal.h)
+static void fill_ctx_block(const Base &b, const Big &N, size_t limbs, const Big &in_bound, size_t in_limbs,
+                           const Big *khi_half, const Big *qinv, u32 *x) {
+    const int k = b.k;
+    x[CX_K] = k;
+    x[CX_LIMBS] = (u32)limbs;
+    x[CX_INLIMBS] = (u32)in_limbs;
+    x[CX_NMINV_R] = N[0] * inv32(b.M_r);                        // N M^-1 mod 2^32
+    for (int i = 0; i < k; i++) {                               // σ_i = |-N^-1 M_i^-1|_{m_i}
+        u32 Ni = mod_word(N, b.B[i]);
+        u32 inv = invp(mulm(Ni, b.Mi_self[i], b.B[i]), b.B[i]);
+        x[cx_sigma(k) + i] = (b.B[i] - inv) % b.B[i];
+    }
+    for (int j = 0; j < k; j++) {                               // |N M^-1 λ_j|_{m'_j}
+        u32 Nj = mod_word(N, b.Bp[j]);
+        x[cx_c2(k) + j] = mulm(mulm(Nj, b.mu[j], b.Bp[j]), b.lambda[j], b.Bp[j]);
+    }
+    Big Rm = mod(b.M, N);                                       // R = M ("By choosing R = M")
+    Big R2 = mod(mul(Rm, Rm), N);
+    to_rns_host(b, R2, x + cx_r2(k));
+    to_rns_host(b, Big{1}, x + cx_one(k));
+    if (khi_half) {  // 2^(32 half) R^2 mod N: enters the high half of a CRT ciphertext (a3)
+        int half = (int)(*khi_half)[0];
+        to_rns_host(b, mod(mul(pow2(32 * half), R2), N), x + cx_khi(k));
+    }
+    if (qinv) to_rns_host(b, mod(mul(*qinv, Rm), N), x + cx_qinvr(k));  // mm(diff, .) = diff qinv mod p
+    for (int l = 0; l <= k && l < (int)N.size(); l++) x[cx_n(k) + l] = N[l];
+    for (int l = 0; l < 2 * k + 2 && l < (int)in_bound.size(); l++) x[cx_inb(k) + l] = in_bound[l];
+}
+
+static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, int device, const Big &in_bound,
+                     size_t in_limbs, const Big *khi_shift_limbs_half /* CRT: half limbs */, const Big *qinv) {
+    *out = nullptr;
+    if (N.empty() || !(N[0] & 1) || (N.size() == 1 && N[0] < 3)) return MR_ERR_EVEN_MODULUS;
+    int k;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int kmin = 1;
+        if (k_req > 0) {
+            kmin = -1;
+            for (int i = 0; i < kNumK; i++)
+                if (kSupportedK[i] >= k_req) { kmin = kSupportedK[i]; break; }
+            if (kmin < 0) return MR_ERR_ARG;
+            if (!fits(base_for(kmin), N)) return MR_ERR_CAPACITY;
+        }
+        k = auto_k(N, kmin);
+        if (k < 0) return MR_ERR_CAPACITY;
+    }
+    if (limbs > (size_t)k || in_limbs > (size_t)(2 * k + 2)) return MR_ERR_CAPACITY;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const Base &b = base_for(k);
+    for (u32 m : b.B)
+        if (mod_word(N, m) == 0) return MR_ERR_NOT_COPRIME;
+    for (u32 m : b.Bp)
+        if (mod_word(N, m) == 0) return MR_ERR_NOT_COPRIME;
+    mr_rns_ctx *c = new (std::nothrow) mr_rns_ctx;
+    if (!c) return MR_ERR_NOMEM;
+    c->k = k;
+    c->device = device;
+    c->limbs = limbs;
+    c->bits = bits(N);
+    c->N = N;
+    c->h_cx.assign(cx_words(k), 0);
+    fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
+    int rc = ensure_device_base(k, device, &c->d_pow);
+    if (rc != MR_OK) { delete c; return rc; }
+    if (cudaSetDevice(device) != cudaSuccess) { delete c; return MR_ERR_CUDA; }
+    if (cudaMalloc(&c->d_cx, c->h_cx.size() * 4) != cudaSuccess) { delete c; return MR_ERR_NOMEM; }
+    if (cudaMemcpy(c->d_cx, c->h_cx.data(), c->h_cx.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(c->d_cx);
+        delete c;
+        return MR_ERR_CUDA;
+    }
+    *out = c;
+    return MR_OK;
+}
+
+// ------------------------------------------------------------------ optional per-launch CUDA-event timing
+// (bench hook: records an event pair around each kernel on the stream it is launched on)
+namespace mr {
+struct EvPair {
+    cudaEvent_t a, b;
+    int kind;  // 0 ladder (k_modexp), 1 combine
+};
+static std::mutex g_tmu;
+static int g_timing = 0;
+static std::vector<EvPair> g_events;
+
+template <class F>
+static int timed_launch(int kind, cudaStream_t st, F &&launch) {
+    int on;
+    {
+        std::lock_guard<std::mutex> lk(g_tmu);
+        on = g_timing;
+    }
+    if (!on) return launch();
+    EvPair e;
+    e.kind = kind;
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    cudaEventRecord(e.a, st);
+    int rc = launch();
+    cudaEventRecord(e.b, st);
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_events.push_back(e);
+    return rc;
+}
+}  // namespace mr
+
+// ------------------------------------------------------------------ exponent -> program (R6)
+namespace mr {
+struct Ladder {
+    int w = 1;
+    std::vector<u64> ops;
+};
+
+// sliding-window recoding of E (HAC Alg. 14.85 shape), window w: appends ladder ops that start
+// with acc = x̃^(first window) loaded from the table; table slot i holds x̃^(2i+1).
+static int sliding_ops(const Big &E, int w, std::vector<u64> *ops) {
+    int n = 0;
+    bool first = true;
+    int i = bits(E) - 1;
+    while (i >= 0) {
+        if (!bit(E, i)) {
+            if (ops) ops->push_back(make_op(0, OPND_SQ));
+            n++;
+            i--;
+            continue;
+        }
+        int l = std::max(i - w + 1, 0);
+        while (!bit(E, l)) l++;
+        u32 v = 0;
+        for (int t = i; t >= l; t--) v = (v << 1) | (u32)bit(E, t);
+        if (first) {
+            if (ops) ops->push_back(make_op(OPF_LOAD | OPF_NOMUL, 0, (v - 1) / 2));
+            first = false;
+        } else {
+            for (int t = i; t >= l; t--) {
+                if (ops) ops->push_back(make_op(0, OPND_SQ));
+                n++;
+            }
+            if (ops) ops->push_back(make_op(0, (v - 1) / 2));
+            n++;
+        }
+        i = l - 1;
+    }
+    return n;
+}
+
+static int table_cost(int w) { return w > 1 ? (1 << (w - 1)) : 0; }
+
+static int best_window(const Big &E) {
+    int best = 1, bestc = 1 << 30;
+    for (int w = 1; w <= 7; w++) {
+        int c = table_cost(w) + sliding_ops(E, w, nullptr);
+        if (c < bestc) bestc = c, best = w;
+    }
+    return best;
+}
+
+// full program: entry (plain or CRT), table, ladder, exit multiply by 1
+static Ladder build_program(const Big &E, bool crt) {
+    Ladder L;
+    if (E.empty()) {  // x^0 = 1: acc = R^2 · 1 / M = R (Montgomery one), then the exit multiply
+        L.w = 1;
+        L.ops.push_back(make_op(OPF_LOAD | OPF_NOMUL, 0, OPND_R2));
+        L.ops.push_back(make_op(0, OPND_ONE));
+        L.ops.push_back(make_op(0, OPND_ONE));
+        return L;
+    }
+    L.w = best_window(E);
+    const u32 S = 1u << (L.w - 1);  // scratch slot (x̃^2, CRT high half)
+    if (crt) {
+        L.ops.push_back(make_op(OPF_TORNS_HI | OPF_STORE, OPND_KHI, 0, 0, S));
+        L.ops.push_back(make_op(OPF_TORNS_LO | OPF_ADD | OPF_STORE, OPND_R2, 0, S, 0));
+    } else {
+        L.ops.push_back(make_op(OPF_TORNS_ALL | OPF_STORE, OPND_R2, 0, 0, 0));
+    }
+    if (L.w > 1) {
+        L.ops.push_back(make_op(OPF_STORE, OPND_SQ, 0, 0, S));
+        for (u32 i = 1; i < S; i++) L.ops.push_back(make_op(OPF_STORE | (i == 1 ? OPF_LOAD : 0), S, 0, 0, i));
+    }
+    sliding_ops(E, L.w, &L.ops);
+    L.ops.push_back(make_op(0, OPND_ONE));
+    return L;
+}
+static u32 table_slots(int w) { return (1u << (w - 1)) + 1; }
+}  // namespace mr
+
+// program for exponent E on ctx, built and uploaded once, then reused by every batch call
+static int get_prog(mr_rns_ctx *c, const Big &E, bool crt, DevProg *out) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    auto key = std::make_pair(E, crt);
+    auto it = c->progs.find(key);
+    if (it == c->progs.end()) {
+        Ladder L = build_program(E, crt);
+        DevProg dp;
+        dp.nops = (u32)L.ops.size();
+        dp.w = L.w;
+        if (cudaSetDevice(c->device) != cudaSuccess) return MR_ERR_CUDA;
+        if (cudaMalloc(&dp.d_ops, L.ops.size() * 8) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMemcpy(dp.d_ops, L.ops.data(), L.ops.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(dp.d_ops);
+            return MR_ERR_CUDA;
+        }
+        if (c->progs.size() > 64) {  // bound the cache: drop everything (programs are cheap to rebuild)
+            cudaDeviceSynchronize();
+            for (auto &kv : c->progs) cudaFree(kv.second.d_ops);
+            c->progs.clear();
+        }
+        it = c->progs.emplace(key, dp).first;
+    }
+    *out = it->second;
+    return MR_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char *mr_strerror(int code) {
+    switch (code) {
+        case MR_OK: return "ok";
+        case MR_ERR_ARG: return "invalid argument";
+        case MR_ERR_EVEN_MODULUS: return "modulus must be odd and >= 3";
+        case MR_ERR_NOT_COPRIME: return "modulus shares a prime with the RNS base";
+        case MR_ERR_CAPACITY: return "modulus too large for the RNS base";
+        case MR_ERR_RANGE: return "input out of range";
+        case MR_ERR_CUDA: return "CUDA error";
+        case MR_ERR_NOMEM: return "out of memory";
+        default: return "unknown error";
+    }
+}
+
+int mr_rns_supported_k(int *ks, int cap) {
+    for (int i = 0; i < kNumK && i < cap; i++) ks[i] = kSupportedK[i];
+    return kNumK;
+}
+
+int mr_rns_ctx_create(mr_rns_ctx **out, const uint32_t *modulus, size_t limbs, int k, int device) {
+    if (!out) return MR_ERR_ARG;
+    *out = nullptr;
+    if (!modulus || limbs == 0 || k < 0) return MR_ERR_ARG;
+    Big N = big_of(modulus, limbs);
+    return build_ctx(out, N, limbs, k, device, N, limbs, nullptr, nullptr);
+}
+
+void mr_rns_ctx_destroy(mr_rns_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->d_cx) cudaFree(ctx->d_cx);
+    for (auto &kv : ctx->progs) cudaFree(kv.second.d_ops);
+    delete ctx;
+}
+
+int mr_rns_ctx_info(const mr_rns_ctx *ctx, int *k, size_t *limbs, int *modulus_bits, int *paper_cap_bits) {
+    if (!ctx) return MR_ERR_ARG;
+    if (k) *k = ctx->k;
+    if (limbs) *limbs = ctx->limbs;
+    if (modulus_bits) *modulus_bits = ctx->bits;
+    if (paper_cap_bits) *paper_cap_bits = ctx->k * 31;  // P:48 "128 32-bit primes ... 3,968-bit" = 128 x 31 (R4)
+    return MR_OK;
+}
+
+static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x, size_t in_limbs,
+                          size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status, void *stream) {
+    const mr_rns_ctx *c0 = ctxs[0];
+    const KernelSet &ks = kernel_set_for(c0->k);
+    if (cudaSetDevice(c0->device) != cudaSuccess) return MR_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    const u32 T = (u32)ks.threads;
+    const u32 ctas0 = (u32)((count + T - 1) / T);
+    const u32 jobs_total = ctas0 * T * nctx;
+    int w = 1;
+    for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
+    const size_t nch = 2 * (size_t)c0->k + 1;
+    const size_t table_words = (size_t)table_slots(w) * nch * jobs_total;
+    u32 *d_table = nullptr;
+    if (cudaMallocAsync(&d_table, table_words * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    ModexpParams P;
+    memset(&P, 0, sizeof P);
+    for (int i = 0; i < 2; i++) {
+        const int s = i < nctx ? i : nctx - 1;
+        P.ctx[i] = ctxs[s]->d_cx;
+        P.prog[i] = progs[s].d_ops;
+        P.nops[i] = progs[s].nops;
+    }
+    P.ctas0 = ctas0;
+    P.count = (u32)count;
+    P.x = d_x;
+    P.in_limbs = (u32)in_limbs;
+    P.half = (u32)half;
+    P.y = d_y;
+    P.out_limbs = (u32)out_limbs;
+    P.out_stride = count * out_limbs;
+    P.status = d_status;
+    P.table = d_table;
+    P.jobs_total = jobs_total;
+    P.pow_tab = c0->d_pow;
+    int rc = timed_launch(0, st, [&] { return ks.launch_modexp(P, ctas0 * nctx, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
+    cudaFreeAsync(d_table, st);
+    return rc;
+}
+
+int mr_modexp_batch(const mr_rns_ctx *ctx, const uint32_t *d_x, uint32_t *d_y, size_t count, const uint32_t *exp,
+                    size_t exp_limbs, int32_t *d_status, void *stream) {
+    if (!ctx || (count && (!d_x || !d_y)) || (exp_limbs && !exp)) return MR_ERR_ARG;
+    if (count == 0) return MR_OK;
+    if (count > 0x7FFFFFFFu / 2) return MR_ERR_ARG;
+    Big E = exp_limbs ? big_of(exp, exp_limbs) : Big();
+    mr_rns_ctx *c = const_cast<mr_rns_ctx *>(ctx);
+    DevProg dp;
+    int rc = get_prog(c, E, false, &dp);
+    if (rc != MR_OK) return rc;
+    return launch_ladders(&c, &dp, 1, d_x, ctx->limbs, 0, d_y, ctx->limbs, count, d_status, stream);
+}
+
+int mr_rsa_encrypt_batch(const mr_rns_ctx *n_ctx, const uint32_t *e, size_t e_limbs, const uint32_t *d_m,
+                         uint32_t *d_c, size_t count, int32_t *d_status, void *stream) {
+    return mr_modexp_batch(n_ctx, d_m, d_c, count, e, e_limbs, d_status, stream);
+}
+
+int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, size_t half_limbs, const uint32_t *d_p,
+                       const uint32_t *d_q, const uint32_t *q_inv, int k_half, int device) {
+    if (!out) return MR_ERR_ARG;
+    *out = nullptr;
+    if (!p || !q || !d_p || !d_q || !q_inv || half_limbs == 0 || k_half < 0) return MR_ERR_ARG;
+    Big P = big_of(p, half_limbs), Q = big_of(q, half_limbs), QI = big_of(q_inv, half_limbs);
+    if (P.empty() || Q.empty() || cmp(P, Q) == 0) return MR_ERR_ARG;
+    if (cmp(mod(mul(QI, Q), P), Big{1}) != 0) return MR_ERR_ARG;
+    Big N = mul(P, Q);
+    // both halves share one base pair: pick k that fits the larger prime
+    int k;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        const Big &big = cmp(P, Q) > 0 ? P : Q;
+        int kmin = 1;
+        if (k_half > 0) {
+            kmin = -1;
+            for (int i = 0; i < kNumK; i++)
+                if (kSupportedK[i] >= k_half) { kmin = kSupportedK[i]; break; }
+            if (kmin < 0) return MR_ERR_ARG;
+        }
+        k = auto_k(big, kmin);
+        if (k < 0) return MR_ERR_CAPACITY;
+    }
+    Big hl{(u32)half_limbs};
+    mr_rsa_priv *pr = new (std::nothrow) mr_rsa_priv;
+    if (!pr) return MR_ERR_NOMEM;
+    pr->half = half_limbs;
+    pr->dp = big_of(d_p, half_limbs);
+    pr->dq = big_of(d_q, half_limbs);
+    int rc = build_ctx(&pr->cp, P, half_limbs, k, device, N, 2 * half_limbs, &hl, &QI);
+    if (rc == MR_OK) rc = build_ctx(&pr->cq, Q, half_limbs, k, device, N, 2 * half_limbs, &hl, nullptr);
+    if (rc == MR_OK && pr->cp->k != pr->cq->k) rc = MR_ERR_CAPACITY;
+    if (rc == MR_OK) {
+        if (cudaMalloc(&pr->d_q, half_limbs * 4) != cudaSuccess) rc = MR_ERR_NOMEM;
+        else if (cudaMemcpy(pr->d_q, q, half_limbs * 4, cudaMemcpyHostToDevice) != cudaSuccess) rc = MR_ERR_CUDA;
+    }
+    if (rc != MR_OK) {
+        mr_rsa_priv_destroy(pr);
+        return rc;
+    }
+    *out = pr;
+    return MR_OK;
+}
+
+void mr_rsa_priv_destroy(mr_rsa_priv *priv) {
+    if (!priv) return;
+    mr_rns_ctx_destroy(priv->cp);
+    mr_rns_ctx_destroy(priv->cq);
+    if (priv->d_q) cudaFree(priv->d_q);
+    delete priv;
+}
+
+int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t *d_m, size_t count, int32_t *d_status,
+                         void *stream) {
+    if (!priv || (count && (!d_c || !d_m))) return MR_ERR_ARG;
+    if (count == 0) return MR_OK;
+    if (count > 0x7FFFFFFFu / 2) return MR_ERR_ARG;
+    const size_t H = priv->half;
+    mr_rns_ctx *cs[2] = {priv->cp, priv->cq};
+    DevProg L[2];
+    int rc0 = get_prog(priv->cp, priv->dp, true, &L[0]);
+    if (rc0 == MR_OK) rc0 = get_prog(priv->cq, priv->dq, true, &L[1]);
+    if (rc0 != MR_OK) return rc0;
+    if (cudaSetDevice(priv->cp->device) != cudaSuccess) return MR_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    u32 *d_mpq = nullptr;
+    int32_t *d_st = d_status;
+    int32_t *d_tmpst = nullptr;
+    if (cudaMallocAsync(&d_mpq, 2 * count * H * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    if (!d_st) {
+        if (cudaMallocAsync(&d_tmpst, count * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+        d_st = d_tmpst;
+    }
+    int rc = launch_ladders(cs, L, 2, d_c, 2 * H, H, d_mpq, H, count, d_st, stream);
+    if (rc == MR_OK) {
+        CombineParams C;
+        memset(&C, 0, sizeof C);
+        C.ctx_p = priv->cp->d_cx;
+        C.q = priv->d_q;
+        C.mpq = d_mpq;
+        C.count = (u32)count;
+        C.half = (u32)H;
+        C.m = d_m;
+        C.status = d_st;
+        C.pow_tab = priv->cp->d_pow;
+        const KernelSet &ks = kernel_set_for(priv->cp->k);
+        rc = timed_launch(1, st, [&] { return ks.launch_combine(C, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
+    }
+    cudaFreeAsync(d_mpq, st);
+    if (d_tmpst) cudaFreeAsync(d_tmpst, st);
+    return rc;
+}
+
+int mr_miller_rabin_batch(const uint32_t *d_n, size_t limbs, size_t count, const uint32_t *d_bases, int rounds, int k,
+                          uint8_t *d_verdict, int16_t *d_witness_round, int32_t *d_status, int device, void *stream) {
+    (void)d_n; (void)limbs; (void)d_bases; (void)rounds; (void)k; (void)d_verdict; (void)d_witness_round;
+    (void)d_status; (void)device; (void)stream;
+    if (count == 0) return MR_OK;
+    return MR_ERR_ARG;  // implemented in a later milestone
+}
+
+// ---- test hooks (not part of include/mr_rns.h): host images of the precomputed tables, so the
+// CPU test suite can check the identities of DESIGN.md §3 without a GPU.
+int mr_internal_base_table(int k, uint32_t *out, size_t cap, uint32_t *primes_out) {
+    bool ok = false;
+    for (int i = 0; i < kNumK; i++) ok |= kSupportedK[i] == k;
+    if (!ok) return -1;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const Base &b = base_for(k);
+    if (out) memcpy(out, b.flat.data(), std::min(cap, b.flat.size()) * 4);
+    if (primes_out) {
+        memcpy(primes_out, b.B.data(), 4 * k);
+        memcpy(primes_out + k, b.Bp.data(), 4 * k);
+    }
+    return (int)b.flat.size();
+}
+
+int mr_internal_pow_table(int k, uint32_t *out, size_t cap) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const Base &b = base_for(k);
+    if (out) memcpy(out, b.pow.data(), std::min(cap, b.pow.size()) * 4);
+    return (int)b.pow.size();
+}
+
+// builds the context block of modulus N for a given k (no device work); returns its word count or
+// a negative MR_* error code
+int mr_internal_ctx_table(const uint32_t *modulus, size_t limbs, int k, uint32_t *out, size_t cap) {
+    Big N = big_of(modulus, limbs);
+    if (N.empty() || !(N[0] & 1)) return -MR_ERR_EVEN_MODULUS;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const Base &b = base_for(k);
+    if (!fits(b, N)) return -MR_ERR_CAPACITY;
+    for (u32 m : b.B)
+        if (mod_word(N, m) == 0) return -MR_ERR_NOT_COPRIME;
+    for (u32 m : b.Bp)
+        if (mod_word(N, m) == 0) return -MR_ERR_NOT_COPRIME;
+    std::vector<u32> x(cx_words(k), 0);
+    fill_ctx_block(b, N, limbs, N, limbs, nullptr, nullptr, x.data());
+    if (out) memcpy(out, x.data(), std::min(cap, x.size()) * 4);
+    return (int)x.size();
+}
+
+// bench hook: enable/disable event timing of every launch; mr_internal_timing_collect waits for the
+// recorded events and returns the summed milliseconds and launch counts per kernel kind.
+int mr_internal_timing(int enable) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_timing = enable;
+    return MR_OK;
+}
+
+int mr_internal_timing_collect(double *ms_ladder, int *n_ladder, double *ms_combine, int *n_combine) {
+    std::vector<EvPair> ev;
+    {
+        std::lock_guard<std::mutex> lk(g_tmu);
+        ev.swap(g_events);
+    }
+    double t[2] = {0, 0};
+    int n[2] = {0, 0};
+    int rc = MR_OK;
+    for (auto &e : ev) {
+        float ms = 0;
+        if (cudaEventSynchronize(e.b) != cudaSuccess || cudaEventElapsedTime(&ms, e.a, e.b) != cudaSuccess) rc = MR_ERR_CUDA;
+        t[e.kind] += ms;
+        n[e.kind]++;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    if (ms_ladder) *ms_ladder = t[0];
+    if (n_ladder) *n_ladder = n[0];
+    if (ms_combine) *ms_combine = t[1];
+    if (n_combine) *n_combine = n[1];
+    return rc;
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

@@ -1,0 +1,144 @@
+// mr_internal.h — layouts shared by the host runtime (mr_host.cpp) and the per-k CUDA
+// translation units (mr_k*.cu).  Not part of the public ABI (include/mr_rns.h is).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace mr {
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+
+// ---------------------------------------------------------------------------------------------
+// Per-context constant block (device global memory, copied to shared memory by every CTA).
+// Offsets are constexpr functions of k so the host (runtime k) and device (template K) agree.
+// B' residues are stored in "ξ-form" x*_j = x_j · λ_j mod m'_j (λ_j = |M'_j^-1|_{m'_j}), so the
+// second base extension reads its CRT digits directly (DESIGN.md §4 "ξ-form").
+// ---------------------------------------------------------------------------------------------
+enum : u32 {
+    CX_K = 0,        // k
+    CX_LIMBS,        // limbs of N (canonical output width)
+    CX_INLIMBS,      // limbs of the input bound (N, or p·q for CRT halves)
+    CX_SMAX,         // largest s with N·2^s used by the exit reduction
+    CX_NMINV_R,      // N · M^-1 mod 2^32
+    CX_HDR = 8       // header words
+};
+__host__ __device__ constexpr u32 cx_sigma(u32 k) { return CX_HDR; }                 // [k]  |-N^-1 M_i^-1|_{m_i}
+__host__ __device__ constexpr u32 cx_c2(u32 k) { return cx_sigma(k) + k; }           // [k]  |N M^-1 λ_j|_{m'_j}
+__host__ __device__ constexpr u32 cx_r2(u32 k) { return cx_c2(k) + k; }              // [2k+1] R^2 mod N
+__host__ __device__ constexpr u32 cx_one(u32 k) { return cx_r2(k) + 2 * k + 1; }     // [2k+1] 1
+__host__ __device__ constexpr u32 cx_khi(u32 k) { return cx_one(k) + 2 * k + 1; }    // [2k+1] 2^(32 Lh) R^2 mod p
+__host__ __device__ constexpr u32 cx_qinvr(u32 k) { return cx_khi(k) + 2 * k + 1; }  // [2k+1] qinv R mod p
+__host__ __device__ constexpr u32 cx_n(u32 k) { return cx_qinvr(k) + 2 * k + 1; }    // [k+1] N limbs
+__host__ __device__ constexpr u32 cx_inb(u32 k) { return cx_n(k) + k + 1; }          // [2k+2] input bound limbs
+__host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_inb(k) + 2 * k + 2 + 3) & ~3u; }
+
+// ---------------------------------------------------------------------------------------------
+// Per-k base tables (N-independent).  The CUDA TU for k keeps the hot ones in __constant__ memory
+// and the to_rns powers in global memory.  Flat layout produced by the host:
+// ---------------------------------------------------------------------------------------------
+struct BaseLayout {
+    u32 k;
+    u32 c, c2, A1, A1r, A2, A2r, C1, pin, misc, MpL, NMp, words;  // offsets into the flat table
+};
+__host__ __device__ constexpr BaseLayout base_layout(u32 k) {
+    BaseLayout b{};
+    b.k = k;
+    b.c = 0;                        // [2k]     c = 2^32 - m (B then B')
+    b.c2 = b.c + 2 * k;             // [2k]     c^2
+    b.A1 = b.c2 + 2 * k;            // [k][k]   |M_i|_{m'_j}          (row i, column j)
+    b.A1r = b.A1 + k * k;           // [k]      |M_i|_{2^32}
+    b.A2 = b.A1r + k;               // [k][k]   |M'_j|_{m_i}          (row j, column i)
+    b.A2r = b.A2 + k * k;           // [k]      |M'_j|_{2^32}
+    b.C1 = b.A2r + k;               // [k]      |M^-1 λ_j^-1|_{m'_j}
+    b.pin = b.C1 + k;               // [k]      m_i - |M'|_{m_i}
+    b.misc = b.pin + k;             // [4]      M^-1 mod 2^32, M'^-1 mod 2^32
+    b.MpL = b.misc + 4;             // [k][k+1] M'_j positional limbs
+    b.NMp = b.MpL + k * (k + 1);    // [k+1]    2^(32(k+1)) - M' limbs
+    b.words = b.NMp + k + 1;
+    return b;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Exponentiation "program": one u64 op per Montgomery multiplication step, executed by a single
+// inlined mont_mul inside the kernel's interpreter loop (keeps one copy of the unrolled code).
+// ---------------------------------------------------------------------------------------------
+enum : u32 {
+    OPF_TORNS_ALL = 1u,   // before: acc = to_rns(input limbs [0, in_limbs))
+    OPF_TORNS_LO = 2u,    // before: acc = to_rns(input limbs [0, half))
+    OPF_TORNS_HI = 4u,    // before: acc = to_rns(input limbs [half, 2 half))
+    OPF_LOAD = 8u,        // before: acc = operand(load)
+    OPF_NOMUL = 16u,      // skip the Montgomery multiplication
+    OPF_ADD = 32u,        // after: acc = acc + table[add]  (channel-wise)
+    OPF_STORE = 64u,      // after: table[store] = acc
+};
+enum : u32 { OPND_SQ = 0xFF, OPND_R2 = 0xF0, OPND_ONE = 0xF1, OPND_KHI = 0xF2, OPND_QINVR = 0xF3 };
+__host__ __device__ constexpr u64 make_op(u32 flags, u32 opnd, u32 load = 0, u32 add = 0, u32 store = 0) {
+    return (u64)(flags & 0xFF) | ((u64)(opnd & 0xFF) << 8) | ((u64)(load & 0xFF) << 16) |
+           ((u64)(add & 0xFF) << 24) | ((u64)(store & 0xFF) << 32);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Kernel launch parameter blocks (plain structs passed by value).
+// ---------------------------------------------------------------------------------------------
+struct ModexpParams {
+    const u32 *ctx[2];        // device context blocks; CTA b uses ctx[b >= ctas0]
+    const u64 *prog[2];       // device programs
+    u32 nops[2];
+    u32 ctas0;                // CTAs of the first context
+    u32 count;                // messages per context
+    const u32 *x;             // [count][in_limbs]
+    u32 in_limbs;             // limbs per input row
+    u32 half;                 // CRT: limbs per half (inputs split at `half`)
+    u32 *y;                   // [count][out_limbs] per context: y + ctxsel * out_stride
+    u32 out_limbs;
+    size_t out_stride;        // words between the two contexts' outputs
+    int32_t *status;          // nullable
+    u32 *table;               // window table [slot][2k+1][jobs_total]
+    u32 jobs_total;           // = 2 * ctas0 * blockDim (or ctas0 * blockDim)
+    const u32 *pow_tab;       // to_rns powers [k][2k]
+};
+
+struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qinv mod p)
+    const u32 *ctx_p;
+    const u32 *q;               // [half] limbs of q
+    const u32 *mpq;             // [2][count][half]: m_p rows then m_q rows
+    u32 count, half;
+    u32 *m;                     // [count][2 half]
+    int32_t *status;            // nullable (range flag already written by the ladder kernel)
+    const u32 *pow_tab;
+};
+
+struct MrParams {               // Miller-Rabin
+    const u32 *n;               // [count][limbs]
+    const u32 *bases;           // [count][rounds][limbs]
+    u32 count, limbs, rounds, window;
+    u32 *pc;                    // per-candidate constants [PC_WORDS(k)][count]
+    u32 *table;                 // [2^w][2k+1][count]
+    uint8_t *verdict;
+    int16_t *witness;
+    int32_t *status;
+    const u32 *pow_tab;
+};
+
+// per-candidate constant rows for Miller-Rabin (structure of arrays, row r at pc + r*count)
+__host__ __device__ constexpr u32 pc_sigma(u32 k) { return 0; }                 // [k]
+__host__ __device__ constexpr u32 pc_c2(u32 k) { return k; }                    // [k]
+__host__ __device__ constexpr u32 pc_r2(u32 k) { return 2 * k; }                // [2k+1] R^2 mod n
+__host__ __device__ constexpr u32 pc_nminv(u32 k) { return 4 * k + 1; }         // [1]
+__host__ __device__ constexpr u32 pc_misc(u32 k) { return 4 * k + 2; }          // [2]: s, flags
+__host__ __device__ constexpr u32 pc_words(u32 k) { return 4 * k + 4; }
+
+// ---------------------------------------------------------------------------------------------
+// Per-k entry points exported by each mr_k<K>.cu translation unit.
+// ---------------------------------------------------------------------------------------------
+struct KernelSet {
+    int k;
+    int (*upload_base)(const u32 *flat, int device);     // fills __constant__ tables on `device`
+    int (*launch_modexp)(const ModexpParams &p, u32 ctas, void *stream);
+    int (*launch_combine)(const CombineParams &p, void *stream);
+    int (*launch_mr)(const MrParams &p, void *stream);
+    int threads;                                          // CTA size used by launch_modexp
+};
+
+}  // namespace mr

@@ -1,0 +1,7 @@
+// Channel-count instantiation K = 5 of the RNS Montgomery kernels (see mr_kernels.cuh).
+#define MR_K 5
+#include "mr_kernels.cuh"
+
+namespace mr {
+KernelSet kernels_k5() { return KernelSet{MR_K, upload_base, launch_modexp, launch_combine, launch_mr, THREADS}; }
+}  // namespace mr

@@ -1,0 +1,7 @@
+// Channel-count instantiation K = 9 of the RNS Montgomery kernels (see mr_kernels.cuh).
+#define MR_K 9
+#include "mr_kernels.cuh"
+
+namespace mr {
+KernelSet kernels_k9() { return KernelSet{MR_K, upload_base, launch_modexp, launch_combine, launch_mr, THREADS}; }
+}  // namespace mr

@@ -1,0 +1,197 @@
+"""CPU-side checks of the boundary: the shared library loads, exports every symbol declared in
+include/mr_rns.h, reports errors without a GPU, and its host-side precomputation satisfies the
+identities of DESIGN.md §3 (checked with independent CPython arithmetic, no oracle involvement
+needed: these are definitions of the tables, not results of the method)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HDR = os.path.join(ROOT, "include", "mr_rns.h")
+
+
+def _lib():
+    import paper_1305_3699_b200 as mr
+    return mr, mr.lib()
+
+
+def test_exports_every_header_symbol():
+    mr, L = _lib()
+    src = open(HDR).read()
+    names = set(re.findall(r"\b(mr_[a-z0-9_]+)\s*\(", src))
+    assert {"mr_rns_ctx_create", "mr_modexp_batch", "mr_rsa_encrypt_batch", "mr_rsa_decrypt_batch",
+            "mr_miller_rabin_batch"} <= names
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(mr.EXPORTS) == names
+
+
+def test_strerror_and_supported_k():
+    mr, L = _lib()
+    assert mr.mr_strerror(0) == "ok"
+    assert "range" in mr.mr_strerror(5)
+    ks = mr.mr_rns_supported_k()
+    assert ks == sorted(ks) and 33 in ks and 65 in ks
+
+
+def test_no_gpu_reports_cuda_error():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    mr, L = _lib()
+    with pytest.raises(mr.MrError) as e:
+        mr.mr_rns_ctx_create(3233, 1)
+    assert e.value.code == mr.MR_ERR_CUDA
+    with pytest.raises(mr.MrError) as e:
+        mr.mr_rns_ctx_create(3232, 1)                  # even modulus is rejected before any device work
+    assert e.value.code == mr.MR_ERR_EVEN_MODULUS
+
+
+def test_argument_errors():
+    mr, L = _lib()
+    h = ctypes.c_void_p()
+    assert L.mr_rns_ctx_create(ctypes.byref(h), None, 1, 0, 0) == mr.MR_ERR_ARG
+    assert L.mr_modexp_batch(None, None, None, 0, None, 0, None, None) == mr.MR_ERR_ARG
+    assert L.mr_rsa_decrypt_batch(None, None, None, 0, None, None) == mr.MR_ERR_ARG
+
+
+def _tables(k):
+    mr, L = _lib()
+    L.mr_internal_base_table.restype = ctypes.c_int
+    L.mr_internal_ctx_table.restype = ctypes.c_int
+    n = L.mr_internal_base_table(k, None, 0, None)
+    flat = np.zeros(n, dtype=np.uint32)
+    primes = np.zeros(2 * k, dtype=np.uint32)
+    P = ctypes.POINTER(ctypes.c_uint32)
+    L.mr_internal_base_table(k, flat.ctypes.data_as(P), n, primes.ctypes.data_as(P))
+    npow = L.mr_internal_pow_table(k, None, 0)
+    pw = np.zeros(npow, dtype=np.uint32)
+    L.mr_internal_pow_table(k, pw.ctypes.data_as(P), npow)
+    return flat, [int(p) for p in primes], pw
+
+
+def _layout(k):
+    o = {}
+    o["c"] = 0
+    o["c2"] = 2 * k
+    o["A1"] = 4 * k
+    o["A1r"] = o["A1"] + k * k
+    o["A2"] = o["A1r"] + k
+    o["A2r"] = o["A2"] + k * k
+    o["C1"] = o["A2r"] + k
+    o["pin"] = o["C1"] + k
+    o["misc"] = o["pin"] + k
+    o["MpL"] = o["misc"] + 4
+    o["NMp"] = o["MpL"] + k * (k + 1)
+    return o
+
+
+@pytest.mark.parametrize("k", [1, 3, 17, 33])
+def test_base_table_identities(k):
+    import sympy
+    flat, primes, pw = _tables(k)
+    B, Bp = primes[:k], primes[k:]
+    # reading R1: the 2k largest primes below 2^32, descending
+    expect, x = [], 1 << 32
+    while len(expect) < 2 * k:
+        x = sympy.prevprime(x)
+        expect.append(x)
+    assert primes == expect
+    M, Mp = 1, 1
+    for m in B:
+        M *= m
+    for m in Bp:
+        Mp *= m
+    o = _layout(k)
+    f = [int(v) for v in flat]
+    W = 1 << 32
+    for ch, m in enumerate(B + Bp):
+        assert f[o["c"] + ch] == W - m and f[o["c2"] + ch] == (W - m) ** 2
+    for i in range(k):
+        Mi = M // B[i]
+        for j in range(k):
+            assert f[o["A1"] + i * k + j] == Mi % Bp[j]
+        assert f[o["A1r"] + i] == Mi % W
+    for j in range(k):
+        Mpj = Mp // Bp[j]
+        for i in range(k):
+            assert f[o["A2"] + j * k + i] == Mpj % B[i]
+        assert f[o["A2r"] + j] == Mpj % W
+        lam = pow(Mpj, -1, Bp[j])
+        assert f[o["C1"] + j] == pow(M, -1, Bp[j]) * pow(lam, -1, Bp[j]) % Bp[j]
+        limbs = sum(f[o["MpL"] + j * (k + 1) + l] << (32 * l) for l in range(k + 1))
+        assert limbs == Mpj
+    for i in range(k):
+        assert (f[o["pin"] + i] + Mp) % B[i] == 0                      # m_i - |M'|_{m_i}
+    assert f[o["misc"]] * M % W == 1 and f[o["misc"] + 1] * Mp % W == 1
+    nmp = sum(f[o["NMp"] + l] << (32 * l) for l in range(k + 1))
+    assert nmp + Mp == 1 << (32 * (k + 1))
+    # to_rns powers: |2^(32 l)|_{m_i} and |2^(32 l) λ_j|_{m'_j}
+    for l in range(k):
+        for i in range(k):
+            assert int(pw[l * 2 * k + i]) == pow(2, 32 * l, B[i])
+        for j in range(k):
+            lam = pow(Mp // Bp[j], -1, Bp[j])
+            assert int(pw[l * 2 * k + k + j]) == pow(2, 32 * l, Bp[j]) * lam % Bp[j]
+    # capacity headroom of reading R5: 4 (k+3)^2 N < M leaves ~20 bits for N of 32(k-1) bits
+    if k >= 17:
+        assert 4 * (k + 3) ** 2 * (1 << (32 * (k - 1))) < M
+
+
+@pytest.mark.parametrize("name", ["rsa1024", "rsa2048"])
+def test_ctx_table_identities(keys, name):
+    mr, L = _lib()
+    key = keys[name]
+    N = key["n"] if name == "rsa1024" else key["p"]          # 1024-bit moduli -> k = 33
+    k = 33
+    flat, primes, _ = _tables(k)
+    B, Bp = primes[:k], primes[k:]
+    limbs = (N.bit_length() + 31) // 32
+    P = ctypes.POINTER(ctypes.c_uint32)
+    nl = np.frombuffer(N.to_bytes(4 * limbs, "little"), dtype=np.uint32).copy()
+    nw = L.mr_internal_ctx_table(nl.ctypes.data_as(P), limbs, k, None, 0)
+    assert nw > 0
+    cx = np.zeros(nw, dtype=np.uint32)
+    L.mr_internal_ctx_table(nl.ctypes.data_as(P), limbs, k, cx.ctypes.data_as(P), nw)
+    cx = [int(v) for v in cx]
+    M, Mp = 1, 1
+    for m in B:
+        M *= m
+    for m in Bp:
+        Mp *= m
+    W = 1 << 32
+    assert cx[0] == k and cx[1] == limbs
+    assert cx[4] == N * pow(M, -1, W) % W
+    sig, c2, r2, one = 8, 8 + k, 8 + 2 * k, 8 + 2 * k + 2 * k + 1
+    for i in range(k):
+        assert cx[sig + i] * N * (M // B[i]) % B[i] == B[i] - 1       # σ_i N M_i = -1 (mod m_i)
+    for j in range(k):
+        lam = pow(Mp // Bp[j], -1, Bp[j])
+        assert cx[c2 + j] == N * pow(M, -1, Bp[j]) * lam % Bp[j]
+    R2 = M * M % N
+    for i in range(k):
+        assert cx[r2 + i] == R2 % B[i] and cx[one + i] == 1
+    for j in range(k):
+        lam = pow(Mp // Bp[j], -1, Bp[j])
+        assert cx[r2 + k + j] == R2 % Bp[j] * lam % Bp[j] and cx[one + k + j] == lam
+    assert cx[r2 + 2 * k] == R2 % W
+
+
+def test_ctx_table_rejections():
+    mr, L = _lib()
+    P = ctypes.POINTER(ctypes.c_uint32)
+    _, primes, _ = _tables(33)
+    bad = primes[5] * ((1 << 900) + 1)                          # shares a base prime
+    while bad % 2 == 0:
+        bad += primes[5]
+    limbs = (bad.bit_length() + 31) // 32
+    nl = np.frombuffer(bad.to_bytes(4 * limbs, "little"), dtype=np.uint32).copy()
+    assert L.mr_internal_ctx_table(nl.ctypes.data_as(P), limbs, 33, None, 0) == -mr.MR_ERR_NOT_COPRIME
+    big = (1 << 1100) + 1
+    limbs = 35
+    nl = np.frombuffer(big.to_bytes(4 * limbs, "little"), dtype=np.uint32).copy()
+    assert L.mr_internal_ctx_table(nl.ctypes.data_as(P), limbs, 33, None, 0) == -mr.MR_ERR_CAPACITY
