@@ -177,6 +177,7 @@ struct Base {
     Big M, Mp;                     // products
     std::vector<u32> flat;         // constant-bank image (BaseLayout)
     std::vector<u32> pow;          // to_rns powers [k][2k]
+    std::vector<u32> be;           // base-extension shared-memory image (mr_internal.h be_*)
 };
 static std::map<int, Base> g_bases;
 
@@ -243,12 +244,45 @@ static const Base &base_for(int k) {
         Big NMp = sub(pow2(32 * (k + 1)), b.Mp);
         for (int l = 0; l <= k; l++) f[L.NMp + l] = l < (int)NMp.size() ? NMp[l] : 0;
     }
+    for (int i = 0; i < k; i++) f[L.MiS + i] = b.Mi_self[i];
+    for (int j = 0; j < k; j++) f[L.MU + j] = b.mu[j];
+    for (int i = 0; i < k; i++) f[L.ONE + i] = 1;
+    for (int j = 0; j < k; j++) f[L.ONE + k + j] = b.lambda[j];
+    f[L.ONE + 2 * k] = 1;
+    for (int l = 0; l <= k; l++) f[L.ML + l] = l < (int)b.M.size() ? b.M[l] : 0;
     b.pow.assign((size_t)k * 2 * k, 0);
     for (int l = 0; l < k; l++) {
         Big p2 = pow2(32 * l);
         for (int i = 0; i < k; i++) b.pow[(size_t)l * 2 * k + i] = mod_word(p2, b.B[i]);
         for (int j = 0; j < k; j++)
             b.pow[(size_t)l * 2 * k + k + j] = mulm(mod_word(p2, b.Bp[j]), b.lambda[j], b.Bp[j]);
+    }
+    // base-extension image: BE1 tiles of A1[i][j] (columns j), then BE2 tiles of A2[j][i] (columns i)
+    b.be.assign(be_words(k), 0);
+    for (int half = 0; half < 2; half++) {
+        const u32 *tab = f + (half ? L.A2 : L.A1);
+        u32 *out = b.be.data() + half * be_half_words(k);
+        const u32 ch = be_ch(k), nt = be_nfull(k) + (be_tail(k) ? 1 : 0);
+        u32 off = 0;
+        for (u32 t = 0; t < nt; t++) {
+            const u32 w = t < be_nfull(k) ? ch : be_tail(k), pw = pad4(w);
+            for (int i = 0; i < k; i++)
+                for (u32 jj = 0; jj < w; jj++) out[off + i * pw + jj] = tab[i * k + t * ch + jj];
+            off += k * pw;
+        }
+    }
+    {
+        u32 *v = b.be.data();
+        for (int ch = 0; ch < 2 * k; ch++) {
+            v[bev_c(k) + ch] = f[L.c + ch];
+            v[bev_c2(k) + ch] = f[L.c2 + ch];
+        }
+        for (int i = 0; i < k; i++) {
+            v[bev_C1(k) + i] = f[L.C1 + i];
+            v[bev_pin(k) + i] = f[L.pin + i];
+            v[bev_A1r(k) + i] = f[L.A1r + i];
+            v[bev_A2r(k) + i] = f[L.A2r + i];
+        }
     }
     return g_bases.emplace(k, std::move(b)).first->second;
 }
@@ -264,14 +298,16 @@ static void to_rns_host(const Base &b, const Big &x, u32 *out) {
 // device residency of per-k tables
 struct DevBase {
     u32 *d_pow = nullptr;
+    u32 *d_be = nullptr;
 };
 static std::map<std::pair<int, int>, DevBase> g_devbases;
 
-static int ensure_device_base(int k, int device, const u32 **d_pow) {
+static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **d_be) {
     auto key = std::make_pair(device, k);
     auto it = g_devbases.find(key);
     if (it != g_devbases.end()) {
         *d_pow = it->second.d_pow;
+        *d_be = it->second.d_be;
         return MR_OK;
     }
     const Base &b = base_for(k);
@@ -282,8 +318,12 @@ static int ensure_device_base(int k, int device, const u32 **d_pow) {
     if (cudaMalloc(&db.d_pow, b.pow.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
     if (cudaMemcpy(db.d_pow, b.pow.data(), b.pow.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
         return MR_ERR_CUDA;
+    if (cudaMalloc(&db.d_be, b.be.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
+    if (cudaMemcpy(db.d_be, b.be.data(), b.be.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        return MR_ERR_CUDA;
     g_devbases[key] = db;
     *d_pow = db.d_pow;
+    *d_be = db.d_be;
     return MR_OK;
 }
 
@@ -321,6 +361,7 @@ struct mr_rns_ctx {
     Big N;
     u32 *d_cx = nullptr;       // device context block
     const u32 *d_pow = nullptr;
+    const u32 *d_be = nullptr;
     std::vector<u32> h_cx;
     std::mutex mu;             // guards the program cache
     std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program
@@ -397,7 +438,7 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->N = N;
     c->h_cx.assign(cx_words(k), 0);
     fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
-    int rc = ensure_device_base(k, device, &c->d_pow);
+    int rc = ensure_device_base(k, device, &c->d_pow, &c->d_be);
     if (rc != MR_OK) { delete c; return rc; }
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return MR_ERR_CUDA; }
     if (cudaMalloc(&c->d_cx, c->h_cx.size() * 4) != cudaSuccess) { delete c; return MR_ERR_NOMEM; }
@@ -415,11 +456,13 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
 namespace mr {
 struct EvPair {
     cudaEvent_t a, b;
-    int kind;  // 0 ladder (k_modexp), 1 combine
+    int kind;  // 0 ladder (k_modexp), 1 combine, 2 Miller-Rabin (setup + rounds)
 };
 static std::mutex g_tmu;
 static int g_timing = 0;
 static std::vector<EvPair> g_events;
+static double g_last_mr_ms = 0;
+static int g_last_mr_n = 0;
 
 template <class F>
 static int timed_launch(int kind, cudaStream_t st, F &&launch) {
@@ -553,6 +596,9 @@ static int get_prog(mr_rns_ctx *c, const Big &E, bool crt, DevProg *out) {
 
 #pragma GCC visibility push(default)
 extern "C" {
+int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, const uint32_t *d_bases, int rounds,
+                             int k, uint8_t *d_verdict, int16_t *d_witness_round, int32_t *d_status, int device,
+                             void *stream, int forced, int window);
 
 const char *mr_strerror(int code) {
     switch (code) {
@@ -633,6 +679,7 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     P.table = d_table;
     P.jobs_total = jobs_total;
     P.pow_tab = c0->d_pow;
+    P.be_tab = c0->d_be;
     int rc = timed_launch(0, st, [&] { return ks.launch_modexp(P, ctas0 * nctx, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
     cudaFreeAsync(d_table, st);
     return rc;
@@ -742,6 +789,7 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
         C.m = d_m;
         C.status = d_st;
         C.pow_tab = priv->cp->d_pow;
+        C.be_tab = priv->cp->d_be;
         const KernelSet &ks = kernel_set_for(priv->cp->k);
         rc = timed_launch(1, st, [&] { return ks.launch_combine(C, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
     }
@@ -752,10 +800,68 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
 
 int mr_miller_rabin_batch(const uint32_t *d_n, size_t limbs, size_t count, const uint32_t *d_bases, int rounds, int k,
                           uint8_t *d_verdict, int16_t *d_witness_round, int32_t *d_status, int device, void *stream) {
-    (void)d_n; (void)limbs; (void)d_bases; (void)rounds; (void)k; (void)d_verdict; (void)d_witness_round;
-    (void)d_status; (void)device; (void)stream;
+    return mr_internal_miller_rabin(d_n, limbs, count, d_bases, rounds, k, d_verdict, d_witness_round, d_status,
+                                    device, stream, 0, 4);
+}
+
+// Miller-Rabin with benchmark controls: forced = 1 runs every round for every candidate (MR-rounds/s),
+// window = fixed-window width of the a^d ladder.
+int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, const uint32_t *d_bases, int rounds,
+                             int k, uint8_t *d_verdict, int16_t *d_witness_round, int32_t *d_status, int device,
+                             void *stream, int forced, int window) {
+    if ((count && (!d_n || !d_verdict || (rounds > 0 && !d_bases))) || limbs == 0 || rounds < 0 || k < 0 ||
+        window < 1 || window > 6)
+        return MR_ERR_ARG;
     if (count == 0) return MR_OK;
-    return MR_ERR_ARG;  // implemented in a later milestone
+    if (count > 0x7FFFFFFFu) return MR_ERR_ARG;
+    int kk;
+    const u32 *d_pow = nullptr, *d_be = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        Big top = sub(pow2(32 * (int)limbs), Big{1});   // capacity for any n < 2^(32 limbs)
+        int kmin = 1;
+        if (k > 0) {
+            kmin = -1;
+            for (int i = 0; i < kNumK; i++)
+                if (kSupportedK[i] >= k) { kmin = kSupportedK[i]; break; }
+            if (kmin < 0) return MR_ERR_ARG;
+        }
+        kk = auto_k(top, kmin);
+        if (kk < 0) return MR_ERR_CAPACITY;
+        if ((int)limbs > kk - 1) return MR_ERR_CAPACITY;
+        int rc = ensure_device_base(kk, device, &d_pow, &d_be);
+        if (rc != MR_OK) return rc;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return MR_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t nch = 2 * (size_t)kk + 1;
+    u32 *d_pc = nullptr, *d_tab = nullptr;
+    if (cudaMallocAsync(&d_pc, (size_t)pc_words(kk) * count * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    if (cudaMallocAsync(&d_tab, ((size_t)(1u << window) + 1) * nch * count * 4, st) != cudaSuccess) {
+        cudaFreeAsync(d_pc, st);
+        return MR_ERR_NOMEM;
+    }
+    MrParams P;
+    memset(&P, 0, sizeof P);
+    P.n = d_n;
+    P.bases = d_bases;
+    P.count = (u32)count;
+    P.limbs = (u32)limbs;
+    P.rounds = (u32)rounds;
+    P.window = (u32)window;
+    P.forced = (u32)forced;
+    P.pc = d_pc;
+    P.table = d_tab;
+    P.verdict = d_verdict;
+    P.witness = d_witness_round;
+    P.status = d_status;
+    P.pow_tab = d_pow;
+    P.be_tab = d_be;
+    const KernelSet &ks = kernel_set_for(kk);
+    int rc = timed_launch(2, st, [&] { return ks.launch_mr(P, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
+    cudaFreeAsync(d_pc, st);
+    cudaFreeAsync(d_tab, st);
+    return rc;
 }
 
 // ---- test hooks (not part of include/mr_rns.h): host images of the precomputed tables, so the
@@ -801,6 +907,13 @@ int mr_internal_ctx_table(const uint32_t *modulus, size_t limbs, int k, uint32_t
 
 // bench hook: enable/disable event timing of every launch; mr_internal_timing_collect waits for the
 // recorded events and returns the summed milliseconds and launch counts per kernel kind.
+// Miller-Rabin launch time collected by the last mr_internal_timing_collect
+int mr_internal_timing_mr(double *ms, int *n) {
+    if (ms) *ms = g_last_mr_ms;
+    if (n) *n = g_last_mr_n;
+    return MR_OK;
+}
+
 int mr_internal_timing(int enable) {
     std::lock_guard<std::mutex> lk(g_tmu);
     g_timing = enable;
@@ -813,8 +926,8 @@ int mr_internal_timing_collect(double *ms_ladder, int *n_ladder, double *ms_comb
         std::lock_guard<std::mutex> lk(g_tmu);
         ev.swap(g_events);
     }
-    double t[2] = {0, 0};
-    int n[2] = {0, 0};
+    double t[3] = {0, 0, 0};
+    int n[3] = {0, 0, 0};
     int rc = MR_OK;
     for (auto &e : ev) {
         float ms = 0;
@@ -828,6 +941,8 @@ int mr_internal_timing_collect(double *ms_ladder, int *n_ladder, double *ms_comb
     if (n_ladder) *n_ladder = n[0];
     if (ms_combine) *ms_combine = t[1];
     if (n_combine) *n_combine = n[1];
+    g_last_mr_ms = t[2];
+    g_last_mr_n = n[2];
     return rc;
 }
 

@@ -39,7 +39,7 @@ __host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_inb(k) + 2 * k + 
 // ---------------------------------------------------------------------------------------------
 struct BaseLayout {
     u32 k;
-    u32 c, c2, A1, A1r, A2, A2r, C1, pin, misc, MpL, NMp, words;  // offsets into the flat table
+    u32 c, c2, A1, A1r, A2, A2r, C1, pin, misc, MpL, NMp, MiS, MU, ONE, ML, words;  // offsets
 };
 __host__ __device__ constexpr BaseLayout base_layout(u32 k) {
     BaseLayout b{};
@@ -55,9 +55,39 @@ __host__ __device__ constexpr BaseLayout base_layout(u32 k) {
     b.misc = b.pin + k;             // [4]      M^-1 mod 2^32, M'^-1 mod 2^32
     b.MpL = b.misc + 4;             // [k][k+1] M'_j positional limbs
     b.NMp = b.MpL + k * (k + 1);    // [k+1]    2^(32(k+1)) - M' limbs
-    b.words = b.NMp + k + 1;
+    b.MiS = b.NMp + k + 1;          // [k]      |M_i|_{m_i}           (Miller-Rabin setup)
+    b.MU = b.MiS + k;               // [k]      |M^-1|_{m'_j}         (Miller-Rabin setup)
+    b.ONE = b.MU + k;               // [2k+1]   RNS image of 1 (B' in ξ-form)
+    b.ML = b.ONE + 2 * k + 1;       // [k+1]    M positional limbs    (Miller-Rabin setup)
+    b.words = b.ML + k + 1;
     return b;
 }
+
+// ---------------------------------------------------------------------------------------------
+// Base-extension constant image staged in shared memory (read with 16-byte broadcast loads).
+// Outputs are processed in tiles of be_ch(k) columns; tile t holds, for every input row i, the
+// tile's columns padded to a multiple of 4 words.  Image = BE1 tiles (A1[i][j]) then BE2 tiles
+// (A2[j][i]).  Full tiles first, then the tail tile (k mod be_ch(k) columns) if any.
+// ---------------------------------------------------------------------------------------------
+__host__ __device__ constexpr u32 be_ch(u32 k) {
+    for (u32 c = 13; c >= 6; c--)
+        if (k % c == 0) return c;
+    return k <= 13 ? k : 8;
+}
+__host__ __device__ constexpr u32 pad4(u32 x) { return (x + 3) & ~3u; }
+__host__ __device__ constexpr u32 be_nfull(u32 k) { return k / be_ch(k); }
+__host__ __device__ constexpr u32 be_tail(u32 k) { return k - be_nfull(k) * be_ch(k); }
+__host__ __device__ constexpr u32 be_half_words(u32 k) {
+    return be_nfull(k) * k * pad4(be_ch(k)) + (be_tail(k) ? k * pad4(be_tail(k)) : 0);
+}
+// per-channel vectors after the two matrices (each padded to a multiple of 4 words)
+__host__ __device__ constexpr u32 bev_c(u32 k) { return 2 * be_half_words(k); }          // [2k] c = 2^32 - m
+__host__ __device__ constexpr u32 bev_c2(u32 k) { return bev_c(k) + pad4(2 * k); }       // [2k] c^2
+__host__ __device__ constexpr u32 bev_C1(u32 k) { return bev_c2(k) + pad4(2 * k); }      // [k]  |M^-1 λ_j^-1|_{m'_j}
+__host__ __device__ constexpr u32 bev_pin(u32 k) { return bev_C1(k) + pad4(k); }         // [k]  m_i - |M'|_{m_i}
+__host__ __device__ constexpr u32 bev_A1r(u32 k) { return bev_pin(k) + pad4(k); }        // [k]  |M_i|_{2^32}
+__host__ __device__ constexpr u32 bev_A2r(u32 k) { return bev_A1r(k) + pad4(k); }        // [k]  |M'_j|_{2^32}
+__host__ __device__ constexpr u32 be_words(u32 k) { return bev_A2r(k) + pad4(k); }
 
 // ---------------------------------------------------------------------------------------------
 // Exponentiation "program": one u64 op per Montgomery multiplication step, executed by a single
@@ -97,6 +127,7 @@ struct ModexpParams {
     u32 *table;               // window table [slot][2k+1][jobs_total]
     u32 jobs_total;           // = 2 * ctas0 * blockDim (or ctas0 * blockDim)
     const u32 *pow_tab;       // to_rns powers [k][2k]
+    const u32 *be_tab;        // base-extension image (be_words(k))
 };
 
 struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qinv mod p)
@@ -107,27 +138,32 @@ struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qi
     u32 *m;                     // [count][2 half]
     int32_t *status;            // nullable (range flag already written by the ladder kernel)
     const u32 *pow_tab;
+    const u32 *be_tab;
 };
 
-struct MrParams {               // Miller-Rabin
-    const u32 *n;               // [count][limbs]
+struct MrParams {               // Miller-Rabin (§3.2; HAC 4.24)
+    const u32 *n;               // [count][limbs] candidates
     const u32 *bases;           // [count][rounds][limbs]
     u32 count, limbs, rounds, window;
-    u32 *pc;                    // per-candidate constants [PC_WORDS(k)][count]
-    u32 *table;                 // [2^w][2k+1][count]
+    u32 forced;                 // 1: run every round for every candidate (benchmark mode)
+    u32 *pc;                    // per-candidate constants [pc_words(k)][count] (structure of arrays)
+    u32 *table;                 // [2^w + 1][2k+1][count] window table + stash slot
     uint8_t *verdict;
     int16_t *witness;
     int32_t *status;
     const u32 *pow_tab;
+    const u32 *be_tab;
 };
 
-// per-candidate constant rows for Miller-Rabin (structure of arrays, row r at pc + r*count)
-__host__ __device__ constexpr u32 pc_sigma(u32 k) { return 0; }                 // [k]
-__host__ __device__ constexpr u32 pc_c2(u32 k) { return k; }                    // [k]
-__host__ __device__ constexpr u32 pc_r2(u32 k) { return 2 * k; }                // [2k+1] R^2 mod n
-__host__ __device__ constexpr u32 pc_nminv(u32 k) { return 4 * k + 1; }         // [1]
-__host__ __device__ constexpr u32 pc_misc(u32 k) { return 4 * k + 2; }          // [2]: s, flags
-__host__ __device__ constexpr u32 pc_words(u32 k) { return 4 * k + 4; }
+// per-candidate constant rows for Miller-Rabin (row r at pc + r * count)
+__host__ __device__ constexpr u32 pc_sigma(u32 k) { return 0; }                 // [k]  |-n^-1 M_i^-1|_{m_i}
+__host__ __device__ constexpr u32 pc_c2(u32 k) { return k; }                    // [k]  |n M^-1 λ_j|_{m'_j}
+__host__ __device__ constexpr u32 pc_r2(u32 k) { return 2 * k; }                // [2k+1] M^2 mod n (RNS)
+__host__ __device__ constexpr u32 pc_nminv(u32 k) { return 4 * k + 1; }         // [1]  n M^-1 mod 2^32
+__host__ __device__ constexpr u32 pc_s(u32 k) { return 4 * k + 2; }             // [1]  s with n - 1 = 2^s d
+__host__ __device__ constexpr u32 pc_live(u32 k) { return 4 * k + 3; }          // [1]  1 = run the rounds
+__host__ __device__ constexpr u32 pc_d(u32 k) { return 4 * k + 4; }             // [k]  d limbs
+__host__ __device__ constexpr u32 pc_words(u32 k) { return 5 * k + 4; }
 
 // ---------------------------------------------------------------------------------------------
 // Per-k entry points exported by each mr_k<K>.cu translation unit.

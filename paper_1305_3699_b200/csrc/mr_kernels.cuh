@@ -3,13 +3,19 @@
 // Included once per channel count by mr_k<K>.cu with MR_K defined.  Each translation unit is its
 // own CUDA module, so the __constant__ base tables below are private to that K.
 //
-// Mapping: thread-per-message.  A thread keeps the 2K+1 residues of its message in
-// registers for the whole exponentiation; the two base extensions (92-97% of the word products,
-// SURVEY §8(a6)) run as fully-unrolled 96-bit multiply-accumulate chains whose constant operands
-// come from the __constant__ bank (warp-uniform, no load instruction), CH output accumulators at a
-// time for ILP.  Every residue reduction uses the pseudo-Mersenne form m = 2^32 - c, c < 2^13.
-// Residues are kept lazily in [0, 2^32) (congruent, not necessarily < m); DESIGN.md §3 shows the
-// value bound r < (K+3)N still holds, and the exit conversion canonicalises.
+// Mapping: thread-per-message.  A CTA of T = 128 threads owns 128 messages; the
+// 2K+1 residues of every message live in shared memory in [channel][thread] layout (conflict-free),
+// and each phase of the RNS Montgomery multiplication pulls its input vector into registers:
+//   phase 1  channel products -> ξ (registers) and t*_B' (smem)
+//   BE1      ξ[K] (registers) x |M_i|_{m'_j} (constant bank)  -> ξ'_j (smem), CH outputs per pass
+//   BE2      ξ'[K] (registers) x |M'_j|_{m_i} (constant bank) -> r_i  (smem)
+// The base-extension contractions (92-97% of the word products) are 96-bit
+// multiply-accumulate chains (IMAD.WIDE.U32 with carry-out + IADD3.X), CH independent accumulators
+// per pass for ILP, the inner loop over the K inputs fully unrolled and the outer loop over output
+// tiles rolled, so the kernel body stays small enough for the instruction cache.
+// Every residue reduction uses the pseudo-Mersenne form m = 2^32 - c, c < 2^13.  Residues are kept
+// lazily in [0, 2^32) (congruent, not necessarily < m); DESIGN.md §3 shows the value bound
+// r < (K+3)N still holds, and the exit conversion canonicalises.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -24,18 +30,28 @@ namespace {  // everything below is private to this K's translation unit
 
 constexpr int K = MR_K;
 constexpr int NCH = 2 * K + 1;                // residues per value: B, B', m_r
-constexpr int CH = 8;                         // base-extension outputs per register tile
-constexpr int THREADS = 128;
-constexpr int MINB = K <= 9 ? 6 : (K <= 33 ? 4 : 2);
-constexpr int SMAX = (K + 3 <= 2) ? 0 : (32 - __builtin_clz((unsigned)(K + 3 - 1))) - 1;  // N·2^s, s ≤ SMAX
+constexpr int T = 128;                        // threads (messages) per CTA
+constexpr int CH = be_ch(K);                  // base-extension outputs per register tile
+constexpr int KF = (K / CH) * CH;             // outputs covered by full tiles
+constexpr int KT = K - KF;                    // tail tile
+constexpr u32 BEW = be_words(K);              // base-extension image words (smem)
+constexpr u32 BEH = be_half_words(K);         // BE1 part; BE2 follows
+constexpr int MINB = K <= 33 ? 4 : (K <= 65 ? 3 : 2);   // CTAs per SM the register budget targets
+constexpr int SMAX = (K + 3 <= 2) ? 0 : (32 - __builtin_clz((unsigned)(K + 3 - 1))) - 1;  // X < 2^(SMAX+1) N
+enum : u32 { MR_COMPOSITE_V = 0, MR_PROBABLY_PRIME_V = 1, MR_FACTOR_V = 2 };
 
 constexpr BaseLayout BL = base_layout(K);
 constexpr u32 O_C = BL.c, O_C2 = BL.c2, O_A1 = BL.A1, O_A1R = BL.A1r, O_A2 = BL.A2, O_A2R = BL.A2r;
 constexpr u32 O_C1 = BL.C1, O_PIN = BL.pin, O_MISC = BL.misc, O_MPL = BL.MpL, O_NMP = BL.NMp;
+constexpr u32 O_MIS = BL.MiS, O_MU = BL.MU, O_ONE = BL.ONE, O_ML = BL.ML;
 constexpr u32 BASE_WORDS = BL.words;
 constexpr u32 CXW = cx_words(K);
+constexpr u32 SMEM_STATE = NCH * T;           // words of per-CTA residue state
+constexpr size_t SMEM_BYTES = 4 * (size_t)(SMEM_STATE + BEW + CXW);   // state | BE image | context
 
 __constant__ u32 g_base[BASE_WORDS];
+
+#define GB(off) g_base[(off)]
 
 // ------------------------------------------------------------------ word arithmetic
 
@@ -50,37 +66,56 @@ __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) 
 
 // h·2^32 + l  ->  congruent value in [0, 2^32) modulo m = 2^32 - c  (c < 2^13)
 __device__ __forceinline__ u32 red64(u32 h, u32 l, u32 c) {
-    u64 u = (u64)h * c + l;                   // < 2^32 (c + 1)
-    u64 v = (u64)(u32)(u >> 32) * c + (u32)u; // < 2^32 + c^2
-    u32 vl = (u32)v;
-    return (v >> 32) ? vl + c : vl;           // 2^32 ≡ c; vl < c^2 then, so no wrap
+    const u64 u = (u64)h * c + l;                       // < 2^32 (c + 1)
+    const u64 v = (u64)(u32)(u >> 32) * c + (u32)u;     // < 2^32 + c^2
+    const u32 vl = (u32)v;
+    return (u32)(v >> 32) ? vl + c : vl;                // 2^32 ≡ c; vl < c^2 then, so no wrap
 }
 
 // hi·2^64 + mid·2^32 + lo -> congruent value in [0, 2^32), hi < 2^7, c2 = c^2
 __device__ __forceinline__ u32 red96(u32 hi, u32 mid, u32 lo, u32 c, u32 c2) {
-    u64 u = (u64)mid * c + lo;                // < 2^45 + 2^32
-    u = (u64)hi * c2 + u;                     // + < 2^33
-    u64 v = (u64)(u32)(u >> 32) * c + (u32)u; // < 2^27 + 2^32
-    u32 vl = (u32)v;
-    return (v >> 32) ? vl + c : vl;
+    u64 u = (u64)mid * c + lo;                          // < 2^45 + 2^32
+    u += (u64)hi * c2;                                  // < 2^33
+    const u64 v = (u64)(u32)(u >> 32) * c + (u32)u;     // < 2^27 + 2^32
+    const u32 vl = (u32)v;
+    return (u32)(v >> 32) ? vl + c : vl;
 }
 
 __device__ __forceinline__ u32 mulmod(u32 a, u32 b, u32 c) {
-    u64 p = (u64)a * b;
+    const u64 p = (u64)a * b;
     return red64((u32)(p >> 32), (u32)p, c);
 }
 
 __device__ __forceinline__ u32 canon(u32 x, u32 c) {  // lazy residue -> [0, m)
-    u32 m = 0u - c;
+    const u32 m = 0u - c;
     return x >= m ? x - m : x;
 }
 
-#define CC(ch) g_base[O_C + (ch)]
-#define CC2(ch) g_base[O_C2 + (ch)]
+__device__ __forceinline__ u32 &S(u32 *st, int ch) { return st[ch * T + threadIdx.x]; }
+
+// ------------------------------------------------------------------ per-modulus constant sources
+
+struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt): context block in smem
+    const u32 *cx;
+    __device__ u32 sigma(int i) const { return cx[cx_sigma(K) + i]; }
+    __device__ u32 c2(int j) const { return cx[cx_c2(K) + j]; }
+    __device__ u32 nminv() const { return cx[CX_NMINV_R]; }
+    __device__ u32 nlimb(int l) const { return cx[cx_n(K) + l]; }        // l in [0, K]
+};
+
+struct CtxThread {                    // one modulus per thread (Miller-Rabin): per-candidate rows
+    const u32 *pc;
+    const u32 *nrow;                  // candidate limbs
+    u32 stride, limbs;
+    __device__ u32 sigma(int i) const { return pc[(size_t)(pc_sigma(K) + i) * stride]; }
+    __device__ u32 c2(int j) const { return pc[(size_t)(pc_c2(K) + j) * stride]; }
+    __device__ u32 nminv() const { return pc[(size_t)pc_nminv(K) * stride]; }
+    __device__ u32 nlimb(int l) const { return (u32)l < limbs ? nrow[l] : 0u; }
+};
 
 // ------------------------------------------------------------------ RNS Montgomery multiplication
 //
-// a <- a · b · M^-1 (mod N), SURVEY §8(a6) / DESIGN.md §3, values < (K+3)N throughout.
+// st <- st · b · M^-1 (mod N), SURVEY §8(a6) / DESIGN.md §3, values < (K+3)N throughout.
 //   6.1/6.2  B:   ξ_i = (a_i b_i mod m_i) σ_i mod m_i,      σ_i = |-N^-1 M_i^-1|_{m_i}
 //            B':  t*_j = a*_j b*_j mod m'_j  (ξ-form operands)
 //            m_r: t_r = a_r b_r mod 2^32
@@ -89,158 +124,181 @@ __device__ __forceinline__ u32 canon(u32 x, u32 c) {  // lazy residue -> [0, m)
 //            r_r = (t_r + q̂_r N) M^-1 mod 2^32
 //   6.6  BE2 (exact, Shenoy-Kumaresan through m_r = 2^32): S_i = Σ_j ξ'_j |M'_j|_{m_i},
 //        α' = (Σ_j ξ'_j |M'_j|_{2^32} - r_r) M'^-1 mod 2^32,  r_i = S_i - α'|M'|_{m_i}
-// b is either a itself (square) or the vector at bp[c * bstride] (global window table or the
-// global context block).  cx = this CTA's context block in shared memory.
-__device__ __forceinline__ void mont_mul(u32 (&a)[NCH], const u32 *__restrict__ bp, u32 bstride, bool sq,
-                                         const u32 *__restrict__ cx) {
-    // ---- 6.1 / 6.2: channel products, q-digits
-#pragma unroll
+// b is st itself (square) or the vector at bp[c * bstride] (global window table or a constant
+// vector in shared memory).
+
+// Register tile of the base-extension contraction: W outputs as 96-bit accumulators; the K inputs
+// are read from shared-memory rows xr .. xr+K-1 of the state (one LDS per W MACs), the constants
+// from the tile's shared-memory image via 16-byte broadcast loads.  The loop over the inputs is
+// rolled (unrolled by UI) so the whole multiplication stays resident in the instruction cache.
+constexpr int UI = (K % 3 == 0) ? 3 : ((K % 5 == 0) ? 5 : ((K % 7 == 0) ? 7 : 4));
+template <int W>
+__device__ __forceinline__ void be_tile_acc(const u32 *st, int xr, const u32 *tile, u32 (&lo)[W], u32 (&mi)[W],
+                                            u32 (&hi)[W]) {
+    constexpr int Q = (W + 3) / 4;
+    const uint4 *tb = reinterpret_cast<const uint4 *>(tile);
+#pragma unroll UI
     for (int i = 0; i < K; i++) {
-        u32 b = sq ? a[i] : bp[(size_t)i * bstride];
-        u32 t = mulmod(a[i], b, CC(i));
-        a[i] = mulmod(t, cx[cx_sigma(K) + i], CC(i));
-    }
+        const u32 xi = st[(xr + i) * T + threadIdx.x];
 #pragma unroll
-    for (int j = 0; j < K; j++) {
-        u32 b = sq ? a[K + j] : bp[(size_t)(K + j) * bstride];
-        a[K + j] = mulmod(a[K + j], b, CC(K + j));
-    }
-    const u32 tr = a[2 * K] * (sq ? a[2 * K] : bp[(size_t)(2 * K) * bstride]);
-
-    // ---- 6.3 BE1, m_r column and r_r
-    u32 qr = 0;
-#pragma unroll
-    for (int i = 0; i < K; i++) qr += a[i] * g_base[O_A1R + i];
-    const u32 rr = tr * g_base[O_MISC + 0] + qr * cx[CX_NMINV_R];
-
-    // ---- 6.3 BE1 main [1 x K]·[K x K] contraction, CH outputs per pass; 6.4/6.5 fused in the epilogue
-#pragma unroll
-    for (int j0 = 0; j0 < K; j0 += CH) {
-        u32 lo[CH], mi[CH], hi[CH];
-#pragma unroll
-        for (int jj = 0; jj < CH; jj++) lo[jj] = mi[jj] = hi[jj] = 0;
-#pragma unroll
-        for (int i = 0; i < K; i++) {
-#pragma unroll
-            for (int jj = 0; jj < CH; jj++)
-                if (j0 + jj < K) mac96(lo[jj], mi[jj], hi[jj], a[i], g_base[O_A1 + i * K + j0 + jj]);
-        }
-#pragma unroll
-        for (int jj = 0; jj < CH; jj++) {
-            const int j = j0 + jj;
-            if (j < K) {
-                const u32 c = CC(K + j), c2 = CC2(K + j);
-                const u32 q = red96(hi[jj], mi[jj], lo[jj], c, c2);
-                u64 p = (u64)a[K + j] * g_base[O_C1 + j];
-                u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
-                mac96(l2, m2, h2, q, cx[cx_c2(K) + j]);
-                a[K + j] = red96(h2, m2, l2, c, c2);
-            }
-        }
-    }
-    a[2 * K] = rr;
-
-    // ---- 6.6 BE2 [1 x K]·[K x K] contraction, exact via the extra modulus
-    u32 sr = 0;
-#pragma unroll
-    for (int j = 0; j < K; j++) sr += a[K + j] * g_base[O_A2R + j];
-    const u32 alpha = (sr - rr) * g_base[O_MISC + 1];
-#pragma unroll
-    for (int i0 = 0; i0 < K; i0 += CH) {
-        u32 lo[CH], mi[CH], hi[CH];
-#pragma unroll
-        for (int ii = 0; ii < CH; ii++) {
-            if (i0 + ii < K) {
-                u64 p = (u64)alpha * g_base[O_PIN + i0 + ii];
-                lo[ii] = (u32)p;
-                mi[ii] = (u32)(p >> 32);
-                hi[ii] = 0;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < K; j++) {
-#pragma unroll
-            for (int ii = 0; ii < CH; ii++)
-                if (i0 + ii < K) mac96(lo[ii], mi[ii], hi[ii], a[K + j], g_base[O_A2 + j * K + i0 + ii]);
-        }
-#pragma unroll
-        for (int ii = 0; ii < CH; ii++) {
-            const int i = i0 + ii;
-            if (i < K) a[i] = red96(hi[ii], mi[ii], lo[ii], CC(i), CC2(i));
+        for (int q = 0; q < Q; q++) {
+            const uint4 v = tb[i * Q + q];
+            if (4 * q + 0 < W) mac96(lo[(4 * q + 0) % W], mi[(4 * q + 0) % W], hi[(4 * q + 0) % W], xi, v.x);
+            if (4 * q + 1 < W) mac96(lo[(4 * q + 1) % W], mi[(4 * q + 1) % W], hi[(4 * q + 1) % W], xi, v.y);
+            if (4 * q + 2 < W) mac96(lo[(4 * q + 2) % W], mi[(4 * q + 2) % W], hi[(4 * q + 2) % W], xi, v.z);
+            if (4 * q + 3 < W) mac96(lo[(4 * q + 3) % W], mi[(4 * q + 3) % W], hi[(4 * q + 3) % W], xi, v.w);
         }
     }
 }
 
+// BE1 tile: q̂_j for j in [j0, j0+W), then ξ'_j = t*_j C1_j + q̂_j C2_j (6.4/6.5) into row K+j;
+// also accumulates the m_r column of BE2, sr += ξ'_j |M'_j|_{2^32}.
+template <int W, class CS>
+__device__ __forceinline__ void be1_tile(int j0, const u32 *tile, u32 *st, const u32 *s_be, const CS &cs, u32 &sr) {
+    u32 lo[W], mi[W], hi[W];
+#pragma unroll
+    for (int jj = 0; jj < W; jj++) lo[jj] = mi[jj] = hi[jj] = 0;
+    be_tile_acc<W>(st, 0, tile, lo, mi, hi);
+#pragma unroll
+    for (int jj = 0; jj < W; jj++) {
+        const int j = j0 + jj;
+        const u32 c = s_be[bev_c(K) + K + j], c2 = s_be[bev_c2(K) + K + j];
+        const u32 q = red96(hi[jj], mi[jj], lo[jj], c, c2);
+        const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
+        u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
+        mac96(l2, m2, h2, q, cs.c2(j));
+        const u32 xp = red96(h2, m2, l2, c, c2);
+        S(st, K + j) = xp;
+        sr += xp * s_be[bev_A2r(K) + j];
+    }
+}
+
+// BE2 tile: r_i for i in [i0, i0+W) into row i (the inputs ξ' are rows K..2K-1).
+template <int W>
+__device__ __forceinline__ void be2_tile(int i0, const u32 *tile, u32 alpha, u32 *st, const u32 *s_be) {
+    u32 lo[W], mi[W], hi[W];
+#pragma unroll
+    for (int ii = 0; ii < W; ii++) {
+        const u64 p = (u64)alpha * s_be[bev_pin(K) + i0 + ii];
+        lo[ii] = (u32)p;
+        mi[ii] = (u32)(p >> 32);
+        hi[ii] = 0;
+    }
+    be_tile_acc<W>(st, K, tile, lo, mi, hi);
+#pragma unroll
+    for (int ii = 0; ii < W; ii++) {
+        const int i = i0 + ii;
+        S(st, i) = red96(hi[ii], mi[ii], lo[ii], s_be[bev_c(K) + i], s_be[bev_c2(K) + i]);
+    }
+}
+
+template <class CS>
+__device__ __forceinline__ void mont_mul(u32 *st, const u32 *__restrict__ bp, u32 bstride, bool sq, const CS &cs,
+                                         const u32 *s_be) {
+    // ---- 6.1 / 6.2: channel products; q-digits ξ_i overwrite a_i; m_r column of BE1 on the fly
+    u32 qr = 0;
+#pragma unroll 3
+    for (int i = 0; i < K; i++) {
+        const u32 a = S(st, i);
+        const u32 b = sq ? a : bp[(size_t)i * bstride];
+        const u32 c = s_be[bev_c(K) + i];
+        const u32 xi = mulmod(mulmod(a, b, c), cs.sigma(i), c);
+        S(st, i) = xi;
+        qr += xi * s_be[bev_A1r(K) + i];
+    }
+#pragma unroll 3
+    for (int j = 0; j < K; j++) {
+        const u32 a = S(st, K + j);
+        const u32 b = sq ? a : bp[(size_t)(K + j) * bstride];
+        S(st, K + j) = mulmod(a, b, s_be[bev_c(K) + K + j]);
+    }
+    const u32 ar = S(st, 2 * K);
+    const u32 tr = ar * (sq ? ar : bp[(size_t)(2 * K) * bstride]);
+    const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();       // 6.4 on m_r
+    // ---- 6.3-6.5 BE1 [1 x K]·[K x K] contraction, CH outputs per tile, ξ' epilogue
+    u32 sr = 0;
+#pragma unroll 1
+    for (int t = 0; t < KF / CH; t++) be1_tile<CH>(t * CH, s_be + t * K * pad4(CH), st, s_be, cs, sr);
+    if (KT) be1_tile<KT ? KT : 1>(KF, s_be + (KF / CH) * K * pad4(CH), st, s_be, cs, sr);
+    // ---- 6.6 BE2 [1 x K]·[K x K] contraction, exact through the extra modulus
+    const u32 alpha = (sr - rr) * GB(O_MISC + 1);
+    S(st, 2 * K) = rr;
+#pragma unroll 1
+    for (int t = 0; t < KF / CH; t++) be2_tile<CH>(t * CH, s_be + BEH + t * K * pad4(CH), alpha, st, s_be);
+    if (KT) be2_tile<KT ? KT : 1>(KF, s_be + BEH + (KF / CH) * K * pad4(CH), alpha, st, s_be);
+}
+
 // ------------------------------------------------------------------ positional -> RNS (a2)
-// a_c = Σ_l x_l |2^(32 l)|_{m_c} (B' entries of pow_tab already carry λ_j: ξ-form), a_r = x_0.
-// Limbs are masked to zero when `ok` is false (out-of-range inputs run on x = 0).
-__device__ __forceinline__ void to_rns(u32 (&a)[NCH], const u32 *__restrict__ x, u32 nl, bool ok,
+// st_c = Σ_l x_l |2^(32 l)|_{m_c} (B' entries of pow_tab carry λ_j: ξ-form), st_r = x_0.
+// x is read at x[l * xstride]; limbs are masked to zero when `ok` is false.
+__device__ __forceinline__ void to_rns(u32 *st, const u32 *__restrict__ x, u32 xstride, u32 nl, bool ok,
                                        const u32 *__restrict__ pow_tab) {
     const u32 mask = ok ? 0xFFFFFFFFu : 0u;
+    constexpr int W = 8;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 2 * K; c0 += W) {
+        u32 lo[W], mi[W], hi[W];
 #pragma unroll
-    for (int c0 = 0; c0 < 2 * K; c0 += CH) {
-        u32 lo[CH], mi[CH], hi[CH];
-#pragma unroll
-        for (int jj = 0; jj < CH; jj++) lo[jj] = mi[jj] = hi[jj] = 0;
+        for (int jj = 0; jj < W; jj++) lo[jj] = mi[jj] = hi[jj] = 0;
 #pragma unroll 1
         for (u32 l = 0; l < nl; l++) {
-            const u32 xl = x[l] & mask;
+            const u32 xl = x[(size_t)l * xstride] & mask;
             const u32 *pr = pow_tab + (size_t)l * (2 * K) + c0;
 #pragma unroll
-            for (int jj = 0; jj < CH; jj++)
+            for (int jj = 0; jj < W; jj++)
                 if (c0 + jj < 2 * K) mac96(lo[jj], mi[jj], hi[jj], xl, __ldg(pr + jj));
         }
 #pragma unroll
-        for (int jj = 0; jj < CH; jj++)
-            if (c0 + jj < 2 * K) a[c0 + jj] = red96(hi[jj], mi[jj], lo[jj], CC(c0 + jj), CC2(c0 + jj));
+        for (int jj = 0; jj < W; jj++)
+            if (c0 + jj < 2 * K) S(st, c0 + jj) = red96(hi[jj], mi[jj], lo[jj], GB(O_C + c0 + jj), GB(O_C2 + c0 + jj));
     }
-    a[2 * K] = x[0] & mask;
+    S(st, 2 * K) = x[0] & mask;
 }
 
 // ------------------------------------------------------------------ RNS -> positional, canonical (a7)
 // z on B' ∪ {m_r}, z < (K+3)N < M': α' = (Σ ξ'_j |M'_j|_{2^32} - z_r) M'^-1 mod 2^32 (exact, P:42
 // "provided an extra modulus"), X = Σ_j ξ'_j M'_j + α'(2^(32(K+1)) - M') mod 2^(32(K+1)) = z, then
-// X mod N by conditional subtraction of N·2^s, s = SMAX..0.  Writes X[0..K].
-__device__ __forceinline__ void from_rns(const u32 (&a)[NCH], const u32 *__restrict__ nlimbs, u32 (&X)[K + 1]) {
+// X mod N by conditional subtraction of N·2^s, s = SMAX..0.  Leaves X in st[0..K] (limb l in row l).
+template <class CS>
+__device__ __forceinline__ void from_rns(u32 *st, const CS &cs) {
+    u32 x[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) x[j] = S(st, K + j);
     u32 sr = 0;
 #pragma unroll
-    for (int j = 0; j < K; j++) sr += a[K + j] * g_base[O_A2R + j];
-    const u32 alpha = (sr - a[2 * K]) * g_base[O_MISC + 1];
+    for (int j = 0; j < K; j++) sr += x[j] * GB(O_A2R + j);
+    const u32 alpha = (sr - S(st, 2 * K)) * GB(O_MISC + 1);
     u32 clo = 0, cmi = 0;
-#pragma unroll
+#pragma unroll 1
     for (int l = 0; l <= K; l++) {
         u32 lo = clo, mi = cmi, hi = 0;
 #pragma unroll
-        for (int j = 0; j < K; j++) mac96(lo, mi, hi, a[K + j], g_base[O_MPL + j * (K + 1) + l]);
-        mac96(lo, mi, hi, alpha, g_base[O_NMP + l]);
-        X[l] = lo;
+        for (int j = 0; j < K; j++) mac96(lo, mi, hi, x[j], GB(O_MPL + j * (K + 1) + l));
+        mac96(lo, mi, hi, alpha, GB(O_NMP + l));
+        S(st, l) = lo;
         clo = mi;
         cmi = hi;
     }
-    // X < 2^(SMAX+1) N  ->  X mod N
 #pragma unroll 1
     for (int s = SMAX; s >= 0; s--) {
-        u32 Y[K + 1];
-        u32 borrow = 0;
-#pragma unroll
-        for (int l = 0; l <= K; l++) {
-            const u32 cur = nlimbs[l];
-            const u32 prev = l ? nlimbs[l - 1] : 0u;
-            const u32 nsh = s ? ((cur << s) | (prev >> (32 - s))) : cur;
-            const u64 t = (u64)X[l] - nsh - borrow;
-            Y[l] = (u32)t;
-            borrow = (u32)(t >> 63);
-        }
-        if (!borrow) {
-#pragma unroll
-            for (int l = 0; l <= K; l++) X[l] = Y[l];
+#pragma unroll 1
+        for (int pass = 0; pass < 2; pass++) {   // pass 0: borrow of X - N·2^s; pass 1: subtract
+            u32 br = 0;
+#pragma unroll 1
+            for (int l = 0; l <= K; l++) {
+                const u32 nsh = __funnelshift_l(l ? cs.nlimb(l - 1) : 0u, cs.nlimb(l), s);
+                const u64 t = (u64)S(st, l) - nsh - br;
+                if (pass) S(st, l) = (u32)t;
+                br = (u32)(t >> 63);
+            }
+            if (br) break;
         }
     }
 }
 
 // x (nl limbs) < bound (nl limbs)?
 __device__ __forceinline__ bool less_than(const u32 *__restrict__ x, const u32 *__restrict__ bound, u32 nl) {
-    int res = 0;  // -1 less, 1 greater, 0 equal so far (scan from the top)
+    int res = 0;
 #pragma unroll 1
     for (int l = (int)nl - 1; l >= 0 && res == 0; l--) {
         const u32 xv = x[l], bv = bound[l];
@@ -250,15 +308,21 @@ __device__ __forceinline__ bool less_than(const u32 *__restrict__ x, const u32 *
 }
 
 // ------------------------------------------------------------------ modexp interpreter kernel (a2-a7, a8 ladders)
-__global__ void __launch_bounds__(THREADS, MINB) k_modexp(const ModexpParams P) {
-    __shared__ u32 s_cx[CXW];
+__global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
+    extern __shared__ __align__(16) u32 smem[];
+    u32 *st = smem;
+    u32 *s_be = smem + SMEM_STATE;
+    u32 *s_cx = s_be + BEW;
     const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
     const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
-    for (u32 w = threadIdx.x; w < CXW; w += blockDim.x) s_cx[w] = gcx[w];
+    for (u32 w = threadIdx.x; w < CXW; w += T) s_cx[w] = gcx[w];
+    for (u32 w = threadIdx.x; w < BEW / 4; w += T)
+        reinterpret_cast<uint4 *>(s_be)[w] = __ldg(reinterpret_cast<const uint4 *>(P.be_tab) + w);
     __syncthreads();
-    const u32 jl = (blockIdx.x - sel * P.ctas0) * blockDim.x + threadIdx.x;
+    const u32 jl = (blockIdx.x - sel * P.ctas0) * T + threadIdx.x;
     if (jl >= P.count) return;
-    const u32 slot = sel * P.ctas0 * blockDim.x + jl;
+    const CtxSmem cs{s_cx};
+    const u32 slot = sel * P.ctas0 * T + jl;
     const size_t tstride = P.jobs_total;
     const size_t entry = (size_t)NCH * tstride;
     const u32 *xrow = P.x + (size_t)jl * P.in_limbs;
@@ -267,161 +331,130 @@ __global__ void __launch_bounds__(THREADS, MINB) k_modexp(const ModexpParams P) 
 
     const u64 *prog = sel ? P.prog[1] : P.prog[0];
     const u32 nops = sel ? P.nops[1] : P.nops[0];
-    u32 a[NCH];
-#pragma unroll
-    for (int c = 0; c < NCH; c++) a[c] = 0;
-
 #pragma unroll 1
     for (u32 s = 0; s < nops; s++) {
         const u64 op = __ldg(prog + s);
         const u32 fl = (u32)op & 0xFF, opnd = (u32)(op >> 8) & 0xFF, ld = (u32)(op >> 16) & 0xFF;
-        const u32 ad = (u32)(op >> 24) & 0xFF, st = (u32)(op >> 32) & 0xFF;
+        const u32 ad = (u32)(op >> 24) & 0xFF, sto = (u32)(op >> 32) & 0xFF;
         if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) {
             const u32 off = (fl & OPF_TORNS_HI) ? P.half : 0u;
             const u32 nl = (fl & OPF_TORNS_ALL) ? P.in_limbs : P.half;
-            to_rns(a, xrow + off, nl, ok, P.pow_tab);
+            to_rns(st, xrow + off, 1, nl, ok, P.pow_tab);
         }
         if (fl & OPF_LOAD) {
             const u32 *src;
             size_t str;
-            if (ld >= 0xF0) { src = gcx + cx_r2(K) + (ld - 0xF0) * NCH; str = 1; }
+            if (ld >= 0xF0) { src = s_cx + cx_r2(K) + (ld - 0xF0) * NCH; str = 1; }
             else { src = P.table + ld * entry + slot; str = tstride; }
-#pragma unroll
-            for (int c = 0; c < NCH; c++) a[c] = src[c * str];
+#pragma unroll 1
+            for (int c = 0; c < NCH; c++) S(st, c) = src[c * str];
         }
         if (!(fl & OPF_NOMUL)) {
             const bool sq = opnd == OPND_SQ;
             const u32 *bp;
             u32 bs;
-            if (sq) { bp = gcx; bs = 0; }
-            else if (opnd >= 0xF0) { bp = gcx + cx_r2(K) + (opnd - 0xF0) * NCH; bs = 1; }
+            if (sq) { bp = s_cx; bs = 0; }
+            else if (opnd >= 0xF0) { bp = s_cx + cx_r2(K) + (opnd - 0xF0) * NCH; bs = 1; }
             else { bp = P.table + opnd * entry + slot; bs = (u32)tstride; }
-            mont_mul(a, bp, bs, sq, s_cx);
+            mont_mul(st, bp, bs, sq, cs, s_be);
         }
         if (fl & OPF_ADD) {  // channel-wise modular addition (CRT entry, a3)
             const u32 *src = P.table + ad * entry + slot;
-#pragma unroll
+#pragma unroll 1
             for (int c = 0; c < 2 * K; c++) {
                 const u32 b = src[c * tstride];
-                const u32 s2 = a[c] + b;
-                a[c] = red64(s2 < b ? 1u : 0u, s2, CC(c));
+                const u32 s2 = S(st, c) + b;
+                S(st, c) = red64(s2 < b ? 1u : 0u, s2, GB(O_C + c));
             }
-            a[2 * K] += src[(2 * K) * tstride];
+            S(st, 2 * K) += src[(2 * K) * tstride];
         }
         if (fl & OPF_STORE) {
-            u32 *dst = P.table + st * entry + slot;
-#pragma unroll
-            for (int c = 0; c < NCH; c++) dst[c * tstride] = a[c];
+            u32 *dst = P.table + sto * entry + slot;
+#pragma unroll 1
+            for (int c = 0; c < NCH; c++) dst[c * tstride] = S(st, c);
         }
     }
-    u32 X[K + 1];
-    from_rns(a, s_cx + cx_n(K), X);
+    from_rns(st, cs);
     u32 *yrow = P.y + sel * P.out_stride + (size_t)jl * P.out_limbs;
-#pragma unroll
-    for (int l = 0; l <= K; l++)
-        if ((u32)l < P.out_limbs) yrow[l] = ok ? X[l] : 0u;
+#pragma unroll 1
+    for (u32 l = 0; l < P.out_limbs; l++) yrow[l] = ok ? S(st, l) : 0u;
 }
 
 // ------------------------------------------------------------------ CRT recombination (a8)
 // m = m_q + q · h,  h = (m_p - m_q mod p) · qinv mod p computed as one RNS Montgomery
-// multiplication by qinv·R mod p followed by the canonical exit.
-__global__ void __launch_bounds__(THREADS, MINB) k_combine(const CombineParams P) {
-    __shared__ u32 s_cx[CXW];
-    for (u32 w = threadIdx.x; w < CXW; w += blockDim.x) s_cx[w] = P.ctx_p[w];
+// multiplication by qinv·R mod p followed by the canonical exit.  The output row doubles as
+// positional scratch (it is overwritten by m at the end).
+__global__ void __launch_bounds__(T, MINB) k_combine(const CombineParams P) {
+    extern __shared__ __align__(16) u32 smem[];
+    u32 *st = smem;
+    u32 *s_be = smem + SMEM_STATE;
+    u32 *s_cx = s_be + BEW;
+    for (u32 w = threadIdx.x; w < CXW; w += T) s_cx[w] = P.ctx_p[w];
+    for (u32 w = threadIdx.x; w < BEW / 4; w += T)
+        reinterpret_cast<uint4 *>(s_be)[w] = __ldg(reinterpret_cast<const uint4 *>(P.be_tab) + w);
     __syncthreads();
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 i = blockIdx.x * T + threadIdx.x;
     if (i >= P.count) return;
+    const CtxSmem cs{s_cx};
     const u32 H = P.half;
     const u32 *mp = P.mpq + (size_t)i * H;
     const u32 *mq = P.mpq + ((size_t)P.count + i) * H;
-    const u32 *pl = s_cx + cx_n(K);
-    // t = m_q mod p  (m_q < q < 2^(32H) ≤ 2^32 p): conditional subtraction of p·2^s, s = 32..0
-    u32 t[K + 1];
-#pragma unroll
-    for (int l = 0; l <= K; l++) t[l] = (u32)l < H ? mq[l] : 0u;
+    u32 *mrow = P.m + (size_t)i * 2 * H;
+    // t = m_q mod p in st rows [0, H]:  m_q < 2^(32H) <= 2^32 p, subtract p·2^s for s = 32..0
+#pragma unroll 1
+    for (u32 l = 0; l <= H; l++) S(st, l) = l < H ? mq[l] : 0u;
 #pragma unroll 1
     for (int s = 32; s >= 0; s--) {
-        u32 Y[K + 1];
-        u32 borrow = 0;
-#pragma unroll
-        for (int l = 0; l <= K; l++) {
-            u32 nsh;
-            if (s == 32) nsh = l ? pl[l - 1] : 0u;
-            else {
-                const u32 prev = l ? pl[l - 1] : 0u;
-                nsh = s ? ((pl[l] << s) | (prev >> (32 - s))) : pl[l];
+#pragma unroll 1
+        for (int pass = 0; pass < 2; pass++) {
+            u32 br = 0;
+#pragma unroll 1
+            for (u32 l = 0; l <= H; l++) {
+                u32 nsh;
+                if (s == 32) nsh = l ? cs.nlimb(l - 1) : 0u;
+                else nsh = __funnelshift_l(l ? cs.nlimb(l - 1) : 0u, cs.nlimb(l), s);
+                const u64 t = (u64)S(st, l) - nsh - br;
+                if (pass) S(st, l) = (u32)t;
+                br = (u32)(t >> 63);
             }
-            const u64 d = (u64)t[l] - nsh - borrow;
-            Y[l] = (u32)d;
-            borrow = (u32)(d >> 63);
-        }
-        if (!borrow) {
-#pragma unroll
-            for (int l = 0; l <= K; l++) t[l] = Y[l];
+            if (br) break;   // pass 0 found t < p·2^s: skip the subtraction
         }
     }
-    // diff = m_p - t mod p  (both < p)
-    u32 diff[K + 1];
-    u32 borrow = 0;
-#pragma unroll
-    for (int l = 0; l <= K; l++) {
-        const u64 d = (u64)((u32)l < H ? mp[l] : 0u) - t[l] - borrow;
-        diff[l] = (u32)d;
-        borrow = (u32)(d >> 63);
+    // diff = m_p - t mod p -> mrow[0, H)
+    u32 br = 0;
+#pragma unroll 1
+    for (u32 l = 0; l < H; l++) {
+        const u64 d = (u64)mp[l] - S(st, l) - br;
+        mrow[l] = (u32)d;
+        br = (u32)(d >> 63);
     }
-    if (borrow) {
+    if (br) {
         u32 carry = 0;
-#pragma unroll
-        for (int l = 0; l <= K; l++) {
-            const u64 s2 = (u64)diff[l] + pl[l] + carry;
-            diff[l] = (u32)s2;
+#pragma unroll 1
+        for (u32 l = 0; l < H; l++) {
+            const u64 s2 = (u64)mrow[l] + cs.nlimb(l) + carry;
+            mrow[l] = (u32)s2;
             carry = (u32)(s2 >> 32);
         }
     }
-    // h = diff · qinv mod p in RNS:  mm(diff, qinv R mod p) = diff qinv (mod p)
-    u32 a[NCH];
-    {
-        // to_rns of a register-resident number: reuse the table contraction on a local copy
-        const u32 mask = 0xFFFFFFFFu;
-#pragma unroll
-        for (int c0 = 0; c0 < 2 * K; c0 += CH) {
-            u32 lo[CH], mi[CH], hi[CH];
-#pragma unroll
-            for (int jj = 0; jj < CH; jj++) lo[jj] = mi[jj] = hi[jj] = 0;
-#pragma unroll
-            for (int l = 0; l <= K; l++) {
-                if ((u32)l < H) {
-                    const u32 *pr = P.pow_tab + (size_t)l * (2 * K) + c0;
-#pragma unroll
-                    for (int jj = 0; jj < CH; jj++)
-                        if (c0 + jj < 2 * K) mac96(lo[jj], mi[jj], hi[jj], diff[l] & mask, __ldg(pr + jj));
-                }
-            }
-#pragma unroll
-            for (int jj = 0; jj < CH; jj++)
-                if (c0 + jj < 2 * K) a[c0 + jj] = red96(hi[jj], mi[jj], lo[jj], CC(c0 + jj), CC2(c0 + jj));
-        }
-        a[2 * K] = diff[0];
-    }
-    mont_mul(a, P.ctx_p + cx_qinvr(K), 1, false, s_cx);
-    u32 h[K + 1];
-    from_rns(a, pl, h);
+    // h = diff · qinv mod p in RNS:  mm(diff, qinv R mod p) ≡ diff qinv (mod p), then canonical
+    to_rns(st, mrow, 1, H, true, P.pow_tab);
+    mont_mul(st, s_cx + cx_qinvr(K), 1, false, cs, s_be);
+    from_rns(st, cs);
     // m = m_q + q · h  (schoolbook, H x H limbs)
-    u32 *mrow = P.m + (size_t)i * 2 * H;
 #pragma unroll 1
     for (u32 l = 0; l < 2 * H; l++) mrow[l] = l < H ? mq[l] : 0u;
 #pragma unroll 1
     for (u32 r = 0; r < H; r++) {
         const u32 qr = P.q[r];
         u32 carry = 0;
-#pragma unroll
-        for (int l = 0; l < K; l++) {
-            if ((u32)l < H) {
-                const u64 v = (u64)qr * h[l] + mrow[r + l] + carry;
-                mrow[r + l] = (u32)v;
-                carry = (u32)(v >> 32);
-            }
+#pragma unroll 1
+        for (u32 l = 0; l < H; l++) {
+            const u64 v = (u64)qr * S(st, l) + mrow[r + l] + carry;
+            mrow[r + l] = (u32)v;
+            carry = (u32)(v >> 32);
         }
+#pragma unroll 1
         for (u32 l = r + H; l < 2 * H && carry; l++) {
             const u64 v = (u64)mrow[l] + carry;
             mrow[l] = (u32)v;
@@ -429,30 +462,301 @@ __global__ void __launch_bounds__(THREADS, MINB) k_combine(const CombineParams P
         }
     }
     if (P.status && P.status[i] != 0) {
+#pragma unroll 1
         for (u32 l = 0; l < 2 * H; l++) mrow[l] = 0;
     }
 }
 
+// ------------------------------------------------------------------ Miller-Rabin (a9)
+// Per candidate n (one thread), §3.2 "primality testing in the Montgomery domain ... a
+// Miller-Rabin test with a user-parameterized number of iterations", HAC Alg. 4.24.
+
+// word inverse modulo the prime m = 2^32 - c by Fermat: x^(m-2)  (per-channel inversion)
+__device__ __forceinline__ u32 inv_word(u32 x, u32 c) {
+    const u32 e = 0u - c - 2u;
+    u32 r = 1, b = x;
+#pragma unroll 1
+    for (int bit = 0; bit < 32; bit++) {
+        if ((e >> bit) & 1u) r = mulmod(r, b, c);
+        b = mulmod(b, b, c);
+    }
+    return canon(r, c);
+}
+
+// smem-row positional helpers for the setup kernel (row l of a value at v[l * T + tid])
+__device__ __forceinline__ u32 &R(u32 *v, u32 l) { return v[l * T + threadIdx.x]; }
+
+// v = 2 v + bit; if v >= n: v -= n   (v < n on entry; L + 1 rows)
+__device__ __forceinline__ void dbl_sub(u32 *v, u32 bit, const u32 *nrow, u32 L) {
+    u32 carry = bit;
+#pragma unroll 1
+    for (u32 l = 0; l <= L; l++) {
+        const u32 cur = R(v, l);
+        R(v, l) = (cur << 1) | carry;
+        carry = cur >> 31;
+    }
+#pragma unroll 1
+    for (int pass = 0; pass < 2; pass++) {
+        u32 br = 0;
+#pragma unroll 1
+        for (u32 l = 0; l <= L; l++) {
+            const u64 t = (u64)R(v, l) - (l < L ? nrow[l] : 0u) - br;
+            if (pass) R(v, l) = (u32)t;
+            br = (u32)(t >> 63);
+        }
+        if (br) break;
+    }
+}
+
+// v = v + w; if v >= n: v -= n   (v, w < n)
+__device__ __forceinline__ void add_sub(u32 *v, const u32 *w, const u32 *nrow, u32 L) {
+    u32 carry = 0;
+#pragma unroll 1
+    for (u32 l = 0; l <= L; l++) {
+        const u64 t = (u64)R(v, l) + R(const_cast<u32 *>(w), l) + carry;
+        R(v, l) = (u32)t;
+        carry = (u32)(t >> 32);
+    }
+#pragma unroll 1
+    for (int pass = 0; pass < 2; pass++) {
+        u32 br = 0;
+#pragma unroll 1
+        for (u32 l = 0; l <= L; l++) {
+            const u64 t = (u64)R(v, l) - (l < L ? nrow[l] : 0u) - br;
+            if (pass) R(v, l) = (u32)t;
+            br = (u32)(t >> 63);
+        }
+        if (br) break;
+    }
+}
+
+// setup: residues of n, FACTOR check, σ_i, |n M^-1 λ_j|, n M^-1 mod 2^32, s, d, R^2 = M^2 mod n
+__global__ void __launch_bounds__(T) k_mr_setup(const MrParams P) {
+    extern __shared__ __align__(16) u32 smem[];
+    u32 *st = smem;
+    const u32 i = blockIdx.x * T + threadIdx.x;
+    if (i >= P.count) return;
+    const u32 L = P.limbs;
+    const u32 *nrow = P.n + (size_t)i * L;
+    u32 *pc = P.pc + i;
+    const size_t cs = P.count;
+    int32_t status = 0;
+    u32 live = 1;
+    u32 verdict = MR_COMPOSITE_V;
+    u32 nz = 0;                                    // input rules: n odd, n >= 5
+    for (u32 l = 1; l < L; l++) nz |= nrow[l];
+    const bool small = nz == 0;                    // n < 2^32
+    if (!(nrow[0] & 1u) || (small && nrow[0] < 5u)) { status = 5; live = 0; }
+    if (live) {
+        to_rns(st, nrow, 1, L, true, P.pow_tab);
+        bool factor = false;
+#pragma unroll 1
+        for (int c = 0; c < 2 * K; c++) factor |= canon(S(st, c), GB(O_C + c)) == 0u;
+        if (factor) {
+            live = 0;
+            if (small) { status = 3; verdict = MR_PROBABLY_PRIME_V; }   // n is itself a base prime
+            else verdict = MR_FACTOR_V;                                 // reading R14
+        }
+    }
+    if (live) {
+#pragma unroll 1
+        for (int j = 0; j < K; j++) {              // |n M^-1 λ_j| = (n λ_j) μ_j  (ξ-form residue)
+            const u32 c = GB(O_C + K + j);
+            pc[(size_t)(pc_c2(K) + j) * cs] = canon(mulmod(S(st, K + j), GB(O_MU + j), c), c);
+        }
+        pc[(size_t)pc_nminv(K) * cs] = S(st, 2 * K) * GB(O_MISC + 0);
+#pragma unroll 1
+        for (int k = 0; k < K; k++) {              // σ_i = -(n M_i)^-1 mod m_i
+            const u32 c = GB(O_C + k);
+            const u32 v = inv_word(canon(mulmod(S(st, k), GB(O_MIS + k), c), c), c);
+            pc[(size_t)(pc_sigma(K) + k) * cs] = v ? (0u - c) - v : 0u;
+        }
+        // s, d with n - 1 = 2^s d
+        u32 l0 = 0, w0 = nrow[0] & ~1u;
+        while (w0 == 0 && l0 + 1 < L) w0 = nrow[++l0];
+        const u32 s = 32 * l0 + __ffs(w0) - 1;
+        const u32 ls = s / 32, bs = s % 32;
+#pragma unroll 1
+        for (u32 l = 0; l < (u32)K; l++) {
+            const u32 a0 = l + ls < L ? nrow[l + ls] : 0u;
+            const u32 a1 = l + ls + 1 < L ? nrow[l + ls + 1] : 0u;
+            pc[(size_t)(pc_d(K) + l) * cs] = __funnelshift_r(l + ls == 0 ? (a0 & ~1u) : a0, a1, bs);
+        }
+        pc[(size_t)pc_s(K) * cs] = s;
+        // R^2 = M^2 mod n, positional in smem rows: rho = M mod n (bit-serial over M), then
+        // rho^2 mod n by double-and-add over the bits of rho (values < n < 2^(32L), L <= K - 1)
+        u32 *rho = st;                 // rows [0, L]
+        u32 *acc = st + (K + 1) * T;   // rows [K+1, K+1+L]
+#pragma unroll 1
+        for (u32 l = 0; l <= L; l++) R(rho, l) = 0;
+#pragma unroll 1
+        for (int b = 32 * (K + 1) - 1; b >= 0; b--) dbl_sub(rho, (GB(O_ML + b / 32) >> (b % 32)) & 1u, nrow, L);
+#pragma unroll 1
+        for (u32 l = 0; l <= L; l++) R(acc, l) = 0;
+#pragma unroll 1
+        for (int b = 32 * L - 1; b >= 0; b--) {
+            dbl_sub(acc, 0, nrow, L);
+            if ((R(rho, b / 32) >> (b % 32)) & 1u) add_sub(acc, rho, nrow, L);
+        }
+        // positional R^2 -> pc rows (scratch) -> RNS -> pc rows
+        u32 *r2 = pc + (size_t)pc_r2(K) * cs;
+#pragma unroll 1
+        for (u32 l = 0; l < L; l++) r2[l * cs] = R(acc, l);
+        to_rns(st, r2, (u32)cs, L, true, P.pow_tab);
+#pragma unroll 1
+        for (int c = 0; c < NCH; c++) r2[c * cs] = S(st, c);
+    }
+    pc[(size_t)pc_live(K) * cs] = live;
+    P.verdict[i] = (uint8_t)verdict;
+    if (P.witness) P.witness[i] = -1;
+    if (P.status) P.status[i] = status;
+}
+
+// canonical X in st rows [0, K] vs 1 and n - 1
+__device__ __forceinline__ bool x_is_one(u32 *st) {
+    u32 nz = S(st, 0) ^ 1u;
+#pragma unroll 1
+    for (int l = 1; l <= K; l++) nz |= S(st, l);
+    return nz == 0;
+}
+__device__ __forceinline__ bool x_is_nm1(u32 *st, const u32 *nrow, u32 L) {
+    u32 diff = S(st, 0) ^ (nrow[0] - 1u);          // n odd: n - 1 only changes limb 0
+#pragma unroll 1
+    for (u32 l = 1; l <= (u32)K; l++) diff |= S(st, l) ^ (l < L ? nrow[l] : 0u);
+    return diff == 0;
+}
+
+// one thread per candidate, all rounds; early exit per candidate unless P.forced
+__global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
+    extern __shared__ __align__(16) u32 smem[];
+    u32 *st = smem;
+    u32 *s_be = smem + SMEM_STATE;
+    u32 *s_one = s_be + BEW;
+    for (u32 w = threadIdx.x; w < (u32)NCH; w += T) s_one[w] = GB(O_ONE + w);
+    for (u32 w = threadIdx.x; w < BEW / 4; w += T)
+        reinterpret_cast<uint4 *>(s_be)[w] = __ldg(reinterpret_cast<const uint4 *>(P.be_tab) + w);
+    __syncthreads();
+    const u32 i = blockIdx.x * T + threadIdx.x;
+    if (i >= P.count) return;
+    const size_t cnt = P.count;
+    const u32 *pcol = P.pc + i;
+    if (!pcol[(size_t)pc_live(K) * cnt]) return;
+    const u32 L = P.limbs;
+    const u32 *nrow = P.n + (size_t)i * L;
+    const CtxThread cs{pcol, nrow, (u32)cnt, L};
+    const u32 w = P.window, E = 1u << w;
+    const size_t entry = (size_t)NCH * cnt;
+    u32 *tab = P.table + i;                       // slot e at tab + e * entry, channel c at + c * cnt
+    u32 *stash = tab + E * entry;
+    const u32 *r2 = pcol + (size_t)pc_r2(K) * cnt;
+    const u32 s = pcol[(size_t)pc_s(K) * cnt];
+    const u32 *dl = pcol + (size_t)pc_d(K) * cnt;
+    u32 verdict = MR_PROBABLY_PRIME_V;
+    int witness = -1;
+    int32_t status = 0;
+    const u32 ndig = (32 * L + w - 1) / w;        // fixed-window schedule over a padded exponent
+#pragma unroll 1
+    for (u32 r = 0; r < P.rounds; r++) {
+        const u32 *a = P.bases + ((size_t)i * P.rounds + r) * L;
+        {   // base rule: 2 <= a <= n - 2, i.e. a >= 2 and d = n - a >= 2 without borrow
+            u32 br = 0, dhi = 0, ahi = 0, d0 = 0;
+#pragma unroll 1
+            for (u32 l = 0; l < L; l++) {
+                const u64 t = (u64)nrow[l] - a[l] - br;
+                br = (u32)(t >> 63);
+                if (l) { dhi |= (u32)t; ahi |= a[l]; } else d0 = (u32)t;
+            }
+            const bool a_ge2 = ahi || a[0] >= 2u;
+            const bool d_ge2 = !br && (dhi || d0 >= 2u);
+            if (!a_ge2 || !d_ge2) { status = 5; verdict = MR_COMPOSITE_V; break; }
+        }
+        // table: T[0] = 1~ = mm(R^2, 1), T[1] = ã = mm(a, R^2), T[e] = T[e-1] ã
+#pragma unroll 1
+        for (int c = 0; c < NCH; c++) S(st, c) = r2[(size_t)c * cnt];
+        mont_mul(st, s_one, 1, false, cs, s_be);
+#pragma unroll 1
+        for (int c = 0; c < NCH; c++) tab[(size_t)c * cnt] = S(st, c);
+        to_rns(st, a, 1, L, true, P.pow_tab);
+        mont_mul(st, r2, (u32)cnt, false, cs, s_be);
+#pragma unroll 1
+        for (int c = 0; c < NCH; c++) tab[entry + (size_t)c * cnt] = S(st, c);
+#pragma unroll 1
+        for (u32 e = 2; e < E; e++) {
+            mont_mul(st, tab + entry, (u32)cnt, false, cs, s_be);
+#pragma unroll 1
+            for (int c = 0; c < NCH; c++) tab[e * entry + (size_t)c * cnt] = S(st, c);
+        }
+        // y = a^d: fixed window from the top digit; acc starts at 1~
+#pragma unroll 1
+        for (int c = 0; c < NCH; c++) S(st, c) = tab[(size_t)c * cnt];
+#pragma unroll 1
+        for (int dg = (int)ndig - 1; dg >= 0; dg--) {
+            const u32 b0 = dg * w;
+            const u32 lw = b0 / 32, bw = b0 % 32;
+            const u32 lo = lw < (u32)K ? dl[(size_t)lw * cnt] : 0u;
+            const u32 hi = lw + 1 < (u32)K ? dl[(size_t)(lw + 1) * cnt] : 0u;
+            const u32 digit = __funnelshift_r(lo, hi, bw) & (E - 1);
+#pragma unroll 1
+            for (u32 q = 0; q < w; q++) mont_mul(st, s_one, 0, true, cs, s_be);
+            mont_mul(st, tab + digit * entry, (u32)cnt, false, cs, s_be);
+        }
+        // HAC 4.24 steps 2.3-2.6: y in {1, n-1} passes; else up to s-1 squarings looking for n-1
+        bool pass = false, decided = false;
+#pragma unroll 1
+        for (u32 j = 0; j < s && !decided; j++) {
+            if (j) mont_mul(st, s_one, 0, true, cs, s_be);           // y = y^2
+#pragma unroll 1
+            for (int c = 0; c < NCH; c++) stash[(size_t)c * cnt] = S(st, c);
+            mont_mul(st, s_one, 1, false, cs, s_be);                 // leave the Montgomery domain
+            from_rns(st, cs);
+            const bool one = x_is_one(st), nm1 = x_is_nm1(st, nrow, L);
+            if (nm1) { pass = true; decided = true; }
+            else if (one) { pass = (j == 0); decided = true; }  // y = 1 first: pass; later: composite
+#pragma unroll 1
+            for (int c = 0; c < NCH; c++) S(st, c) = stash[(size_t)c * cnt];
+        }
+        if (!pass) {
+            if (verdict == MR_PROBABLY_PRIME_V) { verdict = MR_COMPOSITE_V; witness = (int)r; }
+            if (!P.forced) break;
+        }
+    }
+    P.verdict[i] = (uint8_t)verdict;
+    if (P.witness) P.witness[i] = (int16_t)witness;
+    if (P.status && status) P.status[i] = status;
+}
+
 // ------------------------------------------------------------------ host-side launchers
+
+template <class Prm>
+int launch(void (*kern)(Prm), u32 ctas, const Prm &params, void *stream) {
+    void *args[] = {const_cast<Prm *>(&params)};
+    return cudaLaunchKernel((const void *)kern, dim3(ctas), dim3(T), args, SMEM_BYTES, (cudaStream_t)stream) ==
+                   cudaSuccess
+               ? 0
+               : 6;
+}
 
 int upload_base(const u32 *flat, int device) {
     if (cudaSetDevice(device) != cudaSuccess) return 6;
     if (cudaMemcpyToSymbol(g_base, flat, sizeof(u32) * BASE_WORDS) != cudaSuccess) return 6;
+    const void *kerns[] = {(const void *)k_modexp, (const void *)k_combine, (const void *)k_mr_setup,
+                           (const void *)k_mr_rounds};
+    for (const void *k : kerns)
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) != cudaSuccess)
+            return 6;
     return 0;
 }
 
-int launch_modexp(const ModexpParams &p, u32 ctas, void *stream) {
-    k_modexp<<<ctas, THREADS, 0, (cudaStream_t)stream>>>(p);
-    return cudaGetLastError() == cudaSuccess ? 0 : 6;
-}
+int launch_modexp(const ModexpParams &p, u32 ctas, void *stream) { return launch(k_modexp, ctas, p, stream); }
 
-int launch_combine(const CombineParams &p, void *stream) {
-    const u32 ctas = (p.count + THREADS - 1) / THREADS;
-    k_combine<<<ctas, THREADS, 0, (cudaStream_t)stream>>>(p);
-    return cudaGetLastError() == cudaSuccess ? 0 : 6;
-}
+int launch_combine(const CombineParams &p, void *stream) { return launch(k_combine, (p.count + T - 1) / T, p, stream); }
 
-int launch_mr(const MrParams &, void *) { return 1; }
+int launch_mr(const MrParams &p, void *stream) {
+    const u32 ctas = (p.count + T - 1) / T;
+    int rc = launch(k_mr_setup, ctas, p, stream);
+    if (rc) return rc;
+    return launch(k_mr_rounds, ctas, p, stream);
+}
 
 }  // namespace
 }  // namespace mr

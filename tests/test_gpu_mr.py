@@ -1,0 +1,148 @@
+"""GPU parity of mr_miller_rabin_batch (§3.2, HAC 4.24) against the oracle: verdict and first
+witnessing round must be identical for the same candidates and the same explicit bases (reading
+R13), including the FACTOR verdict of reading R14 and the input rules of include/mr_rns.h."""
+import numpy as np
+import pytest
+
+import synth
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def mr():
+    import paper_1305_3699_b200 as mr
+    mr.lib()
+    return mr
+
+
+def gpu_mr(torch, mr, ns, bases, limbs=None):
+    """ns: list of ints; bases: list of lists (rounds each). Returns (verdict, witness, status)."""
+    limbs = limbs or max(1, max((n.bit_length() + 31) // 32 for n in ns))
+    rounds = len(bases[0])
+    n_arr = mr.ints_to_limbs(ns, limbs)
+    b_arr = np.stack([mr.ints_to_limbs(b, limbs) for b in bases]).reshape(len(ns), rounds, limbs)
+    d_n = torch.from_numpy(n_arr.view(np.int32)).cuda()
+    d_b = torch.from_numpy(np.ascontiguousarray(b_arr).view(np.int32)).cuda()
+    v = torch.zeros(len(ns), dtype=torch.uint8, device="cuda")
+    w = torch.zeros(len(ns), dtype=torch.int16, device="cuda")
+    s = torch.zeros(len(ns), dtype=torch.int32, device="cuda")
+    mr.mr_miller_rabin_batch(d_n, limbs, len(ns), d_b, rounds, v, w, s)
+    torch.cuda.synchronize()
+    return v.cpu().numpy().tolist(), w.cpu().numpy().tolist(), s.cpu().numpy().tolist(), limbs
+
+
+def oracle_mr(orc, ns, bases, limbs, k):
+    fp = orc.base_primes(2 * k)
+    out = []
+    for n, b in zip(ns, bases):
+        v, w = orc.miller_rabin(n, b, fp)
+        out.append((v, w))
+    return [v for v, _ in out], [w for _, w in out]
+
+
+def k_for(mr, limbs):
+    for k in mr.mr_rns_supported_k():
+        if 4 * (k + 3) ** 2 * (1 << (32 * limbs)) < _M(k) and limbs <= k - 1:
+            return k
+
+
+_MC = {}
+
+
+def _M(k):
+    if k not in _MC:
+        import sympy
+        ps, x = [], 1 << 32
+        while len(ps) < k:
+            x = sympy.prevprime(x)
+            ps.append(x)
+        m = 1
+        for p in ps:
+            m *= p
+        _MC[k] = m
+    return _MC[k]
+
+
+def check(torch, mr, orc, ns, bases):
+    v, w, s, limbs = gpu_mr(torch, mr, ns, bases)
+    ov, ow = oracle_mr(orc, ns, bases, limbs, k_for(mr, limbs))
+    assert v == ov, [(n, a, b) for n, a, b in zip(ns, v, ov) if a != b][:5]
+    assert w == ow
+    assert all(x == 0 for x in s)
+    return v, w
+
+
+def test_carmichael_and_small_primes(torch_cuda, mr, orc):
+    nt = load_golden("number_theory.json")
+    car = nt["carmichael_below_100000"]["values"]
+    ns = car + [p for p in orc.small_primes(2000) if p >= 5][:500] + [2147483647, 9, 25, 49, 15, 21]
+    bases = [synth.mr_bases(n, 20, 3, i) for i, n in enumerate(ns)]
+    v, w = check(torch_cuda, mr, orc, ns, bases)
+    assert all(x == 0 for x in v[: len(car)])                          # every Carmichael number rejected
+    assert all(x == 1 for x in v[len(car): len(car) + 501])            # no false composites
+
+
+def test_strong_pseudoprimes_round_level(torch_cuda, mr, orc):
+    nt = load_golden("number_theory.json")["strong_pseudoprimes"]
+    ns, bases = [], []
+    for n, bs in nt["values"]:
+        ns.append(n)
+        bases.append(bs + [nt["fails_next_base"][str(n)]] + [2] * (6 - len(bs)))
+    v, w = check(torch_cuda, mr, orc, ns, bases)
+    assert v == [0] * len(ns)
+    assert w == [len(b) for b, _ in [(bs, 0) for _, bs in nt["values"]]]
+
+
+def test_c5_shape_1024_bit_candidates(torch_cuda, mr, orc):
+    """C5: seeded 1024-bit candidates (top two bits + low bit set), 5 rounds of bases in [2, n-2]."""
+    ns = [synth.odd_with_top_bits(1024, 0x5EEDC005, synth.TAG_CAND, i) for i in range(384)]
+    ns[7] = (1 << 1279) - 1 if False else ns[7]
+    bases = [synth.mr_bases(n, 5, 0x5EEDC005, i) for i, n in enumerate(ns)]
+    check(torch_cuda, mr, orc, ns, bases)
+
+
+def test_known_primes_and_products(torch_cuda, mr, orc):
+    import sympy
+    ps = [sympy.nextprime(synth.odd_with_top_bits(1024, 9, synth.TAG_CAND, i)) for i in range(20)]
+    m521, m607 = (1 << 521) - 1, (1 << 607) - 1
+    ns = ps + [ps[0] * ps[1] % (1 << 1024) | 1, m521, m607]
+    ns = [n if n.bit_length() <= 1024 else n >> (n.bit_length() - 1024) | 1 for n in ns]
+    bases = [synth.mr_bases(n, 8, 10, i) for i, n in enumerate(ns)]
+    v, w = check(torch_cuda, mr, orc, ns, bases)
+    assert v[:20] == [1] * 20
+
+
+def test_factor_verdict_and_input_rules(torch_cuda, mr, orc):
+    fp = orc.base_primes(66)
+    n_factor = fp[5] * ((1 << 900) + 0x1234567) | 1
+    while n_factor % fp[5]:
+        n_factor += 2 * fp[5]
+    ns = [n_factor, 1000001, 3, (1 << 1000) + 1]          # FACTOR, even-after-fix-up-check, n < 5, odd composite
+    ns[1] = 1000000                                         # even
+    bases = [[2, 3], [2, 3], [2, 2], [2, (1 << 1000)]]      # last: base > n - 2
+    limbs = 32
+    v, w, s, _ = gpu_mr(torch_cuda, mr, ns, bases, limbs=limbs)
+    assert v[0] == mr.MR_FACTOR and s[0] == 0
+    assert s[1] == 5 and s[2] == 5 and s[3] == 5
+    ov, _ = orc.miller_rabin(n_factor, [2, 3], orc.base_primes(66))
+    assert ov == 2
+
+
+def test_chernick_carmichael_1024(torch_cuda, mr, orc):
+    import sympy
+    t = 1 << 300
+    while not (sympy.isprime(6 * t + 1) and sympy.isprime(12 * t + 1) and sympy.isprime(18 * t + 1)):
+        t += 1
+    n = (6 * t + 1) * (12 * t + 1) * (18 * t + 1)
+    v, w = check(torch_cuda, mr, orc, [n], [synth.mr_bases(n, 6, 1, 0)])
+    assert v == [0]
