@@ -404,6 +404,26 @@ static void fill_ctx_block(const Base &b, const Big &N, size_t limbs, const Big 
     for (int l = 0; l < 2 * k + 2 && l < (int)in_bound.size(); l++) x[cx_inb(k) + l] = in_bound[l];
 }
 
+// Per-context BE1 image with 6.4 merged into the contraction: the tile layout of
+// mr_internal.h be_* holding A1'[i][j] = |M_i|_{m'_j} · |N M^-1 λ_j|_{m'_j} mod m'_j, so that
+// ξ'_j = t*_j |M^-1 λ_j^-1| + Σ_i ξ_i A1'[i][j] needs one reduction.
+static void fill_merged_be1(const Base &b, u32 *out, const u32 *cx) {
+    const int k = b.k;
+    const BaseLayout L = base_layout(k);
+    const u32 *A1 = b.flat.data() + L.A1;
+    const u32 ch = be_ch(k), nt = be_nfull(k) + (be_tail(k) ? 1 : 0);
+    u32 off = 0;
+    for (u32 t = 0; t < nt; t++) {
+        const u32 w = t < be_nfull(k) ? ch : be_tail(k), pw = pad4(w);
+        for (int i = 0; i < k; i++)
+            for (u32 jj = 0; jj < w; jj++) {
+                const u32 j = t * ch + jj;
+                out[off + i * pw + jj] = mulm(A1[i * k + j], cx[cx_c2(k) + j], b.Bp[j]);
+            }
+        off += k * pw;
+    }
+}
+
 static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, int device, const Big &in_bound,
                      size_t in_limbs, const Big *khi_shift_limbs_half /* CRT: half limbs */, const Big *qinv) {
     *out = nullptr;
@@ -436,8 +456,9 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->limbs = limbs;
     c->bits = bits(N);
     c->N = N;
-    c->h_cx.assign(cx_words(k), 0);
+    c->h_cx.assign(cx_words(k) + be_half_words(k), 0);
     fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
+    fill_merged_be1(b, c->h_cx.data() + cx_words(k), c->h_cx.data());
     int rc = ensure_device_base(k, device, &c->d_pow, &c->d_be);
     if (rc != MR_OK) { delete c; return rc; }
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return MR_ERR_CUDA; }

@@ -66,19 +66,23 @@ __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) 
 
 // h·2^32 + l  ->  congruent value in [0, 2^32) modulo m = 2^32 - c  (c < 2^13)
 __device__ __forceinline__ u32 red64(u32 h, u32 l, u32 c) {
-    const u64 u = (u64)h * c + l;                       // < 2^32 (c + 1)
-    const u64 v = (u64)(u32)(u >> 32) * c + (u32)u;     // < 2^32 + c^2
-    const u32 vl = (u32)v;
-    return (u32)(v >> 32) ? vl + c : vl;                // 2^32 ≡ c; vl < c^2 then, so no wrap
+    const u64 u = (u64)h * c + l;                       // < 2^32 (c + 1): uh <= c
+    const u32 uh = (u32)(u >> 32), ul = (u32)u;
+    const u32 vl = uh * c + ul;                         // uh c < 2^26: wraps at most once
+    return vl < ul ? vl + c : vl;                       // wrapped: 2^32 ≡ c and vl < 2^26
 }
 
-// hi·2^64 + mid·2^32 + lo -> congruent value in [0, 2^32), hi < 2^7, c2 = c^2
+// hi·2^64 + mid·2^32 + lo -> congruent value in [0, 2^32), hi < 2^7
+// hi·2^64 ≡ hi·c·2^32, so V ≡ W·2^32 + lo with W = mid + hi·c (may carry once: wc), then
+// W·2^32 ≡ w·c + wc·c·2^32 and one more fold.
 __device__ __forceinline__ u32 red96(u32 hi, u32 mid, u32 lo, u32 c, u32 c2) {
-    u64 u = (u64)mid * c + lo;                          // < 2^45 + 2^32
-    u += (u64)hi * c2;                                  // < 2^33
-    const u64 v = (u64)(u32)(u >> 32) * c + (u32)u;     // < 2^27 + 2^32
-    const u32 vl = (u32)v;
-    return (u32)(v >> 32) ? vl + c : vl;
+    (void)c2;
+    const u32 w = mid + hi * c;                          // hi c < 2^20
+    const u32 wc = w < mid ? c : 0u;                     // carry out of W, as its weight c at 2^32
+    const u64 u = (u64)w * c + lo;                       // < 2^45 + 2^32
+    const u32 uh = (u32)(u >> 32) + wc, ul = (u32)u;     // uh < 2^14
+    const u32 vl = uh * c + ul;                          // uh c < 2^27: wraps at most once
+    return vl < ul ? vl + c : vl;
 }
 
 __device__ __forceinline__ u32 mulmod(u32 a, u32 b, u32 c) {
@@ -96,6 +100,7 @@ __device__ __forceinline__ u32 &S(u32 *st, int ch) { return st[ch * T + threadId
 // ------------------------------------------------------------------ per-modulus constant sources
 
 struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt): context block in smem
+    static constexpr bool kMerged = true;   // BE1 image carries |N M^-1 λ_j| (per-context image)
     const u32 *cx;
     __device__ u32 sigma(int i) const { return cx[cx_sigma(K) + i]; }
     __device__ u32 c2(int j) const { return cx[cx_c2(K) + j]; }
@@ -104,6 +109,7 @@ struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt)
 };
 
 struct CtxThread {                    // one modulus per thread (Miller-Rabin): per-candidate rows
+    static constexpr bool kMerged = false;
     const u32 *pc;
     const u32 *nrow;                  // candidate limbs
     u32 stride, limbs;
@@ -151,23 +157,39 @@ __device__ __forceinline__ void be_tile_acc(const u32 *st, int xr, const u32 *ti
     }
 }
 
-// BE1 tile: q̂_j for j in [j0, j0+W), then ξ'_j = t*_j C1_j + q̂_j C2_j (6.4/6.5) into row K+j;
-// also accumulates the m_r column of BE2, sr += ξ'_j |M'_j|_{2^32}.
-template <int W, class CS>
+// BE1 tile: for j in [j0, j0+W) produce ξ'_j (6.3-6.5) into row K+j and accumulate the m_r column of
+// BE2, sr += ξ'_j |M'_j|_{2^32}.  MERGED (one modulus per CTA): the tile image holds
+// A1'[i][j] = |M_i|_{m'_j}|N M^-1 λ_j|, so ξ'_j = red(t*_j |M^-1 λ_j^-1| + Σ_i ξ_i A1'[i][j]).
+// Otherwise (one modulus per thread, Miller-Rabin): q̂_j = red(Σ_i ξ_i |M_i|_{m'_j}) first.
+template <int W, bool MERGED, class CS>
 __device__ __forceinline__ void be1_tile(int j0, const u32 *tile, u32 *st, const u32 *s_be, const CS &cs, u32 &sr) {
     u32 lo[W], mi[W], hi[W];
 #pragma unroll
-    for (int jj = 0; jj < W; jj++) lo[jj] = mi[jj] = hi[jj] = 0;
+    for (int jj = 0; jj < W; jj++) {
+        if (MERGED) {
+            const u64 p = (u64)S(st, K + j0 + jj) * s_be[bev_C1(K) + j0 + jj];
+            lo[jj] = (u32)p;
+            mi[jj] = (u32)(p >> 32);
+        } else {
+            lo[jj] = mi[jj] = 0;
+        }
+        hi[jj] = 0;
+    }
     be_tile_acc<W>(st, 0, tile, lo, mi, hi);
 #pragma unroll
     for (int jj = 0; jj < W; jj++) {
         const int j = j0 + jj;
-        const u32 c = s_be[bev_c(K) + K + j], c2 = s_be[bev_c2(K) + K + j];
-        const u32 q = red96(hi[jj], mi[jj], lo[jj], c, c2);
-        const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
-        u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
-        mac96(l2, m2, h2, q, cs.c2(j));
-        const u32 xp = red96(h2, m2, l2, c, c2);
+        const u32 c = s_be[bev_c(K) + K + j];
+        u32 xp;
+        if (MERGED) {
+            xp = red96(hi[jj], mi[jj], lo[jj], c, 0);
+        } else {
+            const u32 q = red96(hi[jj], mi[jj], lo[jj], c, 0);
+            const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
+            u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
+            mac96(l2, m2, h2, q, cs.c2(j));
+            xp = red96(h2, m2, l2, c, 0);
+        }
         S(st, K + j) = xp;
         sr += xp * s_be[bev_A2r(K) + j];
     }
@@ -195,6 +217,7 @@ __device__ __forceinline__ void be2_tile(int i0, const u32 *tile, u32 alpha, u32
 template <class CS>
 __device__ __forceinline__ void mont_mul(u32 *st, const u32 *__restrict__ bp, u32 bstride, bool sq, const CS &cs,
                                          const u32 *s_be) {
+    constexpr bool MERGED = CS::kMerged;
     // ---- 6.1 / 6.2: channel products; q-digits ξ_i overwrite a_i; m_r column of BE1 on the fly
     u32 qr = 0;
 #pragma unroll 3
@@ -218,8 +241,8 @@ __device__ __forceinline__ void mont_mul(u32 *st, const u32 *__restrict__ bp, u3
     // ---- 6.3-6.5 BE1 [1 x K]·[K x K] contraction, CH outputs per tile, ξ' epilogue
     u32 sr = 0;
 #pragma unroll 1
-    for (int t = 0; t < KF / CH; t++) be1_tile<CH>(t * CH, s_be + t * K * pad4(CH), st, s_be, cs, sr);
-    if (KT) be1_tile<KT ? KT : 1>(KF, s_be + (KF / CH) * K * pad4(CH), st, s_be, cs, sr);
+    for (int t = 0; t < KF / CH; t++) be1_tile<CH, MERGED>(t * CH, s_be + t * K * pad4(CH), st, s_be, cs, sr);
+    if (KT) be1_tile<KT ? KT : 1, MERGED>(KF, s_be + (KF / CH) * K * pad4(CH), st, s_be, cs, sr);
     // ---- 6.6 BE2 [1 x K]·[K x K] contraction, exact through the extra modulus
     const u32 alpha = (sr - rr) * GB(O_MISC + 1);
     S(st, 2 * K) = rr;
@@ -307,6 +330,17 @@ __device__ __forceinline__ bool less_than(const u32 *__restrict__ x, const u32 *
     return res < 0;
 }
 
+// stage the per-CTA constants: context block, its merged BE1 image (stored right after the block),
+// and the per-k BE2 image + vectors
+__device__ __forceinline__ void stage_smem(u32 *s_be, u32 *s_cx, const u32 *gcx, const u32 *be_tab) {
+    for (u32 w = threadIdx.x; w < CXW; w += T) s_cx[w] = gcx[w];
+    const uint4 *be1 = reinterpret_cast<const uint4 *>(gcx + CXW);
+    for (u32 w = threadIdx.x; w < BEH / 4; w += T) reinterpret_cast<uint4 *>(s_be)[w] = __ldg(be1 + w);
+    for (u32 w = BEH / 4 + threadIdx.x; w < BEW / 4; w += T)
+        reinterpret_cast<uint4 *>(s_be)[w] = __ldg(reinterpret_cast<const uint4 *>(be_tab) + w);
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ modexp interpreter kernel (a2-a7, a8 ladders)
 __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
     extern __shared__ __align__(16) u32 smem[];
@@ -315,10 +349,7 @@ __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
     u32 *s_cx = s_be + BEW;
     const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
     const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
-    for (u32 w = threadIdx.x; w < CXW; w += T) s_cx[w] = gcx[w];
-    for (u32 w = threadIdx.x; w < BEW / 4; w += T)
-        reinterpret_cast<uint4 *>(s_be)[w] = __ldg(reinterpret_cast<const uint4 *>(P.be_tab) + w);
-    __syncthreads();
+    stage_smem(s_be, s_cx, gcx, P.be_tab);
     const u32 jl = (blockIdx.x - sel * P.ctas0) * T + threadIdx.x;
     if (jl >= P.count) return;
     const CtxSmem cs{s_cx};
@@ -389,10 +420,7 @@ __global__ void __launch_bounds__(T, MINB) k_combine(const CombineParams P) {
     u32 *st = smem;
     u32 *s_be = smem + SMEM_STATE;
     u32 *s_cx = s_be + BEW;
-    for (u32 w = threadIdx.x; w < CXW; w += T) s_cx[w] = P.ctx_p[w];
-    for (u32 w = threadIdx.x; w < BEW / 4; w += T)
-        reinterpret_cast<uint4 *>(s_be)[w] = __ldg(reinterpret_cast<const uint4 *>(P.be_tab) + w);
-    __syncthreads();
+    stage_smem(s_be, s_cx, P.ctx_p, P.be_tab);
     const u32 i = blockIdx.x * T + threadIdx.x;
     if (i >= P.count) return;
     const CtxSmem cs{s_cx};
@@ -655,21 +683,29 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
     int witness = -1;
     int32_t status = 0;
     const u32 ndig = (32 * L + w - 1) / w;        // fixed-window schedule over a padded exponent
+    // base rule for every round first: 2 <= a <= n - 2, i.e. a >= 2 and d = n - a >= 2 without borrow
+#pragma unroll 1
+    for (u32 r = 0; r < P.rounds && !status; r++) {
+        const u32 *a = P.bases + ((size_t)i * P.rounds + r) * L;
+        u32 br = 0, dhi = 0, ahi = 0, d0 = 0;
+#pragma unroll 1
+        for (u32 l = 0; l < L; l++) {
+            const u64 t = (u64)nrow[l] - a[l] - br;
+            br = (u32)(t >> 63);
+            if (l) { dhi |= (u32)t; ahi |= a[l]; } else d0 = (u32)t;
+        }
+        const bool a_ge2 = ahi || a[0] >= 2u;
+        const bool d_ge2 = !br && (dhi || d0 >= 2u);
+        if (!a_ge2 || !d_ge2) status = 5;
+    }
+    if (status) {
+        P.verdict[i] = (uint8_t)MR_COMPOSITE_V;
+        if (P.status) P.status[i] = status;
+        return;
+    }
 #pragma unroll 1
     for (u32 r = 0; r < P.rounds; r++) {
         const u32 *a = P.bases + ((size_t)i * P.rounds + r) * L;
-        {   // base rule: 2 <= a <= n - 2, i.e. a >= 2 and d = n - a >= 2 without borrow
-            u32 br = 0, dhi = 0, ahi = 0, d0 = 0;
-#pragma unroll 1
-            for (u32 l = 0; l < L; l++) {
-                const u64 t = (u64)nrow[l] - a[l] - br;
-                br = (u32)(t >> 63);
-                if (l) { dhi |= (u32)t; ahi |= a[l]; } else d0 = (u32)t;
-            }
-            const bool a_ge2 = ahi || a[0] >= 2u;
-            const bool d_ge2 = !br && (dhi || d0 >= 2u);
-            if (!a_ge2 || !d_ge2) { status = 5; verdict = MR_COMPOSITE_V; break; }
-        }
         // table: T[0] = 1~ = mm(R^2, 1), T[1] = ã = mm(a, R^2), T[e] = T[e-1] ã
 #pragma unroll 1
         for (int c = 0; c < NCH; c++) S(st, c) = r2[(size_t)c * cnt];
