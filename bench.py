@@ -204,6 +204,7 @@ def workload_config(args, reference=False):
     return {"workload": "C2: RSA-2048 batched CRT decryption, 65,536 messages per GPU (BASELINE configs[1])",
             "key": "tests/golden/keys/rsa2048.json (oracle-generated, seed 0x5EEDC002)",
             "messages_per_gpu": args.count, "rns_k_per_half": K_HALF, "modulus_bits": 2048,
+            "base_extension": "imad" if os.environ.get("MR_RNS_IMAD_ONLY", "0") == "1" else "tcgen05-i8",
             "inputs": "SplitMix64 ciphertexts uniform in [0, N) + edge values (synth/)",
             "l2": "flushed between timed steps (256 MiB write)" if not reference else "n/a (CPU)"}
 
@@ -300,6 +301,15 @@ def run_ours(args, world, rank, local):
         cpu = cpu_baseline(key)
     if rank != 0:
         return
+    tensor = os.environ.get("MR_RNS_IMAD_ONLY", "0") != "1"
+    kname = "k_modexp_tc (CRT half-ladders, k=33, base extensions on tcgen05 int8)" if tensor else \
+        "k_modexp (CRT half-ladders, k=33, IMAD-pipe base extensions)"
+    # tensor-core work of the two base extensions: useful u8 MACs per Montgomery multiplication
+    # = 2 x (4k)^2, 2 ops each; peak = measured bf16 burst x (4.5 / 2.25) nominal i8:bf16 ratio
+    mm_per_dec = 2 * (sliding_window_mm(key["dp"]) + sliding_window_mm(key["dq"])) // 2
+    i8_ops_per_dec = 2 * mm_per_dec * 2 * (4 * K_HALF) ** 2 if tensor else 0
+    i8_peak = measured_peaks().get("bf16_tflops", 1611.6) * 2.0 * 1e12
+    i8_achieved = i8_ops_per_dec * count / (ladder_ms / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -307,7 +317,11 @@ def run_ours(args, world, rank, local):
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "T IMAD-eq/s (INT32 IMAD pipe, 64/clk/SM x 148 SM x 1965 MHz)",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "k_modexp (CRT half-ladders, k=33)", "ladder_ms_per_launch": ladder_ms,
+                     "kernel": kname, "ladder_ms_per_launch": ladder_ms,
+                     "tensor_i8": {"achieved_tops": i8_achieved / 1e12, "peak_tops": i8_peak / 1e12,
+                                   "frac": i8_achieved / i8_peak,
+                                   "peak_source": "MEASURED_PEAKS bf16_tflops x 2 (nominal i8:bf16 4.5:2.25)"}
+                     if tensor else None,
                      "combine_ms_per_launch": ms_c.value / max(1, n_c.value),
                      "imad_eq_per_decrypt": per_dec,
                      "frac_at_median_clock": (achieved / peak_imad_eq_per_s(clocks["sm_mhz"]))

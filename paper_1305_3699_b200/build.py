@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libmr_rns.so")
 ROOT = os.path.dirname(HERE)
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
-KS = [1, 2, 3, 5, 9, 17, 33, 49, 65]
+KS = [1, 2, 3, 5, 9, 17, 33, 49, 65, 97, 129]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                   "-I", os.path.join(ROOT, "include")]

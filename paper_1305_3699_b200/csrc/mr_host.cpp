@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -26,15 +27,18 @@ MR_DECLARE_K(17)
 MR_DECLARE_K(33)
 MR_DECLARE_K(49)
 MR_DECLARE_K(65)
+MR_DECLARE_K(97)
+MR_DECLARE_K(129)
 
 static const KernelSet &kernel_set_for(int k) {
     static std::vector<KernelSet> sets = {kernels_k1(),  kernels_k2(),  kernels_k3(),  kernels_k5(), kernels_k9(),
-                                          kernels_k17(), kernels_k33(), kernels_k49(), kernels_k65()};
+                                          kernels_k17(), kernels_k33(), kernels_k49(), kernels_k65(),
+                                          kernels_k97(), kernels_k129()};
     for (const auto &s : sets)
         if (s.k == k) return s;
     return sets[0];
 }
-static const int kSupportedK[] = {1, 2, 3, 5, 9, 17, 33, 49, 65};
+static const int kSupportedK[] = {1, 2, 3, 5, 9, 17, 33, 49, 65, 97, 129};
 static const int kNumK = sizeof(kSupportedK) / sizeof(kSupportedK[0]);
 
 // ------------------------------------------------------------------ host positional helpers
@@ -295,10 +299,25 @@ static void to_rns_host(const Base &b, const Big &x, u32 *out) {
     out[2 * k] = x.empty() ? 0 : x[0];
 }
 
+// Tensor-core B image (mr_internal.h tc_*): row (j, b), k byte (i, a) holds byte b of
+// 2^(8a) A[i][j] mod m_j, where A[i][j] is the contraction constant of input i for output j.
+static void fill_tc_image(int k, const u32 *A /* [k][k], row i, column j */, const std::vector<u32> &mods,
+                          uint8_t *out) {
+    memset(out, 0, tc_bbytes(k));
+    for (int j = 0; j < k; j++)
+        for (int i = 0; i < k; i++)
+            for (int a = 0; a < 4; a++) {
+                const u32 v = (u32)(((u64)A[i * k + j] << (8 * a)) % mods[j]);
+                for (int b = 0; b < 4; b++) out[tc_off(k, 4 * j + b, 4 * i + a)] = (uint8_t)(v >> (8 * b));
+            }
+}
+
 // device residency of per-k tables
 struct DevBase {
     u32 *d_pow = nullptr;
     u32 *d_be = nullptr;
+    u32 *d_mpl = nullptr;      // M'_j limbs [k][k+1] for the exit conversion
+    u32 *d_tcb2 = nullptr;     // tensor-core BE2 image (k <= 64)
 };
 static std::map<std::pair<int, int>, DevBase> g_devbases;
 
@@ -318,9 +337,22 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
     if (cudaMalloc(&db.d_pow, b.pow.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
     if (cudaMemcpy(db.d_pow, b.pow.data(), b.pow.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
         return MR_ERR_CUDA;
+    {
+        const BaseLayout L = base_layout(k);
+        const size_t n = (size_t)k * (k + 1);
+        if (cudaMalloc(&db.d_mpl, n * 4) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMemcpy(db.d_mpl, b.flat.data() + L.MpL, n * 4, cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
+    }
     if (cudaMalloc(&db.d_be, b.be.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
     if (cudaMemcpy(db.d_be, b.be.data(), b.be.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
         return MR_ERR_CUDA;
+    if (tc_ok(k)) {   // tensor BE2 image of A2 as [input j][output i]
+        const u32 *A2 = b.flat.data() + base_layout(k).A2;   // row j, column i
+        std::vector<uint8_t> img(tc_bbytes(k));
+        fill_tc_image(k, A2, b.B, img.data());
+        if (cudaMalloc(&db.d_tcb2, img.size()) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMemcpy(db.d_tcb2, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
+    }
     g_devbases[key] = db;
     *d_pow = db.d_pow;
     *d_be = db.d_be;
@@ -362,6 +394,8 @@ struct mr_rns_ctx {
     u32 *d_cx = nullptr;       // device context block
     const u32 *d_pow = nullptr;
     const u32 *d_be = nullptr;
+    const u32 *d_tcb2 = nullptr;
+    const u32 *d_mpl = nullptr;
     std::vector<u32> h_cx;
     std::mutex mu;             // guards the program cache
     std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program
@@ -456,10 +490,22 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->limbs = limbs;
     c->bits = bits(N);
     c->N = N;
-    c->h_cx.assign(cx_words(k) + be_half_words(k), 0);
+    const size_t tc_words = tc_ok(k) ? tc_bbytes(k) / 4 : 0;
+    c->h_cx.assign(cx_words(k) + be_half_words(k) + tc_words, 0);
     fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
     fill_merged_be1(b, c->h_cx.data() + cx_words(k), c->h_cx.data());
+    if (tc_ok(k)) {   // tensor BE1 image of A1'[i][j] = |M_i|_{m'_j} |N M^-1 λ_j|
+        const u32 *A1 = b.flat.data() + base_layout(k).A1;
+        std::vector<u32> A1m((size_t)k * k);
+        for (int i = 0; i < k; i++)
+            for (int j = 0; j < k; j++) A1m[i * k + j] = mulm(A1[i * k + j], c->h_cx[cx_c2(k) + j], b.Bp[j]);
+        fill_tc_image(k, A1m.data(), b.Bp, reinterpret_cast<uint8_t *>(c->h_cx.data() + cx_words(k) + be_half_words(k)));
+    }
     int rc = ensure_device_base(k, device, &c->d_pow, &c->d_be);
+    if (rc == MR_OK) {
+        c->d_tcb2 = g_devbases[std::make_pair(device, k)].d_tcb2;
+        c->d_mpl = g_devbases[std::make_pair(device, k)].d_mpl;
+    }
     if (rc != MR_OK) { delete c; return rc; }
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return MR_ERR_CUDA; }
     if (cudaMalloc(&c->d_cx, c->h_cx.size() * 4) != cudaSuccess) { delete c; return MR_ERR_NOMEM; }
@@ -665,15 +711,33 @@ int mr_rns_ctx_info(const mr_rns_ctx *ctx, int *k, size_t *limbs, int *modulus_b
     return MR_OK;
 }
 
+// The tensor-core base extension (k <= 64) is the default; MR_RNS_IMAD_ONLY=1 selects the IMAD-pipe
+// kernel (same results; kept for comparison and parity testing) — see mr_internal_set_path.
+static int g_path_override = -1;   // -1: environment, 0: IMAD only, 1: tensor allowed
+static bool tensor_path_enabled() {
+    if (g_path_override >= 0) return g_path_override == 1;
+    const char *e = getenv("MR_RNS_IMAD_ONLY");
+    return !(e && e[0] == '1');
+}
+
 static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x, size_t in_limbs,
                           size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status, void *stream) {
     const mr_rns_ctx *c0 = ctxs[0];
     const KernelSet &ks = kernel_set_for(c0->k);
     if (cudaSetDevice(c0->device) != cudaSuccess) return MR_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
-    const u32 T = (u32)ks.threads;
+    const bool use_tc = ks.launch_modexp_tc && c0->d_tcb2 && tensor_path_enabled();
+    // IMAD path: one CTA per T messages; tensor path: ctas0 = 128-message tile-jobs per context,
+    // run by Gc persistent CTAs per context (one per SM share)
+    const u32 T = use_tc ? 128u : (u32)ks.threads;
     const u32 ctas0 = (u32)((count + T - 1) / T);
     const u32 jobs_total = ctas0 * T * nctx;
+    u32 gc = 0;
+    if (use_tc) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device);
+        gc = std::min<u32>((u32)((sms + nctx - 1) / nctx), ctas0);
+    }
     int w = 1;
     for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
     const size_t nch = 2 * (size_t)c0->k + 1;
@@ -701,7 +765,15 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     P.jobs_total = jobs_total;
     P.pow_tab = c0->d_pow;
     P.be_tab = c0->d_be;
-    int rc = timed_launch(0, st, [&] { return ks.launch_modexp(P, ctas0 * nctx, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
+    P.tc_b2 = c0->d_tcb2;
+    P.mpl = c0->d_mpl;
+    P.tc_be1_off = cx_words(c0->k) + be_half_words(c0->k);
+    P.tc_gc = gc;
+    int rc = timed_launch(0, st, [&] {
+                 return use_tc ? ks.launch_modexp_tc(P, gc * nctx, stream) : ks.launch_modexp(P, ctas0 * nctx, stream);
+             }) == 0
+                 ? MR_OK
+                 : MR_ERR_CUDA;
     cudaFreeAsync(d_table, st);
     return rc;
 }
@@ -811,6 +883,7 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
         C.status = d_st;
         C.pow_tab = priv->cp->d_pow;
         C.be_tab = priv->cp->d_be;
+        C.mpl = priv->cp->d_mpl;
         const KernelSet &ks = kernel_set_for(priv->cp->k);
         rc = timed_launch(1, st, [&] { return ks.launch_combine(C, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
     }
@@ -878,6 +951,7 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
     P.status = d_status;
     P.pow_tab = d_pow;
     P.be_tab = d_be;
+    P.mpl = g_devbases[std::make_pair(device, kk)].d_mpl;
     const KernelSet &ks = kernel_set_for(kk);
     int rc = timed_launch(2, st, [&] { return ks.launch_mr(P, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
     cudaFreeAsync(d_pc, st);
@@ -932,6 +1006,13 @@ int mr_internal_ctx_table(const uint32_t *modulus, size_t limbs, int k, uint32_t
 int mr_internal_timing_mr(double *ms, int *n) {
     if (ms) *ms = g_last_mr_ms;
     if (n) *n = g_last_mr_n;
+    return MR_OK;
+}
+
+// select the Montgomery-multiplication kernel: 0 = IMAD pipe only, 1 = tensor core where compiled,
+// -1 = follow MR_RNS_IMAD_ONLY
+int mr_internal_set_path(int path) {
+    g_path_override = path;
     return MR_OK;
 }
 

@@ -39,27 +39,30 @@ __host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_inb(k) + 2 * k + 
 // ---------------------------------------------------------------------------------------------
 struct BaseLayout {
     u32 k;
-    u32 c, c2, A1, A1r, A2, A2r, C1, pin, misc, MpL, NMp, MiS, MU, ONE, ML, words;  // offsets
+    u32 c, c2, A1r, A2r, C1, pin, misc, NMp, MiS, MU, ONE, ML;   // device constant bank (prefix)
+    u32 const_words;                                              // words uploaded to __constant__
+    u32 MpL, A1, A2, words;                                       // host-side / global-memory tables
 };
 __host__ __device__ constexpr BaseLayout base_layout(u32 k) {
     BaseLayout b{};
     b.k = k;
     b.c = 0;                        // [2k]     c = 2^32 - m (B then B')
     b.c2 = b.c + 2 * k;             // [2k]     c^2
-    b.A1 = b.c2 + 2 * k;            // [k][k]   |M_i|_{m'_j}          (row i, column j)
-    b.A1r = b.A1 + k * k;           // [k]      |M_i|_{2^32}
-    b.A2 = b.A1r + k;               // [k][k]   |M'_j|_{m_i}          (row j, column i)
-    b.A2r = b.A2 + k * k;           // [k]      |M'_j|_{2^32}
+    b.A1r = b.c2 + 2 * k;           // [k]      |M_i|_{2^32}
+    b.A2r = b.A1r + k;              // [k]      |M'_j|_{2^32}
     b.C1 = b.A2r + k;               // [k]      |M^-1 λ_j^-1|_{m'_j}
     b.pin = b.C1 + k;               // [k]      m_i - |M'|_{m_i}
     b.misc = b.pin + k;             // [4]      M^-1 mod 2^32, M'^-1 mod 2^32
-    b.MpL = b.misc + 4;             // [k][k+1] M'_j positional limbs
-    b.NMp = b.MpL + k * (k + 1);    // [k+1]    2^(32(k+1)) - M' limbs
+    b.NMp = b.misc + 4;             // [k+1]    2^(32(k+1)) - M' limbs
     b.MiS = b.NMp + k + 1;          // [k]      |M_i|_{m_i}           (Miller-Rabin setup)
     b.MU = b.MiS + k;               // [k]      |M^-1|_{m'_j}         (Miller-Rabin setup)
     b.ONE = b.MU + k;               // [2k+1]   RNS image of 1 (B' in ξ-form)
     b.ML = b.ONE + 2 * k + 1;       // [k+1]    M positional limbs    (Miller-Rabin setup)
-    b.words = b.ML + k + 1;
+    b.const_words = b.ML + k + 1;
+    b.MpL = b.const_words;          // [k][k+1] M'_j positional limbs (global memory, exit conversion)
+    b.A1 = b.MpL + k * (k + 1);     // [k][k]   |M_i|_{m'_j}  (row i, column j; source of the BE images)
+    b.A2 = b.A1 + k * k;            // [k][k]   |M'_j|_{m_i}  (row j, column i)
+    b.words = b.A2 + k * k;
     return b;
 }
 
@@ -88,6 +91,24 @@ __host__ __device__ constexpr u32 bev_pin(u32 k) { return bev_C1(k) + pad4(k); }
 __host__ __device__ constexpr u32 bev_A1r(u32 k) { return bev_pin(k) + pad4(k); }        // [k]  |M_i|_{2^32}
 __host__ __device__ constexpr u32 bev_A2r(u32 k) { return bev_A1r(k) + pad4(k); }        // [k]  |M'_j|_{2^32}
 __host__ __device__ constexpr u32 be_words(u32 k) { return bev_A2r(k) + pad4(k); }
+
+// ---------------------------------------------------------------------------------------------
+// Tensor-core base extension (tcgen05.mma.kind::i8).  Byte-split contraction:
+//   Σ_i x_i A_ij ≡ Σ_b 2^(8b) Σ_(i,a) byte_a(x_i) · byte_b(2^(8a) A_ij mod m_j)   (mod m_j)
+// A operand: [128 messages x KP bytes] (row m = the message's K words, little-endian);
+// B operand: [NP rows (j, b) x KP bytes (i, a)]; both K-major, SWIZZLE_NONE core-matrix layout:
+// byte (r, kb) at (r / 8) * SBO + (kb / 16) * 128 + (r % 8) * 16 + kb % 16, SBO = (KP / 16) * 128.
+// D = [128 x NP] s32 in TMEM; every D value < 4k·255² < 2^24 for k <= 64.
+// ---------------------------------------------------------------------------------------------
+__host__ __device__ constexpr u32 tc_kp(u32 k) { return (4 * k + 31) & ~31u; }     // K bytes, multiple of 32
+__host__ __device__ constexpr u32 tc_np(u32 k) { return (4 * k + 15) & ~15u; }     // N rows, multiple of 16
+__host__ __device__ constexpr bool tc_ok(u32 k) { return 4 * k <= 256; }
+__host__ __device__ constexpr u32 tc_sbo(u32 k) { return (tc_kp(k) / 16) * 128; }
+__host__ __device__ constexpr u32 tc_off(u32 k, u32 r, u32 kb) {
+    return (r / 8) * tc_sbo(k) + (kb / 16) * 128 + (r % 8) * 16 + kb % 16;
+}
+__host__ __device__ constexpr u32 tc_bbytes(u32 k) { return tc_np(k) * tc_kp(k); }   // one B image
+__host__ __device__ constexpr u32 tc_abytes(u32 k) { return 128 * tc_kp(k); }        // one A tile
 
 // ---------------------------------------------------------------------------------------------
 // Exponentiation "program": one u64 op per Montgomery multiplication step, executed by a single
@@ -128,6 +149,10 @@ struct ModexpParams {
     u32 jobs_total;           // = 2 * ctas0 * blockDim (or ctas0 * blockDim)
     const u32 *pow_tab;       // to_rns powers [k][2k]
     const u32 *be_tab;        // base-extension image (be_words(k))
+    const u32 *tc_b2;         // tensor-core BE2 image (tc_bbytes(k)); BE1 image follows each ctx block
+    const u32 *mpl;           // M'_j limbs [k][k+1] (global; exit conversion)
+    u32 tc_be1_off;           // word offset of the BE1 tensor image inside a context buffer
+    u32 tc_gc;                // tensor kernel: persistent CTAs per context group
 };
 
 struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qinv mod p)
@@ -139,6 +164,7 @@ struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qi
     int32_t *status;            // nullable (range flag already written by the ladder kernel)
     const u32 *pow_tab;
     const u32 *be_tab;
+    const u32 *mpl;
 };
 
 struct MrParams {               // Miller-Rabin (§3.2; HAC 4.24)
@@ -153,6 +179,7 @@ struct MrParams {               // Miller-Rabin (§3.2; HAC 4.24)
     int32_t *status;
     const u32 *pow_tab;
     const u32 *be_tab;
+    const u32 *mpl;
 };
 
 // per-candidate constant rows for Miller-Rabin (row r at pc + r * count)
@@ -174,6 +201,8 @@ struct KernelSet {
     int (*launch_modexp)(const ModexpParams &p, u32 ctas, void *stream);
     int (*launch_combine)(const CombineParams &p, void *stream);
     int (*launch_mr)(const MrParams &p, void *stream);
+    int (*launch_modexp_tc)(const ModexpParams &p, u32 ctas, void *stream);   // null when unsupported
+    int tc_tiles;                                         // 128-message tiles per CTA of the TC kernel
     int threads;                                          // CTA size used by launch_modexp
 };
 

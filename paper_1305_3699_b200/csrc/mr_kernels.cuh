@@ -30,7 +30,7 @@ namespace {  // everything below is private to this K's translation unit
 
 constexpr int K = MR_K;
 constexpr int NCH = 2 * K + 1;                // residues per value: B, B', m_r
-constexpr int T = 128;                        // threads (messages) per CTA
+constexpr int T = K > 65 ? 64 : 128;          // threads (messages) per CTA of the IMAD-path kernels
 constexpr int CH = be_ch(K);                  // base-extension outputs per register tile
 constexpr int KF = (K / CH) * CH;             // outputs covered by full tiles
 constexpr int KT = K - KF;                    // tail tile
@@ -41,10 +41,10 @@ constexpr int SMAX = (K + 3 <= 2) ? 0 : (32 - __builtin_clz((unsigned)(K + 3 - 1
 enum : u32 { MR_COMPOSITE_V = 0, MR_PROBABLY_PRIME_V = 1, MR_FACTOR_V = 2 };
 
 constexpr BaseLayout BL = base_layout(K);
-constexpr u32 O_C = BL.c, O_C2 = BL.c2, O_A1 = BL.A1, O_A1R = BL.A1r, O_A2 = BL.A2, O_A2R = BL.A2r;
-constexpr u32 O_C1 = BL.C1, O_PIN = BL.pin, O_MISC = BL.misc, O_MPL = BL.MpL, O_NMP = BL.NMp;
+constexpr u32 O_C = BL.c, O_C2 = BL.c2, O_A1R = BL.A1r, O_A2R = BL.A2r;
+constexpr u32 O_C1 = BL.C1, O_PIN = BL.pin, O_MISC = BL.misc, O_NMP = BL.NMp;
 constexpr u32 O_MIS = BL.MiS, O_MU = BL.MU, O_ONE = BL.ONE, O_ML = BL.ML;
-constexpr u32 BASE_WORDS = BL.words;
+constexpr u32 BASE_WORDS = BL.const_words;          // __constant__ prefix of the base table
 constexpr u32 CXW = cx_words(K);
 constexpr u32 SMEM_STATE = NCH * T;           // words of per-CTA residue state
 constexpr size_t SMEM_BYTES = 4 * (size_t)(SMEM_STATE + BEW + CXW);   // state | BE image | context
@@ -283,7 +283,7 @@ __device__ __forceinline__ void to_rns(u32 *st, const u32 *__restrict__ x, u32 x
 // "provided an extra modulus"), X = Σ_j ξ'_j M'_j + α'(2^(32(K+1)) - M') mod 2^(32(K+1)) = z, then
 // X mod N by conditional subtraction of N·2^s, s = SMAX..0.  Leaves X in st[0..K] (limb l in row l).
 template <class CS>
-__device__ __forceinline__ void from_rns(u32 *st, const CS &cs) {
+__device__ __forceinline__ void from_rns(u32 *st, const CS &cs, const u32 *__restrict__ mpl) {
     u32 x[K];
 #pragma unroll
     for (int j = 0; j < K; j++) x[j] = S(st, K + j);
@@ -296,7 +296,7 @@ __device__ __forceinline__ void from_rns(u32 *st, const CS &cs) {
     for (int l = 0; l <= K; l++) {
         u32 lo = clo, mi = cmi, hi = 0;
 #pragma unroll
-        for (int j = 0; j < K; j++) mac96(lo, mi, hi, x[j], GB(O_MPL + j * (K + 1) + l));
+        for (int j = 0; j < K; j++) mac96(lo, mi, hi, x[j], __ldg(mpl + j * (K + 1) + l));
         mac96(lo, mi, hi, alpha, GB(O_NMP + l));
         S(st, l) = lo;
         clo = mi;
@@ -342,23 +342,19 @@ __device__ __forceinline__ void stage_smem(u32 *s_be, u32 *s_cx, const u32 *gcx,
 }
 
 // ------------------------------------------------------------------ modexp interpreter kernel (a2-a7, a8 ladders)
-__global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
-    extern __shared__ __align__(16) u32 smem[];
-    u32 *st = smem;
-    u32 *s_be = smem + SMEM_STATE;
-    u32 *s_cx = s_be + BEW;
-    const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
-    const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
-    stage_smem(s_be, s_cx, gcx, P.be_tab);
-    const u32 jl = (blockIdx.x - sel * P.ctas0) * T + threadIdx.x;
-    if (jl >= P.count) return;
+// The exponentiation program of one message (one thread): entry, window table, ladder, exit
+// multiply, canonical exit, store.  MM is the Montgomery multiplication (IMAD tiles or tensor core);
+// `valid` = false runs the program on zeros without storing (tail threads of a tensor-core tile
+// must still take part in the tile's barriers).
+template <class MM>
+__device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 jl, u32 slot, bool valid, u32 *st,
+                                            const u32 *s_cx, MM &mm) {
     const CtxSmem cs{s_cx};
-    const u32 slot = sel * P.ctas0 * T + jl;
     const size_t tstride = P.jobs_total;
     const size_t entry = (size_t)NCH * tstride;
-    const u32 *xrow = P.x + (size_t)jl * P.in_limbs;
-    const bool ok = less_than(xrow, s_cx + cx_inb(K), P.in_limbs);
-    if (sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
+    const u32 *xrow = P.x + (size_t)(valid ? jl : 0) * P.in_limbs;
+    const bool ok = valid && less_than(xrow, s_cx + cx_inb(K), P.in_limbs);
+    if (valid && sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
 
     const u64 *prog = sel ? P.prog[1] : P.prog[0];
     const u32 nops = sel ? P.nops[1] : P.nops[0];
@@ -387,7 +383,7 @@ __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
             if (sq) { bp = s_cx; bs = 0; }
             else if (opnd >= 0xF0) { bp = s_cx + cx_r2(K) + (opnd - 0xF0) * NCH; bs = 1; }
             else { bp = P.table + opnd * entry + slot; bs = (u32)tstride; }
-            mont_mul(st, bp, bs, sq, cs, s_be);
+            mm(st, bp, bs, sq, cs);
         }
         if (fl & OPF_ADD) {  // channel-wise modular addition (CRT entry, a3)
             const u32 *src = P.table + ad * entry + slot;
@@ -405,18 +401,290 @@ __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
             for (int c = 0; c < NCH; c++) dst[c * tstride] = S(st, c);
         }
     }
-    from_rns(st, cs);
-    u32 *yrow = P.y + sel * P.out_stride + (size_t)jl * P.out_limbs;
+    from_rns(st, cs, P.mpl);
+    if (valid) {
+        u32 *yrow = P.y + sel * P.out_stride + (size_t)jl * P.out_limbs;
 #pragma unroll 1
-    for (u32 l = 0; l < P.out_limbs; l++) yrow[l] = ok ? S(st, l) : 0u;
+        for (u32 l = 0; l < P.out_limbs; l++) yrow[l] = ok ? S(st, l) : 0u;
+    }
 }
+
+struct MulImad {                      // IMAD-pipe Montgomery multiplication (register-tiled contraction)
+    const u32 *s_be;
+    __device__ __forceinline__ void operator()(u32 *st, const u32 *bp, u32 bs, bool sq, const CtxSmem &cs) {
+        mont_mul(st, bp, bs, sq, cs, s_be);
+    }
+};
+
+__global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
+    extern __shared__ __align__(1024) u32 smem[];
+    u32 *st = smem;
+    u32 *s_be = smem + SMEM_STATE;
+    u32 *s_cx = s_be + BEW;
+    const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
+    const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
+    stage_smem(s_be, s_cx, gcx, P.be_tab);
+    const u32 jl = (blockIdx.x - sel * P.ctas0) * T + threadIdx.x;
+    if (jl >= P.count) return;
+    MulImad mm{s_be};
+    run_program(P, sel, jl, sel * P.ctas0 * T + jl, true, st, s_cx, mm);
+}
+
+#if MR_K * 4 <= 256
+// ------------------------------------------------------------------ tensor-core Montgomery multiplication
+// DESIGN.md §4b.  Both base extensions run on the 5th-generation tensor cores as u8 x u8 -> s32
+// contractions (tcgen05.mma.kind::i8): with x_i = Σ_a byte_a(x_i) 2^(8a) and the pre-shifted
+// constants C^(a)_ij = 2^(8a) A_ij mod m_j split into bytes b,
+//     D[m][(j, b)] = Σ_(i, a) byte_a(x_{m,i}) · byte_b(C^(a)_ij),   Σ_i x_i A_ij ≡ Σ_b 2^(8b) D[m][(j, b)].
+// One tile = 128 messages = 128 threads = the 128 TMEM lanes of an M = 128 MMA.  A CTA runs TCT
+// independent tiles; each tile keeps its q-digits as the A operand in shared memory (core-matrix
+// layout), its accumulator in TCNP TMEM columns, and synchronises with a named barrier and an
+// mbarrier signalled by tcgen05.commit.  Elementwise steps and the m_r column stay on the CUDA cores.
+constexpr u32 TCKP = tc_kp(K), TCNP = tc_np(K), TCSBO = tc_sbo(K);
+constexpr u32 BEV_ = BEW - bev_c(K);
+constexpr size_t tc_smem_for(int tiles) {
+    return 4 * (size_t)(tiles * SMEM_STATE + BEV_ + CXW) + (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
+}
+// tiles per CTA: as many as fit the 227 KB of shared memory and the 512 TMEM columns
+constexpr int TCT = (tc_smem_for(3) <= 232448 && 3 * TCNP <= 512) ? 3 : ((tc_smem_for(2) <= 232448 && 2 * TCNP <= 512) ? 2 : 1);
+static_assert(tc_smem_for(TCT) <= 232448, "tensor-core tile does not fit shared memory");
+constexpr u32 TC_IDESC = (2u << 4) | ((TCNP >> 3) << 17) | ((128u >> 4) << 24);  // s32 = u8 x u8, K-major, M=128
+constexpr u32 tmem_cols_for(u32 n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
+constexpr u32 TC_TMEM_COLS = tmem_cols_for(TCT * TCNP);   // power of two >= 32
+constexpr u32 BEV = BEV_;                                      // the per-channel vectors of the BE image
+constexpr size_t TC_SMEM = tc_smem_for(TCT);
+
+__device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ u64 umma_desc(u32 saddr) {
+    return (u64)((saddr >> 4) & 0x3FFF) | ((u64)(128u >> 4) << 16) | ((u64)(TCSBO >> 4) << 32) | ((u64)1 << 46);
+}
+
+struct TcTile {
+    uint8_t *a;                       // A operand tile (128 x TCKP bytes)
+    const uint8_t *b1, *b2;           // B images: BE1 (this context), BE2 (this k)
+    u32 tmem;                         // TMEM address of this tile's accumulator (lane 0, first column)
+    u32 mbar;                         // shared address of this tile's mbarrier
+    u32 phase;                        // mbarrier phase parity
+    int bar;                          // named barrier id (1 + tile)
+    bool leader;                      // thread 0 of the tile issues the MMAs
+    u32 m;                            // message (= TMEM lane) index inside the tile
+};
+
+__device__ __forceinline__ void tile_sync(const TcTile &t) { asm volatile("bar.sync %0, 128;" ::"r"(t.bar) : "memory"); }
+
+// issue the K-steps of one base extension and wait for completion
+__device__ __forceinline__ void tc_contract(TcTile &t, const uint8_t *bimg) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // A tile written by the generic proxy
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    tile_sync(t);
+    if (t.leader) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const u32 sa = smem_u32(t.a), sb = smem_u32(bimg);
+#pragma unroll
+        for (u32 ks = 0; ks < TCKP / 32; ks++) {
+            const u64 da = umma_desc(sa + ks * 256), db = umma_desc(sb + ks * 256);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t.tmem),
+                "l"(da), "l"(db), "r"(TC_IDESC), "r"(ks) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(t.mbar)
+                     : "memory");
+    }
+    // bounded wait: a lost completion traps (kernel error) instead of hanging the GPU
+    u32 done = 0;
+#pragma unroll 1
+    for (u32 spin = 0; !done; spin++) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n\t}"
+            : "=r"(done)
+            : "r"(t.mbar), "r"(t.phase)
+            : "memory");
+        if (spin > (1u << 26)) __trap();
+    }
+    t.phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(u32 taddr, u32 (&v)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Σ_b 2^(8b) d_b as a 64-bit (hi, lo) pair; d_b < 2^24, so d0 + 2^8 d1 and d2 + 2^8 d3 fit in 32 bits
+__device__ __forceinline__ void tc_combine(u32 d0, u32 d1, u32 d2, u32 d3, u32 &hi, u32 &lo) {
+    const u32 x = d0 + (d1 << 8), y = d2 + (d3 << 8);
+    lo = x + (y << 16);
+    hi = (y >> 16) + (lo < x ? 1u : 0u);
+}
+
+// (hi, lo) with hi < 2^17 -> congruent value in [0, 2^32) mod 2^32 - c
+__device__ __forceinline__ u32 fold_small(u32 hi, u32 lo, u32 c) {
+    const u32 r = hi * c + lo;
+    return r < lo ? r + c : r;
+}
+
+struct MulTc {
+    const u32 *s_be;
+    TcTile t;
+    __device__ __forceinline__ void operator()(u32 *st, const u32 *bp, u32 bs, bool sq, const CtxSmem &cs) {
+        const u32 lane_base = (u32)(t.m & ~31u) << 16;
+        // a multiplicand from the window table (HBM) is loaded into registers up front (all loads in
+        // flight together) so the channel products do not wait on HBM latency one by one
+        u32 bv[NCH];
+        if (!sq) {
+#pragma unroll
+            for (int c = 0; c < NCH; c++) bv[c] = bp[(size_t)c * bs];
+        }
+        // ---- 6.1/6.2: q-digits ξ_i (B) -> A tile, t*_j (B') -> state rows; m_r column of BE1
+        u32 qr = 0;
+        uint8_t *arow = t.a + (t.m / 8) * TCSBO + (t.m % 8) * 16;
+#pragma unroll
+        for (int c = 0; c < (K + 3) / 4; c++) {
+            u32 w[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int i = 4 * c + q;
+                w[q] = 0;
+                if (i < K) {
+                    const u32 a = S(st, i);
+                    const u32 b = sq ? a : bv[i];
+                    const u32 cc = s_be[bev_c(K) + i];
+                    const u32 xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
+                    qr += xi * s_be[bev_A1r(K) + i];
+                    w[q] = xi;
+                }
+            }
+            *reinterpret_cast<uint4 *>(arow + c * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+#pragma unroll
+        for (int j = 0; j < K; j++) {
+            const u32 a = S(st, K + j);
+            const u32 b = sq ? a : bv[K + j];
+            S(st, K + j) = mulmod(a, b, s_be[bev_c(K) + K + j]);
+        }
+        const u32 ar = S(st, 2 * K);
+        const u32 tr = ar * (sq ? ar : bv[2 * K]);
+        const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
+        // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij)
+        tc_contract(t, t.b1);
+        u32 sr = 0;
+#pragma unroll 2
+        for (int g = 0; g < (K + 3) / 4; g++) {
+            u32 v[16];
+            tmem_ld16(t.tmem + lane_base + 16 * g, v);
+            u32 w[4];
+#pragma unroll
+            for (int o = 0; o < 4; o++) {
+                const int j = 4 * g + o;
+                w[o] = 0;
+                if (j < K) {
+                    const u32 c = s_be[bev_c(K) + K + j];
+                    u32 hi, lo;
+                    tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
+                    const u32 q = fold_small(hi, lo, c);
+                    const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + q;   // <= (2^32-1) 2^32: no carry
+                    const u32 xp = red64((u32)(p >> 32), (u32)p, c);
+                    S(st, K + j) = xp;
+                    sr += xp * s_be[bev_A2r(K) + j];
+                    w[o] = xp;
+                }
+            }
+            *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        // ---- 6.6 BE2 on the tensor core, exact through the extra modulus
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // TMEM reads done before reuse
+        tc_contract(t, t.b2);
+        const u32 alpha = (sr - rr) * GB(O_MISC + 1);
+        S(st, 2 * K) = rr;
+#pragma unroll 2
+        for (int g = 0; g < (K + 3) / 4; g++) {
+            u32 v[16];
+            tmem_ld16(t.tmem + lane_base + 16 * g, v);
+#pragma unroll
+            for (int o = 0; o < 4; o++) {
+                const int i = 4 * g + o;
+                if (i < K) {
+                    u32 hi, lo;
+                    tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
+                    const u64 p = (u64)alpha * s_be[bev_pin(K) + i] + (((u64)hi << 32) | lo);  // < 2^48
+                    S(st, i) = fold_small((u32)(p >> 32), (u32)p, s_be[bev_c(K) + i]);
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+};
+
+__global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P) {
+    extern __shared__ __align__(1024) u32 smem[];
+    // layout: [B1 image | B2 image | A tiles | states | BE image | ctx | mbarriers + TMEM slot]
+    uint8_t *s_b1 = reinterpret_cast<uint8_t *>(smem);
+    uint8_t *s_b2 = s_b1 + tc_bbytes(K);
+    uint8_t *s_a = s_b2 + tc_bbytes(K);
+    u32 *st_all = reinterpret_cast<u32 *>(s_a + TCT * tc_abytes(K));
+    u32 *s_vec = st_all + TCT * SMEM_STATE;          // vectors only: s_be[bev_*(K) + i] = s_vec[...]
+    u32 *s_be = s_vec - bev_c(K);
+    u32 *s_cx = s_vec + BEV;
+    u64 *mbar = reinterpret_cast<u64 *>(s_cx + CXW);
+    u32 *tslot = reinterpret_cast<u32 *>(mbar + TCT);
+    const u32 sel = blockIdx.x >= P.tc_gc ? 1u : 0u;
+    const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
+    const u32 tid = threadIdx.x, tile = tid / 128, m = tid % 128;
+    // stage constants: context block, IMAD-path BE image words, tensor images
+    for (u32 w = tid; w < CXW; w += blockDim.x) s_cx[w] = gcx[w];
+    for (u32 w = tid; w < BEV; w += blockDim.x) s_vec[w] = __ldg(P.be_tab + bev_c(K) + w);
+    const uint4 *g_b1 = reinterpret_cast<const uint4 *>(gcx + P.tc_be1_off);
+    for (u32 w = tid; w < tc_bbytes(K) / 16; w += blockDim.x) {
+        reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(g_b1 + w);
+        reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b2) + w);
+    }
+    if (tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
+    if (tid < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(TC_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const u32 tmem_base = *tslot;
+
+    MulTc mm{s_be, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP, smem_u32(mbar + tile), 0u,
+                          1 + (int)tile, m == 0, m}};
+    // per-tile state rows, addressed by S(st, ch) = st[ch * 128 + threadIdx.x]
+    u32 *st = st_all + tile * SMEM_STATE - tile * 128;
+    // Persistent, balanced schedule.  The CTAs form one group per context (so the
+    // shared-memory constants of a CTA serve all its tiles); the tile-jobs t of a group (128
+    // messages each) go round-robin, t -> CTA t % Gc, slot (t / Gc) % TCT: every CTA gets
+    // floor(ctas0/Gc) or one more job, and a final partial round runs one tile per SM instead of
+    // leaving a whole wave of tile slots idle.
+    const u32 Gc = P.tc_gc, cta = blockIdx.x - sel * Gc;
+#pragma unroll 1
+    for (u32 t = cta + Gc * tile; t < P.ctas0; t += Gc * TCT) {
+        const u32 jl = t * 128 + m;
+        run_program(P, sel, jl, sel * P.ctas0 * 128 + jl, jl < P.count, st, s_cx, mm);
+    }
+
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS));
+}
+#endif
 
 // ------------------------------------------------------------------ CRT recombination (a8)
 // m = m_q + q · h,  h = (m_p - m_q mod p) · qinv mod p computed as one RNS Montgomery
 // multiplication by qinv·R mod p followed by the canonical exit.  The output row doubles as
 // positional scratch (it is overwritten by m at the end).
 __global__ void __launch_bounds__(T, MINB) k_combine(const CombineParams P) {
-    extern __shared__ __align__(16) u32 smem[];
+    extern __shared__ __align__(1024) u32 smem[];
     u32 *st = smem;
     u32 *s_be = smem + SMEM_STATE;
     u32 *s_cx = s_be + BEW;
@@ -468,7 +736,7 @@ __global__ void __launch_bounds__(T, MINB) k_combine(const CombineParams P) {
     // h = diff · qinv mod p in RNS:  mm(diff, qinv R mod p) ≡ diff qinv (mod p), then canonical
     to_rns(st, mrow, 1, H, true, P.pow_tab);
     mont_mul(st, s_cx + cx_qinvr(K), 1, false, cs, s_be);
-    from_rns(st, cs);
+    from_rns(st, cs, P.mpl);
     // m = m_q + q · h  (schoolbook, H x H limbs)
 #pragma unroll 1
     for (u32 l = 0; l < 2 * H; l++) mrow[l] = l < H ? mq[l] : 0u;
@@ -560,7 +828,7 @@ __device__ __forceinline__ void add_sub(u32 *v, const u32 *w, const u32 *nrow, u
 
 // setup: residues of n, FACTOR check, σ_i, |n M^-1 λ_j|, n M^-1 mod 2^32, s, d, R^2 = M^2 mod n
 __global__ void __launch_bounds__(T) k_mr_setup(const MrParams P) {
-    extern __shared__ __align__(16) u32 smem[];
+    extern __shared__ __align__(1024) u32 smem[];
     u32 *st = smem;
     const u32 i = blockIdx.x * T + threadIdx.x;
     if (i >= P.count) return;
@@ -656,7 +924,7 @@ __device__ __forceinline__ bool x_is_nm1(u32 *st, const u32 *nrow, u32 L) {
 
 // one thread per candidate, all rounds; early exit per candidate unless P.forced
 __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
-    extern __shared__ __align__(16) u32 smem[];
+    extern __shared__ __align__(1024) u32 smem[];
     u32 *st = smem;
     u32 *s_be = smem + SMEM_STATE;
     u32 *s_one = s_be + BEW;
@@ -744,7 +1012,7 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
 #pragma unroll 1
             for (int c = 0; c < NCH; c++) stash[(size_t)c * cnt] = S(st, c);
             mont_mul(st, s_one, 1, false, cs, s_be);                 // leave the Montgomery domain
-            from_rns(st, cs);
+            from_rns(st, cs, P.mpl);
             const bool one = x_is_one(st), nm1 = x_is_nm1(st, nrow, L);
             if (nm1) { pass = true; decided = true; }
             else if (one) { pass = (j == 0); decided = true; }  // y = 1 first: pass; later: composite
@@ -780,10 +1048,29 @@ int upload_base(const u32 *flat, int device) {
     for (const void *k : kerns)
         if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) != cudaSuccess)
             return 6;
+#if MR_K * 4 <= 256
+    if (cudaFuncSetAttribute((const void *)k_modexp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM) !=
+        cudaSuccess)
+        return 6;
+#endif
     return 0;
 }
 
 int launch_modexp(const ModexpParams &p, u32 ctas, void *stream) { return launch(k_modexp, ctas, p, stream); }
+
+#if MR_K * 4 <= 256
+int launch_modexp_tc(const ModexpParams &p, u32 ctas, void *stream) {
+    void *args[] = {const_cast<ModexpParams *>(&p)};
+    return cudaLaunchKernel((const void *)k_modexp_tc, dim3(ctas), dim3(TCT * 128), args, TC_SMEM,
+                            (cudaStream_t)stream) == cudaSuccess
+               ? 0
+               : 6;
+}
+constexpr int TC_TILES = TCT;
+#else
+constexpr int (*launch_modexp_tc)(const ModexpParams &, u32, void *) = nullptr;
+constexpr int TC_TILES = 0;
+#endif
 
 int launch_combine(const CombineParams &p, void *stream) { return launch(k_combine, (p.count + T - 1) / T, p, stream); }
 

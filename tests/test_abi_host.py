@@ -75,22 +75,27 @@ def _tables(k):
 
 
 def _layout(k):
+    """python mirror of mr_internal.h base_layout (prefix = __constant__ bank)."""
     o = {}
     o["c"] = 0
     o["c2"] = 2 * k
-    o["A1"] = 4 * k
-    o["A1r"] = o["A1"] + k * k
-    o["A2"] = o["A1r"] + k
-    o["A2r"] = o["A2"] + k * k
+    o["A1r"] = 4 * k
+    o["A2r"] = o["A1r"] + k
     o["C1"] = o["A2r"] + k
     o["pin"] = o["C1"] + k
     o["misc"] = o["pin"] + k
-    o["MpL"] = o["misc"] + 4
-    o["NMp"] = o["MpL"] + k * (k + 1)
+    o["NMp"] = o["misc"] + 4
+    o["MiS"] = o["NMp"] + k + 1
+    o["MU"] = o["MiS"] + k
+    o["ONE"] = o["MU"] + k
+    o["ML"] = o["ONE"] + 2 * k + 1
+    o["MpL"] = o["ML"] + k + 1
+    o["A1"] = o["MpL"] + k * (k + 1)
+    o["A2"] = o["A1"] + k * k
     return o
 
 
-@pytest.mark.parametrize("k", [1, 3, 17, 33])
+@pytest.mark.parametrize("k", [1, 3, 17, 33, 97])
 def test_base_table_identities(k):
     import sympy
     flat, primes, pw = _tables(k)
@@ -130,6 +135,13 @@ def test_base_table_identities(k):
     assert f[o["misc"]] * M % W == 1 and f[o["misc"] + 1] * Mp % W == 1
     nmp = sum(f[o["NMp"] + l] << (32 * l) for l in range(k + 1))
     assert nmp + Mp == 1 << (32 * (k + 1))
+    assert sum(f[o["ML"] + l] << (32 * l) for l in range(k + 1)) == M
+    for i in range(k):
+        assert f[o["MiS"] + i] == (M // B[i]) % B[i] and f[o["ONE"] + i] == 1
+    for j in range(k):
+        assert f[o["MU"] + j] == pow(M, -1, Bp[j])
+        assert f[o["ONE"] + k + j] == pow(Mp // Bp[j], -1, Bp[j])
+    assert f[o["ONE"] + 2 * k] == 1
     # to_rns powers: |2^(32 l)|_{m_i} and |2^(32 l) λ_j|_{m'_j}
     for l in range(k):
         for i in range(k):

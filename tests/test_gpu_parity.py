@@ -80,7 +80,7 @@ def test_brute_force_tiny_moduli(torch_cuda, mr, orc):
             assert all(s == 0 for s in st)
 
 
-@pytest.mark.parametrize("bits", [64, 256, 512, 1000, 1024, 1536, 2048])
+@pytest.mark.parametrize("bits", [64, 256, 512, 1000, 1024, 1536, 2048, 3072, 4000])
 def test_random_moduli_and_exponents(torch_cuda, mr, orc, bits):
     rng = random.Random(bits)
     N = rng.getrandbits(bits) | 1 | (1 << (bits - 1))
@@ -211,3 +211,22 @@ def test_c2_full_size_sampled(torch_cuda, mr, orc, keys):
     idx = list(range(0, 512)) + list(range(512, count, 257))
     ref = orc.crt_decrypt_batch(cs[idx], k["p"], k["q"], k["dp"], k["dq"], k["qinv"], 32, threads=8)
     assert np.array_equal(host(m)[idx], ref)
+
+
+def test_c3_rsa3072_encrypt_decrypt(torch_cuda, mr, orc, keys):
+    """C3 shape: RSA-3072 encryption (k = 97) and CRT decryption (k = 49 per half), ragged batch."""
+    k = keys["rsa3072"]
+    n, L = k["n"], 96
+    msgs = synth.messages(n, 300, 0x5EEDC003, L, edge=synth.edge_values(n, k["p"], k["q"]))
+    ctx = mr.RnsContext(n, L)
+    assert ctx.k == 97
+    x = dev(torch_cuda, msgs)
+    c = torch_cuda.empty_like(x)
+    ctx.encrypt(x, c, k["e"])
+    key = mr.RsaPrivateKey(k["p"], k["q"], k["dp"], k["dq"], k["qinv"])
+    m = torch_cuda.empty_like(x)
+    key.decrypt(c, m)
+    torch_cuda.cuda.synchronize()
+    ref = orc.modexp_batch(msgs[:96], k["e"], n, threads=8)
+    assert np.array_equal(host(c)[:96], ref)
+    assert np.array_equal(host(m), msgs)
