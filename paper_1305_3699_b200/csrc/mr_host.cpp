@@ -331,6 +331,14 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
     }
     const Base &b = base_for(k);
     if (cudaSetDevice(device) != cudaSuccess) return MR_ERR_CUDA;
+    {   // scratch (window tables, CRT halves) is stream-ordered: keep freed blocks in the device's
+        // default pool instead of returning them to the OS at every synchronisation
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     const KernelSet &ks = kernel_set_for(k);
     if (ks.upload_base(b.flat.data(), device) != 0) return MR_ERR_CUDA;
     DevBase db;

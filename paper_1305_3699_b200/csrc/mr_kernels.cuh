@@ -97,6 +97,16 @@ __device__ __forceinline__ u32 canon(u32 x, u32 c) {  // lazy residue -> [0, m)
 
 __device__ __forceinline__ u32 &S(u32 *st, int ch) { return st[ch * T + threadIdx.x]; }
 
+// Tensor-core tiles keep the B channels of a value inside the tile's A operand (the message's row of
+// the core-matrix layout, where the base extension reads them) and B' ∪ {m_r} in [channel][lane] rows.
+struct StTile {
+    uint8_t *arow;                    // this message's row in the A tile: (m/8)*SBO + (m%8)*16
+    u32 *rows;                        // rows[(ch - K) * 128] = channel ch >= K of this message
+};
+__device__ __forceinline__ u32 &S(const StTile &s, int ch) {
+    return ch < K ? *reinterpret_cast<u32 *>(s.arow + (ch >> 2) * 128 + 4 * (ch & 3)) : s.rows[(ch - K) * 128];
+}
+
 // ------------------------------------------------------------------ per-modulus constant sources
 
 struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt): context block in smem
@@ -254,7 +264,8 @@ __device__ __forceinline__ void mont_mul(u32 *st, const u32 *__restrict__ bp, u3
 // ------------------------------------------------------------------ positional -> RNS (a2)
 // st_c = Σ_l x_l |2^(32 l)|_{m_c} (B' entries of pow_tab carry λ_j: ξ-form), st_r = x_0.
 // x is read at x[l * xstride]; limbs are masked to zero when `ok` is false.
-__device__ __forceinline__ void to_rns(u32 *st, const u32 *__restrict__ x, u32 xstride, u32 nl, bool ok,
+template <class STT>
+__device__ __forceinline__ void to_rns(STT st, const u32 *__restrict__ x, u32 xstride, u32 nl, bool ok,
                                        const u32 *__restrict__ pow_tab) {
     const u32 mask = ok ? 0xFFFFFFFFu : 0u;
     constexpr int W = 8;
@@ -282,8 +293,8 @@ __device__ __forceinline__ void to_rns(u32 *st, const u32 *__restrict__ x, u32 x
 // z on B' ∪ {m_r}, z < (K+3)N < M': α' = (Σ ξ'_j |M'_j|_{2^32} - z_r) M'^-1 mod 2^32 (exact, P:42
 // "provided an extra modulus"), X = Σ_j ξ'_j M'_j + α'(2^(32(K+1)) - M') mod 2^(32(K+1)) = z, then
 // X mod N by conditional subtraction of N·2^s, s = SMAX..0.  Leaves X in st[0..K] (limb l in row l).
-template <class CS>
-__device__ __forceinline__ void from_rns(u32 *st, const CS &cs, const u32 *__restrict__ mpl) {
+template <class STT, class CS>
+__device__ __forceinline__ void from_rns(STT st, const CS &cs, const u32 *__restrict__ mpl) {
     u32 x[K];
 #pragma unroll
     for (int j = 0; j < K; j++) x[j] = S(st, K + j);
@@ -346,8 +357,8 @@ __device__ __forceinline__ void stage_smem(u32 *s_be, u32 *s_cx, const u32 *gcx,
 // multiply, canonical exit, store.  MM is the Montgomery multiplication (IMAD tiles or tensor core);
 // `valid` = false runs the program on zeros without storing (tail threads of a tensor-core tile
 // must still take part in the tile's barriers).
-template <class MM>
-__device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 jl, u32 slot, bool valid, u32 *st,
+template <class STT, class MM>
+__device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 jl, u32 slot, bool valid, STT st,
                                             const u32 *s_cx, MM &mm) {
     const CtxSmem cs{s_cx};
     const size_t tstride = P.jobs_total;
@@ -442,8 +453,9 @@ __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
 // mbarrier signalled by tcgen05.commit.  Elementwise steps and the m_r column stay on the CUDA cores.
 constexpr u32 TCKP = tc_kp(K), TCNP = tc_np(K), TCSBO = tc_sbo(K);
 constexpr u32 BEV_ = BEW - bev_c(K);
+constexpr u32 TC_ROWS = (K + 1) * 128;                          // B' and m_r rows of a tile (words)
 constexpr size_t tc_smem_for(int tiles) {
-    return 4 * (size_t)(tiles * SMEM_STATE + BEV_ + CXW) + (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
+    return 4 * (size_t)(tiles * TC_ROWS + BEV_ + CXW) + (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
 }
 // tiles per CTA: as many as fit the 227 KB of shared memory and the 512 TMEM columns
 constexpr int TCT = (tc_smem_for(3) <= 232448 && 3 * TCNP <= 512) ? 3 : ((tc_smem_for(2) <= 232448 && 2 * TCNP <= 512) ? 2 : 1);
@@ -533,7 +545,7 @@ __device__ __forceinline__ u32 fold_small(u32 hi, u32 lo, u32 c) {
 struct MulTc {
     const u32 *s_be;
     TcTile t;
-    __device__ __forceinline__ void operator()(u32 *st, const u32 *bp, u32 bs, bool sq, const CtxSmem &cs) {
+    __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CtxSmem &cs) {
         const u32 lane_base = (u32)(t.m & ~31u) << 16;
         // a multiplicand from the window table (HBM) is loaded into registers up front (all loads in
         // flight together) so the channel products do not wait on HBM latency one by one
@@ -542,18 +554,22 @@ struct MulTc {
 #pragma unroll
             for (int c = 0; c < NCH; c++) bv[c] = bp[(size_t)c * bs];
         }
-        // ---- 6.1/6.2: q-digits ξ_i (B) -> A tile, t*_j (B') -> state rows; m_r column of BE1
+        // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
+        //      t*_j (B') -> rows; m_r column of BE1
         u32 qr = 0;
-        uint8_t *arow = t.a + (t.m / 8) * TCSBO + (t.m % 8) * 16;
+        uint8_t *arow = st.arow;
 #pragma unroll
         for (int c = 0; c < (K + 3) / 4; c++) {
+            uint4 *chunk = reinterpret_cast<uint4 *>(arow + c * 128);
+            const uint4 av = *chunk;
+            const u32 aw[4] = {av.x, av.y, av.z, av.w};
             u32 w[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const int i = 4 * c + q;
                 w[q] = 0;
                 if (i < K) {
-                    const u32 a = S(st, i);
+                    const u32 a = aw[q];
                     const u32 b = sq ? a : bv[i];
                     const u32 cc = s_be[bev_c(K) + i];
                     const u32 xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
@@ -561,7 +577,7 @@ struct MulTc {
                     w[q] = xi;
                 }
             }
-            *reinterpret_cast<uint4 *>(arow + c * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+            *chunk = make_uint4(w[0], w[1], w[2], w[3]);
         }
 #pragma unroll
         for (int j = 0; j < K; j++) {
@@ -596,9 +612,9 @@ struct MulTc {
                     w[o] = xp;
                 }
             }
-            *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);   // BE2 operand
         }
-        // ---- 6.6 BE2 on the tensor core, exact through the extra modulus
+        // ---- 6.6 BE2 on the tensor core, exact through the extra modulus; r_i back into the A tile
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // TMEM reads done before reuse
         tc_contract(t, t.b2);
         const u32 alpha = (sr - rr) * GB(O_MISC + 1);
@@ -607,16 +623,19 @@ struct MulTc {
         for (int g = 0; g < (K + 3) / 4; g++) {
             u32 v[16];
             tmem_ld16(t.tmem + lane_base + 16 * g, v);
+            u32 w[4];
 #pragma unroll
             for (int o = 0; o < 4; o++) {
                 const int i = 4 * g + o;
+                w[o] = 0;
                 if (i < K) {
                     u32 hi, lo;
                     tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
                     const u64 p = (u64)alpha * s_be[bev_pin(K) + i] + (((u64)hi << 32) | lo);  // < 2^48
-                    S(st, i) = fold_small((u32)(p >> 32), (u32)p, s_be[bev_c(K) + i]);
+                    w[o] = fold_small((u32)(p >> 32), (u32)p, s_be[bev_c(K) + i]);
                 }
             }
+            *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
@@ -629,7 +648,7 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     uint8_t *s_b2 = s_b1 + tc_bbytes(K);
     uint8_t *s_a = s_b2 + tc_bbytes(K);
     u32 *st_all = reinterpret_cast<u32 *>(s_a + TCT * tc_abytes(K));
-    u32 *s_vec = st_all + TCT * SMEM_STATE;          // vectors only: s_be[bev_*(K) + i] = s_vec[...]
+    u32 *s_vec = st_all + TCT * TC_ROWS;             // vectors only: s_be[bev_*(K) + i] = s_vec[...]
     u32 *s_be = s_vec - bev_c(K);
     u32 *s_cx = s_vec + BEV;
     u64 *mbar = reinterpret_cast<u64 *>(s_cx + CXW);
@@ -659,8 +678,9 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
 
     MulTc mm{s_be, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP, smem_u32(mbar + tile), 0u,
                           1 + (int)tile, m == 0, m}};
-    // per-tile state rows, addressed by S(st, ch) = st[ch * 128 + threadIdx.x]
-    u32 *st = st_all + tile * SMEM_STATE - tile * 128;
+    // per-message state: B channels in the A tile row, B' and m_r in the tile's rows
+    uint8_t *tile_a = s_a + tile * tc_abytes(K);
+    const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
     // Persistent, balanced schedule.  The CTAs form one group per context (so the
     // shared-memory constants of a CTA serve all its tiles); the tile-jobs t of a group (128
     // messages each) go round-robin, t -> CTA t % Gc, slot (t / Gc) % TCT: every CTA gets

@@ -103,7 +103,7 @@ def c4(torch, mr, orc, quick):
     n = k["n"]
     ctx = mr.RnsContext(n, 64)
     for ell in ([1024, 16128] if quick else [17, 1024, 2048, 4096, 8192, 16128]):
-        cnt = 65536 if ell <= 2048 else (16384 if ell <= 8192 else 8192)
+        cnt = 65536 if ell <= 8192 else 32768
         E = synth.exponent(ell, 0x5EEDC004)
         xs = synth.messages(n, cnt, 0x5EEDC004, 64)
         x = torch.from_numpy(xs.view(np.int32)).cuda()
