@@ -304,7 +304,7 @@ static void to_rns_host(const Base &b, const Big &x, u32 *out) {
 static void fill_tc_image(int k, const u32 *A /* [k][k], row i, column j */, const std::vector<u32> &mods,
                           uint8_t *out) {
     memset(out, 0, tc_bbytes(k));
-    for (int j = 0; j < k; j++)
+    for (int j = 0; j < (int)tc_nt(k); j++)
         for (int i = 0; i < k; i++)
             for (int a = 0; a < 4; a++) {
                 const u32 v = (u32)(((u64)A[i * k + j] << (8 * a)) % mods[j]);

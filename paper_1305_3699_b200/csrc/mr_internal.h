@@ -101,7 +101,10 @@ __host__ __device__ constexpr u32 be_words(u32 k) { return bev_A2r(k) + pad4(k);
 // D = [128 x NP] s32 in TMEM; every D value < 4k·255² < 2^24 for k <= 64.
 // ---------------------------------------------------------------------------------------------
 __host__ __device__ constexpr u32 tc_kp(u32 k) { return (4 * k + 31) & ~31u; }     // K bytes, multiple of 32
-__host__ __device__ constexpr u32 tc_np(u32 k) { return (4 * k + 15) & ~15u; }     // N rows, multiple of 16
+// outputs of each base extension computed on the tensor core; for k = 33 the 33rd output runs on the
+// CUDA cores so that N = 128 columns and four 128-message tiles fit the 512 TMEM columns of an SM
+__host__ __device__ constexpr u32 tc_nt(u32 k) { return (4 * k > 128 && 4 * k <= 136) ? 32 : k; }
+__host__ __device__ constexpr u32 tc_np(u32 k) { return (4 * tc_nt(k) + 15) & ~15u; }  // N rows, multiple of 16
 __host__ __device__ constexpr bool tc_ok(u32 k) { return 4 * k <= 256; }
 __host__ __device__ constexpr u32 tc_sbo(u32 k) { return (tc_kp(k) / 16) * 128; }
 __host__ __device__ constexpr u32 tc_off(u32 k, u32 r, u32 kb) {

@@ -452,13 +452,20 @@ __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
 // layout), its accumulator in TCNP TMEM columns, and synchronises with a named barrier and an
 // mbarrier signalled by tcgen05.commit.  Elementwise steps and the m_r column stay on the CUDA cores.
 constexpr u32 TCKP = tc_kp(K), TCNP = tc_np(K), TCSBO = tc_sbo(K);
+constexpr int TCNT = tc_nt(K);                                  // outputs per base extension on the tensor core
+constexpr int TCNC = K - TCNT;                                  // outputs on the CUDA cores (k = 33: the last one)
+static_assert(TCNC <= 1, "at most one CUDA-core output per base extension");
+static_assert(TCNT % 4 == 0 || TCNC == 0, "tensor outputs must fill whole 16-column groups when split");
 constexpr u32 BEV_ = BEW - bev_c(K);
 constexpr u32 TC_ROWS = (K + 1) * 128;                          // B' and m_r rows of a tile (words)
+constexpr u32 TC_CVEC = 2 * pad4(K);                            // CUDA-core output columns: A1' col, A2 col
 constexpr size_t tc_smem_for(int tiles) {
-    return 4 * (size_t)(tiles * TC_ROWS + BEV_ + CXW) + (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
+    return 4 * (size_t)(tiles * TC_ROWS + BEV_ + CXW + TC_CVEC) + (size_t)tiles * tc_abytes(K) +
+           2 * (size_t)tc_bbytes(K) + 64;
 }
-// tiles per CTA: as many as fit the 227 KB of shared memory and the 512 TMEM columns
-constexpr int TCT = (tc_smem_for(3) <= 232448 && 3 * TCNP <= 512) ? 3 : ((tc_smem_for(2) <= 232448 && 2 * TCNP <= 512) ? 2 : 1);
+constexpr bool tc_fits(int tiles) { return tc_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
+// tiles per CTA: as many as fit the 227 KB of shared memory and the 512 TMEM columns (at most 4)
+constexpr int TCT = tc_fits(4) ? 4 : (tc_fits(3) ? 3 : (tc_fits(2) ? 2 : 1));
 static_assert(tc_smem_for(TCT) <= 232448, "tensor-core tile does not fit shared memory");
 constexpr u32 TC_IDESC = (2u << 4) | ((TCNP >> 3) << 17) | ((128u >> 4) << 24);  // s32 = u8 x u8, K-major, M=128
 constexpr u32 tmem_cols_for(u32 n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
@@ -467,6 +474,13 @@ constexpr u32 BEV = BEV_;                                      // the per-channe
 constexpr size_t TC_SMEM = tc_smem_for(TCT);
 
 __device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+
+// word index of (input row i, output column j) inside one half of the IMAD-path tile image (be_*)
+__device__ __forceinline__ u32 be_img_index(u32 i, u32 j) {
+    const u32 t = j / CH;
+    if (t < (u32)(KF / CH)) return t * K * pad4(CH) + i * pad4(CH) + (j - t * CH);
+    return (KF / CH) * K * pad4(CH) + i * pad4(KT ? KT : 1) + (j - KF);
+}
 
 __device__ __forceinline__ u64 umma_desc(u32 saddr) {
     return (u64)((saddr >> 4) & 0x3FFF) | ((u64)(128u >> 4) << 16) | ((u64)(TCSBO >> 4) << 32) | ((u64)1 << 46);
@@ -485,8 +499,8 @@ struct TcTile {
 
 __device__ __forceinline__ void tile_sync(const TcTile &t) { asm volatile("bar.sync %0, 128;" ::"r"(t.bar) : "memory"); }
 
-// issue the K-steps of one base extension and wait for completion
-__device__ __forceinline__ void tc_contract(TcTile &t, const uint8_t *bimg) {
+// issue the K-steps of one base extension (tile leader) after the A tile is complete
+__device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // A tile written by the generic proxy
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     tile_sync(t);
@@ -504,7 +518,10 @@ __device__ __forceinline__ void tc_contract(TcTile &t, const uint8_t *bimg) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(t.mbar)
                      : "memory");
     }
-    // bounded wait: a lost completion traps (kernel error) instead of hanging the GPU
+}
+
+// wait for the tile's MMA chain (bounded: a lost completion traps instead of hanging the GPU)
+__device__ __forceinline__ void tc_wait(TcTile &t) {
     u32 done = 0;
 #pragma unroll 1
     for (u32 spin = 0; !done; spin++) {
@@ -544,20 +561,16 @@ __device__ __forceinline__ u32 fold_small(u32 hi, u32 lo, u32 c) {
 
 struct MulTc {
     const u32 *s_be;
+    const u32 *s_a1c;                 // CUDA-core output column of BE1: A1'[i][TCNT] (this context)
+    const u32 *s_a2c;                 // CUDA-core output column of BE2: A2[j][TCNT]
     TcTile t;
     __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CtxSmem &cs) {
         const u32 lane_base = (u32)(t.m & ~31u) << 16;
-        // a multiplicand from the window table (HBM) is loaded into registers up front (all loads in
-        // flight together) so the channel products do not wait on HBM latency one by one
-        u32 bv[NCH];
-        if (!sq) {
-#pragma unroll
-            for (int c = 0; c < NCH; c++) bv[c] = bp[(size_t)c * bs];
-        }
-        // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
-        //      t*_j (B') -> rows; m_r column of BE1
-        u32 qr = 0;
         uint8_t *arow = st.arow;
+        // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
+        //      t*_j (B') -> rows; m_r column of BE1; CUDA-core BE1 output accumulated on the fly
+        u32 qr = 0;
+        u32 c1lo = 0, c1mi = 0, c1hi = 0;
 #pragma unroll
         for (int c = 0; c < (K + 3) / 4; c++) {
             uint4 *chunk = reinterpret_cast<uint4 *>(arow + c * 128);
@@ -570,29 +583,41 @@ struct MulTc {
                 w[q] = 0;
                 if (i < K) {
                     const u32 a = aw[q];
-                    const u32 b = sq ? a : bv[i];
+                    const u32 b = sq ? a : bp[(size_t)i * bs];
                     const u32 cc = s_be[bev_c(K) + i];
                     const u32 xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
                     qr += xi * s_be[bev_A1r(K) + i];
+                    if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
                     w[q] = xi;
                 }
             }
             *chunk = make_uint4(w[0], w[1], w[2], w[3]);
         }
-#pragma unroll
+#pragma unroll 4
         for (int j = 0; j < K; j++) {
             const u32 a = S(st, K + j);
-            const u32 b = sq ? a : bv[K + j];
+            const u32 b = sq ? a : bp[(size_t)(K + j) * bs];
             S(st, K + j) = mulmod(a, b, s_be[bev_c(K) + K + j]);
         }
         const u32 ar = S(st, 2 * K);
-        const u32 tr = ar * (sq ? ar : bv[2 * K]);
+        const u32 tr = ar * (sq ? ar : bp[(size_t)(2 * K) * bs]);
         const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
         // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij)
-        tc_contract(t, t.b1);
+        tc_issue(t, t.b1);
+        u32 xp_c = 0;
+        if (TCNC) {   // the CUDA-core output overlaps the MMA
+            const int j = TCNT;
+            const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
+            mac96(c1lo, c1mi, c1hi, (u32)p, 1u);
+            u32 hi2 = c1hi;
+            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(c1mi), "+r"(hi2) : "r"((u32)(p >> 32)));
+            xp_c = red96(hi2, c1mi, c1lo, s_be[bev_c(K) + K + j], 0);
+        }
+        tc_wait(t);
         u32 sr = 0;
+        u32 c2lo = 0, c2mi = 0, c2hi = 0;
 #pragma unroll 2
-        for (int g = 0; g < (K + 3) / 4; g++) {
+        for (int g = 0; g < TCNT / 4 + (TCNT % 4 ? 1 : 0); g++) {
             u32 v[16];
             tmem_ld16(t.tmem + lane_base + 16 * g, v);
             u32 w[4];
@@ -600,7 +625,7 @@ struct MulTc {
             for (int o = 0; o < 4; o++) {
                 const int j = 4 * g + o;
                 w[o] = 0;
-                if (j < K) {
+                if (j < TCNT) {
                     const u32 c = s_be[bev_c(K) + K + j];
                     u32 hi, lo;
                     tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
@@ -609,18 +634,33 @@ struct MulTc {
                     const u32 xp = red64((u32)(p >> 32), (u32)p, c);
                     S(st, K + j) = xp;
                     sr += xp * s_be[bev_A2r(K) + j];
+                    if (TCNC) mac96(c2lo, c2mi, c2hi, xp, s_a2c[j]);
                     w[o] = xp;
                 }
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);   // BE2 operand
         }
+        if (TCNC) {   // CUDA-core output of BE1 completes the BE2 operand and its own BE2 term
+            const int j = TCNT;
+            S(st, K + j) = xp_c;
+            sr += xp_c * s_be[bev_A2r(K) + j];
+            mac96(c2lo, c2mi, c2hi, xp_c, s_a2c[j]);
+            *reinterpret_cast<uint4 *>(arow + (j / 4) * 128) = make_uint4(xp_c, 0u, 0u, 0u);
+        }
         // ---- 6.6 BE2 on the tensor core, exact through the extra modulus; r_i back into the A tile
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // TMEM reads done before reuse
-        tc_contract(t, t.b2);
+        tc_issue(t, t.b2);
         const u32 alpha = (sr - rr) * GB(O_MISC + 1);
         S(st, 2 * K) = rr;
+        u32 r_c = 0;
+        if (TCNC) {
+            const int i = TCNT;
+            mac96(c2lo, c2mi, c2hi, alpha, s_be[bev_pin(K) + i]);
+            r_c = red96(c2hi, c2mi, c2lo, s_be[bev_c(K) + i], 0);
+        }
+        tc_wait(t);
 #pragma unroll 2
-        for (int g = 0; g < (K + 3) / 4; g++) {
+        for (int g = 0; g < TCNT / 4 + (TCNT % 4 ? 1 : 0); g++) {
             u32 v[16];
             tmem_ld16(t.tmem + lane_base + 16 * g, v);
             u32 w[4];
@@ -628,7 +668,7 @@ struct MulTc {
             for (int o = 0; o < 4; o++) {
                 const int i = 4 * g + o;
                 w[o] = 0;
-                if (i < K) {
+                if (i < TCNT) {
                     u32 hi, lo;
                     tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
                     const u64 p = (u64)alpha * s_be[bev_pin(K) + i] + (((u64)hi << 32) | lo);  // < 2^48
@@ -637,6 +677,7 @@ struct MulTc {
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
         }
+        if (TCNC) *reinterpret_cast<uint4 *>(arow + (TCNT / 4) * 128) = make_uint4(r_c, 0u, 0u, 0u);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     }
 };
@@ -651,7 +692,9 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     u32 *s_vec = st_all + TCT * TC_ROWS;             // vectors only: s_be[bev_*(K) + i] = s_vec[...]
     u32 *s_be = s_vec - bev_c(K);
     u32 *s_cx = s_vec + BEV;
-    u64 *mbar = reinterpret_cast<u64 *>(s_cx + CXW);
+    u32 *s_a1c = s_cx + CXW;                         // CUDA-core output columns (k = 33)
+    u32 *s_a2c = s_a1c + pad4(K);
+    u64 *mbar = reinterpret_cast<u64 *>(s_a2c + pad4(K));
     u32 *tslot = reinterpret_cast<u32 *>(mbar + TCT);
     const u32 sel = blockIdx.x >= P.tc_gc ? 1u : 0u;
     const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
@@ -663,6 +706,12 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     for (u32 w = tid; w < tc_bbytes(K) / 16; w += blockDim.x) {
         reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(g_b1 + w);
         reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b2) + w);
+    }
+    if (TCNC) {   // columns TCNT of the IMAD-path tile images (BE1 merged from this context, BE2 per k)
+        for (u32 i = tid; i < (u32)K; i += blockDim.x) {
+            s_a1c[i] = gcx[CXW + be_img_index(i, TCNT)];
+            s_a2c[i] = __ldg(P.be_tab + BEH + be_img_index(i, TCNT));
+        }
     }
     if (tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
     if (tid < 32) {
@@ -676,7 +725,7 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem_base = *tslot;
 
-    MulTc mm{s_be, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP, smem_u32(mbar + tile), 0u,
+    MulTc mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP, smem_u32(mbar + tile), 0u,
                           1 + (int)tile, m == 0, m}};
     // per-message state: B channels in the A tile row, B' and m_r in the tile's rows
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
