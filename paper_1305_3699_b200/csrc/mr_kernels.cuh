@@ -372,6 +372,15 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
 #pragma unroll 1
     for (u32 s = 0; s < nops; s++) {
         const u64 op = __ldg(prog + s);
+        if (s + 1 < nops) {   // next multiplicand from the window table: pull it from HBM into L2 now
+            const u64 nx = __ldg(prog + s + 1);
+            const u32 nopnd = (u32)(nx >> 8) & 0xFF;
+            if (!(nx & OPF_NOMUL) && nopnd < 0xF0) {
+                const u32 *np = P.table + nopnd * entry + slot;
+#pragma unroll 1
+                for (int c = 0; c < NCH; c += 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(np + c * tstride));
+            }
+        }
         const u32 fl = (u32)op & 0xFF, opnd = (u32)(op >> 8) & 0xFF, ld = (u32)(op >> 16) & 0xFF;
         const u32 ad = (u32)(op >> 24) & 0xFF, sto = (u32)(op >> 32) & 0xFF;
         if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) {
@@ -571,6 +580,7 @@ struct MulTc {
         //      t*_j (B') -> rows; m_r column of BE1; CUDA-core BE1 output accumulated on the fly
         u32 qr = 0;
         u32 c1lo = 0, c1mi = 0, c1hi = 0;
+        const u32 *bq = bp;                          // multiplicand channel pointer, advanced by bs
 #pragma unroll
         for (int c = 0; c < (K + 3) / 4; c++) {
             uint4 *chunk = reinterpret_cast<uint4 *>(arow + c * 128);
@@ -583,24 +593,26 @@ struct MulTc {
                 w[q] = 0;
                 if (i < K) {
                     const u32 a = aw[q];
-                    const u32 b = sq ? a : bp[(size_t)i * bs];
-                    const u32 cc = s_be[bev_c(K) + i];
+                    const u32 b = sq ? a : *bq;
+                    bq += bs;
+                    const u32 cc = GB(O_C + i);       // unrolled: constant-bank operands
                     const u32 xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
-                    qr += xi * s_be[bev_A1r(K) + i];
+                    qr += xi * GB(O_A1R + i);
                     if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
                     w[q] = xi;
                 }
             }
             *chunk = make_uint4(w[0], w[1], w[2], w[3]);
         }
-#pragma unroll 4
+#pragma unroll
         for (int j = 0; j < K; j++) {
             const u32 a = S(st, K + j);
-            const u32 b = sq ? a : bp[(size_t)(K + j) * bs];
-            S(st, K + j) = mulmod(a, b, s_be[bev_c(K) + K + j]);
+            const u32 b = sq ? a : *bq;
+            bq += bs;
+            S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
         }
         const u32 ar = S(st, 2 * K);
-        const u32 tr = ar * (sq ? ar : bp[(size_t)(2 * K) * bs]);
+        const u32 tr = ar * (sq ? ar : *bq);
         const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
         // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij)
         tc_issue(t, t.b1);
