@@ -318,6 +318,7 @@ struct DevBase {
     u32 *d_be = nullptr;
     u32 *d_mpl = nullptr;      // M'_j limbs [k][k+1] for the exit conversion
     u32 *d_tcb2 = nullptr;     // tensor-core BE2 image (k <= 64)
+    u32 *d_tcb1u = nullptr;    // tensor-core unmerged BE1 image (Miller-Rabin, per-thread modulus)
 };
 static std::map<std::pair<int, int>, DevBase> g_devbases;
 
@@ -360,6 +361,9 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
         fill_tc_image(k, A2, b.B, img.data());
         if (cudaMalloc(&db.d_tcb2, img.size()) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_tcb2, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
+        fill_tc_image(k, b.flat.data() + base_layout(k).A1, b.Bp, img.data());
+        if (cudaMalloc(&db.d_tcb1u, img.size()) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMemcpy(db.d_tcb1u, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
     }
     g_devbases[key] = db;
     *d_pow = db.d_pow;
@@ -960,6 +964,17 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
     P.pow_tab = d_pow;
     P.be_tab = d_be;
     P.mpl = g_devbases[std::make_pair(device, kk)].d_mpl;
+    {
+        const DevBase &db = g_devbases[std::make_pair(device, kk)];
+        const KernelSet &ks0 = kernel_set_for(kk);
+        if (db.d_tcb1u && ks0.launch_modexp_tc && tensor_path_enabled()) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+            P.tc_b1 = db.d_tcb1u;
+            P.tc_b2 = db.d_tcb2;
+            P.tc_gc = std::min<u32>((u32)sms, (u32)((count + 127) / 128));
+        }
+    }
     const KernelSet &ks = kernel_set_for(kk);
     int rc = timed_launch(2, st, [&] { return ks.launch_mr(P, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
     cudaFreeAsync(d_pc, st);

@@ -183,6 +183,9 @@ struct MrParams {               // Miller-Rabin (§3.2; HAC 4.24)
     const u32 *pow_tab;
     const u32 *be_tab;
     const u32 *mpl;
+    const u32 *tc_b1;           // tensor path: unmerged BE1 image (per k); null = IMAD path
+    const u32 *tc_b2;           // tensor path: BE2 image
+    u32 tc_gc;                  // tensor path: persistent CTAs
 };
 
 // per-candidate constant rows for Miller-Rabin (row r at pc + r * count)

@@ -573,7 +573,9 @@ struct MulTc {
     const u32 *s_a1c;                 // CUDA-core output column of BE1: A1'[i][TCNT] (this context)
     const u32 *s_a2c;                 // CUDA-core output column of BE2: A2[j][TCNT]
     TcTile t;
-    __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CtxSmem &cs) {
+    template <class CS>
+    __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CS &cs) {
+        constexpr bool MERGED = CS::kMerged;      // false: per-thread modulus (Miller-Rabin), unmerged BE1
         const u32 lane_base = (u32)(t.m & ~31u) << 16;
         uint8_t *arow = st.arow;
         // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
@@ -619,11 +621,19 @@ struct MulTc {
         u32 xp_c = 0;
         if (TCNC) {   // the CUDA-core output overlaps the MMA
             const int j = TCNT;
+            const u32 cj = s_be[bev_c(K) + K + j];
             const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
-            mac96(c1lo, c1mi, c1hi, (u32)p, 1u);
-            u32 hi2 = c1hi;
-            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(c1mi), "+r"(hi2) : "r"((u32)(p >> 32)));
-            xp_c = red96(hi2, c1mi, c1lo, s_be[bev_c(K) + K + j], 0);
+            if (MERGED) {
+                mac96(c1lo, c1mi, c1hi, (u32)p, 1u);
+                u32 hi2 = c1hi;
+                asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(c1mi), "+r"(hi2) : "r"((u32)(p >> 32)));
+                xp_c = red96(hi2, c1mi, c1lo, cj, 0);
+            } else {
+                const u32 q = red96(c1hi, c1mi, c1lo, cj, 0);
+                u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
+                mac96(l2, m2, h2, q, cs.c2(j));
+                xp_c = red96(h2, m2, l2, cj, 0);
+            }
         }
         tc_wait(t);
         u32 sr = 0;
@@ -642,8 +652,16 @@ struct MulTc {
                     u32 hi, lo;
                     tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
                     const u32 q = fold_small(hi, lo, c);
-                    const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + q;   // <= (2^32-1) 2^32: no carry
-                    const u32 xp = red64((u32)(p >> 32), (u32)p, c);
+                    u32 xp;
+                    if (MERGED) {
+                        const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + q;   // <= (2^32-1) 2^32: no carry
+                        xp = red64((u32)(p >> 32), (u32)p, c);
+                    } else {   // ξ'_j = t*_j C1_j + q̂_j |n M^-1 λ_j|  (6.4 with a per-thread modulus)
+                        const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
+                        u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
+                        mac96(l2, m2, h2, q, cs.c2(j));
+                        xp = red96(h2, m2, l2, c, 0);
+                    }
                     S(st, K + j) = xp;
                     sr += xp * s_be[bev_A2r(K) + j];
                     if (TCNC) mac96(c2lo, c2mi, c2hi, xp, s_a2c[j]);
@@ -1110,6 +1128,233 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
     if (P.status && status) P.status[i] = status;
 }
 
+#if MR_K * 4 <= 256
+// ------------------------------------------------------------------ Miller-Rabin rounds on the tensor cores
+// Same tiles as k_modexp_tc (128 candidates = 128 TMEM lanes, up to TCT tiles per CTA, persistent
+// round-robin tile-jobs), with a per-candidate modulus: the BE1 image is the unmerged per-k one and
+// 6.4 multiplies by |n M^-1 λ_j| per thread (CtxMr).  Every thread of a tile takes part in every
+// Montgomery multiplication of the tile (the MMA is collective); a thread that is already decided,
+// past the end of the batch, or not live (setup verdict) computes on its stale state and its results
+// are ignored.  Early exit is per tile: a round is skipped when no candidate of the tile is pending.
+struct CtxMr {                        // per-candidate constants of one thread
+    static constexpr bool kMerged = false;
+    u32 sig[K];                       // σ_i in registers (the channel-product loop is fully unrolled)
+    const u32 *c2row;                 // shared memory: c2row[j * 128] = |n M^-1 λ_j|_{m'_j}
+    u32 nmv;                          // n M^-1 mod 2^32
+    const u32 *nrow;
+    u32 limbs;
+    __device__ u32 sigma(int i) const { return sig[i]; }
+    __device__ u32 c2(int j) const { return c2row[j * 128]; }
+    __device__ u32 nminv() const { return nmv; }
+    __device__ u32 nlimb(int l) const { return (u32)l < limbs ? nrow[l] : 0u; }
+};
+
+__device__ __forceinline__ bool tile_any(const TcTile &t, bool v) {
+    u32 r;
+    asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+                 "bar.red.or.pred q, %2, 128, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                 : "=r"(r) : "r"((u32)v), "r"(t.bar) : "memory");
+    return r != 0;
+}
+
+__device__ __forceinline__ bool x_is_one_t(const StTile &st) {
+    u32 nz = S(st, 0) ^ 1u;
+#pragma unroll 1
+    for (int l = 1; l <= K; l++) nz |= S(st, l);
+    return nz == 0;
+}
+__device__ __forceinline__ bool x_is_nm1_t(const StTile &st, const u32 *nrow, u32 L) {
+    u32 diff = S(st, 0) ^ (nrow[0] - 1u);
+#pragma unroll 1
+    for (u32 l = 1; l <= (u32)K; l++) diff |= S(st, l) ^ (l < L ? nrow[l] : 0u);
+    return diff == 0;
+}
+
+constexpr size_t tc_mr_smem_for(int tiles) {
+    return 4 * (size_t)(tiles * TC_ROWS + tiles * K * 128 + BEV + pad4(NCH) + 2 * pad4(K)) +
+           (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
+}
+constexpr bool tc_mr_fits(int tiles) { return tc_mr_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
+constexpr int TCM = tc_mr_fits(4) ? 4 : (tc_mr_fits(3) ? 3 : (tc_mr_fits(2) ? 2 : 1));   // MR tiles per CTA
+constexpr u32 TC_MR_TMEM = tmem_cols_for(TCM * TCNP);
+
+__global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P) {
+    extern __shared__ __align__(1024) u32 smem[];
+    // layout: [B1 (unmerged, per k) | B2 | A tiles | state rows | c2 rows | vectors | ONE | a1c | a2c | mbar]
+    uint8_t *s_b1 = reinterpret_cast<uint8_t *>(smem);
+    uint8_t *s_b2 = s_b1 + tc_bbytes(K);
+    uint8_t *s_a = s_b2 + tc_bbytes(K);
+    u32 *st_all = reinterpret_cast<u32 *>(s_a + TCM * tc_abytes(K));
+    u32 *c2_all = st_all + TCM * TC_ROWS;
+    u32 *s_vec = c2_all + TCM * K * 128;
+    u32 *s_be = s_vec - bev_c(K);
+    u32 *s_one = s_vec + BEV;
+    u32 *s_a1c = s_one + pad4(NCH);
+    u32 *s_a2c = s_a1c + pad4(K);
+    u64 *mbar = reinterpret_cast<u64 *>(s_a2c + pad4(K));
+    u32 *tslot = reinterpret_cast<u32 *>(mbar + TCM);
+    const u32 tid = threadIdx.x, tile = tid / 128, m = tid % 128;
+    for (u32 w = tid; w < BEV; w += blockDim.x) s_vec[w] = __ldg(P.be_tab + bev_c(K) + w);
+    for (u32 w = tid; w < (u32)NCH; w += blockDim.x) s_one[w] = GB(O_ONE + w);
+    if (TCNC)
+        for (u32 i = tid; i < (u32)K; i += blockDim.x) {
+            s_a1c[i] = __ldg(P.be_tab + be_img_index(i, TCNT));
+            s_a2c[i] = __ldg(P.be_tab + BEH + be_img_index(i, TCNT));
+        }
+    for (u32 w = tid; w < tc_bbytes(K) / 16; w += blockDim.x) {
+        reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b1) + w);
+        reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b2) + w);
+    }
+    if (tid < (u32)TCM) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
+    if (tid < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(TC_MR_TMEM));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const u32 tmem_base = *tslot;
+
+    MulTc mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
+                                        smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m}};
+    uint8_t *tile_a = s_a + tile * tc_abytes(K);
+    const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
+    u32 *c2rows = c2_all + tile * K * 128 + m;
+    const size_t cnt = P.count;
+    const u32 L = P.limbs, w = P.window, E = 1u << w;
+    const size_t entry = (size_t)NCH * cnt;
+    const u32 ndig = (32 * L + w - 1) / w;
+    const u32 jobs = (P.count + 127) / 128, G = gridDim.x;
+#pragma unroll 1
+    for (u32 job = blockIdx.x + G * tile; job < jobs; job += G * TCM) {
+        const u32 i0 = job * 128 + m;
+        const u32 i = i0 < P.count ? i0 : P.count - 1;          // tail lanes shadow the last candidate
+        const u32 *pcol = P.pc + i;
+        bool pending = i0 < P.count && pcol[(size_t)pc_live(K) * cnt] != 0;
+        const u32 *nrow = P.n + (size_t)i * L;
+        // base rule for every round (HAC 4.24 input), as in k_mr_rounds
+        int32_t status = 0;
+#pragma unroll 1
+        for (u32 r = 0; r < P.rounds && pending && !status; r++) {
+            const u32 *a = P.bases + ((size_t)i * P.rounds + r) * L;
+            u32 br = 0, dhi = 0, ahi = 0, d0 = 0;
+#pragma unroll 1
+            for (u32 l = 0; l < L; l++) {
+                const u64 tt = (u64)nrow[l] - a[l] - br;
+                br = (u32)(tt >> 63);
+                if (l) { dhi |= (u32)tt; ahi |= a[l]; } else d0 = (u32)tt;
+            }
+            if (!(ahi || a[0] >= 2u) || !(!br && (dhi || d0 >= 2u))) status = 5;
+        }
+        if (pending && status) {
+            P.verdict[i] = (uint8_t)MR_COMPOSITE_V;
+            if (P.status) P.status[i] = status;
+            pending = false;
+        }
+        CtxMr cs;
+#pragma unroll
+        for (int k = 0; k < K; k++) cs.sig[k] = pcol[(size_t)(pc_sigma(K) + k) * cnt];
+#pragma unroll 1
+        for (int j = 0; j < K; j++) c2rows[j * 128] = pcol[(size_t)(pc_c2(K) + j) * cnt];
+        cs.c2row = c2rows;
+        cs.nmv = pcol[(size_t)pc_nminv(K) * cnt];
+        cs.nrow = nrow;
+        cs.limbs = L;
+        const u32 *r2 = pcol + (size_t)pc_r2(K) * cnt;
+        const u32 s = pcol[(size_t)pc_s(K) * cnt];
+        const u32 *dl = pcol + (size_t)pc_d(K) * cnt;
+        u32 *tab = P.table + i;
+        u32 *stash = tab + E * entry;
+        u32 verdict = MR_PROBABLY_PRIME_V;
+        int witness = -1;
+        const bool was_live = pending;
+#pragma unroll 1
+        for (u32 r = 0; r < P.rounds; r++) {
+            if (!tile_any(mm.t, pending || (P.forced && was_live))) break;
+            const u32 *a = P.bases + ((size_t)i * P.rounds + r) * L;
+            // uniform part: T0 = mm(R^2, 1), T1 = mm(a, R^2), T[e] = T[e-1] T1, then the fixed-window ladder
+            const u32 nuni = E + ndig * (w + 1);
+#pragma unroll 1
+            for (u32 u = 0; u < nuni; u++) {
+                const u32 *bp;
+                u32 bs;
+                bool sq = false;
+                if (u == 0) {
+#pragma unroll 1
+                    for (int c = 0; c < NCH; c++) S(st, c) = r2[(size_t)c * cnt];
+                    bp = s_one; bs = 1;
+                } else if (u == 1) {
+                    to_rns(st, a, 1, L, true, P.pow_tab);
+                    bp = r2; bs = (u32)cnt;
+                } else if (u < E) {
+                    bp = tab + entry; bs = (u32)cnt;
+                } else {
+                    const u32 q = u - E, dg = ndig - 1 - q / (w + 1), sub = q % (w + 1);
+                    if (q == 0) {
+#pragma unroll 1
+                        for (int c = 0; c < NCH; c++) S(st, c) = tab[(size_t)c * cnt];
+                    }
+                    if (sub < w) { sq = true; bp = s_one; bs = 0; }
+                    else {
+                        const u32 b0 = dg * w, lw = b0 / 32, bw = b0 % 32;
+                        const u32 lo = lw < (u32)K ? dl[(size_t)lw * cnt] : 0u;
+                        const u32 hi = lw + 1 < (u32)K ? dl[(size_t)(lw + 1) * cnt] : 0u;
+                        bp = tab + (size_t)(__funnelshift_r(lo, hi, bw) & (E - 1)) * entry;
+                        bs = (u32)cnt;
+                    }
+                }
+                mm(st, bp, bs, sq, cs);
+                if (u < E) {
+                    u32 *dst = tab + (size_t)u * entry;
+#pragma unroll 1
+                    for (int c = 0; c < NCH; c++) dst[(size_t)c * cnt] = S(st, c);
+                }
+            }
+            // checks (HAC 4.24): even steps leave the Montgomery domain and compare, odd steps square
+            bool need = true, pass = false;
+            u32 jj = 0;
+#pragma unroll 1
+            for (u32 v = 0;; v++) {
+                const bool check = (v % 2) == 0;
+                if (check) {
+#pragma unroll 1
+                    for (int c = 0; c < NCH; c++) stash[(size_t)c * cnt] = S(st, c);
+                }
+                mm(st, s_one, check ? 1u : 0u, !check, cs);
+                if (check) {
+                    from_rns(st, cs, P.mpl);
+                    const bool one = x_is_one_t(st), nm1 = x_is_nm1_t(st, nrow, L);
+                    if (need) {
+                        if (nm1) { pass = true; need = false; }
+                        else if (one) { pass = (jj == 0); need = false; }
+                        else if (jj + 1 >= s) need = false;
+                    }
+                    jj++;
+#pragma unroll 1
+                    for (int c = 0; c < NCH; c++) S(st, c) = stash[(size_t)c * cnt];
+                    if (!tile_any(mm.t, need)) break;
+                }
+            }
+            if (pending && !pass) {
+                if (verdict == MR_PROBABLY_PRIME_V) { verdict = MR_COMPOSITE_V; witness = (int)r; }
+                if (!P.forced) pending = false;
+            }
+        }
+        if (was_live) {
+            P.verdict[i] = (uint8_t)verdict;
+            if (P.witness) P.witness[i] = (int16_t)witness;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_MR_TMEM));
+}
+constexpr size_t TC_MR_SMEM = tc_mr_smem_for(TCM);
+static_assert(TC_MR_SMEM <= 232448, "Miller-Rabin tensor tiles do not fit shared memory");
+#endif
+
 // ------------------------------------------------------------------ host-side launchers
 
 template <class Prm>
@@ -1132,6 +1377,9 @@ int upload_base(const u32 *flat, int device) {
 #if MR_K * 4 <= 256
     if (cudaFuncSetAttribute((const void *)k_modexp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM) !=
         cudaSuccess)
+        return 6;
+    if (cudaFuncSetAttribute((const void *)k_mr_rounds_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TC_MR_SMEM) != cudaSuccess)
         return 6;
 #endif
     return 0;
@@ -1159,6 +1407,15 @@ int launch_mr(const MrParams &p, void *stream) {
     const u32 ctas = (p.count + T - 1) / T;
     int rc = launch(k_mr_setup, ctas, p, stream);
     if (rc) return rc;
+#if MR_K * 4 <= 256
+    if (p.tc_b1 && p.tc_gc) {
+        void *args[] = {const_cast<MrParams *>(&p)};
+        return cudaLaunchKernel((const void *)k_mr_rounds_tc, dim3(p.tc_gc), dim3(TCM * 128), args, TC_MR_SMEM,
+                                (cudaStream_t)stream) == cudaSuccess
+                   ? 0
+                   : 6;
+    }
+#endif
     return launch(k_mr_rounds, ctas, p, stream);
 }
 
