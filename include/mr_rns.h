@@ -128,6 +128,29 @@ int mr_miller_rabin_batch(const uint32_t *d_n, size_t limbs, size_t count, const
                           int k, uint8_t *d_verdict, int16_t *d_witness_round, int32_t *d_status, int device,
                           void *stream);
 
+/* ------------------------------------------------------------------------------------------
+ * mr_rsa_keygen_batch — RSA key generation on the GPU ("RSA key generation ... is completely
+ * performed on the GPU with only e ... and N being transferred back to the CPU host", §3.3;
+ * "small primes testing (up to the first 10,000 primes) combined with Miller-Rabin compositeness
+ * tests", §4.3; d, d_p, d_q by Arazi's inversion, §3.1).
+ * Key i (global index first_key + i) follows the recipe of DESIGN.md reading R19: attempt a draws
+ * start = odd_with_top_bits(bits/2, seed, TAG_KEY, (first_key + i) * 65536 + a) (synth/ SplitMix64
+ * stream); its prime is the first probable prime >= start that survives trial division by the odd
+ * primes among the first 10,000 and `rounds` Miller-Rabin rounds with bases 2, 3, 5, ... (the first
+ * `rounds` primes).  Primes with gcd(e, p - 1) != 1, and a second prime q with |p - q| <= 2^(bits/2-100),
+ * are skipped; p is the first accepted prime, q the second.
+ * bits: multiple of 64 in [256, 4096]; e: an odd prime < 2^32 (e.g. 65537); rounds in [1, 256].
+ * Outputs, DEVICE, little-endian 32-bit limbs: d_n, d_d [count][bits/32] (n = p q, d = e^-1 mod
+ * (p-1)(q-1)); d_p, d_q, d_dp, d_dq, d_qinv [count][bits/64] (d_p = d mod (p-1), d_q = d mod (q-1),
+ * q_inv = q^-1 mod p).  Synchronous: returns after the keys are in the output buffers (the host
+ * schedules the search from per-search flags it reads back; no key material leaves the device).
+ * Errors: MR_ERR_ARG (bad bits/e/rounds/count, NULL output), MR_ERR_RANGE (a key needed more than
+ * 65,536 prime searches), MR_ERR_CUDA, MR_ERR_NOMEM.
+ * ------------------------------------------------------------------------------------------ */
+int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t seed, uint64_t first_key, int rounds,
+                        uint32_t *d_n, uint32_t *d_p, uint32_t *d_q, uint32_t *d_d, uint32_t *d_dp, uint32_t *d_dq,
+                        uint32_t *d_qinv, int device, void *stream);
+
 /* Human-readable name of an MR_* code (static storage). */
 const char *mr_strerror(int code);
 

@@ -35,7 +35,7 @@ MR_COMPOSITE, MR_PROBABLY_PRIME, MR_FACTOR = 0, 1, 2
 EXPORTS = (
     "mr_rns_ctx_create", "mr_rns_ctx_destroy", "mr_rns_ctx_info", "mr_rns_supported_k", "mr_modexp_batch",
     "mr_rsa_encrypt_batch", "mr_rsa_priv_create", "mr_rsa_priv_destroy", "mr_rsa_decrypt_batch",
-    "mr_miller_rabin_batch", "mr_strerror",
+    "mr_miller_rabin_batch", "mr_rsa_keygen_batch", "mr_strerror",
 )
 
 
@@ -70,6 +70,8 @@ def lib() -> ctypes.CDLL:
         L.mr_rsa_priv_destroy.restype = None
         L.mr_rsa_decrypt_batch.argtypes = [vp, vp, vp, sz, vp, vp]
         L.mr_miller_rabin_batch.argtypes = [vp, sz, sz, vp, i32, i32, vp, vp, vp, i32, vp]
+        L.mr_rsa_keygen_batch.argtypes = [sz, i32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, i32] + \
+            [vp] * 7 + [i32, vp]
         L.mr_strerror.argtypes = [i32]
         L.mr_strerror.restype = ctypes.c_char_p
         for name in EXPORTS:
@@ -202,6 +204,15 @@ def mr_miller_rabin_batch(d_n, limbs: int, count: int, d_bases, rounds: int, d_v
     _check(lib().mr_miller_rabin_batch(_dptr(d_n), limbs, count, _dptr(d_bases), rounds, k, _dptr(d_verdict),
                                        _dptr(d_witness), _dptr(d_status), device, _stream(d_n, stream)),
            "mr_miller_rabin_batch")
+
+
+def mr_rsa_keygen_batch(count: int, bits: int, e: int, seed: int, rounds: int, d_n, d_p, d_q, d_d, d_dp, d_dq, d_qinv,
+                        first_key: int = 0, device: int = 0, stream=None) -> None:
+    """RSA key generation on the GPU (include/mr_rns.h).  Outputs are device uint32/int32 tensors of
+    [count][bits/32] (n, d) and [count][bits/64] (p, q, dp, dq, qinv) limbs."""
+    _check(lib().mr_rsa_keygen_batch(count, bits, e, seed, first_key, rounds, _dptr(d_n), _dptr(d_p), _dptr(d_q),
+                                     _dptr(d_d), _dptr(d_dp), _dptr(d_dq), _dptr(d_qinv), device,
+                                     _stream(d_n, stream)), "mr_rsa_keygen_batch")
 
 
 # ------------------------------------------------------------------ RAII conveniences

@@ -57,12 +57,19 @@ def build(force: bool = False, jobs: int | None = None) -> str:
         objs.append(obj)
         if force or _stale(obj, [src] + deps):
             steps.append(([NVCC] + NVFLAGS + ["-c", src, "-o", obj], obj + ".log"))
-    host_src = os.path.join(CSRC, "mr_host.cpp")
-    host_obj = os.path.join(OBJ, "mr_host.o")
-    objs.append(host_obj)
-    if force or _stale(host_obj, [host_src] + deps):
-        steps.append((["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-fvisibility=hidden",
-                       "-I", os.path.join(CUDA, "include"), "-c", host_src, "-o", host_obj], host_obj + ".log"))
+    for cu in ("mr_keygen",):
+        src = os.path.join(CSRC, cu + ".cu")
+        obj = os.path.join(OBJ, cu + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + deps):
+            steps.append(([NVCC] + NVFLAGS + ["-c", src, "-o", obj], obj + ".log"))
+    for cpp in ("mr_host", "mr_keygen_host"):
+        host_src = os.path.join(CSRC, cpp + ".cpp")
+        host_obj = os.path.join(OBJ, cpp + ".o")
+        objs.append(host_obj)
+        if force or _stale(host_obj, [host_src] + deps):
+            steps.append((["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-fvisibility=hidden",
+                           "-I", os.path.join(CUDA, "include"), "-c", host_src, "-o", host_obj], host_obj + ".log"))
     if steps:
         jobs = jobs or min(len(steps), os.cpu_count() or 4)
         with cf.ThreadPoolExecutor(jobs) as ex:

@@ -25,15 +25,18 @@ KEYS = [("rsa1024", 1024, 0x5EEDC001), ("rsa2048", 2048, 0x5EEDC002), ("rsa3072"
 E = 65537
 
 
-def gen_key(bits: int, seed: int) -> dict:
+def gen_key(bits: int, seed: int, key_index: int = 0, rounds: int = 64, e: int = E) -> dict:
+    """key `key_index` of the recipe: attempt a starts at stream index key_index * 65536 + a (reading
+    R19; the committed fixtures are key 0)."""
+    E = e
     half = bits // 2
     nl = half // 32
     primes = []
     idx = 0
     while len(primes) < 2:
-        start = synth.odd_with_top_bits(half, seed, synth.TAG_KEY, idx)
+        start = synth.odd_with_top_bits(half, seed, synth.TAG_KEY, key_index * 65536 + idx)
         idx += 1
-        p = oracle.next_prime(start, nl, rounds=64)
+        p = oracle.next_prime(start, nl, rounds=rounds)
         try:
             oracle.modinv(E, oracle.sub(p, 1))       # gcd(e, p - 1) = 1
         except ValueError:

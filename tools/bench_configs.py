@@ -162,6 +162,30 @@ def c5(torch, mr, orc, quick):
           "verdicts_equal_forced_vs_early_exit": same, "bit_exact_sample_vs_oracle": ok, "sample": s})
 
 
+def kg(torch, mr, quick):
+    """GPU RSA key generation: keys/s, e = 65537; rounds = 5 (FIPS 186-4 C.3 count
+    for 1024-bit primes is 4-5) and 64 (the fixture recipe).  Sample: 4 keys checked for n = p q and
+    e d = 1 mod phi on the host."""
+    for bits, cnt, rounds in ([(1024, 1024, 5), (2048, 256, 5)] if quick else
+                              [(1024, 4096, 5), (2048, 1024, 5), (2048, 1024, 64), (3072, 256, 5)]):
+        full, half = bits // 32, bits // 64
+        bufs = [torch.zeros((cnt, full if f in ("n", "d") else half), dtype=torch.int32, device="cuda")
+                for f in ("n", "p", "q", "d", "dp", "dq", "qinv")]
+        mr.mr_rsa_keygen_batch(8, bits, 65537, 1, rounds, *[b[:8] for b in bufs])     # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        mr.mr_rsa_keygen_batch(cnt, bits, 65537, 0x5EEDC0DE, rounds, *bufs)
+        torch.cuda.synchronize()
+        t = time.perf_counter() - t0
+        h = [b.cpu().numpy().view(np.uint32) for b in bufs]
+        ok = True
+        for i in range(4):
+            n, p, q, d = (int.from_bytes(h[j][i].tobytes(), "little") for j in (0, 1, 2, 3))
+            ok &= n == p * q and 65537 * d % ((p - 1) * (q - 1)) == 1
+        emit({"config": "KG", "bits": bits, "keys": cnt, "mr_rounds": rounds, "seconds": t, "keys_per_s": cnt / t,
+              "sample_valid": bool(ok), "timing": "host wall clock around the synchronous call"})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C3,C4,C5")
@@ -182,6 +206,8 @@ def main():
             c4(torch, mr, oracle, a.quick)
         elif c == "C5":
             c5(torch, mr, oracle, a.quick)
+        elif c == "KG":
+            kg(torch, mr, a.quick)
         print(f"# {c} done in {time.time() - t0:.1f} s", file=sys.stderr)
 
 
