@@ -881,47 +881,59 @@ __device__ __forceinline__ u32 inv_word(u32 x, u32 c) {
 // smem-row positional helpers for the setup kernel (row l of a value at v[l * T + tid])
 __device__ __forceinline__ u32 &R(u32 *v, u32 l) { return v[l * T + threadIdx.x]; }
 
-// v = 2 v + bit; if v >= n: v -= n   (v < n on entry; L + 1 rows)
-__device__ __forceinline__ void dbl_sub(u32 *v, u32 bit, const u32 *nrow, u32 L) {
-    u32 carry = bit;
-#pragma unroll 1
-    for (u32 l = 0; l <= L; l++) {
-        const u32 cur = R(v, l);
-        R(v, l) = (cur << 1) | carry;
-        carry = cur >> 31;
-    }
-#pragma unroll 1
-    for (int pass = 0; pass < 2; pass++) {
-        u32 br = 0;
-#pragma unroll 1
-        for (u32 l = 0; l <= L; l++) {
-            const u64 t = (u64)R(v, l) - (l < L ? nrow[l] : 0u) - br;
-            if (pass) R(v, l) = (u32)t;
-            br = (u32)(t >> 63);
-        }
-        if (br) break;
-    }
+// remainder of the positional value u (smem rows [0, ulen)) modulo n (global limbs, Ln significant,
+// top limb nonzero), Knuth Algorithm D with the divisor normalised on the fly (TAOCP 4.3.1): the
+// remainder is left in rows [0, Ln); rows [0, ulen] are clobbered (ulen + 1 rows needed).
+__device__ __forceinline__ u32 vnorm(const u32 *n, u32 l, u32 sh) {
+    return sh ? (n[l] << sh) | (l ? n[l - 1] >> (32 - sh) : 0u) : n[l];
 }
-
-// v = v + w; if v >= n: v -= n   (v, w < n)
-__device__ __forceinline__ void add_sub(u32 *v, const u32 *w, const u32 *nrow, u32 L) {
-    u32 carry = 0;
+__device__ void rem_knuth(u32 *u, u32 ulen, const u32 *n, u32 Ln) {
+    const u32 sh = __clz(n[Ln - 1]);
+    if (sh) {                                        // normalise u into ulen + 1 rows
+        R(u, ulen) = R(u, ulen - 1) >> (32 - sh);
 #pragma unroll 1
-    for (u32 l = 0; l <= L; l++) {
-        const u64 t = (u64)R(v, l) + R(const_cast<u32 *>(w), l) + carry;
-        R(v, l) = (u32)t;
-        carry = (u32)(t >> 32);
+        for (int l = (int)ulen - 1; l > 0; l--) R(u, l) = (R(u, l) << sh) | (R(u, l - 1) >> (32 - sh));
+        R(u, 0) <<= sh;
+    } else {
+        R(u, ulen) = 0;
     }
+    if (ulen < Ln) return;
+    const u32 vt = vnorm(n, Ln - 1, sh), vs = Ln > 1 ? vnorm(n, Ln - 2, sh) : 0u;
 #pragma unroll 1
-    for (int pass = 0; pass < 2; pass++) {
-        u32 br = 0;
-#pragma unroll 1
-        for (u32 l = 0; l <= L; l++) {
-            const u64 t = (u64)R(v, l) - (l < L ? nrow[l] : 0u) - br;
-            if (pass) R(v, l) = (u32)t;
-            br = (u32)(t >> 63);
+    for (int j = (int)(ulen - Ln); j >= 0; j--) {
+        const u64 num = ((u64)R(u, j + Ln) << 32) | R(u, j + Ln - 1);
+        u64 qh = num / vt, rh = num - qh * vt;
+        while (qh >> 32 || (Ln > 1 && qh * vs > ((rh << 32) | R(u, j + Ln - 2)))) {
+            qh--;
+            rh += vt;
+            if (rh >> 32) break;
         }
-        if (br) break;
+        u64 carry = 0;
+        long long br = 0;
+#pragma unroll 1
+        for (u32 i = 0; i < Ln; i++) {
+            const u64 pr = qh * vnorm(n, i, sh) + carry;
+            carry = pr >> 32;
+            const long long t = (long long)R(u, i + j) - (long long)(u32)pr + br;
+            R(u, i + j) = (u32)t;
+            br = t >> 32;
+        }
+        const long long t = (long long)R(u, j + Ln) - (long long)carry + br;
+        R(u, j + Ln) = (u32)t;
+        if (t < 0) {                                 // add back (probability ~2/2^32)
+            u64 c = 0;
+#pragma unroll 1
+            for (u32 i = 0; i < Ln; i++) {
+                const u64 s2 = (u64)R(u, i + j) + vnorm(n, i, sh) + c;
+                R(u, i + j) = (u32)s2;
+                c = s2 >> 32;
+            }
+            R(u, j + Ln) += (u32)c;
+        }
+    }
+    if (sh) {                                        // unnormalise the remainder
+#pragma unroll 1
+        for (u32 l = 0; l < Ln; l++) R(u, l) = (R(u, l) >> sh) | (l + 1 < Ln ? R(u, l + 1) << (32 - sh) : 0u);
     }
 }
 
@@ -978,25 +990,34 @@ __global__ void __launch_bounds__(T) k_mr_setup(const MrParams P) {
             pc[(size_t)(pc_d(K) + l) * cs] = __funnelshift_r(l + ls == 0 ? (a0 & ~1u) : a0, a1, bs);
         }
         pc[(size_t)pc_s(K) * cs] = s;
-        // R^2 = M^2 mod n, positional in smem rows: rho = M mod n (bit-serial over M), then
-        // rho^2 mod n by double-and-add over the bits of rho (values < n < 2^(32L), L <= K - 1)
-        u32 *rho = st;                 // rows [0, L]
-        u32 *acc = st + (K + 1) * T;   // rows [K+1, K+1+L]
-#pragma unroll 1
-        for (u32 l = 0; l <= L; l++) R(rho, l) = 0;
-#pragma unroll 1
-        for (int b = 32 * (K + 1) - 1; b >= 0; b--) dbl_sub(rho, (GB(O_ML + b / 32) >> (b % 32)) & 1u, nrow, L);
-#pragma unroll 1
-        for (u32 l = 0; l <= L; l++) R(acc, l) = 0;
-#pragma unroll 1
-        for (int b = 32 * L - 1; b >= 0; b--) {
-            dbl_sub(acc, 0, nrow, L);
-            if ((R(rho, b / 32) >> (b % 32)) & 1u) add_sub(acc, rho, nrow, L);
-        }
-        // positional R^2 -> pc rows (scratch) -> RNS -> pc rows
+        // R^2 = M^2 mod n, positional: rho = M mod n and rho^2 mod n by Knuth D remainders in smem rows
+        // (rho parked in the pc R^2 rows, which are scratch until the RNS image is written)
+        u32 Ln = L;
+        while (Ln > 1 && nrow[Ln - 1] == 0) Ln--;
+        u32 *u = st;
         u32 *r2 = pc + (size_t)pc_r2(K) * cs;
 #pragma unroll 1
-        for (u32 l = 0; l < L; l++) r2[l * cs] = R(acc, l);
+        for (u32 l = 0; l <= (u32)K; l++) R(u, l) = GB(O_ML + l);
+        rem_knuth(u, K + 1, nrow, Ln);                      // rows [0, K + 2)
+#pragma unroll 1
+        for (u32 l = 0; l < Ln; l++) r2[l * cs] = R(u, l);
+#pragma unroll 1
+        for (u32 l = 0; l < 2 * Ln; l++) R(u, l) = 0;
+#pragma unroll 1
+        for (u32 a = 0; a < Ln; a++) {                     // rho^2, schoolbook
+            const u32 ra = r2[a * cs];
+            u64 c = 0;
+#pragma unroll 1
+            for (u32 b = 0; b < Ln; b++) {
+                const u64 t = (u64)ra * r2[b * cs] + R(u, a + b) + c;
+                R(u, a + b) = (u32)t;
+                c = t >> 32;
+            }
+            R(u, a + Ln) = (u32)c;
+        }
+        rem_knuth(u, 2 * Ln, nrow, Ln);                     // rows [0, 2 Ln + 1)
+#pragma unroll 1
+        for (u32 l = 0; l < L; l++) r2[l * cs] = l < Ln ? R(u, l) : 0u;
         to_rns(st, r2, (u32)cs, L, true, P.pow_tab);
 #pragma unroll 1
         for (int c = 0; c < NCH; c++) r2[c * cs] = S(st, c);

@@ -42,35 +42,79 @@ __global__ void k_kg_start(u64 seed, const u64 *index, u32 nslots, u32 L, u32 *s
     o[0] |= 1u;
 }
 
-// trial division of window w of search s (candidates start + 2 (W w + t), t < W) by the odd primes
-// among the first 10,000 (P:124): bit t of the bitmap is set when a small prime divides the candidate
-// (the candidates exceed 2^31 > 104,729, so "divides" means "composite").  One CTA per listed search.
-__global__ void k_kg_sieve(const u32 *starts, const u32 *window, const u32 *list, u32 L, const u32 *small, u32 nsmall,
-                           u32 W, u32 *bitmap) {
-    extern __shared__ u32 bm[];
-    const u32 s = list[blockIdx.x];
-    const u32 *st = starts + (size_t)s * L;
-    for (u32 w = threadIdx.x; w < W / 32; w += blockDim.x) bm[w] = 0;
-    __syncthreads();
-    const u64 base_off = 2ull * W * window[s];
-    for (u32 i = threadIdx.x; i < nsmall; i += blockDim.x) {
-        const u32 p = small[i];
-        u64 r = 0;
-        for (int l = (int)L - 1; l >= 0; l--) r = ((r << 32) | st[l]) % p;
-        r = (r + base_off % p) % p;
-        // (r + 2t) = 0 (mod p)  <=>  t = (p - r) (p + 1)/2 (mod p)
-        u64 t = ((p - r) % p) * ((p + 1) / 2) % p;
-        for (; t < W; t += p) atomicOr(&bm[t / 32], 1u << (t % 32));
+// powers for the sieve: pw[l][i] = 2^(32 l) mod p_i, mu[i] = floor((2^64 - 1) / p_i)
+__global__ void k_kg_pow(const u32 *small, u32 nsmall, u32 L, u32 *pw, u64 *mu) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nsmall) return;
+    const u32 p = small[i];
+    u64 v = 1 % p;
+    for (u32 l = 0; l < L; l++) {
+        pw[(size_t)l * nsmall + i] = (u32)v;
+        v = (v << 32) % p;
     }
-    __syncthreads();
-    for (u32 w = threadIdx.x; w < W / 32; w += blockDim.x) bitmap[(size_t)s * (W / 32) + w] = bm[w];
+    mu[i] = ~0ull / p;
 }
 
-// for every active search a = 0..nact-1 (search act[a]): the next G sieve survivors, in candidate
-// order, after the tested[s] already handed to Miller-Rabin, as rows cand[a G + g]; ncand[a] = how many
+__global__ void k_kg_zero(const u32 *list, u32 W, u32 *bitmap) {
+    const u32 s = list[blockIdx.x];
+    for (u32 w = threadIdx.x; w < W / 32; w += blockDim.x) bitmap[(size_t)s * (W / 32) + w] = 0;
+}
+
+// trial division of window w of search s (candidates start + 2 (W w + t), t < W) by the odd primes
+// among the first 10,000 (P:124): bit t of the bitmap is set when a small prime divides the candidate
+// (the candidates exceed 2^31 > 104,729, so "divides" means "composite").
+// CTA (x, y): KG_SB listed searches x KG_SB.. x 256 primes y*256..; thread = one prime.  The residue of
+// a start is the contraction sum_l limb_l * (2^(32 l) mod p) (< 2^56 for L <= 64), reduced once by
+// Barrett with mu = floor(2^64/p); the marks t = (p - r)(p + 1)/2 + j p < W go to the global bitmap.
+constexpr u32 KG_SB = 16;
+__global__ void __launch_bounds__(256) k_kg_sieve(const u32 *starts, const u32 *window, const u32 *list, u32 nlist,
+                                                  u32 L, const u32 *small, const u32 *pw, const u64 *mu, u32 nsmall,
+                                                  u32 W, u32 *bitmap) {
+    __shared__ u32 limbs[KG_SB][KG_MAXL];
+    __shared__ u64 off[KG_SB];
+    const u32 s0 = blockIdx.x * KG_SB;
+    const u32 ns = min(KG_SB, nlist - s0);
+    for (u32 x = threadIdx.x; x < KG_SB * L; x += blockDim.x) {
+        const u32 j = x / L, l = x % L;
+        limbs[j][l] = j < ns ? starts[(size_t)list[s0 + j] * L + l] : 0u;
+    }
+    if (threadIdx.x < KG_SB) off[threadIdx.x] = threadIdx.x < ns ? 2ull * W * window[list[s0 + threadIdx.x]] : 0ull;
+    __syncthreads();
+    const u32 i = blockIdx.y * blockDim.x + threadIdx.x;
+    if (i >= nsmall) return;
+    const u32 p = small[i];
+    const u64 m = mu[i];
+    u64 acc[KG_SB];
+#pragma unroll
+    for (u32 j = 0; j < KG_SB; j++) acc[j] = off[j];
+    for (u32 l = 0; l < L; l++) {
+        const u32 w = pw[(size_t)l * nsmall + i];
+#pragma unroll
+        for (u32 j = 0; j < KG_SB; j++) acc[j] += (u64)w * limbs[j][l];
+    }
+    const u32 half = (p + 1) / 2;
+#pragma unroll
+    for (u32 j = 0; j < KG_SB; j++) {
+        if (j >= ns) break;
+        const u64 x = acc[j];
+        u64 r = x - __umul64hi(x, m) * p;
+        while (r >= p) r -= p;
+        // (r + 2t) = 0 (mod p)  <=>  t = (p - r) (p + 1)/2 (mod p)
+        const u64 y = (u64)(r ? p - (u32)r : 0u) * half;
+        u64 t = y - __umul64hi(y, m) * p;
+        while (t >= p) t -= p;
+        u32 *bm = bitmap + (size_t)list[s0 + j] * (W / 32);
+        for (; t < W; t += p) atomicOr(&bm[t / 32], 1u << (t % 32));
+    }
+}
+
+// Miller-Rabin items are (candidate, base) pairs run as one-round tests in a single batch (reading
+// R19: the verdict of a candidate is the AND over its rounds, so rounds may run as separate items).
+// Phase-A items: for every listed search a (search act[a]) the next G sieve survivors in candidate
+// order, after the tested[s] already consumed, as rows cand[a G + g] with base 2; ncand[a] = how many
 // (< G: the window is exhausted after them).  Unused rows repeat the start (odd, never chosen).
 __global__ void k_kg_pick(const u32 *starts, const u32 *window, const u32 *bitmap, const u32 *tested, const u32 *act,
-                          u32 nact, u32 L, u32 W, u32 G, u32 *cand, u32 *ncand) {
+                          u32 nact, u32 L, u32 W, u32 G, u32 *cand, u32 *base, u32 *ncand) {
     const u32 a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= nact) return;
     const u32 s = act[a];
@@ -99,25 +143,25 @@ __global__ void k_kg_pick(const u32 *starts, const u32 *window, const u32 *bitma
         u32 *c = cand + ((size_t)a * G + g) * L;
         for (u32 l = 0; l < L; l++) c[l] = st[l];
     }
+    for (u32 g = 0; g < G; g++) {
+        u32 *bs = base + ((size_t)a * G + g) * L;
+        for (u32 l = 0; l < L; l++) bs[l] = l ? 0u : 2u;
+    }
 }
 
-// Miller-Rabin bases: the first `rounds` primes 2, 3, 5, ... for every candidate, as in the fixture
-// recipe's prime search (reading R19): bases[c][r] = small_all[r]
-__global__ void k_kg_bases(const u32 *small_all, u32 rounds, u32 L, u32 ncand, u32 *bases) {
-    const u32 c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncand) return;
-    for (u32 r = 0; r < rounds; r++)
-        for (u32 l = 0; l < L; l++) bases[((size_t)c * rounds + r) * L + l] = l ? 0u : small_all[r];
-}
-
-// first candidate of each active search that passed the base-2 round: first[a] = g, or -1
-__global__ void k_kg_first(const uint8_t *verdict, const u32 *ncand, u32 nact, u32 G, int *first) {
-    const u32 a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= nact) return;
-    int f = -1;
-    for (u32 g = 0; g < ncand[a]; g++)
-        if (verdict[(size_t)a * G + g] == 1u) { f = (int)g; break; }   // MR_PROBABLY_PRIME
-    first[a] = f;
+// Verification items: rounds 2..R of the search's pending candidate vcand[s] (bases 3, 5, 7, ... = the
+// 2nd..R-th primes), rows (v (R-1) + r) of cand/base for listed search v (search vl[v]).
+__global__ void k_kg_vitems(const u32 *vl, u32 nv, const u32 *vcand, const u32 *small_all, u32 R, u32 L, u32 *cand,
+                            u32 *base) {
+    const u32 item = blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= nv * (R - 1)) return;
+    const u32 v = item / (R - 1), r = item % (R - 1);
+    const u32 *src = vcand + (size_t)vl[v] * L;
+    u32 *c = cand + (size_t)item * L, *bs = base + (size_t)item * L;
+    for (u32 l = 0; l < L; l++) {
+        c[l] = src[l];
+        bs[l] = l ? 0u : small_all[r + 1];
+    }
 }
 
 // dst[dst_row[i]] = src[src_row[i]] (rows of L words)
@@ -328,27 +372,30 @@ int kg_launch_start(u64 seed, const u64 *index, u32 nslots, u32 L, u32 *starts, 
     k_kg_start<<<(nslots + 127) / 128, 128, 0, (cudaStream_t)st>>>(seed, index, nslots, L, starts);
     return kg_err();
 }
+int kg_launch_pow(const u32 *small, u32 nsmall, u32 L, u32 *pw, u64 *mu, void *st) {
+    k_kg_pow<<<(nsmall + 127) / 128, 128, 0, (cudaStream_t)st>>>(small, nsmall, L, pw, mu);
+    return kg_err();
+}
 int kg_launch_sieve(const u32 *starts, const u32 *window, const u32 *list, u32 nlist, u32 L, const u32 *small,
-                    u32 nsmall, u32 W, u32 *bitmap, void *st) {
+                    const u32 *pw, const u64 *mu, u32 nsmall, u32 W, u32 *bitmap, void *st) {
     if (!nlist) return 0;
-    k_kg_sieve<<<nlist, 256, W / 8, (cudaStream_t)st>>>(starts, window, list, L, small, nsmall, W, bitmap);
+    k_kg_zero<<<nlist, 128, 0, (cudaStream_t)st>>>(list, W, bitmap);
+    dim3 grid((nlist + KG_SB - 1) / KG_SB, (nsmall + 255) / 256);
+    k_kg_sieve<<<grid, 256, 0, (cudaStream_t)st>>>(starts, window, list, nlist, L, small, pw, mu, nsmall, W, bitmap);
     return kg_err();
 }
 int kg_launch_pick(const u32 *starts, const u32 *window, const u32 *bitmap, const u32 *tested, const u32 *act, u32 nact,
-                   u32 L, u32 W, u32 G, u32 *cand, u32 *ncand, void *st) {
+                   u32 L, u32 W, u32 G, u32 *cand, u32 *base, u32 *ncand, void *st) {
     if (!nact) return 0;
     k_kg_pick<<<(nact + 63) / 64, 64, 0, (cudaStream_t)st>>>(starts, window, bitmap, tested, act, nact, L, W, G, cand,
-                                                             ncand);
+                                                             base, ncand);
     return kg_err();
 }
-int kg_launch_bases(const u32 *small_all, u32 rounds, u32 L, u32 ncand, u32 *bases, void *st) {
-    if (!ncand) return 0;
-    k_kg_bases<<<(ncand + 127) / 128, 128, 0, (cudaStream_t)st>>>(small_all, rounds, L, ncand, bases);
-    return kg_err();
-}
-int kg_launch_first(const uint8_t *verdict, const u32 *ncand, u32 nact, u32 G, int *first, void *st) {
-    if (!nact) return 0;
-    k_kg_first<<<(nact + 127) / 128, 128, 0, (cudaStream_t)st>>>(verdict, ncand, nact, G, first);
+int kg_launch_vitems(const u32 *vl, u32 nv, const u32 *vcand, const u32 *small_all, u32 R, u32 L, u32 *cand, u32 *base,
+                     void *st) {
+    if (!nv || R < 2) return 0;
+    const u32 n = nv * (R - 1);
+    k_kg_vitems<<<(n + 127) / 128, 128, 0, (cudaStream_t)st>>>(vl, nv, vcand, small_all, R, L, cand, base);
     return kg_err();
 }
 int kg_launch_copy_rows(const u32 *src, const u32 *src_row, u32 *dst, const u32 *dst_row, u32 cnt, u32 L, void *st) {

@@ -29,12 +29,13 @@ extern "C" int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_
 
 namespace mr {
 int kg_launch_start(u64 seed, const u64 *index, u32 nslots, u32 L, u32 *starts, void *st);
+int kg_launch_pow(const u32 *small, u32 nsmall, u32 L, u32 *pw, u64 *mu, void *st);
 int kg_launch_sieve(const u32 *starts, const u32 *window, const u32 *list, u32 nlist, u32 L, const u32 *small,
-                    u32 nsmall, u32 W, u32 *bitmap, void *st);
+                    const u32 *pw, const u64 *mu, u32 nsmall, u32 W, u32 *bitmap, void *st);
 int kg_launch_pick(const u32 *starts, const u32 *window, const u32 *bitmap, const u32 *tested, const u32 *act, u32 nact,
-                   u32 L, u32 W, u32 G, u32 *cand, u32 *ncand, void *st);
-int kg_launch_bases(const u32 *small_all, u32 rounds, u32 L, u32 ncand, u32 *bases, void *st);
-int kg_launch_first(const uint8_t *verdict, const u32 *ncand, u32 nact, u32 G, int *first, void *st);
+                   u32 L, u32 W, u32 G, u32 *cand, u32 *base, u32 *ncand, void *st);
+int kg_launch_vitems(const u32 *vl, u32 nv, const u32 *vcand, const u32 *small_all, u32 R, u32 L, u32 *cand, u32 *base,
+                     void *st);
 int kg_launch_copy_rows(const u32 *src, const u32 *src_row, u32 *dst, const u32 *dst_row, u32 cnt, u32 L, void *st);
 int kg_launch_check(const u32 *pool, u32 n, u32 e, const u32 *which, const u32 *first, u32 cnt, u32 *ok, void *st);
 int kg_launch_assemble(const u32 *prime, const u32 *key_slot, u32 nkeys, u32 n, u32 e, u32 *N, u32 *P, u32 *Q, u32 *D,
@@ -44,7 +45,9 @@ namespace {
 
 constexpr u32 kNumSmall = 10000;       // "up to the first 10,000 primes"
 constexpr u32 kWindow = 4096;          // odd candidates per sieve window
-constexpr u32 kTarget = 2 * 148 * 128; // candidates per round-1 Miller-Rabin batch (two waves of tiles)
+constexpr u32 kTarget = 4 * 148 * 128; // phase-A items per Miller-Rabin batch (4 tiles per SM)
+constexpr u32 kMaxG = 256;             // survivors per search per batch: a small tail batch costs one
+                                       // round of latency whatever its size, so it takes more survivors
 
 const std::vector<u32> &small_primes() {
     static std::vector<u32> sp = [] {
@@ -115,64 +118,82 @@ int down(std::vector<T> &h, const T *d, size_t n, cudaStream_t st) {
     if (!var) return MR_ERR_NOMEM
 
 // Runs searches (one per entry of `index`) to completion; prime of search s -> pool row row0 + s.
+// Every iteration is ONE Miller-Rabin launch of one-round items: phase-A items (the next G sieve
+// survivors of each search in phase A, base 2) and verification items (rounds 2..R of the candidate
+// each search in phase V found in the previous iteration).
 int run_searches(Dev &dev, cudaStream_t st, const std::vector<u64> &index, u32 L, int rounds, u64 seed,
-                 const u32 *d_small, u32 *pool, u32 row0, int device) {
+                 const u32 *d_small, const u32 *d_pw, const u64 *d_mu, u32 *pool, u32 row0, int device) {
     const u32 S = (u32)index.size();
-    const u32 W = kWindow;
+    const u32 W = kWindow, R = (u32)rounds;
     KG_NEW(d_index, u64, S);
     KG_NEW(d_starts, u32, (size_t)S * L);
     KG_NEW(d_window, u32, S);
     KG_NEW(d_tested, u32, S);
     KG_NEW(d_bitmap, u32, (size_t)S * (W / 32));
     KG_NEW(d_list, u32, S);
+    KG_NEW(d_vlist, u32, S);
     KG_NEW(d_ncand, u32, S);
-    KG_NEW(d_first, int, S);
-    const size_t capA = std::max<size_t>((size_t)S * 8, (size_t)kTarget + S);   // >= nact G
-    KG_NEW(d_cand, u32, capA * L);
-    KG_NEW(d_basesA, u32, capA * L);
-    KG_NEW(d_verdA, uint8_t, capA);
-    KG_NEW(d_cand2, u32, (size_t)S * L);
-    KG_NEW(d_basesB, u32, (size_t)S * rounds * L);
-    KG_NEW(d_verdB, uint8_t, S);
+    KG_NEW(d_vcand, u32, (size_t)S * L);
+    // items: phase A <= max(8 S, kTarget + S); verification <= S (R - 1)
+    const size_t capA = std::max<size_t>((size_t)S * 8, (size_t)kTarget + S);
+    const size_t cap = capA + (size_t)S * (R - 1);
+    KG_NEW(d_cand, u32, cap * L);
+    KG_NEW(d_base, u32, cap * L);
+    KG_NEW(d_verd, uint8_t, cap);
     KG_NEW(d_rows, u32, 2 * (size_t)S);
     KG_TRY(up(d_index, index, st));
     KG_TRY(kg_launch_start(seed, d_index, S, L, d_starts, st));
-    KG_TRY(kg_launch_bases(d_small, 1, L, (u32)capA, d_basesA, st));
-    KG_TRY(kg_launch_bases(d_small, (u32)rounds, L, S, d_basesB, st));
 
-    std::vector<u32> window(S, 0), tested(S, 0), act, resieve(S), ncand;
-    std::vector<int> first;
+    std::vector<u32> window(S, 0), tested(S, 0), pend_first(S, 0), resieve(S), ncand;
     std::vector<uint8_t> verd;
-    std::vector<char> found(S, 0);
-    for (u32 s = 0; s < S; s++) resieve[s] = s;
-    for (u32 s = 0; s < S; s++) act.push_back(s);
+    std::vector<char> found(S, 0), verify(S, 0);
+    std::vector<u32> act(S);
+    for (u32 s = 0; s < S; s++) resieve[s] = act[s] = s;
     int guard = 0;
     while (!act.empty()) {
         if (++guard > 1000000) return MR_ERR_CUDA;
+        std::vector<u32> A, V;
+        for (u32 s : act) (verify[s] ? V : A).push_back(s);
         KG_TRY(up(d_window, window, st));
         KG_TRY(up(d_tested, tested, st));
         if (!resieve.empty()) {
             KG_TRY(up(d_list, resieve, st));
-            KG_TRY(kg_launch_sieve(d_starts, d_window, d_list, (u32)resieve.size(), L, d_small + 1, kNumSmall - 1, W,
-                                   d_bitmap, st));
+            KG_TRY(kg_launch_sieve(d_starts, d_window, d_list, (u32)resieve.size(), L, d_small + 1, d_pw, d_mu,
+                                   kNumSmall - 1, W, d_bitmap, st));
             resieve.clear();
         }
-        const u32 nact = (u32)act.size();
-        const u32 G = std::min<u32>(64, std::max<u32>(8, (kTarget + nact - 1) / nact));
-        KG_TRY(up(d_list, act, st));
-        KG_TRY(kg_launch_pick(d_starts, d_window, d_bitmap, d_tested, d_list, nact, L, W, G, d_cand, d_ncand, st));
-        int rc = mr_internal_miller_rabin(d_cand, L, (size_t)nact * G, d_basesA, 1, 0, d_verdA, nullptr, nullptr,
-                                          device, st, 0, 4);
-        if (rc != MR_OK) return rc;
-        KG_TRY(kg_launch_first(d_verdA, d_ncand, nact, G, d_first, st));
-        KG_TRY(down(first, d_first, nact, st));
-        KG_TRY(down(ncand, d_ncand, nact, st));
-        std::vector<u32> brow, bact;                 // verification batch: candidate rows, active index
-        for (u32 a = 0; a < nact; a++) {
-            const u32 s = act[a];
-            if (first[a] >= 0) {
-                brow.push_back(a * G + (u32)first[a]);
-                bact.push_back(a);
+        const u32 nA = (u32)A.size(), nV = (u32)V.size();
+        const u32 G = nA ? std::min<u32>(kMaxG, std::max<u32>(8, (kTarget + nA - 1) / nA)) : 0;
+        const size_t itemsA = (size_t)nA * G, items = itemsA + (size_t)nV * (R - 1);
+        KG_TRY(up(d_list, A, st));
+        KG_TRY(up(d_vlist, V, st));
+        KG_TRY(kg_launch_pick(d_starts, d_window, d_bitmap, d_tested, d_list, nA, L, W, G, d_cand, d_base, d_ncand,
+                              st));
+        KG_TRY(kg_launch_vitems(d_vlist, nV, d_vcand, d_small, R, L, d_cand + itemsA * L, d_base + itemsA * L, st));
+        if (items) {
+            int rc = mr_internal_miller_rabin(d_cand, L, items, d_base, 1, 0, d_verd, nullptr, nullptr, device, st, 0,
+                                              4);
+            if (rc != MR_OK) return rc;
+        }
+        KG_TRY(down(ncand, d_ncand, nA, st));
+        KG_TRY(down(verd, d_verd, items, st));
+        std::vector<u32> to_v_src, to_v_dst, to_p_src, to_p_dst, vc_src, vc_dst;
+        for (u32 a = 0; a < nA; a++) {
+            const u32 s = A[a];
+            int f = -1;
+            for (u32 g = 0; g < ncand[a]; g++)
+                if (verd[(size_t)a * G + g] == MR_PROBABLY_PRIME) { f = (int)g; break; }
+            if (f >= 0) {
+                if (R == 1) {                        // one round: the first passer is the prime
+                    found[s] = 1;
+                    to_p_src.push_back(a * G + (u32)f);
+                    to_p_dst.push_back(row0 + s);
+                } else {
+                    verify[s] = 1;
+                    pend_first[s] = (u32)f;
+                    to_v_src.push_back(a * G + (u32)f);
+                    to_v_dst.push_back(s);
+                }
             } else {
                 tested[s] += ncand[a];
                 if (ncand[a] < G) {                  // window exhausted: next window
@@ -182,34 +203,29 @@ int run_searches(Dev &dev, cudaStream_t st, const std::vector<u64> &index, u32 L
                 }
             }
         }
-        if (!brow.empty()) {
-            const u32 nb = (u32)brow.size();
-            std::vector<u32> seq(nb);
-            for (u32 b = 0; b < nb; b++) seq[b] = b;
-            KG_TRY(up(d_rows, brow, st));
-            KG_TRY(up(d_rows + S, seq, st));
-            KG_TRY(kg_launch_copy_rows(d_cand, d_rows, d_cand2, d_rows + S, nb, L, st));
-            rc = mr_internal_miller_rabin(d_cand2, L, nb, d_basesB, rounds, 0, d_verdB, nullptr, nullptr, device, st,
-                                          0, 4);
-            if (rc != MR_OK) return rc;
-            KG_TRY(down(verd, d_verdB, nb, st));
-            std::vector<u32> src, dst;
-            for (u32 b = 0; b < nb; b++) {
-                const u32 a = bact[b], s = act[a];
-                if (verd[b] == MR_PROBABLY_PRIME) {
-                    found[s] = 1;
-                    src.push_back(b);
-                    dst.push_back(row0 + s);
-                } else {
-                    tested[s] += (u32)first[a] + 1;
-                }
-            }
-            if (!src.empty()) {
-                KG_TRY(up(d_rows, src, st));
-                KG_TRY(up(d_rows + S, dst, st));
-                KG_TRY(kg_launch_copy_rows(d_cand2, d_rows, pool, d_rows + S, (u32)src.size(), L, st));
+        for (u32 v = 0; v < nV; v++) {
+            const u32 s = V[v];
+            bool ok = true;
+            for (u32 r = 0; r + 1 < R; r++) ok &= verd[itemsA + (size_t)v * (R - 1) + r] == MR_PROBABLY_PRIME;
+            verify[s] = 0;
+            if (ok) {
+                found[s] = 1;
+                vc_src.push_back(s);
+                vc_dst.push_back(row0 + s);
+            } else {
+                tested[s] += pend_first[s] + 1;      // resume after the failed candidate
             }
         }
+        auto copy = [&](const u32 *src, std::vector<u32> &sr, u32 *dst, std::vector<u32> &dr) {
+            if (sr.empty()) return 0;
+            if (up(d_rows, sr, st) || up(d_rows + S, dr, st)) return 1;
+            return kg_launch_copy_rows(src, d_rows, dst, d_rows + S, (u32)sr.size(), L, st);
+        };
+        // d_rows is reused by the three copies: the uploads and kernels are ordered on one stream, and
+        // pageable uploads are staged before cudaMemcpyAsync returns, so the host vectors may go away
+        KG_TRY(copy(d_cand, to_p_src, pool, to_p_dst));
+        KG_TRY(copy(d_cand, to_v_src, d_vcand, to_v_dst));
+        KG_TRY(copy(d_vcand, vc_src, pool, vc_dst));
         std::vector<u32> next;
         for (u32 s : act)
             if (!found[s]) next.push_back(s);
@@ -240,6 +256,9 @@ extern "C" int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t 
     const std::vector<u32> &sp = small_primes();
     KG_NEW(d_small, u32, kNumSmall);
     KG_TRY(up(d_small, sp, st));
+    KG_NEW(d_pw, u32, (size_t)L * (kNumSmall - 1));
+    KG_NEW(d_mu, u64, kNumSmall - 1);
+    KG_TRY(kg_launch_pow(d_small + 1, kNumSmall - 1, L, d_pw, d_mu, st));      // odd primes
 
     // prime pool: every prime found, in search order; grows as keys need more attempts
     u32 cap = (u32)(2 * count + 64), npool = 0;
@@ -278,7 +297,7 @@ extern "C" int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t 
         }
         {
             Dev scratch(st);
-            int rc = run_searches(scratch, st, index, L, rounds, seed, d_small, pool, npool, device);
+            int rc = run_searches(scratch, st, index, L, rounds, seed, d_small, d_pw, d_mu, pool, npool, device);
             if (rc != MR_OK) return rc;
         }
         for (u32 s = 0; s < S; s++) pend[owner[s]].push_back(Row{npool + s, 0xFFFFFFFEu, 0});

@@ -167,7 +167,8 @@ def kg(torch, mr, quick):
     for 1024-bit primes is 4-5) and 64 (the fixture recipe).  Sample: 4 keys checked for n = p q and
     e d = 1 mod phi on the host."""
     for bits, cnt, rounds in ([(1024, 1024, 5), (2048, 256, 5)] if quick else
-                              [(1024, 4096, 5), (2048, 1024, 5), (2048, 1024, 64), (3072, 256, 5)]):
+                              [(1024, 4096, 5), (1024, 16384, 5), (2048, 1024, 5), (2048, 4096, 5), (2048, 4096, 64),
+                               (3072, 1024, 5)]):
         full, half = bits // 32, bits // 64
         bufs = [torch.zeros((cnt, full if f in ("n", "d") else half), dtype=torch.int32, device="cuda")
                 for f in ("n", "p", "q", "d", "dp", "dq", "qinv")]
