@@ -14,9 +14,10 @@
  *  - Big integers are little-endian arrays of uint32_t limbs, fixed width per call (R16).
  *  - Batch buffers (d_*) are DEVICE pointers owned by the caller (e.g. torch tensors), row-major
  *    [count][limbs], 4-byte aligned (16-byte alignment is faster).  Host pointers are marked HOST.
- *  - Every batch call is asynchronous on `stream` (a cudaStream_t passed as void*; NULL = legacy
- *    default stream) and returns after enqueuing.  The return code reports host-detectable problems
- *    only (arguments, capacity, launch failure) and never synchronises the device.
+ *  - Every batch call except mr_rsa_keygen_batch is asynchronous on `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream) and returns after enqueuing.  The return code reports
+ *    host-detectable problems only (arguments, capacity, launch failure) and never synchronises the
+ *    device.  mr_rsa_keygen_batch is synchronous (its search schedule depends on device results).
  *  - Per-message data errors go to d_status[i] (nullable): MR_OK, or MR_ERR_RANGE when the input is
  *    >= its bound, in which case that output is zero-filled.
  *  - count = 0 is MR_OK and launches nothing.

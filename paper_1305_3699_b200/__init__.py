@@ -26,7 +26,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmr_rns.so")
+LIB_PATH = os.environ.get("MR_RNS_LIB") or os.path.join(HERE, "libmr_rns.so")   # override: A/B builds
 
 MR_OK, MR_ERR_ARG, MR_ERR_EVEN_MODULUS, MR_ERR_NOT_COPRIME = 0, 1, 2, 3
 MR_ERR_CAPACITY, MR_ERR_RANGE, MR_ERR_CUDA, MR_ERR_NOMEM = 4, 5, 6, 7

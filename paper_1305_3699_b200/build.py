@@ -22,7 +22,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 KS = [1, 2, 3, 5, 9, 17, 33, 49, 65, 97, 129]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                  "-I", os.path.join(ROOT, "include")]
+                  "-I", os.path.join(ROOT, "include")] + os.environ.get("MR_NVCC_DEFS", "").split()
 
 
 def _deps() -> list[str]:

@@ -922,6 +922,7 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
     if (count > 0x7FFFFFFFu) return MR_ERR_ARG;
     int kk;
     const u32 *d_pow = nullptr, *d_be = nullptr;
+    DevBase db;
     {
         std::lock_guard<std::mutex> lk(g_mu);
         Big top = sub(pow2(32 * (int)limbs), Big{1});   // capacity for any n < 2^(32 limbs)
@@ -937,14 +938,32 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
         if ((int)limbs > kk - 1) return MR_ERR_CAPACITY;
         int rc = ensure_device_base(kk, device, &d_pow, &d_be);
         if (rc != MR_OK) return rc;
+        db = g_devbases[std::make_pair(device, kk)];
     }
     if (cudaSetDevice(device) != cudaSuccess) return MR_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t nch = 2 * (size_t)kk + 1;
-    u32 *d_pc = nullptr, *d_tab = nullptr;
+    const KernelSet &ks = kernel_set_for(kk);
+    const bool tc = db.d_tcb1u && ks.launch_modexp_tc && ks.mr_tiles > 0 && tensor_path_enabled();
+    u32 gc = 0;
+    if (tc) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        gc = std::min<u32>((u32)sms, (u32)((count + 127) / 128));
+    }
+    // early-exit compaction on the tensor path (round 0 for all, then (survivor, round) items)
+    const bool compact = tc && !forced && rounds > 1;
+    const size_t slots = compact ? (size_t)gc * ks.mr_tiles * 128 : 0;
+    const size_t tcols = std::max<size_t>(count, slots);
+    u32 *d_pc = nullptr, *d_tab = nullptr, *d_aux = nullptr;
     if (cudaMallocAsync(&d_pc, (size_t)pc_words(kk) * count * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
-    if (cudaMallocAsync(&d_tab, ((size_t)(1u << window) + 1) * nch * count * 4, st) != cudaSuccess) {
+    if (cudaMallocAsync(&d_tab, ((size_t)(1u << window) + 1) * nch * tcols * 4, st) != cudaSuccess) {
         cudaFreeAsync(d_pc, st);
+        return MR_ERR_NOMEM;
+    }
+    if (compact && cudaMallocAsync(&d_aux, (2 * count + 4) * 4, st) != cudaSuccess) {
+        cudaFreeAsync(d_pc, st);
+        cudaFreeAsync(d_tab, st);
         return MR_ERR_NOMEM;
     }
     MrParams P;
@@ -963,22 +982,22 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
     P.status = d_status;
     P.pow_tab = d_pow;
     P.be_tab = d_be;
-    P.mpl = g_devbases[std::make_pair(device, kk)].d_mpl;
-    {
-        const DevBase &db = g_devbases[std::make_pair(device, kk)];
-        const KernelSet &ks0 = kernel_set_for(kk);
-        if (db.d_tcb1u && ks0.launch_modexp_tc && tensor_path_enabled()) {
-            int sms = 148;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-            P.tc_b1 = db.d_tcb1u;
-            P.tc_b2 = db.d_tcb2;
-            P.tc_gc = std::min<u32>((u32)sms, (u32)((count + 127) / 128));
-        }
+    P.mpl = db.d_mpl;
+    if (tc) {
+        P.tc_b1 = db.d_tcb1u;
+        P.tc_b2 = db.d_tcb2;
+        P.tc_gc = gc;
     }
-    const KernelSet &ks = kernel_set_for(kk);
+    if (compact) {
+        P.live = d_aux;
+        P.wit32 = d_aux + count;
+        P.nlive = d_aux + 2 * count;
+        P.tstride = (u32)slots;
+    }
     int rc = timed_launch(2, st, [&] { return ks.launch_mr(P, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
     cudaFreeAsync(d_pc, st);
     cudaFreeAsync(d_tab, st);
+    if (d_aux) cudaFreeAsync(d_aux, st);
     return rc;
 }
 

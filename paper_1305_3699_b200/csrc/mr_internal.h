@@ -186,6 +186,15 @@ struct MrParams {               // Miller-Rabin (§3.2; HAC 4.24)
     const u32 *tc_b1;           // tensor path: unmerged BE1 image (per k); null = IMAD path
     const u32 *tc_b2;           // tensor path: BE2 image
     u32 tc_gc;                  // tensor path: persistent CTAs
+    // tensor path, early-exit compaction: mode 0 = every round in one tile-job (forced, or a
+    // single round); mode 1 = round 0 for every candidate, survivors appended to live[] (count *nlive);
+    // mode 2 = items (live candidate, round r >= 1) as independent one-round jobs, the first failing
+    // round min-reduced into wit32[]; k_mr_final folds wit32 into verdict/witness.
+    u32 mode;
+    u32 *live;                  // [count]
+    u32 *nlive;                 // device counter
+    u32 *wit32;                 // [count]
+    u32 tstride;                // window-table stride: count (modes 0, 1) or persistent slots (mode 2)
 };
 
 // per-candidate constant rows for Miller-Rabin (row r at pc + r * count)
@@ -210,6 +219,7 @@ struct KernelSet {
     int (*launch_modexp_tc)(const ModexpParams &p, u32 ctas, void *stream);   // null when unsupported
     int tc_tiles;                                         // 128-message tiles per CTA of the TC kernel
     int threads;                                          // CTA size used by launch_modexp
+    int mr_tiles;                                         // 128-candidate tiles per CTA of k_mr_rounds_tc
 };
 
 }  // namespace mr

@@ -3,5 +3,5 @@
 #include "mr_kernels.cuh"
 
 namespace mr {
-KernelSet kernels_k65() { return KernelSet{MR_K, upload_base, launch_modexp, launch_combine, launch_mr, launch_modexp_tc, TC_TILES, T}; }
+KernelSet kernels_k65() { return KernelSet{MR_K, upload_base, launch_modexp, launch_combine, launch_mr, launch_modexp_tc, TC_TILES, T, MR_TC_TILES}; }
 }  // namespace mr

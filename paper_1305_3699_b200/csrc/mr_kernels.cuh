@@ -54,6 +54,12 @@ __constant__ u32 g_base[BASE_WORDS];
 #define GB(off) g_base[(off)]
 
 // ------------------------------------------------------------------ word arithmetic
+#ifndef MR_ABL_NOMMA
+#define MR_ABL_NOMMA 0
+#endif
+#ifndef MR_RED_VARIANT
+#define MR_RED_VARIANT 1
+#endif
 
 // 96-bit multiply-accumulate (lo, mid, hi) += x * y; lowers to IMAD.WIDE.U32 with carry-out + IADD3.X
 __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) {
@@ -64,13 +70,29 @@ __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) 
         : "r"(x), "r"(y));
 }
 
-// h·2^32 + l  ->  congruent value in [0, 2^32) modulo m = 2^32 - c  (c < 2^13)
-__device__ __forceinline__ u32 red64(u32 h, u32 l, u32 c) {
-    const u64 u = (u64)h * c + l;                       // < 2^32 (c + 1): uh <= c
+// p = h·2^32 + l  ->  congruent value in [0, 2^32) modulo m = 2^32 - c  (c < 2^13).
+// h·2^32 + l ≡ h·c + l = uh·2^32 + ul (uh <= c) ≡ uh·c + ul = cy·2^32 + vl (cy <= 1) ≡ vl + cy·c, and when
+// cy = 1, vl < 2^26 so vl + c does not wrap.  Both products take the previous 64-bit value as their
+// addend pair, so each is one IMAD.WIDE with no register moves: u = h c + p has high word uh + h
+// (mod 2^32), v = uh c + u has high word cy + uh + h; the differences recover uh and cy.
+#if MR_RED_VARIANT == 1
+__device__ __forceinline__ u32 red64p(u64 p, u32 c) {
+    const u64 u = (u64)(u32)(p >> 32) * c + (u32)p;
     const u32 uh = (u32)(u >> 32), ul = (u32)u;
-    const u32 vl = uh * c + ul;                         // uh c < 2^26: wraps at most once
-    return vl < ul ? vl + c : vl;                       // wrapped: 2^32 ≡ c and vl < 2^26
+    const u32 vl = uh * c + ul;
+    return vl < ul ? vl + c : vl;
 }
+#else
+__device__ __forceinline__ u32 red64p(u64 p, u32 c) {
+    const u32 h = (u32)(p >> 32);
+    const u64 u = (u64)h * c + p;
+    const u32 uh = (u32)(u >> 32) - h;
+    const u64 v = (u64)uh * c + u;
+    const u32 cy = (u32)(v >> 32) - (u32)(u >> 32);
+    return (u32)v + cy * c;
+}
+#endif
+__device__ __forceinline__ u32 red64(u32 h, u32 l, u32 c) { return red64p(((u64)h << 32) | l, c); }
 
 // hi·2^64 + mid·2^32 + lo -> congruent value in [0, 2^32), hi < 2^7
 // hi·2^64 ≡ hi·c·2^32, so V ≡ W·2^32 + lo with W = mid + hi·c (may carry once: wc), then
@@ -85,10 +107,7 @@ __device__ __forceinline__ u32 red96(u32 hi, u32 mid, u32 lo, u32 c, u32 c2) {
     return vl < ul ? vl + c : vl;
 }
 
-__device__ __forceinline__ u32 mulmod(u32 a, u32 b, u32 c) {
-    const u64 p = (u64)a * b;
-    return red64((u32)(p >> 32), (u32)p, c);
-}
+__device__ __forceinline__ u32 mulmod(u32 a, u32 b, u32 c) { return red64p((u64)a * b, c); }
 
 __device__ __forceinline__ u32 canon(u32 x, u32 c) {  // lazy residue -> [0, m)
     const u32 m = 0u - c;
@@ -513,6 +532,9 @@ __device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // A tile written by the generic proxy
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     tile_sync(t);
+#if MR_ABL_NOMMA
+    return;
+#endif
     if (t.leader) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u32 sa = smem_u32(t.a), sb = smem_u32(bimg);
@@ -531,6 +553,9 @@ __device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
 
 // wait for the tile's MMA chain (bounded: a lost completion traps instead of hanging the GPU)
 __device__ __forceinline__ void tc_wait(TcTile &t) {
+#if MR_ABL_NOMMA
+    return;
+#endif
     u32 done = 0;
 #pragma unroll 1
     for (u32 spin = 0; !done; spin++) {
@@ -546,6 +571,14 @@ __device__ __forceinline__ void tc_wait(TcTile &t) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16_nowait(u32 taddr, u32 (&v)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(taddr)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(u32 taddr, u32 (&v)[16]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
@@ -638,10 +671,18 @@ struct MulTc {
         tc_wait(t);
         u32 sr = 0;
         u32 c2lo = 0, c2mi = 0, c2hi = 0;
-#pragma unroll 2
-        for (int g = 0; g < TCNT / 4 + (TCNT % 4 ? 1 : 0); g++) {
-            u32 v[16];
-            tmem_ld16(t.tmem + lane_base + 16 * g, v);
+        constexpr int NG = TCNT / 4 + (TCNT % 4 ? 1 : 0);
+#pragma unroll 1
+        for (int g0 = 0; g0 < NG; g0 += 2) {
+          u32 vv[2][16];                              // two TMEM loads in flight, one wait
+          tmem_ld16_nowait(t.tmem + lane_base + 16 * g0, vv[0]);
+          if (g0 + 1 < NG) tmem_ld16_nowait(t.tmem + lane_base + 16 * (g0 + 1), vv[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int g = g0 + h;
+            if (g >= NG) break;
+            const u32 (&v)[16] = vv[h];
             u32 w[4];
 #pragma unroll
             for (int o = 0; o < 4; o++) {
@@ -655,7 +696,7 @@ struct MulTc {
                     u32 xp;
                     if (MERGED) {
                         const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + q;   // <= (2^32-1) 2^32: no carry
-                        xp = red64((u32)(p >> 32), (u32)p, c);
+                        xp = red64p(p, c);
                     } else {   // ξ'_j = t*_j C1_j + q̂_j |n M^-1 λ_j|  (6.4 with a per-thread modulus)
                         const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
                         u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
@@ -669,6 +710,7 @@ struct MulTc {
                 }
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);   // BE2 operand
+          }
         }
         if (TCNC) {   // CUDA-core output of BE1 completes the BE2 operand and its own BE2 term
             const int j = TCNT;
@@ -689,10 +731,17 @@ struct MulTc {
             r_c = red96(c2hi, c2mi, c2lo, s_be[bev_c(K) + i], 0);
         }
         tc_wait(t);
-#pragma unroll 2
-        for (int g = 0; g < TCNT / 4 + (TCNT % 4 ? 1 : 0); g++) {
-            u32 v[16];
-            tmem_ld16(t.tmem + lane_base + 16 * g, v);
+#pragma unroll 1
+        for (int g0 = 0; g0 < NG; g0 += 2) {
+          u32 vv[2][16];
+          tmem_ld16_nowait(t.tmem + lane_base + 16 * g0, vv[0]);
+          if (g0 + 1 < NG) tmem_ld16_nowait(t.tmem + lane_base + 16 * (g0 + 1), vv[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int g = g0 + h;
+            if (g >= NG) break;
+            const u32 (&v)[16] = vv[h];
             u32 w[4];
 #pragma unroll
             for (int o = 0; o < 4; o++) {
@@ -706,6 +755,7 @@ struct MulTc {
                 }
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
         }
         if (TCNC) *reinterpret_cast<uint4 *>(arow + (TCNT / 4) * 128) = make_uint4(r_c, 0u, 0u, 0u);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1244,21 +1294,33 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
     u32 *c2rows = c2_all + tile * K * 128 + m;
     const size_t cnt = P.count;
-    const u32 L = P.limbs, w = P.window, E = 1u << w;
-    const size_t entry = (size_t)NCH * cnt;
+    const u32 L = P.limbs, w = P.window, E = 1u << w, R = P.rounds;
+    const size_t tst = P.mode == 2 ? P.tstride : cnt;              // window-table stride
+    const size_t entry = (size_t)NCH * tst;
     const u32 ndig = (32 * L + w - 1) / w;
-    const u32 jobs = (P.count + 127) / 128, G = gridDim.x;
+    const u32 items = P.mode == 2 ? *P.nlive * (R - 1) : 0u;
+    const u32 jobs = P.mode == 2 ? (items + 127) / 128 : (P.count + 127) / 128, G = gridDim.x;
 #pragma unroll 1
     for (u32 job = blockIdx.x + G * tile; job < jobs; job += G * TCM) {
-        const u32 i0 = job * 128 + m;
-        const u32 i = i0 < P.count ? i0 : P.count - 1;          // tail lanes shadow the last candidate
+        u32 i, r_first = 0, r_count = P.mode == 1 ? 1u : R;
+        bool pending;
+        if (P.mode == 2) {                                          // item = (live candidate, round >= 1)
+            const u32 q = job * 128 + m, qq = q < items ? q : items - 1;
+            i = P.live[qq / (R - 1)];
+            r_first = 1 + qq % (R - 1);
+            r_count = 1;
+            pending = q < items;
+        } else {
+            const u32 i0 = job * 128 + m;
+            i = i0 < P.count ? i0 : P.count - 1;                    // tail lanes shadow the last candidate
+            pending = i0 < P.count && P.pc[i + (size_t)pc_live(K) * cnt] != 0;
+        }
         const u32 *pcol = P.pc + i;
-        bool pending = i0 < P.count && pcol[(size_t)pc_live(K) * cnt] != 0;
         const u32 *nrow = P.n + (size_t)i * L;
-        // base rule for every round (HAC 4.24 input), as in k_mr_rounds
+        // base rule for every round (HAC 4.24 input), as in k_mr_rounds (items were checked in mode 1)
         int32_t status = 0;
 #pragma unroll 1
-        for (u32 r = 0; r < P.rounds && pending && !status; r++) {
+        for (u32 r = 0; r < P.rounds && pending && !status && P.mode != 2; r++) {
             const u32 *a = P.bases + ((size_t)i * P.rounds + r) * L;
             u32 br = 0, dhi = 0, ahi = 0, d0 = 0;
 #pragma unroll 1
@@ -1286,13 +1348,13 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
         const u32 *r2 = pcol + (size_t)pc_r2(K) * cnt;
         const u32 s = pcol[(size_t)pc_s(K) * cnt];
         const u32 *dl = pcol + (size_t)pc_d(K) * cnt;
-        u32 *tab = P.table + i;
+        u32 *tab = P.table + (P.mode == 2 ? (size_t)(blockIdx.x * TCM + tile) * 128 + m : (size_t)i);
         u32 *stash = tab + E * entry;
         u32 verdict = MR_PROBABLY_PRIME_V;
         int witness = -1;
         const bool was_live = pending;
 #pragma unroll 1
-        for (u32 r = 0; r < P.rounds; r++) {
+        for (u32 r = r_first; r < r_first + r_count; r++) {
             if (!tile_any(mm.t, pending || (P.forced && was_live))) break;
             const u32 *a = P.bases + ((size_t)i * P.rounds + r) * L;
             // uniform part: T0 = mm(R^2, 1), T1 = mm(a, R^2), T[e] = T[e-1] T1, then the fixed-window ladder
@@ -1310,12 +1372,12 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                     to_rns(st, a, 1, L, true, P.pow_tab);
                     bp = r2; bs = (u32)cnt;
                 } else if (u < E) {
-                    bp = tab + entry; bs = (u32)cnt;
+                    bp = tab + entry; bs = (u32)tst;
                 } else {
                     const u32 q = u - E, dg = ndig - 1 - q / (w + 1), sub = q % (w + 1);
                     if (q == 0) {
 #pragma unroll 1
-                        for (int c = 0; c < NCH; c++) S(st, c) = tab[(size_t)c * cnt];
+                        for (int c = 0; c < NCH; c++) S(st, c) = tab[(size_t)c * tst];
                     }
                     if (sub < w) { sq = true; bp = s_one; bs = 0; }
                     else {
@@ -1323,14 +1385,14 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                         const u32 lo = lw < (u32)K ? dl[(size_t)lw * cnt] : 0u;
                         const u32 hi = lw + 1 < (u32)K ? dl[(size_t)(lw + 1) * cnt] : 0u;
                         bp = tab + (size_t)(__funnelshift_r(lo, hi, bw) & (E - 1)) * entry;
-                        bs = (u32)cnt;
+                        bs = (u32)tst;
                     }
                 }
                 mm(st, bp, bs, sq, cs);
                 if (u < E) {
                     u32 *dst = tab + (size_t)u * entry;
 #pragma unroll 1
-                    for (int c = 0; c < NCH; c++) dst[(size_t)c * cnt] = S(st, c);
+                    for (int c = 0; c < NCH; c++) dst[(size_t)c * tst] = S(st, c);
                 }
             }
             // checks (HAC 4.24): even steps leave the Montgomery domain and compare, odd steps square
@@ -1341,7 +1403,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                 const bool check = (v % 2) == 0;
                 if (check) {
 #pragma unroll 1
-                    for (int c = 0; c < NCH; c++) stash[(size_t)c * cnt] = S(st, c);
+                    for (int c = 0; c < NCH; c++) stash[(size_t)c * tst] = S(st, c);
                 }
                 mm(st, s_one, check ? 1u : 0u, !check, cs);
                 if (check) {
@@ -1354,7 +1416,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                     }
                     jj++;
 #pragma unroll 1
-                    for (int c = 0; c < NCH; c++) S(st, c) = stash[(size_t)c * cnt];
+                    for (int c = 0; c < NCH; c++) S(st, c) = stash[(size_t)c * tst];
                     if (!tile_any(mm.t, need)) break;
                 }
             }
@@ -1363,9 +1425,15 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                 if (!P.forced) pending = false;
             }
         }
-        if (was_live) {
+        if (P.mode == 2) {
+            if (was_live && verdict != MR_PROBABLY_PRIME_V) atomicMin(P.wit32 + i, (u32)witness);
+        } else if (was_live) {
             P.verdict[i] = (uint8_t)verdict;
             if (P.witness) P.witness[i] = (int16_t)witness;
+            if (P.mode == 1 && verdict == MR_PROBABLY_PRIME_V && R > 1) {   // survivor of round 0
+                P.wit32[i] = 0xFFFFFFFFu;
+                P.live[atomicAdd(P.nlive, 1u)] = i;
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1374,6 +1442,20 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
 }
 constexpr size_t TC_MR_SMEM = tc_mr_smem_for(TCM);
 static_assert(TC_MR_SMEM <= 232448, "Miller-Rabin tensor tiles do not fit shared memory");
+
+// fold the items' first failing rounds into the verdicts of the round-0 survivors
+__global__ void k_mr_final(const MrParams P) {
+    const u32 q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= *P.nlive) return;
+    const u32 i = P.live[q], wr = P.wit32[i];
+    if (wr != 0xFFFFFFFFu) {
+        P.verdict[i] = (uint8_t)MR_COMPOSITE_V;
+        if (P.witness) P.witness[i] = (int16_t)wr;
+    }
+}
+constexpr int MR_TC_TILES = TCM;
+#else
+constexpr int MR_TC_TILES = 0;
 #endif
 
 // ------------------------------------------------------------------ host-side launchers
@@ -1430,11 +1512,23 @@ int launch_mr(const MrParams &p, void *stream) {
     if (rc) return rc;
 #if MR_K * 4 <= 256
     if (p.tc_b1 && p.tc_gc) {
-        void *args[] = {const_cast<MrParams *>(&p)};
-        return cudaLaunchKernel((const void *)k_mr_rounds_tc, dim3(p.tc_gc), dim3(TCM * 128), args, TC_MR_SMEM,
-                                (cudaStream_t)stream) == cudaSuccess
-                   ? 0
-                   : 6;
+        auto run = [&](u32 mode) {
+            MrParams q = p;
+            q.mode = mode;
+            void *args[] = {&q};
+            return cudaLaunchKernel((const void *)k_mr_rounds_tc, dim3(p.tc_gc), dim3(TCM * 128), args, TC_MR_SMEM,
+                                    (cudaStream_t)stream) == cudaSuccess;
+        };
+        if (p.live && !p.forced && p.rounds > 1) {          // round 0 for all, then compacted items
+            if (cudaMemsetAsync(p.nlive, 0, 4, (cudaStream_t)stream) != cudaSuccess || !run(1) || !run(2)) return 6;
+            MrParams q = p;
+            void *args[] = {&q};
+            return cudaLaunchKernel((const void *)k_mr_final, dim3((p.count + 255) / 256), dim3(256), args, 0,
+                                    (cudaStream_t)stream) == cudaSuccess
+                       ? 0
+                       : 6;
+        }
+        return run(0) ? 0 : 6;
     }
 #endif
     return launch(k_mr_rounds, ctas, p, stream);

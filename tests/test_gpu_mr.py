@@ -146,3 +146,35 @@ def test_chernick_carmichael_1024(torch_cuda, mr, orc):
     n = (6 * t + 1) * (12 * t + 1) * (18 * t + 1)
     v, w = check(torch_cuda, mr, orc, [n], [synth.mr_bases(n, 6, 1, 0)])
     assert v == [0]
+
+
+def test_forced_equals_compacted_early_exit(torch_cuda, mr):
+    """the early-exit path (round 0 for all, then compacted (survivor, round) items) and the forced path
+    (every round in one tile-job) give identical verdicts and witness rounds; batch spans several
+    persistent CTAs with more items than window-table slots."""
+    import ctypes
+    import sympy
+    torch = torch_cuda
+    ns = [synth.odd_with_top_bits(512, 21, synth.TAG_CAND, i) for i in range(1500)]
+    ns[::5] = [sympy.nextprime(n) for n in ns[::5]]                    # 300 planted primes
+    rounds = 12
+    limbs = 16
+    bases = np.stack([mr.ints_to_limbs(synth.mr_bases(n, rounds, 22, i), limbs) for i, n in enumerate(ns)])
+    d_n = torch.from_numpy(mr.ints_to_limbs(ns, limbs).view(np.int32)).cuda()
+    d_b = torch.from_numpy(np.ascontiguousarray(bases).view(np.int32)).cuda()
+    L = mr.lib()
+    L.mr_internal_miller_rabin.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_void_p,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+    out = {}
+    for forced in (0, 1):
+        v = torch.full((len(ns),), 9, dtype=torch.uint8, device="cuda")
+        w = torch.full((len(ns),), 99, dtype=torch.int16, device="cuda")
+        rc = L.mr_internal_miller_rabin(d_n.data_ptr(), limbs, len(ns), d_b.data_ptr(), rounds, 0, v.data_ptr(),
+                                        w.data_ptr(), None, 0, torch.cuda.current_stream().cuda_stream, forced, 4)
+        assert rc == 0
+        torch.cuda.synchronize()
+        out[forced] = (v.cpu().numpy().tolist(), w.cpu().numpy().tolist())
+    assert out[0] == out[1]
+    assert out[0][0] == [1 if sympy.isprime(n) else 0 for n in ns]      # 300 planted + the natural primes
+    assert all(x == -1 for x, y in zip(out[0][1], out[0][0]) if y == 1)
