@@ -57,6 +57,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_ABL_NOMMA
 #define MR_ABL_NOMMA 0
 #endif
+#ifndef MR_SQ_SPLIT
+#define MR_SQ_SPLIT 1
+#endif
 #ifndef MR_RED_VARIANT
 #define MR_RED_VARIANT 1
 #endif
@@ -601,20 +604,30 @@ __device__ __forceinline__ u32 fold_small(u32 hi, u32 lo, u32 c) {
     return r < lo ? r + c : r;
 }
 
+// Σ_b 2^(8b) d_b as a 64-bit value (d_b < 2^23.1: x = d0 + 2^8 d1 and y = d2 + 2^8 d3 are < 2^31.1)
+__device__ __forceinline__ u64 tc_value(u32 d0, u32 d1, u32 d2, u32 d3) {
+    const u32 x = d0 + (d1 << 8), y = d2 + (d3 << 8);
+    return ((u64)y << 16) + x;
+}
+// V < 2^48 -> congruent value in [0, 2^32) mod 2^32 - c: V ≡ hi c + lo = cy 2^32 + r (cy <= 1, and
+// r < 2^29 when cy = 1, so r + cy c does not wrap)
+__device__ __forceinline__ u32 fold48(u64 v, u32 c) {
+    const u64 u = (u64)(u32)(v >> 32) * c + (u32)v;
+    return (u32)u + (u32)(u >> 32) * c;
+}
+
 struct MulTc {
     const u32 *s_be;
     const u32 *s_a1c;                 // CUDA-core output column of BE1: A1'[i][TCNT] (this context)
     const u32 *s_a2c;                 // CUDA-core output column of BE2: A2[j][TCNT]
     TcTile t;
-    template <class CS>
-    __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CS &cs) {
-        constexpr bool MERGED = CS::kMerged;      // false: per-thread modulus (Miller-Rabin), unmerged BE1
-        const u32 lane_base = (u32)(t.m & ~31u) << 16;
+    // 6.1/6.2 channel products: ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk),
+    // t*_j (B') -> rows, m_r column of BE1 (qr), CUDA-core BE1 output accumulated on the fly; returns the
+    // m_r product.  SQ: the multiplicand is the state itself (no operand loads, no pointer walk).
+    template <bool SQ, class CS>
+    __device__ __forceinline__ u32 chan(const StTile &st, const u32 *bp, u32 bs, const CS &cs, u32 &qr, u32 &c1lo,
+                                        u32 &c1mi, u32 &c1hi, bool sq = SQ) {
         uint8_t *arow = st.arow;
-        // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
-        //      t*_j (B') -> rows; m_r column of BE1; CUDA-core BE1 output accumulated on the fly
-        u32 qr = 0;
-        u32 c1lo = 0, c1mi = 0, c1hi = 0;
         const u32 *bq = bp;                          // multiplicand channel pointer, advanced by bs
 #pragma unroll
         for (int c = 0; c < (K + 3) / 4; c++) {
@@ -628,8 +641,11 @@ struct MulTc {
                 w[q] = 0;
                 if (i < K) {
                     const u32 a = aw[q];
-                    const u32 b = sq ? a : *bq;
-                    bq += bs;
+                    u32 b = a;
+                    if (!SQ) {
+                        b = sq ? a : *bq;
+                        bq += bs;
+                    }
                     const u32 cc = GB(O_C + i);       // unrolled: constant-bank operands
                     const u32 xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
                     qr += xi * GB(O_A1R + i);
@@ -642,12 +658,32 @@ struct MulTc {
 #pragma unroll
         for (int j = 0; j < K; j++) {
             const u32 a = S(st, K + j);
-            const u32 b = sq ? a : *bq;
-            bq += bs;
+            u32 b = a;
+            if (!SQ) {
+                b = sq ? a : *bq;
+                bq += bs;
+            }
             S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
         }
         const u32 ar = S(st, 2 * K);
-        const u32 tr = ar * (sq ? ar : *bq);
+        return ar * (SQ || sq ? ar : *bq);
+    }
+
+    template <class CS>
+    __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CS &cs) {
+        constexpr bool MERGED = CS::kMerged;      // false: per-thread modulus (Miller-Rabin), unmerged BE1
+        const u32 lane_base = (u32)(t.m & ~31u) << 16;
+        uint8_t *arow = st.arow;
+        // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
+        //      t*_j (B') -> rows; m_r column of BE1; CUDA-core BE1 output accumulated on the fly
+        u32 qr = 0, tr;
+        u32 c1lo = 0, c1mi = 0, c1hi = 0;
+#if MR_SQ_SPLIT
+        if (sq) tr = chan<true>(st, bp, bs, cs, qr, c1lo, c1mi, c1hi);
+        else tr = chan<false>(st, bp, bs, cs, qr, c1lo, c1mi, c1hi);
+#else
+        tr = chan<false>(st, bp, bs, cs, qr, c1lo, c1mi, c1hi, sq);
+#endif
         const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
         // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij)
         tc_issue(t, t.b1);
@@ -690,9 +726,7 @@ struct MulTc {
                 w[o] = 0;
                 if (j < TCNT) {
                     const u32 c = s_be[bev_c(K) + K + j];
-                    u32 hi, lo;
-                    tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
-                    const u32 q = fold_small(hi, lo, c);
+                    const u32 q = fold48(tc_value(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]), c);
                     u32 xp;
                     if (MERGED) {
                         const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + q;   // <= (2^32-1) 2^32: no carry
@@ -748,10 +782,9 @@ struct MulTc {
                 const int i = 4 * g + o;
                 w[o] = 0;
                 if (i < TCNT) {
-                    u32 hi, lo;
-                    tc_combine(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], hi, lo);
-                    const u64 p = (u64)alpha * s_be[bev_pin(K) + i] + (((u64)hi << 32) | lo);  // < 2^48
-                    w[o] = fold_small((u32)(p >> 32), (u32)p, s_be[bev_c(K) + i]);
+                    const u64 p = (u64)alpha * s_be[bev_pin(K) + i] +
+                                  tc_value(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);   // < 2^48
+                    w[o] = fold48(p, s_be[bev_c(K) + i]);
                 }
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
