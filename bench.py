@@ -316,7 +316,7 @@ def run_ours(args, world, rank, local):
         "dtype": "u32", "data": "synthetic", "config": workload_config(args),
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "T IMAD-eq/s (INT32 IMAD pipe, 64/clk/SM x 148 SM x 1965 MHz)",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": ncu_traffic(tensor, count),
                      "kernel": kname, "ladder_ms_per_launch": ladder_ms,
                      "tensor_i8": {"achieved_tops": i8_achieved / 1e12, "peak_tops": i8_peak / 1e12,
                                    "frac": i8_achieved / i8_peak,
@@ -334,6 +334,17 @@ def run_ours(args, world, rank, local):
         "verified": verified,
     }
     print(json.dumps(line), flush=True)
+
+
+def ncu_traffic(tensor: bool, count: int):
+    """DRAM bytes per launch of the ladder kernel from the committed ncu --set full capture of the same
+    configuration (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f).get(f"{'k_modexp_tc' if tensor else 'k_modexp'}/c2/{count}")
+    except (OSError, ValueError):
+        return None
+    return None if rec is None else rec["dram_bytes_read"] + rec["dram_bytes_write"]
 
 
 def cpu_baseline(key, budget_s: float = 10.0):

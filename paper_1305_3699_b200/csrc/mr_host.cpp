@@ -317,7 +317,7 @@ struct DevBase {
     u32 *d_pow = nullptr;
     u32 *d_be = nullptr;
     u32 *d_mpl = nullptr;      // M'_j limbs [k][k+1] for the exit conversion
-    u32 *d_tcb2 = nullptr;     // tensor-core BE2 image (k <= 64)
+    u32 *d_tcb2 = nullptr;     // tensor-core BE2 image (k <= 64, and k = 65 in CTA-pair mode)
     u32 *d_tcb1u = nullptr;    // tensor-core unmerged BE1 image (Miller-Rabin, per-thread modulus)
 };
 static std::map<std::pair<int, int>, DevBase> g_devbases;
@@ -742,13 +742,21 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     // IMAD path: one CTA per T messages; tensor path: ctas0 = 128-message tile-jobs per context,
     // run by Gc persistent CTAs per context (one per SM share)
     const u32 T = use_tc ? 128u : (u32)ks.threads;
-    const u32 ctas0 = (u32)((count + T - 1) / T);
+    const bool pair = use_tc && tc_pair((u32)c0->k);   // CTA-pair tensor kernel: 256-message jobs
+    u32 ctas0 = (u32)((count + T - 1) / T);
+    if (pair) ctas0 += ctas0 & 1u;
     const u32 jobs_total = ctas0 * T * nctx;
-    u32 gc = 0;
+    u32 gc = 0, grid = 0;
     if (use_tc) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device);
-        gc = std::min<u32>((u32)((sms + nctx - 1) / nctx), ctas0);
+        if (pair) {   // gc = CTA pairs per context
+            gc = std::max<u32>(1u, std::min<u32>((u32)(sms / 2) / (u32)nctx, ctas0 / 2));
+            grid = 2 * gc * nctx;
+        } else {
+            gc = std::min<u32>((u32)((sms + nctx - 1) / nctx), ctas0);
+            grid = gc * nctx;
+        }
     }
     int w = 1;
     for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
@@ -782,7 +790,7 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     P.tc_be1_off = cx_words(c0->k) + be_half_words(c0->k);
     P.tc_gc = gc;
     int rc = timed_launch(0, st, [&] {
-                 return use_tc ? ks.launch_modexp_tc(P, gc * nctx, stream) : ks.launch_modexp(P, ctas0 * nctx, stream);
+                 return use_tc ? ks.launch_modexp_tc(P, grid, stream) : ks.launch_modexp(P, ctas0 * nctx, stream);
              }) == 0
                  ? MR_OK
                  : MR_ERR_CUDA;

@@ -98,14 +98,21 @@ __host__ __device__ constexpr u32 be_words(u32 k) { return bev_A2r(k) + pad4(k);
 // A operand: [128 messages x KP bytes] (row m = the message's K words, little-endian);
 // B operand: [NP rows (j, b) x KP bytes (i, a)]; both K-major, SWIZZLE_NONE core-matrix layout:
 // byte (r, kb) at (r / 8) * SBO + (kb / 16) * 128 + (r % 8) * 16 + kb % 16, SBO = (KP / 16) * 128.
-// D = [128 x NP] s32 in TMEM; every D value < 4k·255² < 2^24 for k <= 64.
+// D = [128 x NP] s32 in TMEM; every D value < 4k·255² (< 2^24 for k <= 64, < 2^24.02 at k = 65).
 // ---------------------------------------------------------------------------------------------
 __host__ __device__ constexpr u32 tc_kp(u32 k) { return (4 * k + 31) & ~31u; }     // K bytes, multiple of 32
 // outputs of each base extension computed on the tensor core; for k = 33 the 33rd output runs on the
-// CUDA cores so that N = 128 columns and four 128-message tiles fit the 512 TMEM columns of an SM
-__host__ __device__ constexpr u32 tc_nt(u32 k) { return (4 * k > 128 && 4 * k <= 136) ? 32 : k; }
+// CUDA cores so that N = 128 columns and four 128-message tiles fit the 512 TMEM columns of an SM;
+// for k = 65 the 65th, so that N = 256 (the largest MMA N) covers the other 64
+__host__ __device__ constexpr u32 tc_nt(u32 k) {
+    return (4 * k > 128 && 4 * k <= 136) ? 32 : ((4 * k > 256 && 4 * k <= 264) ? 64 : k);
+}
 __host__ __device__ constexpr u32 tc_np(u32 k) { return (4 * tc_nt(k) + 15) & ~15u; }  // N rows, multiple of 16
-__host__ __device__ constexpr bool tc_ok(u32 k) { return 4 * k <= 256; }
+// CTA-pair mode: the two B images of k = 65 (2 x 72 KB) do not fit one CTA next to two
+// tiles, so a 2-CTA cluster runs M = 256 MMAs (tcgen05 cta_group::2) and each CTA holds half of the
+// B rows (N/2 = 128 of the (j, b) columns); each CTA's TMEM still receives all N columns of its rows.
+__host__ __device__ constexpr bool tc_pair(u32 k) { return 4 * k > 256; }
+__host__ __device__ constexpr bool tc_ok(u32 k) { return 4 * k <= 256 || tc_nt(k) == 64; }
 __host__ __device__ constexpr u32 tc_sbo(u32 k) { return (tc_kp(k) / 16) * 128; }
 __host__ __device__ constexpr u32 tc_off(u32 k, u32 r, u32 kb) {
     return (r / 8) * tc_sbo(k) + (kb / 16) * 128 + (r % 8) * 16 + kb % 16;
@@ -155,7 +162,7 @@ struct ModexpParams {
     const u32 *tc_b2;         // tensor-core BE2 image (tc_bbytes(k)); BE1 image follows each ctx block
     const u32 *mpl;           // M'_j limbs [k][k+1] (global; exit conversion)
     u32 tc_be1_off;           // word offset of the BE1 tensor image inside a context buffer
-    u32 tc_gc;                // tensor kernel: persistent CTAs per context group
+    u32 tc_gc;                // tensor kernel: persistent CTAs (CTA pairs in pair mode) per context group
 };
 
 struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qinv mod p)

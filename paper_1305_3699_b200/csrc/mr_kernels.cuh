@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
     run_program(P, sel, jl, sel * P.ctas0 * T + jl, true, st, s_cx, mm);
 }
 
-#if MR_K * 4 <= 256
+#if MR_K * 4 <= 256 || MR_K == 65
 // ------------------------------------------------------------------ tensor-core Montgomery multiplication
 // DESIGN.md §4b.  Both base extensions run on the 5th-generation tensor cores as u8 x u8 -> s32
 // contractions (tcgen05.mma.kind::i8): with x_i = Σ_a byte_a(x_i) 2^(8a) and the pre-shifted
@@ -483,6 +483,11 @@ __global__ void __launch_bounds__(T, MINB) k_modexp(const ModexpParams P) {
 // layout), its accumulator in TCNP TMEM columns, and synchronises with a named barrier and an
 // mbarrier signalled by tcgen05.commit.  Elementwise steps and the m_r column stay on the CUDA cores.
 constexpr u32 TCKP = tc_kp(K), TCNP = tc_np(K), TCSBO = tc_sbo(K);
+// CTA-pair mode (k = 65): a 2-CTA cluster issues M = 256 MMAs (cta_group::2); each CTA
+// holds 128 of the B image's NP rows and receives all NP accumulator columns for its own 128 messages
+constexpr bool PAIR = tc_pair(K);
+constexpr u32 TC_BB = PAIR ? tc_bbytes(K) / 2 : tc_bbytes(K);   // B image bytes resident per CTA
+static_assert(!PAIR || TCNP == 256, "pair mode splits N = 256 into two CTA halves of 128 rows");
 constexpr int TCNT = tc_nt(K);                                  // outputs per base extension on the tensor core
 constexpr int TCNC = K - TCNT;                                  // outputs on the CUDA cores (k = 33: the last one)
 static_assert(TCNC <= 1, "at most one CUDA-core output per base extension");
@@ -492,13 +497,14 @@ constexpr u32 TC_ROWS = (K + 1) * 128;                          // B' and m_r ro
 constexpr u32 TC_CVEC = 2 * pad4(K);                            // CUDA-core output columns: A1' col, A2 col
 constexpr size_t tc_smem_for(int tiles) {
     return 4 * (size_t)(tiles * TC_ROWS + BEV_ + CXW + TC_CVEC) + (size_t)tiles * tc_abytes(K) +
-           2 * (size_t)tc_bbytes(K) + 64;
+           2 * (size_t)TC_BB + 128;
 }
 constexpr bool tc_fits(int tiles) { return tc_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
 // tiles per CTA: as many as fit the 227 KB of shared memory and the 512 TMEM columns (at most 4)
 constexpr int TCT = tc_fits(4) ? 4 : (tc_fits(3) ? 3 : (tc_fits(2) ? 2 : 1));
 static_assert(tc_smem_for(TCT) <= 232448, "tensor-core tile does not fit shared memory");
-constexpr u32 TC_IDESC = (2u << 4) | ((TCNP >> 3) << 17) | ((128u >> 4) << 24);  // s32 = u8 x u8, K-major, M=128
+constexpr u32 TC_M = PAIR ? 256u : 128u;
+constexpr u32 TC_IDESC = (2u << 4) | ((TCNP >> 3) << 17) | ((TC_M >> 4) << 24);  // s32 = u8 x u8, K-major
 constexpr u32 tmem_cols_for(u32 n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 constexpr u32 TC_TMEM_COLS = tmem_cols_for(TCT * TCNP);   // power of two >= 32
 constexpr u32 BEV = BEV_;                                      // the per-channel vectors of the BE image
@@ -526,6 +532,11 @@ struct TcTile {
     int bar;                          // named barrier id (1 + tile)
     bool leader;                      // thread 0 of the tile issues the MMAs
     u32 m;                            // message (= TMEM lane) index inside the tile
+    // pair mode: the tile's A operand is complete in both CTAs when rank 0's "ready" mbarrier (count 2)
+    // has one arrival from each CTA's tile leader; only rank 0's leader issues
+    u32 rbar;                         // cluster-window address of rank 0's ready mbarrier for this tile
+    u32 rphase;                       // its phase parity (rank 0 leader)
+    bool issuer;                      // leader && (rank 0 || !PAIR)
 };
 
 __device__ __forceinline__ void tile_sync(const TcTile &t) { asm volatile("bar.sync %0, 128;" ::"r"(t.bar) : "memory"); }
@@ -538,19 +549,46 @@ __device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
 #if MR_ABL_NOMMA
     return;
 #endif
-    if (t.leader) {
+    if (PAIR && t.leader)   // this CTA's half of the M = 256 operand is complete
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(t.rbar) : "memory");
+    if (t.issuer) {
+        if (PAIR) {         // wait for the peer CTA's half (bounded: a lost arrival traps)
+            u32 done = 0;
+#pragma unroll 1
+            for (u32 spin = 0; !done; spin++) {
+                asm volatile(
+                    "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, P1;\n\t}"
+                    : "=r"(done)
+                    : "r"(t.mbar + 8 * TCT), "r"(t.rphase)   // own ready barrier, shared::cta address
+                    : "memory");
+                if (spin > (1u << 26)) __trap();
+            }
+            t.rphase ^= 1u;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u32 sa = smem_u32(t.a), sb = smem_u32(bimg);
 #pragma unroll
         for (u32 ks = 0; ks < TCKP / 32; ks++) {
             const u64 da = umma_desc(sa + ks * 256), db = umma_desc(sb + ks * 256);
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t.tmem),
-                "l"(da), "l"(db), "r"(TC_IDESC), "r"(ks) : "memory");
+            if (PAIR)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t.tmem),
+                    "l"(da), "l"(db), "r"(TC_IDESC), "r"(ks) : "memory");
+            else
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t.tmem),
+                    "l"(da), "l"(db), "r"(TC_IDESC), "r"(ks) : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(t.mbar)
-                     : "memory");
+        if (PAIR)           // completion to the same mbarrier offset in both CTAs
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                    t.mbar), "h"((unsigned short)3) : "memory");
+        else
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(t.mbar)
+                         : "memory");
     }
 }
 
@@ -604,10 +642,15 @@ __device__ __forceinline__ u32 fold_small(u32 hi, u32 lo, u32 c) {
     return r < lo ? r + c : r;
 }
 
-// Σ_b 2^(8b) d_b as a 64-bit value (d_b < 2^23.1: x = d0 + 2^8 d1 and y = d2 + 2^8 d3 are < 2^31.1)
+// Σ_b 2^(8b) d_b as a 64-bit value.  k <= 64: d_b < 4k·255² < 2^24, so x = d0 + 2^8 d1 and
+// y = d2 + 2^8 d3 fit 32 bits; k = 65: d_b < 2^24.02 and x, y may not, so they are formed in 64 bits.
 __device__ __forceinline__ u64 tc_value(u32 d0, u32 d1, u32 d2, u32 d3) {
-    const u32 x = d0 + (d1 << 8), y = d2 + (d3 << 8);
-    return ((u64)y << 16) + x;
+    if (4ull * K * 255 * 255 < (1ull << 24)) {
+        const u32 x = d0 + (d1 << 8), y = d2 + (d3 << 8);
+        return ((u64)y << 16) + x;
+    }
+    const u64 x = (u64)d1 * 256u + d0, y = (u64)d3 * 256u + d2;
+    return (y << 16) + x;
 }
 // V < 2^48 -> congruent value in [0, 2^32) mod 2^32 - c: V ≡ hi c + lo = cy 2^32 + r (cy <= 1, and
 // r < 2^29 when cy = 1, so r + cy c does not wrap)
@@ -799,26 +842,31 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     extern __shared__ __align__(1024) u32 smem[];
     // layout: [B1 image | B2 image | A tiles | states | BE image | ctx | mbarriers + TMEM slot]
     uint8_t *s_b1 = reinterpret_cast<uint8_t *>(smem);
-    uint8_t *s_b2 = s_b1 + tc_bbytes(K);
-    uint8_t *s_a = s_b2 + tc_bbytes(K);
+    uint8_t *s_b2 = s_b1 + TC_BB;
+    uint8_t *s_a = s_b2 + TC_BB;
     u32 *st_all = reinterpret_cast<u32 *>(s_a + TCT * tc_abytes(K));
     u32 *s_vec = st_all + TCT * TC_ROWS;             // vectors only: s_be[bev_*(K) + i] = s_vec[...]
     u32 *s_be = s_vec - bev_c(K);
     u32 *s_cx = s_vec + BEV;
     u32 *s_a1c = s_cx + CXW;                         // CUDA-core output columns (k = 33)
     u32 *s_a2c = s_a1c + pad4(K);
-    u64 *mbar = reinterpret_cast<u64 *>(s_a2c + pad4(K));
-    u32 *tslot = reinterpret_cast<u32 *>(mbar + TCT);
-    const u32 sel = blockIdx.x >= P.tc_gc ? 1u : 0u;
+    u64 *mbar = reinterpret_cast<u64 *>(s_a2c + pad4(K));      // [TCT] MMA done, pair mode: + [TCT] ready
+    u32 *tslot = reinterpret_cast<u32 *>(mbar + (PAIR ? 2 : 1) * TCT);
+    u32 rank = 0;                                               // CTA rank in the pair (pair mode)
+    if (PAIR) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const u32 unit = PAIR ? blockIdx.x / 2 : blockIdx.x;        // CTA, or CTA pair
+    const u32 sel = unit >= P.tc_gc ? 1u : 0u;
     const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
     const u32 tid = threadIdx.x, tile = tid / 128, m = tid % 128;
     // stage constants: context block, IMAD-path BE image words, tensor images
     for (u32 w = tid; w < CXW; w += blockDim.x) s_cx[w] = gcx[w];
     for (u32 w = tid; w < BEV; w += blockDim.x) s_vec[w] = __ldg(P.be_tab + bev_c(K) + w);
-    const uint4 *g_b1 = reinterpret_cast<const uint4 *>(gcx + P.tc_be1_off);
-    for (u32 w = tid; w < tc_bbytes(K) / 16; w += blockDim.x) {
+    // B images (pair mode: this CTA's 128 of the NP rows, a contiguous byte range of the core-matrix layout)
+    const uint4 *g_b1 = reinterpret_cast<const uint4 *>(gcx + P.tc_be1_off) + rank * (TC_BB / 16);
+    const uint4 *g_b2 = reinterpret_cast<const uint4 *>(P.tc_b2) + rank * (TC_BB / 16);
+    for (u32 w = tid; w < TC_BB / 16; w += blockDim.x) {
         reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(g_b1 + w);
-        reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b2) + w);
+        reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(g_b2 + w);
     }
     if (TCNC) {   // columns TCNT of the IMAD-path tile images (BE1 merged from this context, BE2 per k)
         for (u32 i = tid; i < (u32)K; i += blockDim.x) {
@@ -827,19 +875,30 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
         }
     }
     if (tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
+    if (PAIR && tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(mbar + TCT + tid)));
     if (tid < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                     "r"(TC_TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                         "r"(TC_TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                         "r"(TC_TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (PAIR)   // both CTAs' mbarriers initialised before any remote arrive
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem_base = *tslot;
+    u32 rbar = 0;
+    if (PAIR) asm("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rbar) : "r"(smem_u32(mbar + TCT + tile)));
 
     MulTc mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP, smem_u32(mbar + tile), 0u,
-                          1 + (int)tile, m == 0, m}};
+                          1 + (int)tile, m == 0, m, rbar, 0u, m == 0 && rank == 0}};
     // per-message state: B channels in the A tile row, B' and m_r in the tile's rows
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
@@ -848,16 +907,25 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     // messages each) go round-robin, t -> CTA t % Gc, slot (t / Gc) % TCT: every CTA gets
     // floor(ctas0/Gc) or one more job, and a final partial round runs one tile per SM instead of
     // leaving a whole wave of tile slots idle.
-    const u32 Gc = P.tc_gc, cta = blockIdx.x - sel * Gc;
+    // Pair mode: the unit is a CTA pair and a job is 256 messages (128 per CTA); both CTAs walk the same
+    // job list, so every M = 256 MMA finds both halves of its operand (host: ctas0 even).
+    const u32 Gc = P.tc_gc, cta = unit - sel * Gc;
+    const u32 njobs = PAIR ? P.ctas0 / 2 : P.ctas0;
 #pragma unroll 1
-    for (u32 t = cta + Gc * tile; t < P.ctas0; t += Gc * TCT) {
-        const u32 jl = t * 128 + m;
+    for (u32 t = cta + Gc * tile; t < njobs; t += Gc * TCT) {
+        const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
         run_program(P, sel, jl, sel * P.ctas0 * 128 + jl, jl < P.count, st, s_cx, mm);
     }
 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS));
+    if (PAIR) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (tid < 32)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS));
+    } else if (tid < 32) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TC_TMEM_COLS));
+    }
 }
 #endif
 
@@ -1322,7 +1390,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     const u32 tmem_base = *tslot;
 
     MulTc mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
-                                        smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m}};
+                                        smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, 0u, 0u, m == 0}};
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
     u32 *c2rows = c2_all + tile * K * 128 + m;
@@ -1510,10 +1578,12 @@ int upload_base(const u32 *flat, int device) {
     for (const void *k : kerns)
         if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) != cudaSuccess)
             return 6;
-#if MR_K * 4 <= 256
+#if MR_K * 4 <= 256 || MR_K == 65
     if (cudaFuncSetAttribute((const void *)k_modexp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM) !=
         cudaSuccess)
         return 6;
+#endif
+#if MR_K * 4 <= 256
     if (cudaFuncSetAttribute((const void *)k_mr_rounds_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)TC_MR_SMEM) != cudaSuccess)
         return 6;
@@ -1523,13 +1593,23 @@ int upload_base(const u32 *flat, int device) {
 
 int launch_modexp(const ModexpParams &p, u32 ctas, void *stream) { return launch(k_modexp, ctas, p, stream); }
 
-#if MR_K * 4 <= 256
+#if MR_K * 4 <= 256 || MR_K == 65
+// ctas = persistent CTAs (pair mode: 2 x the CTA pairs; the cluster dimension is set here)
 int launch_modexp_tc(const ModexpParams &p, u32 ctas, void *stream) {
     void *args[] = {const_cast<ModexpParams *>(&p)};
-    return cudaLaunchKernel((const void *)k_modexp_tc, dim3(ctas), dim3(TCT * 128), args, TC_SMEM,
-                            (cudaStream_t)stream) == cudaSuccess
-               ? 0
-               : 6;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(TCT * 128);
+    cfg.dynamicSmemBytes = TC_SMEM;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = PAIR ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, (const void *)k_modexp_tc, args) == cudaSuccess ? 0 : 6;
 }
 constexpr int TC_TILES = TCT;
 #else

@@ -230,3 +230,36 @@ def test_c3_rsa3072_encrypt_decrypt(torch_cuda, mr, orc, keys):
     ref = orc.modexp_batch(msgs[:96], k["e"], n, threads=8)
     assert np.array_equal(host(c)[:96], ref)
     assert np.array_equal(host(m), msgs)
+
+
+def test_k65_pair_path_ragged(torch_cuda, mr, orc, keys):
+    """k = 65 (2048-bit N, CTA-pair tensor kernel): a ragged batch over several
+    256-message pair jobs, every output vs the oracle, for e = 65537 and for the full d."""
+    k = keys["rsa2048"]
+    n = k["n"]
+    xs = synth.messages(n, 1000, 0x5EEDC065, 64, edge=synth.edge_values(n, k["p"], k["q"]))
+    y, st, ctx = run_modexp(torch_cuda, mr, n, ints(xs), k["e"])
+    assert ctx.k == 65 and st == [0] * 1000
+    assert y == ints(orc.modexp_batch(xs, k["e"], n, threads=8))
+    sub = xs[:300]
+    yd, _, _ = run_modexp(torch_cuda, mr, n, ints(sub), k["d"])
+    assert yd == ints(orc.modexp_batch(sub, k["d"], n, threads=8))
+
+
+def test_c4_full_size_round_trip(torch_cuda, mr, orc, keys):
+    """C4 launch size (65,536 messages over a 2048-bit N, k = 65): (x^d)^e = x for every message
+    (both legs on the GPU; the e leg is oracle-checked above) and x^d vs the oracle on a sample."""
+    k = keys["rsa2048"]
+    n, count = k["n"], 65536
+    xs = synth.messages(n, count, 0x5EEDC004, 64, edge=synth.edge_values(n, k["p"], k["q"]))
+    ctx = mr.RnsContext(n)
+    assert ctx.k == 65
+    x = dev(torch_cuda, xs)
+    y = torch_cuda.empty_like(x)
+    z = torch_cuda.empty_like(x)
+    ctx.modexp(x, y, k["d"])
+    ctx.modexp(y, z, k["e"])
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.equal(x, z)
+    idx = list(range(0, 96)) + list(range(96, count, 1021))
+    assert np.array_equal(host(y)[idx], orc.modexp_batch(xs[idx], k["d"], n, threads=8))
