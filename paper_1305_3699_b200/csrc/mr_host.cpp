@@ -301,15 +301,21 @@ static void to_rns_host(const Base &b, const Big &x, u32 *out) {
 
 // Tensor-core B image (mr_internal.h tc_*): row (j, b), k byte (i, a) holds byte b of
 // 2^(8a) A[i][j] mod m_j, where A[i][j] is the contraction constant of input i for output j.
+// extra (BE2 only): row (j, b), k byte 4k holds byte b of extra[j] = m_j - |M'|_{m_j}; the kernel puts
+// α' (< 2^7) in that A column, so the MMA adds the Shenoy-Kumaresan correction α'(m_j - |M'|_{m_j}).
 static void fill_tc_image(int k, const u32 *A /* [k][k], row i, column j */, const std::vector<u32> &mods,
-                          uint8_t *out) {
+                          uint8_t *out, const u32 *extra = nullptr) {
+    static_assert(tc_kp(33) >= 4 * 33 + 4 && tc_kp(65) >= 4 * 65 + 4, "a spare K byte column for α'");
     memset(out, 0, tc_bbytes(k));
-    for (int j = 0; j < (int)tc_nt(k); j++)
+    for (int j = 0; j < (int)tc_nt(k); j++) {
         for (int i = 0; i < k; i++)
             for (int a = 0; a < 4; a++) {
                 const u32 v = (u32)(((u64)A[i * k + j] << (8 * a)) % mods[j]);
                 for (int b = 0; b < 4; b++) out[tc_off(k, 4 * j + b, 4 * i + a)] = (uint8_t)(v >> (8 * b));
             }
+        if (extra)
+            for (int b = 0; b < 4; b++) out[tc_off(k, 4 * j + b, 4 * k)] = (uint8_t)(extra[j] >> (8 * b));
+    }
 }
 
 // device residency of per-k tables
@@ -358,7 +364,8 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
     if (tc_ok(k)) {   // tensor BE2 image of A2 as [input j][output i]
         const u32 *A2 = b.flat.data() + base_layout(k).A2;   // row j, column i
         std::vector<uint8_t> img(tc_bbytes(k));
-        fill_tc_image(k, A2, b.B, img.data());
+        if (4 * k + 4 > (int)tc_kp(k)) return MR_ERR_ARG;   // no spare K column for α' (not a supported k)
+        fill_tc_image(k, A2, b.B, img.data(), b.flat.data() + base_layout(k).pin);
         if (cudaMalloc(&db.d_tcb2, img.size()) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_tcb2, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
         fill_tc_image(k, b.flat.data() + base_layout(k).A1, b.Bp, img.data());

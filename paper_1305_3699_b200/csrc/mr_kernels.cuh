@@ -491,6 +491,7 @@ static_assert(!PAIR || TCNP == 256, "pair mode splits N = 256 into two CTA halve
 constexpr int TCNT = tc_nt(K);                                  // outputs per base extension on the tensor core
 constexpr int TCNC = K - TCNT;                                  // outputs on the CUDA cores (k = 33: the last one)
 static_assert(TCNC <= 1, "at most one CUDA-core output per base extension");
+static_assert(TCNC == 0 || (TCNT + 1 == K && TCNT % 4 == 0), "α' word K sits right after the CUDA-core output");
 static_assert(TCNT % 4 == 0 || TCNC == 0, "tensor outputs must fill whole 16-column groups when split");
 constexpr u32 BEV_ = BEW - bev_c(K);
 constexpr u32 TC_ROWS = (K + 1) * 128;                          // B' and m_r rows of a tile (words)
@@ -629,34 +630,31 @@ __device__ __forceinline__ void tmem_ld16(u32 taddr, u32 (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Σ_b 2^(8b) d_b as a 64-bit (hi, lo) pair; d_b < 2^24, so d0 + 2^8 d1 and d2 + 2^8 d3 fit in 32 bits
-__device__ __forceinline__ void tc_combine(u32 d0, u32 d1, u32 d2, u32 d3, u32 &hi, u32 &lo) {
-    const u32 x = d0 + (d1 << 8), y = d2 + (d3 << 8);
-    lo = x + (y << 16);
-    hi = (y >> 16) + (lo < x ? 1u : 0u);
-}
-
-// (hi, lo) with hi < 2^17 -> congruent value in [0, 2^32) mod 2^32 - c
-__device__ __forceinline__ u32 fold_small(u32 hi, u32 lo, u32 c) {
-    const u32 r = hi * c + lo;
-    return r < lo ? r + c : r;
-}
-
-// Σ_b 2^(8b) d_b as a 64-bit value.  k <= 64: d_b < 4k·255² < 2^24, so x = d0 + 2^8 d1 and
-// y = d2 + 2^8 d3 fit 32 bits; k = 65: d_b < 2^24.02 and x, y may not, so they are formed in 64 bits.
-__device__ __forceinline__ u64 tc_value(u32 d0, u32 d1, u32 d2, u32 d3) {
+// Byte-column combine of a tensor-core output: V = Σ_b 2^(8b) d_b = hi·2^32 + lo, formed with shifts and
+// one carry chain (ALU pipe, no IMAD).  k <= 64: d_b < 4k·255² < 2^24, so x = d0 + 2^8 d1 and
+// y = d2 + 2^8 d3 fit 32 bits and V = x + 2^16 y; k = 65: d_b < 2^24.02, every term is split.
+// hi < 2^16.1 (V < 2^48.1, plus the α·pin byte column of BE2, < 2^15).
+__device__ __forceinline__ void tc_split(u32 d0, u32 d1, u32 d2, u32 d3, u32 &lo, u32 &hi) {
     if (4ull * K * 255 * 255 < (1ull << 24)) {
         const u32 x = d0 + (d1 << 8), y = d2 + (d3 << 8);
-        return ((u64)y << 16) + x;
+        asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;" : "=r"(lo), "=r"(hi) : "r"(x), "r"(y << 16), "r"(y >> 16));
+    } else {
+        asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;\n\t"
+            "add.cc.u32 %0, %0, %5;\n\taddc.u32 %1, %1, %6;\n\t"
+            "add.cc.u32 %0, %0, %7;\n\taddc.u32 %1, %1, %8;"
+            : "=r"(lo), "=r"(hi)
+            : "r"(d0), "r"(d1 << 8), "r"(d1 >> 24), "r"(d2 << 16), "r"(d2 >> 16), "r"(d3 << 24), "r"(d3 >> 8));
     }
-    const u64 x = (u64)d1 * 256u + d0, y = (u64)d3 * 256u + d2;
-    return (y << 16) + x;
 }
-// V < 2^48 -> congruent value in [0, 2^32) mod 2^32 - c: V ≡ hi c + lo = cy 2^32 + r (cy <= 1, and
-// r < 2^29 when cy = 1, so r + cy c does not wrap)
-__device__ __forceinline__ u32 fold48(u64 v, u32 c) {
-    const u64 u = (u64)(u32)(v >> 32) * c + (u32)v;
-    return (u32)u + (u32)(u >> 32) * c;
+// hi·2^32 + lo ≡ lo + hi·c (mod 2^32 - c) = cw·2^32 + w with cw <= 1 (hi c < 2^29.1): one 32-bit IMAD
+__device__ __forceinline__ void fold_hi(u32 lo, u32 hi, u32 c, u32 &w, u32 &cw) {
+    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\taddc.u32 %1, 0, 0;" : "=r"(w), "=r"(cw) : "r"(hi), "r"(c), "r"(lo));
+}
+// ... and to a word: cw·2^32 + w ≡ w + cw·c, no wrap (cw = 1 leaves w < 2^29.1)
+__device__ __forceinline__ u32 fold_word(u32 lo, u32 hi, u32 c) {
+    u32 w, cw;
+    fold_hi(lo, hi, c, w, cw);
+    return cw ? w + c : w;
 }
 
 struct MulTc {
@@ -769,12 +767,15 @@ struct MulTc {
                 w[o] = 0;
                 if (j < TCNT) {
                     const u32 c = s_be[bev_c(K) + K + j];
-                    const u32 q = fold48(tc_value(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]), c);
+                    u32 lo, hi, w33, c33;
+                    tc_split(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], lo, hi);
+                    fold_hi(lo, hi, c, w33, c33);                  // q̂_j (merged: + Σ term) as w33 + c33·2^32
                     u32 xp;
-                    if (MERGED) {
-                        const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + q;   // <= (2^32-1) 2^32: no carry
+                    if (MERGED) {   // t*_j C1_j + (w33 + c33 2^32) <= (2^32-1)(2^32-6) + 2^33 < 2^64: no carry
+                        const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + (((u64)c33 << 32) | w33);
                         xp = red64p(p, c);
                     } else {   // ξ'_j = t*_j C1_j + q̂_j |n M^-1 λ_j|  (6.4 with a per-thread modulus)
+                        const u32 q = c33 ? w33 + c : w33;
                         const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
                         u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
                         mac96(l2, m2, h2, q, cs.c2(j));
@@ -789,17 +790,23 @@ struct MulTc {
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);   // BE2 operand
           }
         }
-        if (TCNC) {   // CUDA-core output of BE1 completes the BE2 operand and its own BE2 term
+        // α' (6.6, exact through the extra modulus) goes into the A row at word K, the K-byte column where
+        // the BE2 image holds the bytes of m_i - |M'|_{m_i}: the MMA adds α'·(m_i - |M'|_{m_i}) itself
+        u32 alpha;
+        if constexpr (TCNC != 0) {   // CUDA-core output of BE1 completes the BE2 operand and its own BE2 term
             const int j = TCNT;
             S(st, K + j) = xp_c;
             sr += xp_c * s_be[bev_A2r(K) + j];
             mac96(c2lo, c2mi, c2hi, xp_c, s_a2c[j]);
-            *reinterpret_cast<uint4 *>(arow + (j / 4) * 128) = make_uint4(xp_c, 0u, 0u, 0u);
+            alpha = (sr - rr) * GB(O_MISC + 1);
+            *reinterpret_cast<uint4 *>(arow + (j / 4) * 128) = make_uint4(xp_c, alpha, 0u, 0u);
+        } else {
+            alpha = (sr - rr) * GB(O_MISC + 1);
+            *reinterpret_cast<u32 *>(arow + (K / 4) * 128 + 4 * (K % 4)) = alpha;
         }
-        // ---- 6.6 BE2 on the tensor core, exact through the extra modulus; r_i back into the A tile
+        // ---- 6.6 BE2 on the tensor core; r_i back into the A tile
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // TMEM reads done before reuse
         tc_issue(t, t.b2);
-        const u32 alpha = (sr - rr) * GB(O_MISC + 1);
         S(st, 2 * K) = rr;
         u32 r_c = 0;
         if (TCNC) {
@@ -824,10 +831,10 @@ struct MulTc {
             for (int o = 0; o < 4; o++) {
                 const int i = 4 * g + o;
                 w[o] = 0;
-                if (i < TCNT) {
-                    const u64 p = (u64)alpha * s_be[bev_pin(K) + i] +
-                                  tc_value(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);   // < 2^48
-                    w[o] = fold48(p, s_be[bev_c(K) + i]);
+                if (i < TCNT) {   // V = S_i + α'(m_i - |M'|_{m_i}) < 2^48.1
+                    u32 lo, hi;
+                    tc_split(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], lo, hi);
+                    w[o] = fold_word(lo, hi, s_be[bev_c(K) + i]);
                 }
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
