@@ -183,7 +183,8 @@ def small_primes(count: int) -> list[int]:
 
 
 def base_primes(two_k: int) -> list[int]:
-    """the 2k largest primes below 2^32, descending (reading R1), derived by the oracle itself."""
+    """the 2k largest primes below 2^32 (only those = 3 mod 4 when 2k <= 130), descending (reading R1),
+    derived by the oracle itself."""
     out = _buf(two_k)
     n = lib().orc_base_primes(_p(out), two_k)
     return [int(v) for v in out[:n]]

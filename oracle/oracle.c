@@ -384,13 +384,15 @@ static int word_is_prime(u32 w) {
 
 /*
  * The RNS base pair of the GPU library (reading R1): B = the k largest primes below
- * 2^32, B' = the next k.  The oracle derives them on its own (trial division on words) and uses
- * them only to define the MR "FACTOR" verdict (reading R14).  out receives 2k primes, descending.
+ * 2^32, B' = the next k, where for k <= 65 (2k <= 130) only primes congruent to 3 mod 4 are
+ * taken.  The oracle derives them on its own (trial division on words) and uses them only to
+ * define the MR "FACTOR" verdict (reading R14).  out receives 2k primes, descending.
  */
 ORC_EXPORT int orc_base_primes(u32 *out, int two_k) {
     int found = 0;
+    const int only_3mod4 = two_k <= 130;
     for (u64 w = 0xFFFFFFFFull; found < two_k && w > 1; w--)
-        if (word_is_prime((u32)w)) out[found++] = (u32)w;
+        if ((!only_3mod4 || (w & 3u) == 3u) && word_is_prime((u32)w)) out[found++] = (u32)w;
     return found;
 }
 

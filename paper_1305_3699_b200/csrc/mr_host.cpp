@@ -156,18 +156,21 @@ static bool is_prime32(u32 n) {  // deterministic Miller-Rabin for n < 2^32: bas
     return true;
 }
 
-// reading R1: B = the k largest primes below 2^32 (descending), B' = the next k
+// reading R1: B = the k largest primes below 2^32 (descending), B' = the next k; for k <= 65 only primes
+// m ≡ 3 (mod 4) are taken (-1 is then a non-residue, which the ρ-scaled tensor path needs, §4e)
 static std::mutex g_mu;
-static std::vector<u32> g_primes;
-static const std::vector<u32> &primes_desc(size_t n) {
-    if (g_primes.size() < n) {
-        u32 w = g_primes.empty() ? 0xFFFFFFFFu : g_primes.back() - 1;
-        while (g_primes.size() < n) {
-            if (is_prime32(w)) g_primes.push_back(w);
+static std::vector<u32> g_primes[2];   // [0] all primes, [1] primes ≡ 3 mod 4; descending from 2^32
+static bool base_3mod4(int k) { return k <= 65; }
+static const std::vector<u32> &primes_desc(size_t n, bool three_mod_four) {
+    std::vector<u32> &g = g_primes[three_mod_four ? 1 : 0];
+    if (g.size() < n) {
+        u32 w = g.empty() ? 0xFFFFFFFFu : g.back() - 1;
+        while (g.size() < n) {
+            if ((!three_mod_four || (w & 3u) == 3u) && is_prime32(w)) g.push_back(w);
             w--;
         }
     }
-    return g_primes;
+    return g;
 }
 
 // ------------------------------------------------------------------ per-k base data
@@ -190,7 +193,7 @@ static const Base &base_for(int k) {
     if (it != g_bases.end()) return it->second;
     Base b;
     b.k = k;
-    const std::vector<u32> &pr = primes_desc(2 * k);
+    const std::vector<u32> &pr = primes_desc(2 * k, base_3mod4(k));
     b.B.assign(pr.begin(), pr.begin() + k);
     b.Bp.assign(pr.begin() + k, pr.begin() + 2 * k);
     b.M = Big{1};
@@ -301,10 +304,12 @@ static void to_rns_host(const Base &b, const Big &x, u32 *out) {
 
 // Tensor-core B image (mr_internal.h tc_*): row (j, b), k byte (i, a) holds byte b of
 // 2^(8a) A[i][j] mod m_j, where A[i][j] is the contraction constant of input i for output j.
-// extra (BE2 only): row (j, b), k byte 4k holds byte b of extra[j] = m_j - |M'|_{m_j}; the kernel puts
-// α' (< 2^7) in that A column, so the MMA adds the Shenoy-Kumaresan correction α'(m_j - |M'|_{m_j}).
+// col0 (BE2): row (j, b), k byte 4k holds byte b of col0[j] = m_j - |M'|_{m_j} (times ρ_j on the scaled
+// path); the kernel puts α' (< 2^7) in that A column, so the MMA adds the Shenoy-Kumaresan term.
+// col1 (scaled BE1): k byte 4k + 1 holds byte b of col1[j], the constant offset of the sign-folded digits;
+// the kernel keeps a 1 in that A column.
 static void fill_tc_image(int k, const u32 *A /* [k][k], row i, column j */, const std::vector<u32> &mods,
-                          uint8_t *out, const u32 *extra = nullptr) {
+                          uint8_t *out, const u32 *col0 = nullptr, const u32 *col1 = nullptr) {
     static_assert(tc_kp(33) >= 4 * 33 + 4 && tc_kp(65) >= 4 * 65 + 4, "a spare K byte column for α'");
     memset(out, 0, tc_bbytes(k));
     for (int j = 0; j < (int)tc_nt(k); j++) {
@@ -313,8 +318,10 @@ static void fill_tc_image(int k, const u32 *A /* [k][k], row i, column j */, con
                 const u32 v = (u32)(((u64)A[i * k + j] << (8 * a)) % mods[j]);
                 for (int b = 0; b < 4; b++) out[tc_off(k, 4 * j + b, 4 * i + a)] = (uint8_t)(v >> (8 * b));
             }
-        if (extra)
-            for (int b = 0; b < 4; b++) out[tc_off(k, 4 * j + b, 4 * k)] = (uint8_t)(extra[j] >> (8 * b));
+        if (col0)
+            for (int b = 0; b < 4; b++) out[tc_off(k, 4 * j + b, 4 * k)] = (uint8_t)(col0[j] >> (8 * b));
+        if (col1)
+            for (int b = 0; b < 4; b++) out[tc_off(k, 4 * j + b, 4 * k + 1)] = (uint8_t)(col1[j] >> (8 * b));
     }
 }
 
@@ -477,6 +484,67 @@ static void fill_merged_be1(const Base &b, u32 *out, const u32 *cx) {
     }
 }
 
+// Tensor-core (ρ-scaled) part of a context, after fill_ctx_block and fill_merged_be1:
+// ε_i = Legendre(σ_i | m_i), ρ_i = (ε_i σ_i)^((m_i+1)/4) (m_i ≡ 3 mod 4, so ρ_i² = ε_i σ_i); the scaled
+// constant vectors, the sign-folded BE1 image with its offset column, the ρ-scaled BE2 image with the
+// α' column, and the CUDA-core output column vectors.
+static bool fill_tc_scaled(const Base &b, u32 *x) {
+    const int k = b.k;
+    const BaseLayout L = base_layout(k);
+    const u32 *A1 = b.flat.data() + L.A1, *A2 = b.flat.data() + L.A2, *pin = b.flat.data() + L.pin;
+    const int nt = (int)tc_nt(k);
+    std::vector<u32> rho(k), v(k);
+    std::vector<int> neg(k);
+    for (int i = 0; i < k; i++) {
+        const u32 m = b.B[i], s = x[cx_sigma(k) + i];
+        neg[i] = powm(s, (m - 1) / 2, m) != 1;                  // σ_i a non-residue: use -σ_i
+        v[i] = neg[i] ? (m - s) % m : s;                         // v_i = ε_i σ_i = ρ_i²
+        rho[i] = powm(v[i], ((u64)m + 1) / 4, m);
+        if ((m & 3u) != 3u || mulm(rho[i], rho[i], m) != v[i]) return false;
+    }
+    // constants: [0] R2 twice-scaled (operand right after to_rns), [1] ONE scaled, [2] KHI twice-scaled,
+    // [3] R2 scaled (loaded as an accumulator); B' and m_r channels unchanged
+    const u32 srcs[4] = {cx_r2(k), cx_one(k), cx_khi(k), cx_r2(k)};
+    for (int t = 0; t < 4; t++) {
+        u32 *dst = x + cx_sc(k) + t * (2 * k + 1);
+        const u32 *src = x + srcs[t];
+        for (int ch = 0; ch <= 2 * k; ch++) dst[ch] = src[ch];
+        for (int i = 0; i < k; i++) dst[i] = mulm(src[i] % b.B[i], (t == 1 || t == 3) ? rho[i] : v[i], b.B[i]);
+    }
+    // merged BE1 constants A1'[i][j] = |M_i|_{m'_j} |N M^-1 λ_j|, signed by ε_i; offsets Σ_{ε_i = -1} m_i A1'[i][j]
+    std::vector<u32> A1s((size_t)k * k), off(k, 0);
+    const u32 *c2 = x + cx_c2(k);
+    u32 qr_off = 0;
+    for (int i = 0; i < k; i++) {
+        for (int j = 0; j < k; j++) {
+            const u32 mj = b.Bp[j], a = mulm(A1[i * k + j], c2[j], mj);
+            A1s[(size_t)i * k + j] = neg[i] ? (mj - a) % mj : a;
+            if (neg[i]) off[j] = (u32)(((u64)off[j] + mulm(b.B[i] % mj, a, mj)) % mj);
+        }
+        const u32 a1r = b.flat[L.A1r + i];
+        x[cx_a1x(k) + 2 * i] = neg[i] ? 0u - a1r : a1r;
+        if (neg[i]) qr_off += b.B[i] * a1r;
+        if (nt < k) x[cx_a1x(k) + 2 * i + 1] = A1s[(size_t)i * k + nt];
+    }
+    x[cx_scv(k) + 0] = qr_off;
+    if (nt < k) {
+        x[cx_scv(k) + 1] = off[nt];
+        x[cx_scv(k) + 2] = mulm(pin[nt], rho[nt], b.B[nt]);
+        for (int j = 0; j < k; j++) x[cx_a2s(k) + j] = mulm(A2[j * k + nt], rho[nt], b.B[nt]);
+    }
+    const size_t tcw = tc_bbytes(k) / 4;
+    uint8_t *img1 = reinterpret_cast<uint8_t *>(x + cx_words(k) + be_half_words(k));
+    fill_tc_image(k, A1s.data(), b.Bp, img1, nullptr, off.data());
+    // BE2: |M'_j|_{m_i} ρ_i (row j, column i) and the α' column (m_i - |M'|_{m_i}) ρ_i
+    std::vector<u32> A2s((size_t)k * k), pins(k);
+    for (int j = 0; j < k; j++)
+        for (int i = 0; i < k; i++) A2s[(size_t)j * k + i] = mulm(A2[j * k + i], rho[i], b.B[i]);
+    for (int i = 0; i < k; i++) pins[i] = mulm(pin[i], rho[i], b.B[i]);
+    fill_tc_image(k, A2s.data(), b.B, reinterpret_cast<uint8_t *>(x + cx_words(k) + be_half_words(k) + tcw),
+                  pins.data());
+    return true;
+}
+
 static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, int device, const Big &in_bound,
                      size_t in_limbs, const Big *khi_shift_limbs_half /* CRT: half limbs */, const Big *qinv) {
     *out = nullptr;
@@ -510,17 +578,12 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->bits = bits(N);
     c->N = N;
     const size_t tc_words = tc_ok(k) ? tc_bbytes(k) / 4 : 0;
-    c->h_cx.assign(cx_words(k) + be_half_words(k) + tc_words, 0);
+    c->h_cx.assign(cx_words(k) + be_half_words(k) + 2 * tc_words, 0);
     fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
     fill_merged_be1(b, c->h_cx.data() + cx_words(k), c->h_cx.data());
-    if (tc_ok(k)) {   // tensor BE1 image of A1'[i][j] = |M_i|_{m'_j} |N M^-1 λ_j|
-        const u32 *A1 = b.flat.data() + base_layout(k).A1;
-        std::vector<u32> A1m((size_t)k * k);
-        for (int i = 0; i < k; i++)
-            for (int j = 0; j < k; j++) A1m[i * k + j] = mulm(A1[i * k + j], c->h_cx[cx_c2(k) + j], b.Bp[j]);
-        fill_tc_image(k, A1m.data(), b.Bp, reinterpret_cast<uint8_t *>(c->h_cx.data() + cx_words(k) + be_half_words(k)));
-    }
-    int rc = ensure_device_base(k, device, &c->d_pow, &c->d_be);
+    int rc = MR_OK;
+    if (tc_ok(k) && !fill_tc_scaled(b, c->h_cx.data())) rc = MR_ERR_ARG;   // not reachable for the R1 bases
+    if (rc == MR_OK) rc = ensure_device_base(k, device, &c->d_pow, &c->d_be);
     if (rc == MR_OK) {
         c->d_tcb2 = g_devbases[std::make_pair(device, k)].d_tcb2;
         c->d_mpl = g_devbases[std::make_pair(device, k)].d_mpl;
@@ -795,6 +858,7 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     P.tc_b2 = c0->d_tcb2;
     P.mpl = c0->d_mpl;
     P.tc_be1_off = cx_words(c0->k) + be_half_words(c0->k);
+    P.tc_be2_off = P.tc_be1_off + tc_bbytes(c0->k) / 4;
     P.tc_gc = gc;
     int rc = timed_launch(0, st, [&] {
                  return use_tc ? ks.launch_modexp_tc(P, grid, stream) : ks.launch_modexp(P, ctas0 * nctx, stream);

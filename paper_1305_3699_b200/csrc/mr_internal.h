@@ -31,7 +31,15 @@ __host__ __device__ constexpr u32 cx_khi(u32 k) { return cx_one(k) + 2 * k + 1; 
 __host__ __device__ constexpr u32 cx_qinvr(u32 k) { return cx_khi(k) + 2 * k + 1; }  // [2k+1] qinv R mod p
 __host__ __device__ constexpr u32 cx_n(u32 k) { return cx_qinvr(k) + 2 * k + 1; }    // [k+1] N limbs
 __host__ __device__ constexpr u32 cx_inb(u32 k) { return cx_n(k) + k + 1; }          // [2k+2] input bound limbs
-__host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_inb(k) + 2 * k + 2 + 3) & ~3u; }
+// Tensor-core path only: B residues are stored ρ-scaled, s_i = x_i ρ_i with ρ_i² = ε_i σ_i (ε_i = ±1; the
+// B primes are ≡ 3 mod 4 for k <= 65, so one of ±σ_i is a square), which turns the q-digit step
+// ξ_i = σ_i a_i b_i into ε_i ξ_i = s_a s_b mod m_i; the signs ε_i and the scales ρ_i live in the
+// per-context constants below and in the per-context tensor images.
+__host__ __device__ constexpr u32 cx_sc(u32 k) { return cx_inb(k) + 2 * k + 2; }     // [4][2k+1] R2ρ², ONEρ, KHIρ², R2ρ
+__host__ __device__ constexpr u32 cx_a1x(u32 k) { return (cx_sc(k) + 4 * (2 * k + 1) + 1) & ~1u; }  // [k][2] (ε_i|M_i|_{2^32}, ε_i A1'[i][TCNT])
+__host__ __device__ constexpr u32 cx_a2s(u32 k) { return cx_a1x(k) + 2 * k; }        // [k]  A2[j][TCNT] ρ_TCNT
+__host__ __device__ constexpr u32 cx_scv(u32 k) { return cx_a2s(k) + k; }            // [4]  q̂_r offset, BE1-TCNT offset, pin_TCNT ρ_TCNT, 0
+__host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_scv(k) + 4 + 3) & ~3u; }
 
 // ---------------------------------------------------------------------------------------------
 // Per-k base tables (N-independent).  The CUDA TU for k keeps the hot ones in __constant__ memory
@@ -162,6 +170,7 @@ struct ModexpParams {
     const u32 *tc_b2;         // tensor-core BE2 image (tc_bbytes(k)); BE1 image follows each ctx block
     const u32 *mpl;           // M'_j limbs [k][k+1] (global; exit conversion)
     u32 tc_be1_off;           // word offset of the BE1 tensor image inside a context buffer
+    u32 tc_be2_off;           // word offset of the (ρ-scaled, per-context) BE2 tensor image
     u32 tc_gc;                // tensor kernel: persistent CTAs (CTA pairs in pair mode) per context group
 };
 

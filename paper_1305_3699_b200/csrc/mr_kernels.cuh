@@ -133,6 +133,7 @@ __device__ __forceinline__ u32 &S(const StTile &s, int ch) {
 
 struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt): context block in smem
     static constexpr bool kMerged = true;   // BE1 image carries |N M^-1 λ_j| (per-context image)
+    static constexpr bool kScaled = false;  // B residues stored plainly; q-digits via σ_i
     const u32 *cx;
     __device__ u32 sigma(int i) const { return cx[cx_sigma(K) + i]; }
     __device__ u32 c2(int j) const { return cx[cx_c2(K) + j]; }
@@ -142,6 +143,7 @@ struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt)
 
 struct CtxThread {                    // one modulus per thread (Miller-Rabin): per-candidate rows
     static constexpr bool kMerged = false;
+    static constexpr bool kScaled = false;
     const u32 *pc;
     const u32 *nrow;                  // candidate limbs
     u32 stride, limbs;
@@ -149,6 +151,17 @@ struct CtxThread {                    // one modulus per thread (Miller-Rabin): 
     __device__ u32 c2(int j) const { return pc[(size_t)(pc_c2(K) + j) * stride]; }
     __device__ u32 nminv() const { return pc[(size_t)pc_nminv(K) * stride]; }
     __device__ u32 nlimb(int l) const { return (u32)l < limbs ? nrow[l] : 0u; }
+};
+
+// Tensor-core modexp contexts: B residues stored ρ-scaled (s_i = x_i ρ_i, ρ_i² = ε_i σ_i),
+// so the q-digit step is one product, ε_i ξ_i = s_a s_b mod m_i; the signs are folded into the
+// per-context BE1 image (offset column) and the vectors below, the scales into the BE2 image.
+struct CtxTc : CtxSmem {
+    static constexpr bool kScaled = true;
+    __device__ uint2 a1x(int i) const { return reinterpret_cast<const uint2 *>(cx + cx_a1x(K))[i]; }
+    __device__ u32 qr_off() const { return cx[cx_scv(K) + 0]; }
+    __device__ u32 c1_off() const { return cx[cx_scv(K) + 1]; }
+    __device__ u32 pin_nc() const { return cx[cx_scv(K) + 2]; }
 };
 
 // ------------------------------------------------------------------ RNS Montgomery multiplication
@@ -379,10 +392,13 @@ __device__ __forceinline__ void stage_smem(u32 *s_be, u32 *s_cx, const u32 *gcx,
 // multiply, canonical exit, store.  MM is the Montgomery multiplication (IMAD tiles or tensor core);
 // `valid` = false runs the program on zeros without storing (tail threads of a tensor-core tile
 // must still take part in the tile's barriers).
-template <class STT, class MM>
+template <class STT, class MM, class CS = CtxSmem>
 __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 jl, u32 slot, bool valid, STT st,
                                             const u32 *s_cx, MM &mm) {
-    const CtxSmem cs{s_cx};
+    const CS cs{s_cx};
+    // constant operands / accumulators (0xF0 + i): plain vectors at cx_r2; the ρ-scaled path (§4e) uses
+    // cx_sc: operands right after to_rns twice-scaled (R2, KHI), ONE scaled, the loaded R2 scaled
+    const u32 *cvec = s_cx + (CS::kScaled ? cx_sc(K) : cx_r2(K));
     const size_t tstride = P.jobs_total;
     const size_t entry = (size_t)NCH * tstride;
     const u32 *xrow = P.x + (size_t)(valid ? jl : 0) * P.in_limbs;
@@ -413,7 +429,7 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
         if (fl & OPF_LOAD) {
             const u32 *src;
             size_t str;
-            if (ld >= 0xF0) { src = s_cx + cx_r2(K) + (ld - 0xF0) * NCH; str = 1; }
+            if (ld >= 0xF0) { src = cvec + (CS::kScaled && ld == OPND_R2 ? 3u : ld - 0xF0) * NCH; str = 1; }
             else { src = P.table + ld * entry + slot; str = tstride; }
 #pragma unroll 1
             for (int c = 0; c < NCH; c++) S(st, c) = src[c * str];
@@ -423,7 +439,7 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
             const u32 *bp;
             u32 bs;
             if (sq) { bp = s_cx; bs = 0; }
-            else if (opnd >= 0xF0) { bp = s_cx + cx_r2(K) + (opnd - 0xF0) * NCH; bs = 1; }
+            else if (opnd >= 0xF0) { bp = cvec + (opnd - 0xF0) * NCH; bs = 1; }
             else { bp = P.table + opnd * entry + slot; bs = (u32)tstride; }
             mm(st, bp, bs, sq, cs);
         }
@@ -679,7 +695,7 @@ struct MulTc {
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const int i = 4 * c + q;
-                w[q] = 0;
+                w[q] = (CS::kScaled && i == K) ? 0x100u : 0u;   // scaled: the BE1 offset column holds 1
                 if (i < K) {
                     const u32 a = aw[q];
                     u32 b = a;
@@ -688,9 +704,17 @@ struct MulTc {
                         bq += bs;
                     }
                     const u32 cc = GB(O_C + i);       // unrolled: constant-bank operands
-                    const u32 xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
-                    qr += xi * GB(O_A1R + i);
-                    if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
+                    u32 xi;
+                    if constexpr (CS::kScaled) {      // ε_i ξ_i = s_a s_b, canonical (the signed digit is m_i - xi)
+                        xi = canon(mulmod(a, b, cc), cc);
+                        const uint2 ax = cs.a1x(i);
+                        qr += xi * ax.x;
+                        if (TCNC) mac96(c1lo, c1mi, c1hi, xi, ax.y);
+                    } else {
+                        xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
+                        qr += xi * GB(O_A1R + i);
+                        if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
+                    }
                     w[q] = xi;
                 }
             }
@@ -713,12 +737,17 @@ struct MulTc {
     template <class CS>
     __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CS &cs) {
         constexpr bool MERGED = CS::kMerged;      // false: per-thread modulus (Miller-Rabin), unmerged BE1
+        constexpr u32 ONECOL = CS::kScaled ? 0x100u : 0u;   // byte 1 of A word K: the BE1 offset column
         const u32 lane_base = (u32)(t.m & ~31u) << 16;
         uint8_t *arow = st.arow;
         // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
         //      t*_j (B') -> rows; m_r column of BE1; CUDA-core BE1 output accumulated on the fly
         u32 qr = 0, tr;
         u32 c1lo = 0, c1mi = 0, c1hi = 0;
+        if constexpr (CS::kScaled) {      // constant offsets of the sign-folded digits
+            qr = cs.qr_off();
+            if (TCNC) c1lo = cs.c1_off();
+        }
 #if MR_SQ_SPLIT
         if (sq) tr = chan<true>(st, bp, bs, cs, qr, c1lo, c1mi, c1hi);
         else tr = chan<false>(st, bp, bs, cs, qr, c1lo, c1mi, c1hi);
@@ -799,10 +828,10 @@ struct MulTc {
             sr += xp_c * s_be[bev_A2r(K) + j];
             mac96(c2lo, c2mi, c2hi, xp_c, s_a2c[j]);
             alpha = (sr - rr) * GB(O_MISC + 1);
-            *reinterpret_cast<uint4 *>(arow + (j / 4) * 128) = make_uint4(xp_c, alpha, 0u, 0u);
+            *reinterpret_cast<uint4 *>(arow + (j / 4) * 128) = make_uint4(xp_c, alpha | ONECOL, 0u, 0u);
         } else {
             alpha = (sr - rr) * GB(O_MISC + 1);
-            *reinterpret_cast<u32 *>(arow + (K / 4) * 128 + 4 * (K % 4)) = alpha;
+            *reinterpret_cast<u32 *>(arow + (K / 4) * 128 + 4 * (K % 4)) = alpha | ONECOL;
         }
         // ---- 6.6 BE2 on the tensor core; r_i back into the A tile
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // TMEM reads done before reuse
@@ -811,7 +840,8 @@ struct MulTc {
         u32 r_c = 0;
         if (TCNC) {
             const int i = TCNT;
-            mac96(c2lo, c2mi, c2hi, alpha, s_be[bev_pin(K) + i]);
+            if constexpr (CS::kScaled) mac96(c2lo, c2mi, c2hi, alpha, cs.pin_nc());
+            else mac96(c2lo, c2mi, c2hi, alpha, s_be[bev_pin(K) + i]);
             r_c = red96(c2hi, c2mi, c2lo, s_be[bev_c(K) + i], 0);
         }
         tc_wait(t);
@@ -870,16 +900,10 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     for (u32 w = tid; w < BEV; w += blockDim.x) s_vec[w] = __ldg(P.be_tab + bev_c(K) + w);
     // B images (pair mode: this CTA's 128 of the NP rows, a contiguous byte range of the core-matrix layout)
     const uint4 *g_b1 = reinterpret_cast<const uint4 *>(gcx + P.tc_be1_off) + rank * (TC_BB / 16);
-    const uint4 *g_b2 = reinterpret_cast<const uint4 *>(P.tc_b2) + rank * (TC_BB / 16);
+    const uint4 *g_b2 = reinterpret_cast<const uint4 *>(gcx + P.tc_be2_off) + rank * (TC_BB / 16);   // ρ-scaled, per context
     for (u32 w = tid; w < TC_BB / 16; w += blockDim.x) {
         reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(g_b1 + w);
         reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(g_b2 + w);
-    }
-    if (TCNC) {   // columns TCNT of the IMAD-path tile images (BE1 merged from this context, BE2 per k)
-        for (u32 i = tid; i < (u32)K; i += blockDim.x) {
-            s_a1c[i] = gcx[CXW + be_img_index(i, TCNT)];
-            s_a2c[i] = __ldg(P.be_tab + BEH + be_img_index(i, TCNT));
-        }
     }
     if (tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
     if (PAIR && tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(mbar + TCT + tid)));
@@ -904,8 +928,10 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     u32 rbar = 0;
     if (PAIR) asm("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rbar) : "r"(smem_u32(mbar + TCT + tile)));
 
-    MulTc mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP, smem_u32(mbar + tile), 0u,
-                          1 + (int)tile, m == 0, m, rbar, 0u, m == 0 && rank == 0}};
+    // CUDA-core output columns of the scaled path come from the context block (cx_a1x via CtxTc, cx_a2s)
+    MulTc mm{s_be, s_a1c, s_cx + cx_a2s(K), TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
+                                                 smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, rbar, 0u,
+                                                 m == 0 && rank == 0}};
     // per-message state: B channels in the A tile row, B' and m_r in the tile's rows
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
@@ -921,7 +947,7 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
 #pragma unroll 1
     for (u32 t = cta + Gc * tile; t < njobs; t += Gc * TCT) {
         const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
-        run_program(P, sel, jl, sel * P.ctas0 * 128 + jl, jl < P.count, st, s_cx, mm);
+        run_program<StTile, MulTc, CtxTc>(P, sel, jl, sel * P.ctas0 * 128 + jl, jl < P.count, st, s_cx, mm);
     }
 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1317,6 +1343,7 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
 // are ignored.  Early exit is per tile: a round is skipped when no candidate of the tile is pending.
 struct CtxMr {                        // per-candidate constants of one thread
     static constexpr bool kMerged = false;
+    static constexpr bool kScaled = false;
     u32 sig[K];                       // σ_i in registers (the channel-product loop is fully unrolled)
     const u32 *c2row;                 // shared memory: c2row[j * 128] = |n M^-1 λ_j|_{m'_j}
     u32 nmv;                          // n M^-1 mod 2^32

@@ -275,13 +275,16 @@ def test_mr_vs_sympy(orc):
         assert (v == 1) == sympy.isprime(n)
 
 
-def test_base_primes_are_the_largest_primes(orc):
+@pytest.mark.parametrize("two_k", [20, 130, 194])
+def test_base_primes_are_the_largest_primes(orc, two_k):
+    """reading R1: the largest primes below 2^32, restricted to primes = 3 mod 4 for k <= 65."""
     import sympy
-    bp = orc.base_primes(20)
+    bp = orc.base_primes(two_k)
     expect, x = [], 1 << 32
-    while len(expect) < 20:
+    while len(expect) < two_k:
         x = sympy.prevprime(x)
-        expect.append(x)
+        if two_k > 130 or x % 4 == 3:
+            expect.append(x)
     assert bp == expect
 
 
