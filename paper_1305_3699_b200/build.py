@@ -14,8 +14,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(CSRC, "obj")
-LIB = os.path.join(HERE, "libmr_rns.so")
+# MR_BUILD_OBJ / MR_BUILD_LIB: build a variant (e.g. with MR_NVCC_DEFS) elsewhere, for A/B runs (tools/ab.sh)
+OBJ = os.environ.get("MR_BUILD_OBJ") or os.path.join(CSRC, "obj")
+LIB = os.environ.get("MR_BUILD_LIB") or os.path.join(HERE, "libmr_rns.so")
 ROOT = os.path.dirname(HERE)
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")

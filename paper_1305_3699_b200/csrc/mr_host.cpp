@@ -831,9 +831,20 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     int w = 1;
     for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
     const size_t nch = 2 * (size_t)c0->k + 1;
-    const size_t table_words = (size_t)table_slots(w) * nch * jobs_total;
+    // split schedule when jobs do not divide evenly over the tile slots: one more table
+    // slot for the handed-over states, and one flag per (context, job, rank)
+    const u32 njobs = pair ? ctas0 / 2 : ctas0;
+    const u32 slots_per_group = gc * (u32)ks.tc_tiles;
+    const char *ns = getenv("MR_RNS_NO_SPLIT");
+    const bool split = use_tc && !(ns && ns[0] == '1') && njobs > slots_per_group && njobs % slots_per_group != 0;
+    const size_t table_words = (size_t)(table_slots(w) + (split ? 1 : 0)) * nch * jobs_total;
+    const size_t flag_words = split ? (size_t)2 * njobs * 2 : 0;
     u32 *d_table = nullptr;
-    if (cudaMallocAsync(&d_table, table_words * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    if (cudaMallocAsync(&d_table, (table_words + flag_words) * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    if (split && cudaMemsetAsync(d_table + table_words, 0, flag_words * 4, st) != cudaSuccess) {
+        cudaFreeAsync(d_table, st);
+        return MR_ERR_CUDA;
+    }
     ModexpParams P;
     memset(&P, 0, sizeof P);
     for (int i = 0; i < 2; i++) {
@@ -860,6 +871,8 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     P.tc_be1_off = cx_words(c0->k) + be_half_words(c0->k);
     P.tc_be2_off = P.tc_be1_off + tc_bbytes(c0->k) / 4;
     P.tc_gc = gc;
+    P.hslot = table_slots(w);
+    P.flags = split ? d_table + table_words : nullptr;
     int rc = timed_launch(0, st, [&] {
                  return use_tc ? ks.launch_modexp_tc(P, grid, stream) : ks.launch_modexp(P, ctas0 * nctx, stream);
              }) == 0

@@ -172,6 +172,10 @@ struct ModexpParams {
     u32 tc_be1_off;           // word offset of the BE1 tensor image inside a context buffer
     u32 tc_be2_off;           // word offset of the (ρ-scaled, per-context) BE2 tensor image
     u32 tc_gc;                // tensor kernel: persistent CTAs (CTA pairs in pair mode) per context group
+    // tensor kernel, split schedule: a job whose ops straddle two tile slots hands its
+    // state over through table slot `hslot` and a per-(job, rank) flag (zeroed before the launch)
+    u32 hslot;                // handoff slot index in the window table (= table_slots(w))
+    u32 *flags;               // [2 contexts][jobs][2 ranks]; null = no split schedule
 };
 
 struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qinv mod p)

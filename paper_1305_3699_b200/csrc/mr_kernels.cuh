@@ -63,6 +63,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_RED_VARIANT
 #define MR_RED_VARIANT 1
 #endif
+#ifndef MR_PF_L1
+#define MR_PF_L1 0          // A/B hook: prefetch the next window-table operand into L1 instead of L2
+#endif
 
 // 96-bit multiply-accumulate (lo, mid, hi) += x * y; lowers to IMAD.WIDE.U32 with carry-out + IADD3.X
 __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) {
@@ -392,9 +395,11 @@ __device__ __forceinline__ void stage_smem(u32 *s_be, u32 *s_cx, const u32 *gcx,
 // multiply, canonical exit, store.  MM is the Montgomery multiplication (IMAD tiles or tensor core);
 // `valid` = false runs the program on zeros without storing (tail threads of a tensor-core tile
 // must still take part in the tile's barriers).
+// Ops [o_begin, o_end) of the program (split schedule, §4f): o_begin > 0 resumes from the handoff slot
+// (loaded by the caller), o_end < nops stops before the exit and leaves the state in st.
 template <class STT, class MM, class CS = CtxSmem>
 __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 jl, u32 slot, bool valid, STT st,
-                                            const u32 *s_cx, MM &mm) {
+                                            const u32 *s_cx, MM &mm, u32 o_begin = 0, u32 o_end = 0xFFFFFFFFu) {
     const CS cs{s_cx};
     // constant operands / accumulators (0xF0 + i): plain vectors at cx_r2; the ρ-scaled path (§4e) uses
     // cx_sc: operands right after to_rns twice-scaled (R2, KHI), ONE scaled, the loaded R2 scaled
@@ -403,12 +408,13 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
     const size_t entry = (size_t)NCH * tstride;
     const u32 *xrow = P.x + (size_t)(valid ? jl : 0) * P.in_limbs;
     const bool ok = valid && less_than(xrow, s_cx + cx_inb(K), P.in_limbs);
-    if (valid && sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
+    if (valid && sel == 0 && P.status && o_begin == 0) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
 
     const u64 *prog = sel ? P.prog[1] : P.prog[0];
-    const u32 nops = sel ? P.nops[1] : P.nops[0];
+    const u32 nops_all = sel ? P.nops[1] : P.nops[0];
+    const u32 nops = o_end < nops_all ? o_end : nops_all;
 #pragma unroll 1
-    for (u32 s = 0; s < nops; s++) {
+    for (u32 s = o_begin; s < nops; s++) {
         const u64 op = __ldg(prog + s);
         if (s + 1 < nops) {   // next multiplicand from the window table: pull it from HBM into L2 now
             const u64 nx = __ldg(prog + s + 1);
@@ -416,7 +422,13 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
             if (!(nx & OPF_NOMUL) && nopnd < 0xF0) {
                 const u32 *np = P.table + nopnd * entry + slot;
 #pragma unroll 1
-                for (int c = 0; c < NCH; c += 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(np + c * tstride));
+                for (int c = 0; c < NCH; c += 1) {
+#if MR_PF_L1
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(np + c * tstride));
+#else
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(np + c * tstride));
+#endif
+                }
             }
         }
         const u32 fl = (u32)op & 0xFF, opnd = (u32)(op >> 8) & 0xFF, ld = (u32)(op >> 16) & 0xFF;
@@ -459,6 +471,7 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
             for (int c = 0; c < NCH; c++) dst[c * tstride] = S(st, c);
         }
     }
+    if (nops < nops_all) return;        // first part of a split job: the caller hands the state over
     from_rns(st, cs, P.mpl);
     if (valid) {
         u32 *yrow = P.y + sel * P.out_stride + (size_t)jl * P.out_limbs;
@@ -944,10 +957,61 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     // job list, so every M = 256 MMA finds both halves of its operand (host: ctas0 even).
     const u32 Gc = P.tc_gc, cta = unit - sel * Gc;
     const u32 njobs = PAIR ? P.ctas0 / 2 : P.ctas0;
+    if (!P.flags) {
 #pragma unroll 1
-    for (u32 t = cta + Gc * tile; t < njobs; t += Gc * TCT) {
-        const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
-        run_program<StTile, MulTc, CtxTc>(P, sel, jl, sel * P.ctas0 * 128 + jl, jl < P.count, st, s_cx, mm);
+        for (u32 t = cta + Gc * tile; t < njobs; t += Gc * TCT) {
+            const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
+            run_program<StTile, MulTc, CtxTc>(P, sel, jl, sel * P.ctas0 * 128 + jl, jl < P.count, st, s_cx, mm);
+        }
+    } else {
+        // Split (McNaughton wrap-around) schedule: the group's njobs x L op-units are laid out
+        // linearly and slot s = cta * TCT + tile takes units [s C, (s+1) C), C = max(L, ceil(njobs L / NS)).
+        // A job straddling the boundary of slots s and s+1 runs its EARLY ops at the start of slot s+1 and
+        // its LATE ops at the end of slot s (C >= L keeps the two parts apart in time); the state passes
+        // through table slot hslot and a release/acquire flag.
+        const u32 L = sel ? P.nops[1] : P.nops[0], NS = Gc * TCT;
+        const u64 W = (u64)njobs * L;
+        const u64 C = (W + NS - 1) / NS > L ? (W + NS - 1) / NS : (u64)L;
+        const u64 s0 = (u64)(cta * TCT + tile) * C;
+        const u64 s1 = s0 + C < W ? s0 + C : W;
+        const size_t hoff = (size_t)P.hslot * NCH * P.jobs_total;
+        u32 *flag_base = P.flags + (size_t)sel * njobs * 2 + rank;
+        u64 u = s0;
+#pragma unroll 1
+        while (u < s1) {
+            const u32 t = (u32)(u / L), o = (u32)(u % L);
+            const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
+            const u32 col = sel * P.ctas0 * 128 + jl;
+            u32 ob, oe;
+            if (o) { ob = 0; oe = L - o; }                          // early part of a job shared with slot s-1
+            else if (u + L <= s1) { ob = 0; oe = L; }               // whole job
+            else { ob = L - (u32)(s1 - u); oe = L; }                // late part of a job shared with slot s+1
+            u32 *flag = flag_base + (size_t)t * 2;
+            if (ob) {   // wait for the early part, then resume from the handed-over state
+                if (m == 0) {
+                    u32 v = 0;
+#pragma unroll 1
+                    for (u32 spin = 0; !v; spin++) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                        if (spin > (1u << 28)) __trap();
+                    }
+                }
+                tile_sync(mm.t);
+                const u32 *src = P.table + hoff + col;
+#pragma unroll 1
+                for (int c = 0; c < NCH; c++) S(st, c) = __ldcg(src + (size_t)c * P.jobs_total);
+            }
+            run_program<StTile, MulTc, CtxTc>(P, sel, jl, col, jl < P.count, st, s_cx, mm, ob, oe);
+            if (oe < L) {   // hand the state over to the slot that runs the late part
+                u32 *dst = P.table + hoff + col;
+#pragma unroll 1
+                for (int c = 0; c < NCH; c++) __stcg(dst + (size_t)c * P.jobs_total, S(st, c));
+                __threadfence();
+                tile_sync(mm.t);
+                if (m == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+            }
+            u += oe - ob;
+        }
     }
 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
