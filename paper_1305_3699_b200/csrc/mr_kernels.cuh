@@ -404,6 +404,9 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
     // constant operands / accumulators (0xF0 + i): plain vectors at cx_r2; the ρ-scaled path (§4e) uses
     // cx_sc: operands right after to_rns twice-scaled (R2, KHI), ONE scaled, the loaded R2 scaled
     const u32 *cvec = s_cx + (CS::kScaled ? cx_sc(K) : cx_r2(K));
+    // the scaled (tensor) path reads every multiplicand from global memory (window table, or the constant
+    // vectors of the context block in HBM), so its operand loads are explicit ld.global (mulop_ld)
+    const u32 *gcvec = (sel ? P.ctx[1] : P.ctx[0]) + cx_sc(K);
     const size_t tstride = P.jobs_total;
     const size_t entry = (size_t)NCH * tstride;
     const u32 *xrow = P.x + (size_t)(valid ? jl : 0) * P.in_limbs;
@@ -451,7 +454,7 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
             const u32 *bp;
             u32 bs;
             if (sq) { bp = s_cx; bs = 0; }
-            else if (opnd >= 0xF0) { bp = cvec + (opnd - 0xF0) * NCH; bs = 1; }
+            else if (opnd >= 0xF0) { bp = (CS::kScaled ? gcvec : cvec) + (opnd - 0xF0) * NCH; bs = 1; }
             else { bp = P.table + opnd * entry + slot; bs = (u32)tstride; }
             mm(st, bp, bs, sq, cs);
         }
@@ -686,6 +689,14 @@ __device__ __forceinline__ u32 fold_word(u32 lo, u32 hi, u32 c) {
     return cw ? w + c : w;
 }
 
+// multiplicand load: global-only on the scaled modexp path (no aliasing with the A-tile stores, so the
+// compiler may issue the loads early), generic otherwise (Miller-Rabin passes shared-memory constants)
+template <class CS>
+__device__ __forceinline__ u32 mulop_ld(const u32 *p) {
+    if constexpr (CS::kScaled) return __ldcg(p);
+    else return *p;
+}
+
 struct MulTc {
     const u32 *s_be;
     const u32 *s_a1c;                 // CUDA-core output column of BE1: A1'[i][TCNT] (this context)
@@ -713,7 +724,7 @@ struct MulTc {
                     const u32 a = aw[q];
                     u32 b = a;
                     if (!SQ) {
-                        b = sq ? a : *bq;
+                        b = sq ? a : mulop_ld<CS>(bq);
                         bq += bs;
                     }
                     const u32 cc = GB(O_C + i);       // unrolled: constant-bank operands
@@ -738,13 +749,13 @@ struct MulTc {
             const u32 a = S(st, K + j);
             u32 b = a;
             if (!SQ) {
-                b = sq ? a : *bq;
+                b = sq ? a : mulop_ld<CS>(bq);
                 bq += bs;
             }
             S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
         }
         const u32 ar = S(st, 2 * K);
-        return ar * (SQ || sq ? ar : *bq);
+        return ar * (SQ || sq ? ar : mulop_ld<CS>(bq));
     }
 
     template <class CS>
