@@ -61,7 +61,7 @@ __constant__ u32 g_base[BASE_WORDS];
 #define MR_SQ_SPLIT 1
 #endif
 #ifndef MR_RED_VARIANT
-#define MR_RED_VARIANT 1
+#define MR_RED_VARIANT 2
 #endif
 #ifndef MR_PF_L1
 #define MR_PF_L1 0          // A/B hook: prefetch the next window-table operand into L1 instead of L2
@@ -81,7 +81,17 @@ __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) 
 // cy = 1, vl < 2^26 so vl + c does not wrap.  Both products take the previous 64-bit value as their
 // addend pair, so each is one IMAD.WIDE with no register moves: u = h c + p has high word uh + h
 // (mod 2^32), v = uh c + u has high word cy + uh + h; the differences recover uh and cy.
-#if MR_RED_VARIANT == 1
+#if MR_RED_VARIANT == 2
+// u = h c (IMAD.WIDE, no addend pair to build) + l with an ALU carry chain; then v = uh c + ul (uh < 2^13:
+// one 32-bit IMAD), a wrap adds c (v < 2^26 then)
+__device__ __forceinline__ u32 red64p(u64 p, u32 c) {
+    const u64 hc = (u64)(u32)(p >> 32) * c;
+    u32 ul, uh;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;" : "=r"(ul), "=r"(uh) : "r"((u32)hc), "r"((u32)p), "r"((u32)(hc >> 32)));
+    const u32 vl = uh * c + ul;
+    return vl < ul ? vl + c : vl;
+}
+#elif MR_RED_VARIANT == 1
 __device__ __forceinline__ u32 red64p(u64 p, u32 c) {
     const u64 u = (u64)(u32)(p >> 32) * c + (u32)p;
     const u32 uh = (u32)(u >> 32), ul = (u32)u;
