@@ -257,6 +257,11 @@ static const Base &base_for(int k) {
     for (int j = 0; j < k; j++) f[L.ONE + k + j] = b.lambda[j];
     f[L.ONE + 2 * k] = 1;
     for (int l = 0; l <= k; l++) f[L.ML + l] = l < (int)b.M.size() ? b.M[l] : 0;
+    for (int ch = 0; ch < 2 * k; ch++) {
+        const u32 m = ch < k ? b.B[ch] : b.Bp[ch - k];
+        f[L.MM + ch] = m;
+        f[L.MINV + ch] = 0u - inv32(m);
+    }
     b.pow.assign((size_t)k * 2 * k, 0);
     for (int l = 0; l < k; l++) {
         Big p2 = pow2(32 * l);
@@ -484,10 +489,12 @@ static void fill_merged_be1(const Base &b, u32 *out, const u32 *cx) {
     }
 }
 
-// Tensor-core (ρ-scaled) part of a context, after fill_ctx_block and fill_merged_be1:
-// ε_i = Legendre(σ_i | m_i), ρ_i = (ε_i σ_i)^((m_i+1)/4) (m_i ≡ 3 mod 4, so ρ_i² = ε_i σ_i); the scaled
-// constant vectors, the sign-folded BE1 image with its offset column, the ρ-scaled BE2 image with the
-// α' column, and the CUDA-core output column vectors.
+// Tensor-core (ρ-scaled) part of a context, after fill_ctx_block and fill_merged_be1.
+// The tensor path reduces channel products with word Montgomery reductions (result T·2^-32 mod m), so
+// the constants absorb R32 = 2^32 mod m = c: ε_i = Legendre(σ_i c_i | m_i), ρ_i = (ε_i σ_i c_i)^((m_i+1)/4)
+// (m_i ≡ 3 mod 4, so ρ_i² = ε_i σ_i c_i); the scaled constant vectors, the sign-folded BE1 image (× c'_j)
+// with its offset column, the ρ-scaled BE2 image (× c_i) with the α' column, the CUDA-core output
+// column vectors (plain red96, no R32) and the epilogue constants.
 static bool fill_tc_scaled(const Base &b, u32 *x) {
     const int k = b.k;
     const BaseLayout L = base_layout(k);
@@ -496,9 +503,9 @@ static bool fill_tc_scaled(const Base &b, u32 *x) {
     std::vector<u32> rho(k), v(k);
     std::vector<int> neg(k);
     for (int i = 0; i < k; i++) {
-        const u32 m = b.B[i], s = x[cx_sigma(k) + i];
-        neg[i] = powm(s, (m - 1) / 2, m) != 1;                  // σ_i a non-residue: use -σ_i
-        v[i] = neg[i] ? (m - s) % m : s;                         // v_i = ε_i σ_i = ρ_i²
+        const u32 m = b.B[i], s = mulm(x[cx_sigma(k) + i], 0u - m, m);   // σ_i c_i, c_i = 2^32 mod m_i
+        neg[i] = powm(s, (m - 1) / 2, m) != 1;                  // σ_i c_i a non-residue: use -σ_i c_i
+        v[i] = neg[i] ? (m - s) % m : s;                         // v_i = ε_i σ_i c_i = ρ_i²
         rho[i] = powm(v[i], ((u64)m + 1) / 4, m);
         if ((m & 3u) != 3u || mulm(rho[i], rho[i], m) != v[i]) return false;
     }
@@ -527,19 +534,38 @@ static bool fill_tc_scaled(const Base &b, u32 *x) {
         if (nt < k) x[cx_a1x(k) + 2 * i + 1] = A1s[(size_t)i * k + nt];
     }
     x[cx_scv(k) + 0] = qr_off;
-    if (nt < k) {
+    if (nt < k) {   // CUDA-core output (plain red96): its t* carries 2^-32, so C1 is taken times c'
         x[cx_scv(k) + 1] = off[nt];
         x[cx_scv(k) + 2] = mulm(pin[nt], rho[nt], b.B[nt]);
+        x[cx_scv(k) + 3] = mulm(b.flat[L.C1 + nt], 0u - b.Bp[nt], b.Bp[nt]);
         for (int j = 0; j < k; j++) x[cx_a2s(k) + j] = mulm(A2[j * k + nt], rho[nt], b.B[nt]);
+    }
+    for (int j = 0; j < k; j++) {   // BE1 epilogue: ξ'_j = mont(t*_j · C1_j c'^2 + V'_j), V' carries × c'
+        const u32 mj = b.Bp[j], cj = 0u - mj;
+        x[cx_ep1(k) + 4 * j + 0] = mj;
+        x[cx_ep1(k) + 4 * j + 1] = 0u - inv32(mj);
+        x[cx_ep1(k) + 4 * j + 2] = mulm(mulm(b.flat[L.C1 + j], cj, mj), cj, mj);
+        x[cx_ep1(k) + 4 * j + 3] = b.flat[L.A2r + j];
+    }
+    for (int i = 0; i < k; i++) {   // BE2 epilogue: s_i = mont(V_i), V carries × c_i
+        x[cx_ep2(k) + 2 * i + 0] = b.B[i];
+        x[cx_ep2(k) + 2 * i + 1] = 0u - inv32(b.B[i]);
     }
     const size_t tcw = tc_bbytes(k) / 4;
     uint8_t *img1 = reinterpret_cast<uint8_t *>(x + cx_words(k) + be_half_words(k));
-    fill_tc_image(k, A1s.data(), b.Bp, img1, nullptr, off.data());
-    // BE2: |M'_j|_{m_i} ρ_i (row j, column i) and the α' column (m_i - |M'|_{m_i}) ρ_i
+    std::vector<u32> A1t((size_t)k * k), offt(k);   // tensor copies × c'_j (the Montgomery factor)
+    for (int j = 0; j < k; j++) {
+        const u32 mj = b.Bp[j], cj = 0u - mj;
+        for (int i = 0; i < k; i++) A1t[(size_t)i * k + j] = mulm(A1s[(size_t)i * k + j], cj, mj);
+        offt[j] = mulm(off[j], cj, mj);
+    }
+    fill_tc_image(k, A1t.data(), b.Bp, img1, nullptr, offt.data());
+    // BE2: |M'_j|_{m_i} ρ_i c_i (row j, column i) and the α' column (m_i - |M'|_{m_i}) ρ_i c_i
     std::vector<u32> A2s((size_t)k * k), pins(k);
     for (int j = 0; j < k; j++)
-        for (int i = 0; i < k; i++) A2s[(size_t)j * k + i] = mulm(A2[j * k + i], rho[i], b.B[i]);
-    for (int i = 0; i < k; i++) pins[i] = mulm(pin[i], rho[i], b.B[i]);
+        for (int i = 0; i < k; i++)
+            A2s[(size_t)j * k + i] = mulm(mulm(A2[j * k + i], rho[i], b.B[i]), 0u - b.B[i], b.B[i]);
+    for (int i = 0; i < k; i++) pins[i] = mulm(mulm(pin[i], rho[i], b.B[i]), 0u - b.B[i], b.B[i]);
     fill_tc_image(k, A2s.data(), b.B, reinterpret_cast<uint8_t *>(x + cx_words(k) + be_half_words(k) + tcw),
                   pins.data());
     return true;

@@ -31,15 +31,19 @@ __host__ __device__ constexpr u32 cx_khi(u32 k) { return cx_one(k) + 2 * k + 1; 
 __host__ __device__ constexpr u32 cx_qinvr(u32 k) { return cx_khi(k) + 2 * k + 1; }  // [2k+1] qinv R mod p
 __host__ __device__ constexpr u32 cx_n(u32 k) { return cx_qinvr(k) + 2 * k + 1; }    // [k+1] N limbs
 __host__ __device__ constexpr u32 cx_inb(u32 k) { return cx_n(k) + k + 1; }          // [2k+2] input bound limbs
-// Tensor-core path only: B residues are stored ρ-scaled, s_i = x_i ρ_i with ρ_i² = ε_i σ_i (ε_i = ±1; the
+// Tensor-core path only: B residues are stored ρ-scaled, s_i = x_i ρ_i with ρ_i² = ε_i σ_i 2^32 (ε_i = ±1; the
 // B primes are ≡ 3 mod 4 for k <= 65, so one of ±σ_i is a square), which turns the q-digit step
 // ξ_i = σ_i a_i b_i into ε_i ξ_i = s_a s_b mod m_i; the signs ε_i and the scales ρ_i live in the
 // per-context constants below and in the per-context tensor images.
 __host__ __device__ constexpr u32 cx_sc(u32 k) { return cx_inb(k) + 2 * k + 2; }     // [4][2k+1] R2ρ², ONEρ, KHIρ², R2ρ
 __host__ __device__ constexpr u32 cx_a1x(u32 k) { return (cx_sc(k) + 4 * (2 * k + 1) + 1) & ~1u; }  // [k][2] (ε_i|M_i|_{2^32}, ε_i A1'[i][TCNT])
 __host__ __device__ constexpr u32 cx_a2s(u32 k) { return cx_a1x(k) + 2 * k; }        // [k]  A2[j][TCNT] ρ_TCNT
-__host__ __device__ constexpr u32 cx_scv(u32 k) { return cx_a2s(k) + k; }            // [4]  q̂_r offset, BE1-TCNT offset, pin_TCNT ρ_TCNT, 0
-__host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_scv(k) + 4 + 3) & ~3u; }
+__host__ __device__ constexpr u32 cx_scv(u32 k) { return cx_a2s(k) + k; }            // [4]  q̂_r offset, BE1-TCNT offset, pin_TCNT ρ_TCNT, C1_TCNT R32
+// epilogue constants of the word-Montgomery reductions (§4g): BE1 output j: (m'_j, -m'_j^-1, C1_j R32², |M'_j|_{2^32});
+// BE2 output i: (m_i, -m_i^-1)
+__host__ __device__ constexpr u32 cx_ep1(u32 k) { return (cx_scv(k) + 4 + 3) & ~3u; }   // [k][4]
+__host__ __device__ constexpr u32 cx_ep2(u32 k) { return cx_ep1(k) + 4 * k; }          // [k][2]
+__host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_ep2(k) + 2 * k + 3) & ~3u; }
 
 // ---------------------------------------------------------------------------------------------
 // Per-k base tables (N-independent).  The CUDA TU for k keeps the hot ones in __constant__ memory
@@ -47,7 +51,7 @@ __host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_scv(k) + 4 + 3) &
 // ---------------------------------------------------------------------------------------------
 struct BaseLayout {
     u32 k;
-    u32 c, c2, A1r, A2r, C1, pin, misc, NMp, MiS, MU, ONE, ML;   // device constant bank (prefix)
+    u32 c, c2, A1r, A2r, C1, pin, misc, NMp, MiS, MU, ONE, ML, MM, MINV;   // device constant bank (prefix)
     u32 const_words;                                              // words uploaded to __constant__
     u32 MpL, A1, A2, words;                                       // host-side / global-memory tables
 };
@@ -66,7 +70,9 @@ __host__ __device__ constexpr BaseLayout base_layout(u32 k) {
     b.MU = b.MiS + k;               // [k]      |M^-1|_{m'_j}         (Miller-Rabin setup)
     b.ONE = b.MU + k;               // [2k+1]   RNS image of 1 (B' in ξ-form)
     b.ML = b.ONE + 2 * k + 1;       // [k+1]    M positional limbs    (Miller-Rabin setup)
-    b.const_words = b.ML + k + 1;
+    b.MM = b.ML + k + 1;            // [2k]     m (B then B')         (word Montgomery reduction, §4g)
+    b.MINV = b.MM + 2 * k;          // [2k]     -m^-1 mod 2^32
+    b.const_words = b.MINV + 2 * k;
     b.MpL = b.const_words;          // [k][k+1] M'_j positional limbs (global memory, exit conversion)
     b.A1 = b.MpL + k * (k + 1);     // [k][k]   |M_i|_{m'_j}  (row i, column j; source of the BE images)
     b.A2 = b.A1 + k * k;            // [k][k]   |M'_j|_{m_i}  (row j, column i)

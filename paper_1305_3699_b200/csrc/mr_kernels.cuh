@@ -43,7 +43,7 @@ enum : u32 { MR_COMPOSITE_V = 0, MR_PROBABLY_PRIME_V = 1, MR_FACTOR_V = 2 };
 constexpr BaseLayout BL = base_layout(K);
 constexpr u32 O_C = BL.c, O_C2 = BL.c2, O_A1R = BL.A1r, O_A2R = BL.A2r;
 constexpr u32 O_C1 = BL.C1, O_PIN = BL.pin, O_MISC = BL.misc, O_NMP = BL.NMp;
-constexpr u32 O_MIS = BL.MiS, O_MU = BL.MU, O_ONE = BL.ONE, O_ML = BL.ML;
+constexpr u32 O_MIS = BL.MiS, O_MU = BL.MU, O_ONE = BL.ONE, O_ML = BL.ML, O_MM = BL.MM, O_MINV = BL.MINV;
 constexpr u32 BASE_WORDS = BL.const_words;          // __constant__ prefix of the base table
 constexpr u32 CXW = cx_words(K);
 constexpr u32 SMEM_STATE = NCH * T;           // words of per-CTA residue state
@@ -125,6 +125,20 @@ __device__ __forceinline__ u32 red96(u32 hi, u32 mid, u32 lo, u32 c, u32 c2) {
 
 __device__ __forceinline__ u32 mulmod(u32 a, u32 b, u32 c) { return red64p((u64)a * b, c); }
 
+// Word Montgomery reduction (tensor path): T = thi·2^32 + tlo < 2^64 -> R ≡ T·2^-32 (mod m),
+// R in [0, 2^32) (lazy).  q = tlo·(-m^-1) makes q·m + T ≡ 0 mod 2^32; U = (q·m + T) / 2^32 < 2^32 + m;
+// a carry out of the 64-bit sum means U ≥ 2^32, and U - 2^32 + c ≡ U with no wrap (U - 2^32 < m).
+// Three instructions (IMAD, IMAD.WIDE with carry, predicated add) instead of the ~8 of red64p.
+__device__ __forceinline__ u32 mont_red(u32 tlo, u32 thi, u32 m, u32 minv) {
+    const u32 q = tlo * minv;
+    u32 ulo, uhi, cy;
+    asm("mad.lo.cc.u32 %0, %3, %4, %5;\n\tmadc.hi.cc.u32 %1, %3, %4, %6;\n\taddc.u32 %2, 0, 0;"
+        : "=r"(ulo), "=r"(uhi), "=r"(cy)
+        : "r"(q), "r"(m), "r"(tlo), "r"(thi));
+    (void)ulo;
+    return cy ? uhi - m : uhi;             // - m ≡ + c (mod 2^32)
+}
+
 __device__ __forceinline__ u32 canon(u32 x, u32 c) {  // lazy residue -> [0, m)
     const u32 m = 0u - c;
     return x >= m ? x - m : x;
@@ -175,6 +189,9 @@ struct CtxTc : CtxSmem {
     __device__ u32 qr_off() const { return cx[cx_scv(K) + 0]; }
     __device__ u32 c1_off() const { return cx[cx_scv(K) + 1]; }
     __device__ u32 pin_nc() const { return cx[cx_scv(K) + 2]; }
+    __device__ u32 c1nc() const { return cx[cx_scv(K) + 3]; }
+    __device__ uint4 ep1(int j) const { return reinterpret_cast<const uint4 *>(cx + cx_ep1(K))[j]; }
+    __device__ uint2 ep2(int i) const { return reinterpret_cast<const uint2 *>(cx + cx_ep2(K))[i]; }
 };
 
 // ------------------------------------------------------------------ RNS Montgomery multiplication
@@ -739,8 +756,9 @@ struct MulTc {
                     }
                     const u32 cc = GB(O_C + i);       // unrolled: constant-bank operands
                     u32 xi;
-                    if constexpr (CS::kScaled) {      // ε_i ξ_i = s_a s_b, canonical (the signed digit is m_i - xi)
-                        xi = canon(mulmod(a, b, cc), cc);
+                    if constexpr (CS::kScaled) {      // ε_i ξ_i = s_a s_b 2^-32, canonical (signed digit m_i - xi)
+                        const u64 pr = (u64)a * b;
+                        xi = canon(mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + i), GB(O_MINV + i)), cc);
                         const uint2 ax = cs.a1x(i);
                         qr += xi * ax.x;
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, ax.y);
@@ -762,7 +780,12 @@ struct MulTc {
                 b = sq ? a : mulop_ld<CS>(bq);
                 bq += bs;
             }
-            S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
+            if constexpr (CS::kScaled) {              // t*_j 2^-32 (the epilogue constants carry 2^64)
+                const u64 pr = (u64)a * b;
+                S(st, K + j) = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + K + j), GB(O_MINV + K + j));
+            } else {
+                S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
+            }
         }
         const u32 ar = S(st, 2 * K);
         return ar * (SQ || sq ? ar : mulop_ld<CS>(bq));
@@ -795,7 +818,10 @@ struct MulTc {
         if (TCNC) {   // the CUDA-core output overlaps the MMA
             const int j = TCNT;
             const u32 cj = s_be[bev_c(K) + K + j];
-            const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
+            u32 c1j;
+            if constexpr (CS::kScaled) c1j = cs.c1nc();     // t* carries 2^-32: C1 c'
+            else c1j = s_be[bev_C1(K) + j];
+            const u64 p = (u64)S(st, K + j) * c1j;
             if (MERGED) {
                 mac96(c1lo, c1mi, c1hi, (u32)p, 1u);
                 u32 hi2 = c1hi;
@@ -829,11 +855,22 @@ struct MulTc {
                 const int j = 4 * g + o;
                 w[o] = 0;
                 if (j < TCNT) {
-                    const u32 c = s_be[bev_c(K) + K + j];
                     u32 lo, hi, w33, c33;
                     tc_split(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], lo, hi);
-                    fold_hi(lo, hi, c, w33, c33);                  // q̂_j (merged: + Σ term) as w33 + c33·2^32
                     u32 xp;
+                    if constexpr (CS::kScaled) {   // ξ'_j = mont(t*_j C1_j c'^2 + V'_j): (m', -m'^-1, C1 c'^2, A2r)
+                        const uint4 e = cs.ep1(j);
+                        fold_hi(lo, hi, 0u - e.x, w33, c33);
+                        const u64 p = (u64)S(st, K + j) * e.z + (((u64)c33 << 32) | w33);
+                        xp = mont_red((u32)p, (u32)(p >> 32), e.x, e.y);
+                        S(st, K + j) = xp;
+                        sr += xp * e.w;
+                        if (TCNC) mac96(c2lo, c2mi, c2hi, xp, s_a2c[j]);
+                        w[o] = xp;
+                        continue;
+                    }
+                    const u32 c = s_be[bev_c(K) + K + j];
+                    fold_hi(lo, hi, c, w33, c33);                  // q̂_j (merged: + Σ term) as w33 + c33·2^32
                     if (MERGED) {   // t*_j C1_j + (w33 + c33 2^32) <= (2^32-1)(2^32-6) + 2^33 < 2^64: no carry
                         const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + (((u64)c33 << 32) | w33);
                         xp = red64p(p, c);
@@ -898,7 +935,12 @@ struct MulTc {
                 if (i < TCNT) {   // V = S_i + α'(m_i - |M'|_{m_i}) < 2^48.1
                     u32 lo, hi;
                     tc_split(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], lo, hi);
-                    w[o] = fold_word(lo, hi, s_be[bev_c(K) + i]);
+                    if constexpr (CS::kScaled) {   // s_i = mont(V_i) (the image carries × c_i)
+                        const uint2 e = cs.ep2(i);
+                        w[o] = mont_red(lo, hi, e.x, e.y);
+                    } else {
+                        w[o] = fold_word(lo, hi, s_be[bev_c(K) + i]);
+                    }
                 }
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);

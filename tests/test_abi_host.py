@@ -89,7 +89,9 @@ def _layout(k):
     o["MU"] = o["MiS"] + k
     o["ONE"] = o["MU"] + k
     o["ML"] = o["ONE"] + 2 * k + 1
-    o["MpL"] = o["ML"] + k + 1
+    o["MM"] = o["ML"] + k + 1
+    o["MINV"] = o["MM"] + 2 * k
+    o["MpL"] = o["MINV"] + 2 * k
     o["A1"] = o["MpL"] + k * (k + 1)
     o["A2"] = o["A1"] + k * k
     return o
@@ -117,6 +119,7 @@ def test_base_table_identities(k):
     W = 1 << 32
     for ch, m in enumerate(B + Bp):
         assert f[o["c"] + ch] == W - m and f[o["c2"] + ch] == (W - m) ** 2
+        assert f[o["MM"] + ch] == m and f[o["MINV"] + ch] * m % W == W - 1     # -m^-1 mod 2^32
     for i in range(k):
         Mi = M // B[i]
         for j in range(k):
