@@ -1154,8 +1154,11 @@ int mr_internal_ctx_table(const uint32_t *modulus, size_t limbs, int k, uint32_t
         if (mod_word(N, m) == 0) return -MR_ERR_NOT_COPRIME;
     for (u32 m : b.Bp)
         if (mod_word(N, m) == 0) return -MR_ERR_NOT_COPRIME;
-    std::vector<u32> x(cx_words(k), 0);
+    const size_t tc_words = tc_ok(k) ? tc_bbytes(k) / 4 : 0;
+    std::vector<u32> x(cx_words(k) + be_half_words(k) + 2 * tc_words, 0);   // the device context buffer
     fill_ctx_block(b, N, limbs, N, limbs, nullptr, nullptr, x.data());
+    fill_merged_be1(b, x.data() + cx_words(k), x.data());
+    if (tc_ok(k) && !fill_tc_scaled(b, x.data())) return -MR_ERR_ARG;
     if (out) memcpy(out, x.data(), std::min(cap, x.size()) * 4);
     return (int)x.size();
 }

@@ -195,6 +195,46 @@ def test_ctx_table_identities(keys, name):
         lam = pow(Mp // Bp[j], -1, Bp[j])
         assert cx[r2 + k + j] == R2 % Bp[j] * lam % Bp[j] and cx[one + k + j] == lam
     assert cx[r2 + 2 * k] == R2 % W
+    _check_tensor_constants(cx, k, N, B, Bp, M, Mp, sig, r2, one)
+
+
+def _cx_tc_offsets(k):
+    """python mirror of the tensor-path part of mr_internal.h cx_* (DESIGN.md §4e, §4g)."""
+    inb = 8 + 2 * k + 4 * (2 * k + 1) + k + 1
+    sc = inb + 2 * k + 2
+    a1x = (sc + 4 * (2 * k + 1) + 1) & ~1
+    a2s = a1x + 2 * k
+    scv = a2s + k
+    ep1 = (scv + 4 + 3) & ~3
+    ep2 = ep1 + 4 * k
+    return {"sc": sc, "a1x": a1x, "a2s": a2s, "scv": scv, "ep1": ep1, "ep2": ep2}
+
+
+def _check_tensor_constants(cx, k, N, B, Bp, M, Mp, sig, r2, one):
+    """ρ-scaling with word-Montgomery factors: ρ_i² = ε_i σ_i 2^32 (mod m_i); the scaled constant
+    vectors; the signed m_r column; the epilogue constants (m, -m^-1 mod 2^32, C1 2^64, |M'_j|_{2^32})."""
+    W = 1 << 32
+    o = _cx_tc_offsets(k)
+    n = 2 * k + 1
+    for i, m in enumerate(B):
+        rho = cx[o["sc"] + 1 * n + i]                                  # ONE scaled once: ρ_i
+        v = rho * rho % m
+        eps = 1 if v == cx[sig + i] * W % m else -1
+        assert v == eps * cx[sig + i] * W % m                          # ρ² = ε σ 2^32
+        assert m % 4 == 3                                              # reading R1 (k <= 65)
+        assert cx[o["sc"] + 0 * n + i] == cx[r2 + i] * v % m           # R² ρ² (operand right after to_rns)
+        assert cx[o["sc"] + 3 * n + i] == cx[r2 + i] * rho % m         # R² ρ (loaded accumulator)
+        assert cx[o["a1x"] + 2 * i] == (eps * ((M // m) % W)) % W       # ε_i |M_i|_{2^32}
+    for ch in range(n):                                                # B' and m_r channels unscaled
+        if ch >= k:
+            assert cx[o["sc"] + 0 * n + ch] == cx[r2 + ch] and cx[o["sc"] + 1 * n + ch] == cx[one + ch]
+    for j, m in enumerate(Bp):
+        lam = pow(Mp // m, -1, m)
+        c1 = pow(M, -1, m) * pow(lam, -1, m) % m
+        e = cx[o["ep1"] + 4 * j: o["ep1"] + 4 * j + 4]
+        assert e[0] == m and e[1] * m % W == W - 1 and e[2] == c1 * W * W % m and e[3] == (Mp // m) % W
+    for i, m in enumerate(B):
+        assert cx[o["ep2"] + 2 * i] == m and cx[o["ep2"] + 2 * i + 1] * m % W == W - 1
 
 
 def test_ctx_table_rejections():
