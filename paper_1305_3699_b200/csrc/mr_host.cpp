@@ -337,6 +337,7 @@ struct DevBase {
     u32 *d_mpl = nullptr;      // M'_j limbs [k][k+1] for the exit conversion
     u32 *d_tcb2 = nullptr;     // tensor-core BE2 image (k <= 64, and k = 65 in CTA-pair mode)
     u32 *d_tcb1u = nullptr;    // tensor-core unmerged BE1 image (Miller-Rabin, per-thread modulus)
+    u32 *d_one = nullptr;      // RNS image of 1 (2k+1 words; Miller-Rabin tensor path multiplicand)
 };
 static std::map<std::pair<int, int>, DevBase> g_devbases;
 
@@ -370,6 +371,10 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
         if (cudaMalloc(&db.d_mpl, n * 4) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_mpl, b.flat.data() + L.MpL, n * 4, cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
     }
+    if (cudaMalloc(&db.d_one, (2 * (size_t)k + 1) * 4) != cudaSuccess) return MR_ERR_NOMEM;
+    if (cudaMemcpy(db.d_one, b.flat.data() + base_layout(k).ONE, (2 * (size_t)k + 1) * 4, cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+        return MR_ERR_CUDA;
     if (cudaMalloc(&db.d_be, b.be.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
     if (cudaMemcpy(db.d_be, b.be.data(), b.be.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
         return MR_ERR_CUDA;
@@ -1105,6 +1110,7 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
         P.tc_b1 = db.d_tcb1u;
         P.tc_b2 = db.d_tcb2;
         P.tc_gc = gc;
+        P.one_g = db.d_one;
     }
     if (compact) {
         P.live = d_aux;

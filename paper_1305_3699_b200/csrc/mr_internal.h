@@ -212,6 +212,7 @@ struct MrParams {               // Miller-Rabin (§3.2; HAC 4.24)
     const u32 *tc_b1;           // tensor path: unmerged BE1 image (per k); null = IMAD path
     const u32 *tc_b2;           // tensor path: BE2 image
     u32 tc_gc;                  // tensor path: persistent CTAs
+    const u32 *one_g;           // tensor path: RNS image of 1 (per k) in global memory (multiplicand loads are ld.global)
     // tensor path, early-exit compaction: mode 0 = every round in one tile-job (forced, or a
     // single round); mode 1 = round 0 for every candidate, survivors appended to live[] (count *nlive);
     // mode 2 = items (live candidate, round r >= 1) as independent one-round jobs, the first failing

@@ -131,11 +131,11 @@ __device__ __forceinline__ u32 mulmod(u32 a, u32 b, u32 c) { return red64p((u64)
 // Three instructions (IMAD, IMAD.WIDE with carry, predicated add) instead of the ~8 of red64p.
 __device__ __forceinline__ u32 mont_red(u32 tlo, u32 thi, u32 m, u32 minv) {
     const u32 q = tlo * minv;
-    u32 ulo, uhi, cy;
+    [[maybe_unused]] u32 ulo;
+    u32 uhi, cy;
     asm("mad.lo.cc.u32 %0, %3, %4, %5;\n\tmadc.hi.cc.u32 %1, %3, %4, %6;\n\taddc.u32 %2, 0, 0;"
         : "=r"(ulo), "=r"(uhi), "=r"(cy)
         : "r"(q), "r"(m), "r"(tlo), "r"(thi));
-    (void)ulo;
     return cy ? uhi - m : uhi;             // - m ≡ + c (mod 2^32)
 }
 
@@ -161,6 +161,7 @@ __device__ __forceinline__ u32 &S(const StTile &s, int ch) {
 struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt): context block in smem
     static constexpr bool kMerged = true;   // BE1 image carries |N M^-1 λ_j| (per-context image)
     static constexpr bool kScaled = false;  // B residues stored plainly; q-digits via σ_i
+    static constexpr bool kMont = false;    // word-Montgomery reductions in the tensor multiplication (§4g)
     const u32 *cx;
     __device__ u32 sigma(int i) const { return cx[cx_sigma(K) + i]; }
     __device__ u32 c2(int j) const { return cx[cx_c2(K) + j]; }
@@ -171,6 +172,7 @@ struct CtxSmem {                      // one modulus per CTA (encrypt / decrypt)
 struct CtxThread {                    // one modulus per thread (Miller-Rabin): per-candidate rows
     static constexpr bool kMerged = false;
     static constexpr bool kScaled = false;
+    static constexpr bool kMont = false;
     const u32 *pc;
     const u32 *nrow;                  // candidate limbs
     u32 stride, limbs;
@@ -185,6 +187,7 @@ struct CtxThread {                    // one modulus per thread (Miller-Rabin): 
 // per-context BE1 image (offset column) and the vectors below, the scales into the BE2 image.
 struct CtxTc : CtxSmem {
     static constexpr bool kScaled = true;
+    static constexpr bool kMont = true;
     __device__ uint2 a1x(int i) const { return reinterpret_cast<const uint2 *>(cx + cx_a1x(K))[i]; }
     __device__ u32 qr_off() const { return cx[cx_scv(K) + 0]; }
     __device__ u32 c1_off() const { return cx[cx_scv(K) + 1]; }
@@ -720,7 +723,7 @@ __device__ __forceinline__ u32 fold_word(u32 lo, u32 hi, u32 c) {
 // compiler may issue the loads early), generic otherwise (Miller-Rabin passes shared-memory constants)
 template <class CS>
 __device__ __forceinline__ u32 mulop_ld(const u32 *p) {
-    if constexpr (CS::kScaled) return __ldcg(p);
+    if constexpr (CS::kScaled || CS::kMont) return __ldcg(p);
     else return *p;
 }
 
@@ -762,6 +765,13 @@ struct MulTc {
                         const uint2 ax = cs.a1x(i);
                         qr += xi * ax.x;
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, ax.y);
+                    } else if constexpr (CS::kMont) {   // ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i, canonical
+                        const u64 pr = (u64)a * b;
+                        const u32 t = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + i), GB(O_MINV + i));
+                        const u64 ps = (u64)t * cs.sigma(i);
+                        xi = canon(mont_red((u32)ps, (u32)(ps >> 32), GB(O_MM + i), GB(O_MINV + i)), cc);
+                        qr += xi * GB(O_A1R + i);
+                        if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
                     } else {
                         xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
                         qr += xi * GB(O_A1R + i);
@@ -780,7 +790,7 @@ struct MulTc {
                 b = sq ? a : mulop_ld<CS>(bq);
                 bq += bs;
             }
-            if constexpr (CS::kScaled) {              // t*_j 2^-32 (the epilogue constants carry 2^64)
+            if constexpr (CS::kMont) {                // t*_j 2^-32 (the epilogue constants carry the 2^32s)
                 const u64 pr = (u64)a * b;
                 S(st, K + j) = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + K + j), GB(O_MINV + K + j));
             } else {
@@ -820,6 +830,7 @@ struct MulTc {
             const u32 cj = s_be[bev_c(K) + K + j];
             u32 c1j;
             if constexpr (CS::kScaled) c1j = cs.c1nc();     // t* carries 2^-32: C1 c'
+            else if constexpr (CS::kMont) c1j = cs.c1c[j];
             else c1j = s_be[bev_C1(K) + j];
             const u64 p = (u64)S(st, K + j) * c1j;
             if (MERGED) {
@@ -871,12 +882,15 @@ struct MulTc {
                     }
                     const u32 c = s_be[bev_c(K) + K + j];
                     fold_hi(lo, hi, c, w33, c33);                  // q̂_j (merged: + Σ term) as w33 + c33·2^32
-                    if (MERGED) {   // t*_j C1_j + (w33 + c33 2^32) <= (2^32-1)(2^32-6) + 2^33 < 2^64: no carry
+                    if constexpr (MERGED) {   // t*_j C1_j + (w33 + c33 2^32) <= (2^32-1)(2^32-6) + 2^33 < 2^64: no carry
                         const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + (((u64)c33 << 32) | w33);
                         xp = red64p(p, c);
                     } else {   // ξ'_j = t*_j C1_j + q̂_j |n M^-1 λ_j|  (6.4 with a per-thread modulus)
                         const u32 q = c33 ? w33 + c : w33;
-                        const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j];
+                        u32 c1j;
+                        if constexpr (CS::kMont) c1j = cs.c1c[j];   // t* carries 2^-32
+                        else c1j = s_be[bev_C1(K) + j];
+                        const u64 p = (u64)S(st, K + j) * c1j;
                         u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
                         mac96(l2, m2, h2, q, cs.c2(j));
                         xp = red96(h2, m2, l2, c, 0);
@@ -1106,11 +1120,19 @@ __global__ void __launch_bounds__(T, MINB) k_combine(const CombineParams P) {
     const u32 *mp = P.mpq + (size_t)i * H;
     const u32 *mq = P.mpq + ((size_t)P.count + i) * H;
     u32 *mrow = P.m + (size_t)i * 2 * H;
-    // t = m_q mod p in st rows [0, H]:  m_q < 2^(32H) <= 2^32 p, subtract p·2^s for s = 32..0
+    // t = m_q mod p in st rows [0, H]:  m_q < 2^(32H) <= 2^32 p, subtract p·2^s for s = s0..0 where
+    // s0 = bits(m_q) - bits(p) (p·2^s > m_q beyond it; for RSA keys s0 <= 1, so one or two passes)
+    int bt = 0, bp = 0;
 #pragma unroll 1
     for (u32 l = 0; l <= H; l++) S(st, l) = l < H ? mq[l] : 0u;
 #pragma unroll 1
-    for (int s = 32; s >= 0; s--) {
+    for (int l = (int)H - 1; l >= 0 && !(bt && bp); l--) {
+        if (!bt && mq[l]) bt = 32 * l + 32 - __clz(mq[l]);
+        if (!bp && cs.nlimb(l)) bp = 32 * l + 32 - __clz(cs.nlimb(l));
+    }
+    const int s0 = bt > bp ? (bt - bp < 32 ? bt - bp : 32) : 0;
+#pragma unroll 1
+    for (int s = s0; s >= 0; s--) {
 #pragma unroll 1
         for (int pass = 0; pass < 2; pass++) {
             u32 br = 0;
@@ -1471,7 +1493,9 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
 struct CtxMr {                        // per-candidate constants of one thread
     static constexpr bool kMerged = false;
     static constexpr bool kScaled = false;
-    u32 sig[K];                       // σ_i in registers (the channel-product loop is fully unrolled)
+    static constexpr bool kMont = true;   // word-Montgomery reductions: σ_i held as σ_i 2^64, C1 as C1 2^32
+    u32 sig[K];                       // σ_i 2^64 mod m_i in registers (the channel-product loop is fully unrolled)
+    const u32 *c1c;                   // shared memory: |M^-1 λ_j^-1| 2^32 mod m'_j (per k)
     const u32 *c2row;                 // shared memory: c2row[j * 128] = |n M^-1 λ_j|_{m'_j}
     u32 nmv;                          // n M^-1 mod 2^32
     const u32 *nrow;
@@ -1504,7 +1528,7 @@ __device__ __forceinline__ bool x_is_nm1_t(const StTile &st, const u32 *nrow, u3
 }
 
 constexpr size_t tc_mr_smem_for(int tiles) {
-    return 4 * (size_t)(tiles * TC_ROWS + tiles * K * 128 + BEV + pad4(NCH) + 2 * pad4(K)) +
+    return 4 * (size_t)(tiles * TC_ROWS + tiles * K * 128 + BEV + pad4(NCH) + 3 * pad4(K)) +
            (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
 }
 constexpr bool tc_mr_fits(int tiles) { return tc_mr_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
@@ -1524,11 +1548,17 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     u32 *s_one = s_vec + BEV;
     u32 *s_a1c = s_one + pad4(NCH);
     u32 *s_a2c = s_a1c + pad4(K);
-    u64 *mbar = reinterpret_cast<u64 *>(s_a2c + pad4(K));
+    u32 *s_c1c = s_a2c + pad4(K);                          // |M^-1 λ_j^-1| 2^32 (word-Montgomery t*, §4g)
+    u64 *mbar = reinterpret_cast<u64 *>(s_c1c + pad4(K));
     u32 *tslot = reinterpret_cast<u32 *>(mbar + TCM);
     const u32 tid = threadIdx.x, tile = tid / 128, m = tid % 128;
     for (u32 w = tid; w < BEV; w += blockDim.x) s_vec[w] = __ldg(P.be_tab + bev_c(K) + w);
     for (u32 w = tid; w < (u32)NCH; w += blockDim.x) s_one[w] = GB(O_ONE + w);
+    __syncthreads();   // s_vec complete
+    for (u32 j = tid; j < (u32)K; j += blockDim.x) {
+        const u32 c = s_be[bev_c(K) + K + j];
+        s_c1c[j] = canon(mulmod(s_be[bev_C1(K) + j], c, c), c);
+    }
     if (TCNC)
         for (u32 i = tid; i < (u32)K; i += blockDim.x) {
             s_a1c[i] = __ldg(P.be_tab + be_img_index(i, TCNT));
@@ -1600,7 +1630,11 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
         }
         CtxMr cs;
 #pragma unroll
-        for (int k = 0; k < K; k++) cs.sig[k] = pcol[(size_t)(pc_sigma(K) + k) * cnt];
+        for (int k = 0; k < K; k++) {   // σ_k 2^64 ≡ σ_k c_k² (mod m_k)
+            const u32 c = GB(O_C + k);
+            cs.sig[k] = mulmod(mulmod(pcol[(size_t)(pc_sigma(K) + k) * cnt], c, c), c, c);
+        }
+        cs.c1c = s_c1c;
 #pragma unroll 1
         for (int j = 0; j < K; j++) c2rows[j * 128] = pcol[(size_t)(pc_c2(K) + j) * cnt];
         cs.c2row = c2rows;
@@ -1629,7 +1663,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                 if (u == 0) {
 #pragma unroll 1
                     for (int c = 0; c < NCH; c++) S(st, c) = r2[(size_t)c * cnt];
-                    bp = s_one; bs = 1;
+                    bp = P.one_g; bs = 1;
                 } else if (u == 1) {
                     to_rns(st, a, 1, L, true, P.pow_tab);
                     bp = r2; bs = (u32)cnt;
@@ -1667,7 +1701,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
 #pragma unroll 1
                     for (int c = 0; c < NCH; c++) stash[(size_t)c * tst] = S(st, c);
                 }
-                mm(st, s_one, check ? 1u : 0u, !check, cs);
+                mm(st, P.one_g, check ? 1u : 0u, !check, cs);
                 if (check) {
                     from_rns(st, cs, P.mpl);
                     const bool one = x_is_one_t(st), nm1 = x_is_nm1_t(st, nrow, L);
