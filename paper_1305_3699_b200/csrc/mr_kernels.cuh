@@ -1169,29 +1169,20 @@ __global__ void __launch_bounds__(T, MINB) k_combine(const CombineParams P) {
     to_rns(st, mrow, 1, H, true, P.pow_tab);
     mont_mul(st, s_cx + cx_qinvr(K), 1, false, cs, s_be);
     from_rns(st, cs, P.mpl);
-    // m = m_q + q · h  (schoolbook, H x H limbs)
+    // m = m_q + q · h  (schoolbook by product scanning: column sums in a 96-bit register accumulator, q
+    // broadcast through L1, h in shared-memory rows; each output limb is stored once)
+    const bool bad = P.status && P.status[i] != 0;
+    u32 lo = 0, mi = 0, hi = 0;
 #pragma unroll 1
-    for (u32 l = 0; l < 2 * H; l++) mrow[l] = l < H ? mq[l] : 0u;
-#pragma unroll 1
-    for (u32 r = 0; r < H; r++) {
-        const u32 qr = P.q[r];
-        u32 carry = 0;
-#pragma unroll 1
-        for (u32 l = 0; l < H; l++) {
-            const u64 v = (u64)qr * S(st, l) + mrow[r + l] + carry;
-            mrow[r + l] = (u32)v;
-            carry = (u32)(v >> 32);
-        }
-#pragma unroll 1
-        for (u32 l = r + H; l < 2 * H && carry; l++) {
-            const u64 v = (u64)mrow[l] + carry;
-            mrow[l] = (u32)v;
-            carry = (u32)(v >> 32);
-        }
-    }
-    if (P.status && P.status[i] != 0) {
-#pragma unroll 1
-        for (u32 l = 0; l < 2 * H; l++) mrow[l] = 0;
+    for (u32 col = 0; col < 2 * H; col++) {
+        if (col < H) mac96(lo, mi, hi, mq[col], 1u);
+        const u32 r0 = col >= H ? col - H + 1 : 0u, r1 = col < H ? col : H - 1;
+#pragma unroll 4
+        for (u32 r = r0; r <= r1; r++) mac96(lo, mi, hi, __ldg(P.q + r), S(st, col - r));
+        mrow[col] = bad ? 0u : lo;
+        lo = mi;
+        mi = hi;
+        hi = 0;
     }
 }
 
