@@ -345,6 +345,7 @@ def run_ours(args, world, rank, local):
                                    "frac": i8_achieved / i8_peak,
                                    "peak_source": "MEASURED_PEAKS bf16_tflops x 2 (nominal i8:bf16 4.5:2.25)"}
                      if tensor else None,
+                     "cuda_core_pipes_ncu": ncu_pipes(tensor, count),
                      "combine_ms_per_launch": ms_c.value / max(1, n_c.value),
                      "imad_eq_per_decrypt": per_dec,
                      "frac_at_median_clock": (achieved / peak_imad_eq_per_s(clocks["sm_mhz"]))
@@ -360,15 +361,29 @@ def run_ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
-def ncu_traffic(tensor: bool, count: int):
-    """DRAM bytes per launch of the ladder kernel from the committed ncu --set full capture of the same
-    configuration (profiles/ncu_traffic.json), else None."""
+def ncu_record(tensor: bool, count: int):
+    """the committed ncu --set full summary of the ladder kernel in this configuration
+    (profiles/ncu_traffic.json), else None."""
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as f:
-            rec = json.load(f).get(f"{'k_modexp_tc' if tensor else 'k_modexp'}/c2/{count}")
+            return json.load(f).get(f"{'k_modexp_tc' if tensor else 'k_modexp'}/c2/{count}")
     except (OSError, ValueError):
         return None
+
+
+def ncu_traffic(tensor: bool, count: int):
+    """DRAM bytes (read + write) per launch of the ladder kernel from the committed ncu capture."""
+    rec = ncu_record(tensor, count)
     return None if rec is None else rec["dram_bytes_read"] + rec["dram_bytes_write"]
+
+
+def ncu_pipes(tensor: bool, count: int):
+    """utilisation of the binding CUDA-core resources from the same capture (issue slots, FMA-heavy pipe)."""
+    rec = ncu_record(tensor, count)
+    if rec is None or "issue_active_pct" not in rec:
+        return None
+    return {k: rec[k] for k in ("issue_active_pct", "fmaheavy_pipe_pct", "alu_pipe_pct", "tensor_imma_pct",
+                                "warp_instructions_per_multiplication", "source") if k in rec}
 
 
 def cpu_baseline(key, budget_s: float = 10.0):

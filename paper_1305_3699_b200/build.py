@@ -70,7 +70,9 @@ def build(force: bool = False, jobs: int | None = None) -> str:
         objs.append(host_obj)
         if force or _stale(host_obj, [host_src] + deps):
             steps.append((["g++", "-O2", "-std=c++17", "-fPIC", "-Wall", "-fvisibility=hidden",
-                           "-I", os.path.join(CUDA, "include"), "-c", host_src, "-o", host_obj], host_obj + ".log"))
+                           "-I", os.path.join(CUDA, "include"), "-c", host_src, "-o", host_obj]
+                          + [d for d in os.environ.get("MR_NVCC_DEFS", "").split() if d.startswith("-D")],
+                          host_obj + ".log"))
     if steps:
         jobs = jobs or min(len(steps), os.cpu_count() or 4)
         with cf.ThreadPoolExecutor(jobs) as ex:

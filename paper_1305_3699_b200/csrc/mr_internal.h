@@ -118,8 +118,11 @@ __host__ __device__ constexpr u32 tc_kp(u32 k) { return (4 * k + 31) & ~31u; }  
 // outputs of each base extension computed on the tensor core; for k = 33 the 33rd output runs on the
 // CUDA cores so that N = 128 columns and four 128-message tiles fit the 512 TMEM columns of an SM;
 // for k = 65 the 65th, so that N = 256 (the largest MMA N) covers the other 64
+#ifndef MR_TC_NT33
+#define MR_TC_NT33 32       // A/B hook: 33 puts every k = 33 output on the tensor core (N = 144, 3 tiles per SM)
+#endif
 __host__ __device__ constexpr u32 tc_nt(u32 k) {
-    return (4 * k > 128 && 4 * k <= 136) ? 32 : ((4 * k > 256 && 4 * k <= 264) ? 64 : k);
+    return (4 * k > 128 && 4 * k <= 136) ? MR_TC_NT33 : ((4 * k > 256 && 4 * k <= 264) ? 64 : k);
 }
 __host__ __device__ constexpr u32 tc_np(u32 k) { return (4 * tc_nt(k) + 15) & ~15u; }  // N rows, multiple of 16
 // CTA-pair mode: the two B images of k = 65 (2 x 72 KB) do not fit one CTA next to two

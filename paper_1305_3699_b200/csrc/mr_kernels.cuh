@@ -676,13 +676,33 @@ __device__ __forceinline__ void tc_wait(TcTile &t) {
 }
 
 __device__ __forceinline__ void tmem_ld16_nowait(u32 taddr, u32 (&v)[16]) {
+    // no memory clobber: volatile keeps it after tc_wait, tmem_wait_ld_regs orders the uses of v
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                    "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                 : "r"(taddr)
-                 : "memory");
+                 : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait for the TMEM loads of vv with the loaded registers as in/out operands instead of a memory clobber: the
+// uses of vv stay after the wait, and independent shared-memory loads (epilogue constants, B' state) may be
+// scheduled above it
+#ifndef MR_TMEM_WAIT_REGS
+#define MR_TMEM_WAIT_REGS 1
+#endif
+__device__ __forceinline__ void tmem_wait_ld_regs(u32 (&v)[2][16]) {
+#if MR_TMEM_WAIT_REGS
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0][0]), "+r"(v[0][1]), "+r"(v[0][2]), "+r"(v[0][3]), "+r"(v[0][4]), "+r"(v[0][5]), "+r"(v[0][6]),
+                   "+r"(v[0][7]), "+r"(v[0][8]), "+r"(v[0][9]), "+r"(v[0][10]), "+r"(v[0][11]), "+r"(v[0][12]),
+                   "+r"(v[0][13]), "+r"(v[0][14]), "+r"(v[0][15]), "+r"(v[1][0]), "+r"(v[1][1]), "+r"(v[1][2]),
+                   "+r"(v[1][3]), "+r"(v[1][4]), "+r"(v[1][5]), "+r"(v[1][6]), "+r"(v[1][7]), "+r"(v[1][8]),
+                   "+r"(v[1][9]), "+r"(v[1][10]), "+r"(v[1][11]), "+r"(v[1][12]), "+r"(v[1][13]), "+r"(v[1][14]),
+                   "+r"(v[1][15]));
+#else
+    (void)v;
+    tmem_wait_ld();
+#endif
+}
 __device__ __forceinline__ void tmem_ld16(u32 taddr, u32 (&v)[16]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
@@ -854,7 +874,7 @@ struct MulTc {
           u32 vv[2][16];                              // two TMEM loads in flight, one wait
           tmem_ld16_nowait(t.tmem + lane_base + 16 * g0, vv[0]);
           if (g0 + 1 < NG) tmem_ld16_nowait(t.tmem + lane_base + 16 * (g0 + 1), vv[1]);
-          tmem_wait_ld();
+          tmem_wait_ld_regs(vv);
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int g = g0 + h;
@@ -935,7 +955,7 @@ struct MulTc {
           u32 vv[2][16];
           tmem_ld16_nowait(t.tmem + lane_base + 16 * g0, vv[0]);
           if (g0 + 1 < NG) tmem_ld16_nowait(t.tmem + lane_base + 16 * (g0 + 1), vv[1]);
-          tmem_wait_ld();
+          tmem_wait_ld_regs(vv);
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int g = g0 + h;
