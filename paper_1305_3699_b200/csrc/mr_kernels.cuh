@@ -63,6 +63,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_RED_VARIANT
 #define MR_RED_VARIANT 2
 #endif
+#ifndef MR_CHAN_FUSE
+#define MR_CHAN_FUSE 0      // A/B hook: interleave the B' channel products with the B chunks
+#endif
 #ifndef MR_PF_L1
 #define MR_PF_L1 0          // A/B hook: prefetch the next window-table operand into L1 instead of L2
 #endif
@@ -801,9 +804,33 @@ struct MulTc {
                 }
             }
             *chunk = make_uint4(w[0], w[1], w[2], w[3]);
+#if MR_CHAN_FUSE
+            // B' channels of the same index range, interleaved with the B chunk (more independent chains)
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int j = 4 * c + q;
+                if (j < K) {
+                    const u32 a = S(st, K + j);
+                    u32 b = a;
+                    if (!SQ) b = sq ? a : mulop_ld<CS>(bp + (size_t)(K + j) * bs);
+                    if constexpr (CS::kMont) {
+                        const u64 pr = (u64)a * b;
+                        S(st, K + j) = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + K + j), GB(O_MINV + K + j));
+                    } else {
+                        S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
+                    }
+                }
+            }
+#endif
         }
+#if MR_CHAN_FUSE
+        bq = bp + (size_t)(2 * K) * bs;
+#pragma unroll
+        for (int j = 0; j < 0; j++) {
+#else
 #pragma unroll
         for (int j = 0; j < K; j++) {
+#endif
             const u32 a = S(st, K + j);
             u32 b = a;
             if (!SQ) {
