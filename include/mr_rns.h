@@ -58,8 +58,10 @@ enum { MR_COMPOSITE = 0, MR_PROBABLY_PRIME = 1, MR_FACTOR = 2 }; /* Miller-Rabin
  *    time" (§3.1).
  * modulus: HOST, `limbs` limbs, odd, N >= 3.
  * k: channels per base.  0 = auto = the smallest compiled k with 4(k+3)^2 N < M and
- *    4(k+3) N < M' (e.g. 33 for 1024-bit, 65 for 2048-bit N).  A nonzero k is rounded up to the
- *    next compiled k (see mr_rns_supported_k); below the bound -> MR_ERR_CAPACITY.
+ *    4(k+3) N < M' (e.g. 33 for 1024-bit, 65 for 2048-bit, 257 for 8192-bit, 505 for 16,128-bit N).
+ *    A nonzero k is rounded up to the next compiled k (see mr_rns_supported_k); below the bound ->
+ *    MR_ERR_CAPACITY.  k <= 65: tensor-core base extensions; 97, 129: IMAD thread-per-message;
+ *    257, 505: the wide-operand channels-on-threads kernel ("keys up to 16,128 bits"; §8(f)).
  * device: CUDA ordinal that will run every batch call on this context.
  * On success *out owns host and device memory until mr_rns_ctx_destroy.
  * Errors: MR_ERR_ARG, MR_ERR_EVEN_MODULUS, MR_ERR_NOT_COPRIME, MR_ERR_CAPACITY, MR_ERR_CUDA,
@@ -101,7 +103,8 @@ int mr_rsa_encrypt_batch(const mr_rns_ctx *n_ctx, const uint32_t *e, size_t e_li
  * p, q, d_p = d mod (p-1), d_q = d mod (q-1), q_inv = q^-1 mod p: HOST, half_limbs limbs each.
  * The two half contexts share one base pair; k_half = 0 picks it automatically.
  * Ciphertexts and plaintexts of mr_rsa_decrypt_batch have 2*half_limbs limbs and must be < p*q.
- * Errors as mr_rns_ctx_create, plus MR_ERR_ARG if p == q or q_inv*q != 1 mod p.
+ * Errors as mr_rns_ctx_create, plus MR_ERR_ARG if p == q or q_inv*q != 1 mod p, and MR_ERR_CAPACITY
+ * when a half needs the wide kernel (p or q above ~4,070 bits: no wide CRT recombination yet).
  * ------------------------------------------------------------------------------------------ */
 int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, size_t half_limbs,
                        const uint32_t *d_p, const uint32_t *d_q, const uint32_t *q_inv, int k_half, int device);
@@ -119,7 +122,8 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
  *  a Miller-Rabin test with a user-parameterized number of iterations", §3.2; HAC 4.24).
  * d_n: DEVICE [count][limbs] candidates; d_bases: DEVICE [count][rounds][limbs], each in [2, n-2]
  *      (bases are inputs, reading R13).
- * k: channels (0 = auto from limbs).  d_verdict: DEVICE uint8 [count] = MR_COMPOSITE |
+ * k: channels (0 = auto from limbs; candidates up to 128 limbs, else MR_ERR_CAPACITY).
+ * d_verdict: DEVICE uint8 [count] = MR_COMPOSITE |
  * MR_PROBABLY_PRIME | MR_FACTOR (n > 2^32 divisible by a prime of B ∪ B', R14).
  * d_witness_round: DEVICE int16 [count] or NULL: first round that proved compositeness, else -1.
  * d_status: DEVICE int32 [count] or NULL: MR_ERR_RANGE if n even, n < 5 or a base outside

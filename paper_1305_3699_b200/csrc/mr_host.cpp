@@ -30,6 +30,10 @@ MR_DECLARE_K(65)
 MR_DECLARE_K(97)
 MR_DECLARE_K(129)
 
+size_t wide_smem_bytes(u32 k);
+int wide_messages_per_cta();
+int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, void *stream);
+
 static const KernelSet &kernel_set_for(int k) {
     static std::vector<KernelSet> sets = {kernels_k1(),  kernels_k2(),  kernels_k3(),  kernels_k5(), kernels_k9(),
                                           kernels_k17(), kernels_k33(), kernels_k49(), kernels_k65(),
@@ -38,7 +42,8 @@ static const KernelSet &kernel_set_for(int k) {
         if (s.k == k) return s;
     return sets[0];
 }
-static const int kSupportedK[] = {1, 2, 3, 5, 9, 17, 33, 49, 65, 97, 129};
+// k > 129: the wide-operand kernel (mr_wide.cu, runtime k): 8192-bit (257) and 16,128-bit (505) moduli
+static const int kSupportedK[] = {1, 2, 3, 5, 9, 17, 33, 49, 65, 97, 129, 257, 505};
 static const int kNumK = sizeof(kSupportedK) / sizeof(kSupportedK[0]);
 
 // ------------------------------------------------------------------ host positional helpers
@@ -338,7 +343,45 @@ struct DevBase {
     u32 *d_tcb2 = nullptr;     // tensor-core BE2 image (k <= 64, and k = 65 in CTA-pair mode)
     u32 *d_tcb1u = nullptr;    // tensor-core unmerged BE1 image (Miller-Rabin, per-thread modulus)
     u32 *d_one = nullptr;      // RNS image of 1 (2k+1 words; Miller-Rabin tensor path multiplicand)
+    u32 *d_wide = nullptr;     // wide-operand table (k > 129, mr_internal.h wide_layout)
 };
+
+// per-k table of the wide kernel (mr_internal.h WideLayout): word-Montgomery constants with their 2^32
+// factors folded in
+static std::vector<u32> build_wide_table(const Base &b) {
+    const int k = b.k;
+    const BaseLayout L = base_layout(k);
+    const WideLayout W = wide_layout(k);
+    const u32 *f = b.flat.data();
+    std::vector<u32> t(W.words, 0);
+    for (int ch = 0; ch < 2 * k; ch++) {
+        const u32 m = ch < k ? b.B[ch] : b.Bp[ch - k];
+        t[W.mm + ch] = m;
+        t[W.minv + ch] = 0u - inv32(m);
+        t[W.r32 + ch] = (u32)((1ull << 32) % m);
+    }
+    for (int j = 0; j < k; j++) {
+        const u32 m = b.Bp[j], r = t[W.r32 + k + j];
+        t[W.xw + j] = mulm(mulm(f[L.C1 + j], r, m), r, m);
+        t[W.a2r + j] = f[L.A2r + j];
+    }
+    for (int i = 0; i < k; i++) {
+        t[W.a1r + i] = f[L.A1r + i];
+        t[W.pinw + i] = mulm(f[L.pin + i], t[W.r32 + i], b.B[i]);
+    }
+    t[W.misc + 0] = f[L.misc + 0];
+    t[W.misc + 1] = f[L.misc + 1];
+    for (int j = 0; j < k; j++)
+        for (int i = 0; i < k; i++) t[W.a2w + (size_t)j * k + i] = mulm(f[L.A2 + j * k + i], t[W.r32 + i], b.B[i]);
+    for (int l = 0; l < k; l++)
+        for (int ch = 0; ch < 2 * k; ch++) {
+            const u32 m = ch < k ? b.B[ch] : b.Bp[ch - k];
+            t[W.pow + (size_t)l * 2 * k + ch] = mulm(b.pow[(size_t)l * 2 * k + ch], t[W.r32 + ch], m);
+        }
+    for (size_t w = 0; w < (size_t)k * (k + 1); w++) t[W.mpl + w] = f[L.MpL + w];
+    for (int l = 0; l <= k; l++) t[W.nmp + l] = f[L.NMp + l];
+    return t;
+}
 static std::map<std::pair<int, int>, DevBase> g_devbases;
 
 static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **d_be) {
@@ -359,9 +402,18 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     }
+    DevBase db;
+    if (is_wide((u32)k)) {   // wide-operand kernel: one table in HBM, no constant bank, no shared-memory images
+        const std::vector<u32> t = build_wide_table(b);
+        if (cudaMalloc(&db.d_wide, t.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMemcpy(db.d_wide, t.data(), t.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
+        g_devbases[key] = db;
+        *d_pow = nullptr;
+        *d_be = nullptr;
+        return MR_OK;
+    }
     const KernelSet &ks = kernel_set_for(k);
     if (ks.upload_base(b.flat.data(), device) != 0) return MR_ERR_CUDA;
-    DevBase db;
     if (cudaMalloc(&db.d_pow, b.pow.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
     if (cudaMemcpy(db.d_pow, b.pow.data(), b.pow.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
         return MR_ERR_CUDA;
@@ -432,6 +484,7 @@ struct mr_rns_ctx {
     const u32 *d_be = nullptr;
     const u32 *d_tcb2 = nullptr;
     const u32 *d_mpl = nullptr;
+    const u32 *d_wide = nullptr;   // wide-operand table of this k (k > 129)
     std::vector<u32> h_cx;
     std::mutex mu;             // guards the program cache
     std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program
@@ -576,6 +629,22 @@ static bool fill_tc_scaled(const Base &b, u32 *x) {
     return true;
 }
 
+// per-context part of the wide kernel's constants (mr_internal.h wide_cx_*): σ_i 2^64 mod m_i and
+// A1'[i][j] 2^32 mod m'_j, A1' = |M_i|_{m'_j} |N M^-1 λ_j| (6.4 merged into BE1, row-major)
+static void fill_wide_ctx(const Base &b, u32 *x) {
+    const int k = b.k;
+    const u32 *A1 = b.flat.data() + base_layout(k).A1;
+    u32 *w = x + cx_words(k);
+    for (int i = 0; i < k; i++) {
+        const u32 m = b.B[i], r = (u32)((1ull << 32) % m);
+        w[wide_cx_sig(k) + i] = mulm(mulm(x[cx_sigma(k) + i], r, m), r, m);
+    }
+    for (int j = 0; j < k; j++) {
+        const u32 m = b.Bp[j], r = (u32)((1ull << 32) % m), nu = mulm(x[cx_c2(k) + j], r, m);
+        for (int i = 0; i < k; i++) w[wide_cx_a1(k) + (size_t)i * k + j] = mulm(A1[i * k + j], nu, m);
+    }
+}
+
 static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, int device, const Big &in_bound,
                      size_t in_limbs, const Big *khi_shift_limbs_half /* CRT: half limbs */, const Big *qinv) {
     *out = nullptr;
@@ -609,15 +678,22 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->bits = bits(N);
     c->N = N;
     const size_t tc_words = tc_ok(k) ? tc_bbytes(k) / 4 : 0;
-    c->h_cx.assign(cx_words(k) + be_half_words(k) + 2 * tc_words, 0);
-    fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
-    fill_merged_be1(b, c->h_cx.data() + cx_words(k), c->h_cx.data());
     int rc = MR_OK;
+    if (is_wide((u32)k)) {   // cx block + wide section (σ 2^64, A1' 2^32 row-major)
+        c->h_cx.assign(cx_words(k) + wide_cx_words(k), 0);
+        fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
+        fill_wide_ctx(b, c->h_cx.data());
+    } else {
+        c->h_cx.assign(cx_words(k) + be_half_words(k) + 2 * tc_words, 0);
+        fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
+        fill_merged_be1(b, c->h_cx.data() + cx_words(k), c->h_cx.data());
+    }
     if (tc_ok(k) && !fill_tc_scaled(b, c->h_cx.data())) rc = MR_ERR_ARG;   // not reachable for the R1 bases
     if (rc == MR_OK) rc = ensure_device_base(k, device, &c->d_pow, &c->d_be);
     if (rc == MR_OK) {
         c->d_tcb2 = g_devbases[std::make_pair(device, k)].d_tcb2;
         c->d_mpl = g_devbases[std::make_pair(device, k)].d_mpl;
+        c->d_wide = g_devbases[std::make_pair(device, k)].d_wide;
     }
     if (rc != MR_OK) { delete c; return rc; }
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return MR_ERR_CUDA; }
@@ -833,12 +909,57 @@ static bool tensor_path_enabled() {
     return !(e && e[0] == '1');
 }
 
+// wide-operand ladders (k > 129): 16 messages per CTA, one CTA per 16 messages and context
+static int launch_ladders_wide(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x,
+                               size_t in_limbs, size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status,
+                               void *stream) {
+    const mr_rns_ctx *c0 = ctxs[0];
+    cudaStream_t st = (cudaStream_t)stream;
+    const u32 MBm = (u32)wide_messages_per_cta();
+    const u32 ctas0 = (u32)((count + MBm - 1) / MBm);
+    const u32 jobs_total = ctas0 * MBm * nctx;
+    int w = 1;
+    for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
+    const size_t nch = 2 * (size_t)c0->k + 1;
+    const size_t rows = std::max<size_t>((size_t)table_slots(w) * nch, 3 * ((size_t)c0->k + 1));   // + exit scratch
+    u32 *d_table = nullptr;
+    if (cudaMallocAsync(&d_table, rows * jobs_total * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    ModexpParams P;
+    memset(&P, 0, sizeof P);
+    for (int i = 0; i < 2; i++) {
+        const int s = i < nctx ? i : nctx - 1;
+        P.ctx[i] = ctxs[s]->d_cx;
+        P.prog[i] = progs[s].d_ops;
+        P.nops[i] = progs[s].nops;
+    }
+    P.ctas0 = ctas0;
+    P.count = (u32)count;
+    P.x = d_x;
+    P.in_limbs = (u32)in_limbs;
+    P.half = (u32)half;
+    P.y = d_y;
+    P.out_limbs = (u32)out_limbs;
+    P.out_stride = count * out_limbs;
+    P.status = d_status;
+    P.table = d_table;
+    P.jobs_total = jobs_total;
+    int rc = timed_launch(0, st, [&] {
+                 return launch_modexp_wide(P, ctas0 * nctx, c0->d_wide, (u32)c0->k, stream);
+             }) == 0
+                 ? MR_OK
+                 : MR_ERR_CUDA;
+    cudaFreeAsync(d_table, st);
+    return rc;
+}
+
 static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x, size_t in_limbs,
                           size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status, void *stream) {
     const mr_rns_ctx *c0 = ctxs[0];
     const KernelSet &ks = kernel_set_for(c0->k);
     if (cudaSetDevice(c0->device) != cudaSuccess) return MR_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
+    if (is_wide((u32)c0->k)) return launch_ladders_wide(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count,
+                                                        d_status, stream);
     const bool use_tc = ks.launch_modexp_tc && c0->d_tcb2 && tensor_path_enabled();
     // IMAD path: one CTA per T messages; tensor path: ctas0 = 128-message tile-jobs per context,
     // run by Gc persistent CTAs per context (one per SM share)
@@ -954,6 +1075,7 @@ int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, 
         }
         k = auto_k(big, kmin);
         if (k < 0) return MR_ERR_CAPACITY;
+        if (is_wide((u32)k)) return MR_ERR_CAPACITY;   // CRT halves above 4096 bits: no wide recombination yet
     }
     Big hl{(u32)half_limbs};
     mr_rsa_priv *pr = new (std::nothrow) mr_rsa_priv;
@@ -1057,7 +1179,7 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
             if (kmin < 0) return MR_ERR_ARG;
         }
         kk = auto_k(top, kmin);
-        if (kk < 0) return MR_ERR_CAPACITY;
+        if (kk < 0 || is_wide((u32)kk)) return MR_ERR_CAPACITY;   // Miller-Rabin: candidates up to 4096 bits
         if ((int)limbs > kk - 1) return MR_ERR_CAPACITY;
         int rc = ensure_device_base(kk, device, &d_pow, &d_be);
         if (rc != MR_OK) return rc;
@@ -1150,6 +1272,18 @@ int mr_internal_pow_table(int k, uint32_t *out, size_t cap) {
 
 // builds the context block of modulus N for a given k (no device work); returns its word count or
 // a negative MR_* error code
+// test hook: the wide-operand per-k table (mr_internal.h WideLayout) without a device
+int mr_internal_wide_table(int k, uint32_t *out, size_t cap) {
+    if (!is_wide((u32)k)) return -MR_ERR_ARG;
+    bool ok = false;
+    for (int i = 0; i < kNumK; i++) ok |= kSupportedK[i] == k;
+    if (!ok) return -MR_ERR_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const std::vector<u32> t = build_wide_table(base_for(k));
+    if (out) memcpy(out, t.data(), std::min(cap, t.size()) * 4);
+    return (int)t.size();
+}
+
 int mr_internal_ctx_table(const uint32_t *modulus, size_t limbs, int k, uint32_t *out, size_t cap) {
     Big N = big_of(modulus, limbs);
     if (N.empty() || !(N[0] & 1)) return -MR_ERR_EVEN_MODULUS;

@@ -138,6 +138,46 @@ __host__ __device__ constexpr u32 tc_bbytes(u32 k) { return tc_np(k) * tc_kp(k);
 __host__ __device__ constexpr u32 tc_abytes(u32 k) { return 128 * tc_kp(k); }        // one A tile
 
 // ---------------------------------------------------------------------------------------------
+// Wide-operand kernel (mr_wide.cu, k > 129: channels on threads, 16 messages per CTA).
+// Per-k table in HBM (word Montgomery reductions: the 2^-32 factors are folded into the constants):
+// ---------------------------------------------------------------------------------------------
+struct WideLayout {
+    u32 mm, minv, r32;        // [2k] m, -m^-1 mod 2^32, 2^32 mod m   (B then B')
+    u32 xw;                   // [k]  |M^-1 λ_j^-1| 2^64 mod m'_j       (t*_j carries 2^-32 twice)
+    u32 a1r, a2r;             // [k]  |M_i|_{2^32}, |M'_j|_{2^32}
+    u32 pinw;                 // [k]  (m_i - |M'|_{m_i}) 2^32 mod m_i
+    u32 misc;                 // [4]  M^-1 mod 2^32, M'^-1 mod 2^32
+    u32 a2w;                  // [k][k] row j, column i: |M'_j|_{m_i} 2^32 mod m_i
+    u32 pow;                  // [k][2k] |2^(32 l) 2^32|_{m_c} (B' × λ_j)
+    u32 mpl;                  // [k][k+1] M'_j limbs
+    u32 nmp;                  // [k+1] 2^(32(k+1)) - M' limbs
+    u32 words;
+};
+__host__ __device__ constexpr WideLayout wide_layout(u32 k) {
+    WideLayout w{};
+    w.mm = 0;
+    w.minv = w.mm + 2 * k;
+    w.r32 = w.minv + 2 * k;
+    w.xw = w.r32 + 2 * k;
+    w.a1r = w.xw + k;
+    w.a2r = w.a1r + k;
+    w.pinw = w.a2r + k;
+    w.misc = w.pinw + k;
+    w.a2w = w.misc + 4;
+    w.pow = w.a2w + k * k;
+    w.mpl = w.pow + 2 * k * k;
+    w.nmp = w.mpl + k * (k + 1);
+    w.words = w.nmp + k + 1;
+    return w;
+}
+// per-context wide section, after the cx block: σ_i 2^64 mod m_i [k], then A1'[i][j] 2^32 mod m'_j [k][k]
+// (A1' = |M_i|_{m'_j} |N M^-1 λ_j|, row-major: coalesced over j)
+__host__ __device__ constexpr u32 wide_cx_sig(u32 k) { return 0; }
+__host__ __device__ constexpr u32 wide_cx_a1(u32 k) { return k; }
+__host__ __device__ constexpr u32 wide_cx_words(u32 k) { return k + k * k; }
+__host__ __device__ constexpr bool is_wide(u32 k) { return k > 129; }
+
+// ---------------------------------------------------------------------------------------------
 // Exponentiation "program": one u64 op per Montgomery multiplication step, executed by a single
 // inlined mont_mul inside the kernel's interpreter loop (keeps one copy of the unrolled code).
 // ---------------------------------------------------------------------------------------------

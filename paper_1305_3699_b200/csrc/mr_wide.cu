@@ -1,0 +1,423 @@
+// mr_wide.cu — wide-operand RNS Montgomery modexp (8192-bit moduli, keys up to
+// 16,128 bits; "up to 16,128-bit long").  DESIGN.md §4h.
+//
+// For k = 257 and 505 channels per base the per-message state (2k+1 words) and the base-extension matrices
+// (k² words each: 264 KB / 1 MB) no longer fit the thread-per-message kernels, so this kernel maps
+// CHANNELS to threads ("channels-on-lanes", the paper's own mapping) and register-blocks MB = 16
+// messages per CTA: every thread owns output channels and accumulates them for the CTA's 16 messages at
+// once, so each constant-matrix word read from L2 serves 16 multiply-accumulates.
+//   state   st[ch][msg] in shared memory (2k+1 rows of 16 words)
+//   BE1     q̂_j = Σ_i ξ_i A1'[i][j]   thread per output j, A1' row-major in HBM (coalesced over j),
+//                                     ξ_i broadcast from shared memory (LDS.128)
+//   BE2     r_i = Σ_j ξ'_j A2[j][i] + α' (m_i - |M'|_{m_i})   same shape
+// Every channel product and every 96-bit column sum is reduced with a word Montgomery reduction; the
+// resulting 2^-32 factors are absorbed into the host-built constants (A1' and A2 × 2^32, σ and C1 × 2^64,
+// powers × 2^32), so any odd 32-bit modulus works (no bound on c = 2^32 mod m).  Runtime k: one kernel
+// for every wide k.  Plain (unscaled) residues; the exit is the same CRT-with-extra-modulus reconstruction
+// as mr_kernels.cuh from_rns, done cooperatively (column sums by thread, carries by one thread per message).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "mr_internal.h"
+
+namespace mr {
+namespace {
+
+constexpr int MB = 16;                 // messages per CTA (register-blocked)
+constexpr int NTMAX = 512;             // threads per CTA (runtime: 32 * ceil((k+1)/32), <= 512)
+
+__device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) {
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32 %2, %2, 0;"
+        : "+r"(lo), "+r"(mid), "+r"(hi)
+        : "r"(x), "r"(y));
+}
+
+// T = thi 2^32 + tlo -> T 2^-32 mod m, lazy in [0, 2^32) (as mr_kernels.cuh mont_red; valid for any odd m)
+__device__ __forceinline__ u32 mont_red(u32 tlo, u32 thi, u32 m, u32 minv) {
+    const u32 q = tlo * minv;
+    [[maybe_unused]] u32 ulo;
+    u32 uhi, cy;
+    asm("mad.lo.cc.u32 %0, %3, %4, %5;\n\tmadc.hi.cc.u32 %1, %3, %4, %6;\n\taddc.u32 %2, 0, 0;"
+        : "=r"(ulo), "=r"(uhi), "=r"(cy)
+        : "r"(q), "r"(m), "r"(tlo), "r"(thi));
+    return cy ? uhi - m : uhi;
+}
+// lazy a + b mod m (a, b < 2^32): each 2^32 carried out is worth r32 = 2^32 mod m; after one fold the value
+// is < 2^32 + r32, and a second carry leaves a low word < r32, so the last add cannot wrap
+__device__ __forceinline__ u32 addmod_lazy(u32 a, u32 b, u32 r32) {
+    const u64 s = (u64)a + b;
+    const u64 t = (u64)(u32)s + (s >> 32) * r32;
+    return (u32)t + (u32)(t >> 32) * r32;
+}
+// (hi 2^64 + mid 2^32 + lo) 2^-32 mod m, hi < 2^9:  mont(mid:lo) + hi r32  (hi r32 < 2^9 2^16)
+__device__ __forceinline__ u32 red96_mont(u32 hi, u32 mid, u32 lo, u32 m, u32 minv, u32 r32) {
+    const u32 r = mont_red(lo, mid, m, minv);
+    const u32 t = hi * r32;
+    const u32 s = r + t;
+    return s < r ? s + r32 : s;
+}
+
+struct WideArgs {
+    const u32 *tab;                    // per-k wide table (mr_internal.h wide_*)
+    u32 k;
+    u32 nt;                            // threads per CTA
+};
+
+__device__ __forceinline__ u32 &ST(u32 *st, u32 ch, u32 msg) { return st[ch * MB + msg]; }
+
+// acc[q] += Σ_{i < n} xs[i * MB + q] · coef[i * cstride]  for the CTA's MB messages (96-bit accumulators).
+// The constants stream from L2/HBM: PF of them are loaded one chunk ahead so their latency overlaps the
+// previous chunk's multiply-accumulates (the loop is otherwise bound by L2 latency).
+constexpr int PF = 8;
+__device__ __forceinline__ void dot_mb(const u32 *__restrict__ coef, size_t cstride, const u32 *xs, u32 n,
+                                       u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
+    u32 cur[PF], nxt[PF];
+#pragma unroll
+    for (int p = 0; p < PF; p++) cur[p] = (u32)p < n ? __ldg(coef + (size_t)p * cstride) : 0u;
+#pragma unroll 1
+    for (u32 i0 = 0; i0 < n; i0 += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; p++) {
+            const u32 i = i0 + PF + p;
+            nxt[p] = i < n ? __ldg(coef + (size_t)i * cstride) : 0u;
+        }
+#pragma unroll
+        for (int p = 0; p < PF; p++) {
+            if (i0 + p < n) {
+                const uint4 *x = reinterpret_cast<const uint4 *>(xs + (i0 + p) * MB);
+                const u32 c = cur[p];
+#pragma unroll
+                for (int v4 = 0; v4 < MB / 4; v4++) {
+                    const uint4 xv = x[v4];
+                    mac96(lo[4 * v4 + 0], mi[4 * v4 + 0], hi[4 * v4 + 0], xv.x, c);
+                    mac96(lo[4 * v4 + 1], mi[4 * v4 + 1], hi[4 * v4 + 1], xv.y, c);
+                    mac96(lo[4 * v4 + 2], mi[4 * v4 + 2], hi[4 * v4 + 2], xv.z, c);
+                    mac96(lo[4 * v4 + 3], mi[4 * v4 + 3], hi[4 * v4 + 3], xv.w, c);
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < PF; p++) cur[p] = nxt[p];
+    }
+}
+
+// block-wide Σ over threads of v[msg] (MB values): warp shuffles, then one partial per warp in red[w][msg];
+// the caller syncs and reads the partials
+__device__ __forceinline__ void block_partials(u32 (&v)[MB], u32 *red) {
+#pragma unroll
+    for (int q = 0; q < MB; q++) {
+        u32 x = v[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+        v[q] = x;
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int q = 0; q < MB; q++) red[(threadIdx.x >> 5) * MB + q] = v[q];
+    }
+}
+
+struct Wide {
+    const WideArgs &W;
+    const u32 *cx;                     // context block (HBM) of this CTA's modulus
+    u32 *st;                           // [2k+1][MB]
+    u32 *red;                          // [NW][MB] warp partials
+    u32 *aux;                          // [4][MB]: t_r, r_r, α', ok
+    u32 k, nch, nw;
+
+    __device__ const u32 *T(u32 off) const { return W.tab + off; }
+
+    // st <- st · b · M^-1 (mod N) for the CTA's MB messages; b at bp[ch * bstride + msg * mstride]
+    __device__ void mont_mul(const u32 *bp, size_t bstride, u32 mstride, bool sq) {
+        const WideLayout L = wide_layout(k);
+        const u32 tid = threadIdx.x, nt = blockDim.x;
+        const u32 *sigw = cx + cx_words(k) + wide_cx_sig(k);
+        // ---- channel products: B: ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i;  B': t*_j = a* b* 2^-32
+        for (u32 ch = tid; ch < 2 * k; ch += nt) {
+            const u32 m = __ldg(T(L.mm) + ch), mi = __ldg(T(L.minv) + ch);
+            const u32 s = ch < k ? __ldg(sigw + ch) : 0u;
+#pragma unroll 4
+            for (int q = 0; q < MB; q++) {
+                const u32 a = ST(st, ch, q);
+                const u32 b = sq ? a : __ldcg(bp + ch * bstride + (size_t)q * mstride);
+                const u64 pr = (u64)a * b;
+                u32 t = mont_red((u32)pr, (u32)(pr >> 32), m, mi);
+                if (ch < k) {
+                    const u64 ps = (u64)t * s;
+                    t = mont_red((u32)ps, (u32)(ps >> 32), m, mi);
+                }
+                ST(st, ch, q) = t;
+            }
+        }
+        if (tid < MB) {   // m_r: t_r = a_r b_r mod 2^32
+            const u32 a = ST(st, 2 * k, tid);
+            const u32 b = sq ? a : __ldcg(bp + (2 * k) * bstride + (size_t)tid * mstride);
+            aux[0 * MB + tid] = a * b;
+        }
+        __syncthreads();
+        // ---- BE1 (approximate, merged with 6.4): thread per output j of B' ∪ {m_r}
+        const u32 *A1w = cx + cx_words(k) + wide_cx_a1(k);
+        u32 part[MB];
+#pragma unroll
+        for (int q = 0; q < MB; q++) part[q] = 0;
+        for (u32 j = tid; j <= k; j += nt) {
+            if (j < k) {
+                u32 lo[MB], mi[MB], hi[MB];
+#pragma unroll
+                for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
+                dot_mb(A1w + j, k, st, k, lo, mi, hi);
+                const u32 ch = k + j;
+                const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
+                const u32 X = __ldg(T(L.xw) + j), a2r = __ldg(T(L.a2r) + j);
+#pragma unroll
+                for (int q = 0; q < MB; q++) {
+                    const u32 v = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);        // Σ ξ A1'  (mod m'_j)
+                    const u64 p = (u64)ST(st, ch, q) * X;                              // t* C1 2^64
+                    const u32 xp = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);
+                    ST(st, ch, q) = xp;                                                // ξ'_j (lazy)
+                    part[q] += xp * a2r;                                               // Σ ξ'_j |M'_j|_{2^32}
+                }
+            } else {   // m_r column: q̂_r = Σ ξ_i |M_i|_{2^32},  r_r = (t_r + q̂_r N) M^-1 mod 2^32
+                u32 qr[MB];
+#pragma unroll
+                for (int q = 0; q < MB; q++) qr[q] = 0;
+                for (u32 i = 0; i < k; i++) {
+                    const u32 a1r = __ldg(T(L.a1r) + i);
+#pragma unroll
+                    for (int q = 0; q < MB; q++) qr[q] += ST(st, i, q) * a1r;
+                }
+                const u32 minv32 = __ldg(T(L.misc) + 0), nminv = cx[CX_NMINV_R];
+#pragma unroll
+                for (int q = 0; q < MB; q++) aux[1 * MB + q] = aux[0 * MB + q] * minv32 + qr[q] * nminv;
+            }
+        }
+        block_partials(part, red);
+        __syncthreads();
+        if (tid < MB) {   // α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 mod 2^32, exact (Shenoy-Kumaresan)
+            u32 sr = 0;
+            for (u32 w = 0; w < nw; w++) sr += red[w * MB + tid];
+            aux[2 * MB + tid] = (sr - aux[1 * MB + tid]) * __ldg(T(L.misc) + 1);
+        }
+        __syncthreads();
+        // ---- BE2 (exact): thread per output i of B; the m_r slot takes r_r
+        const u32 *A2w = T(L.a2w);
+        for (u32 i = tid; i < k; i += nt) {
+            const u32 pinw = __ldg(T(L.pinw) + i);
+            u32 lo[MB], mi[MB], hi[MB];
+#pragma unroll
+            for (int q = 0; q < MB; q++) {
+                const u64 p = (u64)aux[2 * MB + q] * pinw;      // α' (m_i - |M'|_{m_i}) 2^32
+                lo[q] = (u32)p;
+                mi[q] = (u32)(p >> 32);
+                hi[q] = 0;
+            }
+            dot_mb(A2w + i, k, st + k * MB, k, lo, mi, hi);
+            const u32 m = __ldg(T(L.mm) + i), mv = __ldg(T(L.minv) + i), r32 = __ldg(T(L.r32) + i);
+#pragma unroll
+            for (int q = 0; q < MB; q++) ST(st, i, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
+        }
+        if (tid < MB) ST(st, 2 * k, tid) = aux[1 * MB + tid];
+        __syncthreads();
+    }
+
+    // positional -> RNS of x (nl limbs per message, rows xs[l * MB + msg] in shared memory): channel c =
+    // Σ_l x_l |2^(32 l)|_{m_c} (B' in ξ-form; the table carries × 2^32 for the Montgomery fold), m_r = x_0
+    __device__ void to_rns(const u32 *xs, u32 nl) {
+        const WideLayout L = wide_layout(k);
+        const u32 tid = threadIdx.x, nt = blockDim.x;
+        for (u32 ch = tid; ch < 2 * k; ch += nt) {
+            u32 lo[MB], mi[MB], hi[MB];
+#pragma unroll
+            for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
+            dot_mb(T(L.pow) + ch, 2 * k, xs, nl, lo, mi, hi);
+            const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
+#pragma unroll
+            for (int q = 0; q < MB; q++) ST(st, ch, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
+        }
+        if (tid < MB) ST(st, 2 * k, tid) = xs[tid];
+        __syncthreads();
+    }
+};
+
+// Exit (a7): z on B' ∪ {m_r} -> canonical X mod N, written to y rows.  Column sums of
+// X = Σ_j ξ'_j M'_j + α'(2^(32(k+1)) - M') go to the scratch rows (3 words per column and message), one
+// thread per message then propagates carries and conditionally subtracts N 2^s, s = SMAX..0.
+__device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslot, u32 *yrow[MB], const bool *okv,
+                          u32 out_limbs) {
+    const u32 k = w.k, tid = threadIdx.x, nt = blockDim.x;
+    const WideLayout L = wide_layout(k);
+    u32 part[MB];
+#pragma unroll
+    for (int q = 0; q < MB; q++) part[q] = 0;
+    for (u32 j = tid; j < k; j += nt) {
+        const u32 a2r = __ldg(w.T(L.a2r) + j);
+#pragma unroll
+        for (int q = 0; q < MB; q++) part[q] += ST(w.st, k + j, q) * a2r;
+    }
+    block_partials(part, w.red);
+    __syncthreads();
+    if (tid < MB) {
+        u32 sr = 0;
+        for (u32 v = 0; v < w.nw; v++) sr += w.red[v * MB + tid];
+        w.aux[2 * MB + tid] = (sr - ST(w.st, 2 * k, tid)) * __ldg(w.T(L.misc) + 1);
+    }
+    __syncthreads();
+    for (u32 l = tid; l <= k; l += nt) {
+        u32 lo[MB], mi[MB], hi[MB];
+        const u32 nmp = __ldg(w.T(L.nmp) + l);
+#pragma unroll
+        for (int q = 0; q < MB; q++) {
+            const u64 p = (u64)w.aux[2 * MB + q] * nmp;
+            lo[q] = (u32)p;
+            mi[q] = (u32)(p >> 32);
+            hi[q] = 0;
+        }
+        dot_mb(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
+#pragma unroll
+        for (int q = 0; q < MB; q++) {
+            u32 *col = scratch + (size_t)(3 * l) * sstride + sslot[q];
+            col[0] = lo[q];
+            col[sstride] = mi[q];
+            col[2 * sstride] = hi[q];
+        }
+    }
+    __threadfence_block();
+    __syncthreads();
+    if (tid < MB) {   // carries, then X mod N by conditional subtraction of N 2^s
+        const u32 q = tid;
+        u64 carry = 0;   // < 2^42
+        for (u32 l = 0; l <= k; l++) {
+            const u32 *col = scratch + (size_t)(3 * l) * sstride + sslot[q];
+            const u32 lo = col[0], mi = col[sstride], hi = col[2 * sstride];
+            const u64 s = (u64)lo + (u32)carry;                    // limb l of X
+            ST(w.st, l, q) = (u32)s;
+            carry = (carry >> 32) + mi + ((u64)hi << 32) + (s >> 32);
+        }
+        const u32 *nl = w.cx + cx_n(k);
+        const int smax = (int)(32 - __clz(k + 2)) - 1;   // X < (k+3) N <= 2^(smax+1) N (as mr_kernels.cuh SMAX)
+        for (int s = smax; s >= 0; s--) {
+            for (int pass = 0; pass < 2; pass++) {
+                u32 br = 0;
+                for (u32 l = 0; l <= k; l++) {
+                    const u32 nlo = l ? nl[l - 1] : 0u, nhi = l < k ? nl[l] : 0u;
+                    const u32 nsh = s ? __funnelshift_l(nlo, nhi, s) : nhi;
+                    const u64 t = (u64)ST(w.st, l, q) - nsh - br;
+                    if (pass) ST(w.st, l, q) = (u32)t;
+                    br = (u32)(t >> 63);
+                }
+                if (br) break;
+            }
+        }
+        if (yrow[q])
+            for (u32 l = 0; l < out_limbs; l++) yrow[q][l] = okv[q] ? ST(w.st, l, q) : 0u;
+    }
+    __syncthreads();
+}
+
+// modexp interpreter (same op programs as k_modexp, mr_internal.h make_op), CTA = MB messages of one context
+// NTB/MINB: register budget — 512 threads x 1 CTA (k = 505) or 320 threads x 2 CTAs per SM (k = 257)
+template <int NTB, int MINB>
+__global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P, const WideArgs W) {
+    extern __shared__ __align__(16) u32 smem[];
+    const u32 k = W.k, nch = 2 * k + 1, nw = blockDim.x / 32, tid = threadIdx.x;
+    u32 *st = smem;                                   // [nch][MB]
+    u32 *xs = st + nch * MB;                          // [k][MB] staged input limbs
+    u32 *red = xs + k * MB;                           // [16][MB]
+    u32 *aux = red + 16 * MB;                         // [4][MB]
+    __shared__ bool okv[MB];
+    __shared__ u32 sslot[MB];
+    const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
+    const u32 *cx = sel ? P.ctx[1] : P.ctx[0];
+    const u32 j0 = (blockIdx.x - sel * P.ctas0) * MB;
+    Wide w{W, cx, st, red, aux, k, nch, nw};
+    if (tid < MB) {
+        const u32 jl = j0 + tid;
+        const bool valid = jl < P.count;
+        bool ok = false;
+        if (valid) {   // x < input bound (little-endian limbs, most significant first)
+            const u32 *xr = P.x + (size_t)jl * P.in_limbs, *bnd = cx + cx_inb(k);
+            int res = 0;
+            for (int l = (int)P.in_limbs - 1; l >= 0 && res == 0; l--) res = xr[l] < bnd[l] ? -1 : (xr[l] > bnd[l] ? 1 : 0);
+            ok = res < 0;
+            if (sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
+        }
+        okv[tid] = ok;
+        sslot[tid] = sel * P.ctas0 * MB + jl;
+    }
+    __syncthreads();
+    const u64 *prog = sel ? P.prog[1] : P.prog[0];
+    const u32 nops = sel ? P.nops[1] : P.nops[0];
+    const size_t tstride = P.jobs_total, entry = (size_t)nch * tstride;
+    const u32 slot0 = sel * P.ctas0 * MB + j0;
+    for (u32 s = 0; s < nops; s++) {
+        const u64 op = __ldg(prog + s);
+        const u32 fl = (u32)op & 0xFF, opnd = (u32)(op >> 8) & 0xFF, ld = (u32)(op >> 16) & 0xFF;
+        const u32 ad = (u32)(op >> 24) & 0xFF, sto = (u32)(op >> 32) & 0xFF;
+        if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) {
+            const u32 off = (fl & OPF_TORNS_HI) ? P.half : 0u;
+            const u32 nl = (fl & OPF_TORNS_ALL) ? P.in_limbs : P.half;
+            for (u32 e = tid; e < nl * MB; e += blockDim.x) {
+                const u32 l = e / MB, q = e % MB, jl = j0 + q;
+                xs[l * MB + q] = okv[q] ? P.x[(size_t)jl * P.in_limbs + off + l] : 0u;
+            }
+            __syncthreads();
+            w.to_rns(xs, nl);
+        }
+        if (fl & OPF_LOAD) {
+            for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                const u32 ch = e / MB, q = e % MB;
+                st[e] = ld >= 0xF0 ? cx[cx_r2(k) + (ld - 0xF0) * nch + ch] : P.table[ld * entry + ch * tstride + slot0 + q];
+            }
+            __syncthreads();
+        }
+        if (!(fl & OPF_NOMUL)) {
+            if (opnd == OPND_SQ) w.mont_mul(nullptr, 0, 0, true);
+            else if (opnd >= 0xF0) w.mont_mul(cx + cx_r2(k) + (opnd - 0xF0) * nch, 1, 0, false);
+            else w.mont_mul(P.table + opnd * entry + slot0, tstride, 1, false);
+        }
+        if (fl & OPF_ADD) {   // channel-wise lazy modular addition (CRT entry)
+            const WideLayout L = wide_layout(k);
+            for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                const u32 ch = e / MB, q = e % MB;
+                const u32 b = P.table[ad * entry + ch * tstride + slot0 + q];
+                st[e] = ch < 2 * k ? addmod_lazy(st[e], b, __ldg(W.tab + L.r32 + ch)) : st[e] + b;
+            }
+            __syncthreads();
+        }
+        if (fl & OPF_STORE) {
+            for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                const u32 ch = e / MB, q = e % MB;
+                P.table[sto * entry + ch * tstride + slot0 + q] = st[e];
+            }
+            __syncthreads();
+        }
+    }
+    u32 *yrow[MB];
+#pragma unroll
+    for (int q = 0; q < MB; q++) {
+        const u32 jl = j0 + q;
+        yrow[q] = jl < P.count ? P.y + sel * P.out_stride + (size_t)jl * P.out_limbs : nullptr;
+    }
+    // column scratch: the window table (no longer needed) — 3(k+1) rows <= table_slots(w) (2k+1) rows
+    wide_exit(w, P.table, tstride, sslot, yrow, okv, P.out_limbs);
+}
+
+}  // namespace
+
+size_t wide_smem_bytes(u32 k) { return 4 * ((size_t)(2 * k + 1) * MB + (size_t)k * MB + 16 * MB + 4 * MB); }
+int wide_messages_per_cta() { return MB; }
+
+int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, void *stream) {
+    WideArgs W{d_wide_tab, k, 0};
+    const u32 nt32 = 32 * ((k + 1 + 31) / 32), nt = nt32 < (u32)NTMAX ? nt32 : (u32)NTMAX;
+    W.nt = nt;
+    const size_t smem = wide_smem_bytes(k);
+    const void *kern = nt <= 320 ? (const void *)k_modexp_wide<320, 2> : (const void *)k_modexp_wide<NTMAX, 1>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 6;
+    void *args[] = {const_cast<ModexpParams *>(&p), &W};
+    return cudaLaunchKernel(kern, dim3(ctas), dim3(nt), args, smem, (cudaStream_t)stream) == cudaSuccess ? 0 : 6;
+}
+
+}  // namespace mr

@@ -251,3 +251,67 @@ def test_ctx_table_rejections():
     limbs = 35
     nl = np.frombuffer(big.to_bytes(4 * limbs, "little"), dtype=np.uint32).copy()
     assert L.mr_internal_ctx_table(nl.ctypes.data_as(P), limbs, 33, None, 0) == -mr.MR_ERR_CAPACITY
+
+
+def _wide_layout(k):
+    """python mirror of mr_internal.h wide_layout."""
+    o = {"mm": 0}
+    o["minv"] = o["mm"] + 2 * k
+    o["r32"] = o["minv"] + 2 * k
+    o["xw"] = o["r32"] + 2 * k
+    o["a1r"] = o["xw"] + k
+    o["a2r"] = o["a1r"] + k
+    o["pinw"] = o["a2r"] + k
+    o["misc"] = o["pinw"] + k
+    o["a2w"] = o["misc"] + 4
+    o["pow"] = o["a2w"] + k * k
+    o["mpl"] = o["pow"] + 2 * k * k
+    o["nmp"] = o["mpl"] + k * (k + 1)
+    o["words"] = o["nmp"] + k + 1
+    return o
+
+
+def test_wide_table_identities():
+    """host constants of the wide-operand kernel (k = 257): word-Montgomery constants
+    with their 2^32 factors folded in, checked against the definitions on sampled entries."""
+    mr, L = _lib()
+    k = 257
+    assert 257 in mr.mr_rns_supported_k() and 505 in mr.mr_rns_supported_k()
+    P = ctypes.POINTER(ctypes.c_uint32)
+    L.mr_internal_wide_table.restype = ctypes.c_int
+    n = L.mr_internal_wide_table(k, None, 0)
+    o = _wide_layout(k)
+    assert n == o["words"]
+    t = np.zeros(n, dtype=np.uint32)
+    L.mr_internal_wide_table(k, t.ctypes.data_as(P), n)
+    t = [int(v) for v in t]
+    _, primes, _ = _tables(k)
+    B, Bp = primes[:k], primes[k:]
+    W = 1 << 32
+    M, Mp = 1, 1
+    for m in B:
+        M *= m
+    for m in Bp:
+        Mp *= m
+    rng = np.random.default_rng(257)
+    for ch in list(range(4)) + [int(v) for v in rng.integers(0, 2 * k, 20)]:
+        m = (B + Bp)[ch]
+        assert t[o["mm"] + ch] == m and t[o["minv"] + ch] * m % W == W - 1 and t[o["r32"] + ch] == W % m
+    for j in [0, 1, k - 1] + [int(v) for v in rng.integers(0, k, 8)]:
+        m = Bp[j]
+        lam = pow(Mp // m, -1, m)
+        c1 = pow(M, -1, m) * pow(lam, -1, m) % m
+        assert t[o["xw"] + j] == c1 * W * W % m and t[o["a2r"] + j] == (Mp // m) % W
+        for i in [0, k - 1] + [int(v) for v in rng.integers(0, k, 4)]:
+            assert t[o["a2w"] + j * k + i] == (Mp // m) % B[i] * W % B[i]
+    for i in [0, k - 1]:
+        assert t[o["pinw"] + i] == (B[i] - Mp % B[i]) % B[i] * W % B[i] and t[o["a1r"] + i] == (M // B[i]) % W
+    for l in [0, 1, k - 1]:
+        for ch in [0, k - 1, k, 2 * k - 1]:
+            m = (B + Bp)[ch]
+            v = pow(2, 32 * (l + 1), m)
+            if ch >= k:
+                v = v * pow(Mp // m, -1, m) % m
+            assert t[o["pow"] + l * 2 * k + ch] == v
+    assert sum(t[o["nmp"] + l] << (32 * l) for l in range(k + 1)) + Mp == 1 << (32 * (k + 1))
+    assert L.mr_internal_wide_table(129, None, 0) < 0

@@ -263,3 +263,32 @@ def test_c4_full_size_round_trip(torch_cuda, mr, orc, keys):
     assert torch_cuda.equal(x, z)
     idx = list(range(0, 96)) + list(range(96, count, 1021))
     assert np.array_equal(host(y)[idx], orc.modexp_batch(xs[idx], k["d"], n, threads=8))
+
+
+@pytest.mark.parametrize("bits", [8192, 16128])
+def test_wide_moduli_vs_oracle(torch_cuda, mr, orc, bits):
+    """§8(f) row 3, wide operands (k = 257 / 505, channels-on-threads kernel): a ragged batch
+    of 37 messages (three 16-message CTAs) for e = 65537 and a 300-bit exponent, every output vs the oracle,
+    with edge inputs 0, 1, N-1 and one out-of-range input."""
+    rng = random.Random(bits)
+    N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+    limbs = (bits + 31) // 32
+    xs = [0, 1, N - 1] + [rng.randrange(N) for _ in range(33)] + [N + 5]
+    for E in (65537, rng.getrandbits(300) | (1 << 299)):
+        y, st, ctx = run_modexp(torch_cuda, mr, N, xs, E, limbs=limbs)
+        assert ctx.k == (257 if bits == 8192 else 505)
+        assert st == [0] * 36 + [5] and y[36] == 0
+        ref = ints(orc.modexp_batch(mr.ints_to_limbs(xs[:36], limbs), E, N, threads=8))
+        assert y[:36] == ref
+
+
+@pytest.mark.parametrize("n", [8192, 16128])
+def test_wide_closed_forms(torch_cuda, mr, n):
+    """2^E mod (2^n + 1) = ±2^(E mod n) for a 16,128-bit exponent (the paper's long-exponent shape)."""
+    E = synth.exponent(16128, 0x5EEDC0DE)
+    N = (1 << n) + 1
+    limbs = (N.bit_length() + 31) // 32
+    y, _, ctx = run_modexp(torch_cuda, mr, N, [2, 1, N - 1], E, limbs=limbs)
+    r = 1 << (E % n)
+    assert y[0] == (r if (E // n) % 2 == 0 else N - r)
+    assert y[1] == 1 and y[2] == (1 if E % 2 == 0 else N - 1)

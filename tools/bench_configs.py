@@ -7,6 +7,8 @@ prints one JSON line per point and checks a sample of every point against the CP
   C3  RSA-3072: encrypt (k = 97) and CRT decrypt (k = 49 per half), batch sweep
   C4  2048-bit modulus (k = 65), exponents of 1,024 ... 16,128 bits
   C5  Miller-Rabin on seeded 1024-bit candidates (k = 33), 5 rounds, forced and early-exit
+  W   wide operands (§8(f) row 3): 8192-bit (k = 257) and 16,128-bit (k = 505) moduli, e = 65537 and a
+      full-length exponent
 
     python tools/bench_configs.py [--configs C1,C3,C4,C5] [--quick]
 """
@@ -116,6 +118,27 @@ def c4(torch, mr, orc, quick):
               "bit_exact_sample": ok, "sample": s})
 
 
+def wide(torch, mr, orc, quick):
+    import random
+    for bits in (8192, 16128):
+        rng = random.Random(bits)
+        N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+        limbs = (bits + 31) // 32
+        ctx = mr.RnsContext(N, limbs)
+        for ell in (17, bits):
+            E = 65537 if ell == 17 else rng.getrandbits(bits) | (1 << (bits - 1))
+            cnt = 4736 if (ell == 17 or bits == 8192) else 2368   # CTAs of 16 messages: 2 per SM (k = 257), 1 (k = 505)
+            xs = synth.messages(N, cnt, 0x5EEDC0DE, limbs)
+            x = torch.from_numpy(xs.view(np.int32)).cuda()
+            y = torch.empty_like(x)
+            t = timed(torch, lambda: ctx.modexp(x, y, E), reps=2 if ell == 17 else 1)
+            s = 8 if ell == 17 else 1
+            ok = bool(np.array_equal(y.cpu().numpy().view(np.uint32)[:s], orc.modexp_batch(xs[:s], E, N, threads=s)))
+            emit({"config": "W", "modulus_bits": bits, "exponent_bits": ell, "messages": cnt, "k": ctx.k,
+                  "modexps_per_s": cnt / t, "imad_eq_frac": cnt * bench.sliding_window_mm(E) * 2 * per_mm(ctx.k) / t / peak(),
+                  "bit_exact_sample": ok, "sample": s})
+
+
 def c5(torch, mr, orc, quick):
     cnt = 16384 if quick else 65536
     rounds = 5
@@ -207,6 +230,8 @@ def main():
             c4(torch, mr, oracle, a.quick)
         elif c == "C5":
             c5(torch, mr, oracle, a.quick)
+        elif c == "W":
+            wide(torch, mr, oracle, a.quick)
         elif c == "KG":
             kg(torch, mr, a.quick)
         print(f"# {c} done in {time.time() - t0:.1f} s", file=sys.stderr)
