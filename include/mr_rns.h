@@ -103,8 +103,8 @@ int mr_rsa_encrypt_batch(const mr_rns_ctx *n_ctx, const uint32_t *e, size_t e_li
  * p, q, d_p = d mod (p-1), d_q = d mod (q-1), q_inv = q^-1 mod p: HOST, half_limbs limbs each.
  * The two half contexts share one base pair; k_half = 0 picks it automatically.
  * Ciphertexts and plaintexts of mr_rsa_decrypt_batch have 2*half_limbs limbs and must be < p*q.
- * Errors as mr_rns_ctx_create, plus MR_ERR_ARG if p == q or q_inv*q != 1 mod p, and MR_ERR_CAPACITY
- * when a half needs the wide kernel (p or q above ~4,070 bits: no wide CRT recombination yet).
+ * Errors as mr_rns_ctx_create, plus MR_ERR_ARG if p == q or q_inv*q != 1 mod p.  Halves above ~4,070
+ * bits run on the wide kernel with a positional recombination (keys up to 16,128 bits).
  * ------------------------------------------------------------------------------------------ */
 int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, size_t half_limbs,
                        const uint32_t *d_p, const uint32_t *d_q, const uint32_t *q_inv, int k_half, int device);

@@ -33,6 +33,7 @@ MR_DECLARE_K(129)
 size_t wide_smem_bytes(u32 k);
 int wide_messages_per_cta();
 int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, void *stream);
+int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream);
 
 static const KernelSet &kernel_set_for(int k) {
     static std::vector<KernelSet> sets = {kernels_k1(),  kernels_k2(),  kernels_k3(),  kernels_k5(), kernels_k9(),
@@ -495,6 +496,7 @@ struct mr_rsa_priv {
     size_t half = 0;
     Big dp, dq;
     u32 *d_q = nullptr;        // q limbs on device
+    u32 *d_qinv = nullptr;     // q^-1 mod p limbs on device (wide halves: positional recombination)
 };
 
 // the per-context constant block of DESIGN.md §3 (layout cx_* in mr_internal.h)
@@ -1075,7 +1077,6 @@ int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, 
         }
         k = auto_k(big, kmin);
         if (k < 0) return MR_ERR_CAPACITY;
-        if (is_wide((u32)k)) return MR_ERR_CAPACITY;   // CRT halves above 4096 bits: no wide recombination yet
     }
     Big hl{(u32)half_limbs};
     mr_rsa_priv *pr = new (std::nothrow) mr_rsa_priv;
@@ -1090,6 +1091,10 @@ int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, 
         if (cudaMalloc(&pr->d_q, half_limbs * 4) != cudaSuccess) rc = MR_ERR_NOMEM;
         else if (cudaMemcpy(pr->d_q, q, half_limbs * 4, cudaMemcpyHostToDevice) != cudaSuccess) rc = MR_ERR_CUDA;
     }
+    if (rc == MR_OK && is_wide((u32)k)) {
+        if (cudaMalloc(&pr->d_qinv, half_limbs * 4) != cudaSuccess) rc = MR_ERR_NOMEM;
+        else if (cudaMemcpy(pr->d_qinv, q_inv, half_limbs * 4, cudaMemcpyHostToDevice) != cudaSuccess) rc = MR_ERR_CUDA;
+    }
     if (rc != MR_OK) {
         mr_rsa_priv_destroy(pr);
         return rc;
@@ -1103,6 +1108,7 @@ void mr_rsa_priv_destroy(mr_rsa_priv *priv) {
     mr_rns_ctx_destroy(priv->cp);
     mr_rns_ctx_destroy(priv->cq);
     if (priv->d_q) cudaFree(priv->d_q);
+    if (priv->d_qinv) cudaFree(priv->d_qinv);
     delete priv;
 }
 
@@ -1141,8 +1147,22 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
         C.pow_tab = priv->cp->d_pow;
         C.be_tab = priv->cp->d_be;
         C.mpl = priv->cp->d_mpl;
-        const KernelSet &ks = kernel_set_for(priv->cp->k);
-        rc = timed_launch(1, st, [&] { return ks.launch_combine(C, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
+        if (is_wide((u32)priv->cp->k)) {   // positional recombination (mr_wide.cu k_combine_wide)
+            u32 *d_scr = nullptr;
+            if (cudaMallocAsync(&d_scr, count * (2 * H + 2) * 4, st) != cudaSuccess) {
+                rc = MR_ERR_NOMEM;
+            } else {
+                rc = timed_launch(1, st, [&] {
+                         return launch_combine_wide(C, priv->d_qinv, d_scr, (u32)priv->cp->k, stream);
+                     }) == 0
+                         ? MR_OK
+                         : MR_ERR_CUDA;
+                cudaFreeAsync(d_scr, st);
+            }
+        } else {
+            const KernelSet &ks = kernel_set_for(priv->cp->k);
+            rc = timed_launch(1, st, [&] { return ks.launch_combine(C, stream); }) == 0 ? MR_OK : MR_ERR_CUDA;
+        }
     }
     cudaFreeAsync(d_mpq, st);
     if (d_tmpst) cudaFreeAsync(d_tmpst, st);

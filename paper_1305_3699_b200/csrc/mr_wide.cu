@@ -421,3 +421,126 @@ int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u
 }
 
 }  // namespace mr
+
+// ------------------------------------------------------------------ CRT recombination for wide halves (a8)
+// One thread per message, positional (O(H²) word operations, negligible next to the two ladders):
+//   t = m_q mod p;  d = (m_p - t) mod p;  h = d·q_inv mod p (schoolbook product, Knuth Algorithm D
+//   remainder, TAOCP 4.3.1);  m = m_q + q·h  (Garner, HAC 14.71).  scratch: [count][2H + 2] words.
+namespace mr {
+namespace {
+
+// u[0, ulen) mod v[0, n) in place (remainder left in u[0, n)); v top limb non-zero; u needs ulen + 1 words
+__device__ void rem_knuth_row(u32 *u, u32 ulen, const u32 *v, u32 n) {
+    const u32 sh = __clz(v[n - 1]);
+    auto vn = [&](u32 l) -> u32 { return sh ? (v[l] << sh) | (l ? v[l - 1] >> (32 - sh) : 0u) : v[l]; };
+    if (sh) {
+        u[ulen] = u[ulen - 1] >> (32 - sh);
+        for (int l = (int)ulen - 1; l > 0; l--) u[l] = (u[l] << sh) | (u[l - 1] >> (32 - sh));
+        u[0] <<= sh;
+    } else {
+        u[ulen] = 0;
+    }
+    if (ulen >= n) {
+        const u32 vt = vn(n - 1), vs = n > 1 ? vn(n - 2) : 0u;
+        for (int j = (int)(ulen - n); j >= 0; j--) {
+            const u64 num = ((u64)u[j + n] << 32) | u[j + n - 1];
+            u64 qh = num / vt, rh = num - qh * vt;
+            while (qh >> 32 || (n > 1 && qh * vs > ((rh << 32) | u[j + n - 2]))) {
+                qh--;
+                rh += vt;
+                if (rh >> 32) break;
+            }
+            u64 carry = 0;
+            long long br = 0;
+            for (u32 i = 0; i < n; i++) {
+                const u64 pr = qh * vn(i) + carry;
+                carry = pr >> 32;
+                const long long t = (long long)u[i + j] - (long long)(u32)pr + br;
+                u[i + j] = (u32)t;
+                br = t >> 32;
+            }
+            const long long t = (long long)u[j + n] - (long long)carry + br;
+            u[j + n] = (u32)t;
+            if (t < 0) {   // add back (probability ~2/2^32)
+                u64 c = 0;
+                for (u32 i = 0; i < n; i++) {
+                    const u64 s2 = (u64)u[i + j] + vn(i) + c;
+                    u[i + j] = (u32)s2;
+                    c = s2 >> 32;
+                }
+                u[j + n] += (u32)c;
+            }
+        }
+    }
+    if (sh)
+        for (u32 l = 0; l < n; l++) u[l] = (u[l] >> sh) | (l + 1 < n ? u[l + 1] << (32 - sh) : 0u);
+}
+
+__global__ void k_combine_wide(const CombineParams P, const u32 *qinv, u32 *scr, u32 k) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.count) return;
+    const u32 H = P.half;
+    const u32 *mp = P.mpq + (size_t)i * H, *mq = P.mpq + ((size_t)P.count + i) * H;
+    const u32 *pl = P.ctx_p + cx_n(k);
+    u32 *mrow = P.m + (size_t)i * 2 * H;
+    u32 *t = scr + (size_t)i * (2 * H + 2);
+    u32 n = H;
+    while (n > 1 && pl[n - 1] == 0) n--;
+    // t = m_q mod p
+    for (u32 l = 0; l < H; l++) t[l] = mq[l];
+    rem_knuth_row(t, H, pl, n);
+    // d = m_p - t (mod p) -> mrow[0, H)
+    u32 br = 0;
+    for (u32 l = 0; l < H; l++) {
+        const u64 d = (u64)mp[l] - (l < n ? t[l] : 0u) - br;
+        mrow[l] = (u32)d;
+        br = (u32)(d >> 63);
+    }
+    if (br) {
+        u32 c = 0;
+        for (u32 l = 0; l < H; l++) {
+            const u64 s2 = (u64)mrow[l] + (l < n ? pl[l] : 0u) + c;
+            mrow[l] = (u32)s2;
+            c = (u32)(s2 >> 32);
+        }
+    }
+    // h = d q_inv mod p: product into t[0, 2H), remainder -> t[0, n)
+    for (u32 l = 0; l < 2 * H; l++) t[l] = 0;
+    for (u32 a = 0; a < H; a++) {
+        const u32 da = mrow[a];
+        u64 c = 0;
+        for (u32 b = 0; b < H; b++) {
+            const u64 v = (u64)da * qinv[b] + t[a + b] + c;
+            t[a + b] = (u32)v;
+            c = v >> 32;
+        }
+        t[a + H] = (u32)c;
+    }
+    rem_knuth_row(t, 2 * H, pl, n);
+    // m = m_q + q h  (product scanning)
+    const bool bad = P.status && P.status[i] != 0;
+    u32 lo = 0, mi = 0, hi = 0;
+    for (u32 col = 0; col < 2 * H; col++) {
+        if (col < H) mac96(lo, mi, hi, mq[col], 1u);
+        const u32 r0 = col >= H ? col - H + 1 : 0u, r1 = col < H ? col : H - 1;
+        for (u32 r = r0; r <= r1; r++)
+            if (col - r < n) mac96(lo, mi, hi, P.q[r], t[col - r]);
+        mrow[col] = bad ? 0u : lo;
+        lo = mi;
+        mi = hi;
+        hi = 0;
+    }
+}
+
+}  // namespace
+
+int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream) {
+    const u32 nt = 128;
+    void *args[] = {const_cast<CombineParams *>(&p), const_cast<u32 **>(&d_qinv), &d_scratch, &k};
+    return cudaLaunchKernel((const void *)k_combine_wide, dim3((p.count + nt - 1) / nt), dim3(nt), args, 0,
+                            (cudaStream_t)stream) == cudaSuccess
+               ? 0
+               : 6;
+}
+
+}  // namespace mr

@@ -292,3 +292,31 @@ def test_wide_closed_forms(torch_cuda, mr, n):
     r = 1 << (E % n)
     assert y[0] == (r if (E // n) % 2 == 0 else N - r)
     assert y[1] == 1 and y[2] == (1 if E % 2 == 0 else N - 1)
+
+
+def test_wide_crt_decrypt_vs_oracle(torch_cuda, mr, orc):
+    """CRT decryption with 8064-bit halves (a 16,128-bit key shape; halves on the wide kernel with the
+    positional recombination).  Garner's recombination (O7) is defined for any coprime odd p, q and any
+    d_p, d_q, so random ones serve (no 8064-bit prime search on the CPU); every output vs the oracle,
+    ragged batch of 21 with edge inputs and one out-of-range ciphertext."""
+    import math
+    rng = random.Random(16128)
+    while True:
+        p = rng.getrandbits(8064) | (3 << 8062) | 1
+        q = rng.getrandbits(8064) | (3 << 8062) | 1
+        if p != q and math.gcd(p, q) == 1:
+            break
+    n, H = p * q, 252
+    dp, dq = rng.getrandbits(96) | 1, rng.getrandbits(96) | 1
+    qinv = pow(q, -1, p)
+    cs = [0, 1, n - 1, p, q] + [rng.randrange(n) for _ in range(15)] + [n + 3]
+    key = mr.RsaPrivateKey(p, q, dp, dq, qinv)
+    c = dev(torch_cuda, mr.ints_to_limbs(cs, 2 * H))
+    m = torch_cuda.empty_like(c)
+    st = torch_cuda.zeros(len(cs), dtype=torch_cuda.int32, device="cuda")
+    key.decrypt(c, m, d_status=st)
+    torch_cuda.cuda.synchronize()
+    assert host(st).view(np.int32).tolist() == [0] * 20 + [5]
+    got = host(m)
+    ref = orc.crt_decrypt_batch(mr.ints_to_limbs(cs[:20], 2 * H), p, q, dp, dq, qinv, H, threads=8)
+    assert np.array_equal(got[:20], ref) and not got[20].any()
