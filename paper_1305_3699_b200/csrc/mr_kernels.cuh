@@ -456,9 +456,12 @@ __device__ __forceinline__ void run_program(const ModexpParams &P, u32 sel, u32 
             const u64 nx = __ldg(prog + s + 1);
             const u32 nopnd = (u32)(nx >> 8) & 0xFF;
             if (!(nx & OPF_NOMUL) && nopnd < 0xF0) {
-                const u32 *np = P.table + nopnd * entry + slot;
+                // the warp's 32 consecutive slots of channel c form one 128-byte line: lane l prefetches the
+                // lines of channels l, l + 32, ... (3 instructions per lane instead of 2k+1)
+                const u32 lane = threadIdx.x & 31;
+                const u32 *np = P.table + nopnd * entry + (slot - lane);
 #pragma unroll 1
-                for (int c = 0; c < NCH; c += 1) {
+                for (u32 c = lane; c < (u32)NCH; c += 32) {
 #if MR_PF_L1
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(np + c * tstride));
 #else
