@@ -448,9 +448,10 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
     return MR_OK;
 }
 
-// capacity: 4 (k+3)^2 N < M and 4 (k+3) N < M'
+// capacity: 4 (k+3)^2 N < M and 4 (k+3) N < M'; for k <= 65 (tensor path: sign-folded
+// digits up to 2 m_i, §4e) values stay below (2k+3) N, so the bound uses 2k+3
 static bool fits(const Base &b, const Big &N) {
-    const u32 kk = (u32)b.k + 3;
+    const u32 kk = b.k <= 65 ? 2 * (u32)b.k + 3 : (u32)b.k + 3;
     Big lhs = mul_word(mul_word(N, 4 * kk), kk);
     Big lhs2 = mul_word(N, 4 * kk);
     return cmp(lhs, b.M) < 0 && cmp(lhs2, b.Mp) < 0;
@@ -586,11 +587,12 @@ static bool fill_tc_scaled(const Base &b, u32 *x) {
         for (int j = 0; j < k; j++) {
             const u32 mj = b.Bp[j], a = mulm(A1[i * k + j], c2[j], mj);
             A1s[(size_t)i * k + j] = neg[i] ? (mj - a) % mj : a;
-            if (neg[i]) off[j] = (u32)(((u64)off[j] + mulm(b.B[i] % mj, a, mj)) % mj);
+            // ε_i = -1: the digit is 2 m_i - ξ̂_i (lazy ξ̂_i < 2^32 keeps it positive): offset 2 m_i A1'[i][j]
+            if (neg[i]) off[j] = (u32)(((u64)off[j] + mulm((u32)(2ull * b.B[i] % mj), a, mj)) % mj);
         }
         const u32 a1r = b.flat[L.A1r + i];
         x[cx_a1x(k) + 2 * i] = neg[i] ? 0u - a1r : a1r;
-        if (neg[i]) qr_off += b.B[i] * a1r;
+        if (neg[i]) qr_off += 2u * b.B[i] * a1r;
         if (nt < k) x[cx_a1x(k) + 2 * i + 1] = A1s[(size_t)i * k + nt];
     }
     x[cx_scv(k) + 0] = qr_off;

@@ -37,7 +37,9 @@ constexpr int KT = K - KF;                    // tail tile
 constexpr u32 BEW = be_words(K);              // base-extension image words (smem)
 constexpr u32 BEH = be_half_words(K);         // BE1 part; BE2 follows
 constexpr int MINB = K <= 33 ? 4 : (K <= 65 ? 3 : 2);   // CTAs per SM the register budget targets
-constexpr int SMAX = (K + 3 <= 2) ? 0 : (32 - __builtin_clz((unsigned)(K + 3 - 1))) - 1;  // X < 2^(SMAX+1) N
+// X < KB N <= 2^(SMAX+1) N; KB = 2K+3 for K <= 65 (sign-folded digits of the tensor path, §4e), else K+3
+constexpr int KB = K <= 65 ? 2 * K + 3 : K + 3;
+constexpr int SMAX = (KB <= 2) ? 0 : (32 - __builtin_clz((unsigned)(KB - 1))) - 1;
 enum : u32 { MR_COMPOSITE_V = 0, MR_PROBABLY_PRIME_V = 1, MR_FACTOR_V = 2 };
 
 constexpr BaseLayout BL = base_layout(K);
@@ -785,9 +787,9 @@ struct MulTc {
                     }
                     const u32 cc = GB(O_C + i);       // unrolled: constant-bank operands
                     u32 xi;
-                    if constexpr (CS::kScaled) {      // ε_i ξ_i = s_a s_b 2^-32, canonical (signed digit m_i - xi)
+                    if constexpr (CS::kScaled) {      // ε_i ξ_i = s_a s_b 2^-32, lazy (signed digit 2 m_i - xi)
                         const u64 pr = (u64)a * b;
-                        xi = canon(mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + i), GB(O_MINV + i)), cc);
+                        xi = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + i), GB(O_MINV + i));
                         const uint2 ax = cs.a1x(i);
                         qr += xi * ax.x;
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, ax.y);
