@@ -157,6 +157,36 @@ int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t seed, uint6
                         uint32_t *d_qinv, int device, void *stream);
 
 /* Human-readable name of an MR_* code (static storage). */
+/* ------------------------------------------------------------------------------------------
+ * DRBG + FIPS 140-2 health tests (the MR-TRNG layer's deterministic half).
+ * "The unpredictable stream of bits is seeded as an unguessable input key to an approved deterministic
+ *  RBG" (§2); "a self-validating kernel ... streamlines FIPS basic tests right after the generation"
+ *  (§4.2).  Entropy harvesting is out of scope: the caller supplies entropy_input and nonce.
+ * Reading R20: Hash_DRBG with SHA-256 (NIST SP 800-90A §10.1.1, seedlen 440, no additional input, no
+ * prediction resistance), `streams` independent instances; stream s is instantiated with
+ * personalization_string = pers || s (4 bytes big-endian).
+ *
+ * mr_drbg_create: entropy (HOST, >= 32 bytes), nonce (HOST, >= 16 bytes), pers (HOST, may be empty).
+ *   Errors: MR_ERR_ARG (short entropy/nonce, streams == 0), MR_ERR_CUDA, MR_ERR_NOMEM.
+ * mr_drbg_generate: one Hash_DRBG_Generate request of every stream: d_out DEVICE [streams][nbytes] bytes
+ *   (stream s at d_out + s * nbytes), nbytes <= 65,536 (2^19 bits, the per-request maximum); then each
+ *   state is updated (V += Hash(0x03 || V) + C + reseed_counter).  nbytes = 0 only updates the states.
+ *   Asynchronous on `stream`; successive calls must be stream-ordered.  Errors: MR_ERR_ARG, MR_ERR_CUDA,
+ *   MR_ERR_RANGE after 2^48 requests (the reseed interval; reseeding is not provided).
+ * mr_fips_health_batch: the FIPS 140-2 §4.9.1 tests on d_blocks DEVICE [nblocks][2500] bytes (20,000
+ *   bits each, most significant bit of each byte first); d_stats DEVICE uint32 [nblocks][16]: ones,
+ *   poker S = sum of the squared nibble counts, runs of ones of length 1..5, 6+, runs of zeros of length
+ *   1..5, 6+, long-run flag (a run >= 26 exists), verdict bits (1 monobit, 2 poker, 4 runs, 8 long run;
+ *   set = pass).  Thresholds: 9,725 < ones < 10,275; 2.16 < 16 S / 5000 - 5000 < 46.17; runs within
+ *   [2315,2685] [1114,1386] [527,723] [240,384] [103,209] [103,209]; no run >= 26 (reading R21).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct mr_drbg mr_drbg;
+int mr_drbg_create(mr_drbg **out, const uint8_t *entropy, size_t entropy_len, const uint8_t *nonce, size_t nonce_len,
+                   const uint8_t *pers, size_t pers_len, uint32_t streams, int device);
+int mr_drbg_generate(mr_drbg *d, uint8_t *d_out, size_t nbytes, void *stream);
+void mr_drbg_destroy(mr_drbg *d);
+int mr_fips_health_batch(const uint8_t *d_blocks, size_t nblocks, uint32_t *d_stats, void *stream);
+
 const char *mr_strerror(int code);
 
 #ifdef __cplusplus

@@ -22,7 +22,7 @@ __all__ = [
     "mr_rns_ctx_create", "mr_rns_ctx_destroy", "mr_rns_ctx_info", "mr_rns_supported_k",
     "mr_modexp_batch", "mr_rsa_encrypt_batch", "mr_rsa_priv_create", "mr_rsa_priv_destroy",
     "mr_rsa_decrypt_batch", "mr_miller_rabin_batch", "mr_strerror",
-    "RnsContext", "RsaPrivateKey", "limbs_of", "ints_to_limbs", "limbs_to_ints",
+    "RnsContext", "RsaPrivateKey", "Drbg", "fips_health", "limbs_of", "ints_to_limbs", "limbs_to_ints",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -36,6 +36,7 @@ EXPORTS = (
     "mr_rns_ctx_create", "mr_rns_ctx_destroy", "mr_rns_ctx_info", "mr_rns_supported_k", "mr_modexp_batch",
     "mr_rsa_encrypt_batch", "mr_rsa_priv_create", "mr_rsa_priv_destroy", "mr_rsa_decrypt_batch",
     "mr_miller_rabin_batch", "mr_rsa_keygen_batch", "mr_strerror",
+    "mr_drbg_create", "mr_drbg_generate", "mr_drbg_destroy", "mr_fips_health_batch",
 )
 
 
@@ -74,8 +75,14 @@ def lib() -> ctypes.CDLL:
             [vp] * 7 + [i32, vp]
         L.mr_strerror.argtypes = [i32]
         L.mr_strerror.restype = ctypes.c_char_p
+        cp = ctypes.c_char_p
+        L.mr_drbg_create.argtypes = [ctypes.POINTER(vp), cp, sz, cp, sz, cp, sz, ctypes.c_uint32, i32]
+        L.mr_drbg_generate.argtypes = [vp, vp, sz, vp]
+        L.mr_drbg_destroy.argtypes = [vp]
+        L.mr_drbg_destroy.restype = None
+        L.mr_fips_health_batch.argtypes = [vp, sz, vp, vp]
         for name in EXPORTS:
-            if name not in ("mr_rns_ctx_destroy", "mr_rsa_priv_destroy", "mr_strerror"):
+            if name not in ("mr_rns_ctx_destroy", "mr_rsa_priv_destroy", "mr_strerror", "mr_drbg_destroy"):
                 getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -270,3 +277,41 @@ class RsaPrivateKey:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ DRBG + FIPS 140-2 health tests (§8(f) row 4)
+
+class Drbg:
+    """`streams` independent Hash_DRBG (SHA-256, SP 800-90A) instances on the GPU (mr_drbg)."""
+
+    def __init__(self, entropy: bytes, nonce: bytes, pers: bytes = b"", streams: int = 1, device: int = 0):
+        h = ctypes.c_void_p()
+        _check(lib().mr_drbg_create(ctypes.byref(h), entropy, len(entropy), nonce, len(nonce), pers, len(pers),
+                                    streams, device), "mr_drbg_create")
+        self.handle, self.streams, self.device = h, streams, device
+
+    def generate(self, d_out, nbytes: int, stream=None) -> None:
+        """one generate request of every stream into d_out (CUDA uint8 tensor [streams][nbytes])."""
+        if d_out is not None and (d_out.dtype.itemsize != 1 or d_out.numel() != self.streams * nbytes):
+            raise MrError(MR_ERR_ARG, "d_out must be a uint8 tensor of streams * nbytes bytes")
+        ptr = _dptr(d_out) if nbytes else None
+        st = _stream(d_out, stream) if d_out is not None else stream
+        _check(lib().mr_drbg_generate(self.handle, ptr, nbytes, st), "mr_drbg_generate")
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().mr_drbg_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fips_health(d_blocks, d_stats, stream=None) -> None:
+    """FIPS 140-2 tests of d_blocks (CUDA uint8 [n][2500]) into d_stats (CUDA int32 [n][16])."""
+    n = d_blocks.shape[0]
+    _check(lib().mr_fips_health_batch(_dptr(d_blocks), n, _dptr(d_stats), _stream(d_blocks, stream)),
+           "mr_fips_health_batch")

@@ -7,6 +7,7 @@ prints one JSON line per point and checks a sample of every point against the CP
   C3  RSA-3072: encrypt (k = 97) and CRT decrypt (k = 49 per half), batch sweep
   C4  2048-bit modulus (k = 65), exponents of 1,024 ... 16,128 bits
   C5  Miller-Rabin on seeded 1024-bit candidates (k = 33), 5 rounds, forced and early-exit
+  RNG Hash_DRBG (SHA-256) generation and FIPS 140-2 health tests (§8(f) row 4), GB/s
   W   wide operands (§8(f) row 3): 8192-bit (k = 257) and 16,128-bit (k = 505) moduli, e = 65537 and a
       full-length exponent
 
@@ -139,6 +140,31 @@ def wide(torch, mr, orc, quick):
                   "bit_exact_sample": ok, "sample": s})
 
 
+def rng(torch, mr, quick):
+    from oracle import drbg
+    streams, nb = 16384, 65536                      # 1 GiB per request (2^19 bits per stream, the maximum)
+    g = mr.Drbg(bytes(range(32)), bytes(range(16)), b"bench", streams)
+    out = torch.empty(streams * nb, dtype=torch.uint8, device="cuda")
+    t = timed(torch, lambda: g.generate(out, nb), reps=3)
+    host = out[: 4 * nb].cpu().numpy().tobytes()
+    # the sampled streams continue from the same state sequence as the oracle's (warm-up + 3 timed requests)
+    ok = True
+    for s in range(2):
+        d = drbg.HashDrbg(bytes(range(32)), bytes(range(16)), drbg.stream_pers(b"bench", s))
+        for _ in range(4):
+            want = d.generate(nb)
+        ok &= host[s * nb:(s + 1) * nb] == want
+    nblk = streams * nb // 2500
+    blocks = out[: nblk * 2500].view(nblk, 2500)
+    stats = torch.empty((nblk, 16), dtype=torch.int32, device="cuda")
+    th = timed(torch, lambda: mr.fips_health(blocks, stats), reps=3)
+    v = stats[:, 15].cpu().numpy()
+    emit({"config": "RNG", "streams": streams, "bytes_per_request": nb, "generate_GB_per_s": streams * nb / t / 1e9,
+          "health_GB_per_s": nblk * 2500 / th / 1e9, "health_blocks": nblk,
+          "health_pass_fraction": float((v == 15).mean()), "bit_exact_sample": bool(ok), "sample": "2 streams x 64 KiB",
+          "paper_context": "32-40 GB/s of seed bits on 2013 GPUs (P:121)"})
+
+
 def c5(torch, mr, orc, quick):
     cnt = 16384 if quick else 65536
     rounds = 5
@@ -230,6 +256,8 @@ def main():
             c4(torch, mr, oracle, a.quick)
         elif c == "C5":
             c5(torch, mr, oracle, a.quick)
+        elif c == "RNG":
+            rng(torch, mr, a.quick)
         elif c == "W":
             wide(torch, mr, oracle, a.quick)
         elif c == "KG":
