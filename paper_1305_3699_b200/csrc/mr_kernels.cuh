@@ -793,11 +793,11 @@ struct MulTc {
                         const uint2 ax = cs.a1x(i);
                         qr += xi * ax.x;
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, ax.y);
-                    } else if constexpr (CS::kMont) {   // ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i, canonical
+                    } else if constexpr (CS::kMont) {   // ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i
                         const u64 pr = (u64)a * b;
                         const u32 t = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + i), GB(O_MINV + i));
                         const u64 ps = (u64)t * cs.sigma(i);
-                        xi = canon(mont_red((u32)ps, (u32)(ps >> 32), GB(O_MM + i), GB(O_MINV + i)), cc);
+                        xi = mont_red((u32)ps, (u32)(ps >> 32), GB(O_MM + i), GB(O_MINV + i));   // lazy digit < 2^32
                         qr += xi * GB(O_A1R + i);
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
                     } else {
