@@ -169,15 +169,23 @@ __global__ void __launch_bounds__(128) k_fips_health(const uint8_t *__restrict__
     for (u32 q = tid; q < 31; q += blockDim.x) acc[q] = 0;
     __syncthreads();
     const u32 *wb = reinterpret_cast<const u32 *>(blocks + (size_t)blockIdx.x * 2500);
-    u32 ones = 0, runs[2][6] = {{0}}, longf = 0, nib[16] = {0};
+    u32 ones = 0, runs[2][6] = {{0}}, longf = 0, nib[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) nib[q] = 0;
     for (u32 wi = tid; wi < HB_WORDS; wi += blockDim.x) {
         // stream-order words: byte 0 of the word is the most significant byte (bits MSB first)
         const u32 cur = __byte_perm(__ldg(wb + wi), 0, 0x0123);
         const u32 prev = wi ? __byte_perm(__ldg(wb + wi - 1), 0, 0x0123) : 0u;
         const u32 next = wi + 1 < HB_WORDS ? __byte_perm(__ldg(wb + wi + 1), 0, 0x0123) : 0u;
         ones += __popc(cur);
+        // nibble histogram without data-dependent indexing: for each value v, the nibbles of cur ^ (v * 0x11111111)
+        // that are zero are the nibbles equal to v
 #pragma unroll
-        for (int q = 0; q < 8; q++) nib[(cur >> (28 - 4 * q)) & 15]++;
+        for (int v = 0; v < 16; v++) {
+            const u32 z = cur ^ (0x11111111u * (u32)v);
+            const u32 nz = (z | (z >> 1) | (z >> 2) | (z >> 3)) & 0x11111111u;
+            nib[v] += 8 - __popc(nz);
+        }
 #pragma unroll
         for (int b = 0; b < 2; b++) {
             // y: 1 where the stream bit equals b; outside the block y = 0 (runs end at the block edges)
@@ -207,8 +215,13 @@ __global__ void __launch_bounds__(128) k_fips_health(const uint8_t *__restrict__
     for (int b = 0; b < 2; b++)
         for (int l = 0; l < 6; l++) atomicAdd(&acc[2 + 6 * (1 - b) + l], runs[b][l]);   // ones first, then zeros
     if (longf) atomicOr(&acc[14], 1u);
-    for (int q = 0; q < 16; q++)
-        if (nib[q]) atomicAdd(&acc[15 + q], nib[q]);
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        u32 x = nib[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+        if ((tid & 31) == 0 && x) atomicAdd(&acc[15 + q], x);
+    }
     __syncthreads();
     if (tid == 0) {
         u32 *o = stats + (size_t)blockIdx.x * 16;
