@@ -70,7 +70,10 @@ __device__ __forceinline__ u32 &ST(u32 *st, u32 ch, u32 msg) { return st[ch * MB
 // acc[q] += Σ_{i < n} xs[i * MB + q] · coef[i * cstride]  for the CTA's MB messages (96-bit accumulators).
 // The constants stream from L2/HBM: PF of them are loaded one chunk ahead so their latency overlaps the
 // previous chunk's multiply-accumulates (the loop is otherwise bound by L2 latency).
-constexpr int PF = 8;
+#ifndef MR_WIDE_PF
+#define MR_WIDE_PF 8
+#endif
+constexpr int PF = MR_WIDE_PF;
 __device__ __forceinline__ void dot_mb(const u32 *__restrict__ coef, size_t cstride, const u32 *xs, u32 n,
                                        u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
     u32 cur[PF], nxt[PF];
@@ -119,12 +122,64 @@ __device__ __forceinline__ void block_partials(u32 (&v)[MB], u32 *red) {
     }
 }
 
+// Same contraction with the constants staged through shared memory by cp.async (LDGSTS): each thread
+// copies its own column of TI rows one stage ahead into stg[stage][r][tid] (no registers held by the
+// prefetch, so the copy distance is TI rows instead of PF), then reads them back with LDS.  Measured slower
+// than the register prefetch (A/B: 0.25 vs 0.33 IMAD-eq fraction at 8192 bits): off by default.
+#ifndef MR_WIDE_STAGED
+#define MR_WIDE_STAGED 0
+#endif
+constexpr int TI = 16;
+__device__ __forceinline__ void cp_async4(u32 *sdst, const u32 *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((u32)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void dot_mb_staged(const u32 *__restrict__ coef, size_t cstride, const u32 *xs, u32 n,
+                                              u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB], u32 *stg) {
+    const u32 tid = threadIdx.x, nt = blockDim.x;
+    auto issue = [&](u32 stage, u32 i0) {
+#pragma unroll
+        for (int r = 0; r < TI; r++)
+            if (i0 + r < n) cp_async4(stg + (stage * TI + r) * nt + tid, coef + (size_t)(i0 + r) * cstride);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0, 0);
+    u32 stage = 0;
+#pragma unroll 1
+    for (u32 i0 = 0; i0 < n; i0 += TI, stage ^= 1) {
+        issue(stage ^ 1, i0 + TI);                                    // next stage (empty group past the end)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");         // this stage landed (own column only)
+#pragma unroll
+        for (int r = 0; r < TI; r++) {
+            if (i0 + r < n) {
+                const u32 c = stg[(stage * TI + r) * nt + tid];
+                const uint4 *x = reinterpret_cast<const uint4 *>(xs + (i0 + r) * MB);
+#pragma unroll
+                for (int v4 = 0; v4 < MB / 4; v4++) {
+                    const uint4 xv = x[v4];
+                    mac96(lo[4 * v4 + 0], mi[4 * v4 + 0], hi[4 * v4 + 0], xv.x, c);
+                    mac96(lo[4 * v4 + 1], mi[4 * v4 + 1], hi[4 * v4 + 1], xv.y, c);
+                    mac96(lo[4 * v4 + 2], mi[4 * v4 + 2], hi[4 * v4 + 2], xv.z, c);
+                    mac96(lo[4 * v4 + 3], mi[4 * v4 + 3], hi[4 * v4 + 3], xv.w, c);
+                }
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+#if MR_WIDE_STAGED
+#define DOT_MB(coef, cs, xs, n, lo, mi, hi) dot_mb_staged(coef, cs, xs, n, lo, mi, hi, stg)
+#else
+#define DOT_MB(coef, cs, xs, n, lo, mi, hi) dot_mb(coef, cs, xs, n, lo, mi, hi)
+#endif
+
 struct Wide {
     const WideArgs &W;
     const u32 *cx;                     // context block (HBM) of this CTA's modulus
     u32 *st;                           // [2k+1][MB]
     u32 *red;                          // [NW][MB] warp partials
     u32 *aux;                          // [4][MB]: t_r, r_r, α', ok
+    u32 *stg;                          // [2][TI][nt] constant staging (dot_mb_staged)
     u32 k, nch, nw;
 
     __device__ const u32 *T(u32 off) const { return W.tab + off; }
@@ -167,7 +222,7 @@ struct Wide {
                 u32 lo[MB], mi[MB], hi[MB];
 #pragma unroll
                 for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
-                dot_mb(A1w + j, k, st, k, lo, mi, hi);
+                DOT_MB(A1w + j, k, st, k, lo, mi, hi);
                 const u32 ch = k + j;
                 const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
                 const u32 X = __ldg(T(L.xw) + j), a2r = __ldg(T(L.a2r) + j);
@@ -213,7 +268,7 @@ struct Wide {
                 mi[q] = (u32)(p >> 32);
                 hi[q] = 0;
             }
-            dot_mb(A2w + i, k, st + k * MB, k, lo, mi, hi);
+            DOT_MB(A2w + i, k, st + k * MB, k, lo, mi, hi);
             const u32 m = __ldg(T(L.mm) + i), mv = __ldg(T(L.minv) + i), r32 = __ldg(T(L.r32) + i);
 #pragma unroll
             for (int q = 0; q < MB; q++) ST(st, i, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
@@ -231,7 +286,7 @@ struct Wide {
             u32 lo[MB], mi[MB], hi[MB];
 #pragma unroll
             for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
-            dot_mb(T(L.pow) + ch, 2 * k, xs, nl, lo, mi, hi);
+            DOT_MB(T(L.pow) + ch, 2 * k, xs, nl, lo, mi, hi);
             const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
 #pragma unroll
             for (int q = 0; q < MB; q++) ST(st, ch, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
@@ -274,7 +329,8 @@ __device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslo
             mi[q] = (u32)(p >> 32);
             hi[q] = 0;
         }
-        dot_mb(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
+        u32 *stg = w.stg;
+        DOT_MB(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
 #pragma unroll
         for (int q = 0; q < MB; q++) {
             u32 *col = scratch + (size_t)(3 * l) * sstride + sslot[q];
@@ -326,12 +382,13 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
     u32 *xs = st + nch * MB;                          // [k][MB] staged input limbs
     u32 *red = xs + k * MB;                           // [16][MB]
     u32 *aux = red + 16 * MB;                         // [4][MB]
+    u32 *stg = aux + 4 * MB;                          // [2][TI][nt]
     __shared__ bool okv[MB];
     __shared__ u32 sslot[MB];
     const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
     const u32 *cx = sel ? P.ctx[1] : P.ctx[0];
     const u32 j0 = (blockIdx.x - sel * P.ctas0) * MB;
-    Wide w{W, cx, st, red, aux, k, nch, nw};
+    Wide w{W, cx, st, red, aux, stg, k, nch, nw};
     if (tid < MB) {
         const u32 jl = j0 + tid;
         const bool valid = jl < P.count;
@@ -406,7 +463,10 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
 
 }  // namespace
 
-size_t wide_smem_bytes(u32 k) { return 4 * ((size_t)(2 * k + 1) * MB + (size_t)k * MB + 16 * MB + 4 * MB); }
+size_t wide_smem_bytes(u32 k) {
+    const size_t nt = 32 * ((k + 1 + 31) / 32);
+    return 4 * ((size_t)(2 * k + 1) * MB + (size_t)k * MB + 16 * MB + 4 * MB + (MR_WIDE_STAGED ? 2 * TI * nt : 0));
+}
 int wide_messages_per_cta() { return MB; }
 
 int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, void *stream) {
