@@ -320,3 +320,25 @@ def test_wide_crt_decrypt_vs_oracle(torch_cuda, mr, orc):
     got = host(m)
     ref = orc.crt_decrypt_batch(mr.ints_to_limbs(cs[:20], 2 * H), p, q, dp, dq, qinv, H, threads=8)
     assert np.array_equal(got[:20], ref) and not got[20].any()
+
+
+@pytest.mark.parametrize("count", [37889, 38016, 75777])
+def test_split_schedule_geometries(torch_cuda, mr, orc, keys, count):
+    """the wrap-around schedule of DESIGN.md §4f at awkward job counts: CRT decryption with 297 and
+    297 (ragged) tile-jobs per context on 296 slots (one job straddles two slots), and encryption-then-
+    decryption round trips; sampled outputs vs the oracle, every output by the round trip."""
+    k = keys["rsa2048"]
+    n = k["n"]
+    cs = synth.messages(n, count, 0x5EEDC0C0 + count, 64)
+    key = mr.RsaPrivateKey(k["p"], k["q"], k["dp"], k["dq"], k["qinv"])
+    ctx = mr.RnsContext(n)
+    c = dev(torch_cuda, cs)
+    m = torch_cuda.empty_like(c)
+    key.decrypt(c, m)
+    c2 = torch_cuda.empty_like(c)
+    ctx.encrypt(m, c2, k["e"])
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.equal(c, c2)
+    idx = [0, 1, 127, 128, count // 2, count - 129, count - 2, count - 1]
+    ref = orc.crt_decrypt_batch(cs[idx], k["p"], k["q"], k["dp"], k["dq"], k["qinv"], 32, threads=8)
+    assert np.array_equal(host(m)[idx], ref)
