@@ -690,6 +690,31 @@ __device__ __forceinline__ void tmem_ld16_nowait(u32 taddr, u32 (&v)[16]) {
                    "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
                  : "r"(taddr));
 }
+// 32 consecutive accumulator columns in one load (two 16-column groups), no memory clobber (see above)
+__device__ __forceinline__ void tmem_ld32_nowait(u32 taddr, u32 (&v)[2][16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(v[0][0]), "=r"(v[0][1]), "=r"(v[0][2]), "=r"(v[0][3]), "=r"(v[0][4]), "=r"(v[0][5]),
+                   "=r"(v[0][6]), "=r"(v[0][7]), "=r"(v[0][8]), "=r"(v[0][9]), "=r"(v[0][10]), "=r"(v[0][11]),
+                   "=r"(v[0][12]), "=r"(v[0][13]), "=r"(v[0][14]), "=r"(v[0][15]), "=r"(v[1][0]), "=r"(v[1][1]),
+                   "=r"(v[1][2]), "=r"(v[1][3]), "=r"(v[1][4]), "=r"(v[1][5]), "=r"(v[1][6]), "=r"(v[1][7]),
+                   "=r"(v[1][8]), "=r"(v[1][9]), "=r"(v[1][10]), "=r"(v[1][11]), "=r"(v[1][12]), "=r"(v[1][13]),
+                   "=r"(v[1][14]), "=r"(v[1][15])
+                 : "r"(taddr));
+}
+#ifndef MR_TMEM_X32
+#define MR_TMEM_X32 1
+#endif
+__device__ __forceinline__ void tmem_ld_pair(u32 taddr, bool two, u32 (&v)[2][16]) {
+#if MR_TMEM_X32
+    if (two) {
+        tmem_ld32_nowait(taddr, v);
+        return;
+    }
+#endif
+    tmem_ld16_nowait(taddr, v[0]);
+    if (two) tmem_ld16_nowait(taddr + 16, v[1]);
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // wait for the TMEM loads of vv with the loaded registers as in/out operands instead of a memory clobber: the
 // uses of vv stay after the wait, and independent shared-memory loads (epilogue constants, B' state) may be
@@ -904,8 +929,7 @@ struct MulTc {
 #pragma unroll 1
         for (int g0 = 0; g0 < NG; g0 += 2) {
           u32 vv[2][16];                              // two TMEM loads in flight, one wait
-          tmem_ld16_nowait(t.tmem + lane_base + 16 * g0, vv[0]);
-          if (g0 + 1 < NG) tmem_ld16_nowait(t.tmem + lane_base + 16 * (g0 + 1), vv[1]);
+          tmem_ld_pair(t.tmem + lane_base + 16 * g0, g0 + 1 < NG, vv);
           tmem_wait_ld_regs(vv);
 #pragma unroll
           for (int h = 0; h < 2; h++) {
@@ -985,8 +1009,7 @@ struct MulTc {
 #pragma unroll 1
         for (int g0 = 0; g0 < NG; g0 += 2) {
           u32 vv[2][16];
-          tmem_ld16_nowait(t.tmem + lane_base + 16 * g0, vv[0]);
-          if (g0 + 1 < NG) tmem_ld16_nowait(t.tmem + lane_base + 16 * (g0 + 1), vv[1]);
+          tmem_ld_pair(t.tmem + lane_base + 16 * g0, g0 + 1 < NG, vv);
           tmem_wait_ld_regs(vv);
 #pragma unroll
           for (int h = 0; h < 2; h++) {
