@@ -65,6 +65,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_RED_VARIANT
 #define MR_RED_VARIANT 2
 #endif
+#ifndef MR_BP_LATE
+#define MR_BP_LATE 0        // A/B hook: B' products after the BE1 MMA issue (overlap the MMA); measured 0.8 % slower
+#endif
 #ifndef MR_CHAN_FUSE
 #define MR_CHAN_FUSE 0      // A/B hook: interleave the B' channel products with the B chunks
 #endif
@@ -853,7 +856,7 @@ struct MulTc {
             }
 #endif
         }
-#if MR_CHAN_FUSE
+#if MR_CHAN_FUSE || MR_BP_LATE
         bq = bp + (size_t)(2 * K) * bs;
 #pragma unroll
         for (int j = 0; j < 0; j++) {
@@ -874,8 +877,32 @@ struct MulTc {
                 S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
             }
         }
+#if MR_BP_LATE
+        return 0;
+#else
         const u32 ar = S(st, 2 * K);
         return ar * (SQ || sq ? ar : mulop_ld<CS>(bq));
+#endif
+    }
+
+    // B' channel products t*_j and the m_r product (returned); with MR_BP_LATE they run after the BE1 MMA
+    // issue, overlapping the tensor-core latency
+    template <bool SQ, class CS>
+    __device__ __forceinline__ u32 chan_bp(const StTile &st, const u32 *bp, u32 bs, bool sq = SQ) {
+#pragma unroll
+        for (int j = 0; j < K; j++) {
+            const u32 a = S(st, K + j);
+            u32 b = a;
+            if (!SQ) b = sq ? a : mulop_ld<CS>(bp + (size_t)(K + j) * bs);
+            if constexpr (CS::kMont) {
+                const u64 pr = (u64)a * b;
+                S(st, K + j) = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + K + j), GB(O_MINV + K + j));
+            } else {
+                S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
+            }
+        }
+        const u32 ar = S(st, 2 * K);
+        return ar * (SQ || sq ? ar : mulop_ld<CS>(bp + (size_t)(2 * K) * bs));
     }
 
     template <class CS>
@@ -898,9 +925,17 @@ struct MulTc {
 #else
         tr = chan<false>(st, bp, bs, cs, qr, c1lo, c1mi, c1hi, sq);
 #endif
+#if MR_BP_LATE
+        // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij); the B'
+        //      channel products and the m_r product run while the MMA does
+        tc_issue(t, t.b1);
+        tr = sq ? chan_bp<true, CS>(st, bp, bs) : chan_bp<false, CS>(st, bp, bs);
+        const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
+#else
         const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
         // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij)
         tc_issue(t, t.b1);
+#endif
         u32 xp_c = 0;
         if (TCNC) {   // the CUDA-core output overlaps the MMA
             const int j = TCNT;
