@@ -342,3 +342,28 @@ def test_split_schedule_geometries(torch_cuda, mr, orc, keys, count):
     idx = [0, 1, 127, 128, count // 2, count - 129, count - 2, count - 1]
     ref = orc.crt_decrypt_batch(cs[idx], k["p"], k["q"], k["dp"], k["dq"], k["qinv"], 32, threads=8)
     assert np.array_equal(host(m)[idx], ref)
+
+
+@pytest.mark.parametrize("half_bits", [2048, 4096])
+def test_crt_decrypt_large_halves_vs_oracle(torch_cuda, mr, orc, half_bits):
+    """CRT decryption with 2048-bit halves (k = 65: both contexts on the CTA-pair tensor kernel in one
+    launch) and 4096-bit halves (k = 129, IMAD path): random coprime odd p, q (Garner's definition O7 needs
+    no primality), ragged batch of 300 with edge inputs, every output vs the oracle."""
+    import math
+    rng = random.Random(half_bits)
+    while True:
+        p = rng.getrandbits(half_bits) | (3 << (half_bits - 2)) | 1
+        q = rng.getrandbits(half_bits) | (3 << (half_bits - 2)) | 1
+        if p != q and math.gcd(p, q) == 1:
+            break
+    n, H = p * q, half_bits // 32
+    dp, dq = rng.getrandbits(128) | 1, rng.getrandbits(128) | 1
+    qinv = pow(q, -1, p)
+    cs = [0, 1, n - 1, p, q, 2 * p] + [rng.randrange(n) for _ in range(294)]
+    key = mr.RsaPrivateKey(p, q, dp, dq, qinv)
+    c = dev(torch_cuda, mr.ints_to_limbs(cs, 2 * H))
+    m = torch_cuda.empty_like(c)
+    key.decrypt(c, m)
+    torch_cuda.cuda.synchronize()
+    ref = orc.crt_decrypt_batch(mr.ints_to_limbs(cs, 2 * H), p, q, dp, dq, qinv, H, threads=8)
+    assert np.array_equal(host(m), ref)
