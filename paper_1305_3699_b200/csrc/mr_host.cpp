@@ -268,6 +268,10 @@ static const Base &base_for(int k) {
         f[L.MM + ch] = m;
         f[L.MINV + ch] = 0u - inv32(m);
     }
+    for (int j = 0; j < k; j++) {   // C1_j 2^64 mod m'_j  (2^32 ≡ c'_j = -m'_j mod 2^32)
+        const u32 m = b.Bp[j], c = 0u - m;
+        f[L.XW + j] = mulm(mulm(f[L.C1 + j], c, m), c, m);
+    }
     b.pow.assign((size_t)k * 2 * k, 0);
     for (int l = 0; l < k; l++) {
         Big p2 = pow2(32 * l);

@@ -51,7 +51,7 @@ __host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_ep2(k) + 2 * k + 
 // ---------------------------------------------------------------------------------------------
 struct BaseLayout {
     u32 k;
-    u32 c, c2, A1r, A2r, C1, pin, misc, NMp, MiS, MU, ONE, ML, MM, MINV;   // device constant bank (prefix)
+    u32 c, c2, A1r, A2r, C1, pin, misc, NMp, MiS, MU, ONE, ML, MM, MINV, XW;   // device constant bank (prefix)
     u32 const_words;                                              // words uploaded to __constant__
     u32 MpL, A1, A2, words;                                       // host-side / global-memory tables
 };
@@ -72,7 +72,8 @@ __host__ __device__ constexpr BaseLayout base_layout(u32 k) {
     b.ML = b.ONE + 2 * k + 1;       // [k+1]    M positional limbs    (Miller-Rabin setup)
     b.MM = b.ML + k + 1;            // [2k]     m (B then B')         (word Montgomery reduction, §4g)
     b.MINV = b.MM + 2 * k;          // [2k]     -m^-1 mod 2^32
-    b.const_words = b.MINV + 2 * k;
+    b.XW = b.MINV + 2 * k;          // [k]      |M^-1 λ_j^-1| 2^64 mod m'_j (tensor-path BE1 epilogue, §4g)
+    b.const_words = b.XW + k;
     b.MpL = b.const_words;          // [k][k+1] M'_j positional limbs (global memory, exit conversion)
     b.A1 = b.MpL + k * (k + 1);     // [k][k]   |M_i|_{m'_j}  (row i, column j; source of the BE images)
     b.A2 = b.A1 + k * k;            // [k][k]   |M'_j|_{m_i}  (row j, column i)

@@ -45,7 +45,7 @@ enum : u32 { MR_COMPOSITE_V = 0, MR_PROBABLY_PRIME_V = 1, MR_FACTOR_V = 2 };
 constexpr BaseLayout BL = base_layout(K);
 constexpr u32 O_C = BL.c, O_C2 = BL.c2, O_A1R = BL.A1r, O_A2R = BL.A2r;
 constexpr u32 O_C1 = BL.C1, O_PIN = BL.pin, O_MISC = BL.misc, O_NMP = BL.NMp;
-constexpr u32 O_MIS = BL.MiS, O_MU = BL.MU, O_ONE = BL.ONE, O_ML = BL.ML, O_MM = BL.MM, O_MINV = BL.MINV;
+constexpr u32 O_MIS = BL.MiS, O_MU = BL.MU, O_ONE = BL.ONE, O_ML = BL.ML, O_MM = BL.MM, O_MINV = BL.MINV, O_XW = BL.XW;
 constexpr u32 BASE_WORDS = BL.const_words;          // __constant__ prefix of the base table
 constexpr u32 CXW = cx_words(K);
 constexpr u32 SMEM_STATE = NCH * T;           // words of per-CTA residue state
@@ -64,6 +64,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #endif
 #ifndef MR_RED_VARIANT
 #define MR_RED_VARIANT 2
+#endif
+#ifndef MR_EPI_UNROLL
+#define MR_EPI_UNROLL 1     // fully unrolled tensor epilogues with constant-bank operands (+6 % over LDS-fed rolled loops)
 #endif
 #ifndef MR_BP_LATE
 #define MR_BP_LATE 0        // A/B hook: B' products after the BE1 MMA issue (overlap the MMA); measured 0.8 % slower
@@ -961,8 +964,7 @@ struct MulTc {
         u32 sr = 0;
         u32 c2lo = 0, c2mi = 0, c2hi = 0;
         constexpr int NG = TCNT / 4 + (TCNT % 4 ? 1 : 0);
-#pragma unroll 1
-        for (int g0 = 0; g0 < NG; g0 += 2) {
+        auto epi1 = [&](int g0) {
           u32 vv[2][16];                              // two TMEM loads in flight, one wait
           tmem_ld_pair(t.tmem + lane_base + 16 * g0, g0 + 1 < NG, vv);
           tmem_wait_ld_regs(vv);
@@ -981,8 +983,13 @@ struct MulTc {
                     tc_split(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], lo, hi);
                     u32 xp;
                     if constexpr (CS::kScaled) {   // ξ'_j = mont(t*_j C1_j c'^2 + V'_j): (m', -m'^-1, C1 c'^2, A2r)
+#if MR_EPI_UNROLL
+                        const uint4 e = make_uint4(GB(O_MM + K + j), GB(O_MINV + K + j), GB(O_XW + j), GB(O_A2R + j));
+                        fold_hi(lo, hi, GB(O_C + K + j), w33, c33);
+#else
                         const uint4 e = cs.ep1(j);
                         fold_hi(lo, hi, 0u - e.x, w33, c33);
+#endif
                         const u64 p = (u64)S(st, K + j) * e.z + (((u64)c33 << 32) | w33);
                         xp = mont_red((u32)p, (u32)(p >> 32), e.x, e.y);
                         S(st, K + j) = xp;
@@ -1014,6 +1021,13 @@ struct MulTc {
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);   // BE2 operand
           }
+        };
+        if constexpr (CS::kScaled && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
+#pragma unroll
+            for (int g0 = 0; g0 < NG; g0 += 2) epi1(g0);
+        } else {
+#pragma unroll 1
+            for (int g0 = 0; g0 < NG; g0 += 2) epi1(g0);
         }
         // α' (6.6, exact through the extra modulus) goes into the A row at word K, the K-byte column where
         // the BE2 image holds the bytes of m_i - |M'|_{m_i}: the MMA adds α'·(m_i - |M'|_{m_i}) itself
@@ -1041,8 +1055,7 @@ struct MulTc {
             r_c = red96(c2hi, c2mi, c2lo, s_be[bev_c(K) + i], 0);
         }
         tc_wait(t);
-#pragma unroll 1
-        for (int g0 = 0; g0 < NG; g0 += 2) {
+        auto epi2 = [&](int g0) {
           u32 vv[2][16];
           tmem_ld_pair(t.tmem + lane_base + 16 * g0, g0 + 1 < NG, vv);
           tmem_wait_ld_regs(vv);
@@ -1060,7 +1073,11 @@ struct MulTc {
                     u32 lo, hi;
                     tc_split(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3], lo, hi);
                     if constexpr (CS::kScaled) {   // s_i = mont(V_i) (the image carries × c_i)
+#if MR_EPI_UNROLL
+                        const uint2 e = make_uint2(GB(O_MM + i), GB(O_MINV + i));
+#else
                         const uint2 e = cs.ep2(i);
+#endif
                         w[o] = mont_red(lo, hi, e.x, e.y);
                     } else {
                         w[o] = fold_word(lo, hi, s_be[bev_c(K) + i]);
@@ -1069,6 +1086,13 @@ struct MulTc {
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
           }
+        };
+        if constexpr (CS::kScaled && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
+#pragma unroll
+            for (int g0 = 0; g0 < NG; g0 += 2) epi2(g0);
+        } else {
+#pragma unroll 1
+            for (int g0 = 0; g0 < NG; g0 += 2) epi2(g0);
         }
         if (TCNC) *reinterpret_cast<uint4 *>(arow + (TCNT / 4) * 128) = make_uint4(r_c, 0u, 0u, 0u);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

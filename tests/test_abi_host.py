@@ -91,7 +91,8 @@ def _layout(k):
     o["ML"] = o["ONE"] + 2 * k + 1
     o["MM"] = o["ML"] + k + 1
     o["MINV"] = o["MM"] + 2 * k
-    o["MpL"] = o["MINV"] + 2 * k
+    o["XW"] = o["MINV"] + 2 * k
+    o["MpL"] = o["XW"] + k
     o["A1"] = o["MpL"] + k * (k + 1)
     o["A2"] = o["A1"] + k * k
     return o
@@ -132,6 +133,7 @@ def test_base_table_identities(k):
         assert f[o["A2r"] + j] == Mpj % W
         lam = pow(Mpj, -1, Bp[j])
         assert f[o["C1"] + j] == pow(M, -1, Bp[j]) * pow(lam, -1, Bp[j]) % Bp[j]
+        assert f[o["XW"] + j] == f[o["C1"] + j] * (W * W % Bp[j]) % Bp[j]
         limbs = sum(f[o["MpL"] + j * (k + 1) + l] << (32 * l) for l in range(k + 1))
         assert limbs == Mpj
     for i in range(k):
