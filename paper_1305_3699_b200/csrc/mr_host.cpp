@@ -272,6 +272,8 @@ static const Base &base_for(int k) {
         const u32 m = b.Bp[j], c = 0u - m;
         f[L.XW + j] = mulm(mulm(f[L.C1 + j], c, m), c, m);
     }
+    if (tc_nt(k) < (u32)k)
+        for (int j = 0; j < k; j++) f[L.A2C + j] = f[L.A2 + j * k + tc_nt(k)];   // |M'_j|_{m_TCNT}
     b.pow.assign((size_t)k * 2 * k, 0);
     for (int l = 0; l < k; l++) {
         Big p2 = pow2(32 * l);
@@ -602,7 +604,7 @@ static bool fill_tc_scaled(const Base &b, u32 *x) {
     x[cx_scv(k) + 0] = qr_off;
     if (nt < k) {   // CUDA-core output (plain red96): its t* carries 2^-32, so C1 is taken times c'
         x[cx_scv(k) + 1] = off[nt];
-        x[cx_scv(k) + 2] = mulm(pin[nt], rho[nt], b.B[nt]);
+        x[cx_scv(k) + 2] = rho[nt];   // the CUDA-core BE2 output is formed unscaled, then × ρ_TCNT
         x[cx_scv(k) + 3] = mulm(b.flat[L.C1 + nt], 0u - b.Bp[nt], b.Bp[nt]);
         for (int j = 0; j < k; j++) x[cx_a2s(k) + j] = mulm(A2[j * k + nt], rho[nt], b.B[nt]);
     }

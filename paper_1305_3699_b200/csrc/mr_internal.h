@@ -38,7 +38,7 @@ __host__ __device__ constexpr u32 cx_inb(u32 k) { return cx_n(k) + k + 1; }     
 __host__ __device__ constexpr u32 cx_sc(u32 k) { return cx_inb(k) + 2 * k + 2; }     // [4][2k+1] R2ρ², ONEρ, KHIρ², R2ρ
 __host__ __device__ constexpr u32 cx_a1x(u32 k) { return (cx_sc(k) + 4 * (2 * k + 1) + 1) & ~1u; }  // [k][2] (ε_i|M_i|_{2^32}, ε_i A1'[i][TCNT])
 __host__ __device__ constexpr u32 cx_a2s(u32 k) { return cx_a1x(k) + 2 * k; }        // [k]  A2[j][TCNT] ρ_TCNT
-__host__ __device__ constexpr u32 cx_scv(u32 k) { return cx_a2s(k) + k; }            // [4]  q̂_r offset, BE1-TCNT offset, pin_TCNT ρ_TCNT, C1_TCNT R32
+__host__ __device__ constexpr u32 cx_scv(u32 k) { return cx_a2s(k) + k; }            // [4]  q̂_r offset, BE1-TCNT offset, ρ_TCNT, C1_TCNT R32
 // epilogue constants of the word-Montgomery reductions (§4g): BE1 output j: (m'_j, -m'_j^-1, C1_j R32², |M'_j|_{2^32});
 // BE2 output i: (m_i, -m_i^-1)
 __host__ __device__ constexpr u32 cx_ep1(u32 k) { return (cx_scv(k) + 4 + 3) & ~3u; }   // [k][4]
@@ -51,7 +51,7 @@ __host__ __device__ constexpr u32 cx_words(u32 k) { return (cx_ep2(k) + 2 * k + 
 // ---------------------------------------------------------------------------------------------
 struct BaseLayout {
     u32 k;
-    u32 c, c2, A1r, A2r, C1, pin, misc, NMp, MiS, MU, ONE, ML, MM, MINV, XW;   // device constant bank (prefix)
+    u32 c, c2, A1r, A2r, C1, pin, misc, NMp, MiS, MU, ONE, ML, MM, MINV, XW, A2C;   // device constant bank (prefix)
     u32 const_words;                                              // words uploaded to __constant__
     u32 MpL, A1, A2, words;                                       // host-side / global-memory tables
 };
@@ -73,7 +73,8 @@ __host__ __device__ constexpr BaseLayout base_layout(u32 k) {
     b.MM = b.ML + k + 1;            // [2k]     m (B then B')         (word Montgomery reduction, §4g)
     b.MINV = b.MM + 2 * k;          // [2k]     -m^-1 mod 2^32
     b.XW = b.MINV + 2 * k;          // [k]      |M^-1 λ_j^-1| 2^64 mod m'_j (tensor-path BE1 epilogue, §4g)
-    b.const_words = b.XW + k;
+    b.A2C = b.XW + k;               // [k]      |M'_j|_{m_TCNT}: the CUDA-core BE2 output column (tensor path)
+    b.const_words = b.A2C + k;
     b.MpL = b.const_words;          // [k][k+1] M'_j positional limbs (global memory, exit conversion)
     b.A1 = b.MpL + k * (k + 1);     // [k][k]   |M_i|_{m'_j}  (row i, column j; source of the BE images)
     b.A2 = b.A1 + k * k;            // [k][k]   |M'_j|_{m_i}  (row j, column i)

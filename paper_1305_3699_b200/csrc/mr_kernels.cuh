@@ -46,6 +46,7 @@ constexpr BaseLayout BL = base_layout(K);
 constexpr u32 O_C = BL.c, O_C2 = BL.c2, O_A1R = BL.A1r, O_A2R = BL.A2r;
 constexpr u32 O_C1 = BL.C1, O_PIN = BL.pin, O_MISC = BL.misc, O_NMP = BL.NMp;
 constexpr u32 O_MIS = BL.MiS, O_MU = BL.MU, O_ONE = BL.ONE, O_ML = BL.ML, O_MM = BL.MM, O_MINV = BL.MINV, O_XW = BL.XW;
+constexpr u32 O_A2C = BL.A2C;
 constexpr u32 BASE_WORDS = BL.const_words;          // __constant__ prefix of the base table
 constexpr u32 CXW = cx_words(K);
 constexpr u32 SMEM_STATE = NCH * T;           // words of per-CTA residue state
@@ -202,7 +203,7 @@ struct CtxTc : CtxSmem {
     __device__ uint2 a1x(int i) const { return reinterpret_cast<const uint2 *>(cx + cx_a1x(K))[i]; }
     __device__ u32 qr_off() const { return cx[cx_scv(K) + 0]; }
     __device__ u32 c1_off() const { return cx[cx_scv(K) + 1]; }
-    __device__ u32 pin_nc() const { return cx[cx_scv(K) + 2]; }
+    __device__ u32 rho_nc() const { return cx[cx_scv(K) + 2]; }
     __device__ u32 c1nc() const { return cx[cx_scv(K) + 3]; }
     __device__ uint4 ep1(int j) const { return reinterpret_cast<const uint4 *>(cx + cx_ep1(K))[j]; }
     __device__ uint2 ep2(int i) const { return reinterpret_cast<const uint2 *>(cx + cx_ep2(K))[i]; }
@@ -994,7 +995,7 @@ struct MulTc {
                         xp = mont_red((u32)p, (u32)(p >> 32), e.x, e.y);
                         S(st, K + j) = xp;
                         sr += xp * e.w;
-                        if (TCNC) mac96(c2lo, c2mi, c2hi, xp, s_a2c[j]);
+                        if (TCNC) mac96(c2lo, c2mi, c2hi, xp, GB(O_A2C + j));   // unscaled column, × ρ at the end
                         w[o] = xp;
                         continue;
                     }
@@ -1036,7 +1037,8 @@ struct MulTc {
             const int j = TCNT;
             S(st, K + j) = xp_c;
             sr += xp_c * s_be[bev_A2r(K) + j];
-            mac96(c2lo, c2mi, c2hi, xp_c, s_a2c[j]);
+            if constexpr (CS::kScaled) mac96(c2lo, c2mi, c2hi, xp_c, GB(O_A2C + j));
+            else mac96(c2lo, c2mi, c2hi, xp_c, s_a2c[j]);
             alpha = (sr - rr) * GB(O_MISC + 1);
             *reinterpret_cast<uint4 *>(arow + (j / 4) * 128) = make_uint4(xp_c, alpha | ONECOL, 0u, 0u);
         } else {
@@ -1050,9 +1052,9 @@ struct MulTc {
         u32 r_c = 0;
         if (TCNC) {
             const int i = TCNT;
-            if constexpr (CS::kScaled) mac96(c2lo, c2mi, c2hi, alpha, cs.pin_nc());
-            else mac96(c2lo, c2mi, c2hi, alpha, s_be[bev_pin(K) + i]);
+            mac96(c2lo, c2mi, c2hi, alpha, CS::kScaled ? GB(O_PIN + i) : s_be[bev_pin(K) + i]);
             r_c = red96(c2hi, c2mi, c2lo, s_be[bev_c(K) + i], 0);
+            if constexpr (CS::kScaled) r_c = mulmod(r_c, cs.rho_nc(), s_be[bev_c(K) + i]);   // stored B residues carry ρ
         }
         tc_wait(t);
         auto epi2 = [&](int g0) {

@@ -92,7 +92,8 @@ def _layout(k):
     o["MM"] = o["ML"] + k + 1
     o["MINV"] = o["MM"] + 2 * k
     o["XW"] = o["MINV"] + 2 * k
-    o["MpL"] = o["XW"] + k
+    o["A2C"] = o["XW"] + k
+    o["MpL"] = o["A2C"] + k
     o["A1"] = o["MpL"] + k * (k + 1)
     o["A2"] = o["A1"] + k * k
     return o
