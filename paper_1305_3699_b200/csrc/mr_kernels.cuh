@@ -69,9 +69,6 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_EPI_UNROLL
 #define MR_EPI_UNROLL 1     // fully unrolled tensor epilogues with constant-bank operands (+6 % over LDS-fed rolled loops)
 #endif
-#ifndef MR_MMA_SPLIT
-#define MR_MMA_SPLIT 0      // A/B hook: two N-halves per extension, separate commits (measured 10 % slower)
-#endif
 #ifndef MR_BP_LATE
 #define MR_BP_LATE 0        // A/B hook: B' products after the BE1 MMA issue (overlap the MMA); measured 0.8 % slower
 #endif
@@ -586,11 +583,6 @@ constexpr int TCT = tc_fits(4) ? 4 : (tc_fits(3) ? 3 : (tc_fits(2) ? 2 : 1));
 static_assert(tc_smem_for(TCT) <= 232448, "tensor-core tile does not fit shared memory");
 constexpr u32 TC_M = PAIR ? 256u : 128u;
 constexpr u32 TC_IDESC = (2u << 4) | ((TCNP >> 3) << 17) | ((TC_M >> 4) << 24);  // s32 = u8 x u8, K-major
-// split mode: each extension as two MMAs of N/2 columns committed to two mbarriers, so the epilogue can
-// start on the first half of the outputs while the tensor core computes the second (single-CTA tiles
-// whose N/2 is a multiple of 16 and whose output groups split evenly)
-constexpr bool TC_SPLIT = MR_MMA_SPLIT && !PAIR && (TCNP % 32 == 0) && ((TCNT / 4) % 4 == 0);
-constexpr u32 TC_IDESC_H = (2u << 4) | (((TCNP / 2) >> 3) << 17) | ((TC_M >> 4) << 24);
 constexpr u32 tmem_cols_for(u32 n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
 constexpr u32 TC_TMEM_COLS = tmem_cols_for(TCT * TCNP);   // power of two >= 32
 constexpr u32 BEV = BEV_;                                      // the per-channel vectors of the BE image
@@ -623,7 +615,6 @@ struct TcTile {
     u32 rbar;                         // cluster-window address of rank 0's ready mbarrier for this tile
     u32 rphase;                       // its phase parity (rank 0 leader)
     bool issuer;                      // leader && (rank 0 || !PAIR)
-    u32 mbar2;                        // split mode: mbarrier of the second N-half (same phase as mbar)
 };
 
 __device__ __forceinline__ void tile_sync(const TcTile &t) { asm volatile("bar.sync %0, 128;" ::"r"(t.bar) : "memory"); }
@@ -655,23 +646,6 @@ __device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const u32 sa = smem_u32(t.a), sb = smem_u32(bimg);
-        if constexpr (TC_SPLIT) {   // half h: B rows [h N/2, (h+1) N/2) (8-row groups of TCSBO bytes), D columns h N/2
-#pragma unroll
-            for (u32 h = 0; h < 2; h++) {
-#pragma unroll
-                for (u32 ks = 0; ks < TCKP / 32; ks++) {
-                    const u64 da = umma_desc(sa + ks * 256), db = umma_desc(sb + h * (TCNP / 16) * TCSBO + ks * 256);
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t.tmem + h * (TCNP / 2)),
-                        "l"(da), "l"(db), "r"(TC_IDESC_H), "r"(ks) : "memory");
-                }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 h ? t.mbar2 : t.mbar)
-                             : "memory");
-            }
-            return;
-        }
 #pragma unroll
         for (u32 ks = 0; ks < TCKP / 32; ks++) {
             const u64 da = umma_desc(sa + ks * 256), db = umma_desc(sb + ks * 256);
@@ -697,7 +671,7 @@ __device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
 }
 
 // wait for the tile's MMA chain (bounded: a lost completion traps instead of hanging the GPU)
-__device__ __forceinline__ void tc_wait(TcTile &t, int half = -1) {   // half: split mode 0 / 1, -1 = whole
+__device__ __forceinline__ void tc_wait(TcTile &t) {
 #if MR_ABL_NOMMA
     return;
 #endif
@@ -708,11 +682,11 @@ __device__ __forceinline__ void tc_wait(TcTile &t, int half = -1) {   // half: s
             "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, P1;\n\t}"
             : "=r"(done)
-            : "r"(half == 1 ? t.mbar2 : t.mbar), "r"(t.phase)
+            : "r"(t.mbar), "r"(t.phase)
             : "memory");
         if (spin > (1u << 26)) __trap();
     }
-    if (half != 0) t.phase ^= 1u;   // both halves complete one phase per extension
+    t.phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
@@ -987,7 +961,7 @@ struct MulTc {
                 xp_c = red96(h2, m2, l2, cj, 0);
             }
         }
-        tc_wait(t, TC_SPLIT ? 0 : -1);
+        tc_wait(t);
         u32 sr = 0;
         u32 c2lo = 0, c2mi = 0, c2hi = 0;
         constexpr int NG = TCNT / 4 + (TCNT % 4 ? 1 : 0);
@@ -1051,16 +1025,10 @@ struct MulTc {
         };
         if constexpr (CS::kScaled && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
 #pragma unroll
-            for (int g0 = 0; g0 < NG; g0 += 2) {
-                if (TC_SPLIT && g0 == NG / 2) tc_wait(t, 1);
-                epi1(g0);
-            }
+            for (int g0 = 0; g0 < NG; g0 += 2) epi1(g0);
         } else {
 #pragma unroll 1
-            for (int g0 = 0; g0 < NG; g0 += 2) {
-                if (TC_SPLIT && g0 == NG / 2) tc_wait(t, 1);
-                epi1(g0);
-            }
+            for (int g0 = 0; g0 < NG; g0 += 2) epi1(g0);
         }
         // α' (6.6, exact through the extra modulus) goes into the A row at word K, the K-byte column where
         // the BE2 image holds the bytes of m_i - |M'|_{m_i}: the MMA adds α'·(m_i - |M'|_{m_i}) itself
@@ -1088,7 +1056,7 @@ struct MulTc {
             r_c = red96(c2hi, c2mi, c2lo, s_be[bev_c(K) + i], 0);
             if constexpr (CS::kScaled) r_c = mulmod(r_c, cs.rho_nc(), s_be[bev_c(K) + i]);   // stored B residues carry ρ
         }
-        tc_wait(t, TC_SPLIT ? 0 : -1);
+        tc_wait(t);
         auto epi2 = [&](int g0) {
           u32 vv[2][16];
           tmem_ld_pair(t.tmem + lane_base + 16 * g0, g0 + 1 < NG, vv);
@@ -1123,16 +1091,10 @@ struct MulTc {
         };
         if constexpr (CS::kScaled && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
 #pragma unroll
-            for (int g0 = 0; g0 < NG; g0 += 2) {
-                if (TC_SPLIT && g0 == NG / 2) tc_wait(t, 1);
-                epi2(g0);
-            }
+            for (int g0 = 0; g0 < NG; g0 += 2) epi2(g0);
         } else {
 #pragma unroll 1
-            for (int g0 = 0; g0 < NG; g0 += 2) {
-                if (TC_SPLIT && g0 == NG / 2) tc_wait(t, 1);
-                epi2(g0);
-            }
+            for (int g0 = 0; g0 < NG; g0 += 2) epi2(g0);
         }
         if (TCNC) *reinterpret_cast<uint4 *>(arow + (TCNT / 4) * 128) = make_uint4(r_c, 0u, 0u, 0u);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1152,8 +1114,7 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     u32 *s_a1c = s_cx + CXW;                         // CUDA-core output columns (k = 33)
     u32 *s_a2c = s_a1c + pad4(K);
     u64 *mbar = reinterpret_cast<u64 *>(s_a2c + pad4(K));      // [TCT] MMA done, pair mode: + [TCT] ready
-    u64 *mbar2 = mbar + (PAIR ? 2 : 1) * TCT;                   // split mode: [TCT] second-half barriers
-    u32 *tslot = reinterpret_cast<u32 *>(mbar2 + (TC_SPLIT ? TCT : 0));
+    u32 *tslot = reinterpret_cast<u32 *>(mbar + (PAIR ? 2 : 1) * TCT);
     u32 rank = 0;                                               // CTA rank in the pair (pair mode)
     if (PAIR) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
     const u32 unit = PAIR ? blockIdx.x / 2 : blockIdx.x;        // CTA, or CTA pair
@@ -1172,7 +1133,6 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     }
     if (tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
     if (PAIR && tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(mbar + TCT + tid)));
-    if (TC_SPLIT && tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar2 + tid)));
     if (tid < 32) {
         if (PAIR) {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -1197,7 +1157,7 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     // CUDA-core output columns of the scaled path come from the context block (cx_a1x via CtxTc, cx_a2s)
     MulTc mm{s_be, s_a1c, s_cx + cx_a2s(K), TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
                                                  smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, rbar, 0u,
-                                                 m == 0 && rank == 0, smem_u32(mbar2 + tile)}};
+                                                 m == 0 && rank == 0}};
     // per-message state: B channels in the A tile row, B' and m_r in the tile's rows
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
@@ -1696,7 +1656,7 @@ __device__ __forceinline__ bool x_is_nm1_t(const StTile &st, const u32 *nrow, u3
 
 constexpr size_t tc_mr_smem_for(int tiles) {
     return 4 * (size_t)(tiles * TC_ROWS + tiles * K * 128 + BEV + pad4(NCH) + 3 * pad4(K)) +
-           (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 128;
+           (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
 }
 constexpr bool tc_mr_fits(int tiles) { return tc_mr_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
 constexpr int TCM = tc_mr_fits(4) ? 4 : (tc_mr_fits(3) ? 3 : (tc_mr_fits(2) ? 2 : 1));   // MR tiles per CTA
@@ -1717,8 +1677,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     u32 *s_a2c = s_a1c + pad4(K);
     u32 *s_c1c = s_a2c + pad4(K);                          // |M^-1 λ_j^-1| 2^32 (word-Montgomery t*, §4g)
     u64 *mbar = reinterpret_cast<u64 *>(s_c1c + pad4(K));
-    u64 *mbar2 = mbar + TCM;                               // split mode: second-half barriers
-    u32 *tslot = reinterpret_cast<u32 *>(mbar2 + TCM);
+    u32 *tslot = reinterpret_cast<u32 *>(mbar + TCM);
     const u32 tid = threadIdx.x, tile = tid / 128, m = tid % 128;
     for (u32 w = tid; w < BEV; w += blockDim.x) s_vec[w] = __ldg(P.be_tab + bev_c(K) + w);
     for (u32 w = tid; w < (u32)NCH; w += blockDim.x) s_one[w] = GB(O_ONE + w);
@@ -1737,7 +1696,6 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
         reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b2) + w);
     }
     if (tid < (u32)TCM) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
-    if (TC_SPLIT && tid < (u32)TCM) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar2 + tid)));
     if (tid < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                      "r"(TC_MR_TMEM));
@@ -1750,8 +1708,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     const u32 tmem_base = *tslot;
 
     MulTc mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
-                                        smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, 0u, 0u, m == 0,
-                                        smem_u32(mbar2 + tile)}};
+                                        smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, 0u, 0u, m == 0}};
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
     u32 *c2rows = c2_all + tile * K * 128 + m;
