@@ -1170,61 +1170,66 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     // job list, so every M = 256 MMA finds both halves of its operand (host: ctas0 even).
     const u32 Gc = P.tc_gc, cta = unit - sel * Gc;
     const u32 njobs = PAIR ? P.ctas0 / 2 : P.ctas0;
-    if (!P.flags) {
+    // Whole jobs round-robin (no flags), or the split (McNaughton wrap-around) schedule of DESIGN.md §4f: the
+    // group's njobs x L op-units are laid out linearly and slot s = cta * TCT + tile takes units
+    // [s C, (s+1) C), C = max(L, ceil(njobs L / NS)).  A job straddling the boundary of slots s and s+1 runs
+    // its EARLY ops at the start of slot s+1 and its LATE ops at the end of slot s (C >= L keeps the two
+    // parts apart in time); the state passes through table slot hslot and a release/acquire flag.
+    // One loop, one inlined copy of run_program (the multiplication code is large: instruction cache).
+    const bool split = P.flags != nullptr;
+    const u32 L = sel ? P.nops[1] : P.nops[0], NS = Gc * TCT;
+    const u64 W = (u64)njobs * L;
+    const u64 C = (W + NS - 1) / NS > L ? (W + NS - 1) / NS : (u64)L;
+    const u64 s0 = (u64)(cta * TCT + tile) * C;
+    const u64 s1 = s0 + C < W ? s0 + C : W;
+    const size_t hoff = (size_t)P.hslot * NCH * P.jobs_total;
+    u32 *flag_base = split ? P.flags + (size_t)sel * njobs * 2 + rank : nullptr;
+    u64 u = s0;
+    u32 trr = cta + Gc * tile;
 #pragma unroll 1
-        for (u32 t = cta + Gc * tile; t < njobs; t += Gc * TCT) {
-            const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
-            run_program<StTile, MulTc, CtxTc>(P, sel, jl, sel * P.ctas0 * 128 + jl, jl < P.count, st, s_cx, mm);
-        }
-    } else {
-        // Split (McNaughton wrap-around) schedule: the group's njobs x L op-units are laid out
-        // linearly and slot s = cta * TCT + tile takes units [s C, (s+1) C), C = max(L, ceil(njobs L / NS)).
-        // A job straddling the boundary of slots s and s+1 runs its EARLY ops at the start of slot s+1 and
-        // its LATE ops at the end of slot s (C >= L keeps the two parts apart in time); the state passes
-        // through table slot hslot and a release/acquire flag.
-        const u32 L = sel ? P.nops[1] : P.nops[0], NS = Gc * TCT;
-        const u64 W = (u64)njobs * L;
-        const u64 C = (W + NS - 1) / NS > L ? (W + NS - 1) / NS : (u64)L;
-        const u64 s0 = (u64)(cta * TCT + tile) * C;
-        const u64 s1 = s0 + C < W ? s0 + C : W;
-        const size_t hoff = (size_t)P.hslot * NCH * P.jobs_total;
-        u32 *flag_base = P.flags + (size_t)sel * njobs * 2 + rank;
-        u64 u = s0;
-#pragma unroll 1
-        while (u < s1) {
-            const u32 t = (u32)(u / L), o = (u32)(u % L);
-            const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
-            const u32 col = sel * P.ctas0 * 128 + jl;
-            u32 ob, oe;
+    while (true) {
+        u32 t, ob, oe;
+        if (split) {
+            if (u >= s1) break;
+            t = (u32)(u / L);
+            const u32 o = (u32)(u % L);
             if (o) { ob = 0; oe = L - o; }                          // early part of a job shared with slot s-1
             else if (u + L <= s1) { ob = 0; oe = L; }               // whole job
             else { ob = L - (u32)(s1 - u); oe = L; }                // late part of a job shared with slot s+1
-            u32 *flag = flag_base + (size_t)t * 2;
-            if (ob) {   // wait for the early part, then resume from the handed-over state
-                if (m == 0) {
-                    u32 v = 0;
-#pragma unroll 1
-                    for (u32 spin = 0; !v; spin++) {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-                        if (spin > (1u << 28)) __trap();
-                    }
-                }
-                tile_sync(mm.t);
-                const u32 *src = P.table + hoff + col;
-#pragma unroll 1
-                for (int c = 0; c < NCH; c++) S(st, c) = __ldcg(src + (size_t)c * P.jobs_total);
-            }
-            run_program<StTile, MulTc, CtxTc>(P, sel, jl, col, jl < P.count, st, s_cx, mm, ob, oe);
-            if (oe < L) {   // hand the state over to the slot that runs the late part
-                u32 *dst = P.table + hoff + col;
-#pragma unroll 1
-                for (int c = 0; c < NCH; c++) __stcg(dst + (size_t)c * P.jobs_total, S(st, c));
-                __threadfence();
-                tile_sync(mm.t);
-                if (m == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
-            }
-            u += oe - ob;
+        } else {
+            if (trr >= njobs) break;
+            t = trr;
+            trr += Gc * TCT;
+            ob = 0;
+            oe = L;
         }
+        const u32 jl = (PAIR ? t * 256 + rank * 128 : t * 128) + m;
+        const u32 col = sel * P.ctas0 * 128 + jl;
+        u32 *flag = split ? flag_base + (size_t)t * 2 : nullptr;
+        if (ob) {   // wait for the early part, then resume from the handed-over state
+            if (m == 0) {
+                u32 v = 0;
+#pragma unroll 1
+                for (u32 spin = 0; !v; spin++) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                    if (spin > (1u << 28)) __trap();
+                }
+            }
+            tile_sync(mm.t);
+            const u32 *src = P.table + hoff + col;
+#pragma unroll 1
+            for (int c = 0; c < NCH; c++) S(st, c) = __ldcg(src + (size_t)c * P.jobs_total);
+        }
+        run_program<StTile, MulTc, CtxTc>(P, sel, jl, col, jl < P.count, st, s_cx, mm, ob, oe);
+        if (oe < L) {   // hand the state over to the slot that runs the late part
+            u32 *dst = P.table + hoff + col;
+#pragma unroll 1
+            for (int c = 0; c < NCH; c++) __stcg(dst + (size_t)c * P.jobs_total, S(st, c));
+            __threadfence();
+            tile_sync(mm.t);
+            if (m == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+        }
+        u += oe - ob;
     }
 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
