@@ -122,6 +122,29 @@ __device__ __forceinline__ void block_partials(u32 (&v)[MB], u32 *red) {
     }
 }
 
+// Warp-cooperative version for an output column left over when k + 1 exceeds the CTA's threads by a few:
+// lane l sums the inputs i ≡ l (mod 32), then a butterfly of 96-bit adds leaves the total in every lane.
+__device__ __forceinline__ void dot_mb_warp(const u32 *__restrict__ coef, size_t cstride, const u32 *xs, u32 n,
+                                            u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
+    const u32 lane = threadIdx.x & 31;
+    for (u32 i = lane; i < n; i += 32) {
+        const u32 c = __ldg(coef + (size_t)i * cstride);
+#pragma unroll
+        for (int q = 0; q < MB; q++) mac96(lo[q], mi[q], hi[q], xs[i * MB + q], c);
+    }
+#pragma unroll
+    for (int q = 0; q < MB; q++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const u32 l2 = __shfl_xor_sync(0xFFFFFFFFu, lo[q], o), m2 = __shfl_xor_sync(0xFFFFFFFFu, mi[q], o);
+            const u32 h2 = __shfl_xor_sync(0xFFFFFFFFu, hi[q], o);
+            asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+                : "+r"(lo[q]), "+r"(mi[q]), "+r"(hi[q])
+                : "r"(l2), "r"(m2), "r"(h2));
+        }
+    }
+}
+
 // Same contraction with the constants staged through shared memory by cp.async (LDGSTS): each thread
 // copies its own column of TI rows one stage ahead into stg[stage][r][tid] (no registers held by the
 // prefetch, so the copy distance is TI rows instead of PF), then reads them back with LDS.  Measured slower
@@ -185,6 +208,7 @@ struct Wide {
     __device__ const u32 *T(u32 off) const { return W.tab + off; }
 
     // st <- st · b · M^-1 (mod N) for the CTA's MB messages; b at bp[ch * bstride + msg * mstride]
+    template <bool COOP>   // COOP: the CTA has fewer threads than k + 1 outputs (leftovers by whole warps)
     __device__ void mont_mul(const u32 *bp, size_t bstride, u32 mstride, bool sq) {
         const WideLayout L = wide_layout(k);
         const u32 tid = threadIdx.x, nt = blockDim.x;
@@ -217,17 +241,22 @@ struct Wide {
         u32 part[MB];
 #pragma unroll
         for (int q = 0; q < MB; q++) part[q] = 0;
-        for (u32 j = tid; j <= k; j += nt) {
+        // outputs j = 0 .. k (j = k: the m_r column); one per thread for j < nt, and the few left over
+        // (k + 1 > nt, e.g. 258 on 256 threads) cooperatively by one warp each
+        const u32 lane = tid & 31, warp = tid >> 5;
+        auto be1_out = [&](u32 j, bool coop) {
             if (j < k) {
                 u32 lo[MB], mi[MB], hi[MB];
 #pragma unroll
                 for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
-                DOT_MB(A1w + j, k, st, k, lo, mi, hi);
+                if (COOP && coop) dot_mb_warp(A1w + j, k, st, k, lo, mi, hi);
+                else DOT_MB(A1w + j, k, st, k, lo, mi, hi);
                 const u32 ch = k + j;
                 const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
                 const u32 X = __ldg(T(L.xw) + j), a2r = __ldg(T(L.a2r) + j);
 #pragma unroll
                 for (int q = 0; q < MB; q++) {
+                    if (coop && lane != (u32)q) continue;                              // lane q finishes message q
                     const u32 v = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);        // Σ ξ A1'  (mod m'_j)
                     const u64 p = (u64)ST(st, ch, q) * X;                              // t* C1 2^64
                     const u32 xp = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);
@@ -238,16 +267,27 @@ struct Wide {
                 u32 qr[MB];
 #pragma unroll
                 for (int q = 0; q < MB; q++) qr[q] = 0;
-                for (u32 i = 0; i < k; i++) {
+                for (u32 i = coop ? lane : 0u; i < k; i += coop ? 32u : 1u) {
                     const u32 a1r = __ldg(T(L.a1r) + i);
 #pragma unroll
                     for (int q = 0; q < MB; q++) qr[q] += ST(st, i, q) * a1r;
                 }
-                const u32 minv32 = __ldg(T(L.misc) + 0), nminv = cx[CX_NMINV_R];
+                if (coop) {
 #pragma unroll
-                for (int q = 0; q < MB; q++) aux[1 * MB + q] = aux[0 * MB + q] * minv32 + qr[q] * nminv;
+                    for (int q = 0; q < MB; q++)
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) qr[q] += __shfl_xor_sync(0xFFFFFFFFu, qr[q], o);
+                }
+                const u32 minv32 = __ldg(T(L.misc) + 0), nminv = cx[CX_NMINV_R];
+                if (!coop || lane == 0) {
+#pragma unroll
+                    for (int q = 0; q < MB; q++) aux[1 * MB + q] = aux[0 * MB + q] * minv32 + qr[q] * nminv;
+                }
             }
-        }
+        };
+        for (u32 j = tid; j <= k && j < nt; j += nt) be1_out(j, false);
+        if constexpr (COOP)
+            if (k + 1 > nt && nt + warp <= k) be1_out(nt + warp, true);   // leftover outputs, one warp each
         block_partials(part, red);
         __syncthreads();
         if (tid < MB) {   // α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 mod 2^32, exact (Shenoy-Kumaresan)
@@ -258,21 +298,29 @@ struct Wide {
         __syncthreads();
         // ---- BE2 (exact): thread per output i of B; the m_r slot takes r_r
         const u32 *A2w = T(L.a2w);
-        for (u32 i = tid; i < k; i += nt) {
+        auto be2_out = [&](u32 i, bool coop) {
             const u32 pinw = __ldg(T(L.pinw) + i);
             u32 lo[MB], mi[MB], hi[MB];
 #pragma unroll
-            for (int q = 0; q < MB; q++) {
-                const u64 p = (u64)aux[2 * MB + q] * pinw;      // α' (m_i - |M'|_{m_i}) 2^32
+            for (int q = 0; q < MB; q++) {   // α' (m_i - |M'|_{m_i}) 2^32 (the warp-cooperative sum adds it at the end)
+                const u64 p = (COOP && coop) ? 0ull : (u64)aux[2 * MB + q] * pinw;
                 lo[q] = (u32)p;
                 mi[q] = (u32)(p >> 32);
                 hi[q] = 0;
             }
-            DOT_MB(A2w + i, k, st + k * MB, k, lo, mi, hi);
+            if (COOP && coop) dot_mb_warp(A2w + i, k, st + k * MB, k, lo, mi, hi);
+            else DOT_MB(A2w + i, k, st + k * MB, k, lo, mi, hi);
             const u32 m = __ldg(T(L.mm) + i), mv = __ldg(T(L.minv) + i), r32 = __ldg(T(L.r32) + i);
 #pragma unroll
-            for (int q = 0; q < MB; q++) ST(st, i, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
-        }
+            for (int q = 0; q < MB; q++) {
+                if (coop && lane != (u32)q) continue;
+                if (COOP && coop) mac96(lo[q], mi[q], hi[q], aux[2 * MB + q], pinw);
+                ST(st, i, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
+            }
+        };
+        for (u32 i = tid; i < k && i < nt; i += nt) be2_out(i, false);
+        if constexpr (COOP)
+            if (k > nt && nt + warp < k) be2_out(nt + warp, true);
         if (tid < MB) ST(st, 2 * k, tid) = aux[1 * MB + tid];
         __syncthreads();
     }
@@ -299,6 +347,7 @@ struct Wide {
 // Exit (a7): z on B' ∪ {m_r} -> canonical X mod N, written to y rows.  Column sums of
 // X = Σ_j ξ'_j M'_j + α'(2^(32(k+1)) - M') go to the scratch rows (3 words per column and message), one
 // thread per message then propagates carries and conditionally subtracts N 2^s, s = SMAX..0.
+template <bool COOP>
 __device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslot, u32 *yrow[MB], const bool *okv,
                           u32 out_limbs) {
     const u32 k = w.k, tid = threadIdx.x, nt = blockDim.x;
@@ -319,26 +368,33 @@ __device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslo
         w.aux[2 * MB + tid] = (sr - ST(w.st, 2 * k, tid)) * __ldg(w.T(L.misc) + 1);
     }
     __syncthreads();
-    for (u32 l = tid; l <= k; l += nt) {
+    const u32 lane = tid & 31, warp = tid >> 5;
+    auto column = [&](u32 l, bool coop) {
         u32 lo[MB], mi[MB], hi[MB];
         const u32 nmp = __ldg(w.T(L.nmp) + l);
 #pragma unroll
         for (int q = 0; q < MB; q++) {
-            const u64 p = (u64)w.aux[2 * MB + q] * nmp;
+            const u64 p = (COOP && coop) ? 0ull : (u64)w.aux[2 * MB + q] * nmp;
             lo[q] = (u32)p;
             mi[q] = (u32)(p >> 32);
             hi[q] = 0;
         }
         u32 *stg = w.stg;
-        DOT_MB(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
+        if (COOP && coop) dot_mb_warp(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
+        else DOT_MB(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
 #pragma unroll
         for (int q = 0; q < MB; q++) {
+            if (coop && lane != (u32)q) continue;
+            if (COOP && coop) mac96(lo[q], mi[q], hi[q], w.aux[2 * MB + q], nmp);   // + α' (2^(32(k+1)) - M')
             u32 *col = scratch + (size_t)(3 * l) * sstride + sslot[q];
             col[0] = lo[q];
             col[sstride] = mi[q];
             col[2 * sstride] = hi[q];
         }
-    }
+    };
+    for (u32 l = tid; l <= k && l < nt; l += nt) column(l, false);
+    if constexpr (COOP)
+        if (k + 1 > nt && nt + warp <= k) column(nt + warp, true);   // leftover columns, one warp each
     __threadfence_block();
     __syncthreads();
     if (tid < MB) {   // carries, then X mod N by conditional subtraction of N 2^s
@@ -373,8 +429,8 @@ __device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslo
 }
 
 // modexp interpreter (same op programs as k_modexp, mr_internal.h make_op), CTA = MB messages of one context
-// NTB/MINB: register budget — 512 threads x 1 CTA (k = 505) or 320 threads x 2 CTAs per SM (k = 257)
-template <int NTB, int MINB>
+// NTB/MINB: register budget — 512 threads x 1 CTA (k = 505) or 256 threads x 2 CTAs per SM (k = 257)
+template <int NTB, int MINB, bool COOP>
 __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P, const WideArgs W) {
     extern __shared__ __align__(16) u32 smem[];
     const u32 k = W.k, nch = 2 * k + 1, nw = blockDim.x / 32, tid = threadIdx.x;
@@ -430,9 +486,9 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
             __syncthreads();
         }
         if (!(fl & OPF_NOMUL)) {
-            if (opnd == OPND_SQ) w.mont_mul(nullptr, 0, 0, true);
-            else if (opnd >= 0xF0) w.mont_mul(cx + cx_r2(k) + (opnd - 0xF0) * nch, 1, 0, false);
-            else w.mont_mul(P.table + opnd * entry + slot0, tstride, 1, false);
+            if (opnd == OPND_SQ) w.template mont_mul<COOP>(nullptr, 0, 0, true);
+            else if (opnd >= 0xF0) w.template mont_mul<COOP>(cx + cx_r2(k) + (opnd - 0xF0) * nch, 1, 0, false);
+            else w.template mont_mul<COOP>(P.table + opnd * entry + slot0, tstride, 1, false);
         }
         if (fl & OPF_ADD) {   // channel-wise lazy modular addition (CRT entry)
             const WideLayout L = wide_layout(k);
@@ -458,7 +514,7 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
         yrow[q] = jl < P.count ? P.y + sel * P.out_stride + (size_t)jl * P.out_limbs : nullptr;
     }
     // column scratch: the window table (no longer needed) — 3(k+1) rows <= table_slots(w) (2k+1) rows
-    wide_exit(w, P.table, tstride, sslot, yrow, okv, P.out_limbs);
+    wide_exit<COOP>(w, P.table, tstride, sslot, yrow, okv, P.out_limbs);
 }
 
 }  // namespace
@@ -471,10 +527,14 @@ int wide_messages_per_cta() { return MB; }
 
 int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, void *stream) {
     WideArgs W{d_wide_tab, k, 0};
-    const u32 nt32 = 32 * ((k + 1 + 31) / 32), nt = nt32 < (u32)NTMAX ? nt32 : (u32)NTMAX;
+    // threads: one per base-extension output (k + 1 with the m_r column), rounded to whole warps — except
+    // when k + 1 overshoots a multiple of 32 by at most 4 (k = 257: 258 -> 256 threads, the two extra
+    // outputs done by one warp each), which keeps the warps a multiple of the 4 SM sub-partitions
+    const u32 up = 32 * ((k + 1 + 31) / 32), down = 32 * ((k + 1) / 32);
+    const u32 nt32 = (k + 1) - down <= 4 && down >= 64 ? down : up, nt = nt32 < (u32)NTMAX ? nt32 : (u32)NTMAX;
     W.nt = nt;
     const size_t smem = wide_smem_bytes(k);
-    const void *kern = nt <= 320 ? (const void *)k_modexp_wide<320, 2> : (const void *)k_modexp_wide<NTMAX, 1>;
+    const void *kern = nt <= 256 ? (const void *)k_modexp_wide<256, 2, true> : (const void *)k_modexp_wide<NTMAX, 1, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 6;
     void *args[] = {const_cast<ModexpParams *>(&p), &W};
     return cudaLaunchKernel(kern, dim3(ctas), dim3(nt), args, smem, (cudaStream_t)stream) == cudaSuccess ? 0 : 6;
