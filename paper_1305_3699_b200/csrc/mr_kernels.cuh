@@ -30,7 +30,7 @@ namespace {  // everything below is private to this K's translation unit
 
 constexpr int K = MR_K;
 constexpr int NCH = 2 * K + 1;                // residues per value: B, B', m_r
-constexpr int T = K > 65 ? 64 : 128;          // threads (messages) per CTA of the IMAD-path kernels
+constexpr int T = K > 97 ? 64 : 128;          // threads (messages) per CTA of the IMAD-path kernels (k = 129: smem)
 constexpr int CH = be_ch(K);                  // base-extension outputs per register tile
 constexpr int KF = (K / CH) * CH;             // outputs covered by full tiles
 constexpr int KT = K - KF;                    // tail tile
