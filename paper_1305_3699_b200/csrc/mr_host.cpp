@@ -43,7 +43,8 @@ static const KernelSet &kernel_set_for(int k) {
         if (s.k == k) return s;
     return sets[0];
 }
-// k > 129: the wide-operand kernel (mr_wide.cu, runtime k): 8192-bit (257) and 16,128-bit (505) moduli
+// k >= 129: the wide-operand kernel (mr_wide.cu, runtime k): 4096- (129), 8192- (257), 16,128-bit (505) moduli
+// (k = 129 keeps its per-k kernel set for Miller-Rabin)
 static const int kSupportedK[] = {1, 2, 3, 5, 9, 17, 33, 49, 65, 97, 129, 257, 505};
 static const int kNumK = sizeof(kSupportedK) / sizeof(kSupportedK[0]);
 
@@ -350,7 +351,7 @@ struct DevBase {
     u32 *d_tcb2 = nullptr;     // tensor-core BE2 image (k <= 64, and k = 65 in CTA-pair mode)
     u32 *d_tcb1u = nullptr;    // tensor-core unmerged BE1 image (Miller-Rabin, per-thread modulus)
     u32 *d_one = nullptr;      // RNS image of 1 (2k+1 words; Miller-Rabin tensor path multiplicand)
-    u32 *d_wide = nullptr;     // wide-operand table (k > 129, mr_internal.h wide_layout)
+    u32 *d_wide = nullptr;     // wide-operand table (wide_path(k), mr_internal.h wide_layout)
 };
 
 // per-k table of the wide kernel (mr_internal.h WideLayout): word-Montgomery constants with their 2^32
@@ -391,6 +392,15 @@ static std::vector<u32> build_wide_table(const Base &b) {
 }
 static std::map<std::pair<int, int>, DevBase> g_devbases;
 
+// modexp / CRT contexts that run on the wide-operand kernel (mr_wide.cu): every k > 129, and k = 129
+// (4096-bit halves), where the per-k IMAD kernel fits only 64 messages and 2 warps per SM next to its
+// 136 KB base-extension image; Miller-Rabin at k = 129 keeps the per-k kernel (is_wide stays k > 129)
+static bool wide_path(int k) {
+    if (is_wide((u32)k)) return true;
+    static const int kmin = [] { const char *e = getenv("MR_RNS_WIDE_MIN"); return e ? atoi(e) : 129; }();
+    return k >= 97 && k >= kmin;
+}
+
 static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **d_be) {
     auto key = std::make_pair(device, k);
     auto it = g_devbases.find(key);
@@ -410,10 +420,12 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
         }
     }
     DevBase db;
-    if (is_wide((u32)k)) {   // wide-operand kernel: one table in HBM, no constant bank, no shared-memory images
+    if (wide_path(k)) {   // wide-operand kernel: one table in HBM, no constant bank, no shared-memory images
         const std::vector<u32> t = build_wide_table(b);
         if (cudaMalloc(&db.d_wide, t.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_wide, t.data(), t.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
+    }
+    if (is_wide((u32)k)) {   // no per-k kernel set
         g_devbases[key] = db;
         *d_pow = nullptr;
         *d_be = nullptr;
@@ -492,7 +504,7 @@ struct mr_rns_ctx {
     const u32 *d_be = nullptr;
     const u32 *d_tcb2 = nullptr;
     const u32 *d_mpl = nullptr;
-    const u32 *d_wide = nullptr;   // wide-operand table of this k (k > 129)
+    const u32 *d_wide = nullptr;   // wide-operand table of this k (wide_path(k))
     std::vector<u32> h_cx;
     std::mutex mu;             // guards the program cache
     std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program
@@ -689,7 +701,7 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->N = N;
     const size_t tc_words = tc_ok(k) ? tc_bbytes(k) / 4 : 0;
     int rc = MR_OK;
-    if (is_wide((u32)k)) {   // cx block + wide section (σ 2^64, A1' 2^32 row-major)
+    if (wide_path(k)) {   // cx block + wide section (σ 2^64, A1' 2^32 row-major)
         c->h_cx.assign(cx_words(k) + wide_cx_words(k), 0);
         fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
         fill_wide_ctx(b, c->h_cx.data());
@@ -919,7 +931,7 @@ static bool tensor_path_enabled() {
     return !(e && e[0] == '1');
 }
 
-// wide-operand ladders (k > 129): 16 messages per CTA, one CTA per 16 messages and context
+// wide-operand ladders (wide_path(k)): 16 messages per CTA, one CTA per 16 messages and context
 static int launch_ladders_wide(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x,
                                size_t in_limbs, size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status,
                                void *stream) {
@@ -968,7 +980,7 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     const KernelSet &ks = kernel_set_for(c0->k);
     if (cudaSetDevice(c0->device) != cudaSuccess) return MR_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
-    if (is_wide((u32)c0->k)) return launch_ladders_wide(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count,
+    if (wide_path(c0->k)) return launch_ladders_wide(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count,
                                                         d_status, stream);
     const bool use_tc = ks.launch_modexp_tc && c0->d_tcb2 && tensor_path_enabled();
     // IMAD path: one CTA per T messages; tensor path: ctas0 = 128-message tile-jobs per context,
@@ -1099,7 +1111,7 @@ int mr_rsa_priv_create(mr_rsa_priv **out, const uint32_t *p, const uint32_t *q, 
         if (cudaMalloc(&pr->d_q, half_limbs * 4) != cudaSuccess) rc = MR_ERR_NOMEM;
         else if (cudaMemcpy(pr->d_q, q, half_limbs * 4, cudaMemcpyHostToDevice) != cudaSuccess) rc = MR_ERR_CUDA;
     }
-    if (rc == MR_OK && is_wide((u32)k)) {
+    if (rc == MR_OK && wide_path(k)) {
         if (cudaMalloc(&pr->d_qinv, half_limbs * 4) != cudaSuccess) rc = MR_ERR_NOMEM;
         else if (cudaMemcpy(pr->d_qinv, q_inv, half_limbs * 4, cudaMemcpyHostToDevice) != cudaSuccess) rc = MR_ERR_CUDA;
     }
@@ -1155,7 +1167,7 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
         C.pow_tab = priv->cp->d_pow;
         C.be_tab = priv->cp->d_be;
         C.mpl = priv->cp->d_mpl;
-        if (is_wide((u32)priv->cp->k)) {   // positional recombination (mr_wide.cu k_combine_wide)
+        if (wide_path(priv->cp->k)) {   // positional recombination (mr_wide.cu k_combine_wide)
             u32 *d_scr = nullptr;
             if (cudaMallocAsync(&d_scr, count * (2 * H + 2) * 4, st) != cudaSuccess) {
                 rc = MR_ERR_NOMEM;
@@ -1302,7 +1314,7 @@ int mr_internal_pow_table(int k, uint32_t *out, size_t cap) {
 // a negative MR_* error code
 // test hook: the wide-operand per-k table (mr_internal.h WideLayout) without a device
 int mr_internal_wide_table(int k, uint32_t *out, size_t cap) {
-    if (!is_wide((u32)k)) return -MR_ERR_ARG;
+    if (k < 97) return -MR_ERR_ARG;
     bool ok = false;
     for (int i = 0; i < kNumK; i++) ok |= kSupportedK[i] == k;
     if (!ok) return -MR_ERR_ARG;

@@ -265,9 +265,9 @@ def test_c4_full_size_round_trip(torch_cuda, mr, orc, keys):
     assert np.array_equal(host(y)[idx], orc.modexp_batch(xs[idx], k["d"], n, threads=8))
 
 
-@pytest.mark.parametrize("bits", [8192, 16128])
+@pytest.mark.parametrize("bits", [4096, 8192, 16128])
 def test_wide_moduli_vs_oracle(torch_cuda, mr, orc, bits):
-    """§8(f) row 3, wide operands (k = 257 / 505, channels-on-threads kernel): a ragged batch
+    """§8(f) row 3, wide operands (k = 129 / 257 / 505, channels-on-threads kernel): a ragged batch
     of 37 messages (three 16-message CTAs) for e = 65537 and a 300-bit exponent, every output vs the oracle,
     with edge inputs 0, 1, N-1 and one out-of-range input."""
     rng = random.Random(bits)
@@ -276,13 +276,13 @@ def test_wide_moduli_vs_oracle(torch_cuda, mr, orc, bits):
     xs = [0, 1, N - 1] + [rng.randrange(N) for _ in range(33)] + [N + 5]
     for E in (65537, rng.getrandbits(300) | (1 << 299)):
         y, st, ctx = run_modexp(torch_cuda, mr, N, xs, E, limbs=limbs)
-        assert ctx.k == (257 if bits == 8192 else 505)
+        assert ctx.k == {4096: 129, 8192: 257, 16128: 505}[bits]
         assert st == [0] * 36 + [5] and y[36] == 0
         ref = ints(orc.modexp_batch(mr.ints_to_limbs(xs[:36], limbs), E, N, threads=8))
         assert y[:36] == ref
 
 
-@pytest.mark.parametrize("n", [8192, 16128])
+@pytest.mark.parametrize("n", [4000, 8192, 16128])
 def test_wide_closed_forms(torch_cuda, mr, n):
     """2^E mod (2^n + 1) = ±2^(E mod n) for a 16,128-bit exponent (the paper's long-exponent shape)."""
     E = synth.exponent(16128, 0x5EEDC0DE)
@@ -347,7 +347,7 @@ def test_split_schedule_geometries(torch_cuda, mr, orc, keys, count):
 @pytest.mark.parametrize("half_bits", [2048, 4096])
 def test_crt_decrypt_large_halves_vs_oracle(torch_cuda, mr, orc, half_bits):
     """CRT decryption with 2048-bit halves (k = 65: both contexts on the CTA-pair tensor kernel in one
-    launch) and 4096-bit halves (k = 129, IMAD path): random coprime odd p, q (Garner's definition O7 needs
+    launch) and 4096-bit halves (k = 129, wide-operand kernel, positional recombination): random coprime odd p, q (Garner's definition O7 needs
     no primality), ragged batch of 300 with edge inputs, every output vs the oracle."""
     import math
     rng = random.Random(half_bits)

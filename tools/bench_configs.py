@@ -8,8 +8,8 @@ prints one JSON line per point and checks a sample of every point against the CP
   C4  2048-bit modulus (k = 65), exponents of 1,024 ... 16,128 bits
   C5  Miller-Rabin on seeded 1024-bit candidates (k = 33), 5 rounds, forced and early-exit
   RNG Hash_DRBG (SHA-256) generation and FIPS 140-2 health tests (§8(f) row 4), GB/s
-  W   wide operands (§8(f) row 3): 8192-bit (k = 257) and 16,128-bit (k = 505) moduli, e = 65537 and a
-      full-length exponent
+  W   wide operands (§8(f) row 3): 4096-bit (k = 129), 8192-bit (k = 257) and 16,128-bit (k = 505) moduli,
+      e = 65537 and a full-length exponent
 
     python tools/bench_configs.py [--configs C1,C3,C4,C5] [--quick]
 """
@@ -121,14 +121,16 @@ def c4(torch, mr, orc, quick):
 
 def wide(torch, mr, orc, quick):
     import random
-    for bits in (8192, 16128):
+    for bits in (4096, 8192, 16128):
         rng = random.Random(bits)
         N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
         limbs = (bits + 31) // 32
         ctx = mr.RnsContext(N, limbs)
         for ell in (17, bits):
             E = 65537 if ell == 17 else rng.getrandbits(bits) | (1 << (bits - 1))
-            cnt = 4736 if (ell == 17 or bits == 8192) else 2368   # CTAs of 16 messages: 2 per SM (k = 257), 1 (k = 505)
+            # CTAs of 16 messages: 4 per SM (k = 129), 2 (k = 257), 1 (k = 505)
+            cnt = 65536 if bits == 4096 and ell == 17 else 16384 if bits == 4096 else \
+                4736 if (ell == 17 or bits == 8192) else 2368
             xs = synth.messages(N, cnt, 0x5EEDC0DE, limbs)
             x = torch.from_numpy(xs.view(np.int32)).cuda()
             y = torch.empty_like(x)
