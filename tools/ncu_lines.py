@@ -39,11 +39,14 @@ def main(rep, obj, kern, top=40):
             off2line[int(m.group(1), 16)] = cur
     base = int(data[0]["Address"], 16)
     inst, samp = collections.Counter(), collections.Counter()
+    opc = os.environ.get("OPCODE")   # e.g. OPCODE=IMAD.WIDE.U32: count only that SASS opcode
     for d in data:
+        if opc and d["Source"].split()[0 if not d["Source"].startswith("@") else 1] != opc:
+            continue
         ln = off2line.get(int(d["Address"], 16) - base)
         inst[ln] += int(d["Instructions Executed"] or 0)
         samp[ln] += int(d["Warp Stall Sampling (All Samples)"] or 0)
-    ti, ts = sum(inst.values()), sum(samp.values())
+    ti, ts = sum(inst.values()), max(1, sum(samp.values()))
     src = open(os.path.join(os.path.dirname(__file__), "..", "paper_1305_3699_b200", "csrc", "mr_kernels.cuh")).read().splitlines()
     print(f"total warp-instructions {ti:,}  stall samples {ts:,}")
     for ln, c in inst.most_common(int(top)):
