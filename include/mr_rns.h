@@ -60,8 +60,8 @@ enum { MR_COMPOSITE = 0, MR_PROBABLY_PRIME = 1, MR_FACTOR = 2 }; /* Miller-Rabin
  * k: channels per base.  0 = auto = the smallest compiled k with 4(k+3)^2 N < M and
  *    4(k+3) N < M' (e.g. 33 for 1024-bit, 65 for 2048-bit, 257 for 8192-bit, 505 for 16,128-bit N).
  *    A nonzero k is rounded up to the next compiled k (see mr_rns_supported_k); below the bound ->
- *    MR_ERR_CAPACITY.  k <= 65: tensor-core base extensions; 97: IMAD thread-per-message;
- *    129, 257, 505: the wide-operand channels-on-threads kernel ("keys up to 16,128 bits"; §8(f)).
+ *    MR_ERR_CAPACITY.  k <= 65: tensor-core base extensions; 97, 129, 257, 505: the wide-operand
+ *    channels-on-threads kernel ("keys up to 16,128 bits"; §8(f)).
  * device: CUDA ordinal that will run every batch call on this context.
  * On success *out owns host and device memory until mr_rns_ctx_destroy.
  * Errors: MR_ERR_ARG, MR_ERR_EVEN_MODULUS, MR_ERR_NOT_COPRIME, MR_ERR_CAPACITY, MR_ERR_CUDA,

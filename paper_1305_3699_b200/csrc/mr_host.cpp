@@ -43,8 +43,8 @@ static const KernelSet &kernel_set_for(int k) {
         if (s.k == k) return s;
     return sets[0];
 }
-// k >= 129: the wide-operand kernel (mr_wide.cu, runtime k): 4096- (129), 8192- (257), 16,128-bit (505) moduli
-// (k = 129 keeps its per-k kernel set for Miller-Rabin)
+// k >= 97: the wide-operand kernel (mr_wide.cu, runtime k): 3072- (97), 4096- (129), 8192- (257), 16,128-bit (505)
+// moduli (k = 97 / 129 keep their per-k kernel sets for Miller-Rabin)
 static const int kSupportedK[] = {1, 2, 3, 5, 9, 17, 33, 49, 65, 97, 129, 257, 505};
 static const int kNumK = sizeof(kSupportedK) / sizeof(kSupportedK[0]);
 
@@ -380,24 +380,27 @@ static std::vector<u32> build_wide_table(const Base &b) {
     t[W.misc + 0] = f[L.misc + 0];
     t[W.misc + 1] = f[L.misc + 1];
     for (int j = 0; j < k; j++)
-        for (int i = 0; i < k; i++) t[W.a2w + (size_t)j * k + i] = mulm(f[L.A2 + j * k + i], t[W.r32 + i], b.B[i]);
+        for (int i = 0; i < k; i++) t[W.a2w + wch_at(j, i, k)] = mulm(f[L.A2 + j * k + i], t[W.r32 + i], b.B[i]);
     for (int l = 0; l < k; l++)
         for (int ch = 0; ch < 2 * k; ch++) {
             const u32 m = ch < k ? b.B[ch] : b.Bp[ch - k];
-            t[W.pow + (size_t)l * 2 * k + ch] = mulm(b.pow[(size_t)l * 2 * k + ch], t[W.r32 + ch], m);
+            t[W.pow + wch_at(l, ch, 2 * k)] = mulm(b.pow[(size_t)l * 2 * k + ch], t[W.r32 + ch], m);
         }
-    for (size_t w = 0; w < (size_t)k * (k + 1); w++) t[W.mpl + w] = f[L.MpL + w];
+    for (int j = 0; j < k; j++)
+        for (int l = 0; l <= k; l++) t[W.mpl + wch_at(j, l, k + 1)] = f[L.MpL + j * (k + 1) + l];
     for (int l = 0; l <= k; l++) t[W.nmp + l] = f[L.NMp + l];
     return t;
 }
 static std::map<std::pair<int, int>, DevBase> g_devbases;
 
-// modexp / CRT contexts that run on the wide-operand kernel (mr_wide.cu): every k > 129, and k = 129
-// (4096-bit halves), where the per-k IMAD kernel fits only 64 messages and 2 warps per SM next to its
-// 136 KB base-extension image; Miller-Rabin at k = 129 keeps the per-k kernel (is_wide stays k > 129)
+// modexp / CRT contexts that run on the wide-operand kernel (mr_wide.cu): every k >= 97.  At k = 97 / 129
+// the per-k IMAD kernel fits only 128 / 64 messages (4 / 2 warps per SM) next to its 75 / 136 KB shared-
+// memory base-extension image; the wide kernel runs 16 warps per SM with the images streamed from L2
+// (A/B in DESIGN.md §4h).  Miller-Rabin at k = 97 / 129 keeps the per-k kernel (is_wide stays k > 129).
+// MR_RNS_WIDE_MIN=k' moves the threshold (A/B hook; 999 = per-k kernels up to 129).
 static bool wide_path(int k) {
     if (is_wide((u32)k)) return true;
-    static const int kmin = [] { const char *e = getenv("MR_RNS_WIDE_MIN"); return e ? atoi(e) : 129; }();
+    static const int kmin = [] { const char *e = getenv("MR_RNS_WIDE_MIN"); return e ? atoi(e) : 97; }();
     return k >= 97 && k >= kmin;
 }
 
@@ -663,7 +666,7 @@ static void fill_wide_ctx(const Base &b, u32 *x) {
     }
     for (int j = 0; j < k; j++) {
         const u32 m = b.Bp[j], r = (u32)((1ull << 32) % m), nu = mulm(x[cx_c2(k) + j], r, m);
-        for (int i = 0; i < k; i++) w[wide_cx_a1(k) + (size_t)i * k + j] = mulm(A1[i * k + j], nu, m);
+        for (int i = 0; i < k; i++) w[wide_cx_a1(k) + wch_at(i, j, k)] = mulm(A1[i * k + j], nu, m);
     }
 }
 

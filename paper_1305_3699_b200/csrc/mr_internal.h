@@ -143,15 +143,22 @@ __host__ __device__ constexpr u32 tc_abytes(u32 k) { return 128 * tc_kp(k); }   
 // Wide-operand kernel (mr_wide.cu, k > 129: channels on threads, 16 messages per CTA).
 // Per-k table in HBM (word Montgomery reductions: the 2^-32 factors are folded into the constants):
 // ---------------------------------------------------------------------------------------------
+// The four contraction matrices ([R][C], row = input channel / limb, column = output) are stored CHUNKED:
+// rows in groups of 8, element (i, j) at ((i / 8) C + j) 8 + i % 8, rows padded with zeros to a multiple
+// of 8, so the thread of column j loads a group's 8 coefficients as two 16-byte words (coalesced across
+// the warp: 32 columns = 1 KB contiguous).  Offsets are multiples of 4 words (16-byte aligned).
+__host__ __device__ constexpr u32 wch_rows(u32 r) { return (r + 7) & ~7u; }
+__host__ __device__ constexpr u32 wch_words(u32 r, u32 c) { return wch_rows(r) * c; }
+__host__ __device__ constexpr u32 wch_at(u32 i, u32 j, u32 c) { return ((i >> 3) * c + j) * 8 + (i & 7); }
 struct WideLayout {
     u32 mm, minv, r32;        // [2k] m, -m^-1 mod 2^32, 2^32 mod m   (B then B')
     u32 xw;                   // [k]  |M^-1 λ_j^-1| 2^64 mod m'_j       (t*_j carries 2^-32 twice)
     u32 a1r, a2r;             // [k]  |M_i|_{2^32}, |M'_j|_{2^32}
     u32 pinw;                 // [k]  (m_i - |M'|_{m_i}) 2^32 mod m_i
     u32 misc;                 // [4]  M^-1 mod 2^32, M'^-1 mod 2^32
-    u32 a2w;                  // [k][k] row j, column i: |M'_j|_{m_i} 2^32 mod m_i
-    u32 pow;                  // [k][2k] |2^(32 l) 2^32|_{m_c} (B' × λ_j)
-    u32 mpl;                  // [k][k+1] M'_j limbs
+    u32 a2w;                  // chunked [k][k] row j, column i: |M'_j|_{m_i} 2^32 mod m_i
+    u32 pow;                  // chunked [k][2k] |2^(32 l) 2^32|_{m_c} (B' × λ_j)
+    u32 mpl;                  // chunked [k][k+1] M'_j limbs
     u32 nmp;                  // [k+1] 2^(32(k+1)) - M' limbs
     u32 words;
 };
@@ -165,18 +172,18 @@ __host__ __device__ constexpr WideLayout wide_layout(u32 k) {
     w.a2r = w.a1r + k;
     w.pinw = w.a2r + k;
     w.misc = w.pinw + k;
-    w.a2w = w.misc + 4;
-    w.pow = w.a2w + k * k;
-    w.mpl = w.pow + 2 * k * k;
-    w.nmp = w.mpl + k * (k + 1);
+    w.a2w = (w.misc + 4 + 3) & ~3u;
+    w.pow = w.a2w + wch_words(k, k);
+    w.mpl = w.pow + wch_words(k, 2 * k);
+    w.nmp = w.mpl + wch_words(k, k + 1);
     w.words = w.nmp + k + 1;
     return w;
 }
-// per-context wide section, after the cx block: σ_i 2^64 mod m_i [k], then A1'[i][j] 2^32 mod m'_j [k][k]
-// (A1' = |M_i|_{m'_j} |N M^-1 λ_j|, row-major: coalesced over j)
+// per-context wide section, after the cx block: σ_i 2^64 mod m_i [k], then A1'[i][j] 2^32 mod m'_j chunked
+// [k][k] (A1' = |M_i|_{m'_j} |N M^-1 λ_j|)
 __host__ __device__ constexpr u32 wide_cx_sig(u32 k) { return 0; }
-__host__ __device__ constexpr u32 wide_cx_a1(u32 k) { return k; }
-__host__ __device__ constexpr u32 wide_cx_words(u32 k) { return k + k * k; }
+__host__ __device__ constexpr u32 wide_cx_a1(u32 k) { return (k + 3) & ~3u; }
+__host__ __device__ constexpr u32 wide_cx_words(u32 k) { return wide_cx_a1(k) + wch_words(k, k); }
 __host__ __device__ constexpr bool is_wide(u32 k) { return k > 129; }
 
 // ---------------------------------------------------------------------------------------------

@@ -67,43 +67,42 @@ struct WideArgs {
 
 __device__ __forceinline__ u32 &ST(u32 *st, u32 ch, u32 msg) { return st[ch * MB + msg]; }
 
-// acc[q] += Σ_{i < n} xs[i * MB + q] · coef[i * cstride]  for the CTA's MB messages (96-bit accumulators).
-// The constants stream from L2/HBM: PF of them are loaded one chunk ahead so their latency overlaps the
-// previous chunk's multiply-accumulates (the loop is otherwise bound by L2 latency).
-#ifndef MR_WIDE_PF
-#define MR_WIDE_PF 8
-#endif
-constexpr int PF = MR_WIDE_PF;
-__device__ __forceinline__ void dot_mb(const u32 *__restrict__ coef, size_t cstride, const u32 *xs, u32 n,
+// acc[q] += Σ_{i < n} xs[i * MB + q] · A[i][j]  for the CTA's MB messages (96-bit accumulators); A is a
+// chunked [R][ncols] matrix (mr_internal.h wch_at, R >= n): the thread's 8 coefficients of a row group are
+// two 16-byte loads, issued one group ahead so their L2 latency overlaps the previous group's 128
+// multiply-accumulates.  Rows i >= n of the last group are skipped (the xs rows there may be anything).
+__device__ __forceinline__ void dot_mb(const u32 *__restrict__ mat, u32 ncols, u32 j, const u32 *xs, u32 n,
                                        u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
-    u32 cur[PF], nxt[PF];
+    const uint4 *cp = reinterpret_cast<const uint4 *>(mat + (size_t)j * 8);
+    const u32 gs = 2 * ncols;                         // uint4 per row group
+    const u32 ng = (n + 7) / 8;
+    uint4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
+    auto group = [&](const u32 *xg, const uint4 &a, const uint4 &b, u32 rows) {
+        const u32 c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int p = 0; p < PF; p++) cur[p] = (u32)p < n ? __ldg(coef + (size_t)p * cstride) : 0u;
-#pragma unroll 1
-    for (u32 i0 = 0; i0 < n; i0 += PF) {
-#pragma unroll
-        for (int p = 0; p < PF; p++) {
-            const u32 i = i0 + PF + p;
-            nxt[p] = i < n ? __ldg(coef + (size_t)i * cstride) : 0u;
-        }
-#pragma unroll
-        for (int p = 0; p < PF; p++) {
-            if (i0 + p < n) {
-                const uint4 *x = reinterpret_cast<const uint4 *>(xs + (i0 + p) * MB);
-                const u32 c = cur[p];
+        for (int p = 0; p < 8; p++) {
+            if ((u32)p < rows) {
+                const uint4 *x = reinterpret_cast<const uint4 *>(xg + p * MB);
 #pragma unroll
                 for (int v4 = 0; v4 < MB / 4; v4++) {
                     const uint4 xv = x[v4];
-                    mac96(lo[4 * v4 + 0], mi[4 * v4 + 0], hi[4 * v4 + 0], xv.x, c);
-                    mac96(lo[4 * v4 + 1], mi[4 * v4 + 1], hi[4 * v4 + 1], xv.y, c);
-                    mac96(lo[4 * v4 + 2], mi[4 * v4 + 2], hi[4 * v4 + 2], xv.z, c);
-                    mac96(lo[4 * v4 + 3], mi[4 * v4 + 3], hi[4 * v4 + 3], xv.w, c);
+                    mac96(lo[4 * v4 + 0], mi[4 * v4 + 0], hi[4 * v4 + 0], xv.x, c[p]);
+                    mac96(lo[4 * v4 + 1], mi[4 * v4 + 1], hi[4 * v4 + 1], xv.y, c[p]);
+                    mac96(lo[4 * v4 + 2], mi[4 * v4 + 2], hi[4 * v4 + 2], xv.z, c[p]);
+                    mac96(lo[4 * v4 + 3], mi[4 * v4 + 3], hi[4 * v4 + 3], xv.w, c[p]);
                 }
             }
         }
-#pragma unroll
-        for (int p = 0; p < PF; p++) cur[p] = nxt[p];
+    };
+#pragma unroll 1
+    for (u32 g = 0; g + 1 < ng; g++) {                // whole groups, the next one prefetched
+        const uint4 *np = cp + (size_t)(g + 1) * gs;
+        const uint4 n0 = __ldg(np), n1 = __ldg(np + 1);
+        group(xs + g * 8 * MB, c0, c1, 8);
+        c0 = n0;
+        c1 = n1;
     }
+    if (ng) group(xs + (ng - 1) * 8 * MB, c0, c1, n - (ng - 1) * 8);
 }
 
 // block-wide Σ over threads of v[msg] (MB values): warp shuffles, then one partial per warp in red[w][msg];
@@ -124,11 +123,11 @@ __device__ __forceinline__ void block_partials(u32 (&v)[MB], u32 *red) {
 
 // Warp-cooperative version for an output column left over when k + 1 exceeds the CTA's threads by a few:
 // lane l sums the inputs i ≡ l (mod 32), then a butterfly of 96-bit adds leaves the total in every lane.
-__device__ __forceinline__ void dot_mb_warp(const u32 *__restrict__ coef, size_t cstride, const u32 *xs, u32 n,
+__device__ __forceinline__ void dot_mb_warp(const u32 *__restrict__ mat, u32 ncols, u32 j, const u32 *xs, u32 n,
                                             u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
     const u32 lane = threadIdx.x & 31;
     for (u32 i = lane; i < n; i += 32) {
-        const u32 c = __ldg(coef + (size_t)i * cstride);
+        const u32 c = __ldg(mat + wch_at(i, j, ncols));
 #pragma unroll
         for (int q = 0; q < MB; q++) mac96(lo[q], mi[q], hi[q], xs[i * MB + q], c);
     }
@@ -145,56 +144,7 @@ __device__ __forceinline__ void dot_mb_warp(const u32 *__restrict__ coef, size_t
     }
 }
 
-// Same contraction with the constants staged through shared memory by cp.async (LDGSTS): each thread
-// copies its own column of TI rows one stage ahead into stg[stage][r][tid] (no registers held by the
-// prefetch, so the copy distance is TI rows instead of PF), then reads them back with LDS.  Measured slower
-// than the register prefetch (A/B: 0.25 vs 0.33 IMAD-eq fraction at 8192 bits): off by default.
-#ifndef MR_WIDE_STAGED
-#define MR_WIDE_STAGED 0
-#endif
-constexpr int TI = 16;
-__device__ __forceinline__ void cp_async4(u32 *sdst, const u32 *gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((u32)__cvta_generic_to_shared(sdst)), "l"(gsrc)
-                 : "memory");
-}
-__device__ __forceinline__ void dot_mb_staged(const u32 *__restrict__ coef, size_t cstride, const u32 *xs, u32 n,
-                                              u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB], u32 *stg) {
-    const u32 tid = threadIdx.x, nt = blockDim.x;
-    auto issue = [&](u32 stage, u32 i0) {
-#pragma unroll
-        for (int r = 0; r < TI; r++)
-            if (i0 + r < n) cp_async4(stg + (stage * TI + r) * nt + tid, coef + (size_t)(i0 + r) * cstride);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    issue(0, 0);
-    u32 stage = 0;
-#pragma unroll 1
-    for (u32 i0 = 0; i0 < n; i0 += TI, stage ^= 1) {
-        issue(stage ^ 1, i0 + TI);                                    // next stage (empty group past the end)
-        asm volatile("cp.async.wait_group 1;" ::: "memory");         // this stage landed (own column only)
-#pragma unroll
-        for (int r = 0; r < TI; r++) {
-            if (i0 + r < n) {
-                const u32 c = stg[(stage * TI + r) * nt + tid];
-                const uint4 *x = reinterpret_cast<const uint4 *>(xs + (i0 + r) * MB);
-#pragma unroll
-                for (int v4 = 0; v4 < MB / 4; v4++) {
-                    const uint4 xv = x[v4];
-                    mac96(lo[4 * v4 + 0], mi[4 * v4 + 0], hi[4 * v4 + 0], xv.x, c);
-                    mac96(lo[4 * v4 + 1], mi[4 * v4 + 1], hi[4 * v4 + 1], xv.y, c);
-                    mac96(lo[4 * v4 + 2], mi[4 * v4 + 2], hi[4 * v4 + 2], xv.z, c);
-                    mac96(lo[4 * v4 + 3], mi[4 * v4 + 3], hi[4 * v4 + 3], xv.w, c);
-                }
-            }
-        }
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-#if MR_WIDE_STAGED
-#define DOT_MB(coef, cs, xs, n, lo, mi, hi) dot_mb_staged(coef, cs, xs, n, lo, mi, hi, stg)
-#else
-#define DOT_MB(coef, cs, xs, n, lo, mi, hi) dot_mb(coef, cs, xs, n, lo, mi, hi)
-#endif
+
 
 struct Wide {
     const WideArgs &W;
@@ -202,7 +152,6 @@ struct Wide {
     u32 *st;                           // [2k+1][MB]
     u32 *red;                          // [NW][MB] warp partials
     u32 *aux;                          // [4][MB]: t_r, r_r, α', ok
-    u32 *stg;                          // [2][TI][nt] constant staging (dot_mb_staged)
     u32 k, nch, nw;
 
     __device__ const u32 *T(u32 off) const { return W.tab + off; }
@@ -249,8 +198,8 @@ struct Wide {
                 u32 lo[MB], mi[MB], hi[MB];
 #pragma unroll
                 for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
-                if (COOP && coop) dot_mb_warp(A1w + j, k, st, k, lo, mi, hi);
-                else DOT_MB(A1w + j, k, st, k, lo, mi, hi);
+                if (COOP && coop) dot_mb_warp(A1w, k, j, st, k, lo, mi, hi);
+                else dot_mb(A1w, k, j, st, k, lo, mi, hi);
                 const u32 ch = k + j;
                 const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
                 const u32 X = __ldg(T(L.xw) + j), a2r = __ldg(T(L.a2r) + j);
@@ -308,8 +257,8 @@ struct Wide {
                 mi[q] = (u32)(p >> 32);
                 hi[q] = 0;
             }
-            if (COOP && coop) dot_mb_warp(A2w + i, k, st + k * MB, k, lo, mi, hi);
-            else DOT_MB(A2w + i, k, st + k * MB, k, lo, mi, hi);
+            if (COOP && coop) dot_mb_warp(A2w, k, i, st + k * MB, k, lo, mi, hi);
+            else dot_mb(A2w, k, i, st + k * MB, k, lo, mi, hi);
             const u32 m = __ldg(T(L.mm) + i), mv = __ldg(T(L.minv) + i), r32 = __ldg(T(L.r32) + i);
 #pragma unroll
             for (int q = 0; q < MB; q++) {
@@ -334,7 +283,7 @@ struct Wide {
             u32 lo[MB], mi[MB], hi[MB];
 #pragma unroll
             for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
-            DOT_MB(T(L.pow) + ch, 2 * k, xs, nl, lo, mi, hi);
+            dot_mb(T(L.pow), 2 * k, ch, xs, nl, lo, mi, hi);
             const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
 #pragma unroll
             for (int q = 0; q < MB; q++) ST(st, ch, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
@@ -379,9 +328,8 @@ __device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslo
             mi[q] = (u32)(p >> 32);
             hi[q] = 0;
         }
-        u32 *stg = w.stg;
-        if (COOP && coop) dot_mb_warp(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
-        else DOT_MB(w.T(L.mpl) + l, k + 1, w.st + k * MB, k, lo, mi, hi);
+        if (COOP && coop) dot_mb_warp(w.T(L.mpl), k + 1, l, w.st + k * MB, k, lo, mi, hi);
+        else dot_mb(w.T(L.mpl), k + 1, l, w.st + k * MB, k, lo, mi, hi);
 #pragma unroll
         for (int q = 0; q < MB; q++) {
             if (coop && lane != (u32)q) continue;
@@ -438,13 +386,12 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
     u32 *xs = st + nch * MB;                          // [k][MB] staged input limbs
     u32 *red = xs + k * MB;                           // [16][MB]
     u32 *aux = red + 16 * MB;                         // [4][MB]
-    u32 *stg = aux + 4 * MB;                          // [2][TI][nt]
     __shared__ bool okv[MB];
     __shared__ u32 sslot[MB];
     const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
     const u32 *cx = sel ? P.ctx[1] : P.ctx[0];
     const u32 j0 = (blockIdx.x - sel * P.ctas0) * MB;
-    Wide w{W, cx, st, red, aux, stg, k, nch, nw};
+    Wide w{W, cx, st, red, aux, k, nch, nw};
     if (tid < MB) {
         const u32 jl = j0 + tid;
         const bool valid = jl < P.count;
@@ -520,8 +467,7 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
 }  // namespace
 
 size_t wide_smem_bytes(u32 k) {
-    const size_t nt = 32 * ((k + 1 + 31) / 32);
-    return 4 * ((size_t)(2 * k + 1) * MB + (size_t)k * MB + 16 * MB + 4 * MB + (MR_WIDE_STAGED ? 2 * TI * nt : 0));
+    return 4 * ((size_t)(2 * k + 1) * MB + (size_t)k * MB + 16 * MB + 4 * MB);
 }
 int wide_messages_per_cta() { return MB; }
 

@@ -266,12 +266,22 @@ def _wide_layout(k):
     o["a2r"] = o["a1r"] + k
     o["pinw"] = o["a2r"] + k
     o["misc"] = o["pinw"] + k
-    o["a2w"] = o["misc"] + 4
-    o["pow"] = o["a2w"] + k * k
-    o["mpl"] = o["pow"] + 2 * k * k
-    o["nmp"] = o["mpl"] + k * (k + 1)
+    o["a2w"] = (o["misc"] + 4 + 3) & ~3
+    o["pow"] = o["a2w"] + _wch_rows(k) * k
+    o["mpl"] = o["pow"] + _wch_rows(k) * 2 * k
+    o["nmp"] = o["mpl"] + _wch_rows(k) * (k + 1)
     o["words"] = o["nmp"] + k + 1
     return o
+
+
+def _wch_rows(r):
+    return (r + 7) & ~7
+
+
+def _wch_at(i, j, ncols):
+    """mr_internal.h wch_at: chunked [R][C] matrix, rows in groups of 8, element (i, j) at
+    ((i // 8) C + j) 8 + i % 8."""
+    return ((i >> 3) * ncols + j) * 8 + (i & 7)
 
 
 def test_wide_table_identities():
@@ -306,7 +316,7 @@ def test_wide_table_identities():
         c1 = pow(M, -1, m) * pow(lam, -1, m) % m
         assert t[o["xw"] + j] == c1 * W * W % m and t[o["a2r"] + j] == (Mp // m) % W
         for i in [0, k - 1] + [int(v) for v in rng.integers(0, k, 4)]:
-            assert t[o["a2w"] + j * k + i] == (Mp // m) % B[i] * W % B[i]
+            assert t[o["a2w"] + _wch_at(j, i, k)] == (Mp // m) % B[i] * W % B[i]
     for i in [0, k - 1]:
         assert t[o["pinw"] + i] == (B[i] - Mp % B[i]) % B[i] * W % B[i] and t[o["a1r"] + i] == (M // B[i]) % W
     for l in [0, 1, k - 1]:
@@ -315,6 +325,11 @@ def test_wide_table_identities():
             v = pow(2, 32 * (l + 1), m)
             if ch >= k:
                 v = v * pow(Mp // m, -1, m) % m
-            assert t[o["pow"] + l * 2 * k + ch] == v
+            assert t[o["pow"] + _wch_at(l, ch, 2 * k)] == v
     assert sum(t[o["nmp"] + l] << (32 * l) for l in range(k + 1)) + Mp == 1 << (32 * (k + 1))
+    for j in [0, k - 1] + [int(v) for v in rng.integers(0, k, 4)]:   # M'_j positional limbs
+        m = Bp[j]
+        assert sum(t[o["mpl"] + _wch_at(j, l, k + 1)] << (32 * l) for l in range(k + 1)) == Mp // m
+    pad = [t[o["a2w"] + _wch_at(i, j, k)] for i in range(k, _wch_rows(k)) for j in (0, k - 1)]
+    assert not any(pad)                                                # zero rows up to the group size
     assert L.mr_internal_wide_table(65, None, 0) < 0 and L.mr_internal_wide_table(129, None, 0) > 0

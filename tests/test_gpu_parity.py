@@ -265,9 +265,9 @@ def test_c4_full_size_round_trip(torch_cuda, mr, orc, keys):
     assert np.array_equal(host(y)[idx], orc.modexp_batch(xs[idx], k["d"], n, threads=8))
 
 
-@pytest.mark.parametrize("bits", [4096, 8192, 16128])
+@pytest.mark.parametrize("bits", [3072, 4096, 8192, 16128])
 def test_wide_moduli_vs_oracle(torch_cuda, mr, orc, bits):
-    """§8(f) row 3, wide operands (k = 129 / 257 / 505, channels-on-threads kernel): a ragged batch
+    """§8(f) row 3, wide operands (k = 97 / 129 / 257 / 505, channels-on-threads kernel): a ragged batch
     of 37 messages (three 16-message CTAs) for e = 65537 and a 300-bit exponent, every output vs the oracle,
     with edge inputs 0, 1, N-1 and one out-of-range input."""
     rng = random.Random(bits)
@@ -276,7 +276,7 @@ def test_wide_moduli_vs_oracle(torch_cuda, mr, orc, bits):
     xs = [0, 1, N - 1] + [rng.randrange(N) for _ in range(33)] + [N + 5]
     for E in (65537, rng.getrandbits(300) | (1 << 299)):
         y, st, ctx = run_modexp(torch_cuda, mr, N, xs, E, limbs=limbs)
-        assert ctx.k == {4096: 129, 8192: 257, 16128: 505}[bits]
+        assert ctx.k == {3072: 97, 4096: 129, 8192: 257, 16128: 505}[bits]
         assert st == [0] * 36 + [5] and y[36] == 0
         ref = ints(orc.modexp_batch(mr.ints_to_limbs(xs[:36], limbs), E, N, threads=8))
         assert y[:36] == ref

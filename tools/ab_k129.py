@@ -1,7 +1,7 @@
 """A/B probe for b-bit operands (default 4096, k = 129): b-bit modexp with a full-length exponent, RSA-b
 encryption (e = 65537) and RSA-2b CRT decryption (b-bit halves).  Prints one line per workload with the
 rate and a sampled bit-exact check against Python's pow.  MR_RNS_WIDE_MIN=k' moves every k >= k' (>= 97)
-onto the wide-operand kernel (default 129; 999: the per-k IMAD kernels).
+onto the wide-operand kernel (default 97; 999: the per-k IMAD kernels).
     python tools/ab_k129.py [b]"""
 import math
 import os
@@ -29,7 +29,7 @@ def timed(fn, reps=3):
 
 
 rng = random.Random(129)
-tag = os.environ.get("MR_RNS_WIDE_MIN", "129")
+tag = os.environ.get("MR_RNS_WIDE_MIN", "97")
 BITS = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 L = BITS // 32
 # BITS-bit modexp, full exponent

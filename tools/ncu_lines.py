@@ -30,9 +30,9 @@ def main(rep, obj, kern, top=40):
     for l in lines[start + 1:]:
         if l.startswith(".text."):
             break
-        m = re.search(r'//## File ".*?", line (\d+)', l)
+        m = re.search(r'//## File "(.*?)", line (\d+)', l)
         if m:
-            cur = int(m.group(1))
+            cur = (os.path.basename(m.group(1)), int(m.group(2)))
             continue
         m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", l)
         if m:
@@ -47,10 +47,21 @@ def main(rep, obj, kern, top=40):
         inst[ln] += int(d["Instructions Executed"] or 0)
         samp[ln] += int(d["Warp Stall Sampling (All Samples)"] or 0)
     ti, ts = sum(inst.values()), max(1, sum(samp.values()))
-    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_1305_3699_b200", "csrc", "mr_kernels.cuh")).read().splitlines()
+    csrc = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1305_3699_b200", "csrc")
+    srcs = {}
+
+    def text(key):
+        if not key:
+            return ""
+        f, ln = key
+        if f not in srcs:
+            path = os.path.join(csrc, f)
+            srcs[f] = open(path).read().splitlines() if os.path.exists(path) else []
+        return srcs[f][ln - 1].strip()[:90] if ln <= len(srcs[f]) else ""
     print(f"total warp-instructions {ti:,}  stall samples {ts:,}")
-    for ln, c in inst.most_common(int(top)):
-        print(f"{ln!s:>5} {100 * c / ti:5.1f}% inst {100 * samp[ln] / ts:5.1f}% samp | {src[ln - 1].strip()[:96] if ln else ''}")
+    for key, c in inst.most_common(int(top)):
+        where = f"{key[0]}:{key[1]}" if key else "?"
+        print(f"{where:>22} {100 * c / ti:5.1f}% inst {100 * samp[key] / ts:5.1f}% samp | {text(key)}")
 
 
 if __name__ == "__main__":

@@ -1,5 +1,5 @@
-"""One wide-operand launch for profiling: 4,736 messages over a random 8192-bit modulus (k = 257).
-    python tools/wide_probe.py [bits] [exponent_bits]"""
+"""One wide-operand launch for profiling: 4,736 messages (default) over a random 8192-bit modulus (k = 257).
+    python tools/wide_probe.py [bits] [exponent_bits] [messages]"""
 import random
 import sys
 
@@ -16,7 +16,8 @@ rng = random.Random(bits)
 N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
 limbs = (bits + 31) // 32
 ctx = mr.RnsContext(N, limbs)
-xs = synth.messages(N, 4736, 1, limbs)
+cnt = int(sys.argv[3]) if len(sys.argv) > 3 else 4736
+xs = synth.messages(N, cnt, 1, limbs)
 x = torch.from_numpy(xs.view(np.int32)).cuda()
 y = torch.empty_like(x)
 E = rng.getrandbits(ebits) | (1 << (ebits - 1))
