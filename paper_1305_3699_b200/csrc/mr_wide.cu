@@ -17,6 +17,7 @@
 // as mr_kernels.cuh from_rns, done cooperatively (column sums by thread, carries by one thread per message).
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mr_internal.h"
 
@@ -71,6 +72,7 @@ __device__ __forceinline__ u32 &ST(u32 *st, u32 ch, u32 msg) { return st[ch * MB
 // chunked [R][ncols] matrix (mr_internal.h wch_at, R >= n): the thread's 8 coefficients of a row group are
 // two 16-byte loads, issued one group ahead so their L2 latency overlaps the previous group's 128
 // multiply-accumulates.  Rows i >= n of the last group are skipped (the xs rows there may be anything).
+template <bool PP>
 __device__ __forceinline__ void dot_mb(const u32 *__restrict__ mat, u32 ncols, u32 j, const u32 *xs, u32 n,
                                        u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
     const uint4 *cp = reinterpret_cast<const uint4 *>(mat + (size_t)j * 8);
@@ -94,6 +96,27 @@ __device__ __forceinline__ void dot_mb(const u32 *__restrict__ mat, u32 ncols, u
             }
         }
     };
+if constexpr (PP) {
+    // two groups per iteration with ping-pong coefficient registers (no copies between the buffers)
+    u32 g = 0;
+#pragma unroll 1
+    for (; g + 2 < ng; g += 2) {
+        const uint4 *np = cp + (size_t)(g + 1) * gs;
+        const uint4 n0 = __ldg(np), n1 = __ldg(np + 1);
+        group(xs + g * 8 * MB, c0, c1, 8);
+        c0 = __ldg(np + gs);
+        c1 = __ldg(np + gs + 1);
+        group(xs + (g + 1) * 8 * MB, n0, n1, 8);
+    }
+    if (g + 1 < ng) {
+        const uint4 *np = cp + (size_t)(g + 1) * gs;
+        const uint4 n0 = __ldg(np), n1 = __ldg(np + 1);
+        group(xs + g * 8 * MB, c0, c1, 8);
+        group(xs + (g + 1) * 8 * MB, n0, n1, n - (g + 1) * 8);
+    } else if (g < ng) {
+        group(xs + g * 8 * MB, c0, c1, n - g * 8);
+    }
+    } else {
 #pragma unroll 1
     for (u32 g = 0; g + 1 < ng; g++) {                // whole groups, the next one prefetched
         const uint4 *np = cp + (size_t)(g + 1) * gs;
@@ -103,6 +126,7 @@ __device__ __forceinline__ void dot_mb(const u32 *__restrict__ mat, u32 ncols, u
         c1 = n1;
     }
     if (ng) group(xs + (ng - 1) * 8 * MB, c0, c1, n - (ng - 1) * 8);
+    }
 }
 
 // block-wide Σ over threads of v[msg] (MB values): warp shuffles, then one partial per warp in red[w][msg];
@@ -146,6 +170,7 @@ __device__ __forceinline__ void dot_mb_warp(const u32 *__restrict__ mat, u32 nco
 
 
 
+template <bool PP>   // PP: dot_mb with ping-pong coefficient groups (faster at k >= 257, slower at 129)
 struct Wide {
     const WideArgs &W;
     const u32 *cx;                     // context block (HBM) of this CTA's modulus
@@ -199,7 +224,7 @@ struct Wide {
 #pragma unroll
                 for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
                 if (COOP && coop) dot_mb_warp(A1w, k, j, st, k, lo, mi, hi);
-                else dot_mb(A1w, k, j, st, k, lo, mi, hi);
+                else dot_mb<PP>(A1w, k, j, st, k, lo, mi, hi);
                 const u32 ch = k + j;
                 const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
                 const u32 X = __ldg(T(L.xw) + j), a2r = __ldg(T(L.a2r) + j);
@@ -258,7 +283,7 @@ struct Wide {
                 hi[q] = 0;
             }
             if (COOP && coop) dot_mb_warp(A2w, k, i, st + k * MB, k, lo, mi, hi);
-            else dot_mb(A2w, k, i, st + k * MB, k, lo, mi, hi);
+            else dot_mb<PP>(A2w, k, i, st + k * MB, k, lo, mi, hi);
             const u32 m = __ldg(T(L.mm) + i), mv = __ldg(T(L.minv) + i), r32 = __ldg(T(L.r32) + i);
 #pragma unroll
             for (int q = 0; q < MB; q++) {
@@ -283,7 +308,7 @@ struct Wide {
             u32 lo[MB], mi[MB], hi[MB];
 #pragma unroll
             for (int q = 0; q < MB; q++) lo[q] = mi[q] = hi[q] = 0;
-            dot_mb(T(L.pow), 2 * k, ch, xs, nl, lo, mi, hi);
+            dot_mb<PP>(T(L.pow), 2 * k, ch, xs, nl, lo, mi, hi);
             const u32 m = __ldg(T(L.mm) + ch), mv = __ldg(T(L.minv) + ch), r32 = __ldg(T(L.r32) + ch);
 #pragma unroll
             for (int q = 0; q < MB; q++) ST(st, ch, q) = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);
@@ -296,8 +321,8 @@ struct Wide {
 // Exit (a7): z on B' ∪ {m_r} -> canonical X mod N, written to y rows.  Column sums of
 // X = Σ_j ξ'_j M'_j + α'(2^(32(k+1)) - M') go to the scratch rows (3 words per column and message), one
 // thread per message then propagates carries and conditionally subtracts N 2^s, s = SMAX..0.
-template <bool COOP>
-__device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslot, u32 *yrow[MB], const bool *okv,
+template <bool COOP, bool PP>
+__device__ void wide_exit(Wide<PP> &w, u32 *scratch, size_t sstride, const u32 *sslot, u32 *yrow[MB], const bool *okv,
                           u32 out_limbs) {
     const u32 k = w.k, tid = threadIdx.x, nt = blockDim.x;
     const WideLayout L = wide_layout(k);
@@ -329,7 +354,7 @@ __device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslo
             hi[q] = 0;
         }
         if (COOP && coop) dot_mb_warp(w.T(L.mpl), k + 1, l, w.st + k * MB, k, lo, mi, hi);
-        else dot_mb(w.T(L.mpl), k + 1, l, w.st + k * MB, k, lo, mi, hi);
+        else dot_mb<PP>(w.T(L.mpl), k + 1, l, w.st + k * MB, k, lo, mi, hi);
 #pragma unroll
         for (int q = 0; q < MB; q++) {
             if (coop && lane != (u32)q) continue;
@@ -377,8 +402,8 @@ __device__ void wide_exit(Wide &w, u32 *scratch, size_t sstride, const u32 *sslo
 }
 
 // modexp interpreter (same op programs as k_modexp, mr_internal.h make_op), CTA = MB messages of one context
-// NTB/MINB: register budget — 512 threads x 1 CTA (k = 505) or 256 threads x 2 CTAs per SM (k = 257)
-template <int NTB, int MINB, bool COOP>
+// NTB/MINB: register budget — 512 threads x 1 CTA (k = 505) or 256 threads x 2 CTAs per SM (k <= 257)
+template <int NTB, int MINB, bool COOP, bool PP>
 __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P, const WideArgs W) {
     extern __shared__ __align__(16) u32 smem[];
     const u32 k = W.k, nch = 2 * k + 1, nw = blockDim.x / 32, tid = threadIdx.x;
@@ -391,7 +416,7 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
     const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
     const u32 *cx = sel ? P.ctx[1] : P.ctx[0];
     const u32 j0 = (blockIdx.x - sel * P.ctas0) * MB;
-    Wide w{W, cx, st, red, aux, k, nch, nw};
+    Wide<PP> w{W, cx, st, red, aux, k, nch, nw};
     if (tid < MB) {
         const u32 jl = j0 + tid;
         const bool valid = jl < P.count;
@@ -461,7 +486,7 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
         yrow[q] = jl < P.count ? P.y + sel * P.out_stride + (size_t)jl * P.out_limbs : nullptr;
     }
     // column scratch: the window table (no longer needed) — 3(k+1) rows <= table_slots(w) (2k+1) rows
-    wide_exit<COOP>(w, P.table, tstride, sslot, yrow, okv, P.out_limbs);
+    wide_exit<COOP, PP>(w, P.table, tstride, sslot, yrow, okv, P.out_limbs);
 }
 
 }  // namespace
@@ -480,7 +505,12 @@ int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u
     const u32 nt32 = (k + 1) - down <= 4 && down >= 64 ? down : up, nt = nt32 < (u32)NTMAX ? nt32 : (u32)NTMAX;
     W.nt = nt;
     const size_t smem = wide_smem_bytes(k);
-    const void *kern = nt <= 256 ? (const void *)k_modexp_wide<256, 2, true> : (const void *)k_modexp_wide<NTMAX, 1, false>;
+    // ping-pong coefficient groups: A/B +8 % at k = 257, +5 % at 505, -13 % at 129 (tools/ab_w.sh)
+    static const u32 pp_min = [] { const char *e = getenv("MR_WIDE_PP_MIN"); return e ? (u32)atoi(e) : 257u; }();
+    const bool pp = k >= pp_min;
+    const void *kern = nt > 256 ? (const void *)k_modexp_wide<NTMAX, 1, false, true>
+                       : pp     ? (const void *)k_modexp_wide<256, 2, true, true>
+                                : (const void *)k_modexp_wide<256, 2, true, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 6;
     void *args[] = {const_cast<ModexpParams *>(&p), &W};
     return cudaLaunchKernel(kern, dim3(ctas), dim3(nt), args, smem, (cudaStream_t)stream) == cudaSuccess ? 0 : 6;
