@@ -1245,7 +1245,8 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
     const size_t tcols = std::max<size_t>(count, slots);
     u32 *d_pc = nullptr, *d_tab = nullptr, *d_aux = nullptr;
     if (cudaMallocAsync(&d_pc, (size_t)pc_words(kk) * count * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
-    if (cudaMallocAsync(&d_tab, ((size_t)(1u << window) + 1) * nch * tcols * 4, st) != cudaSuccess) {
+    // window tables: (2^w + 1) entries per candidate slot; the tensor kernel pads entries to pad4(nch)
+    if (cudaMallocAsync(&d_tab, ((size_t)(1u << window) + 1) * ((nch + 3) & ~(size_t)3) * tcols * 4, st) != cudaSuccess) {
         cudaFreeAsync(d_pc, st);
         return MR_ERR_NOMEM;
     }

@@ -284,7 +284,9 @@ __host__ __device__ constexpr u32 pc_nminv(u32 k) { return 4 * k + 1; }         
 __host__ __device__ constexpr u32 pc_s(u32 k) { return 4 * k + 2; }             // [1]  s with n - 1 = 2^s d
 __host__ __device__ constexpr u32 pc_live(u32 k) { return 4 * k + 3; }          // [1]  1 = run the rounds
 __host__ __device__ constexpr u32 pc_d(u32 k) { return 4 * k + 4; }             // [k]  d limbs
-__host__ __device__ constexpr u32 pc_words(u32 k) { return 5 * k + 4; }
+__host__ __device__ constexpr u32 pc_n(u32 k) { return 5 * k + 4; }             // [k+1] n limbs (0 above limbs),
+                                                                                  // column layout: coalesced reads
+__host__ __device__ constexpr u32 pc_words(u32 k) { return 6 * k + 5; }
 
 // ---------------------------------------------------------------------------------------------
 // Per-k entry points exported by each mr_k<K>.cu translation unit.

@@ -186,12 +186,13 @@ struct CtxThread {                    // one modulus per thread (Miller-Rabin): 
     static constexpr bool kScaled = false;
     static constexpr bool kMont = false;
     const u32 *pc;
-    const u32 *nrow;                  // candidate limbs
-    u32 stride, limbs;
+    u32 stride;
     __device__ u32 sigma(int i) const { return pc[(size_t)(pc_sigma(K) + i) * stride]; }
     __device__ u32 c2(int j) const { return pc[(size_t)(pc_c2(K) + j) * stride]; }
     __device__ u32 nminv() const { return pc[(size_t)pc_nminv(K) * stride]; }
-    __device__ u32 nlimb(int l) const { return (u32)l < limbs ? nrow[l] : 0u; }
+    // n limbs from the candidate-major pc rows (coalesced across the warp; the caller's [count][limbs]
+    // rows would cost one sector per thread and limb in the exit's conditional subtractions)
+    __device__ u32 nlimb(int l) const { return pc[(size_t)(pc_n(K) + l) * stride]; }   // l in [0, K]
 };
 
 // Tensor-core modexp contexts: B residues stored ρ-scaled (s_i = x_i ρ_i, ρ_i² = ε_i σ_i),
@@ -783,7 +784,10 @@ __device__ __forceinline__ u32 fold_word(u32 lo, u32 hi, u32 c) {
 // compiler may issue the loads early), generic otherwise (Miller-Rabin passes shared-memory constants)
 template <class CS>
 __device__ __forceinline__ u32 mulop_ld(const u32 *p) {
-    if constexpr (CS::kScaled || CS::kMont) return __ldcg(p);
+    // Miller-Rabin (per-candidate exponent, so per-thread window entries): each candidate's entry is
+    // contiguous and read through L1, one 32-byte sector serving 8 consecutive channel loads
+    if constexpr (!CS::kMerged && CS::kMont) return __ldca(p);
+    else if constexpr (CS::kScaled || CS::kMont) return __ldcg(p);
     else return *p;
 }
 
@@ -1412,6 +1416,8 @@ __global__ void __launch_bounds__(T) k_mr_setup(const MrParams P) {
     const u32 *nrow = P.n + (size_t)i * L;
     u32 *pc = P.pc + i;
     const size_t cs = P.count;
+#pragma unroll 1
+    for (u32 l = 0; l <= (u32)K; l++) pc[(size_t)(pc_n(K) + l) * cs] = l < L ? nrow[l] : 0u;   // column copy of n
     int32_t status = 0;
     u32 live = 1;
     u32 verdict = MR_COMPOSITE_V;
@@ -1500,10 +1506,11 @@ __device__ __forceinline__ bool x_is_one(u32 *st) {
     for (int l = 1; l <= K; l++) nz |= S(st, l);
     return nz == 0;
 }
-__device__ __forceinline__ bool x_is_nm1(u32 *st, const u32 *nrow, u32 L) {
-    u32 diff = S(st, 0) ^ (nrow[0] - 1u);          // n odd: n - 1 only changes limb 0
+template <class CS>
+__device__ __forceinline__ bool x_is_nm1(u32 *st, const CS &cs) {
+    u32 diff = S(st, 0) ^ (cs.nlimb(0) - 1u);      // n odd: n - 1 only changes limb 0
 #pragma unroll 1
-    for (u32 l = 1; l <= (u32)K; l++) diff |= S(st, l) ^ (l < L ? nrow[l] : 0u);
+    for (u32 l = 1; l <= (u32)K; l++) diff |= S(st, l) ^ cs.nlimb(l);
     return diff == 0;
 }
 
@@ -1524,7 +1531,7 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
     if (!pcol[(size_t)pc_live(K) * cnt]) return;
     const u32 L = P.limbs;
     const u32 *nrow = P.n + (size_t)i * L;
-    const CtxThread cs{pcol, nrow, (u32)cnt, L};
+    const CtxThread cs{pcol, (u32)cnt};
     const u32 w = P.window, E = 1u << w;
     const size_t entry = (size_t)NCH * cnt;
     u32 *tab = P.table + i;                       // slot e at tab + e * entry, channel c at + c * cnt
@@ -1598,7 +1605,7 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
             for (int c = 0; c < NCH; c++) stash[(size_t)c * cnt] = S(st, c);
             mont_mul(st, s_one, 1, false, cs, s_be);                 // leave the Montgomery domain
             from_rns(st, cs, P.mpl);
-            const bool one = x_is_one(st), nm1 = x_is_nm1(st, nrow, L);
+            const bool one = x_is_one(st), nm1 = x_is_nm1(st, cs);
             if (nm1) { pass = true; decided = true; }
             else if (one) { pass = (j == 0); decided = true; }  // y = 1 first: pass; later: composite
 #pragma unroll 1
@@ -1630,12 +1637,12 @@ struct CtxMr {                        // per-candidate constants of one thread
     const u32 *c1c;                   // shared memory: |M^-1 λ_j^-1| 2^32 mod m'_j (per k)
     const u32 *c2row;                 // shared memory: c2row[j * 128] = |n M^-1 λ_j|_{m'_j}
     u32 nmv;                          // n M^-1 mod 2^32
-    const u32 *nrow;
-    u32 limbs;
+    const u32 *ncol;                  // pcol + pc_n rows: n limb l at ncol[l * nstride] (coalesced)
+    u32 nstride;
     __device__ u32 sigma(int i) const { return sig[i]; }
     __device__ u32 c2(int j) const { return c2row[j * 128]; }
     __device__ u32 nminv() const { return nmv; }
-    __device__ u32 nlimb(int l) const { return (u32)l < limbs ? nrow[l] : 0u; }
+    __device__ u32 nlimb(int l) const { return ncol[(size_t)l * nstride]; }   // l in [0, K]
 };
 
 __device__ __forceinline__ bool tile_any(const TcTile &t, bool v) {
@@ -1652,10 +1659,10 @@ __device__ __forceinline__ bool x_is_one_t(const StTile &st) {
     for (int l = 1; l <= K; l++) nz |= S(st, l);
     return nz == 0;
 }
-__device__ __forceinline__ bool x_is_nm1_t(const StTile &st, const u32 *nrow, u32 L) {
-    u32 diff = S(st, 0) ^ (nrow[0] - 1u);
+__device__ __forceinline__ bool x_is_nm1_t(const StTile &st, const CtxMr &cs) {
+    u32 diff = S(st, 0) ^ (cs.nlimb(0) - 1u);
 #pragma unroll 1
-    for (u32 l = 1; l <= (u32)K; l++) diff |= S(st, l) ^ (l < L ? nrow[l] : 0u);
+    for (u32 l = 1; l <= (u32)K; l++) diff |= S(st, l) ^ cs.nlimb(l);
     return diff == 0;
 }
 
@@ -1719,8 +1726,11 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     u32 *c2rows = c2_all + tile * K * 128 + m;
     const size_t cnt = P.count;
     const u32 L = P.limbs, w = P.window, E = 1u << w, R = P.rounds;
-    const size_t tst = P.mode == 2 ? P.tstride : cnt;              // window-table stride
-    const size_t entry = (size_t)NCH * tst;
+    // window table: each candidate slot's E entries (+ the check stash) contiguous, NCHP words apart,
+    // channel stride 1 (the window digit differs per candidate: a column layout would scatter every
+    // warp load over up to 32 entries; here a 32-byte sector serves 8 channel loads)
+    constexpr u32 NCHP = pad4(NCH);
+    const size_t entry = NCHP;
     const u32 ndig = (32 * L + w - 1) / w;
     const u32 items = P.mode == 2 ? *P.nlive * (R - 1) : 0u;
     const u32 jobs = P.mode == 2 ? (items + 127) / 128 : (P.count + 127) / 128, G = gridDim.x;
@@ -1771,12 +1781,12 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
         for (int j = 0; j < K; j++) c2rows[j * 128] = pcol[(size_t)(pc_c2(K) + j) * cnt];
         cs.c2row = c2rows;
         cs.nmv = pcol[(size_t)pc_nminv(K) * cnt];
-        cs.nrow = nrow;
-        cs.limbs = L;
+        cs.ncol = pcol + (size_t)pc_n(K) * cnt;
+        cs.nstride = (u32)cnt;
         const u32 *r2 = pcol + (size_t)pc_r2(K) * cnt;
         const u32 s = pcol[(size_t)pc_s(K) * cnt];
         const u32 *dl = pcol + (size_t)pc_d(K) * cnt;
-        u32 *tab = P.table + (P.mode == 2 ? (size_t)(blockIdx.x * TCM + tile) * 128 + m : (size_t)i);
+        u32 *tab = P.table + (P.mode == 2 ? (size_t)(blockIdx.x * TCM + tile) * 128 + m : (size_t)i) * (E + 1) * NCHP;
         u32 *stash = tab + E * entry;
         u32 verdict = MR_PROBABLY_PRIME_V;
         int witness = -1;
@@ -1800,12 +1810,12 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                     to_rns(st, a, 1, L, true, P.pow_tab);
                     bp = r2; bs = (u32)cnt;
                 } else if (u < E) {
-                    bp = tab + entry; bs = (u32)tst;
+                    bp = tab + entry; bs = 1;
                 } else {
                     const u32 q = u - E, dg = ndig - 1 - q / (w + 1), sub = q % (w + 1);
                     if (q == 0) {
 #pragma unroll 1
-                        for (int c = 0; c < NCH; c++) S(st, c) = tab[(size_t)c * tst];
+                        for (int c = 0; c < NCH; c++) S(st, c) = tab[c];
                     }
                     if (sub < w) { sq = true; bp = s_one; bs = 0; }
                     else {
@@ -1813,14 +1823,14 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                         const u32 lo = lw < (u32)K ? dl[(size_t)lw * cnt] : 0u;
                         const u32 hi = lw + 1 < (u32)K ? dl[(size_t)(lw + 1) * cnt] : 0u;
                         bp = tab + (size_t)(__funnelshift_r(lo, hi, bw) & (E - 1)) * entry;
-                        bs = (u32)tst;
+                        bs = 1;
                     }
                 }
                 mm(st, bp, bs, sq, cs);
                 if (u < E) {
                     u32 *dst = tab + (size_t)u * entry;
 #pragma unroll 1
-                    for (int c = 0; c < NCH; c++) dst[(size_t)c * tst] = S(st, c);
+                    for (int c = 0; c < NCH; c++) dst[c] = S(st, c);
                 }
             }
             // checks (HAC 4.24): even steps leave the Montgomery domain and compare, odd steps square
@@ -1831,12 +1841,12 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                 const bool check = (v % 2) == 0;
                 if (check) {
 #pragma unroll 1
-                    for (int c = 0; c < NCH; c++) stash[(size_t)c * tst] = S(st, c);
+                    for (int c = 0; c < NCH; c++) stash[c] = S(st, c);
                 }
                 mm(st, P.one_g, check ? 1u : 0u, !check, cs);
                 if (check) {
                     from_rns(st, cs, P.mpl);
-                    const bool one = x_is_one_t(st), nm1 = x_is_nm1_t(st, nrow, L);
+                    const bool one = x_is_one_t(st), nm1 = x_is_nm1_t(st, cs);
                     if (need) {
                         if (nm1) { pass = true; need = false; }
                         else if (one) { pass = (jj == 0); need = false; }
@@ -1844,7 +1854,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                     }
                     jj++;
 #pragma unroll 1
-                    for (int c = 0; c < NCH; c++) S(st, c) = stash[(size_t)c * tst];
+                    for (int c = 0; c < NCH; c++) S(st, c) = stash[c];
                     if (!tile_any(mm.t, need)) break;
                 }
             }
