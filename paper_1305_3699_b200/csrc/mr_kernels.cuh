@@ -1533,8 +1533,10 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
     const u32 *nrow = P.n + (size_t)i * L;
     const CtxThread cs{pcol, (u32)cnt};
     const u32 w = P.window, E = 1u << w;
-    const size_t entry = (size_t)NCH * cnt;
-    u32 *tab = P.table + i;                       // slot e at tab + e * entry, channel c at + c * cnt
+    // window table: the candidate's E entries (+ stash) contiguous, pad4(NCH) words apart (per-candidate
+    // window digits: a column layout would scatter every warp load over up to 2^w entries)
+    const size_t entry = pad4(NCH);
+    u32 *tab = P.table + (size_t)i * (E + 1) * entry;   // slot e at tab + e * entry, channel c at + c
     u32 *stash = tab + E * entry;
     const u32 *r2 = pcol + (size_t)pc_r2(K) * cnt;
     const u32 s = pcol[(size_t)pc_s(K) * cnt];
@@ -1571,20 +1573,20 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
         for (int c = 0; c < NCH; c++) S(st, c) = r2[(size_t)c * cnt];
         mont_mul(st, s_one, 1, false, cs, s_be);
 #pragma unroll 1
-        for (int c = 0; c < NCH; c++) tab[(size_t)c * cnt] = S(st, c);
+        for (int c = 0; c < NCH; c++) tab[c] = S(st, c);
         to_rns(st, a, 1, L, true, P.pow_tab);
         mont_mul(st, r2, (u32)cnt, false, cs, s_be);
 #pragma unroll 1
-        for (int c = 0; c < NCH; c++) tab[entry + (size_t)c * cnt] = S(st, c);
+        for (int c = 0; c < NCH; c++) tab[entry + c] = S(st, c);
 #pragma unroll 1
         for (u32 e = 2; e < E; e++) {
-            mont_mul(st, tab + entry, (u32)cnt, false, cs, s_be);
+            mont_mul(st, tab + entry, 1u, false, cs, s_be);
 #pragma unroll 1
-            for (int c = 0; c < NCH; c++) tab[e * entry + (size_t)c * cnt] = S(st, c);
+            for (int c = 0; c < NCH; c++) tab[e * entry + c] = S(st, c);
         }
         // y = a^d: fixed window from the top digit; acc starts at 1~
 #pragma unroll 1
-        for (int c = 0; c < NCH; c++) S(st, c) = tab[(size_t)c * cnt];
+        for (int c = 0; c < NCH; c++) S(st, c) = tab[c];
 #pragma unroll 1
         for (int dg = (int)ndig - 1; dg >= 0; dg--) {
             const u32 b0 = dg * w;
@@ -1594,7 +1596,7 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
             const u32 digit = __funnelshift_r(lo, hi, bw) & (E - 1);
 #pragma unroll 1
             for (u32 q = 0; q < w; q++) mont_mul(st, s_one, 0, true, cs, s_be);
-            mont_mul(st, tab + digit * entry, (u32)cnt, false, cs, s_be);
+            mont_mul(st, tab + digit * entry, 1u, false, cs, s_be);
         }
         // HAC 4.24 steps 2.3-2.6: y in {1, n-1} passes; else up to s-1 squarings looking for n-1
         bool pass = false, decided = false;
@@ -1602,14 +1604,14 @@ __global__ void __launch_bounds__(T) k_mr_rounds(const MrParams P) {
         for (u32 j = 0; j < s && !decided; j++) {
             if (j) mont_mul(st, s_one, 0, true, cs, s_be);           // y = y^2
 #pragma unroll 1
-            for (int c = 0; c < NCH; c++) stash[(size_t)c * cnt] = S(st, c);
+            for (int c = 0; c < NCH; c++) stash[c] = S(st, c);
             mont_mul(st, s_one, 1, false, cs, s_be);                 // leave the Montgomery domain
             from_rns(st, cs, P.mpl);
             const bool one = x_is_one(st), nm1 = x_is_nm1(st, cs);
             if (nm1) { pass = true; decided = true; }
             else if (one) { pass = (j == 0); decided = true; }  // y = 1 first: pass; later: composite
 #pragma unroll 1
-            for (int c = 0; c < NCH; c++) S(st, c) = stash[(size_t)c * cnt];
+            for (int c = 0; c < NCH; c++) S(st, c) = stash[c];
         }
         if (!pass) {
             if (verdict == MR_PROBABLY_PRIME_V) { verdict = MR_COMPOSITE_V; witness = (int)r; }
