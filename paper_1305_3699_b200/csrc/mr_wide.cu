@@ -508,8 +508,11 @@ int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u
     // ping-pong coefficient groups: A/B +8 % at k = 257, +5 % at 505, -13 % at 129 (tools/ab_w.sh)
     static const u32 pp_min = [] { const char *e = getenv("MR_WIDE_PP_MIN"); return e ? (u32)atoi(e) : 257u; }();
     const bool pp = k >= pp_min;
+    // k = 97 (96 threads): a 168-register budget (no accumulator-pair shuffling) beats the 128-register
+    // one by 5-8 %; at k = 129 (128 threads) the 4th resident CTA is worth more (tools/ab_k129.py)
     const void *kern = nt > 256 ? (const void *)k_modexp_wide<NTMAX, 1, false, true>
                        : pp     ? (const void *)k_modexp_wide<256, 2, true, true>
+                       : nt <= 96 ? (const void *)k_modexp_wide<128, 3, true, false>
                                 : (const void *)k_modexp_wide<256, 2, true, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 6;
     void *args[] = {const_cast<ModexpParams *>(&p), &W};
