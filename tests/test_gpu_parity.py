@@ -367,3 +367,38 @@ def test_crt_decrypt_large_halves_vs_oracle(torch_cuda, mr, orc, half_bits):
     torch_cuda.cuda.synchronize()
     ref = orc.crt_decrypt_batch(mr.ints_to_limbs(cs, 2 * H), p, q, dp, dq, qinv, H, threads=8)
     assert np.array_equal(host(m), ref)
+
+
+_PER_K_SNIPPET = r"""
+import random, sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1305_3699_b200 as mr
+for bits in (3072, 4096):
+    rng = random.Random(bits + 1)
+    N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+    L = bits // 32
+    xs = [0, 1, N - 1] + [rng.randrange(N) for _ in range(130)]
+    E = rng.getrandbits(200) | (1 << 199)
+    ctx = mr.RnsContext(N, L)
+    x = torch.from_numpy(mr.ints_to_limbs(xs, L).view(np.int32)).cuda()
+    y = torch.empty_like(x)
+    ctx.modexp(x, y, E)
+    got = mr.limbs_to_ints(y.cpu().numpy())
+    assert got == [pow(v, E, N) for v in xs], bits
+print("per-k ok")
+"""
+
+
+def test_per_k_imad_modexp_k97_k129(torch_cuda):
+    """The per-k IMAD modexp kernels of k = 97 / 129 are no longer the default (the wide kernel runs those
+    sizes) but stay selectable (MR_RNS_WIDE_MIN=999, read once per process): a subprocess
+    runs 133 messages (ragged over 64/128-message CTAs, edges 0, 1, N-1) per size against Python's pow."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MR_RNS_WIDE_MIN="999")
+    r = subprocess.run([sys.executable, "-c", _PER_K_SNIPPET.format(root=root)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "per-k ok" in r.stdout, r.stderr[-2000:]
