@@ -167,6 +167,9 @@ def rng(torch, mr, quick):
           "paper_context": "32-40 GB/s of seed bits on 2013 GPUs (P:121)"})
 
 
+MR_WINDOW = int(os.environ.get("MR_BENCH_WINDOW", "5"))   # fixed window of the a^d ladder (public API at 1024 bits: 5)
+
+
 def c5(torch, mr, orc, quick):
     cnt = 16384 if quick else 65536
     rounds = 5
@@ -191,7 +194,7 @@ def c5(torch, mr, orc, quick):
     for forced in (1, 0):
         def run():
             rc = L.mr_internal_miller_rabin(d_n.data_ptr(), 32, cnt, d_b.data_ptr(), rounds, 0, v.data_ptr(),
-                                            w.data_ptr(), None, 0, stream, forced, 4)
+                                            w.data_ptr(), None, 0, stream, forced, MR_WINDOW)
             assert rc == 0
         t = timed(torch, run, reps=2)
         res[forced] = (t, v.cpu().numpy().copy(), w.cpu().numpy().copy())
