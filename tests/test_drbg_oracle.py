@@ -6,7 +6,8 @@ run counts; every statistic is pinned on constructed blocks whose values follow 
 alternating bits, exact ones counts at the monobit edges, a run of exactly 25 / 26, chosen nibble
 histograms at the poker edges).  Hash_DRBG itself has no offline SP 800-90A vector here: its pins are the
 structural properties (determinism, domain separation of streams, the mod 2^440 counter wrap, the
-reseed-counter update) — DESIGN.md lists it as "parity unpinned against the standard's vectors"."""
+reseed-counter update); its values are pinned against OpenSSL 3's HASH-DRBG in
+tests/test_oracle_standard_pins.py."""
 import numpy as np
 import pytest
 
