@@ -22,7 +22,11 @@
  *    >= its bound, in which case that output is zero-filled.
  *  - count = 0 is MR_OK and launches nothing.
  *  - Contexts are immutable after creation and may be used concurrently from any host thread or
- *    stream.  Scratch memory is allocated stream-ordered (cudaMallocAsync) inside each call.
+ *    stream (also several batches of one context at once: the persistent kernels never wait for a CTA
+ *    that has not started).  Scratch memory is allocated stream-ordered (cudaMallocAsync)
+ *    inside each call.  Exception to "never synchronises": the first call with a new exponent on a
+ *    context uploads its ladder program (one small copy on a private stream that the host waits for;
+ *    the first 64 programs per context are cached, later ones are uploaded and freed stream-ordered).
  *  - There is no CPU fallback: on a machine without a usable CUDA device every call returns
  *    MR_ERR_CUDA.
  */
@@ -70,10 +74,13 @@ enum { MR_COMPOSITE = 0, MR_PROBABLY_PRIME = 1, MR_FACTOR = 2 }; /* Miller-Rabin
 int mr_rns_ctx_create(mr_rns_ctx **out, const uint32_t *modulus, size_t limbs, int k, int device);
 void mr_rns_ctx_destroy(mr_rns_ctx *ctx);
 
-/* k actually used, limbs of N, bits(N), and the paper's nominal key-size cap k*31 bits for k
- * 32-bit primes ("128 32-bit prime integers, sufficient for RSA keys up to 3,968-bit"; R4).
+/* k actually used; limbs of N; max_modulus_bits = the largest b such that every odd N < 2^b passes this
+ * k's admission test (4 K_B^2 N < M and 4 K_B N < M', DESIGN.md §3 / R5: the enforced capacity, SURVEY
+ * §8(b)); bits(N); and the paper's nominal key-size cap k*31 bits for k 32-bit primes ("128 32-bit prime
+ * integers, sufficient for RSA keys up to 3,968-bit"; R4, reported for reference only).
  * Any out pointer may be NULL. */
-int mr_rns_ctx_info(const mr_rns_ctx *ctx, int *k, size_t *limbs, int *modulus_bits, int *paper_cap_bits);
+int mr_rns_ctx_info(const mr_rns_ctx *ctx, int *k, size_t *limbs, int *max_modulus_bits, int *modulus_bits,
+                    int *paper_cap_bits);
 
 /* Writes up to `cap` compiled channel counts k (ascending) into ks (HOST); returns how many exist. */
 int mr_rns_supported_k(int *ks, int cap);
@@ -151,6 +158,11 @@ int mr_miller_rabin_batch(const uint32_t *d_n, size_t limbs, size_t count, const
  * schedules the search from per-search flags it reads back; no key material leaves the device).
  * Errors: MR_ERR_ARG (bad bits/e/rounds/count, NULL output), MR_ERR_RANGE (a key needed more than
  * 65,536 prime searches), MR_ERR_CUDA, MR_ERR_NOMEM.
+ * WARNING — DETERMINISTIC FIXTURE RECIPE, NOT FOR PRODUCTION KEYS: every prime follows from the 64-bit
+ * `seed` through SplitMix64 (not a cryptographic generator) and the Miller-Rabin bases are the fixed
+ * primes 2, 3, 5, ...; anyone who knows or guesses the seed can regenerate p, q and d.  It exists so the
+ * GPU pipeline can be checked limb for limb against the oracle's fixture keys.  Real keys:
+ * mr_rsa_keygen_batch_drbg (below, after the DRBG declarations).
  * ------------------------------------------------------------------------------------------ */
 int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t seed, uint64_t first_key, int rounds,
                         uint32_t *d_n, uint32_t *d_p, uint32_t *d_q, uint32_t *d_d, uint32_t *d_dp, uint32_t *d_dq,
@@ -186,6 +198,24 @@ int mr_drbg_create(mr_drbg **out, const uint8_t *entropy, size_t entropy_len, co
 int mr_drbg_generate(mr_drbg *d, uint8_t *d_out, size_t nbytes, void *stream);
 void mr_drbg_destroy(mr_drbg *d);
 int mr_fips_health_batch(const uint8_t *d_blocks, size_t nblocks, uint32_t *d_stats, void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * mr_rsa_keygen_batch_drbg — production form of mr_rsa_keygen_batch: the same GPU pipeline (sieve by the
+ * first 10,000 primes, Miller-Rabin in the RNS Montgomery domain, Arazi inversion)
+ * with every random choice drawn from the caller's Hash_DRBG `rng` (§2 "an approved deterministic
+ * RBG", seeded by the caller with >= 256 bits of entropy):
+ *   - each prime search starts at bits/2 DRBG bits with the top two bits and bit 0 set (FIPS 186-4 B.3.3);
+ *   - each of the `rounds` Miller-Rabin rounds of a candidate w uses its own base b = 2 + (c mod (w - 3)),
+ *     c = bits/2 + 64 DRBG bits (uniform in [2, w - 2] up to 2^-62: FIPS 186-4 C.3.1 with the
+ *     "extra random bits" method of B.5.1).  FIPS 186-4 Table C.2 asks for 5 (bits = 2048) / 4 (3072)
+ *     rounds after trial division; more are allowed.
+ * The acceptance rules (gcd(e, p - 1) = 1, |p - q| > 2^(bits/2 - 100)) and outputs are those of
+ * mr_rsa_keygen_batch; rng must live on `device`; the call advances rng (its requests are ordered on
+ * `stream`).  Synchronous.  Same errors as mr_rsa_keygen_batch, plus MR_ERR_ARG for rng == NULL.
+ * ------------------------------------------------------------------------------------------ */
+int mr_rsa_keygen_batch_drbg(mr_drbg *rng, size_t count, int bits, uint32_t e, int rounds, uint32_t *d_n,
+                             uint32_t *d_p, uint32_t *d_q, uint32_t *d_d, uint32_t *d_dp, uint32_t *d_dq,
+                             uint32_t *d_qinv, int device, void *stream);
 
 const char *mr_strerror(int code);
 

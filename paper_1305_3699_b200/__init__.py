@@ -21,7 +21,7 @@ __all__ = [
     "lib", "MrError", "MR_OK", "MR_ERR_RANGE", "MR_COMPOSITE", "MR_PROBABLY_PRIME", "MR_FACTOR",
     "mr_rns_ctx_create", "mr_rns_ctx_destroy", "mr_rns_ctx_info", "mr_rns_supported_k",
     "mr_modexp_batch", "mr_rsa_encrypt_batch", "mr_rsa_priv_create", "mr_rsa_priv_destroy",
-    "mr_rsa_decrypt_batch", "mr_miller_rabin_batch", "mr_strerror",
+    "mr_rsa_decrypt_batch", "mr_miller_rabin_batch", "mr_rsa_keygen_batch", "mr_rsa_keygen_batch_drbg", "mr_strerror",
     "RnsContext", "RsaPrivateKey", "Drbg", "fips_health", "limbs_of", "ints_to_limbs", "limbs_to_ints",
 ]
 
@@ -36,7 +36,7 @@ EXPORTS = (
     "mr_rns_ctx_create", "mr_rns_ctx_destroy", "mr_rns_ctx_info", "mr_rns_supported_k", "mr_modexp_batch",
     "mr_rsa_encrypt_batch", "mr_rsa_priv_create", "mr_rsa_priv_destroy", "mr_rsa_decrypt_batch",
     "mr_miller_rabin_batch", "mr_rsa_keygen_batch", "mr_strerror",
-    "mr_drbg_create", "mr_drbg_generate", "mr_drbg_destroy", "mr_fips_health_batch",
+    "mr_drbg_create", "mr_drbg_generate", "mr_drbg_destroy", "mr_fips_health_batch", "mr_rsa_keygen_batch_drbg",
 )
 
 
@@ -62,7 +62,7 @@ def lib() -> ctypes.CDLL:
         L.mr_rns_ctx_create.argtypes = [ctypes.POINTER(vp), up, sz, i32, i32]
         L.mr_rns_ctx_destroy.argtypes = [vp]
         L.mr_rns_ctx_destroy.restype = None
-        L.mr_rns_ctx_info.argtypes = [vp, ip, ctypes.POINTER(sz), ip, ip]
+        L.mr_rns_ctx_info.argtypes = [vp, ip, ctypes.POINTER(sz), ip, ip, ip]
         L.mr_rns_supported_k.argtypes = [ip, i32]
         L.mr_modexp_batch.argtypes = [vp, vp, vp, sz, up, sz, vp, vp]
         L.mr_rsa_encrypt_batch.argtypes = [vp, up, sz, vp, vp, sz, vp, vp]
@@ -73,6 +73,7 @@ def lib() -> ctypes.CDLL:
         L.mr_miller_rabin_batch.argtypes = [vp, sz, sz, vp, i32, i32, vp, vp, vp, i32, vp]
         L.mr_rsa_keygen_batch.argtypes = [sz, i32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, i32] + \
             [vp] * 7 + [i32, vp]
+        L.mr_rsa_keygen_batch_drbg.argtypes = [vp, sz, i32, ctypes.c_uint32, i32] + [vp] * 7 + [i32, vp]
         L.mr_strerror.argtypes = [i32]
         L.mr_strerror.restype = ctypes.c_char_p
         cp = ctypes.c_char_p
@@ -133,6 +134,24 @@ def _dptr(t) -> Optional[int]:
     return t.data_ptr()
 
 
+def _arg(t, what: str, itemsize: int, numel: int, width: Optional[int] = None, device: Optional[int] = None):
+    """Validate a device buffer before its pointer crosses the C ABI (which cannot see sizes): a CUDA,
+    contiguous tensor of `itemsize`-byte elements with at least `numel` of them; `width` given: 2-D with
+    shape[1] == width; `device` given: on that CUDA ordinal.  Returns the pointer, or None for None."""
+    if t is None:
+        return None
+    p = _dptr(t)
+    if t.dtype.itemsize != itemsize:
+        raise MrError(MR_ERR_ARG, f"{what}: expected {itemsize}-byte elements, got {t.dtype}")
+    if width is not None and (t.dim() != 2 or t.shape[1] != width):
+        raise MrError(MR_ERR_ARG, f"{what}: expected shape [count][{width}], got {tuple(t.shape)}")
+    if t.numel() < numel:
+        raise MrError(MR_ERR_ARG, f"{what}: {t.numel()} elements, the call needs {numel}")
+    if device is not None and t.device.index != device:
+        raise MrError(MR_ERR_ARG, f"{what}: tensor on cuda:{t.device.index}, context on cuda:{device}")
+    return p
+
+
 def _stream(t, stream) -> Optional[int]:
     if stream is not None:
         return getattr(stream, "cuda_stream", stream)
@@ -161,31 +180,50 @@ def mr_rns_ctx_create(modulus: int, limbs: int, k: int = 0, device: int = 0) -> 
     m = limbs_of(modulus, limbs)
     h = ctypes.c_void_p()
     _check(lib().mr_rns_ctx_create(ctypes.byref(h), _hp(m), limbs, k, device), "mr_rns_ctx_create")
+    _devices[h.value] = (limbs, device)
     return h
 
 
 def mr_rns_ctx_destroy(ctx) -> None:
+    _devices.pop(getattr(ctx, "value", ctx), None)
     lib().mr_rns_ctx_destroy(ctx)
 
 
 def mr_rns_ctx_info(ctx) -> dict:
-    k, bits, cap = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    k, maxb, bits, cap = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     limbs = ctypes.c_size_t()
-    _check(lib().mr_rns_ctx_info(ctx, ctypes.byref(k), ctypes.byref(limbs), ctypes.byref(bits), ctypes.byref(cap)),
-           "mr_rns_ctx_info")
-    return {"k": k.value, "limbs": limbs.value, "modulus_bits": bits.value, "paper_cap_bits": cap.value}
+    _check(lib().mr_rns_ctx_info(ctx, ctypes.byref(k), ctypes.byref(limbs), ctypes.byref(maxb), ctypes.byref(bits),
+                                 ctypes.byref(cap)), "mr_rns_ctx_info")
+    return {"k": k.value, "limbs": limbs.value, "max_modulus_bits": maxb.value, "modulus_bits": bits.value,
+            "paper_cap_bits": cap.value}
+
+
+_devices: dict = {}   # handle value -> (limbs per row, device) of contexts and private keys made here
+
+
+def _geom(handle, what: str):
+    g = _devices.get(getattr(handle, "value", handle))
+    if g is None:
+        raise MrError(MR_ERR_ARG, f"{what}: unknown handle (create it with this module)")
+    return g
 
 
 def mr_modexp_batch(ctx, d_x, d_y, count: int, exp: int, d_status=None, stream=None) -> None:
+    limbs, dev = _geom(ctx, "mr_modexp_batch")
     e = limbs_of(exp, max(1, (exp.bit_length() + 31) // 32))
-    _check(lib().mr_modexp_batch(ctx, _dptr(d_x), _dptr(d_y), count, _hp(e), len(e) if exp else 0,
-                                 _dptr(d_status), _stream(d_x, stream)), "mr_modexp_batch")
+    _check(lib().mr_modexp_batch(ctx, _arg(d_x, "d_x", 4, count * limbs, limbs, dev),
+                                 _arg(d_y, "d_y", 4, count * limbs, limbs, dev), count, _hp(e), len(e) if exp else 0,
+                                 _arg(d_status, "d_status", 4, count, None, dev), _stream(d_x, stream)),
+           "mr_modexp_batch")
 
 
 def mr_rsa_encrypt_batch(ctx, e: int, d_m, d_c, count: int, d_status=None, stream=None) -> None:
+    limbs, dev = _geom(ctx, "mr_rsa_encrypt_batch")
     el = limbs_of(e, max(1, (e.bit_length() + 31) // 32))
-    _check(lib().mr_rsa_encrypt_batch(ctx, _hp(el), len(el) if e else 0, _dptr(d_m), _dptr(d_c), count,
-                                      _dptr(d_status), _stream(d_m, stream)), "mr_rsa_encrypt_batch")
+    _check(lib().mr_rsa_encrypt_batch(ctx, _hp(el), len(el) if e else 0, _arg(d_m, "d_m", 4, count * limbs, limbs, dev),
+                                      _arg(d_c, "d_c", 4, count * limbs, limbs, dev), count,
+                                      _arg(d_status, "d_status", 4, count, None, dev), _stream(d_m, stream)),
+           "mr_rsa_encrypt_batch")
 
 
 def mr_rsa_priv_create(p: int, q: int, half_limbs: int, d_p: int, d_q: int, q_inv: int, k_half: int = 0,
@@ -194,22 +232,33 @@ def mr_rsa_priv_create(p: int, q: int, half_limbs: int, d_p: int, d_q: int, q_in
     h = ctypes.c_void_p()
     _check(lib().mr_rsa_priv_create(ctypes.byref(h), *[_hp(a) for a in arrs[:2]], half_limbs,
                                     *[_hp(a) for a in arrs[2:]], k_half, device), "mr_rsa_priv_create")
+    _devices[h.value] = (2 * half_limbs, device)
     return h
 
 
 def mr_rsa_priv_destroy(priv) -> None:
+    _devices.pop(getattr(priv, "value", priv), None)
     lib().mr_rsa_priv_destroy(priv)
 
 
 def mr_rsa_decrypt_batch(priv, d_c, d_m, count: int, d_status=None, stream=None) -> None:
-    _check(lib().mr_rsa_decrypt_batch(priv, _dptr(d_c), _dptr(d_m), count, _dptr(d_status), _stream(d_c, stream)),
+    limbs, dev = _geom(priv, "mr_rsa_decrypt_batch")
+    _check(lib().mr_rsa_decrypt_batch(priv, _arg(d_c, "d_c", 4, count * limbs, limbs, dev),
+                                      _arg(d_m, "d_m", 4, count * limbs, limbs, dev), count,
+                                      _arg(d_status, "d_status", 4, count, None, dev), _stream(d_c, stream)),
            "mr_rsa_decrypt_batch")
 
 
 def mr_miller_rabin_batch(d_n, limbs: int, count: int, d_bases, rounds: int, d_verdict, d_witness=None,
                           d_status=None, k: int = 0, device: int = 0, stream=None) -> None:
-    _check(lib().mr_miller_rabin_batch(_dptr(d_n), limbs, count, _dptr(d_bases), rounds, k, _dptr(d_verdict),
-                                       _dptr(d_witness), _dptr(d_status), device, _stream(d_n, stream)),
+    if rounds < 1:
+        raise MrError(MR_ERR_ARG, "mr_miller_rabin_batch: rounds >= 1")
+    _check(lib().mr_miller_rabin_batch(_arg(d_n, "d_n", 4, count * limbs, limbs, device), limbs, count,
+                                       _arg(d_bases, "d_bases", 4, count * rounds * limbs, None, device), rounds, k,
+                                       _arg(d_verdict, "d_verdict", 1, count, None, device),
+                                       _arg(d_witness, "d_witness", 2, count, None, device),
+                                       _arg(d_status, "d_status", 4, count, None, device), device,
+                                       _stream(d_n, stream)),
            "mr_miller_rabin_batch")
 
 
@@ -217,9 +266,24 @@ def mr_rsa_keygen_batch(count: int, bits: int, e: int, seed: int, rounds: int, d
                         first_key: int = 0, device: int = 0, stream=None) -> None:
     """RSA key generation on the GPU (include/mr_rns.h).  Outputs are device uint32/int32 tensors of
     [count][bits/32] (n, d) and [count][bits/64] (p, q, dp, dq, qinv) limbs."""
-    _check(lib().mr_rsa_keygen_batch(count, bits, e, seed, first_key, rounds, _dptr(d_n), _dptr(d_p), _dptr(d_q),
-                                     _dptr(d_d), _dptr(d_dp), _dptr(d_dq), _dptr(d_qinv), device,
+    L, H = bits // 32, bits // 64
+    outs = [_arg(t, nm, 4, count * w, w, device) for t, nm, w in
+            ((d_n, "d_n", L), (d_p, "d_p", H), (d_q, "d_q", H), (d_d, "d_d", L), (d_dp, "d_dp", H), (d_dq, "d_dq", H),
+             (d_qinv, "d_qinv", H))]
+    _check(lib().mr_rsa_keygen_batch(count, bits, e, seed, first_key, rounds, *outs, device,
                                      _stream(d_n, stream)), "mr_rsa_keygen_batch")
+
+
+def mr_rsa_keygen_batch_drbg(rng: "Drbg", count: int, bits: int, e: int, rounds: int, d_n, d_p, d_q, d_d, d_dp, d_dq,
+                             d_qinv, device: int = 0, stream=None) -> None:
+    """RSA key generation with every random choice (search starts, Miller-Rabin bases) drawn from the
+    GPU Hash_DRBG `rng` (include/mr_rns.h).  Same outputs as mr_rsa_keygen_batch."""
+    L, H = bits // 32, bits // 64
+    outs = [_arg(t, nm, 4, count * w, w, device) for t, nm, w in
+            ((d_n, "d_n", L), (d_p, "d_p", H), (d_q, "d_q", H), (d_d, "d_d", L), (d_dp, "d_dp", H), (d_dq, "d_dq", H),
+             (d_qinv, "d_qinv", H))]
+    _check(lib().mr_rsa_keygen_batch_drbg(rng.handle, count, bits, e, rounds, *outs, device, _stream(d_n, stream)),
+           "mr_rsa_keygen_batch_drbg")
 
 
 # ------------------------------------------------------------------ RAII conveniences
@@ -313,5 +377,6 @@ class Drbg:
 def fips_health(d_blocks, d_stats, stream=None) -> None:
     """FIPS 140-2 tests of d_blocks (CUDA uint8 [n][2500]) into d_stats (CUDA int32 [n][16])."""
     n = d_blocks.shape[0]
-    _check(lib().mr_fips_health_batch(_dptr(d_blocks), n, _dptr(d_stats), _stream(d_blocks, stream)),
+    _check(lib().mr_fips_health_batch(_arg(d_blocks, "d_blocks", 1, n * 2500, 2500),
+                                      n, _arg(d_stats, "d_stats", 4, n * 16), _stream(d_blocks, stream)),
            "mr_fips_health_batch")

@@ -316,6 +316,8 @@ struct mr_drbg {
 
 extern "C" {
 
+uint32_t mr_internal_drbg_streams(const mr_drbg *d) { return d ? d->streams : 0; }
+
 int mr_drbg_create(mr_drbg **out, const uint8_t *entropy, size_t entropy_len, const uint8_t *nonce, size_t nonce_len,
                    const uint8_t *pers, size_t pers_len, uint32_t streams, int device) {
     using namespace mr;

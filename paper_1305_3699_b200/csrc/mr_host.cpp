@@ -478,6 +478,16 @@ static bool fits(const Base &b, const Big &N) {
     return cmp(lhs, b.M) < 0 && cmp(lhs2, b.Mp) < 0;
 }
 
+// largest b such that every modulus below 2^b passes fits() for this base (mr_rns_ctx_info)
+static int max_modulus_bits(const Base &b) {
+    for (int nb = 32 * b.k; nb > 1; nb--) {
+        Big t((size_t)(nb + 31) / 32, 0xFFFFFFFFu);
+        if (nb % 32) t.back() = (1u << (nb % 32)) - 1u;
+        if (fits(b, t)) return nb;
+    }
+    return 1;
+}
+
 static int auto_k(const Big &N, int min_k) {
     for (int i = 0; i < kNumK; i++) {
         int k = kSupportedK[i];
@@ -495,12 +505,14 @@ struct DevProg {
     u64 *d_ops = nullptr;
     u32 nops = 0;
     int w = 1;
+    bool transient = false;    // not cached: stream-ordered allocation, freed by release_prog after the launch
 };
 
 struct mr_rns_ctx {
     int k = 0, device = 0;
     size_t limbs = 0;
     int bits = 0;
+    int max_bits = 0;          // capacity of this k's base pair (admission test of DESIGN.md §3)
     Big N;
     u32 *d_cx = nullptr;       // device context block
     const u32 *d_pow = nullptr;
@@ -510,7 +522,8 @@ struct mr_rns_ctx {
     const u32 *d_wide = nullptr;   // wide-operand table of this k (wide_path(k))
     std::vector<u32> h_cx;
     std::mutex mu;             // guards the program cache
-    std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program
+    std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program (<= kProgCache)
+    cudaStream_t upload = nullptr;                   // private stream for program uploads
 };
 
 struct mr_rsa_priv {
@@ -701,6 +714,7 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->device = device;
     c->limbs = limbs;
     c->bits = bits(N);
+    c->max_bits = max_modulus_bits(b);
     c->N = N;
     const size_t tc_words = tc_ok(k) ? tc_bbytes(k) / 4 : 0;
     int rc = MR_OK;
@@ -846,31 +860,57 @@ static Ladder build_program(const Big &E, bool crt) {
 static u32 table_slots(int w) { return (1u << (w - 1)) + 1; }
 }  // namespace mr
 
-// program for exponent E on ctx, built and uploaded once, then reused by every batch call
-static int get_prog(mr_rns_ctx *c, const Big &E, bool crt, DevProg *out) {
+// Program for exponent E on ctx.  The first kProgCache distinct (exponent, crt) programs of a context are
+// built, uploaded once (cudaMalloc + a copy on a private stream that the host waits for: no device-wide
+// synchronisation) and cached until the context is destroyed; cached programs are never evicted, so a pointer
+// handed to one thread can never be freed under another thread's launch.  Past the bound, a program is
+// TRANSIENT: allocated and copied stream-ordered on the caller's stream and released with cudaFreeAsync on the
+// same stream after the launch (release_prog), so an unbounded stream of distinct exponents costs one small
+// H2D copy per call and no memory growth.
+static constexpr size_t kProgCache = 64;
+
+static int get_prog(mr_rns_ctx *c, const Big &E, bool crt, DevProg *out, void *stream) {
     std::lock_guard<std::mutex> lk(c->mu);
     auto key = std::make_pair(E, crt);
     auto it = c->progs.find(key);
-    if (it == c->progs.end()) {
-        Ladder L = build_program(E, crt);
-        DevProg dp;
-        dp.nops = (u32)L.ops.size();
-        dp.w = L.w;
-        if (cudaSetDevice(c->device) != cudaSuccess) return MR_ERR_CUDA;
-        if (cudaMalloc(&dp.d_ops, L.ops.size() * 8) != cudaSuccess) return MR_ERR_NOMEM;
-        if (cudaMemcpy(dp.d_ops, L.ops.data(), L.ops.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
-            cudaFree(dp.d_ops);
+    if (it != c->progs.end()) {
+        *out = it->second;
+        return MR_OK;
+    }
+    Ladder L = build_program(E, crt);
+    DevProg dp;
+    dp.nops = (u32)L.ops.size();
+    dp.w = L.w;
+    if (cudaSetDevice(c->device) != cudaSuccess) return MR_ERR_CUDA;
+    const size_t bytes = L.ops.size() * 8;
+    if (c->progs.size() >= kProgCache) {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (cudaMallocAsync(&dp.d_ops, bytes, st) != cudaSuccess) return MR_ERR_NOMEM;
+        // pageable source: staged before the call returns, so L may go out of scope
+        if (cudaMemcpyAsync(dp.d_ops, L.ops.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            cudaFreeAsync(dp.d_ops, st);
             return MR_ERR_CUDA;
         }
-        if (c->progs.size() > 64) {  // bound the cache: drop everything (programs are cheap to rebuild)
-            cudaDeviceSynchronize();
-            for (auto &kv : c->progs) cudaFree(kv.second.d_ops);
-            c->progs.clear();
-        }
-        it = c->progs.emplace(key, dp).first;
+        dp.transient = true;
+        *out = dp;
+        return MR_OK;
     }
-    *out = it->second;
+    if (!c->upload) {
+        if (cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking) != cudaSuccess) return MR_ERR_CUDA;
+    }
+    if (cudaMalloc(&dp.d_ops, bytes) != cudaSuccess) return MR_ERR_NOMEM;
+    if (cudaMemcpyAsync(dp.d_ops, L.ops.data(), bytes, cudaMemcpyHostToDevice, c->upload) != cudaSuccess ||
+        cudaStreamSynchronize(c->upload) != cudaSuccess) {
+        cudaFree(dp.d_ops);
+        return MR_ERR_CUDA;
+    }
+    c->progs.emplace(key, dp);
+    *out = dp;
     return MR_OK;
+}
+
+static void release_prog(const DevProg &dp, void *stream) {
+    if (dp.transient) cudaFreeAsync(dp.d_ops, (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------ C ABI
@@ -913,13 +953,16 @@ void mr_rns_ctx_destroy(mr_rns_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->d_cx) cudaFree(ctx->d_cx);
     for (auto &kv : ctx->progs) cudaFree(kv.second.d_ops);
+    if (ctx->upload) cudaStreamDestroy(ctx->upload);
     delete ctx;
 }
 
-int mr_rns_ctx_info(const mr_rns_ctx *ctx, int *k, size_t *limbs, int *modulus_bits, int *paper_cap_bits) {
+int mr_rns_ctx_info(const mr_rns_ctx *ctx, int *k, size_t *limbs, int *max_modulus_bits, int *modulus_bits,
+                    int *paper_cap_bits) {
     if (!ctx) return MR_ERR_ARG;
     if (k) *k = ctx->k;
     if (limbs) *limbs = ctx->limbs;
+    if (max_modulus_bits) *max_modulus_bits = ctx->max_bits;
     if (modulus_bits) *modulus_bits = ctx->bits;
     if (paper_cap_bits) *paper_cap_bits = ctx->k * 31;  // P:48 "128 32-bit primes ... 3,968-bit" = 128 x 31 (R4)
     return MR_OK;
@@ -997,6 +1040,10 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     if (use_tc) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device);
+        // MR_RNS_MAX_SMS=n: size the persistent grid as if only n SMs existed (tests and sanitizer runs reach
+        // the split schedule with small batches this way; results do not depend on it)
+        static const int max_sms = [] { const char *e = getenv("MR_RNS_MAX_SMS"); return e ? atoi(e) : 0; }();
+        if (max_sms > 0) sms = std::min(sms, std::max(2, max_sms));
         if (pair) {   // gc = CTA pairs per context
             gc = std::max<u32>(1u, std::min<u32>((u32)(sms / 2) / (u32)nctx, ctas0 / 2));
             grid = 2 * gc * nctx;
@@ -1015,7 +1062,7 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     const char *ns = getenv("MR_RNS_NO_SPLIT");
     const bool split = use_tc && !(ns && ns[0] == '1') && njobs > slots_per_group && njobs % slots_per_group != 0;
     const size_t table_words = (size_t)(table_slots(w) + (split ? 1 : 0)) * nch * jobs_total;
-    const size_t flag_words = split ? (size_t)2 * njobs * 2 : 0;
+    const size_t flag_words = split ? (size_t)2 * njobs * 2 + 1 : 0;   // + the start-order ticket
     u32 *d_table = nullptr;
     if (cudaMallocAsync(&d_table, (table_words + flag_words) * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
     if (split && cudaMemsetAsync(d_table + table_words, 0, flag_words * 4, st) != cudaSuccess) {
@@ -1067,9 +1114,11 @@ int mr_modexp_batch(const mr_rns_ctx *ctx, const uint32_t *d_x, uint32_t *d_y, s
     Big E = exp_limbs ? big_of(exp, exp_limbs) : Big();
     mr_rns_ctx *c = const_cast<mr_rns_ctx *>(ctx);
     DevProg dp;
-    int rc = get_prog(c, E, false, &dp);
+    int rc = get_prog(c, E, false, &dp, stream);
     if (rc != MR_OK) return rc;
-    return launch_ladders(&c, &dp, 1, d_x, ctx->limbs, 0, d_y, ctx->limbs, count, d_status, stream);
+    rc = launch_ladders(&c, &dp, 1, d_x, ctx->limbs, 0, d_y, ctx->limbs, count, d_status, stream);
+    release_prog(dp, stream);
+    return rc;
 }
 
 int mr_rsa_encrypt_batch(const mr_rns_ctx *n_ctx, const uint32_t *e, size_t e_limbs, const uint32_t *d_m,
@@ -1143,17 +1192,29 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
     const size_t H = priv->half;
     mr_rns_ctx *cs[2] = {priv->cp, priv->cq};
     DevProg L[2];
-    int rc0 = get_prog(priv->cp, priv->dp, true, &L[0]);
-    if (rc0 == MR_OK) rc0 = get_prog(priv->cq, priv->dq, true, &L[1]);
-    if (rc0 != MR_OK) return rc0;
+    int rc0 = get_prog(priv->cp, priv->dp, true, &L[0], stream);
+    if (rc0 == MR_OK) rc0 = get_prog(priv->cq, priv->dq, true, &L[1], stream);
+    if (rc0 != MR_OK) {
+        release_prog(L[0], stream);
+        return rc0;
+    }
     if (cudaSetDevice(priv->cp->device) != cudaSuccess) return MR_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
     u32 *d_mpq = nullptr;
     int32_t *d_st = d_status;
     int32_t *d_tmpst = nullptr;
-    if (cudaMallocAsync(&d_mpq, 2 * count * H * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    if (cudaMallocAsync(&d_mpq, 2 * count * H * 4, st) != cudaSuccess) {
+        release_prog(L[0], stream);
+        release_prog(L[1], stream);
+        return MR_ERR_NOMEM;
+    }
     if (!d_st) {
-        if (cudaMallocAsync(&d_tmpst, count * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMallocAsync(&d_tmpst, count * 4, st) != cudaSuccess) {
+            cudaFreeAsync(d_mpq, st);
+            release_prog(L[0], stream);
+            release_prog(L[1], stream);
+            return MR_ERR_NOMEM;
+        }
         d_st = d_tmpst;
     }
     int rc = launch_ladders(cs, L, 2, d_c, 2 * H, H, d_mpq, H, count, d_st, stream);
@@ -1189,6 +1250,8 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
     }
     cudaFreeAsync(d_mpq, st);
     if (d_tmpst) cudaFreeAsync(d_tmpst, st);
+    release_prog(L[0], stream);
+    release_prog(L[1], stream);
     return rc;
 }
 

@@ -233,7 +233,7 @@ struct ModexpParams {
     // tensor kernel, split schedule: a job whose ops straddle two tile slots hands its
     // state over through table slot `hslot` and a per-(job, rank) flag (zeroed before the launch)
     u32 hslot;                // handoff slot index in the window table (= table_slots(w))
-    u32 *flags;               // [2 contexts][jobs][2 ranks]; null = no split schedule
+    u32 *flags;               // [2 contexts][jobs][2 ranks] + 1 start ticket; null = no split schedule
 };
 
 struct CombineParams {          // CRT recombination m = m_q + q ((m_p - m_q) qinv mod p)

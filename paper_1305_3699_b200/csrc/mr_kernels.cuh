@@ -590,6 +590,11 @@ constexpr u32 BEV = BEV_;                                      // the per-channe
 constexpr size_t TC_SMEM = tc_smem_for(TCT);
 
 __device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ u64 globaltimer_ns() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // word index of (input row i, output column j) inside one half of the IMAD-path tile image (be_*)
 __device__ __forceinline__ u32 be_img_index(u32 i, u32 j) {
@@ -1121,10 +1126,28 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     u32 *tslot = reinterpret_cast<u32 *>(mbar + (PAIR ? 2 : 1) * TCT);
     u32 rank = 0;                                               // CTA rank in the pair (pair mode)
     if (PAIR) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    const u32 unit = PAIR ? blockIdx.x / 2 : blockIdx.x;        // CTA, or CTA pair
+    const u32 tid = threadIdx.x, tile = tid / 128, m = tid % 128;
+    // Unit = CTA (or CTA pair).  Split schedule: units are numbered in START order by a ticket, so a unit
+    // that waits for a hand-over (below) only ever waits for a unit that has already started, i.e. is
+    // resident or finished: no deadlock whatever part of the grid is resident (concurrent kernels on other
+    // streams, MPS SM limits).  Whole-job round robin has no inter-CTA waits and uses blockIdx.
+    u32 unit = PAIR ? blockIdx.x / 2 : blockIdx.x;
+    if (P.flags) {
+        __shared__ u32 s_ticket;
+        const u32 njobs_ = PAIR ? P.ctas0 / 2 : P.ctas0;
+        if (tid == 0 && rank == 0) s_ticket = atomicAdd(P.flags + (size_t)4 * njobs_, 1u);
+        if (PAIR) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            u32 ra;
+            asm("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(smem_u32(&s_ticket)));
+            asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(unit) : "r"(ra) : "memory");
+        } else {
+            __syncthreads();
+            unit = s_ticket;
+        }
+    }
     const u32 sel = unit >= P.tc_gc ? 1u : 0u;
     const u32 *gcx = sel ? P.ctx[1] : P.ctx[0];
-    const u32 tid = threadIdx.x, tile = tid / 128, m = tid % 128;
     // stage constants: context block, IMAD-path BE image words, tensor images
     for (u32 w = tid; w < CXW; w += blockDim.x) s_cx[w] = gcx[w];
     for (u32 w = tid; w < BEV; w += blockDim.x) s_vec[w] = __ldg(P.be_tab + bev_c(K) + w);
@@ -1175,16 +1198,18 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     const u32 Gc = P.tc_gc, cta = unit - sel * Gc;
     const u32 njobs = PAIR ? P.ctas0 / 2 : P.ctas0;
     // Whole jobs round-robin (no flags), or the split (McNaughton wrap-around) schedule of DESIGN.md §4f: the
-    // group's njobs x L op-units are laid out linearly and slot s = cta * TCT + tile takes units
+    // group's njobs x L op-units are laid out linearly and slot s = NS - 1 - (cta * TCT + tile) takes units
     // [s C, (s+1) C), C = max(L, ceil(njobs L / NS)).  A job straddling the boundary of slots s and s+1 runs
     // its EARLY ops at the start of slot s+1 and its LATE ops at the end of slot s (C >= L keeps the two
-    // parts apart in time); the state passes through table slot hslot and a release/acquire flag.
+    // parts apart in time); the state passes through table slot hslot and a release/acquire flag.  The
+    // reversed numbering puts slot s+1 in an earlier-started unit (or an earlier tile of the same CTA), and
+    // an early part is the first thing its slot runs, so every wait is for work that is already running.
     // One loop, one inlined copy of run_program (the multiplication code is large: instruction cache).
     const bool split = P.flags != nullptr;
     const u32 L = sel ? P.nops[1] : P.nops[0], NS = Gc * TCT;
     const u64 W = (u64)njobs * L;
     const u64 C = (W + NS - 1) / NS > L ? (W + NS - 1) / NS : (u64)L;
-    const u64 s0 = (u64)(cta * TCT + tile) * C;
+    const u64 s0 = (u64)(NS - 1 - (cta * TCT + tile)) * C;
     const u64 s1 = s0 + C < W ? s0 + C : W;
     const size_t hoff = (size_t)P.hslot * NCH * P.jobs_total;
     u32 *flag_base = split ? P.flags + (size_t)sel * njobs * 2 + rank : nullptr;
@@ -1213,10 +1238,12 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
         if (ob) {   // wait for the early part, then resume from the handed-over state
             if (m == 0) {
                 u32 v = 0;
+                const u64 t0 = globaltimer_ns();
 #pragma unroll 1
-                for (u32 spin = 0; !v; spin++) {
+                while (true) {
                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-                    if (spin > (1u << 28)) __trap();
+                    if (v) break;
+                    if (globaltimer_ns() - t0 > 120000000000ull) __trap();   // 120 s: a lost hand-over
                 }
             }
             tile_sync(mm.t);

@@ -42,6 +42,68 @@ __global__ void k_kg_start(u64 seed, const u64 *index, u32 nslots, u32 L, u32 *s
     o[0] |= 1u;
 }
 
+// DRBG-seeded variant (mr_rsa_keygen_batch_drbg): start of search s = L words of Hash_DRBG output with the
+// top two bits and bit 0 forced (FIPS 186-4 B.3.3 draws the candidate from an approved RBG)
+__global__ void k_kg_start_rand(const u32 *rnd, u32 nslots, u32 L, u32 *starts) {
+    const u32 s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    u32 *o = starts + (size_t)s * L;
+    for (u32 l = 0; l < L; l++) o[l] = rnd[(size_t)s * L + l];
+    o[L - 1] |= 0xC0000000u;
+    o[0] |= 1u;
+}
+
+// Random Miller-Rabin bases for the DRBG-seeded variant: FIPS 186-4 C.3.1 step 4.3 wants b uniform in
+// [2, w - 2]; the "extra random bits" method of FIPS 186-4 B.5.1 gives b = 2 + (c mod (w - 3)) with c of
+// 32 (L + 2) DRBG bits (statistical distance from uniform < 2^-62).  w has its top two bits set, so
+// m = w - 3 > 2^(32 L - 1): the top L words of c are < 2m (one conditional subtraction), then the low 64
+// bits enter one at a time (r = 2 r + bit, minus m when it reaches m).  One thread per item.
+__global__ void k_kg_rand_bases(const u32 *cand, const u32 *rnd, u32 items, u32 L, u32 *base) {
+    const u32 it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= items) return;
+    const u32 *w = cand + (size_t)it * L, *c = rnd + (size_t)it * (L + 2);
+    u32 m[KG_MAXL], r[KG_MAXL];
+    u64 br = 3;
+    for (u32 l = 0; l < L; l++) {                 // m = w - 3
+        const u64 v = (u64)w[l] - (br & 0xFFFFFFFFull);
+        m[l] = (u32)v;
+        br = (br >> 32) + ((v >> 63) & 1);
+        r[l] = c[l + 2];
+    }
+    auto ge = [&](u32 top) {                      // (top, r) >= m
+        if (top) return true;
+        for (int l = (int)L - 1; l >= 0; l--)
+            if (r[l] != m[l]) return r[l] > m[l];
+        return true;
+    };
+    auto subm = [&]() {
+        u64 b = 0;
+        for (u32 l = 0; l < L; l++) {
+            const u64 v = (u64)r[l] - m[l] - b;
+            r[l] = (u32)v;
+            b = (v >> 63) & 1;
+        }
+    };
+    if (ge(0)) subm();
+    for (int bit = 63; bit >= 0; bit--) {
+        const u32 in = (bit >= 32 ? c[1] >> (bit - 32) : c[0] >> bit) & 1u;
+        u32 carry = in;
+        for (u32 l = 0; l < L; l++) {
+            const u32 nv = (r[l] << 1) | carry;
+            carry = r[l] >> 31;
+            r[l] = nv;
+        }
+        if (ge(carry)) subm();
+    }
+    u64 cy = 2;
+    u32 *o = base + (size_t)it * L;
+    for (u32 l = 0; l < L; l++) {                 // b = r + 2 <= w - 2
+        const u64 v = (u64)r[l] + cy;
+        o[l] = (u32)v;
+        cy = v >> 32;
+    }
+}
+
 // powers for the sieve: pw[l][i] = 2^(32 l) mod p_i, mu[i] = floor((2^64 - 1) / p_i)
 __global__ void k_kg_pow(const u32 *small, u32 nsmall, u32 L, u32 *pw, u64 *mu) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -396,6 +458,16 @@ int kg_launch_vitems(const u32 *vl, u32 nv, const u32 *vcand, const u32 *small_a
     if (!nv || R < 2) return 0;
     const u32 n = nv * (R - 1);
     k_kg_vitems<<<(n + 127) / 128, 128, 0, (cudaStream_t)st>>>(vl, nv, vcand, small_all, R, L, cand, base);
+    return kg_err();
+}
+int kg_launch_start_rand(const u32 *rnd, u32 nslots, u32 L, u32 *starts, void *st) {
+    if (!nslots) return 0;
+    k_kg_start_rand<<<(nslots + 127) / 128, 128, 0, (cudaStream_t)st>>>(rnd, nslots, L, starts);
+    return kg_err();
+}
+int kg_launch_rand_bases(const u32 *cand, const u32 *rnd, u32 items, u32 L, u32 *base, void *st) {
+    if (!items) return 0;
+    k_kg_rand_bases<<<(items + 127) / 128, 128, 0, (cudaStream_t)st>>>(cand, rnd, items, L, base);
     return kg_err();
 }
 int kg_launch_copy_rows(const u32 *src, const u32 *src_row, u32 *dst, const u32 *dst_row, u32 cnt, u32 L, void *st) {

@@ -27,8 +27,12 @@ extern "C" int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_
                                         int rounds, int k, uint8_t *d_verdict, int16_t *d_witness_round,
                                         int32_t *d_status, int device, void *stream, int forced, int window);
 
+extern "C" uint32_t mr_internal_drbg_streams(const mr_drbg *d);
+
 namespace mr {
 int kg_launch_start(u64 seed, const u64 *index, u32 nslots, u32 L, u32 *starts, void *st);
+int kg_launch_start_rand(const u32 *rnd, u32 nslots, u32 L, u32 *starts, void *st);
+int kg_launch_rand_bases(const u32 *cand, const u32 *rnd, u32 items, u32 L, u32 *base, void *st);
 int kg_launch_pow(const u32 *small, u32 nsmall, u32 L, u32 *pw, u64 *mu, void *st);
 int kg_launch_sieve(const u32 *starts, const u32 *window, const u32 *list, u32 nlist, u32 L, const u32 *small,
                     const u32 *pw, const u64 *mu, u32 nsmall, u32 W, u32 *bitmap, void *st);
@@ -117,12 +121,28 @@ int down(std::vector<T> &h, const T *d, size_t n, cudaStream_t st) {
     T *var = dev.get<T>(n);                    \
     if (!var) return MR_ERR_NOMEM
 
+// `words` fresh 32-bit words of Hash_DRBG output into a new scratch buffer of dev (rng's streams each
+// contribute one request of <= 2^16 bytes per generate call; several calls if more is needed)
+u32 *draw(Dev &dev, mr_drbg *rng, size_t words, cudaStream_t st) {
+    const size_t S = mr_internal_drbg_streams(rng);
+    const size_t per = std::min<size_t>(65536, ((words * 4 + S - 1) / S + 3) / 4 * 4);
+    const size_t chunk = S * per, calls = (words * 4 + chunk - 1) / chunk;
+    u32 *buf = dev.get<u32>(calls * chunk / 4);
+    if (!buf) return nullptr;
+    for (size_t i = 0; i < calls; i++)
+        if (mr_drbg_generate(rng, reinterpret_cast<uint8_t *>(buf) + i * chunk, per, st) != MR_OK) return nullptr;
+    return buf;
+}
+
 // Runs searches (one per entry of `index`) to completion; prime of search s -> pool row row0 + s.
+// rng != NULL (mr_rsa_keygen_batch_drbg): starts and every Miller-Rabin base come from the DRBG instead
+// of the seeded recipe (index is then only a count).
 // Every iteration is ONE Miller-Rabin launch of one-round items: phase-A items (the next G sieve
 // survivors of each search in phase A, base 2) and verification items (rounds 2..R of the candidate
 // each search in phase V found in the previous iteration).
 int run_searches(Dev &dev, cudaStream_t st, const std::vector<u64> &index, u32 L, int rounds, u64 seed,
-                 const u32 *d_small, const u32 *d_pw, const u64 *d_mu, u32 *pool, u32 row0, int device) {
+                 const u32 *d_small, const u32 *d_pw, const u64 *d_mu, u32 *pool, u32 row0, int device,
+                 mr_drbg *rng) {
     const u32 S = (u32)index.size();
     const u32 W = kWindow, R = (u32)rounds;
     KG_NEW(d_index, u64, S);
@@ -141,8 +161,14 @@ int run_searches(Dev &dev, cudaStream_t st, const std::vector<u64> &index, u32 L
     KG_NEW(d_base, u32, cap * L);
     KG_NEW(d_verd, uint8_t, cap);
     KG_NEW(d_rows, u32, 2 * (size_t)S);
-    KG_TRY(up(d_index, index, st));
-    KG_TRY(kg_launch_start(seed, d_index, S, L, d_starts, st));
+    if (rng) {
+        const u32 *rnd = draw(dev, rng, (size_t)S * L, st);
+        if (!rnd) return MR_ERR_CUDA;
+        KG_TRY(kg_launch_start_rand(rnd, S, L, d_starts, st));
+    } else {
+        KG_TRY(up(d_index, index, st));
+        KG_TRY(kg_launch_start(seed, d_index, S, L, d_starts, st));
+    }
 
     std::vector<u32> window(S, 0), tested(S, 0), pend_first(S, 0), resieve(S), ncand;
     std::vector<uint8_t> verd;
@@ -170,6 +196,12 @@ int run_searches(Dev &dev, cudaStream_t st, const std::vector<u64> &index, u32 L
         KG_TRY(kg_launch_pick(d_starts, d_window, d_bitmap, d_tested, d_list, nA, L, W, G, d_cand, d_base, d_ncand,
                               st));
         KG_TRY(kg_launch_vitems(d_vlist, nV, d_vcand, d_small, R, L, d_cand + itemsA * L, d_base + itemsA * L, st));
+        if (rng && items) {   // every item (candidate, round) gets its own random base
+            Dev rscratch(st);
+            const u32 *rnd = draw(rscratch, rng, items * (L + 2), st);
+            if (!rnd) return MR_ERR_CUDA;
+            KG_TRY(kg_launch_rand_bases(d_cand, rnd, (u32)items, L, d_base, st));
+        }
         if (items) {
             int rc = mr_internal_miller_rabin(d_cand, L, items, d_base, 1, 0, d_verd, nullptr, nullptr, device, st, 0,
                                               4);   // w = 5 measured slower here (KG 64 rounds: 14.6 k -> 11.8 k keys/s)
@@ -239,10 +271,9 @@ int run_searches(Dev &dev, cudaStream_t st, const std::vector<u64> &index, u32 L
 
 using namespace mr;
 
-#pragma GCC visibility push(default)
-extern "C" int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t seed, uint64_t first_key, int rounds,
-                                   uint32_t *d_n, uint32_t *d_p, uint32_t *d_q, uint32_t *d_d, uint32_t *d_dp,
-                                   uint32_t *d_dq, uint32_t *d_qinv, int device, void *stream) {
+static int keygen_impl(mr_drbg *rng, size_t count, int bits, uint32_t e, uint64_t seed, uint64_t first_key, int rounds,
+                       uint32_t *d_n, uint32_t *d_p, uint32_t *d_q, uint32_t *d_d, uint32_t *d_dp, uint32_t *d_dq,
+                       uint32_t *d_qinv, int device, void *stream) {
     if (bits < 256 || bits > 4096 || bits % 64 != 0 || e < 3 || !is_prime_u32(e) || rounds < 1 || rounds > 256 ||
         count > (1u << 24))
         return MR_ERR_ARG;
@@ -297,7 +328,7 @@ extern "C" int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t 
         }
         {
             Dev scratch(st);
-            int rc = run_searches(scratch, st, index, L, rounds, seed, d_small, d_pw, d_mu, pool, npool, device);
+            int rc = run_searches(scratch, st, index, L, rounds, seed, d_small, d_pw, d_mu, pool, npool, device, rng);
             if (rc != MR_OK) return rc;
         }
         for (u32 s = 0; s < S; s++) pend[owner[s]].push_back(Row{npool + s, 0xFFFFFFFEu, 0});
@@ -361,5 +392,20 @@ extern "C" int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t 
     KG_TRY(up(d_ks, ks, st));
     KG_TRY(kg_launch_assemble(pool, d_ks, (u32)count, L, e, d_n, d_p, d_q, d_d, d_dp, d_dq, d_qinv, st));
     return cudaStreamSynchronize(st) == cudaSuccess ? MR_OK : MR_ERR_CUDA;
+}
+
+#pragma GCC visibility push(default)
+extern "C" int mr_rsa_keygen_batch(size_t count, int bits, uint32_t e, uint64_t seed, uint64_t first_key, int rounds,
+                                   uint32_t *d_n, uint32_t *d_p, uint32_t *d_q, uint32_t *d_d, uint32_t *d_dp,
+                                   uint32_t *d_dq, uint32_t *d_qinv, int device, void *stream) {
+    return keygen_impl(nullptr, count, bits, e, seed, first_key, rounds, d_n, d_p, d_q, d_d, d_dp, d_dq, d_qinv,
+                       device, stream);
+}
+
+extern "C" int mr_rsa_keygen_batch_drbg(mr_drbg *rng, size_t count, int bits, uint32_t e, int rounds, uint32_t *d_n,
+                                        uint32_t *d_p, uint32_t *d_q, uint32_t *d_d, uint32_t *d_dp, uint32_t *d_dq,
+                                        uint32_t *d_qinv, int device, void *stream) {
+    if (!rng) return MR_ERR_ARG;
+    return keygen_impl(rng, count, bits, e, 0, 0, rounds, d_n, d_p, d_q, d_d, d_dp, d_dq, d_qinv, device, stream);
 }
 #pragma GCC visibility pop

@@ -333,3 +333,47 @@ def test_wide_table_identities():
     pad = [t[o["a2w"] + _wch_at(i, j, k)] for i in range(k, _wch_rows(k)) for j in (0, k - 1)]
     assert not any(pad)                                                # zero rows up to the group size
     assert L.mr_internal_wide_table(65, None, 0) < 0 and L.mr_internal_wide_table(129, None, 0) > 0
+
+
+def test_keygen_drbg_argument_errors():
+    mr, L = _lib()
+    assert L.mr_rsa_keygen_batch_drbg(None, 1, 1024, 65537, 5, *([None] * 7), 0, None) == mr.MR_ERR_ARG
+
+
+class _FakeCuda:
+    """Just enough of a torch CUDA tensor for the binding's argument checks (no device needed)."""
+
+    def __init__(self, shape, itemsize=4, device=0):
+        import math
+        self.shape, self.is_cuda, self._n = tuple(shape), True, math.prod(shape)
+        self.dtype = type("dt", (), {"itemsize": itemsize})()
+        self.device = type("dev", (), {"index": device})()
+
+    def is_contiguous(self):
+        return True
+
+    def dim(self):
+        return len(self.shape)
+
+    def numel(self):
+        return self._n
+
+    def data_ptr(self):
+        return 0x1000
+
+
+def test_binding_validates_device_buffers():
+    """the C ABI cannot see tensor sizes, so the binding checks element size, 2-D width,
+    element count and device before any pointer crosses it."""
+    mr, _ = _lib()
+    ok = _FakeCuda((10, 32))
+    assert mr._arg(ok, "x", 4, 10 * 32, 32, 0) == 0x1000
+    assert mr._arg(None, "x", 4, 1) is None
+    for bad, why in ((_FakeCuda((10, 32), itemsize=8), "8-byte"), (_FakeCuda((320,)), "1-D"),
+                     (_FakeCuda((10, 31)), "width"), (_FakeCuda((9, 32)), "short"),
+                     (_FakeCuda((10, 32), device=1), "device")):
+        with pytest.raises(mr.MrError) as e:
+            mr._arg(bad, "x", 4, 10 * 32, 32, 0)
+        assert e.value.code == mr.MR_ERR_ARG, why
+    with pytest.raises(mr.MrError):
+        mr.mr_modexp_batch(ctypes.c_void_p(12345), ok, ok, 10, 3)        # handle not created here

@@ -108,3 +108,60 @@ def test_keygen_batch_properties_and_sample(orc):
         for x in (g["p"], g["q"]):
             v, _ = orc.miller_rabin(x, [rng.randrange(2, x - 1) for _ in range(20)], fp)
             assert v == orc.PROBABLY_PRIME
+
+
+def keygen_drbg(count, bits, e, rounds, entropy, nonce=b"\x00" * 16, streams=64):
+    import torch
+    mr = _mr()
+    rng = mr.Drbg(entropy, nonce, b"keygen", streams=streams)
+    full, half = bits // 32, bits // 64
+    out = {f: torch.zeros((count, full if f in ("n", "d") else half), dtype=torch.int32, device="cuda")
+           for f in FIELDS}
+    mr.mr_rsa_keygen_batch_drbg(rng, count, bits, e, rounds, out["n"], out["p"], out["q"], out["d"], out["dp"],
+                                out["dq"], out["qinv"])
+    torch.cuda.synchronize()
+    host = {f: out[f].cpu().numpy().view(np.uint32) for f in FIELDS}
+    return [{f: int.from_bytes(host[f][i].tobytes(), "little") for f in FIELDS} for i in range(count)]
+
+
+@pytest.mark.gpu
+def test_keygen_drbg_valid_keys_and_determinism(orc):
+    """the production entry draws starts and every Miller-Rabin base from the GPU
+    Hash_DRBG.  Every key is a valid RSA key whose primes pass 20 oracle MR rounds and sympy's BPSW; the
+    same entropy gives the same keys, other entropy other keys; the keys differ from the seeded recipe."""
+    import random
+    import sympy
+    e = 65537
+    ent = bytes(range(32))
+    got = keygen_drbg(64, 2048, e, 5, ent)
+    for g in got:
+        p, q = g["p"], g["q"]
+        assert g["n"] == p * q and g["n"].bit_length() == 2048
+        assert p >> 1022 == 3 and q >> 1022 == 3 and abs(p - q).bit_length() > 1024 - 100
+        phi = (p - 1) * (q - 1)
+        assert g["d"] * e % phi == 1 and g["dp"] == g["d"] % (p - 1) and g["dq"] == g["d"] % (q - 1)
+        assert g["qinv"] * q % p == 1
+    rng = random.Random(9)
+    fp = orc.base_primes(66)
+    for g in got[:8]:
+        for x in (g["p"], g["q"]):
+            assert sympy.isprime(x)
+            v, _ = orc.miller_rabin(x, [rng.randrange(2, x - 1) for _ in range(20)], fp)
+            assert v == orc.PROBABLY_PRIME
+    assert len({g["p"] for g in got} | {g["q"] for g in got}) == 128
+    assert keygen_drbg(64, 2048, e, 5, ent) == got      # same entropy and request pattern: same keys
+    other = keygen_drbg(8, 2048, e, 5, bytes(range(1, 33)))
+    assert not ({o["n"] for o in other} & {g["n"] for g in got})
+    seeded = keygen(1, 2048, e, 0, 5)[0]
+    assert seeded["n"] not in {g["n"] for g in got}
+
+
+@pytest.mark.gpu
+def test_keygen_drbg_random_bases_reject_composites():
+    """RSA-1024 keys with a single Miller-Rabin round per prime (random base): the primes must still be
+    prime with overwhelming probability (a composite that survives sieving passes one random round with
+    probability <= 1/4 and typically ~2^-40); checked by sympy for all 32 keys."""
+    import sympy
+    got = keygen_drbg(32, 1024, 65537, 1, b"\x5a" * 32, streams=8)
+    for g in got:
+        assert sympy.isprime(g["p"]) and sympy.isprime(g["q"])
