@@ -286,7 +286,8 @@ __host__ __device__ constexpr u32 pc_live(u32 k) { return 4 * k + 3; }          
 __host__ __device__ constexpr u32 pc_d(u32 k) { return 4 * k + 4; }             // [k]  d limbs
 __host__ __device__ constexpr u32 pc_n(u32 k) { return 5 * k + 4; }             // [k+1] n limbs (0 above limbs),
                                                                                   // column layout: coalesced reads
-__host__ __device__ constexpr u32 pc_words(u32 k) { return 6 * k + 5; }
+__host__ __device__ constexpr u32 pc_sig64(u32 k) { return 6 * k + 5; }         // [k]  σ_i 2^64 mod m_i (canonical)
+__host__ __device__ constexpr u32 pc_words(u32 k) { return 7 * k + 5; }
 
 // ---------------------------------------------------------------------------------------------
 // Per-k entry points exported by each mr_k<K>.cu translation unit.

@@ -1474,7 +1474,10 @@ __global__ void __launch_bounds__(T) k_mr_setup(const MrParams P) {
         for (int k = 0; k < K; k++) {              // σ_i = -(n M_i)^-1 mod m_i
             const u32 c = GB(O_C + k);
             const u32 v = inv_word(canon(mulmod(S(st, k), GB(O_MIS + k), c), c), c);
-            pc[(size_t)(pc_sigma(K) + k) * cs] = v ? (0u - c) - v : 0u;
+            const u32 sg = v ? (0u - c) - v : 0u;
+            pc[(size_t)(pc_sigma(K) + k) * cs] = sg;
+            // σ_i 2^64 ≡ σ_i c_i^2 (mod m_i): the word-Montgomery form the tensor rounds kernel streams
+            pc[(size_t)(pc_sig64(K) + k) * cs] = canon(mulmod(mulmod(sg, c, c), c, c), c);
         }
         // s, d with n - 1 = 2^s d
         u32 l0 = 0, w0 = nrow[0] & ~1u;
@@ -1662,14 +1665,17 @@ struct CtxMr {                        // per-candidate constants of one thread
     static constexpr bool kMerged = false;
     static constexpr bool kScaled = false;
     static constexpr bool kMont = true;   // word-Montgomery reductions: σ_i held as σ_i 2^64, C1 as C1 2^32
-    u32 sig[K];                       // σ_i 2^64 mod m_i in registers (the channel-product loop is fully unrolled)
+    // σ_i 2^64 and c2_j = |n M^-1 λ_j|_{m'_j} stream from the candidate-major pc block in L2 (coalesced
+    // across the tile: lane m reads column i + m) instead of occupying 33 registers and 17 KB of shared
+    // memory per tile: that is what lets four tiles (16 warps) fit an SM within 128 registers per thread
+    const u32 *sigcol;                // pc + pc_sig64 rows: σ_i 2^64 at sigcol[i * nstride]
     const u32 *c1c;                   // shared memory: |M^-1 λ_j^-1| 2^32 mod m'_j (per k)
-    const u32 *c2row;                 // shared memory: c2row[j * 128] = |n M^-1 λ_j|_{m'_j}
+    const u32 *c2col;                 // pc + pc_c2 rows: c2_j at c2col[j * nstride]
     u32 nmv;                          // n M^-1 mod 2^32
     const u32 *ncol;                  // pcol + pc_n rows: n limb l at ncol[l * nstride] (coalesced)
     u32 nstride;
-    __device__ u32 sigma(int i) const { return sig[i]; }
-    __device__ u32 c2(int j) const { return c2row[j * 128]; }
+    __device__ u32 sigma(int i) const { return __ldcg(sigcol + (size_t)i * nstride); }
+    __device__ u32 c2(int j) const { return __ldcg(c2col + (size_t)j * nstride); }
     __device__ u32 nminv() const { return nmv; }
     __device__ u32 nlimb(int l) const { return ncol[(size_t)l * nstride]; }   // l in [0, K]
 };
@@ -1696,7 +1702,7 @@ __device__ __forceinline__ bool x_is_nm1_t(const StTile &st, const CtxMr &cs) {
 }
 
 constexpr size_t tc_mr_smem_for(int tiles) {
-    return 4 * (size_t)(tiles * TC_ROWS + tiles * K * 128 + BEV + pad4(NCH) + 3 * pad4(K)) +
+    return 4 * (size_t)(tiles * TC_ROWS + BEV + pad4(NCH) + 3 * pad4(K)) +
            (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
 }
 constexpr bool tc_mr_fits(int tiles) { return tc_mr_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
@@ -1705,13 +1711,12 @@ constexpr u32 TC_MR_TMEM = tmem_cols_for(TCM * TCNP);
 
 __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P) {
     extern __shared__ __align__(1024) u32 smem[];
-    // layout: [B1 (unmerged, per k) | B2 | A tiles | state rows | c2 rows | vectors | ONE | a1c | a2c | mbar]
+    // layout: [B1 (unmerged, per k) | B2 | A tiles | state rows | vectors | ONE | a1c | a2c | mbar]
     uint8_t *s_b1 = reinterpret_cast<uint8_t *>(smem);
     uint8_t *s_b2 = s_b1 + tc_bbytes(K);
     uint8_t *s_a = s_b2 + tc_bbytes(K);
     u32 *st_all = reinterpret_cast<u32 *>(s_a + TCM * tc_abytes(K));
-    u32 *c2_all = st_all + TCM * TC_ROWS;
-    u32 *s_vec = c2_all + TCM * K * 128;
+    u32 *s_vec = st_all + TCM * TC_ROWS;
     u32 *s_be = s_vec - bev_c(K);
     u32 *s_one = s_vec + BEV;
     u32 *s_a1c = s_one + pad4(NCH);
@@ -1752,7 +1757,6 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                                         smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, 0u, 0u, m == 0}};
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
-    u32 *c2rows = c2_all + tile * K * 128 + m;
     const size_t cnt = P.count;
     const u32 L = P.limbs, w = P.window, E = 1u << w, R = P.rounds;
     // window table: each candidate slot's E entries (+ the check stash) contiguous, NCHP words apart,
@@ -1800,15 +1804,9 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
             pending = false;
         }
         CtxMr cs;
-#pragma unroll
-        for (int k = 0; k < K; k++) {   // σ_k 2^64 ≡ σ_k c_k² (mod m_k)
-            const u32 c = GB(O_C + k);
-            cs.sig[k] = mulmod(mulmod(pcol[(size_t)(pc_sigma(K) + k) * cnt], c, c), c, c);
-        }
+        cs.sigcol = pcol + (size_t)pc_sig64(K) * cnt;
         cs.c1c = s_c1c;
-#pragma unroll 1
-        for (int j = 0; j < K; j++) c2rows[j * 128] = pcol[(size_t)(pc_c2(K) + j) * cnt];
-        cs.c2row = c2rows;
+        cs.c2col = pcol + (size_t)pc_c2(K) * cnt;
         cs.nmv = pcol[(size_t)pc_nminv(K) * cnt];
         cs.ncol = pcol + (size_t)pc_n(K) * cnt;
         cs.nstride = (u32)cnt;
