@@ -722,13 +722,13 @@ def run_rank(args, world, rank, dev, wl: Workload, step):
     clocks = clk.summary()
     line["clocks"] = clocks
     line["gpu_launches"] = (launch[1] + launch[3]) if launch else None
-    line["roofline"] = roofline(wl, n_loc, launch, clocks, world)
+    line["roofline"] = roofline(wl, n_loc, launch, clocks, world, total_ms / args.steps)
     if not args.no_cpu_baseline and (world == 1 or args.cpu_baseline_multi):
         line["cpu_baseline"] = cpu_baseline(wl)
     return line
 
 
-def roofline(wl: Workload, n_loc: int, launch, clocks, world):
+def roofline(wl: Workload, n_loc: int, launch, clocks, world, step_ms: float):
     """the dominant kernel (the ladder launch) against its binding roofline.  Work per unit is algorithmic
     (SURVEY §8(d)): tensor ops = 2 x 16 u8 MACs x 2k(k+1) base-extension word products per Montgomery
     multiplication; CUDA-core IMAD-eq = 2 x (6k + 4) elementwise word products per multiplication.  The
@@ -736,7 +736,8 @@ def roofline(wl: Workload, n_loc: int, launch, clocks, world):
     is that pipe's achieved / peak.  The all-work IMAD-eq rate over the IMAD peak (what an IMAD-only
     implementation could reach at most) is reported separately as imad_eq_speedup."""
     ms_l, n_l, ms_c, n_c = launch
-    ladder_ms = ms_l / max(1, n_l)
+    # ladder launches are timed by the library hook; Miller-Rabin (not instrumented) takes the step's event time
+    ladder_ms = ms_l / n_l if n_l else step_ms
     t_ops, e_ops, all_ops = wl.work()
     units = units_of(wl, n_loc)
     sec = ladder_ms / 1e3

@@ -1674,8 +1674,10 @@ struct CtxMr {                        // per-candidate constants of one thread
     u32 nmv;                          // n M^-1 mod 2^32
     const u32 *ncol;                  // pcol + pc_n rows: n limb l at ncol[l * nstride] (coalesced)
     u32 nstride;
-    __device__ u32 sigma(int i) const { return __ldcg(sigcol + (size_t)i * nstride); }
-    __device__ u32 c2(int j) const { return __ldcg(c2col + (size_t)j * nstride); }
+    // through L1 (ld.global.ca): a tile's σ and c2 columns (34 KB) stay in L1 when few tiles share the SM
+    // (the early-exit items phase runs one tile per SM and is latency-bound)
+    __device__ u32 sigma(int i) const { return __ldca(sigcol + (size_t)i * nstride); }
+    __device__ u32 c2(int j) const { return __ldca(c2col + (size_t)j * nstride); }
     __device__ u32 nminv() const { return nmv; }
     __device__ u32 nlimb(int l) const { return ncol[(size_t)l * nstride]; }   // l in [0, K]
 };
