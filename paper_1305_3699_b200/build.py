@@ -58,11 +58,12 @@ def build(force: bool = False, jobs: int | None = None) -> str:
         objs.append(obj)
         if force or _stale(obj, [src] + deps):
             steps.append(([NVCC] + NVFLAGS + ["-c", src, "-o", obj], obj + ".log"))
-    for cu in ("mr_keygen", "mr_wide", "mr_drbg"):
+    for cu in ("mr_keygen", "mr_wide", "mr_lanes", "mr_drbg"):
         src = os.path.join(CSRC, cu + ".cu")
         obj = os.path.join(OBJ, cu + ".o")
         objs.append(obj)
-        if force or _stale(obj, [src] + deps):
+        extra = [os.path.join(CSRC, "mr_wide.cu")] if cu == "mr_lanes" else []
+        if force or _stale(obj, [src] + deps + extra):
             steps.append(([NVCC] + NVFLAGS + ["-c", src, "-o", obj], obj + ".log"))
     for cpp in ("mr_host", "mr_keygen_host"):
         host_src = os.path.join(CSRC, cpp + ".cpp")

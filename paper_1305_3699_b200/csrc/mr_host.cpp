@@ -32,7 +32,9 @@ MR_DECLARE_K(129)
 
 size_t wide_smem_bytes(u32 k);
 int wide_messages_per_cta();
-int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, void *stream);
+int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream);
+int wide_messages_per_cta_lanes();
+int launch_modexp_wide_lanes(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream);
 int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream);
 
 static const KernelSet &kernel_set_for(int k) {
@@ -404,6 +406,16 @@ static bool wide_path(int k) {
     return k >= 97 && k >= kmin;
 }
 
+// Small-batch path: narrow k whose contexts also carry the wide section, so a batch too small
+// to fill the SMs with 128-message tensor tiles runs on the channels-on-threads kernel with one message per
+// CTA (mr_lanes.cu).  MR_RNS_SMALL_MAX = the largest count x contexts that takes it (0 disables it).
+static bool small_ok(int k) { return k >= 17 && k <= 65; }
+static long g_small_override = -1;   // mr_internal_set_small_max (tests: both paths at the same batch size)
+static size_t small_max() {
+    static const size_t v = [] { const char *e = getenv("MR_RNS_SMALL_MAX"); return e ? (size_t)atol(e) : (size_t)2048; }();
+    return g_small_override >= 0 ? (size_t)g_small_override : v;
+}
+
 static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **d_be) {
     auto key = std::make_pair(device, k);
     auto it = g_devbases.find(key);
@@ -423,7 +435,7 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
         }
     }
     DevBase db;
-    if (wide_path(k)) {   // wide-operand kernel: one table in HBM, no constant bank, no shared-memory images
+    if (wide_path(k) || small_ok(k)) {   // wide-operand / small-batch kernel: one table in HBM
         const std::vector<u32> t = build_wide_table(b);
         if (cudaMalloc(&db.d_wide, t.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_wide, t.data(), t.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
@@ -519,7 +531,8 @@ struct mr_rns_ctx {
     const u32 *d_be = nullptr;
     const u32 *d_tcb2 = nullptr;
     const u32 *d_mpl = nullptr;
-    const u32 *d_wide = nullptr;   // wide-operand table of this k (wide_path(k))
+    const u32 *d_wide = nullptr;   // wide-operand table of this k (wide_path(k) or small_ok(k))
+    u32 cxw = 0;                   // word offset of the wide section in the context block (0: none)
     std::vector<u32> h_cx;
     std::mutex mu;             // guards the program cache
     std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program (<= kProgCache)
@@ -669,10 +682,10 @@ static bool fill_tc_scaled(const Base &b, u32 *x) {
 
 // per-context part of the wide kernel's constants (mr_internal.h wide_cx_*): σ_i 2^64 mod m_i and
 // A1'[i][j] 2^32 mod m'_j, A1' = |M_i|_{m'_j} |N M^-1 λ_j| (6.4 merged into BE1, row-major)
-static void fill_wide_ctx(const Base &b, u32 *x) {
+static void fill_wide_ctx(const Base &b, u32 *x, u32 cxw) {
     const int k = b.k;
     const u32 *A1 = b.flat.data() + base_layout(k).A1;
-    u32 *w = x + cx_words(k);
+    u32 *w = x + cxw;
     for (int i = 0; i < k; i++) {
         const u32 m = b.B[i], r = (u32)((1ull << 32) % m);
         w[wide_cx_sig(k) + i] = mulm(mulm(x[cx_sigma(k) + i], r, m), r, m);
@@ -721,11 +734,17 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     if (wide_path(k)) {   // cx block + wide section (σ 2^64, A1' 2^32 row-major)
         c->h_cx.assign(cx_words(k) + wide_cx_words(k), 0);
         fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
-        fill_wide_ctx(b, c->h_cx.data());
-    } else {
-        c->h_cx.assign(cx_words(k) + be_half_words(k) + 2 * tc_words, 0);
+        c->cxw = cx_words(k);
+        fill_wide_ctx(b, c->h_cx.data(), c->cxw);
+    } else {   // narrow layout; small-batch k append the wide section after the tensor images
+        const size_t narrow = cx_words(k) + be_half_words(k) + 2 * tc_words;
+        c->h_cx.assign(narrow + (small_ok(k) ? wide_cx_words(k) : 0), 0);
         fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
         fill_merged_be1(b, c->h_cx.data() + cx_words(k), c->h_cx.data());
+        if (small_ok(k)) {
+            c->cxw = (u32)narrow;
+            fill_wide_ctx(b, c->h_cx.data(), c->cxw);
+        }
     }
     if (tc_ok(k) && !fill_tc_scaled(b, c->h_cx.data())) rc = MR_ERR_ARG;   // not reachable for the R1 bases
     if (rc == MR_OK) rc = ensure_device_base(k, device, &c->d_pow, &c->d_be);
@@ -980,10 +999,10 @@ static bool tensor_path_enabled() {
 // wide-operand ladders (wide_path(k)): 16 messages per CTA, one CTA per 16 messages and context
 static int launch_ladders_wide(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x,
                                size_t in_limbs, size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status,
-                               void *stream) {
+                               void *stream, bool lanes) {
     const mr_rns_ctx *c0 = ctxs[0];
     cudaStream_t st = (cudaStream_t)stream;
-    const u32 MBm = (u32)wide_messages_per_cta();
+    const u32 MBm = (u32)(lanes ? wide_messages_per_cta_lanes() : wide_messages_per_cta());
     const u32 ctas0 = (u32)((count + MBm - 1) / MBm);
     const u32 jobs_total = ctas0 * MBm * nctx;
     int w = 1;
@@ -1012,7 +1031,8 @@ static int launch_ladders_wide(mr_rns_ctx *const *ctxs, const DevProg *progs, in
     P.table = d_table;
     P.jobs_total = jobs_total;
     int rc = timed_launch(0, st, [&] {
-                 return launch_modexp_wide(P, ctas0 * nctx, c0->d_wide, (u32)c0->k, stream);
+                 return lanes ? launch_modexp_wide_lanes(P, ctas0 * nctx, c0->d_wide, (u32)c0->k, c0->cxw, stream)
+                              : launch_modexp_wide(P, ctas0 * nctx, c0->d_wide, (u32)c0->k, c0->cxw, stream);
              }) == 0
                  ? MR_OK
                  : MR_ERR_CUDA;
@@ -1027,7 +1047,9 @@ static int launch_ladders(mr_rns_ctx *const *ctxs, const DevProg *progs, int nct
     if (cudaSetDevice(c0->device) != cudaSuccess) return MR_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
     if (wide_path(c0->k)) return launch_ladders_wide(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count,
-                                                        d_status, stream);
+                                                        d_status, stream, false);
+    if (c0->cxw && c0->d_wide && tensor_path_enabled() && count * (size_t)nctx <= small_max())   // small batch (§4j)
+        return launch_ladders_wide(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count, d_status, stream, true);
     const bool use_tc = ks.launch_modexp_tc && c0->d_tcb2 && tensor_path_enabled();
     // IMAD path: one CTA per T messages; tensor path: ctas0 = 128-message tile-jobs per context,
     // run by Gc persistent CTAs per context (one per SM share)
@@ -1427,6 +1449,12 @@ int mr_internal_timing_mr(double *ms, int *n) {
 // -1 = follow MR_RNS_IMAD_ONLY
 int mr_internal_set_path(int path) {
     g_path_override = path;
+    return MR_OK;
+}
+
+// test hook: largest count x contexts routed to the small-batch kernel (§4j); -1 restores the default
+int mr_internal_set_small_max(long n) {
+    g_small_override = n;
     return MR_OK;
 }
 
