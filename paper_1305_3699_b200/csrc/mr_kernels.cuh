@@ -762,10 +762,26 @@ __device__ __forceinline__ void tmem_ld16(u32 taddr, u32 (&v)[16]) {
 // one carry chain (ALU pipe, no IMAD).  k <= 64: d_b < 4k·255² < 2^24, so x = d0 + 2^8 d1 and
 // y = d2 + 2^8 d3 fit 32 bits and V = x + 2^16 y; k = 65: d_b < 2^24.02, every term is split.
 // hi < 2^16.1 (V < 2^48.1, plus the α·pin byte column of BE2, < 2^15).
+#ifndef MR_COMBINE_ALU
+#define MR_COMBINE_ALU 0
+#endif
 __device__ __forceinline__ void tc_split(u32 d0, u32 d1, u32 d2, u32 d3, u32 &lo, u32 &hi) {
     if (4ull * K * 255 * 255 < (1ull << 24)) {
+#if MR_COMBINE_ALU
+        // the same sums as funnel shifts and integer adds (ALU pipe): ptxas otherwise forms x with an IMAD and
+        // y·2^16 + x with an IMAD.WIDE, 6 of the FMA-heavy pipe's cycles per output (profiles/r2_c2_pipe_floor.md)
+        u32 x, y, yl, yh;
+        asm("shf.l.clamp.b32 %0, 0, %1, 8;" : "=r"(x) : "r"(d1));
+        asm("shf.l.clamp.b32 %0, 0, %1, 8;" : "=r"(y) : "r"(d3));
+        x += d0;
+        y += d2;
+        asm("shf.l.clamp.b32 %0, 0, %1, 16;" : "=r"(yl) : "r"(y));
+        asm("shf.r.clamp.b32 %0, %1, 0, 16;" : "=r"(yh) : "r"(y));
+        asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;" : "=r"(lo), "=r"(hi) : "r"(x), "r"(yl), "r"(yh));
+#else
         const u32 x = d0 + (d1 << 8), y = d2 + (d3 << 8);
         asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;" : "=r"(lo), "=r"(hi) : "r"(x), "r"(y << 16), "r"(y >> 16));
+#endif
     } else {
         asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;\n\t"
             "add.cc.u32 %0, %0, %5;\n\taddc.u32 %1, %1, %6;\n\t"
