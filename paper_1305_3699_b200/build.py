@@ -62,7 +62,7 @@ def build(force: bool = False, jobs: int | None = None) -> str:
         src = os.path.join(CSRC, cu + ".cu")
         obj = os.path.join(OBJ, cu + ".o")
         objs.append(obj)
-        extra = [os.path.join(CSRC, "mr_wide.cu")] if cu == "mr_lanes" else []
+        extra = []
         if force or _stale(obj, [src] + deps + extra):
             steps.append(([NVCC] + NVFLAGS + ["-c", src, "-o", obj], obj + ".log"))
     for cpp in ("mr_host", "mr_keygen_host"):

@@ -1,7 +1,354 @@
-// mr_lanes.cu — small-batch path of the narrow channel counts (k <= 65): the wide-operand
-// channels-on-threads kernel (mr_wide.cu, the paper's own mapping "channels are directly mapped onto
-// threads", §3.1) compiled with ONE message per CTA, so a batch of a few hundred messages occupies
-// hundreds of CTAs instead of two or three 128-message tensor tiles.
-#define MR_WIDE_MB 1
-#define MR_WIDE_SYM(x) x##_lanes
-#include "mr_wide.cu"
+// mr_lanes.cu — small-batch ladder kernel for the narrow channel counts (k = 17, 33, 49, 65), DESIGN.md §4j.
+//
+// A batch of a few hundred messages fills two or three 128-message tensor tiles, i.e. two or three SMs, and
+// each tile then runs at the latency of one Montgomery multiplication chain (~3.3 µs per multiplication).
+// This kernel maps ONE message to a CTA and its RNS channels to threads — the paper's own mapping ("channels
+// are directly mapped onto threads", §3.1) — so a 256-message batch occupies 256 CTAs, and splits every
+// base-extension output over FOUR lanes (each lane sums every fourth input, two 96-bit shuffle adds combine
+// them), so the critical path of a multiplication is ~k/4 multiply-accumulates instead of k:
+//   channel products   thread per channel (2k+1 <= threads)
+//   BE1 (6.3-6.5)      output j in B' ∪ {m_r}: lanes 4j..4j+3 of the CTA, Σ_i ξ_i A1'[j][i]
+//   BE2 (6.6)          output i in B: lanes 4i..4i+3, Σ_j ξ'_j A2[i][j] + α' (m_i - |M'|_{m_i})
+// The constant matrices (8.7 KB at k = 33, 33 KB at k = 65) are staged once per CTA in shared memory, rows
+// per output so the four lanes of an output read interleaved words.  Arithmetic is the wide kernel's
+// (mr_wide.cu): word Montgomery reductions with the 2^-32 factors folded into the per-k wide table and the
+// per-context wide section (σ 2^64, A1' 2^32, A2 2^32, powers 2^32), plain B residues, B' in ξ-form, the same op
+// programs (sliding window, CRT entry) and the same exit (CRT with the extra modulus m_r = 2^32, then
+// conditional subtraction of N 2^s).  Results are bit-identical to every other path (tests/test_gpu_paths.py).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mr_internal.h"
+
+namespace mr {
+namespace {
+
+__device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) {
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32 %2, %2, 0;"
+        : "+r"(lo), "+r"(mid), "+r"(hi)
+        : "r"(x), "r"(y));
+}
+__device__ __forceinline__ void add96(u32 &lo, u32 &mi, u32 &hi, u32 l2, u32 m2, u32 h2) {
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+        : "+r"(lo), "+r"(mi), "+r"(hi)
+        : "r"(l2), "r"(m2), "r"(h2));
+}
+// T = thi 2^32 + tlo -> T 2^-32 mod m, lazy in [0, 2^32) (any odd m)
+__device__ __forceinline__ u32 mont_red(u32 tlo, u32 thi, u32 m, u32 minv) {
+    const u32 q = tlo * minv;
+    [[maybe_unused]] u32 ulo;
+    u32 uhi, cy;
+    asm("mad.lo.cc.u32 %0, %3, %4, %5;\n\tmadc.hi.cc.u32 %1, %3, %4, %6;\n\taddc.u32 %2, 0, 0;"
+        : "=r"(ulo), "=r"(uhi), "=r"(cy)
+        : "r"(q), "r"(m), "r"(tlo), "r"(thi));
+    return cy ? uhi - m : uhi;
+}
+__device__ __forceinline__ u32 addmod_lazy(u32 a, u32 b, u32 r32) {
+    const u64 s = (u64)a + b;
+    const u64 t = (u64)(u32)s + (s >> 32) * r32;
+    return (u32)t + (u32)(t >> 32) * r32;
+}
+__device__ __forceinline__ u32 red96_mont(u32 hi, u32 mid, u32 lo, u32 m, u32 minv, u32 r32) {
+    const u32 r = mont_red(lo, mid, m, minv);
+    const u32 t = hi * r32;
+    const u32 s = r + t;
+    return s < r ? s + r32 : s;
+}
+// 96-bit sum over the 4 lanes of an output group (lanes 4g .. 4g+3 of a warp)
+__device__ __forceinline__ void quad_sum(u32 &lo, u32 &mi, u32 &hi) {
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        const u32 l2 = __shfl_xor_sync(0xFFFFFFFFu, lo, o), m2 = __shfl_xor_sync(0xFFFFFFFFu, mi, o);
+        const u32 h2 = __shfl_xor_sync(0xFFFFFFFFu, hi, o);
+        add96(lo, mi, hi, l2, m2, h2);
+    }
+}
+
+template <int K>
+struct LaneCfg {
+    static constexpr int NCH = 2 * K + 1;
+    static constexpr int W = (K + 1 + 7) / 8;       // warps: 8 outputs of 4 lanes each
+    static constexpr int NT = 32 * W;
+    static constexpr int Q = (K + 3) / 4;           // inputs per lane (the last lanes may have one fewer)
+    static_assert(NT >= NCH, "one thread per channel");
+};
+
+// shared memory layout (words)
+template <int K>
+struct LaneSmem {
+    static constexpr u32 st = 0;                             // [2k+1] state
+    static constexpr u32 a1 = (2 * K + 1 + 3) & ~3;          // [k+1][k] BE1 rows: A1'[j][i] 2^32, row k: |M_i|_{2^32}
+    static constexpr u32 a2 = a1 + (K + 1) * K;              // [k][k] BE2 rows: A2[i][j] 2^32 (|M'_j|_{m_i})
+    static constexpr u32 mm = a2 + K * K;                    // [2k] m
+    static constexpr u32 minv = mm + 2 * K;                  // [2k] -m^-1
+    static constexpr u32 r32 = minv + 2 * K;                 // [2k] 2^32 mod m
+    static constexpr u32 sig = r32 + 2 * K;                  // [k]  σ_i 2^64
+    static constexpr u32 xw = sig + K;                       // [k]  |M^-1 λ_j^-1| 2^64
+    static constexpr u32 a2r = xw + K;                       // [k]  |M'_j|_{2^32}
+    static constexpr u32 pinw = a2r + K;                     // [k]  (m_i - |M'|_{m_i}) 2^32
+    static constexpr u32 red = pinw + K;                     // [W]  warp partials
+    static constexpr u32 aux = red + 16;                     // [4]  r_r, α', misc
+    static constexpr u32 xs = aux + 4;                       // [2k+2] staged input limbs / exit scratch
+    static constexpr u32 words = xs + 3 * (K + 1) + 4;       // exit: 3 words per column
+};
+
+template <int K>
+__global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpParams P, const u32 *__restrict__ tab,
+                                                                const u32 cxw) {
+    using C = LaneCfg<K>;
+    using S = LaneSmem<K>;
+    extern __shared__ __align__(16) u32 sm[];
+    constexpr int NCH = C::NCH;
+    const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u32 sel = blockIdx.x >= P.ctas0 ? 1u : 0u;
+    const u32 *cx = sel ? P.ctx[1] : P.ctx[0];
+    const u32 jl = blockIdx.x - sel * P.ctas0;               // message index in the context
+    const WideLayout L = wide_layout(K);
+    u32 *st = sm + S::st;
+    // ---- stage the constants (per context: A1' and σ from the wide section; per k: the rest)
+    const u32 *a1w = cx + cxw + wide_cx_a1(K), *sigw = cx + cxw + wide_cx_sig(K);
+    for (u32 e = tid; e < (u32)(K * K); e += C::NT) {
+        const u32 j = e / K, i = e % K;
+        sm[S::a1 + e] = __ldg(a1w + wch_at(i, j, K));         // row j (output), column i (input)
+        sm[S::a2 + e] = __ldg(tab + L.a2w + wch_at(i, j, K)); // row j here = output i of BE2, column = input
+    }
+    for (u32 i = tid; i < (u32)K; i += C::NT) {
+        sm[S::a1 + K * K + i] = __ldg(tab + L.a1r + i);
+        sm[S::sig + i] = __ldg(sigw + i);
+        sm[S::xw + i] = __ldg(tab + L.xw + i);
+        sm[S::a2r + i] = __ldg(tab + L.a2r + i);
+        sm[S::pinw + i] = __ldg(tab + L.pinw + i);
+    }
+    for (u32 c = tid; c < (u32)(2 * K); c += C::NT) {
+        sm[S::mm + c] = __ldg(tab + L.mm + c);
+        sm[S::minv + c] = __ldg(tab + L.minv + c);
+        sm[S::r32 + c] = __ldg(tab + L.r32 + c);
+    }
+    __shared__ bool ok_s;
+    if (tid == 0) {   // x < input bound (little-endian limbs, most significant first)
+        bool ok = false;
+        if (jl < P.count) {
+            const u32 *xr = P.x + (size_t)jl * P.in_limbs, *bnd = cx + cx_inb(K);
+            int res = 0;
+            for (int l = (int)P.in_limbs - 1; l >= 0 && res == 0; l--) res = xr[l] < bnd[l] ? -1 : (xr[l] > bnd[l] ? 1 : 0);
+            ok = res < 0;
+            if (sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
+        }
+        ok_s = ok;
+    }
+    __syncthreads();
+    const bool ok = ok_s;
+    const u32 minv32 = __ldg(tab + L.misc + 0), minvp = __ldg(tab + L.misc + 1), nminv = cx[CX_NMINV_R];
+    const u32 g = lane >> 2, sub = lane & 3, o = warp * 8 + g;   // this lane's output and quarter
+    const u32 *a1row = sm + S::a1 + o * K, *a2row = sm + S::a2 + o * K;
+
+    // st <- st · b · M^-1 (mod N); b at bp[ch * bstride] or the state itself (sq)
+    auto mont_mul = [&](const u32 *bp, size_t bstride, bool sq) {
+        // channel products: B: ξ_i = mont(mont(a b) σ_i 2^64); B': t*_j = mont(a* b*); m_r: a_r b_r
+        if (tid < (u32)(2 * K)) {
+            const u32 a = st[tid], b = sq ? a : __ldcg(bp + tid * bstride);
+            const u32 m = sm[S::mm + tid], mi = sm[S::minv + tid];
+            const u64 pr = (u64)a * b;
+            u32 t = mont_red((u32)pr, (u32)(pr >> 32), m, mi);
+            if (tid < (u32)K) {
+                const u64 ps = (u64)t * sm[S::sig + tid];
+                t = mont_red((u32)ps, (u32)(ps >> 32), m, mi);
+            }
+            st[tid] = t;
+        } else if (tid == (u32)(2 * K)) {
+            const u32 a = st[tid];
+            st[tid] = a * (sq ? a : __ldcg(bp + tid * bstride));
+        }
+        __syncthreads();
+        // BE1: output o (o < K: B' channel; o = K: the m_r column), lanes split the inputs i = sub + 4 t.
+        // The shuffles run on every lane (groups past the last output sum zeros), so they stay convergent.
+        u32 part = 0;
+        {
+            u32 lo = 0, mi = 0, hi = 0, qr = 0;
+            if (o < (u32)K) {
+#pragma unroll
+                for (int t = 0; t < C::Q; t++) {
+                    const u32 i = sub + 4 * t;
+                    if (4 * t + 3 < K || i < (u32)K) mac96(lo, mi, hi, st[i], a1row[i]);
+                }
+            } else if (o == (u32)K) {
+#pragma unroll
+                for (int t = 0; t < C::Q; t++) {
+                    const u32 i = sub + 4 * t;
+                    if (4 * t + 3 < K || i < (u32)K) qr += st[i] * a1row[i];
+                }
+            }
+            quad_sum(lo, mi, hi);
+            qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 1);
+            qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 2);
+            if (sub == 0 && o < (u32)K) {
+                const u32 ch = K + o, m = sm[S::mm + ch], mv = sm[S::minv + ch], r32 = sm[S::r32 + ch];
+                const u32 v = red96_mont(hi, mi, lo, m, mv, r32);          // Σ ξ A1'  (mod m'_j)
+                const u64 p = (u64)st[ch] * sm[S::xw + o];                 // t* C1 2^64
+                const u32 xp = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);
+                st[ch] = xp;                                               // ξ'_j (lazy)
+                part = xp * sm[S::a2r + o];                                // Σ ξ'_j |M'_j|_{2^32}
+            } else if (sub == 0 && o == (u32)K) {
+                sm[S::aux + 0] = st[2 * K] * minv32 + qr * nminv;          // r_r = (t_r + q̂_r N) M^-1
+            }
+        }
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, s);
+        if (lane == 0) sm[S::red + warp] = part;
+        __syncthreads();
+        // α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 mod 2^32 (exact: Shenoy-Kumaresan through m_r)
+        u32 sr = 0;
+#pragma unroll
+        for (int w = 0; w < C::W; w++) sr += sm[S::red + w];
+        const u32 rr = sm[S::aux + 0];
+        const u32 alpha = (sr - rr) * minvp;
+        // BE2: output o < K of B, lanes split the inputs j = sub + 4 t (convergent shuffles as above)
+        {
+            u32 lo = 0, mi = 0, hi = 0;
+            if (o < (u32)K) {
+                if (sub == 0) mac96(lo, mi, hi, alpha, sm[S::pinw + o]);
+#pragma unroll
+                for (int t = 0; t < C::Q; t++) {
+                    const u32 j = sub + 4 * t;
+                    if (4 * t + 3 < K || j < (u32)K) mac96(lo, mi, hi, st[K + j], a2row[j]);
+                }
+            }
+            quad_sum(lo, mi, hi);
+            if (sub == 0 && o < (u32)K) st[o] = red96_mont(hi, mi, lo, sm[S::mm + o], sm[S::minv + o], sm[S::r32 + o]);
+        }
+        if (tid == 0) st[2 * K] = rr;
+        __syncthreads();
+    };
+
+    const u64 *prog = sel ? P.prog[1] : P.prog[0];
+    const u32 nops = sel ? P.nops[1] : P.nops[0];
+    const size_t tstride = P.jobs_total, entry = (size_t)NCH * tstride;
+    const u32 slot0 = sel * P.ctas0 + jl;
+    u32 *xs = sm + S::xs;
+    for (u32 s = 0; s < nops; s++) {
+        const u64 op = __ldg(prog + s);
+        const u32 fl = (u32)op & 0xFF, opnd = (u32)(op >> 8) & 0xFF, ld = (u32)(op >> 16) & 0xFF;
+        const u32 ad = (u32)(op >> 24) & 0xFF, sto = (u32)(op >> 32) & 0xFF;
+        if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) {   // positional -> RNS (a2)
+            const u32 off = (fl & OPF_TORNS_HI) ? P.half : 0u;
+            const u32 nl = (fl & OPF_TORNS_ALL) ? P.in_limbs : P.half;
+            for (u32 l = tid; l < nl; l += C::NT) xs[l] = ok ? P.x[(size_t)jl * P.in_limbs + off + l] : 0u;
+            __syncthreads();
+            if (tid < (u32)(2 * K)) {   // channel c = Σ_l x_l |2^(32 l) 2^32|_{m_c}, one Montgomery fold
+                u32 lo = 0, mi = 0, hi = 0;
+                for (u32 l = 0; l < nl; l++) mac96(lo, mi, hi, xs[l], __ldg(tab + L.pow + wch_at(l, tid, 2 * K)));
+                st[tid] = red96_mont(hi, mi, lo, sm[S::mm + tid], sm[S::minv + tid], sm[S::r32 + tid]);
+            } else if (tid == (u32)(2 * K)) {
+                st[tid] = xs[0];
+            }
+            __syncthreads();
+        }
+        if (fl & OPF_LOAD) {
+            if (tid < (u32)NCH)
+                st[tid] = ld >= 0xF0 ? cx[cx_r2(K) + (ld - 0xF0) * NCH + tid] : P.table[ld * entry + tid * tstride + slot0];
+            __syncthreads();
+        }
+        if (!(fl & OPF_NOMUL)) {
+            if (opnd == OPND_SQ) mont_mul(nullptr, 0, true);
+            else if (opnd >= 0xF0) mont_mul(cx + cx_r2(K) + (opnd - 0xF0) * NCH, 1, false);
+            else mont_mul(P.table + opnd * entry + slot0, tstride, false);
+        }
+        if (fl & OPF_ADD) {   // channel-wise lazy modular addition (CRT entry)
+            if (tid < (u32)NCH) {
+                const u32 b = P.table[ad * entry + tid * tstride + slot0];
+                st[tid] = tid < (u32)(2 * K) ? addmod_lazy(st[tid], b, sm[S::r32 + tid]) : st[tid] + b;
+            }
+            __syncthreads();
+        }
+        if (fl & OPF_STORE) {
+            if (tid < (u32)NCH) P.table[sto * entry + tid * tstride + slot0] = st[tid];
+            __syncthreads();
+        }
+    }
+
+    // ---- exit (a7): X = Σ_j ξ'_j M'_j + α'(2^(32(k+1)) - M') (column sums), then X mod N
+    {
+        u32 part = 0;
+        if (tid < (u32)K) part = st[K + tid] * sm[S::a2r + tid];
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, s);
+        if (lane == 0) sm[S::red + warp] = part;
+        __syncthreads();
+        u32 sr = 0;
+#pragma unroll
+        for (int w = 0; w < C::W; w++) sr += sm[S::red + w];
+        const u32 alpha = (sr - st[2 * K]) * minvp;
+        if (tid <= (u32)K) {   // column l = tid
+            const u32 l = tid;
+            u32 lo = 0, mi = 0, hi = 0;
+            mac96(lo, mi, hi, alpha, __ldg(tab + L.nmp + l));
+            for (u32 j = 0; j < (u32)K; j++) mac96(lo, mi, hi, st[K + j], __ldg(tab + L.mpl + wch_at(j, l, K + 1)));
+            xs[3 * l] = lo;
+            xs[3 * l + 1] = mi;
+            xs[3 * l + 2] = hi;
+        }
+        __syncthreads();
+        if (tid == 0) {   // carries, then conditional subtraction of N 2^s, s = smax .. 0
+            u32 *X = st;   // the state is no longer needed: X limbs [0, k]
+            u64 carry = 0;
+            for (u32 l = 0; l <= (u32)K; l++) {
+                const u64 s2 = (u64)xs[3 * l] + (u32)carry;
+                X[l] = (u32)s2;
+                carry = (carry >> 32) + xs[3 * l + 1] + ((u64)xs[3 * l + 2] << 32) + (s2 >> 32);
+            }
+            const u32 *nl = cx + cx_n(K);
+            const int smax = (int)(32 - __clz(K + 2)) - 1;   // X < (k+3) N <= 2^(smax+1) N
+            for (int s = smax; s >= 0; s--) {
+                for (int pass = 0; pass < 2; pass++) {
+                    u32 br = 0;
+                    for (u32 l = 0; l <= (u32)K; l++) {
+                        const u32 nlo = l ? nl[l - 1] : 0u, nhi = l < (u32)K ? nl[l] : 0u;
+                        const u32 nsh = s ? __funnelshift_l(nlo, nhi, s) : nhi;
+                        const u64 t = (u64)X[l] - nsh - br;
+                        if (pass) X[l] = (u32)t;
+                        br = (u32)(t >> 63);
+                    }
+                    if (br) break;
+                }
+            }
+        }
+        __syncthreads();
+        if (jl < P.count) {
+            u32 *y = P.y + sel * P.out_stride + (size_t)jl * P.out_limbs;
+            for (u32 l = tid; l < P.out_limbs; l += C::NT) y[l] = ok ? st[l] : 0u;
+        }
+    }
+}
+
+template <int K>
+int launch_k(const ModexpParams &p, u32 ctas, const u32 *tab, u32 cxw, void *stream) {
+    const size_t smem = 4 * (size_t)LaneSmem<K>::words;
+    if (cudaFuncSetAttribute((const void *)k_modexp_lane<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return 6;
+    void *args[] = {const_cast<ModexpParams *>(&p), const_cast<u32 **>(&tab), &cxw};
+    return cudaLaunchKernel((const void *)k_modexp_lane<K>, dim3(ctas), dim3(LaneCfg<K>::NT), args, smem,
+                            (cudaStream_t)stream) == cudaSuccess
+               ? 0
+               : 6;
+}
+
+}  // namespace
+
+int wide_messages_per_cta_lanes() { return 1; }
+
+// one CTA per message and context; k in {17, 33, 49, 65} (host: small_ok)
+int launch_modexp_wide_lanes(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream) {
+    switch (k) {
+        case 17: return launch_k<17>(p, ctas, d_wide_tab, cxw, stream);
+        case 33: return launch_k<33>(p, ctas, d_wide_tab, cxw, stream);
+        case 49: return launch_k<49>(p, ctas, d_wide_tab, cxw, stream);
+        case 65: return launch_k<65>(p, ctas, d_wide_tab, cxw, stream);
+        default: return 6;
+    }
+}
+
+}  // namespace mr

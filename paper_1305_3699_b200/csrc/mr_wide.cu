@@ -24,17 +24,7 @@
 namespace mr {
 namespace {
 
-// MR_WIDE_MB: messages per CTA (register-blocked).  This file is compiled twice: as itself (MB = 16, the
-// wide-operand kernels of k >= 97) and from mr_lanes.cu with MB = 1 (the small-batch path of k <= 65:
-// one message per CTA, channels on lanes); MR_WIDE_SYM renames the exported entry points.
-#ifndef MR_WIDE_MB
-#define MR_WIDE_MB 16
-#define MR_WIDE_SYM(x) x
-#endif
-constexpr int MB = MR_WIDE_MB;
-// independent accumulator sets per message in the contractions: with few messages per CTA the 96-bit
-// carry chains of one output would serialise, so rows are dealt round-robin to NA chains and summed at the end
-constexpr int NA = MB >= 4 ? 1 : 4 / MB;
+constexpr int MB = 16;                 // messages per CTA (register-blocked)
 constexpr int NTMAX = 512;             // threads per CTA (runtime: 32 * ceil((k+1)/32), <= 512)
 
 __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) {
@@ -83,54 +73,9 @@ __device__ __forceinline__ u32 &ST(u32 *st, u32 ch, u32 msg) { return st[ch * MB
 // chunked [R][ncols] matrix (mr_internal.h wch_at, R >= n): the thread's 8 coefficients of a row group are
 // two 16-byte loads, issued one group ahead so their L2 latency overlaps the previous group's 128
 // multiply-accumulates.  Rows i >= n of the last group are skipped (the xs rows there may be anything).
-__device__ __forceinline__ void add96(u32 &lo, u32 &mi, u32 &hi, u32 l2, u32 m2, u32 h2) {
-    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
-        : "+r"(lo), "+r"(mi), "+r"(hi)
-        : "r"(l2), "r"(m2), "r"(h2));
-}
-
-// small MB (< 4 messages per CTA): the same contraction with NA independent accumulator chains per message
-__device__ __forceinline__ void dot_small(const u32 *__restrict__ mat, u32 ncols, u32 j, const u32 *xs, u32 n,
-                                          u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
-    const uint4 *cp = reinterpret_cast<const uint4 *>(mat + (size_t)j * 8);
-    const u32 gs = 2 * ncols, ng = (n + 7) / 8;
-    u32 al[NA][MB], am[NA][MB], ah[NA][MB];
-#pragma unroll
-    for (int a = 0; a < NA; a++)
-#pragma unroll
-        for (int q = 0; q < MB; q++) al[a][q] = am[a][q] = ah[a][q] = 0;
-    uint4 c0 = __ldg(cp), c1 = __ldg(cp + 1);
-#pragma unroll 1
-    for (u32 g = 0; g < ng; g++) {
-        uint4 n0 = c0, n1 = c1;
-        if (g + 1 < ng) {
-            n0 = __ldg(cp + (size_t)(g + 1) * gs);
-            n1 = __ldg(cp + (size_t)(g + 1) * gs + 1);
-        }
-        const u32 c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-        const u32 rows = g + 1 < ng ? 8u : n - g * 8;
-        const u32 *xg = xs + g * 8 * MB;
-#pragma unroll
-        for (int p = 0; p < 8; p++)
-            if ((u32)p < rows)
-#pragma unroll
-                for (int q = 0; q < MB; q++) mac96(al[p % NA][q], am[p % NA][q], ah[p % NA][q], xg[p * MB + q], c[p]);
-        c0 = n0;
-        c1 = n1;
-    }
-#pragma unroll
-    for (int q = 0; q < MB; q++)
-#pragma unroll
-        for (int a = 0; a < NA; a++) add96(lo[q], mi[q], hi[q], al[a][q], am[a][q], ah[a][q]);
-}
-
 template <bool PP>
 __device__ __forceinline__ void dot_mb(const u32 *__restrict__ mat, u32 ncols, u32 j, const u32 *xs, u32 n,
                                        u32 (&lo)[MB], u32 (&mi)[MB], u32 (&hi)[MB]) {
-    if constexpr (MB < 4) {
-        dot_small(mat, ncols, j, xs, n, lo, mi, hi);
-        return;
-    }
     const uint4 *cp = reinterpret_cast<const uint4 *>(mat + (size_t)j * 8);
     const u32 gs = 2 * ncols;                         // uint4 per row group
     const u32 ng = (n + 7) / 8;
@@ -142,7 +87,7 @@ __device__ __forceinline__ void dot_mb(const u32 *__restrict__ mat, u32 ncols, u
             if ((u32)p < rows) {
                 const uint4 *x = reinterpret_cast<const uint4 *>(xg + p * MB);
 #pragma unroll
-                for (int v4 = 0; v4 < (MB >= 4 ? MB / 4 : 0); v4++) {
+                for (int v4 = 0; v4 < MB / 4; v4++) {
                     const uint4 xv = x[v4];
                     mac96(lo[4 * v4 + 0], mi[4 * v4 + 0], hi[4 * v4 + 0], xv.x, c[p]);
                     mac96(lo[4 * v4 + 1], mi[4 * v4 + 1], hi[4 * v4 + 1], xv.y, c[p]);
@@ -547,13 +492,12 @@ __global__ void __launch_bounds__(NTB, MINB) k_modexp_wide(const ModexpParams P,
 
 }  // namespace
 
-size_t MR_WIDE_SYM(wide_smem_bytes)(u32 k) {
+size_t wide_smem_bytes(u32 k) {
     return 4 * ((size_t)(2 * k + 1) * MB + (size_t)k * MB + 16 * MB + 4 * MB);
 }
-int MR_WIDE_SYM(wide_messages_per_cta)() { return MB; }
+int wide_messages_per_cta() { return MB; }
 
-int MR_WIDE_SYM(launch_modexp_wide)(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw,
-                                    void *stream) {
+int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream) {
     WideArgs W{d_wide_tab, k, 0, cxw};
     // threads: one per base-extension output (k + 1 with the m_r column), rounded to whole warps — except
     // when k + 1 overshoots a multiple of 32 by at most 4 (k = 257: 258 -> 256 threads, the two extra
@@ -561,22 +505,16 @@ int MR_WIDE_SYM(launch_modexp_wide)(const ModexpParams &p, u32 ctas, const u32 *
     const u32 up = 32 * ((k + 1 + 31) / 32), down = 32 * ((k + 1) / 32);
     const u32 nt32 = (k + 1) - down <= 4 && down >= 64 ? down : up, nt = nt32 < (u32)NTMAX ? nt32 : (u32)NTMAX;
     W.nt = nt;
-    const size_t smem = MR_WIDE_SYM(wide_smem_bytes)(k);
+    const size_t smem = wide_smem_bytes(k);
     // ping-pong coefficient groups: A/B +8 % at k = 257, +5 % at 505, -13 % at 129 (tools/ab_w.sh)
     static const u32 pp_min = [] { const char *e = getenv("MR_WIDE_PP_MIN"); return e ? (u32)atoi(e) : 257u; }();
     const bool pp = k >= pp_min;
     // k = 97 (96 threads): a 168-register budget (no accumulator-pair shuffling) beats the 128-register
     // one by 5-8 %; at k = 129 (128 threads) the 4th resident CTA is worth more (tools/ab_k129.py)
-#if MR_WIDE_MB >= 4
     const void *kern = nt > 256 ? (const void *)k_modexp_wide<NTMAX, 1, false, true>
                        : pp     ? (const void *)k_modexp_wide<256, 2, true, true>
                        : nt <= 96 ? (const void *)k_modexp_wide<128, 3, true, false>
                                 : (const void *)k_modexp_wide<256, 2, true, false>;
-#else   // small-batch build (k <= 65: at most 96 threads): many small CTAs per SM
-    (void)pp;
-    if (nt > 128) return 6;
-    const void *kern = (const void *)k_modexp_wide<128, 4, true, false>;
-#endif
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 6;
     void *args[] = {const_cast<ModexpParams *>(&p), &W};
     return cudaLaunchKernel(kern, dim3(ctas), dim3(nt), args, smem, (cudaStream_t)stream) == cudaSuccess ? 0 : 6;
@@ -696,7 +634,7 @@ __global__ void k_combine_wide(const CombineParams P, const u32 *qinv, u32 *scr,
 
 }  // namespace
 
-int MR_WIDE_SYM(launch_combine_wide)(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream) {
+int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream) {
     const u32 nt = 128;
     void *args[] = {const_cast<CombineParams *>(&p), const_cast<u32 **>(&d_qinv), &d_scratch, &k};
     return cudaLaunchKernel((const void *)k_combine_wide, dim3((p.count + nt - 1) / nt), dim3(nt), args, 0,
