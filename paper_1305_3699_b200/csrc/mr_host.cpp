@@ -412,7 +412,7 @@ static bool wide_path(int k) {
 static bool small_ok(int k) { return k >= 17 && k <= 65; }
 static long g_small_override = -1;   // mr_internal_set_small_max (tests: both paths at the same batch size)
 static size_t small_max() {
-    static const size_t v = [] { const char *e = getenv("MR_RNS_SMALL_MAX"); return e ? (size_t)atol(e) : (size_t)2048; }();
+    static const size_t v = [] { const char *e = getenv("MR_RNS_SMALL_MAX"); return e ? (size_t)atol(e) : (size_t)1024; }();
     return g_small_override >= 0 ? (size_t)g_small_override : v;
 }
 

@@ -163,17 +163,21 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             st[tid] = a * (sq ? a : __ldcg(bp + tid * bstride));
         }
         __syncthreads();
-        // BE1: output o (o < K: B' channel; o = K: the m_r column), lanes split the inputs i = sub + 4 t.
-        // The shuffles run on every lane (groups past the last output sum zeros), so they stay convergent.
-        u32 part = 0;
+        // BE1: output o (o < K: B' channel; o = K: the m_r column), lanes split the inputs i = sub + 4 t over two
+        // accumulator chains.  The shuffles run on every lane (groups past the last output sum zeros), so they
+        // stay convergent.
         {
-            u32 lo = 0, mi = 0, hi = 0, qr = 0;
+            u32 lo = 0, mi = 0, hi = 0, l1 = 0, m1 = 0, h1 = 0, qr = 0;
             if (o < (u32)K) {
 #pragma unroll
                 for (int t = 0; t < C::Q; t++) {
                     const u32 i = sub + 4 * t;
-                    if (4 * t + 3 < K || i < (u32)K) mac96(lo, mi, hi, st[i], a1row[i]);
+                    if (4 * t + 3 < K || i < (u32)K) {
+                        if (t & 1) mac96(l1, m1, h1, st[i], a1row[i]);
+                        else mac96(lo, mi, hi, st[i], a1row[i]);
+                    }
                 }
+                add96(lo, mi, hi, l1, m1, h1);
             } else if (o == (u32)K) {
 #pragma unroll
                 for (int t = 0; t < C::Q; t++) {
@@ -188,36 +192,40 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                 const u32 ch = K + o, m = sm[S::mm + ch], mv = sm[S::minv + ch], r32 = sm[S::r32 + ch];
                 const u32 v = red96_mont(hi, mi, lo, m, mv, r32);          // Σ ξ A1'  (mod m'_j)
                 const u64 p = (u64)st[ch] * sm[S::xw + o];                 // t* C1 2^64
-                const u32 xp = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);
-                st[ch] = xp;                                               // ξ'_j (lazy)
-                part = xp * sm[S::a2r + o];                                // Σ ξ'_j |M'_j|_{2^32}
+                st[ch] = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);   // ξ'_j (lazy)
             } else if (sub == 0 && o == (u32)K) {
                 sm[S::aux + 0] = st[2 * K] * minv32 + qr * nminv;          // r_r = (t_r + q̂_r N) M^-1
             }
         }
-#pragma unroll
-        for (int s = 16; s > 0; s >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, s);
-        if (lane == 0) sm[S::red + warp] = part;
         __syncthreads();
-        // α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 mod 2^32 (exact: Shenoy-Kumaresan through m_r)
-        u32 sr = 0;
-#pragma unroll
-        for (int w = 0; w < C::W; w++) sr += sm[S::red + w];
+        // BE2: output o < K of B, lanes split the inputs j = sub + 4 t.  Every group also sums its share of
+        // Σ_j ξ'_j |M'_j|_{2^32} over the same j, so each group forms α' = (that sum - r_r) M'^-1 mod 2^32
+        // (exact: Shenoy-Kumaresan through m_r) itself — no block reduction and no extra barrier — and adds
+        // α' (m_i - |M'|_{m_i}) after the contraction.
         const u32 rr = sm[S::aux + 0];
-        const u32 alpha = (sr - rr) * minvp;
-        // BE2: output o < K of B, lanes split the inputs j = sub + 4 t (convergent shuffles as above)
         {
-            u32 lo = 0, mi = 0, hi = 0;
+            u32 lo = 0, mi = 0, hi = 0, l1 = 0, m1 = 0, h1 = 0, sa = 0;
             if (o < (u32)K) {
-                if (sub == 0) mac96(lo, mi, hi, alpha, sm[S::pinw + o]);
 #pragma unroll
                 for (int t = 0; t < C::Q; t++) {
                     const u32 j = sub + 4 * t;
-                    if (4 * t + 3 < K || j < (u32)K) mac96(lo, mi, hi, st[K + j], a2row[j]);
+                    if (4 * t + 3 < K || j < (u32)K) {
+                        const u32 x = st[K + j];
+                        if (t & 1) mac96(l1, m1, h1, x, a2row[j]);
+                        else mac96(lo, mi, hi, x, a2row[j]);
+                        sa += x * sm[S::a2r + j];
+                    }
                 }
+                add96(lo, mi, hi, l1, m1, h1);
             }
             quad_sum(lo, mi, hi);
-            if (sub == 0 && o < (u32)K) st[o] = red96_mont(hi, mi, lo, sm[S::mm + o], sm[S::minv + o], sm[S::r32 + o]);
+            sa += __shfl_xor_sync(0xFFFFFFFFu, sa, 1);
+            sa += __shfl_xor_sync(0xFFFFFFFFu, sa, 2);
+            if (sub == 0 && o < (u32)K) {
+                const u32 alpha = (sa - rr) * minvp;
+                mac96(lo, mi, hi, alpha, sm[S::pinw + o]);
+                st[o] = red96_mont(hi, mi, lo, sm[S::mm + o], sm[S::minv + o], sm[S::r32 + o]);
+            }
         }
         if (tid == 0) st[2 * K] = rr;
         __syncthreads();
