@@ -580,7 +580,12 @@ def run_rank(args, world, rank, dev, wl: Workload, step):
         lib.mr_internal_timing(0)
         ms_l, n_l, ms_c, n_c = ctypes.c_double(), ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
         lib.mr_internal_timing_collect(ctypes.byref(ms_l), ctypes.byref(n_l), ctypes.byref(ms_c), ctypes.byref(n_c))
-        launch = (ms_l.value, n_l.value, ms_c.value, n_c.value)
+        ms_m, n_m = ctypes.c_double(), ctypes.c_int()
+        lib.mr_internal_timing_mr(ctypes.byref(ms_m), ctypes.byref(n_m))
+        if n_m.value:   # Miller-Rabin: each timed call is k_mr_setup + k_mr_rounds_tc (the ladder-kind slot)
+            launch = (ms_m.value, n_m.value, 0.0, n_m.value)
+        else:
+            launch = (ms_l.value, n_l.value, ms_c.value, n_c.value)
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     total_ms_max = max_over_ranks(total_ms, world, dev.dev if not dev.dry else None)
     value = units_of(wl, total) * args.steps / (total_ms_max / 1e3)
@@ -736,7 +741,7 @@ def roofline(wl: Workload, n_loc: int, launch, clocks, world, step_ms: float):
     is that pipe's achieved / peak.  The all-work IMAD-eq rate over the IMAD peak (what an IMAD-only
     implementation could reach at most) is reported separately as imad_eq_speedup."""
     ms_l, n_l, ms_c, n_c = launch
-    # ladder launches are timed by the library hook; Miller-Rabin (not instrumented) takes the step's event time
+    # ladder (or Miller-Rabin) launches are timed by the library hook on their own stream
     ladder_ms = ms_l / n_l if n_l else step_ms
     t_ops, e_ops, all_ops = wl.work()
     units = units_of(wl, n_loc)
@@ -754,7 +759,7 @@ def roofline(wl: Workload, n_loc: int, launch, clocks, world, step_ms: float):
     return {"bound": bound, "achieved": ach, "peak": pk, "unit": unit, "frac": fr,
             "traffic": None if rec is None else rec["dram_bytes_read"] + rec["dram_bytes_write"],
             "kernel": kernel_name(wl), "ladder_ms_per_launch": ladder_ms,
-            "combine_ms_per_launch": ms_c / max(1, n_c) if n_c else None,
+            "combine_ms_per_launch": ms_c / max(1, n_c) if n_c and ms_c else None,
             "peak_source": tsrc if bound == "tensor" else
             "64 IMAD-eq/clk/SM x 148 SM x sm_max_mhz (profiles/r2_peaks_int.json: IMAD 64/clk/SM, IMAD.WIDE 32)",
             "tensor_i8": {"achieved_tops": t_ach / 1e12, "peak_tops": tpk / 1e12, "frac": t_ach / tpk,
@@ -766,6 +771,15 @@ def roofline(wl: Workload, n_loc: int, launch, clocks, world, step_ms: float):
             "imad_eq_speedup_note": "all algorithmic word products as IMAD-eq / the INT32 IMAD peak: >1 means faster "
                                     "than any IMAD-only implementation could be (SURVEY §8(d) 'percent of IMAD peak')",
             "imad_eq_per_unit": all_ops}
+
+
+def base_extension(wl):
+    """which kernel family runs the workload's base extensions (the library routes by k: k <= 65 tensor
+    path unless MR_RNS_IMAD_ONLY=1; k >= 97 the wide kernels)"""
+    k = getattr(wl, "k", None) or 33
+    if k >= 97:
+        return "imad (k_modexp_wide, channels on threads)"
+    return "imad" if os.environ.get("MR_RNS_IMAD_ONLY", "0") == "1" else "tcgen05-i8"
 
 
 def kernel_name(wl):
@@ -781,7 +795,7 @@ def kernel_name(wl):
 def workload_config(args, wl, total, world):
     cfg = {"workload": wl.describe, "units_total": total, "units_per_gpu": -(-total // world),
            "unit": wl.unit.replace("/s", ""),
-           "base_extension": "imad" if os.environ.get("MR_RNS_IMAD_ONLY", "0") == "1" else "tcgen05-i8",
+           "base_extension": base_extension(wl),
            "inputs": "SplitMix64 by global index + edge values (synth/); identical for any GPU count",
            "l2": "flushed between timed steps (256 MiB write)"}
     if isinstance(wl, CrtDecrypt) or isinstance(wl, Encrypt):
