@@ -27,7 +27,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xpt
 
 
 def _deps() -> list[str]:
-    return [os.path.join(CSRC, f) for f in ("mr_kernels.cuh", "mr_internal.h")] + [
+    return [os.path.join(CSRC, f) for f in ("mr_kernels.cuh", "mr_tcw.cuh", "mr_internal.h")] + [
         os.path.join(ROOT, "include", "mr_rns.h")]
 
 
@@ -81,7 +81,8 @@ def build(force: bool = False, jobs: int | None = None) -> str:
                 f.result()
     if force or steps or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl"],
+        _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl",
+                                                         "-Xlinker", "--no-undefined"],
              os.path.join(OBJ, "link.log"))
         shutil.move(tmp, LIB)
     return LIB

@@ -354,6 +354,7 @@ struct DevBase {
     u32 *d_tcb1u = nullptr;    // tensor-core unmerged BE1 image (Miller-Rabin, per-thread modulus)
     u32 *d_one = nullptr;      // RNS image of 1 (2k+1 words; Miller-Rabin tensor path multiplicand)
     u32 *d_wide = nullptr;     // wide-operand table (wide_path(k), mr_internal.h wide_layout)
+    void *d_tcw = nullptr;     // tensor-core wide images (k = 97, 129: mr_internal.h tcw_*)
 };
 
 // per-k table of the wide kernel (mr_internal.h WideLayout): word-Montgomery constants with their 2^32
@@ -416,6 +417,8 @@ static size_t small_max() {
     return g_small_override >= 0 ? (size_t)g_small_override : v;
 }
 
+static std::vector<uint8_t> build_tcw_images(const Base &b);
+
 static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **d_be) {
     auto key = std::make_pair(device, k);
     auto it = g_devbases.find(key);
@@ -439,6 +442,11 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
         const std::vector<u32> t = build_wide_table(b);
         if (cudaMalloc(&db.d_wide, t.size() * 4) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_wide, t.data(), t.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
+    }
+    if (wide_path(k) && tcw_k((u32)k)) {
+        const std::vector<uint8_t> im = build_tcw_images(b);
+        if (cudaMalloc(&db.d_tcw, im.size()) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMemcpy(db.d_tcw, im.data(), im.size(), cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
     }
     if (is_wide((u32)k)) {   // no per-k kernel set
         g_devbases[key] = db;
@@ -533,6 +541,8 @@ struct mr_rns_ctx {
     const u32 *d_mpl = nullptr;
     const u32 *d_wide = nullptr;   // wide-operand table of this k (wide_path(k) or small_ok(k))
     u32 cxw = 0;                   // word offset of the wide section in the context block (0: none)
+    u32 be1w = 0;                  // word offset of the tensor-core wide BE1 image (k = 97 / 129; 0: none)
+    const void *d_tcw = nullptr;   // per-k tensor-core wide images (BE2 | TRN | EXT)
     std::vector<u32> h_cx;
     std::mutex mu;             // guards the program cache
     std::map<std::pair<Big, bool>, DevProg> progs;  // (exponent, crt) -> uploaded program (<= kProgCache)
@@ -696,6 +706,81 @@ static void fill_wide_ctx(const Base &b, u32 *x, u32 cxw) {
     }
 }
 
+// ------------------------------------------------------------------ tensor-core wide kernel images (§4k)
+namespace mr {
+// Byte-split image of a modular contraction (mr_internal.h tcw_*): row (output o, byte b), K byte (input word i,
+// byte a) holds byte b of C(i, a, o) = 2^(8a) A(i, o) mod m_o, so Σ_b 2^(8b) D[(o, b)] ≡ Σ_i x_i A(i, o) (mod m_o).
+// `coef(i, o)` returns A(i, o) already reduced (< m_o), `mod(o)` m_o (0 = 2^32: the m_r column), `nin` inputs.
+template <class Coef, class Mod>
+static void fill_tcw_modular(int k, u32 e, int nin, Coef &&coef, Mod &&modo, uint8_t *img) {
+    memset(img, 0, tcw_img_bytes(k, e));
+    const u32 nout = tcw_nout(k, e), oc = tcw_oc(k, e);
+    for (u32 o = 0; o < nout; o++) {
+        const u32 c = o / oc, rl = 4 * (o - c * oc);
+        const u64 m = modo(o);
+        for (int i = 0; i < nin; i++) {
+            const u64 A = coef(i, o);
+            for (u32 a = 0; a < 4; a++) {
+                const u32 v = m ? (u32)((A << (8 * a)) % m) : (u32)(A << (8 * a));
+                for (u32 b = 0; b < 4; b++) img[tcw_at(k, e, c, rl + b, 4 * i + a)] = (uint8_t)(v >> (8 * b));
+            }
+        }
+    }
+}
+static u32 r32_of(u32 m) { return (u32)((1ull << 32) % m); }
+// per-context BE1: A(i, j) = A1'_ij 2^64 mod m'_j (6.4 merged, the epilogue's two Montgomery folds), and the m_r
+// column A(i, k) = |M_i|_{2^32}
+static void fill_tcw_be1(const Base &b, const u32 *cx, uint8_t *img) {
+    const int k = b.k;
+    const u32 *A1 = b.flat.data() + base_layout(k).A1, *A1r = b.flat.data() + base_layout(k).A1r;
+    fill_tcw_modular(k, TCW_BE1, k,
+        [&](int i, u32 j) -> u64 {
+            if ((int)j == k) return A1r[i];
+            const u32 m = b.Bp[j], r = r32_of(m);
+            return mulm(mulm(mulm(A1[i * k + j], cx[cx_c2(k) + j], m), r, m), r, m);
+        },
+        [&](u32 j) -> u64 { return (int)j == k ? 0 : b.Bp[j]; }, img);
+}
+// per-k BE2 (A2_ji 2^32, α' column (m_i - |M'|_{m_i}) 2^32 at input word k), TRN (|2^(32l)|_{m_c} 2^32, B' × λ_j),
+// EXT (byte convolution with M'_j and 2^(32(k+1)) - M')
+static std::vector<uint8_t> build_tcw_images(const Base &b) {
+    const int k = b.k;
+    const BaseLayout L = base_layout(k);
+    const u32 *f = b.flat.data();
+    std::vector<uint8_t> img(tcw_kimg_bytes(k), 0);
+    fill_tcw_modular(k, TCW_BE2, k + 1,
+        [&](int j, u32 i) -> u64 {
+            const u32 m = b.B[i], r = r32_of(m);
+            return j < k ? mulm(f[L.A2 + j * k + i], r, m) : mulm(f[L.pin + i], r, m);
+        },
+        [&](u32 i) -> u64 { return b.B[i]; }, img.data() + tcw_img_off(k, TCW_BE2));
+    fill_tcw_modular(k, TCW_TRN, k,
+        [&](int l, u32 c) -> u64 {
+            const u32 m = (int)c < k ? b.B[c] : b.Bp[c - k];
+            return mulm(b.pow[(size_t)l * 2 * k + c], r32_of(m), m);
+        },
+        [&](u32 c) -> u64 { return (int)c < k ? b.B[c] : b.Bp[c - k]; }, img.data() + tcw_img_off(k, TCW_TRN));
+    {   // EXT: row p = byte position of X (4 per limb), K byte (j, a): byte p - a of M'_j (j < k) or of 2^(32(k+1)) - M'
+        uint8_t *x = img.data() + tcw_img_off(k, TCW_EXT);
+        const u32 oc = tcw_oc(k, TCW_EXT);
+        auto byte_of = [&](int j, int q) -> uint8_t {   // byte q of M'_j (j < k) / of NMp (j = k)
+            if (q < 0 || q >= 4 * (k + 1)) return 0;
+            const u32 w = j < k ? f[L.MpL + j * (k + 1) + q / 4] : f[L.NMp + q / 4];
+            return (uint8_t)(w >> (8 * (q % 4)));
+        };
+        for (u32 l = 0; l <= (u32)k; l++) {
+            const u32 c = l / oc, rl = 4 * (l - c * oc);
+            for (u32 bb = 0; bb < 4; bb++) {
+                const int p = 4 * (int)l + (int)bb;
+                for (int j = 0; j <= k; j++)
+                    for (int a = 0; a < 4; a++) x[tcw_at(k, TCW_EXT, c, rl + bb, 4 * j + a)] = byte_of(j, p - a);
+            }
+        }
+    }
+    return img;
+}
+}  // namespace mr
+
 static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, int device, const Big &in_bound,
                      size_t in_limbs, const Big *khi_shift_limbs_half /* CRT: half limbs */, const Big *qinv) {
     *out = nullptr;
@@ -731,11 +816,16 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
     c->N = N;
     const size_t tc_words = tc_ok(k) ? tc_bbytes(k) / 4 : 0;
     int rc = MR_OK;
-    if (wide_path(k)) {   // cx block + wide section (σ 2^64, A1' 2^32 row-major)
-        c->h_cx.assign(cx_words(k) + wide_cx_words(k), 0);
+    if (wide_path(k)) {   // cx block + wide section (σ 2^64, A1' 2^32 row-major) [+ tensor BE1 image, k = 97 / 129]
+        const size_t tcw = tcw_k((u32)k) ? tcw_cx_words((u32)k) : 0;
+        c->h_cx.assign(cx_words(k) + wide_cx_words(k) + tcw, 0);
         fill_ctx_block(b, N, limbs, in_bound, in_limbs, khi_shift_limbs_half, qinv, c->h_cx.data());
         c->cxw = cx_words(k);
         fill_wide_ctx(b, c->h_cx.data(), c->cxw);
+        if (tcw) {
+            c->be1w = cx_words(k) + wide_cx_words(k);
+            fill_tcw_be1(b, c->h_cx.data(), reinterpret_cast<uint8_t *>(c->h_cx.data() + c->be1w));
+        }
     } else {   // narrow layout; small-batch k append the wide section after the tensor images
         const size_t narrow = cx_words(k) + be_half_words(k) + 2 * tc_words;
         c->h_cx.assign(narrow + (small_ok(k) ? wide_cx_words(k) : 0), 0);
@@ -752,6 +842,7 @@ static int build_ctx(mr_rns_ctx **out, const Big &N, size_t limbs, int k_req, in
         c->d_tcb2 = g_devbases[std::make_pair(device, k)].d_tcb2;
         c->d_mpl = g_devbases[std::make_pair(device, k)].d_mpl;
         c->d_wide = g_devbases[std::make_pair(device, k)].d_wide;
+        c->d_tcw = g_devbases[std::make_pair(device, k)].d_tcw;
     }
     if (rc != MR_OK) { delete c; return rc; }
     if (cudaSetDevice(device) != cudaSuccess) { delete c; return MR_ERR_CUDA; }
@@ -996,12 +1087,71 @@ static bool tensor_path_enabled() {
     return !(e && e[0] == '1');
 }
 
+// tensor-core wide kernel (k = 97, 129; §4k): MR_RNS_TCW=0 (or the IMAD-only path) keeps the IMAD wide kernel
+static bool tcw_enabled() {
+    if (!tensor_path_enabled()) return false;
+    static const bool on = [] { const char *e = getenv("MR_RNS_TCW"); return !(e && e[0] == '0'); }();
+    return on;
+}
+
+// 128-message tile-jobs (ctas0 per context) on one persistent CTA per SM
+static int launch_ladders_tcw(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x, size_t in_limbs,
+                              size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status, void *stream,
+                              const KernelSet &ks) {
+    const mr_rns_ctx *c0 = ctxs[0];
+    cudaStream_t st = (cudaStream_t)stream;
+    const u32 ctas0 = (u32)((count + 127) / 128);
+    const u32 jobs = ctas0 * (u32)nctx;
+    const u32 jobs_total = ctas0 * 128 * (u32)nctx;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device);
+    static const int max_sms = [] { const char *e = getenv("MR_RNS_MAX_SMS"); return e ? atoi(e) : 0; }();
+    if (max_sms > 0) sms = std::min(sms, std::max(1, max_sms));
+    const u32 grid = std::min<u32>((u32)sms, jobs);
+    int w = 1;
+    for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
+    const size_t nch = 2 * (size_t)c0->k + 1;
+    u32 *d_table = nullptr;
+    if (cudaMallocAsync(&d_table, (size_t)table_slots(w) * nch * jobs_total * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    ModexpParams P;
+    memset(&P, 0, sizeof P);
+    for (int i = 0; i < 2; i++) {
+        const int s = i < nctx ? i : nctx - 1;
+        P.ctx[i] = ctxs[s]->d_cx;
+        P.prog[i] = progs[s].d_ops;
+        P.nops[i] = progs[s].nops;
+    }
+    P.ctas0 = ctas0;
+    P.count = (u32)count;
+    P.x = d_x;
+    P.in_limbs = (u32)in_limbs;
+    P.half = (u32)half;
+    P.y = d_y;
+    P.out_limbs = (u32)out_limbs;
+    P.out_stride = count * out_limbs;
+    P.status = d_status;
+    P.table = d_table;
+    P.jobs_total = jobs_total;
+    int rc = timed_launch(0, st, [&] {
+                 return ks.launch_modexp_tcw(P, grid, c0->d_wide, c0->d_tcw, c0->cxw, c0->be1w, jobs, stream);
+             }) == 0
+                 ? MR_OK
+                 : MR_ERR_CUDA;
+    cudaFreeAsync(d_table, st);
+    return rc;
+}
+
 // wide-operand ladders (wide_path(k)): 16 messages per CTA, one CTA per 16 messages and context
 static int launch_ladders_wide(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x,
                                size_t in_limbs, size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status,
                                void *stream, bool lanes) {
     const mr_rns_ctx *c0 = ctxs[0];
     cudaStream_t st = (cudaStream_t)stream;
+    if (!lanes && c0->d_tcw && c0->be1w && tcw_enabled()) {
+        const KernelSet &ks = kernel_set_for(c0->k);
+        if (ks.launch_modexp_tcw)
+            return launch_ladders_tcw(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count, d_status, stream, ks);
+    }
     const u32 MBm = (u32)(lanes ? wide_messages_per_cta_lanes() : wide_messages_per_cta());
     const u32 ctas0 = (u32)((count + MBm - 1) / MBm);
     const u32 jobs_total = ctas0 * MBm * nctx;

@@ -187,6 +187,74 @@ __host__ __device__ constexpr u32 wide_cx_words(u32 k) { return wide_cx_a1(k) + 
 __host__ __device__ constexpr bool is_wide(u32 k) { return k > 129; }
 
 // ---------------------------------------------------------------------------------------------
+// Tensor-core wide kernel (mr_tcw.cuh, k = 97 and 129: 3072- / 4096-bit moduli and the CRT halves of
+// 6144- / 8192-bit keys).  The byte-split contraction of tc_* above, but the B images
+// (k² words × 16 bytes) no longer fit shared memory, so they are STREAMED from L2 by the bulk-copy
+// (TMA) engine, one [chunk rows × 128 K-bytes] slab per pipeline stage.  Four contraction types share
+// the machinery ("extensions" e):
+//   TCW_BE1  BE1 merged with 6.4: outputs j < k (B') and j = k (the m_r column q̂_r)     k+1 outputs
+//   TCW_BE2  BE2 with the α' column                                                       k outputs
+//   TCW_TRN  positional -> RNS (to_rns): outputs = the 2k channels                       2k outputs
+//   TCW_EXT  RNS -> positional (exit): outputs = the k+1 limbs of X (4 byte positions)   k+1 outputs
+// Each output owns 4 accumulator columns (byte b of the constant; for TCW_EXT byte position 4L+b).
+// Outputs are cut into chunks (multiples of 4 outputs) whose 4·outputs columns, rounded to 16, fit a
+// TMEM accumulator buffer; two buffers alternate (MMA of chunk c+1 under the epilogue of chunk c) and
+// the B residues of the state live in TMEM after them: 2·NCMAX + round4(k) <= 512 columns.
+// K: every extension reads the whole A row of tcw_kp(k) bytes (zero-padded): 13 K-steps of 32 bytes at
+// k = 97, 17 at k = 129, grouped in slabs of 4 steps (the last slab shorter).
+// Global image of an extension: the blocks (chunk c, slab s) back to back, each NC_c × 32·steps_s
+// bytes in the K-major SWIZZLE_NONE core-matrix layout with SBO = steps_s·256 (LBO = 128).
+// ---------------------------------------------------------------------------------------------
+enum : u32 { TCW_BE1 = 0, TCW_BE2 = 1, TCW_TRN = 2, TCW_EXT = 3 };
+__host__ __device__ constexpr bool tcw_k(u32 k) { return k == 97 || k == 129; }
+__host__ __device__ constexpr u32 tcw_kp(u32 k) { return (4 * k + 4 + 31) & ~31u; }     // A row bytes (α' word k)
+__host__ __device__ constexpr u32 tcw_ks(u32 k) { return tcw_kp(k) / 32; }               // K-steps
+__host__ __device__ constexpr u32 tcw_nslab(u32 k) { return (tcw_ks(k) + 3) / 4; }
+__host__ __device__ constexpr u32 tcw_steps(u32 k, u32 s) { return s + 1 < tcw_nslab(k) ? 4u : tcw_ks(k) - 4 * s; }
+__host__ __device__ constexpr u32 tcw_bsw(u32 k) { return (k + 3) & ~3u; }              // TMEM columns of B residues
+__host__ __device__ constexpr u32 tcw_nout(u32 k, u32 e) {
+    return e == TCW_BE1 ? k + 1 : e == TCW_BE2 ? k : e == TCW_TRN ? 2 * k : k + 1;
+}
+// largest outputs per chunk (multiple of 4) whose columns fit a buffer of the TMEM budget
+__host__ __device__ constexpr u32 tcw_ocmax(u32 k) { return (((512 - tcw_bsw(k)) / 2) & ~15u) / 4 & ~3u; }
+__host__ __device__ constexpr u32 tcw_nchunks(u32 k, u32 e) { return (tcw_nout(k, e) + tcw_ocmax(k) - 1) / tcw_ocmax(k); }
+__host__ __device__ constexpr u32 tcw_oc(u32 k, u32 e) {                                 // outputs per chunk (last: rest)
+    return ((tcw_nout(k, e) + tcw_nchunks(k, e) - 1) / tcw_nchunks(k, e) + 3) & ~3u;
+}
+__host__ __device__ constexpr u32 tcw_out0(u32 k, u32 e, u32 c) { return c * tcw_oc(k, e); }
+__host__ __device__ constexpr u32 tcw_outn(u32 k, u32 e, u32 c) {
+    return tcw_out0(k, e, c) + tcw_oc(k, e) <= tcw_nout(k, e) ? tcw_oc(k, e) : tcw_nout(k, e) - tcw_out0(k, e, c);
+}
+__host__ __device__ constexpr u32 tcw_nc(u32 k, u32 e, u32 c) { return (4 * tcw_outn(k, e, c) + 15) & ~15u; }  // MMA N
+__host__ __device__ constexpr u32 tcw_ncmax(u32 k) {
+    u32 m = 0;
+    for (u32 e = 0; e < 4; e++)
+        for (u32 c = 0; c < tcw_nchunks(k, e); c++) m = tcw_nc(k, e, c) > m ? tcw_nc(k, e, c) : m;
+    return m;
+}
+__host__ __device__ constexpr u32 tcw_stage_bytes(u32 k) { return tcw_ncmax(k) * 128; }
+__host__ __device__ constexpr u32 tcw_blk_bytes(u32 k, u32 e, u32 c, u32 s) { return tcw_nc(k, e, c) * 32 * tcw_steps(k, s); }
+__host__ __device__ constexpr u32 tcw_blk_off(u32 k, u32 e, u32 c, u32 s) {              // bytes from the image start
+    u32 o = 0;
+    for (u32 cc = 0; cc < c; cc++) o += tcw_nc(k, e, cc) * tcw_kp(k);
+    for (u32 ss = 0; ss < s; ss++) o += tcw_blk_bytes(k, e, c, ss);
+    return o;
+}
+__host__ __device__ constexpr u32 tcw_img_bytes(u32 k, u32 e) { return tcw_blk_off(k, e, tcw_nchunks(k, e), 0); }
+// byte (row r of chunk c, K byte kb) of an extension image
+__host__ __device__ constexpr u32 tcw_at(u32 k, u32 e, u32 c, u32 r, u32 kb) {
+    const u32 s = kb / 128, kl = kb % 128;
+    return tcw_blk_off(k, e, c, s) + (r / 8) * (tcw_steps(k, s) * 256) + (kl / 16) * 128 + (r % 8) * 16 + kl % 16;
+}
+// per-k image buffer: BE2 | TRN | EXT (each 16-byte aligned; BE1 is per context, after the wide section)
+__host__ __device__ constexpr u32 tcw_img_off(u32 k, u32 e) {
+    return e == TCW_BE2 ? 0u : e == TCW_TRN ? tcw_img_bytes(k, TCW_BE2) : tcw_img_bytes(k, TCW_BE2) + tcw_img_bytes(k, TCW_TRN);
+}
+__host__ __device__ constexpr u32 tcw_kimg_bytes(u32 k) { return tcw_img_off(k, TCW_EXT) + tcw_img_bytes(k, TCW_EXT); }
+// per-context words after the wide section: the BE1 image
+__host__ __device__ constexpr u32 tcw_cx_words(u32 k) { return tcw_img_bytes(k, TCW_BE1) / 4; }
+
+// ---------------------------------------------------------------------------------------------
 // Exponentiation "program": one u64 op per Montgomery multiplication step, executed by a single
 // inlined mont_mul inside the kernel's interpreter loop (keeps one copy of the unrolled code).
 // ---------------------------------------------------------------------------------------------
@@ -302,6 +370,9 @@ struct KernelSet {
     int tc_tiles;                                         // 128-message tiles per CTA of the TC kernel
     int threads;                                          // CTA size used by launch_modexp
     int mr_tiles;                                         // 128-candidate tiles per CTA of k_mr_rounds_tc
+    // tensor-core wide kernel (k = 97, 129; mr_tcw.cuh), null elsewhere: tab = wide table, kimg = per-k images
+    int (*launch_modexp_tcw)(const ModexpParams &p, u32 ctas, const u32 *tab, const void *kimg, u32 cxw, u32 be1w,
+                             u32 jobs, void *stream);
 };
 
 }  // namespace mr

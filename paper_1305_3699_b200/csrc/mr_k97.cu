@@ -3,5 +3,5 @@
 #include "mr_kernels.cuh"
 
 namespace mr {
-KernelSet kernels_k97() { return KernelSet{MR_K, upload_base, launch_modexp, launch_combine, launch_mr, launch_modexp_tc, TC_TILES, T, MR_TC_TILES}; }
+KernelSet kernels_k97() { return KernelSet{MR_K, upload_base, launch_modexp, launch_combine, launch_mr, launch_modexp_tc, TC_TILES, T, MR_TC_TILES, launch_modexp_tcw}; }
 }  // namespace mr

@@ -1941,6 +1941,8 @@ constexpr int MR_TC_TILES = TCM;
 constexpr int MR_TC_TILES = 0;
 #endif
 
+#include "mr_tcw.cuh"   // tensor-core wide kernel (k = 97, 129)
+
 // ------------------------------------------------------------------ host-side launchers
 
 template <class Prm>
@@ -1997,6 +1999,28 @@ constexpr int TC_TILES = TCT;
 #else
 constexpr int (*launch_modexp_tc)(const ModexpParams &, u32, void *) = nullptr;
 constexpr int TC_TILES = 0;
+#endif
+
+#if MR_K == 97 || MR_K == 129
+// ctas = persistent CTAs (one per SM); tab = wide table, kimg = per-k images, cxw / be1w = context offsets (words)
+int launch_modexp_tcw(const ModexpParams &p, u32 ctas, const u32 *tab, const void *kimg, u32 cxw, u32 be1w, u32 jobs,
+                      void *stream) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute((const void *)k_modexp_tcw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM) !=
+            cudaSuccess)
+            return 6;
+        attr = true;
+    }
+    TcwArgs a{tab, reinterpret_cast<const uint8_t *>(kimg), cxw, be1w, jobs};
+    void *args[] = {const_cast<ModexpParams *>(&p), &a};
+    return cudaLaunchKernel((const void *)k_modexp_tcw, dim3(ctas), dim3(W_THREADS), args, W_SMEM, (cudaStream_t)stream) ==
+                   cudaSuccess
+               ? 0
+               : 6;
+}
+#else
+constexpr int (*launch_modexp_tcw)(const ModexpParams &, u32, const u32 *, const void *, u32, u32, u32, void *) = nullptr;
 #endif
 
 int launch_combine(const CombineParams &p, void *stream) { return launch(k_combine, (p.count + T - 1) / T, p, stream); }
