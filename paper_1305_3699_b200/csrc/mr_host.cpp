@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -728,8 +729,8 @@ static void fill_tcw_modular(int k, u32 e, int nin, Coef &&coef, Mod &&modo, uin
     }
 }
 static u32 r32_of(u32 m) { return (u32)((1ull << 32) % m); }
-// per-context BE1: A(i, j) = A1'_ij 2^64 mod m'_j (6.4 merged, the epilogue's two Montgomery folds), and the m_r
-// column A(i, k) = |M_i|_{2^32}
+// per-context BE1: A(i, j) = A1'_ij 2^32 mod m'_j (6.4 merged; the epilogue folds t*_j C1_j 2^64 + D_j with one
+// Montgomery reduction), and the m_r column A(i, k) = |M_i|_{2^32}
 static void fill_tcw_be1(const Base &b, const u32 *cx, uint8_t *img) {
     const int k = b.k;
     const u32 *A1 = b.flat.data() + base_layout(k).A1, *A1r = b.flat.data() + base_layout(k).A1r;
@@ -737,7 +738,7 @@ static void fill_tcw_be1(const Base &b, const u32 *cx, uint8_t *img) {
         [&](int i, u32 j) -> u64 {
             if ((int)j == k) return A1r[i];
             const u32 m = b.Bp[j], r = r32_of(m);
-            return mulm(mulm(mulm(A1[i * k + j], cx[cx_c2(k) + j], m), r, m), r, m);
+            return mulm(mulm(A1[i * k + j], cx[cx_c2(k) + j], m), r, m);
         },
         [&](u32 j) -> u64 { return (int)j == k ? 0 : b.Bp[j]; }, img);
 }
@@ -1088,8 +1089,10 @@ static bool tensor_path_enabled() {
 }
 
 // tensor-core wide kernel (k = 97, 129; §4k): MR_RNS_TCW=0 (or the IMAD-only path) keeps the IMAD wide kernel
+static int g_tcw_override = -1;
 static bool tcw_enabled() {
     if (!tensor_path_enabled()) return false;
+    if (g_tcw_override >= 0) return g_tcw_override == 1;
     static const bool on = [] { const char *e = getenv("MR_RNS_TCW"); return !(e && e[0] == '0'); }();
     return on;
 }
@@ -1107,12 +1110,13 @@ static int launch_ladders_tcw(mr_rns_ctx *const *ctxs, const DevProg *progs, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device);
     static const int max_sms = [] { const char *e = getenv("MR_RNS_MAX_SMS"); return e ? atoi(e) : 0; }();
     if (max_sms > 0) sms = std::min(sms, std::max(1, max_sms));
-    const u32 grid = std::min<u32>((u32)sms, jobs);
+    const u32 grid = std::min<u32>((u32)sms, (jobs + TCW_TILES - 1) / TCW_TILES);
     int w = 1;
     for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
     const size_t nch = 2 * (size_t)c0->k + 1;
     u32 *d_table = nullptr;
-    if (cudaMallocAsync(&d_table, (size_t)table_slots(w) * nch * jobs_total * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    // window table + one spare slot (to_rns parks its B' outputs there, mr_tcw.cuh)
+    if (cudaMallocAsync(&d_table, (size_t)(table_slots(w) + 1) * nch * jobs_total * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
     ModexpParams P;
     memset(&P, 0, sizeof P);
     for (int i = 0; i < 2; i++) {
@@ -1132,11 +1136,27 @@ static int launch_ladders_tcw(mr_rns_ctx *const *ctxs, const DevProg *progs, int
     P.status = d_status;
     P.table = d_table;
     P.jobs_total = jobs_total;
+    P.hslot = table_slots(w);
+    // MR_TCW_TRACE=file: debug timeline of CTA 0 (phase timestamps, mr_tcw.cuh w_trace) appended to `file`
+    static const char *trace_file = getenv("MR_TCW_TRACE");
+    unsigned long long *d_trace = nullptr;
+    if (trace_file && cudaMallocAsync(&d_trace, 16384 * 8, st) == cudaSuccess) cudaMemsetAsync(d_trace, 0, 16384 * 8, st);
     int rc = timed_launch(0, st, [&] {
-                 return ks.launch_modexp_tcw(P, grid, c0->d_wide, c0->d_tcw, c0->cxw, c0->be1w, jobs, stream);
+                 return ks.launch_modexp_tcw(P, grid, c0->d_wide, c0->d_tcw, c0->cxw, c0->be1w, jobs, d_trace, stream);
              }) == 0
                  ? MR_OK
                  : MR_ERR_CUDA;
+    if (d_trace) {
+        std::vector<unsigned long long> h(16384);
+        if (cudaMemcpyAsync(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+            cudaStreamSynchronize(st) == cudaSuccess) {
+            if (FILE *f = fopen(trace_file, "ab")) {
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
+        cudaFreeAsync(d_trace, st);
+    }
     cudaFreeAsync(d_table, st);
     return rc;
 }
@@ -1565,6 +1585,37 @@ int mr_internal_wide_table(int k, uint32_t *out, size_t cap) {
     const std::vector<u32> t = build_wide_table(base_for(k));
     if (out) memcpy(out, t.data(), std::min(cap, t.size()) * 4);
     return (int)t.size();
+}
+
+// test hook (CPU): byte image of tensor-core wide extension e (mr_internal.h TCW_*) for k = 97 / 129; e = TCW_BE1 is
+// per context and needs the modulus (limbs words), the others are per k.  Returns the byte count, < 0 on error.
+int mr_internal_tcw_image(int k, int e, const uint32_t *modulus, size_t limbs, uint8_t *out, size_t cap) {
+    if (!tcw_k((u32)k) || e < 0 || e > 3) return -MR_ERR_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const Base &b = base_for(k);
+    std::vector<uint8_t> img;
+    if (e == TCW_BE1) {
+        Big N = big_of(modulus, limbs);
+        if (N.empty() || !(N[0] & 1)) return -MR_ERR_EVEN_MODULUS;
+        if (!fits(b, N)) return -MR_ERR_CAPACITY;
+        std::vector<u32> x(cx_words(k), 0);
+        fill_ctx_block(b, N, limbs, N, limbs, nullptr, nullptr, x.data());
+        img.resize(tcw_img_bytes(k, TCW_BE1));
+        fill_tcw_be1(b, x.data(), img.data());
+    } else {
+        const std::vector<uint8_t> all = build_tcw_images(b);
+        const u32 o = tcw_img_off(k, e);
+        img.assign(all.begin() + o, all.begin() + o + tcw_img_bytes(k, e));
+    }
+    if (out) memcpy(out, img.data(), std::min(cap, img.size()));
+    return (int)img.size();
+}
+
+// test hook: the tensor-core wide kernel for k = 97 / 129 (§4k): 1 = on (default), 0 = the IMAD wide kernel,
+// -1 = follow MR_RNS_TCW
+int mr_internal_set_tcw(int on) {
+    g_tcw_override = on;
+    return MR_OK;
 }
 
 int mr_internal_ctx_table(const uint32_t *modulus, size_t limbs, int k, uint32_t *out, size_t cap) {

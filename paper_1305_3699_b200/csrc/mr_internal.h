@@ -197,9 +197,9 @@ __host__ __device__ constexpr bool is_wide(u32 k) { return k > 129; }
 //   TCW_TRN  positional -> RNS (to_rns): outputs = the 2k channels                       2k outputs
 //   TCW_EXT  RNS -> positional (exit): outputs = the k+1 limbs of X (4 byte positions)   k+1 outputs
 // Each output owns 4 accumulator columns (byte b of the constant; for TCW_EXT byte position 4L+b).
-// Outputs are cut into chunks (multiples of 4 outputs) whose 4·outputs columns, rounded to 16, fit a
-// TMEM accumulator buffer; two buffers alternate (MMA of chunk c+1 under the epilogue of chunk c) and
-// the B residues of the state live in TMEM after them: 2·NCMAX + round4(k) <= 512 columns.
+// A CTA runs TCW_TILES = 2 independent 128-message tiles; each tile owns, in TMEM, the B residues of its
+// state (round4(k) columns) and one accumulator buffer; outputs are cut into chunks (multiples of 4
+// outputs) whose 4·outputs columns, rounded to 16, fit that buffer: 2·(round4(k) + NCMAX) <= 512.
 // K: every extension reads the whole A row of tcw_kp(k) bytes (zero-padded): 13 K-steps of 32 bytes at
 // k = 97, 17 at k = 129, grouped in slabs of 4 steps (the last slab shorter).
 // Global image of an extension: the blocks (chunk c, slab s) back to back, each NC_c × 32·steps_s
@@ -215,8 +215,9 @@ __host__ __device__ constexpr u32 tcw_bsw(u32 k) { return (k + 3) & ~3u; }      
 __host__ __device__ constexpr u32 tcw_nout(u32 k, u32 e) {
     return e == TCW_BE1 ? k + 1 : e == TCW_BE2 ? k : e == TCW_TRN ? 2 * k : k + 1;
 }
-// largest outputs per chunk (multiple of 4) whose columns fit a buffer of the TMEM budget
-__host__ __device__ constexpr u32 tcw_ocmax(u32 k) { return (((512 - tcw_bsw(k)) / 2) & ~15u) / 4 & ~3u; }
+constexpr u32 TCW_TILES = 2;
+// largest outputs per chunk (multiple of 4) whose columns fit a tile's accumulator buffer
+__host__ __device__ constexpr u32 tcw_ocmax(u32 k) { return ((512 / TCW_TILES - tcw_bsw(k)) & ~15u) / 4 & ~3u; }
 __host__ __device__ constexpr u32 tcw_nchunks(u32 k, u32 e) { return (tcw_nout(k, e) + tcw_ocmax(k) - 1) / tcw_ocmax(k); }
 __host__ __device__ constexpr u32 tcw_oc(u32 k, u32 e) {                                 // outputs per chunk (last: rest)
     return ((tcw_nout(k, e) + tcw_nchunks(k, e) - 1) / tcw_nchunks(k, e) + 3) & ~3u;
@@ -372,7 +373,7 @@ struct KernelSet {
     int mr_tiles;                                         // 128-candidate tiles per CTA of k_mr_rounds_tc
     // tensor-core wide kernel (k = 97, 129; mr_tcw.cuh), null elsewhere: tab = wide table, kimg = per-k images
     int (*launch_modexp_tcw)(const ModexpParams &p, u32 ctas, const u32 *tab, const void *kimg, u32 cxw, u32 be1w,
-                             u32 jobs, void *stream);
+                             u32 jobs, void *trace, void *stream);
 };
 
 }  // namespace mr

@@ -11,30 +11,46 @@
 //   TRN (a2, to_rns)         D ≡ Σ_l x_l |2^(32l)|_{m_c} 2^32 (mod m_c)   (B' entries × λ_j: ξ-form)
 //   EXT (a7, exit)           D[p] = Σ byte_a(ξ'_j) byte_{p-a}(M'_j) + α' bytes × (2^(32(k+1)) - M'): the byte
 //                            convolution of X = Σ_j ξ'_j M'_j + α'(2^(32(k+1)) - M'), carried into limbs per thread
-// The B images (16k² bytes per extension: 150 KB at k = 97) exceed shared memory next to a 128-message tile, so a
-// producer warp streams them from L2 with the bulk-copy (TMA) engine through a ring of stages, one
-// [chunk rows x 128 K-bytes] slab per stage; an MMA warp issues the K-steps of each slab into one of two TMEM
-// accumulator buffers; the four compute warps (one message per thread, 128 messages = the 128 TMEM lanes) run the
-// channel products and the epilogues, the epilogue of chunk c overlapping the MMAs of chunk c+1.
-// State of a message: B residues in TMEM (columns W_BS.., one lane per message), B' and m_r in shared-memory rows,
-// the A row (its K-major operand bytes) as scratch for the current contraction's inputs.
+// The B images (16k² bytes per extension: 150 KB at k = 97) exceed shared memory, so they are STREAMED from L2
+// by the bulk-copy (TMA) engine through a ring of stages, one [chunk rows x 128 K-bytes] slab per stage.
+//
+// A CTA runs TCW_TILES = 2 independent tiles of 128 messages (one message per thread, the 128 TMEM lanes), each
+// with its own producer thread (stage ring), MMA-issuer thread, accumulator buffer and four compute warps, so one
+// tile's CUDA-core phases (channel products, epilogues) run under the other tile's MMAs.
+// State of a message (the shared memory of two tiles holds only their A tiles and stages):
+//   B residues   TMEM columns [BS, BS + k) of the tile, lane = message
+//   B' (ξ-form)  its A row, words 0 .. k-1 — exactly the BE2 / exit input, so no copy after BE2
+//   m_r          its A row, word k+1 (the images are zero in those K columns)
+// The A row is also each contraction's input; an extension whose outputs would overwrite inputs still needed by
+// later chunks parks them in TMEM (BE1: ξ'_j in place of t*_j in the B columns) or in HBM (to_rns: the B' outputs
+// in the window table's spare slot), and the A row is written once all chunks are done.
 #pragma once
 
 #if MR_K == 97 || MR_K == 129
 
 constexpr u32 W_KP = tcw_kp(K);                       // A row bytes
+constexpr u32 W_KC = W_KP / 16;                       // K-cores (4 words) per A row
 constexpr u32 W_SBOA = (W_KP / 16) * 128;             // A tile: bytes between 8-row groups
-constexpr u32 W_NCMAX = tcw_ncmax(K);                 // TMEM columns of one accumulator buffer
-constexpr u32 W_BS = 2 * W_NCMAX;                     // first TMEM column of the B residues
-static_assert(W_BS + tcw_bsw(K) <= 512, "accumulator buffers + B residues exceed the 512 TMEM columns");
+constexpr u32 W_NCMAX = tcw_ncmax(K);                 // TMEM columns of a tile's accumulator buffer
+constexpr u32 W_BSW = tcw_bsw(K);
+constexpr u32 W_TCOLS = W_NCMAX + W_BSW;              // TMEM columns per tile: [acc | B residues]
+static_assert(TCW_TILES * W_TCOLS <= 512, "tiles x (accumulator + B residues) exceed the 512 TMEM columns");
+static_assert(W_KC * 4 >= K + 2, "A row must hold B' (k words), α' (word k) and m_r (word k+1)");
 constexpr u32 W_STG = tcw_stage_bytes(K);
-constexpr u32 W_ROWS = (K + 1) * 128;                 // B' and m_r rows (words)
-constexpr size_t W_FIXED = (size_t)128 * W_KP + 4 * (size_t)W_ROWS + 16 * K + 8 * K + 8 * K + 256;
-constexpr u32 W_NST_FIT = (u32)((232448 - W_FIXED) / W_STG);
-constexpr u32 W_NST = W_NST_FIT > 8 ? 8 : W_NST_FIT;  // pipeline stages
-static_assert(W_NST >= 2, "tensor wide kernel: fewer than two B stages fit shared memory");
-constexpr size_t W_SMEM = W_FIXED + (size_t)W_NST * W_STG;
-constexpr u32 W_THREADS = 192;                        // warps 0-3 compute, 4 producer (TMA), 5 MMA issuer
+constexpr u32 W_ABYTES = 128 * W_KP;
+constexpr size_t W_FIXED = (size_t)TCW_TILES * W_ABYTES + 16 * K + 8 * K + 8 * K + 512 + TCW_TILES * 2048;
+constexpr u32 W_NST_FIT = (u32)((232448 - W_FIXED) / (TCW_TILES * W_STG));
+constexpr u32 W_NST = W_NST_FIT > 6 ? 6 : W_NST_FIT;  // pipeline stages per tile
+static_assert(W_NST >= 2, "tensor wide kernel: fewer than two B stages per tile fit shared memory");
+constexpr size_t W_SMEM = W_FIXED + (size_t)TCW_TILES * W_NST * W_STG;
+#ifndef MR_TCW_HALVES
+#define MR_TCW_HALVES 1       // compute warps per TMEM lane quadrant and tile (2: each takes alternate channel groups)
+#endif
+constexpr u32 W_HV = MR_TCW_HALVES;
+constexpr u32 W_CW = 4 * W_HV * TCW_TILES;            // compute warps
+constexpr u32 W_THREADS = 32 * (W_CW + 2 * TCW_TILES);   // + per tile a producer warp and an MMA warp (one lane each:
+                                                         // two roles in one warp would sleep on each other's waits)
+constexpr u32 W_NBAR = 2 * W_NST + 3;                 // per tile: full[NST] empty[NST] accf acce aready
 
 struct TcwArgs {
     const u32 *wtab;          // per-k wide table (mr_internal.h wide_layout): m, -m^-1, C1 2^64, |M'_j|_{2^32}
@@ -42,10 +58,52 @@ struct TcwArgs {
     u32 cxw;                  // word offset of the wide section (σ_i 2^64) in a context block
     u32 be1w;                 // word offset of the context's BE1 image in its context block
     u32 jobs;                 // 128-message tile-jobs over all contexts (ctas0 per context)
+    unsigned long long *trace;   // debug timeline (MR_TCW_TRACE, CTA 0 only): [0] = count, then (clock << 16 | code)
 };
+// code = tile << 12 | role << 8 | event (role 0 compute thread 0, 1 MMA issuer, 2 producer); each (tile, role) writes
+// its own region of W_TRN entries with plain stores (no atomics: the trace must not perturb the timeline)
+constexpr u32 W_TRN = 2700;
+struct WTrace {
+    unsigned long long *p = nullptr;
+    u32 n = 0, code = 0;
+    __device__ void init(unsigned long long *tr, u32 tile, u32 role) {
+        if (tr && blockIdx.x == 0) {
+            p = tr + 1 + (tile * 3 + role) * W_TRN;
+            code = tile << 12 | role << 8;
+        }
+    }
+    __device__ void operator()(u32 ev) {
+        if (p && n < W_TRN) {
+            long long c;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+            p[n++] = ((unsigned long long)c << 16) | code | ev;
+        }
+    }
+};
+__device__ __forceinline__ u64 mulw(u32 a, u32 b) {   // one IMAD.WIDE.U32
+    u64 r;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ u64 madw(u32 a, u32 b, u64 c) {
+    u64 r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+    return r;
+}
 
 __device__ __forceinline__ u32 smem_u32(const void *p) { return (u32)__cvta_generic_to_shared(p); }
-// byte-column combine V = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3 = hi 2^32 + lo for d_b < 2^31 (one carry chain)
+// byte-column combine V = d0 + 2^8 d1 + 2^16 d2 + 2^24 d3 (< 2^49.2 for d_b < 2^25.1) as three wide multiply-adds
+// (3 IMAD.WIDE instead of 6 shifts + 6 carry adds)
+__device__ __forceinline__ u64 tc_comb(u32 d0, u32 d1, u32 d2, u32 d3) {
+    u64 v;
+    asm("mad.wide.u32 %0, %1, 256, %2;\n\t"
+        "mad.wide.u32 %0, %3, 65536, %0;\n\t"
+        "mad.wide.u32 %0, %4, 16777216, %0;"
+        : "=l"(v)
+        : "r"(d1), "l"((u64)d0), "r"(d2), "r"(d3));
+    return v;
+}
+// the same sum as hi 2^32 + lo with shifts and one carry chain (ALU pipe; the FMA-heavy pipe is the contended one)
 __device__ __forceinline__ void tc_split(u32 d0, u32 d1, u32 d2, u32 d3, u32 &lo, u32 &hi) {
     asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, 0;\n\t"
         "add.cc.u32 %0, %0, %5;\n\taddc.u32 %1, %1, %6;\n\t"
@@ -54,15 +112,27 @@ __device__ __forceinline__ void tc_split(u32 d0, u32 d1, u32 d2, u32 d3, u32 &lo
         : "r"(d0), "r"(d1 << 8), "r"(d1 >> 24), "r"(d2 << 16), "r"(d2 >> 16), "r"(d3 << 24), "r"(d3 >> 8));
 }
 __device__ __forceinline__ void w_mbar_init(u32 a, u32 n) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n)); }
+__device__ __forceinline__ u64 w_gtimer() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// wait for phase `par` of an mbarrier; try_wait with a suspend-time hint parks the thread in hardware until the phase
+// completes (instead of re-issuing the test); a wait longer than 30 s traps instead of hanging the GPU
 __device__ __forceinline__ void w_mbar_wait(u32 a, u32 par) {
     u32 done = 0;
+    u64 t0 = 0;
 #pragma unroll 1
     for (u32 spin = 0; !done; spin++) {
-        asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+        asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
                      : "=r"(done)
-                     : "r"(a), "r"(par)
+                     : "r"(a), "r"(par), "r"(1000000u)
                      : "memory");
-        if (spin > (1u << 26)) __trap();   // a lost arrival traps instead of hanging the GPU
+        if (!done && (spin & 255) == 255) {
+            const u64 t = w_gtimer();
+            if (!t0) t0 = t;
+            else if (t - t0 > 30000000000ull) __trap();
+        }
     }
 }
 __device__ __forceinline__ void w_mbar_arrive(u32 a) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory"); }
@@ -78,13 +148,29 @@ __device__ __forceinline__ void w_bulk_g2s(u32 dst, const void *src, u32 bytes, 
 __device__ __forceinline__ u64 w_desc(u32 saddr, u32 sbo) {
     return (u64)((saddr >> 4) & 0x3FFF) | ((u64)(128u >> 4) << 16) | ((u64)(sbo >> 4) << 32) | ((u64)1 << 46);
 }
+// TMEM loads without a memory clobber: w_tmem_wait(v) orders the uses of the loaded registers, so independent loads
+// (shared memory, the window table) can be issued while the TMEM load is in flight
 __device__ __forceinline__ void w_tmem_ld16(u32 taddr, u32 (&v)[16]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
-                 "tcgen05.wait::ld.sync.aligned;"
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                    "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                 : "r"(taddr)
-                 : "memory");
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void w_tmem_ld8(u32 taddr, u32 (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void w_tmem_ld4(u32 taddr, u32 (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr));
+}
+template <int N>
+__device__ __forceinline__ void w_tmem_wait(u32 (&v)[N]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < N; i++) asm volatile("" : "+r"(v[i]));   // the loaded registers are used after the wait
 }
 __device__ __forceinline__ void w_tmem_st4(u32 taddr, u32 a, u32 b, u32 c, u32 d) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c), "r"(d)
@@ -104,7 +190,7 @@ __device__ __forceinline__ u32 w_addmod(u32 a, u32 b, u32 r32) {
     return (u32)t + (u32)(t >> 32) * r32;
 }
 
-// the extensions of one program op, in the order every role walks them (TRN, then BE1 + BE2)
+// chunk geometry of extension e (runtime e, compile-time K)
 __device__ __forceinline__ u32 w_nchunks(u32 e) {
     return e == TCW_BE1 ? tcw_nchunks(K, TCW_BE1) : e == TCW_BE2 ? tcw_nchunks(K, TCW_BE2)
                         : e == TCW_TRN ? tcw_nchunks(K, TCW_TRN) : tcw_nchunks(K, TCW_EXT);
@@ -113,33 +199,30 @@ __device__ __forceinline__ u32 w_oc(u32 e) {
     return e == TCW_BE1 ? tcw_oc(K, TCW_BE1) : e == TCW_BE2 ? tcw_oc(K, TCW_BE2) : e == TCW_TRN ? tcw_oc(K, TCW_TRN)
                                                                                                 : tcw_oc(K, TCW_EXT);
 }
-__device__ __forceinline__ u32 w_nout(u32 e) { return tcw_nout(K, e); }
 __device__ __forceinline__ u32 w_outn(u32 e, u32 c) {
-    const u32 o0 = c * w_oc(e), n = w_nout(e);
+    const u32 o0 = c * w_oc(e), n = tcw_nout(K, e);
     return o0 + w_oc(e) <= n ? w_oc(e) : n - o0;
 }
 __device__ __forceinline__ u32 w_nc(u32 e, u32 c) { return (4 * w_outn(e, c) + 15) & ~15u; }
 
-struct TcwSm {                 // shared-memory carve-up and barrier addresses
+struct TcwTile {               // one tile's shared memory and barriers
     uint8_t *a;                // A tile [128 x W_KP] core-matrix layout
-    u32 stage0;                // shared address of stage 0
-    u32 *rows;                 // [(K+1)][128]: B' (ξ-form) and m_r
-    const uint4 *ep1;          // [K] (m'_j, -m'_j^-1, C1_j 2^64, |M'_j|_{2^32})
-    const uint2 *ep2;          // [K] (m_i, -m_i^-1)
-    const u32 *sig;            // [2][K] σ_i 2^64 mod m_i per context
-    u32 bar;                   // shared address of the barrier block: full[NST] empty[NST] accf[2] acce[2] aready
+    u32 stage0;                // shared address of its stage 0
+    u32 bar;                   // shared address of its barriers: full[NST] empty[NST] accf acce aready
+    u32 tacc;                  // TMEM column of its accumulator buffer (lane 0)
     __device__ u32 full(u32 s) const { return bar + 8 * s; }
     __device__ u32 empty(u32 s) const { return bar + 8 * (W_NST + s); }
-    __device__ u32 accf(u32 b) const { return bar + 8 * (2 * W_NST + b); }
-    __device__ u32 acce(u32 b) const { return bar + 8 * (2 * W_NST + 2 + b); }
-    __device__ u32 aready() const { return bar + 8 * (2 * W_NST + 4); }
+    __device__ u32 accf() const { return bar + 8 * (2 * W_NST); }
+    __device__ u32 acce() const { return bar + 8 * (2 * W_NST + 1); }
+    __device__ u32 aready() const { return bar + 8 * (2 * W_NST + 2); }
 };
 
 // ---------------------------------------------------------------- producer: stream the B slabs of an extension
 struct TcwProducer {
     u32 st = 0, ph = 0;
     u64 pol;
-    __device__ void ext(const TcwSm &S, u32 e, const uint8_t *img) {
+    WTrace tr;
+    __device__ void ext(const TcwTile &T, u32 e, const uint8_t *img) {
         u32 off = 0;
 #pragma unroll 1
         for (u32 c = 0; c < w_nchunks(e); c++) {
@@ -147,9 +230,10 @@ struct TcwProducer {
 #pragma unroll 1
             for (u32 s = 0; s < tcw_nslab(K); s++) {
                 const u32 bytes = nc * 32 * tcw_steps(K, s);
-                w_mbar_wait(S.empty(st), ph ^ 1u);
-                w_mbar_expect_tx(S.full(st), bytes);
-                w_bulk_g2s(S.stage0 + st * W_STG, img + off, bytes, S.full(st), pol);
+                w_mbar_wait(T.empty(st), ph ^ 1u);
+                tr((e << 4) | (s == 0 ? 1 : 2));
+                w_mbar_expect_tx(T.full(st), bytes);
+                w_bulk_g2s(T.stage0 + st * W_STG, img + off, bytes, T.full(st), pol);
                 off += bytes;
                 if (++st == W_NST) { st = 0; ph ^= 1u; }
             }
@@ -157,29 +241,32 @@ struct TcwProducer {
     }
 };
 
-// ---------------------------------------------------------------- MMA issuer: one thread
+// ---------------------------------------------------------------- MMA issuer: one thread per tile
 struct TcwMma {
-    u32 st = 0, fph = 0, aph = 0, acc = 0, eph[2] = {0, 0};
+    u32 st = 0, fph = 0, aph = 0, eph = 0;
     u32 tmem;
-    __device__ void ext(const TcwSm &S, u32 e) {
-        w_mbar_wait(S.aready(), aph);          // the A rows of all 128 messages are written (and proxy-fenced)
+    WTrace tr;
+    __device__ void ext(const TcwTile &T, u32 e) {
+        w_mbar_wait(T.aready(), aph);          // the A rows of all 128 messages are written (and proxy-fenced)
         aph ^= 1u;
+        tr(e << 4);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const u32 sa = smem_u32(S.a);
+        const u32 sa = smem_u32(T.a), td = tmem + T.tacc;
 #pragma unroll 1
         for (u32 c = 0; c < w_nchunks(e); c++) {
-            const u32 b = acc, nc = w_nc(e, c);
-            w_mbar_wait(S.acce(b), eph[b] ^ 1u);   // the epilogue has read this buffer's previous chunk
-            eph[b] ^= 1u;
+            const u32 nc = w_nc(e, c);
+            w_mbar_wait(T.acce(), eph ^ 1u);   // the epilogue has read the buffer's previous chunk
+            eph ^= 1u;
+            tr((e << 4) | 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const u32 idesc = (2u << 4) | ((nc >> 3) << 17) | ((128u >> 4) << 24);   // s32 = u8 x u8, K-major, M = 128
-            const u32 td = tmem + b * W_NCMAX;
 #pragma unroll 1
             for (u32 s = 0; s < tcw_nslab(K); s++) {
                 const u32 steps = tcw_steps(K, s);
-                w_mbar_wait(S.full(st), fph);
+                w_mbar_wait(T.full(st), fph);
+                tr((e << 4) | 3);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const u32 sb = S.stage0 + st * W_STG;
+                const u32 sb = T.stage0 + st * W_STG;
 #pragma unroll 1
                 for (u32 j = 0; j < steps; j++) {
                     const u64 da = w_desc(sa + (4 * s + j) * 256, W_SBOA), db = w_desc(sb + j * 256, steps * 256);
@@ -189,213 +276,385 @@ struct TcwMma {
                                  "l"(da), "l"(db), "r"(idesc), "r"(accum)
                                  : "memory");
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(S.empty(st))
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(T.empty(st))
                              : "memory");
                 if (++st == W_NST) { st = 0; fph ^= 1u; }
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(S.accf(b))
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(T.accf())
                          : "memory");
-            acc ^= 1u;
+            tr((e << 4) | 2);
         }
     }
 };
 
-// ---------------------------------------------------------------- compute warps: one message per thread
+// ---------------------------------------------------------------- compute warps
+// A tile's 128 messages are served by 8 warps: warp (quadrant q, half h) owns messages 32q .. 32q+31 (its TMEM lane
+// quadrant) and, of every group of 16 channels / 4 extension outputs, the groups whose index is ≡ h (mod 2).  The two
+// halves meet at a named barrier where a step needs the other half's results (α', the B residues before the next
+// multiplication, the parked to_rns outputs, the exit).
 struct TcwCompute {
-    const TcwSm &S;
-    u32 tmem;                 // TMEM base
-    u32 lane_base;            // (warp's first lane) << 16
+    const TcwTile &T;
+    const uint4 *ep1;         // [K] (m'_j, -m'_j^-1, C1_j 2^64, |M'_j|_{2^32})
+    const uint2 *ep2;         // [K] (m_i, -m_i^-1)
+    const u32 *sig;           // [2][K] σ_i 2^64 mod m_i per context
+    u32 tmem;                 // TMEM base + this warp's lane quadrant
+    u32 bs;                   // TMEM column of the tile's B residues
     u32 m;                    // message = TMEM lane
+    u32 h;                    // half: the groups ≡ h (mod 2)
     uint8_t *arow;            // this message's A row
-    u32 acc = 0, fph[2] = {0, 0};
+    uint2 *xch;               // [2][128] per-half partial sums (α')
+    u32 bar_id;               // named barrier of the tile's 256 compute threads
+    u32 fph = 0;
+    WTrace tr;                // trace (thread 0 of the tile only)
+    __device__ void trace(u32 ev) { if (m == 0 && h == 0) tr(ev); }
     u32 sel = 0;              // context of the current job
     const u32 *cx = nullptr;  // its context block (HBM)
 
-    __device__ u32 &row(u32 j) const { return S.rows[j * 128 + m]; }
-    __device__ u32 tb(u32 col) const { return tmem + lane_base + col; }
-    __device__ void put_a(u32 w, const uint4 &v) const { *reinterpret_cast<uint4 *>(arow + w * 128) = v; }   // words 4w..4w+3 (K-core w)
-    __device__ void a_done() const {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy A writes -> async proxy (MMA)
-        w_mbar_arrive(S.aready());
+    __device__ u32 &aw(u32 i) const { return *reinterpret_cast<u32 *>(arow + (i >> 2) * 128 + 4 * (i & 3)); }
+    __device__ uint4 &ac(u32 c) const { return *reinterpret_cast<uint4 *>(arow + c * 128); }   // K-core c: words 4c..4c+3
+    __device__ u32 tb(u32 col) const { return tmem + col; }
+    __device__ bool mine16(u32 g) const { return W_HV == 1 || (g & 1u) == h; }   // 16-word / 16-channel group g
+    static constexpr u32 GW = (K + 16) / 16;                               // 16-word groups covering words 0 .. K+1
+    // both halves of the tile: TMEM stores done, shared / global writes visible
+    __device__ void sync() const {
+        w_tmem_wait_st();
+        if (W_HV == 1) return;
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(128 * W_HV) : "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    // chunk c of an extension: wait for its accumulator, hand each 16-column group (4 outputs) to f, release
-    template <class F>
-    __device__ void chunks(u32 e, F &&f) {
+    // 16 B columns 16g.. of the tile (the last group stops at W_BSW: the next columns are the other tile's)
+    __device__ void st_b16(u32 g, const u32 (&v)[16]) const {
+        if (16 * g + 16 <= W_BSW) {
+            w_tmem_st16(tb(bs + 16 * g), v);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (16 * g + 4 * q < W_BSW) w_tmem_st4(tb(bs + 16 * g + 4 * q), v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+    }
+    __device__ void a_done() {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy A writes -> async proxy (MMA)
+        w_mbar_arrive(T.aready());
+        trace(0x0F);
+    }
+    // Chunks of extension E: wait for the accumulator, combine the four byte columns of every output of this half's
+    // groups into V (64-bit registers), release the buffer at once (the next chunk's MMAs run under the rest of the
+    // epilogue), then f(o0, n4, Vl, Vh): group g = W_HV gi + h of the chunk has outputs o0 + 4g .. +3, V = Vh 2^32 + Vl
+    // at [4 gi ..].
+    template <u32 E>
+    __host__ __device__ static constexpr u32 nloc() { return (tcw_oc(K, E) / 4 + W_HV - 1) / W_HV; }
+    template <u32 E, class F>
+    __device__ void chunks(F &&f) {
+        constexpr u32 OC = tcw_oc(K, E), LG = nloc<E>();
 #pragma unroll 1
-        for (u32 c = 0; c < w_nchunks(e); c++) {
-            const u32 b = acc;
-            w_mbar_wait(S.accf(b), fph[b]);
-            fph[b] ^= 1u;
+        for (u32 c = 0; c < tcw_nchunks(K, E); c++) {
+            w_mbar_wait(T.accf(), fph);
+            fph ^= 1u;
+            trace((E << 4) | 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const u32 n4 = (w_outn(e, c) + 3) / 4, o0 = c * w_oc(e);
-#pragma unroll 1
-            for (u32 g = 0; g < n4; g++) {
-                u32 v[16];
-                w_tmem_ld16(tb(b * W_NCMAX + 16 * g), v);
-                f(o0 + 4 * g, v);
+            const u32 n4 = (w_outn(E, c) + 3) / 4;
+            u32 Vl[4 * LG], Vh[4 * LG];
+            {
+#pragma unroll
+                for (u32 gi = 0; gi < LG; gi += 2) {
+                    const u32 g0 = W_HV * gi + h, g1 = W_HV * (gi + 1) + h;
+                    if (g0 < n4) {
+                        u32 v[16], w[16];
+                        w_tmem_ld16(tb(T.tacc + 16 * g0), v);
+                        if (gi + 1 < LG && g1 < n4) w_tmem_ld16(tb(T.tacc + 16 * g1), w);
+                        w_tmem_wait(v);
+                        if (gi + 1 < LG && g1 < n4) w_tmem_wait(w);
+#pragma unroll
+                        for (int t = 0; t < 4; t++) {
+                            tc_split(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3], Vl[4 * gi + t], Vh[4 * gi + t]);
+                            if (gi + 1 < LG)
+                                tc_split(w[4 * t], w[4 * t + 1], w[4 * t + 2], w[4 * t + 3], Vl[4 * gi + 4 + t], Vh[4 * gi + 4 + t]);
+                        }
+                    }
+                }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if ((m & 31) == 0) w_mbar_arrive(S.acce(b));
-            acc ^= 1u;
+            if ((m & 31) == 0) w_mbar_arrive(T.acce());
+            trace((E << 4) | 2);
+            f(c * OC, n4, Vl, Vh);
+            trace((E << 4) | 3);
         }
     }
 
-    // a2: positional -> RNS of nl limbs at x (masked to zero when !ok); m_r = x_0
-    __device__ void to_rns(const u32 *x, u32 nl, bool ok) {
+    // a2: positional -> RNS of nl limbs at x (masked to zero when !ok); B -> TMEM, B' -> the A row (parked in the
+    // window table's spare slot `park` while the chunks still read the limbs), m_r = x_0 -> word k+1
+    __device__ void to_rns(const u32 *x, u32 nl, bool ok, u32 *park, size_t tstride) {
 #pragma unroll 1
-        for (u32 w = 0; w < W_KP / 16; w++) {
+        for (u32 w = 0; w < W_KC; w++) {
+            if (!mine16(w / 4)) continue;
             u32 q[4];
 #pragma unroll
-            for (int t = 0; t < 4; t++) q[t] = (ok && 4 * w + t < nl) ? x[4 * w + t] : 0u;
-            put_a(w, make_uint4(q[0], q[1], q[2], q[3]));
+            for (int t = 0; t < 4; t++) q[t] = (ok && 4 * w + t < nl) ? __ldg(x + 4 * w + t) : 0u;
+            ac(w) = make_uint4(q[0], q[1], q[2], q[3]);
         }
+        const u32 x0 = ok ? __ldg(x) : 0u;
         a_done();
-        row(K) = ok ? x[0] : 0u;
-        chunks(TCW_TRN, [&](u32 o, const u32 (&v)[16]) {
-            u32 r[4];
+        constexpr u32 LG = nloc<TCW_TRN>();
+        chunks<TCW_TRN>([&](u32 o0, u32 n4, const u32 (&Vl)[4 * LG], const u32 (&Vh)[4 * LG]) {
 #pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const u32 ch = o + t;
-                u32 lo, hi;
-                tc_split(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3], lo, hi);
-                const uint2 mm = ch < K ? S.ep2[ch] : make_uint2(S.ep1[ch - K < K ? ch - K : 0].x, S.ep1[ch - K < K ? ch - K : 0].y);
-                r[t] = mont_red(lo, hi, mm.x, mm.y);
-                if (ch >= K && ch < 2 * K) row(ch - K) = r[t];
-            }
-            if (o < K) w_tmem_st4(tb(W_BS + o), r[0], r[1], r[2], r[3]);   // straddling group: B' lanes land in padding
-        });
-        w_tmem_wait_st();
-    }
-
-    // 6.1-6.6: st <- st · b · M^-1 (mod N); b at bp[c · bs] (window table column or constant vector), or st (sq)
-    __device__ void mont_mul(const u32 *bp, u32 bs, bool sq) {
-        const u32 *sig = S.sig + sel * K;
-        // ---- 6.1 B channels: ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i, into the A row (BE1 input)
-#pragma unroll 1
-        for (u32 g = 0; g < (K + 15) / 16; g++) {
-            u32 a[16];
-            w_tmem_ld16(tb(W_BS + 16 * g), a);
-            u32 xi[16];
+            for (u32 gi = 0; gi < LG; gi++) {
+                const u32 g = W_HV * gi + h;
+                if (g < n4) {
+                    const u32 o = o0 + 4 * g;
+                    u32 r[4];
 #pragma unroll
-            for (int t = 0; t < 16; t++) {
-                const u32 i = 16 * g + t;
-                xi[t] = 0;
-                if (i < K) {
-                    const u32 b = sq ? a[t] : __ldcg(bp + (size_t)i * bs);
-                    const uint2 mm = S.ep2[i];
-                    const u64 pr = (u64)a[t] * b;
-                    const u32 tt = mont_red((u32)pr, (u32)(pr >> 32), mm.x, mm.y);
-                    const u64 ps = (u64)tt * sig[i];
-                    xi[t] = mont_red((u32)ps, (u32)(ps >> 32), mm.x, mm.y);
+                    for (int t = 0; t < 4; t++) {
+                        const u32 ch = o + t;
+                        const u32 j = ch - K < K ? ch - K : 0u;
+                        const uint2 mm = ch < K ? ep2[ch] : make_uint2(ep1[j].x, ep1[j].y);
+                        r[t] = mont_red(Vl[4 * gi + t], Vh[4 * gi + t], mm.x, mm.y);
+                        if (ch >= K && ch < 2 * K) park[(size_t)(ch - K) * tstride] = r[t];
+                    }
+                    if (o < K) w_tmem_st4(tb(bs + o), r[0], r[1], r[2], r[3]);   // straddling group: B' lanes -> padding
                 }
             }
-#pragma unroll
-            for (int q = 0; q < 4; q++)   // (the last group may reach past the row's W_KP / 16 K-cores)
-                if (4 * g + q < W_KP / 16) put_a(4 * g + q, make_uint4(xi[4 * q], xi[4 * q + 1], xi[4 * q + 2], xi[4 * q + 3]));
-        }
-        a_done();
-        // ---- 6.2 B' channels t*_j = a*_j b*_j 2^-32 and the m_r product, under the BE1 MMAs
+        });
+        sync();                                           // both halves' parked B' outputs and B residues written
 #pragma unroll 4
-        for (u32 j = 0; j < K; j++) {
-            const u32 a = row(j);
-            const u32 b = sq ? a : __ldcg(bp + (size_t)(K + j) * bs);
-            const uint4 e1 = S.ep1[j];
-            const u64 pr = (u64)a * b;
-            row(j) = mont_red((u32)pr, (u32)(pr >> 32), e1.x, e1.y);
-        }
-        const u32 ar = row(K);
-        const u32 tr = ar * (sq ? ar : __ldcg(bp + (size_t)(2 * K) * bs));
-        // ---- 6.3-6.5 BE1 epilogue: ξ'_j = mont(t*_j C1_j 2^64 + mont(D_j)); m_r column -> r_r
-        u32 sr = 0, rr = 0;
-        const u32 nminv = cx[CX_NMINV_R];
-        chunks(TCW_BE1, [&](u32 o, const u32 (&v)[16]) {
-#pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const u32 j = o + t;
-                u32 lo, hi;
-                tc_split(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3], lo, hi);
-                if (j < K) {
-                    const uint4 e1 = S.ep1[j];
-                    const u32 x1 = mont_red(lo, hi, e1.x, e1.y);
-                    const u64 p = (u64)row(j) * e1.z + x1;
-                    const u32 xp = mont_red((u32)p, (u32)(p >> 32), e1.x, e1.y);
-                    row(j) = xp;
-                    sr += xp * e1.w;
-                } else if (j == K) {   // q̂_r = Σ ξ_i |M_i|_{2^32} mod 2^32;  r_r = (t_r + q̂_r N) M^-1
-                    rr = tr * GB(O_MISC + 0) + lo * nminv;
-                }
-            }
-        });
-        // ---- 6.6 BE2: A row = (ξ'_0 .. ξ'_{k-1}, α'), α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 exact
-        const u32 alpha = (sr - rr) * GB(O_MISC + 1);
-        fill_a_from_rows(alpha);
-        a_done();
-        row(K) = rr;
-        chunks(TCW_BE2, [&](u32 o, const u32 (&v)[16]) {
-            u32 r[4];
-#pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const u32 i = o + t < K ? o + t : K - 1;
-                u32 lo, hi;
-                tc_split(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3], lo, hi);
-                const uint2 mm = S.ep2[i];
-                r[t] = mont_red(lo, hi, mm.x, mm.y);
-            }
-            w_tmem_st4(tb(W_BS + o), r[0], r[1], r[2], r[3]);
-        });
-        w_tmem_wait_st();
-    }
-
-    // A row words 0..K-1 <- B' rows, word K <- extra (α'), the rest zero
-    __device__ void fill_a_from_rows(u32 extra) {
-#pragma unroll 1
-        for (u32 w = 0; w < W_KP / 16; w++) {
+        for (u32 w = 0; w < W_KC; w++) {
+            if (!mine16(w / 4)) continue;
             u32 q[4];
 #pragma unroll
             for (int t = 0; t < 4; t++) {
                 const u32 j = 4 * w + t;
-                q[t] = j < K ? row(j) : (j == K ? extra : 0u);
+                q[t] = j < K ? park[(size_t)j * tstride] : (j == K + 1 ? x0 : 0u);
             }
-            put_a(w, make_uint4(q[0], q[1], q[2], q[3]));
+            ac(w) = make_uint4(q[0], q[1], q[2], q[3]);
         }
     }
 
-    // a7: X = Σ ξ'_j M'_j + α'(2^(32(K+1)) - M') on the tensor core (byte convolution), limbs into rows 0..K,
-    // then X mod N by conditional subtraction of N 2^s, s = SMAX..0 (X < (K+3) N)
-    __device__ void from_rns() {
-        u32 sr = 0;
-#pragma unroll 4
-        for (u32 j = 0; j < K; j++) sr += row(j) * S.ep1[j].w;
-        const u32 alpha = (sr - row(K)) * GB(O_MISC + 1);
-        fill_a_from_rows(alpha);
-        a_done();
-        u64 carry = 0;
-        chunks(TCW_EXT, [&](u32 o, const u32 (&v)[16]) {
+    // 6.1 / 6.2 for channels c0 .. c0 + N - 1 (N <= 16, c0 a multiple of 8): ξ_i = mont(mont(a_i b_i) σ_i 2^64) (B, into
+    // the A row over the B' words it consumed) and t*_j = mont(a*_j b*_j) (B', into the TMEM columns of the B residues
+    // it consumed)
+    template <bool SQ, u32 N>
+    __device__ __forceinline__ void chan_group(u32 c0, const u32 *bp, u32 bs_, const u32 *sg) {
+        constexpr u32 NW = N > 8 ? 16 : 8;
+        const uint2 *e2 = ep2 + c0;
+        const uint4 *e1 = ep1 + c0;
+        const u32 *sgg = sg + c0;
+        u32 r[NW], xa[NW], b1[N], b2[N];
+        if constexpr (NW == 16) w_tmem_ld16(tb(bs + c0), r);
+        else w_tmem_ld8(tb(bs + c0), r);
 #pragma unroll
-            for (int t = 0; t < 4; t++) {
-                const u32 l = o + t;
-                if (l <= K) {
-                    const u64 s = carry + v[4 * t] + ((u64)v[4 * t + 1] << 8) + ((u64)v[4 * t + 2] << 16) + ((u64)v[4 * t + 3] << 24);
-                    row(l) = (u32)s;
-                    carry = s >> 32;
+        for (u32 q = 0; q < (N + 3) / 4; q++) {
+            const uint4 v = ac(c0 / 4 + q);
+            xa[4 * q] = v.x; xa[4 * q + 1] = v.y; xa[4 * q + 2] = v.z; xa[4 * q + 3] = v.w;
+        }
+        if (!SQ) {
+            const u32 *b = bp + (size_t)c0 * bs_;
+#pragma unroll
+            for (u32 t = 0; t < N; t++) {
+                b1[t] = __ldcg(b + (size_t)t * bs_);
+                b2[t] = __ldcg(b + (size_t)(K + t) * bs_);
+            }
+        }
+        w_tmem_wait(r);
+        u32 xi[NW], ts[NW];
+#pragma unroll
+        for (u32 t = 0; t < NW; t++) xi[t] = ts[t] = 0u;
+#pragma unroll
+        for (u32 t = 0; t < N; t++) {
+            const uint2 mm = e2[t];
+            const u64 pr = mulw(r[t], SQ ? r[t] : b1[t]);
+            const u32 tt = mont_red((u32)pr, (u32)(pr >> 32), mm.x, mm.y);
+            const u64 ps = mulw(tt, sgg[t]);
+            xi[t] = mont_red((u32)ps, (u32)(ps >> 32), mm.x, mm.y);
+            const uint4 c1 = e1[t];
+            const u64 pp = mulw(xa[t], SQ ? xa[t] : b2[t]);
+            ts[t] = mont_red((u32)pp, (u32)(pp >> 32), c1.x, c1.y);
+        }
+#pragma unroll
+        for (u32 q = 0; q < (N + 3) / 4; q++) w_tmem_st4(tb(bs + c0 + 4 * q), ts[4 * q], ts[4 * q + 1], ts[4 * q + 2], ts[4 * q + 3]);
+#pragma unroll
+        for (u32 q = 0; q < (N + 3) / 4; q++) ac(c0 / 4 + q) = make_uint4(xi[4 * q], xi[4 * q + 1], xi[4 * q + 2], xi[4 * q + 3]);
+    }
+
+    // α' and r_r from both halves' partial sums (Σ ξ'_j |M'_j|_{2^32} over each half's outputs; r_r from its owner)
+    __device__ uint2 exchange(u32 sr, u32 rr) {
+        if (W_HV == 1) { sync(); return make_uint2(sr, rr); }
+        xch[h * 128 + m] = make_uint2(sr, rr);
+        sync();
+        const uint2 o = xch[(h ^ 1u) * 128 + m];
+        return make_uint2(sr + o.x, rr + o.y);
+    }
+
+    // 6.1-6.6: st <- st · b · M^-1 (mod N); b at bp[c · bs_] (window table column or constant vector), or st (SQ)
+    template <bool SQ>
+    __device__ void mont_mul(const u32 *bp, u32 bs_) {
+        trace(0x0E);
+        const u32 *sg = sig + sel * K;
+        u32 br = 0;
+        const u32 ar = aw(K + 1);
+        if (!SQ) br = __ldcg(bp + (size_t)(2 * K) * bs_);
+        // ---- 6.1 / 6.2: this half's 16-channel groups
+#pragma unroll 1
+        for (u32 g = h; g < K / 16; g += W_HV) {
+            if (W_HV == 1) {
+                chan_group<SQ, 16>(16 * g, bp, bs_, sg);
+            } else {
+                chan_group<SQ, 8>(16 * g, bp, bs_, sg);
+                chan_group<SQ, 8>(16 * g + 8, bp, bs_, sg);
+            }
+        }
+        static_assert(K % 16 <= 8, "tail channels fit one 8-channel group");
+        if (K % 16 && mine16(K / 16)) chan_group<SQ, K % 16>(16 * (K / 16), bp, bs_, sg);
+        const u32 trm = ar * (SQ ? ar : br);
+        w_tmem_wait_st();
+        a_done();
+        // ---- 6.3-6.5 BE1 epilogue: ξ'_j = mont(t*_j C1_j 2^64 + D_j) over t*_j in TMEM; m_r column -> r_r
+        u32 sr = 0, rr = 0;
+        const u32 nminv = cx[CX_NMINV_R];
+        constexpr u32 LG1 = nloc<TCW_BE1>();
+        chunks<TCW_BE1>([&](u32 o0, u32 n4, const u32 (&Vl)[4 * LG1], const u32 (&Vh)[4 * LG1]) {
+#pragma unroll
+            for (u32 gi = 0; gi < LG1; gi += 2) {
+                const u32 g0 = W_HV * gi + h, g1 = g0 + W_HV;
+                if (g0 < n4) {
+                    const u32 oa = o0 + 4 * g0, ob = o0 + 4 * g1;
+                    u32 ta[4], tc[4];
+                    w_tmem_ld4(tb(bs + (oa < K ? oa : 0)), ta);
+                    if (gi + 1 < LG1 && g1 < n4) w_tmem_ld4(tb(bs + (ob < K ? ob : 0)), tc);
+                    w_tmem_wait(ta);
+                    if (gi + 1 < LG1 && g1 < n4) w_tmem_wait(tc);
+#pragma unroll
+                    for (u32 u = 0; u < 2; u++) {
+                        if (gi + u < LG1 && (u == 0 || g1 < n4)) {
+                            const u32 oh = u ? ob : oa;
+                            u32 xp[4];
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                const u32 j = oh + t, q = 4 * (gi + u) + t;
+                                const uint4 e1 = ep1[j < K ? j : 0];
+                                // ξ'_j = mont(t*_j C1_j 2^64 + V_j): t* C1 2^64 < 2^32 m'_j <= 2^64 - 2^43 (the B' primes
+                                // are below 2^32 - 2^11, reading R1) and V < 2^49.2, so the sum fits 64 bits
+                                const u64 p = madw(u ? tc[t] : ta[t], e1.z, ((u64)Vh[q] << 32) | Vl[q]);
+                                xp[t] = mont_red((u32)p, (u32)(p >> 32), e1.x, e1.y);
+                                if (j < K) sr += xp[t] * e1.w;
+                                if (j == K) rr = trm * GB(O_MISC + 0) + Vl[q] * nminv;   // q̂_r = Σ ξ_i |M_i|_{2^32}
+                            }
+                            if (oh < K) w_tmem_st4(tb(bs + oh), xp[0], xp[1], xp[2], xp[3]);   // ξ'_j in place of t*_j
+                        }
+                    }
                 }
             }
         });
+        // ---- 6.6 BE2: A row = (ξ'_0 .. ξ'_{k-1}, α', r_r), α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 exact
+        const uint2 tot = exchange(sr, rr);              // (also: every ξ'_j of both halves is in TMEM)
+        const u32 alpha = (tot.x - tot.y) * GB(O_MISC + 1);
+        rr = tot.y;
+#pragma unroll 1
+        for (u32 g = h; g < GW; g += W_HV) {
+            u32 v[16];
+            w_tmem_ld16(tb(bs + 16 * g), v);
+            w_tmem_wait(v);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if (4 * g + q < W_KC) {
+                    u32 w4[4];
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        const u32 j = 16 * g + 4 * q + t;
+                        w4[t] = j < K ? v[4 * q + t] : (j == K ? alpha : (j == K + 1 ? rr : 0u));
+                    }
+                    ac(4 * g + q) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                }
+            }
+        }
+        a_done();
+        constexpr u32 LG2 = nloc<TCW_BE2>();
+        chunks<TCW_BE2>([&](u32 o0, u32 n4, const u32 (&Vl)[4 * LG2], const u32 (&Vh)[4 * LG2]) {
+#pragma unroll
+            for (u32 gi = 0; gi < LG2; gi++) {
+                const u32 g = W_HV * gi + h;
+                if (g < n4) {
+                    const u32 o = o0 + 4 * g;
+                    u32 r[4];
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        const uint2 mm = ep2[o + t < K ? o + t : K - 1];
+                        r[t] = mont_red(Vl[4 * gi + t], Vh[4 * gi + t], mm.x, mm.y);
+                    }
+                    w_tmem_st4(tb(bs + o), r[0], r[1], r[2], r[3]);
+                }
+            }
+        });
+        sync();                                           // every r_i in TMEM before the next multiplication reads them
+    }
+
+    // a7: X = Σ ξ'_j M'_j + α'(2^(32(K+1)) - M') on the tensor core (byte convolution); half 0 carries the limbs (parked
+    // in the TMEM B columns, then A row words 0..K) and reduces X mod N by conditional subtraction of N 2^s,
+    // s = SMAX..0 (X < (K+3) N); returns with the limbs in the A row of half 0's thread
+    __device__ void from_rns() {
+        u32 sr = 0;
+#pragma unroll 1
+        for (u32 g = h; g < GW; g += W_HV) {
+#pragma unroll
+            for (u32 t = 0; t < 16; t++)
+                if (16 * g + t < K) sr += aw(16 * g + t) * ep1[16 * g + t].w;
+        }
+        const uint2 tot = exchange(sr, 0u);
+        if (mine16(K / 16)) aw(K) = (tot.x - aw(K + 1)) * GB(O_MISC + 1);
+        a_done();
+        // half 0 carries the byte-position sums into limbs group by group (the buffer is released after the chunk)
+        u64 carry = 0;
+#pragma unroll 1
+        for (u32 c = 0; c < tcw_nchunks(K, TCW_EXT); c++) {
+            w_mbar_wait(T.accf(), fph);
+            fph ^= 1u;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (h == 0) {
+                const u32 n4 = (w_outn(TCW_EXT, c) + 3) / 4, o0 = c * tcw_oc(K, TCW_EXT);
+#pragma unroll 1
+                for (u32 g = 0; g < n4; g++) {
+                    u32 v[16];
+                    w_tmem_ld16(tb(T.tacc + 16 * g), v);
+                    w_tmem_wait(v);
+                    u32 l4[4];
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        const u64 s = carry + tc_comb(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
+                        l4[t] = (u32)s;
+                        carry = s >> 32;
+                    }
+                    w_tmem_st4(tb(bs + o0 + 4 * g), l4[0], l4[1], l4[2], l4[3]);   // limbs (columns < round4(K+1))
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if ((m & 31) == 0) w_mbar_arrive(T.acce());
+        }
+        if (h) return;
+        w_tmem_wait_st();
+#pragma unroll 1
+        for (u32 g = 0; g < GW; g++) {
+            u32 v[16];
+            w_tmem_ld16(tb(bs + 16 * g), v);
+            w_tmem_wait(v);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (4 * g + q < W_KC) ac(4 * g + q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
         const u32 *nl = cx + cx_n(K);
 #pragma unroll 1
         for (int s = SMAX; s >= 0; s--) {
 #pragma unroll 1
             for (int pass = 0; pass < 2; pass++) {   // pass 0: borrow of X - N 2^s; pass 1: subtract
-                u32 br = 0;
+                u32 brw = 0;
 #pragma unroll 4
                 for (u32 l = 0; l <= K; l++) {
                     const u32 nsh = __funnelshift_l(l ? __ldg(nl + l - 1) : 0u, __ldg(nl + l), s);
-                    const u64 t = (u64)row(l) - nsh - br;
-                    if (pass) row(l) = (u32)t;
-                    br = (u32)(t >> 63);
+                    const u64 t = (u64)aw(l) - nsh - brw;
+                    if (pass) aw(l) = (u32)t;
+                    brw = (u32)(t >> 63);
                 }
-                if (br) break;
+                if (brw) break;
             }
         }
     }
@@ -404,19 +663,22 @@ struct TcwCompute {
     __device__ void job(const ModexpParams &P, u32 jl, bool valid) {
         const u32 *xrow = P.x + (size_t)(valid ? jl : 0) * P.in_limbs;
         const bool ok = valid && less_than(xrow, cx + cx_inb(K), P.in_limbs);
-        if (valid && sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
+        if (valid && h == 0 && sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
         const size_t tstride = P.jobs_total, entry = (size_t)NCH * tstride;
         const u32 col = sel * P.ctas0 * 128 + jl;     // window-table column (tail lanes too: jl < ctas0 * 128)
         const u64 *prog = sel ? P.prog[1] : P.prog[0];
         const u32 nops = sel ? P.nops[1] : P.nops[0];
+        u64 nop = __ldg(prog);
 #pragma unroll 1
         for (u32 s = 0; s < nops; s++) {
-            const u64 op = __ldg(prog + s);
+            const u64 op = nop;
+            if (s + 1 < nops) nop = __ldg(prog + s + 1);   // next op under this one (the program lives in L2)
             const u32 fl = (u32)op & 0xFF, opnd = (u32)(op >> 8) & 0xFF, ld = (u32)(op >> 16) & 0xFF;
             const u32 ad = (u32)(op >> 24) & 0xFF, sto = (u32)(op >> 32) & 0xFF;
             if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) {
                 const u32 off = (fl & OPF_TORNS_HI) ? P.half : 0u;
-                to_rns(xrow + off, (fl & OPF_TORNS_ALL) ? P.in_limbs : P.half, ok);
+                to_rns(xrow + off, (fl & OPF_TORNS_ALL) ? P.in_limbs : P.half, ok, P.table + P.hslot * entry + col,
+                       tstride);
             }
             if (fl & OPF_LOAD) {
                 const u32 *src;
@@ -424,81 +686,100 @@ struct TcwCompute {
                 if (ld >= 0xF0) { src = cx + cx_r2(K) + (ld - 0xF0) * NCH; str = 1; }
                 else { src = P.table + ld * entry + col; str = tstride; }
 #pragma unroll 1
-                for (u32 g = 0; g < tcw_bsw(K) / 4; g++) {
-                    u32 q[4];
+                for (u32 g = h; g < GW; g += W_HV) {
 #pragma unroll
-                    for (int t = 0; t < 4; t++) q[t] = 4 * g + t < K ? src[(4 * g + t) * str] : 0u;
-                    w_tmem_st4(tb(W_BS + 4 * g), q[0], q[1], q[2], q[3]);
+                    for (u32 q = 0; q < 4; q++) {
+                        const u32 w = 4 * g + q;
+                        if (w < W_BSW / 4) {
+                            u32 b4[4];
+#pragma unroll
+                            for (int t = 0; t < 4; t++) b4[t] = 4 * w + t < K ? src[(4 * w + t) * str] : 0u;
+                            w_tmem_st4(tb(bs + 4 * w), b4[0], b4[1], b4[2], b4[3]);
+                        }
+                        if (w < W_KC) {
+                            u32 a4[4];
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                const u32 j = 4 * w + t;
+                                a4[t] = j < K ? src[(K + j) * str] : (j == K + 1 ? src[2 * K * str] : 0u);
+                            }
+                            ac(w) = make_uint4(a4[0], a4[1], a4[2], a4[3]);
+                        }
+                    }
                 }
-#pragma unroll 4
-                for (u32 j = 0; j <= K; j++) row(j) = src[(K + j) * str];
                 w_tmem_wait_st();
             }
             if (!(fl & OPF_NOMUL)) {
-                const bool sq = opnd == OPND_SQ;
-                const u32 *bp = sq ? nullptr : (opnd >= 0xF0 ? cx + cx_r2(K) + (opnd - 0xF0) * NCH : P.table + opnd * entry + col);
-                mont_mul(bp, sq ? 0u : (opnd >= 0xF0 ? 1u : (u32)tstride), sq);
+                if (opnd == OPND_SQ) mont_mul<true>(nullptr, 0);
+                else if (opnd >= 0xF0) mont_mul<false>(cx + cx_r2(K) + (opnd - 0xF0) * NCH, 1);
+                else mont_mul<false>(P.table + opnd * entry + col, (u32)tstride);
             }
             if (fl & OPF_ADD) {   // channel-wise modular addition (CRT entry, a3)
                 const u32 *src = P.table + ad * entry + col;
 #pragma unroll 1
-                for (u32 g = 0; g < (K + 15) / 16; g++) {
+                for (u32 g = h; g < GW; g += W_HV) {
                     u32 a[16];
-                    w_tmem_ld16(tb(W_BS + 16 * g), a);
+                    w_tmem_ld16(tb(bs + 16 * g), a);
+                    w_tmem_wait(a);
 #pragma unroll
                     for (int t = 0; t < 16; t++) {
                         const u32 i = 16 * g + t;
-                        if (i < K) a[t] = w_addmod(a[t], src[i * tstride], 0u - S.ep2[i].x);
+                        if (i < K) a[t] = w_addmod(a[t], src[i * tstride], 0u - ep2[i].x);
+                        if (i < K) aw(i) = w_addmod(aw(i), src[(K + i) * tstride], 0u - ep1[i].x);
+                        if (i == K + 1) aw(K + 1) += src[2 * K * tstride];
                     }
-                    w_tmem_st16(tb(W_BS + 16 * g), a);
+                    st_b16(g, a);
                 }
-#pragma unroll 4
-                for (u32 j = 0; j < K; j++) row(j) = w_addmod(row(j), src[(K + j) * tstride], 0u - S.ep1[j].x);
-                row(K) += src[2 * K * tstride];
                 w_tmem_wait_st();
             }
             if (fl & OPF_STORE) {
                 u32 *dst = P.table + sto * entry + col;
 #pragma unroll 1
-                for (u32 g = 0; g < (K + 15) / 16; g++) {
+                for (u32 g = h; g < GW; g += W_HV) {
                     u32 a[16];
-                    w_tmem_ld16(tb(W_BS + 16 * g), a);
+                    w_tmem_ld16(tb(bs + 16 * g), a);
+                    w_tmem_wait(a);
 #pragma unroll
-                    for (int t = 0; t < 16; t++)
-                        if (16 * g + t < K) dst[(16 * g + t) * tstride] = a[t];
+                    for (int t = 0; t < 16; t++) {
+                        const u32 i = 16 * g + t;
+                        if (i < K) dst[i * tstride] = a[t];
+                        if (i < K) dst[(K + i) * tstride] = aw(i);
+                        if (i == K + 1) dst[2 * K * tstride] = aw(K + 1);
+                    }
                 }
-#pragma unroll 4
-                for (u32 j = 0; j <= K; j++) dst[(K + j) * tstride] = row(j);
             }
         }
         from_rns();
-        if (valid) {
+        if (valid && h == 0) {
             u32 *yrow = P.y + sel * P.out_stride + (size_t)jl * P.out_limbs;
 #pragma unroll 1
-            for (u32 l = 0; l < P.out_limbs; l++) yrow[l] = ok ? row(l) : 0u;
+            for (u32 l = 0; l < P.out_limbs; l++) yrow[l] = ok ? aw(l) : 0u;
         }
+        sync();                                           // the A row is free for the next job
     }
 };
 
-// Persistent kernel, one CTA per SM: tile-jobs t = blockIdx.x, blockIdx.x + gridDim.x, ... of 128 messages;
-// job t runs context sel = t / ctas0.  Every role walks the same job list and op programs, so the producer,
-// the MMA issuer and the epilogues meet on the same sequence of (extension, chunk, slab).
+// Persistent kernel, one CTA per SM, TCW_TILES independent tiles per CTA: tile u of CTA b takes the tile-jobs
+// t = b·TILES + u, + gridDim.x·TILES, ...; job t runs context sel = t / ctas0.  The producer, the MMA issuer and
+// the compute warps of a tile walk the same job list and op programs, so they meet on the same sequence of
+// (extension, chunk, slab).
 __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams P, const TcwArgs A) {
     extern __shared__ __align__(1024) uint8_t wsm[];
-    TcwSm S;
-    S.a = wsm;
-    S.stage0 = smem_u32(wsm + (size_t)128 * W_KP);
-    S.rows = reinterpret_cast<u32 *>(wsm + (size_t)128 * W_KP + (size_t)W_NST * W_STG);
-    uint4 *ep1 = reinterpret_cast<uint4 *>(S.rows + W_ROWS);
+    __shared__ u32 tslot;
+    const u32 tid = threadIdx.x, warp = tid / 32;
+    uint8_t *stages = wsm + (size_t)TCW_TILES * W_ABYTES;
+    uint4 *ep1 = reinterpret_cast<uint4 *>(stages + (size_t)TCW_TILES * W_NST * W_STG);
     uint2 *ep2 = reinterpret_cast<uint2 *>(ep1 + K);
     u32 *sig = reinterpret_cast<u32 *>(ep2 + K);
-    S.ep1 = ep1;
-    S.ep2 = ep2;
-    S.sig = sig;
     u64 *bars = reinterpret_cast<u64 *>(((uintptr_t)(sig + 2 * K) + 7) & ~(uintptr_t)7);
-    u32 *tslot = reinterpret_cast<u32 *>(bars + 2 * W_NST + 5);
-    S.bar = smem_u32(bars);
-    const u32 tid = threadIdx.x, warp = tid / 32;
+    // role: compute warps 0 .. W_CW-1 (tile = warp / (4 W_HV), half = (warp / 4) % W_HV; the warp's TMEM lane quadrant
+    // is warp % 4), then per tile a producer warp and an MMA warp (lane 0 works)
+    const u32 tile = warp < W_CW ? warp / (4 * W_HV) : (warp - W_CW) % TCW_TILES;
+    TcwTile T;
+    T.a = wsm + (size_t)tile * W_ABYTES;
+    T.stage0 = smem_u32(stages + (size_t)tile * W_NST * W_STG);
+    T.bar = smem_u32(bars + tile * W_NBAR);
+    T.tacc = tile * W_TCOLS;
     const WideLayout WL = wide_layout(K);
     for (u32 j = tid; j < K; j += W_THREADS) {
         ep1[j] = make_uint4(__ldg(A.wtab + WL.mm + K + j), __ldg(A.wtab + WL.minv + K + j), __ldg(A.wtab + WL.xw + j),
@@ -507,34 +788,36 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
         sig[j] = __ldg(P.ctx[0] + A.cxw + wide_cx_sig(K) + j);
         sig[K + j] = __ldg(P.ctx[1] + A.cxw + wide_cx_sig(K) + j);
     }
-    if (tid == 0) {
+    if (tid < TCW_TILES) {
+        TcwTile U;
+        U.bar = smem_u32(bars + tid * W_NBAR);
         for (u32 s = 0; s < W_NST; s++) {
-            w_mbar_init(S.full(s), 1);
-            w_mbar_init(S.empty(s), 1);
+            w_mbar_init(U.full(s), 1);
+            w_mbar_init(U.empty(s), 1);
         }
-        for (u32 b = 0; b < 2; b++) {
-            w_mbar_init(S.accf(b), 1);
-            w_mbar_init(S.acce(b), 4);
-        }
-        w_mbar_init(S.aready(), 128);
+        w_mbar_init(U.accf(), 1);
+        w_mbar_init(U.acce(), 4 * W_HV);
+        w_mbar_init(U.aready(), 128 * W_HV);
     }
-    if (warp == 5) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(512));
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const u32 tmem = *tslot;
-    const u32 J = A.jobs;
+    const u32 tmem = tslot;
+    const u32 J = A.jobs, stride = gridDim.x * TCW_TILES;
+    const u32 first = blockIdx.x * TCW_TILES + tile;
 
-    if (warp == 4) {                                  // ---- producer
+    if (warp >= W_CW && warp < W_CW + TCW_TILES) {    // ---- producer of `tile`
         if ((tid & 31) == 0) {
             TcwProducer pr;
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pr.pol));
+            pr.tr.init(A.trace, tile, 2);
 #pragma unroll 1
-            for (u32 t = blockIdx.x; t < J; t += gridDim.x) {
+            for (u32 t = first; t < J; t += stride) {
                 const u32 sel = t / P.ctas0;
                 const uint8_t *be1 = reinterpret_cast<const uint8_t *>((sel ? P.ctx[1] : P.ctx[0]) + A.be1w);
                 const u64 *prog = sel ? P.prog[1] : P.prog[0];
@@ -542,50 +825,55 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
 #pragma unroll 1
                 for (u32 s = 0; s < nops; s++) {
                     const u32 fl = (u32)__ldg(prog + s) & 0xFF;
-                    if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) pr.ext(S, TCW_TRN, A.kimg + tcw_img_off(K, TCW_TRN));
+                    if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) pr.ext(T, TCW_TRN, A.kimg + tcw_img_off(K, TCW_TRN));
                     if (!(fl & OPF_NOMUL)) {
-                        pr.ext(S, TCW_BE1, be1);
-                        pr.ext(S, TCW_BE2, A.kimg + tcw_img_off(K, TCW_BE2));
+                        pr.ext(T, TCW_BE1, be1);
+                        pr.ext(T, TCW_BE2, A.kimg + tcw_img_off(K, TCW_BE2));
                     }
                 }
-                pr.ext(S, TCW_EXT, A.kimg + tcw_img_off(K, TCW_EXT));
+                pr.ext(T, TCW_EXT, A.kimg + tcw_img_off(K, TCW_EXT));
             }
         }
-    } else if (warp == 5) {                           // ---- MMA issuer
+    } else if (warp >= W_CW + TCW_TILES) {            // ---- MMA issuer of `tile`
         if ((tid & 31) == 0) {
             TcwMma mm;
             mm.tmem = tmem;
+            mm.tr.init(A.trace, tile, 1);
 #pragma unroll 1
-            for (u32 t = blockIdx.x; t < J; t += gridDim.x) {
+            for (u32 t = first; t < J; t += stride) {
                 const u32 sel = t / P.ctas0;
                 const u64 *prog = sel ? P.prog[1] : P.prog[0];
                 const u32 nops = sel ? P.nops[1] : P.nops[0];
 #pragma unroll 1
                 for (u32 s = 0; s < nops; s++) {
                     const u32 fl = (u32)__ldg(prog + s) & 0xFF;
-                    if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) mm.ext(S, TCW_TRN);
+                    if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) mm.ext(T, TCW_TRN);
                     if (!(fl & OPF_NOMUL)) {
-                        mm.ext(S, TCW_BE1);
-                        mm.ext(S, TCW_BE2);
+                        mm.ext(T, TCW_BE1);
+                        mm.ext(T, TCW_BE2);
                     }
                 }
-                mm.ext(S, TCW_EXT);
+                mm.ext(T, TCW_EXT);
             }
         }
-    } else {                                          // ---- compute warps
-        TcwCompute cw{S, tmem, (tid & ~31u) << 16, tid, S.a + (tid / 8) * W_SBOA + (tid % 8) * 16};
+    } else {                                          // ---- compute warps of `tile`
+        const u32 m = (warp % 4) * 32 + (tid & 31), h = (warp / 4) % W_HV;
+        uint2 *xch = reinterpret_cast<uint2 *>(bars + TCW_TILES * W_NBAR) + tile * 256;
+        TcwCompute cw{T, ep1, ep2, sig, tmem + ((warp % 4) * 32u << 16), T.tacc + W_NCMAX, m, h,
+                      T.a + (m / 8) * W_SBOA + (m % 8) * 16, xch, 1 + tile};
+        cw.tr.init(A.trace, tile, 0);
 #pragma unroll 1
-        for (u32 t = blockIdx.x; t < J; t += gridDim.x) {
+        for (u32 t = first; t < J; t += stride) {
             cw.sel = t / P.ctas0;
             cw.cx = cw.sel ? P.ctx[1] : P.ctx[0];
-            const u32 jl = (t - cw.sel * P.ctas0) * 128 + tid;
+            const u32 jl = (t - cw.sel * P.ctas0) * 128 + m;
             cw.job(P, jl, jl < P.count);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 #endif  // MR_K == 97 || MR_K == 129

@@ -45,7 +45,7 @@ for bits, E in ((3072, 65537), (4096, 65537), (3072, None), (4096, None)):
     N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
     L = bits // 32
     E = E or (rng.getrandbits(bits) | (1 << (bits - 1)))
-    count = 65536 if E == 65537 else 16384
+    count = 65536 if E == 65537 else 37888
     xs = np.ascontiguousarray(mr.ints_to_limbs([rng.randrange(N) for _ in range(256)], L))
     xs = np.tile(xs, (count // 256, 1))
     ctx = mr.RnsContext(N, L)
