@@ -339,7 +339,10 @@ class Encrypt(Workload):
 
     def work(self):
         k = self.k or (self.key["n"].bit_length() // 32 + 1)
-        return 0, 2 * per_mm(k) * self.mm, 2 * per_mm(k) * self.mm
+        # k = 97 / 129 run on the tensor-core wide kernel (base extensions on tcgen05) unless it is switched off
+        tensor = 2 * 16 * 2 * k * (k + 1) * self.mm if tcw_enabled() else 0
+        elementwise = 2 * (6 * k + 4) * self.mm if tcw_enabled() else 2 * per_mm(k) * self.mm
+        return tensor, elementwise, 2 * per_mm(k) * self.mm
 
 
 class MillerRabin(Workload):
@@ -773,12 +776,18 @@ def roofline(wl: Workload, n_loc: int, launch, clocks, world, step_ms: float):
             "imad_eq_per_unit": all_ops}
 
 
+def tcw_enabled():
+    """the library's routing for k = 97 / 129 (mr_host.cpp tcw_enabled): tensor-core wide kernel unless switched off"""
+    return os.environ.get("MR_RNS_IMAD_ONLY", "0") != "1" and os.environ.get("MR_RNS_TCW", "1") != "0"
+
+
 def base_extension(wl):
     """which kernel family runs the workload's base extensions (the library routes by k: k <= 65 tensor
-    path unless MR_RNS_IMAD_ONLY=1; k >= 97 the wide kernels)"""
+    path unless MR_RNS_IMAD_ONLY=1; k = 97 / 129 the tensor-core wide kernel unless MR_RNS_TCW=0)"""
     k = getattr(wl, "k", None) or 33
     if k >= 97:
-        return "imad (k_modexp_wide, channels on threads)"
+        return ("tcgen05-i8 (k_modexp_tcw: base extensions and conversions on the tensor cores, images streamed by "
+                "bulk copy)") if tcw_enabled() else "imad (k_modexp_wide, channels on threads)"
     return "imad" if os.environ.get("MR_RNS_IMAD_ONLY", "0") == "1" else "tcgen05-i8"
 
 
@@ -786,6 +795,8 @@ def kernel_name(wl):
     if isinstance(wl, MillerRabin):
         return "k_mr_rounds_tc (Miller-Rabin rounds, k=33, tcgen05 base extensions)"
     if isinstance(wl, Encrypt):
+        if tcw_enabled():
+            return "k_modexp_tcw (k=97, two 128-message tiles per SM, tcgen05 i8 contractions, TMA-streamed images)"
         return "k_modexp_wide (k=97 channels-on-threads, IMAD base extensions)"
     if os.environ.get("MR_RNS_IMAD_ONLY", "0") == "1":
         return "k_modexp (CRT half-ladders, IMAD-pipe base extensions)"

@@ -1103,7 +1103,8 @@ static int launch_ladders_tcw(mr_rns_ctx *const *ctxs, const DevProg *progs, int
                               const KernelSet &ks) {
     const mr_rns_ctx *c0 = ctxs[0];
     cudaStream_t st = (cudaStream_t)stream;
-    const u32 ctas0 = (u32)((count + 127) / 128);
+    u32 ctas0 = (u32)((count + 127) / 128);
+    if (TCW_LOCK) ctas0 += ctas0 & 1u;        // lockstep tiles take job pairs of one context
     const u32 jobs = ctas0 * (u32)nctx;
     const u32 jobs_total = ctas0 * 128 * (u32)nctx;
     int sms = 148;

@@ -216,8 +216,21 @@ __host__ __device__ constexpr u32 tcw_nout(u32 k, u32 e) {
     return e == TCW_BE1 ? k + 1 : e == TCW_BE2 ? k : e == TCW_TRN ? 2 * k : k + 1;
 }
 constexpr u32 TCW_TILES = 2;
-// largest outputs per chunk (multiple of 4) whose columns fit a tile's accumulator buffer
-__host__ __device__ constexpr u32 tcw_ocmax(u32 k) { return ((512 / TCW_TILES - tcw_bsw(k)) & ~15u) / 4 & ~3u; }
+// MR_TCW_LOCK = 1: the two tiles of a CTA run jobs of the same context in lockstep and share ONE stream of B slabs
+// (each slab feeds both tiles' MMAs: half the L2 traffic); 0: independent tiles, one stream each
+#ifndef MR_TCW_LOCK
+#define MR_TCW_LOCK 0
+#endif
+constexpr bool TCW_LOCK = MR_TCW_LOCK != 0;
+// largest outputs per chunk (multiple of 4) whose columns fit a tile's accumulator buffer (MR_TCW_OCCAP: a smaller cap
+// trades MMA width for epilogue registers; host and device must be built with the same value)
+#ifndef MR_TCW_OCCAP
+#define MR_TCW_OCCAP 64
+#endif
+__host__ __device__ constexpr u32 tcw_ocmax(u32 k) {
+    return (((512 / TCW_TILES - tcw_bsw(k)) & ~15u) / 4 & ~3u) < MR_TCW_OCCAP ? (((512 / TCW_TILES - tcw_bsw(k)) & ~15u) / 4 & ~3u)
+                                                                             : MR_TCW_OCCAP;
+}
 __host__ __device__ constexpr u32 tcw_nchunks(u32 k, u32 e) { return (tcw_nout(k, e) + tcw_ocmax(k) - 1) / tcw_ocmax(k); }
 __host__ __device__ constexpr u32 tcw_oc(u32 k, u32 e) {                                 // outputs per chunk (last: rest)
     return ((tcw_nout(k, e) + tcw_nchunks(k, e) - 1) / tcw_nchunks(k, e) + 3) & ~3u;

@@ -39,10 +39,12 @@ static_assert(W_KC * 4 >= K + 2, "A row must hold B' (k words), α' (word k) and
 constexpr u32 W_STG = tcw_stage_bytes(K);
 constexpr u32 W_ABYTES = 128 * W_KP;
 constexpr size_t W_FIXED = (size_t)TCW_TILES * W_ABYTES + 16 * K + 8 * K + 8 * K + 512 + TCW_TILES * 2048;
-constexpr u32 W_NST_FIT = (u32)((232448 - W_FIXED) / (TCW_TILES * W_STG));
-constexpr u32 W_NST = W_NST_FIT > 6 ? 6 : W_NST_FIT;  // pipeline stages per tile
+constexpr u32 W_RINGS = TCW_LOCK ? 1 : TCW_TILES;     // streams of B slabs per CTA
+constexpr u32 W_NST_FIT = (u32)((232448 - W_FIXED) / (W_RINGS * W_STG));
+constexpr u32 W_NST = W_NST_FIT > 8 ? 8 : W_NST_FIT;  // pipeline stages per stream
 static_assert(W_NST >= 2, "tensor wide kernel: fewer than two B stages per tile fit shared memory");
-constexpr size_t W_SMEM = W_FIXED + (size_t)TCW_TILES * W_NST * W_STG;
+constexpr size_t W_SMEM = W_FIXED + (size_t)W_RINGS * W_NST * W_STG;
+constexpr u32 W_SUB = TCW_LOCK ? TCW_TILES : 1;       // tiles served by one stream (one producer, one MMA issuer)
 #ifndef MR_TCW_HALVES
 #define MR_TCW_HALVES 1       // compute warps per TMEM lane quadrant and tile (2: each takes alternate channel groups)
 #endif
@@ -246,6 +248,7 @@ struct TcwMma {
     u32 st = 0, fph = 0, aph = 0, eph = 0;
     u32 tmem;
     WTrace tr;
+    u32 sa1 = 0, td1 = 0;                  // lockstep: the second tile's A tile and accumulator
     __device__ void ext(const TcwTile &T, u32 e) {
         w_mbar_wait(T.aready(), aph);          // the A rows of all 128 messages are written (and proxy-fenced)
         aph ^= 1u;
@@ -267,14 +270,17 @@ struct TcwMma {
                 tr((e << 4) | 3);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const u32 sb = T.stage0 + st * W_STG;
+#pragma unroll
+                for (u32 u = 0; u < W_SUB; u++) {
 #pragma unroll 1
-                for (u32 j = 0; j < steps; j++) {
-                    const u64 da = w_desc(sa + (4 * s + j) * 256, W_SBOA), db = w_desc(sb + j * 256, steps * 256);
-                    const u32 accum = (s | j) ? 1u : 0u;
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(td),
-                                 "l"(da), "l"(db), "r"(idesc), "r"(accum)
-                                 : "memory");
+                    for (u32 j = 0; j < steps; j++) {
+                        const u64 da = w_desc((u ? sa1 : sa) + (4 * s + j) * 256, W_SBOA), db = w_desc(sb + j * 256, steps * 256);
+                        const u32 accum = (s | j) ? 1u : 0u;
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(u ? td1 : td),
+                                     "l"(da), "l"(db), "r"(idesc), "r"(accum)
+                                     : "memory");
+                    }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(T.empty(st))
                              : "memory");
@@ -768,7 +774,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
     __shared__ u32 tslot;
     const u32 tid = threadIdx.x, warp = tid / 32;
     uint8_t *stages = wsm + (size_t)TCW_TILES * W_ABYTES;
-    uint4 *ep1 = reinterpret_cast<uint4 *>(stages + (size_t)TCW_TILES * W_NST * W_STG);
+    uint4 *ep1 = reinterpret_cast<uint4 *>(stages + (size_t)W_RINGS * W_NST * W_STG);
     uint2 *ep2 = reinterpret_cast<uint2 *>(ep1 + K);
     u32 *sig = reinterpret_cast<u32 *>(ep2 + K);
     u64 *bars = reinterpret_cast<u64 *>(((uintptr_t)(sig + 2 * K) + 7) & ~(uintptr_t)7);
@@ -776,9 +782,10 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
     // is warp % 4), then per tile a producer warp and an MMA warp (lane 0 works)
     const u32 tile = warp < W_CW ? warp / (4 * W_HV) : (warp - W_CW) % TCW_TILES;
     TcwTile T;
+    const u32 ring = TCW_LOCK ? 0u : tile;
     T.a = wsm + (size_t)tile * W_ABYTES;
-    T.stage0 = smem_u32(stages + (size_t)tile * W_NST * W_STG);
-    T.bar = smem_u32(bars + tile * W_NBAR);
+    T.stage0 = smem_u32(stages + (size_t)ring * W_NST * W_STG);
+    T.bar = smem_u32(bars + ring * W_NBAR);
     T.tacc = tile * W_TCOLS;
     const WideLayout WL = wide_layout(K);
     for (u32 j = tid; j < K; j += W_THREADS) {
@@ -788,7 +795,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
         sig[j] = __ldg(P.ctx[0] + A.cxw + wide_cx_sig(K) + j);
         sig[K + j] = __ldg(P.ctx[1] + A.cxw + wide_cx_sig(K) + j);
     }
-    if (tid < TCW_TILES) {
+    if (tid < W_RINGS) {
         TcwTile U;
         U.bar = smem_u32(bars + tid * W_NBAR);
         for (u32 s = 0; s < W_NST; s++) {
@@ -796,8 +803,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
             w_mbar_init(U.empty(s), 1);
         }
         w_mbar_init(U.accf(), 1);
-        w_mbar_init(U.acce(), 4 * W_HV);
-        w_mbar_init(U.aready(), 128 * W_HV);
+        w_mbar_init(U.acce(), 4 * W_HV * W_SUB);
+        w_mbar_init(U.aready(), 128 * W_HV * W_SUB);
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
@@ -808,11 +815,14 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem = tslot;
+    // independent tiles: tile u of CTA b walks jobs b TILES + u + i gridDim.x TILES; lockstep: the producer and the
+    // MMA issuer walk the job PAIRS (jobs 2p, 2p + 1 share a context: the host pads ctas0 to even) and tile u takes 2p + u
     const u32 J = A.jobs, stride = gridDim.x * TCW_TILES;
     const u32 first = blockIdx.x * TCW_TILES + tile;
+    const bool role_on = !TCW_LOCK || tile == 0 || warp < W_CW;   // lockstep: tile 1's producer / MMA warps idle
 
     if (warp >= W_CW && warp < W_CW + TCW_TILES) {    // ---- producer of `tile`
-        if ((tid & 31) == 0) {
+        if ((tid & 31) == 0 && role_on) {
             TcwProducer pr;
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pr.pol));
             pr.tr.init(A.trace, tile, 2);
@@ -835,9 +845,11 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
             }
         }
     } else if (warp >= W_CW + TCW_TILES) {            // ---- MMA issuer of `tile`
-        if ((tid & 31) == 0) {
+        if ((tid & 31) == 0 && role_on) {
             TcwMma mm;
             mm.tmem = tmem;
+            mm.sa1 = smem_u32(wsm + W_ABYTES);
+            mm.td1 = tmem + W_TCOLS;
             mm.tr.init(A.trace, tile, 1);
 #pragma unroll 1
             for (u32 t = first; t < J; t += stride) {
