@@ -80,6 +80,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_PF_L1
 #define MR_PF_L1 0          // A/B hook: prefetch the next window-table operand into L1 instead of L2
 #endif
+#ifndef MR_SIG_PF
+#define MR_SIG_PF 8         // Miller-Rabin: per-candidate σ_i / c2_j loaded this many channels / outputs ahead
+#endif
 
 // 96-bit multiply-accumulate (lo, mid, hi) += x * y; lowers to IMAD.WIDE.U32 with carry-out + IADD3.X
 __device__ __forceinline__ void mac96(u32 &lo, u32 &mid, u32 &hi, u32 x, u32 y) {
@@ -827,6 +830,12 @@ struct MulTc {
                                         u32 &c1mi, u32 &c1hi, bool sq = SQ) {
         uint8_t *arow = st.arow;
         const u32 *bq = bp;                          // multiplicand channel pointer, advanced by bs
+        // per-thread σ_i (Miller-Rabin: candidate-major rows in L1 / L2) loaded MR_SIG_PF channels ahead, so their
+        // latency runs under the products of the channels before (the loop is unrolled: the ring is registers)
+        constexpr int PF = (!CS::kMerged && CS::kMont) ? MR_SIG_PF : 0;
+        u32 sring[PF > 0 ? PF : 1];
+#pragma unroll
+        for (int t = 0; t < PF; t++) sring[t] = t < K ? cs.sigma(t) : 0u;
 #pragma unroll
         for (int c = 0; c < (K + 3) / 4; c++) {
             uint4 *chunk = reinterpret_cast<uint4 *>(arow + c * 128);
@@ -855,7 +864,14 @@ struct MulTc {
                     } else if constexpr (CS::kMont) {   // ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i
                         const u64 pr = (u64)a * b;
                         const u32 t = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + i), GB(O_MINV + i));
-                        const u64 ps = (u64)t * cs.sigma(i);
+                        u32 sg;
+                        if constexpr (PF > 0) {
+                            sg = sring[i % (PF > 0 ? PF : 1)];
+                            if (i + PF < K) sring[i % (PF > 0 ? PF : 1)] = cs.sigma(i + PF);
+                        } else {
+                            sg = cs.sigma(i);
+                        }
+                        const u64 ps = (u64)t * sg;
                         xi = mont_red((u32)ps, (u32)(ps >> 32), GB(O_MM + i), GB(O_MINV + i));   // lazy digit < 2^32
                         qr += xi * GB(O_A1R + i);
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
@@ -993,6 +1009,13 @@ struct MulTc {
         u32 c2lo = 0, c2mi = 0, c2hi = 0;
         constexpr int NG = TCNT / 4 + (TCNT % 4 ? 1 : 0);
         auto epi1 = [&](int g0) {
+          // Miller-Rabin: the 8 per-candidate c2_j of these outputs load while the TMEM loads are in flight
+          constexpr bool C2PF = !MERGED && CS::kMont && MR_SIG_PF > 0;
+          u32 c2v[C2PF ? 8 : 1];
+          if constexpr (C2PF) {
+#pragma unroll
+            for (int o = 0; o < 8; o++) c2v[o] = 4 * g0 + o < TCNT ? cs.c2(4 * g0 + o) : 0u;
+          }
           u32 vv[2][16];                              // two TMEM loads in flight, one wait
           tmem_ld_pair(t.tmem + lane_base + 16 * g0, g0 + 1 < NG, vv);
           tmem_wait_ld_regs(vv);
@@ -1038,7 +1061,10 @@ struct MulTc {
                         else c1j = s_be[bev_C1(K) + j];
                         const u64 p = (u64)S(st, K + j) * c1j;
                         u32 l2 = (u32)p, m2 = (u32)(p >> 32), h2 = 0;
-                        mac96(l2, m2, h2, q, cs.c2(j));
+                        u32 c2j;
+                        if constexpr (C2PF) c2j = c2v[4 * h + o];
+                        else c2j = cs.c2(j);
+                        mac96(l2, m2, h2, q, c2j);
                         xp = red96(h2, m2, l2, c, 0);
                     }
                     S(st, K + j) = xp;
