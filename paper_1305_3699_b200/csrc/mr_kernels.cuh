@@ -80,6 +80,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_PF_L1
 #define MR_PF_L1 0          // A/B hook: prefetch the next window-table operand into L1 instead of L2
 #endif
+#ifndef MR_TAB_PF
+#define MR_TAB_PF 1         // Miller-Rabin: prefetch each window digit's table entry into L2 at its first squaring
+#endif
 #ifndef MR_SIG_PF
 #define MR_SIG_PF 8         // Miller-Rabin: per-candidate σ_i / c2_j loaded this many channels / outputs ahead
 #endif
@@ -1890,8 +1893,18 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
 #pragma unroll 1
                         for (int c = 0; c < NCH; c++) S(st, c) = tab[c];
                     }
-                    if (sub < w) { sq = true; bp = s_one; bs = 0; }
-                    else {
+                    if (sub < w) {
+                        sq = true; bp = s_one; bs = 0;
+                        if (sub == 0 && MR_TAB_PF) {   // this digit's table entry (HBM: the tables exceed L2) -> L2,
+                            const u32 b0 = dg * w, lw = b0 / 32, bw = b0 % 32;   // under the w squarings before its use
+                            const u32 lo = lw < (u32)K ? dl[(size_t)lw * cnt] : 0u;
+                            const u32 hi = lw + 1 < (u32)K ? dl[(size_t)(lw + 1) * cnt] : 0u;
+                            const u32 *ent = tab + (size_t)(__funnelshift_r(lo, hi, bw) & (E - 1)) * entry;
+#pragma unroll
+                            for (u32 l = 0; l < (NCHP * 4 + 127) / 128; l++)
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(ent + 32 * l));
+                        }
+                    } else {
                         const u32 b0 = dg * w, lw = b0 / 32, bw = b0 % 32;
                         const u32 lo = lw < (u32)K ? dl[(size_t)lw * cnt] : 0u;
                         const u32 hi = lw + 1 < (u32)K ? dl[(size_t)(lw + 1) * cnt] : 0u;
