@@ -178,3 +178,20 @@ def test_forced_equals_compacted_early_exit(torch_cuda, mr):
     assert out[0] == out[1]
     assert out[0][0] == [1 if sympy.isprime(n) else 0 for n in ns]      # 300 planted + the natural primes
     assert all(x == -1 for x, y in zip(out[0][1], out[0][0]) if y == 1)
+
+
+def test_small_candidate_equal_to_base_prime(torch_cuda, mr, orc):
+    """reading R14: a one-limb candidate that IS one of the RNS base primes has no n^-1 mod m_i; the library reports
+    status MR_ERR_NOT_COPRIME with verdict PROBABLY_PRIME (it is a prime).  Other one-limb primes and composites in
+    the same batch are decided normally (verdicts vs the oracle)."""
+    k = k_for(mr, 1)
+    fp = orc.base_primes(2 * k)
+    import sympy
+    other_p = sympy.prevprime(fp[-1] - 1000)                  # a prime below the base, not in it
+    ns = [fp[0], fp[k], fp[2 * k - 1], other_p, 65521 * 65519]   # three base primes, a prime, a semiprime < 2^32
+    bases = [[2, 3, 5]] * len(ns)
+    v, w, s, limbs = gpu_mr(torch_cuda, mr, ns, bases, limbs=1)
+    assert s[:3] == [mr.MR_ERR_NOT_COPRIME] * 3 and v[:3] == [mr.MR_PROBABLY_PRIME] * 3
+    assert s[3] == 0 and v[3] == mr.MR_PROBABLY_PRIME
+    ov, _ = orc.miller_rabin(ns[4], [2, 3, 5], fp)
+    assert s[4] == 0 and v[4] == ov
