@@ -86,6 +86,9 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_TAB_PF
 #define MR_TAB_PF 1         // Miller-Rabin: prefetch each window digit's table entry into L2 at its first squaring
 #endif
+#ifndef MR_MR_EPI_UNROLL
+#define MR_MR_EPI_UNROLL 0  // 1: Miller-Rabin tensor epilogues unrolled with constant-bank operands (A/B: 5 % slower, spills)
+#endif
 #ifndef MR_SIG_PF
 #define MR_SIG_PF 8         // Miller-Rabin: per-candidate σ_i / c2_j loaded this many channels / outputs ahead
 #endif
@@ -1075,7 +1078,7 @@ struct MulTc {
                         w[o] = xp;
                         continue;
                     }
-                    const u32 c = s_be[bev_c(K) + K + j];
+                    const u32 c = (MR_MR_EPI_UNROLL && CS::kMont) ? GB(O_C + K + j) : s_be[bev_c(K) + K + j];
                     fold_hi(lo, hi, c, w33, c33);                  // q̂_j (merged: + Σ term) as w33 + c33·2^32
                     if constexpr (MERGED) {   // t*_j C1_j + (w33 + c33 2^32) <= (2^32-1)(2^32-6) + 2^33 < 2^64: no carry
                         const u64 p = (u64)S(st, K + j) * s_be[bev_C1(K) + j] + (((u64)c33 << 32) | w33);
@@ -1094,7 +1097,7 @@ struct MulTc {
                         xp = red96(h2, m2, l2, c, 0);
                     }
                     S(st, K + j) = xp;
-                    sr += xp * s_be[bev_A2r(K) + j];
+                    sr += xp * ((MR_MR_EPI_UNROLL && CS::kMont) ? GB(O_A2R + j) : s_be[bev_A2r(K) + j]);
                     if (TCNC) mac96(c2lo, c2mi, c2hi, xp, s_a2c[j]);
                     w[o] = xp;
                 }
@@ -1102,7 +1105,7 @@ struct MulTc {
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);   // BE2 operand
           }
         };
-        if constexpr (CS::kScaled && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
+        if constexpr ((CS::kScaled || (MR_MR_EPI_UNROLL && CS::kMont)) && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
 #pragma unroll
             for (int g0 = 0; g0 < NG; g0 += 2) epi1(g0);
         } else {
@@ -1161,14 +1164,14 @@ struct MulTc {
 #endif
                         w[o] = mont_red(lo, hi, e.x, e.y);
                     } else {
-                        w[o] = fold_word(lo, hi, s_be[bev_c(K) + i]);
+                        w[o] = fold_word(lo, hi, (MR_MR_EPI_UNROLL && CS::kMont) ? GB(O_C + i) : s_be[bev_c(K) + i]);
                     }
                 }
             }
             *reinterpret_cast<uint4 *>(arow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
           }
         };
-        if constexpr (CS::kScaled && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
+        if constexpr ((CS::kScaled || (MR_MR_EPI_UNROLL && CS::kMont)) && MR_EPI_UNROLL) {   // constant-bank operands need the unrolled loop
 #pragma unroll
             for (int g0 = 0; g0 < NG; g0 += 2) epi2(g0);
         } else {
@@ -1943,7 +1946,9 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
                 }
             }
             // checks (HAC 4.24): even steps leave the Montgomery domain and compare, odd steps square
-            bool need = true, pass = false;
+            // lanes without a live candidate (setup verdict, tail lanes) take no part in the checks: their s is not
+            // set (a stale s once kept a whole tile squaring forever)
+            bool need = pending || (P.forced && was_live), pass = false;
             u32 jj = 0;
 #pragma unroll 1
             for (u32 v = 0;; v++) {

@@ -49,6 +49,9 @@ constexpr u32 W_SUB = TCW_LOCK ? TCW_TILES : 1;       // tiles served by one str
 #define MR_TCW_HALVES 1       // compute warps per TMEM lane quadrant and tile (2: each takes alternate channel groups)
 #endif
 constexpr u32 W_HV = MR_TCW_HALVES;
+#ifndef MR_TCW_CHAN_PIPE
+#define MR_TCW_CHAN_PIPE 0    // 1: next group's operand loads under the current group's products (A/B: 9 % slower, spills)
+#endif
 constexpr u32 W_CW = 4 * W_HV * TCW_TILES;            // compute warps
 constexpr u32 W_THREADS = 32 * (W_CW + 2 * TCW_TILES);   // + per tile a producer warp and an MMA warp (one lane each:
                                                          // two roles in one warp would sleep on each other's waits)
@@ -482,6 +485,59 @@ struct TcwCompute {
         for (u32 q = 0; q < (N + 3) / 4; q++) ac(c0 / 4 + q) = make_uint4(xi[4 * q], xi[4 * q + 1], xi[4 * q + 2], xi[4 * q + 3]);
     }
 
+    // 6.1 / 6.2 over the full 16-channel groups with the TMEM and A-row loads of group g+1 issued under the products of
+    // group g (one warp per lane quadrant: W_HV = 1)
+    template <bool SQ>
+    __device__ __forceinline__ void chan_pipe(const u32 *bp, u32 bs_, const u32 *sg) {
+        u32 r[16], xa[16];
+        auto load_xa = [&](u32 g) {
+#pragma unroll
+            for (u32 q = 0; q < 4; q++) {
+                const uint4 v = ac(4 * g + q);
+                xa[4 * q] = v.x; xa[4 * q + 1] = v.y; xa[4 * q + 2] = v.z; xa[4 * q + 3] = v.w;
+            }
+        };
+        w_tmem_ld16(tb(bs), r);
+        load_xa(0);
+#pragma unroll 1
+        for (u32 g = 0; g < K / 16; g++) {
+            w_tmem_wait(r);
+            u32 u[16], v[16];                        // this group's B residues and B' words (then ξ, t*)
+#pragma unroll
+            for (u32 t = 0; t < 16; t++) { u[t] = r[t]; v[t] = xa[t]; }
+            u32 b1[16], b2[16];
+            if (!SQ) {
+                const u32 *b = bp + (size_t)(16 * g) * bs_;
+#pragma unroll
+                for (u32 t = 0; t < 16; t++) {
+                    b1[t] = __ldcg(b + (size_t)t * bs_);
+                    b2[t] = __ldcg(b + (size_t)(K + t) * bs_);
+                }
+            }
+            if (g + 1 < K / 16) {                    // next group's operands in flight
+                w_tmem_ld16(tb(bs + 16 * (g + 1)), r);
+                load_xa(g + 1);
+            }
+            const uint2 *e2 = ep2 + 16 * g;
+            const uint4 *e1 = ep1 + 16 * g;
+            const u32 *sgg = sg + 16 * g;
+#pragma unroll
+            for (u32 t = 0; t < 16; t++) {
+                const uint2 mm = e2[t];
+                const u64 pr = mulw(u[t], SQ ? u[t] : b1[t]);
+                const u32 tt = mont_red((u32)pr, (u32)(pr >> 32), mm.x, mm.y);
+                const u64 ps = mulw(tt, sgg[t]);
+                u[t] = mont_red((u32)ps, (u32)(ps >> 32), mm.x, mm.y);            // ξ_i
+                const uint4 c1 = e1[t];
+                const u64 pp = mulw(v[t], SQ ? v[t] : b2[t]);
+                v[t] = mont_red((u32)pp, (u32)(pp >> 32), c1.x, c1.y);            // t*_j
+            }
+            w_tmem_st16(tb(bs + 16 * g), v);
+#pragma unroll
+            for (u32 q = 0; q < 4; q++) ac(4 * g + q) = make_uint4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+        }
+    }
+
     // α' and r_r from both halves' partial sums (Σ ξ'_j |M'_j|_{2^32} over each half's outputs; r_r from its owner)
     __device__ uint2 exchange(u32 sr, u32 rr) {
         if (W_HV == 1) { sync(); return make_uint2(sr, rr); }
@@ -500,13 +556,17 @@ struct TcwCompute {
         const u32 ar = aw(K + 1);
         if (!SQ) br = __ldcg(bp + (size_t)(2 * K) * bs_);
         // ---- 6.1 / 6.2: this half's 16-channel groups
+        if (W_HV == 1 && MR_TCW_CHAN_PIPE) {
+            chan_pipe<SQ>(bp, bs_, sg);
+        } else {
 #pragma unroll 1
-        for (u32 g = h; g < K / 16; g += W_HV) {
-            if (W_HV == 1) {
-                chan_group<SQ, 16>(16 * g, bp, bs_, sg);
-            } else {
-                chan_group<SQ, 8>(16 * g, bp, bs_, sg);
-                chan_group<SQ, 8>(16 * g + 8, bp, bs_, sg);
+            for (u32 g = h; g < K / 16; g += W_HV) {
+                if (W_HV == 1) {
+                    chan_group<SQ, 16>(16 * g, bp, bs_, sg);
+                } else {
+                    chan_group<SQ, 8>(16 * g, bp, bs_, sg);
+                    chan_group<SQ, 8>(16 * g + 8, bp, bs_, sg);
+                }
             }
         }
         static_assert(K % 16 <= 8, "tail channels fit one 8-channel group");
