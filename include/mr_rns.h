@@ -129,7 +129,9 @@ int mr_rsa_decrypt_batch(const mr_rsa_priv *priv, const uint32_t *d_c, uint32_t 
  *  a Miller-Rabin test with a user-parameterized number of iterations", §3.2; HAC 4.24).
  * d_n: DEVICE [count][limbs] candidates; d_bases: DEVICE [count][rounds][limbs], each in [2, n-2]
  *      (bases are inputs, reading R13).
- * k: channels (0 = auto from limbs; candidates up to 128 limbs, else MR_ERR_CAPACITY).
+ * k: channels (0 = auto from limbs; candidates up to 504 limbs = 16,128 bits, else MR_ERR_CAPACITY): k <= 65 tensor-core
+ *    rounds, 97 / 129 the per-k IMAD kernel, 257 / 505 (4,097 .. 16,128-bit candidates) the channels-on-threads kernels
+ *    with a per-candidate setup.
  * d_verdict: DEVICE uint8 [count] = MR_COMPOSITE |
  * MR_PROBABLY_PRIME | MR_FACTOR (n > 2^32 divisible by a prime of B ∪ B', R14).
  * d_witness_round: DEVICE int16 [count] or NULL: first round that proved compositeness, else -1.

@@ -37,6 +37,14 @@ int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u
 int wide_messages_per_cta_lanes();
 int launch_modexp_wide_lanes(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream);
 int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream);
+int launch_mr_wide(const u32 *d_wide_tab, u32 k, u32 *d_pcw, u32 *d_scr, const u32 *d_n, const u32 *d_bases, u32 count,
+                   u32 limbs, u32 rounds, u32 window, u32 forced, u32 *d_table, uint8_t *d_verdict, int16_t *d_witness,
+                   int32_t *d_status, void *stream);
+size_t mr_wide_table_words(u32 k, u32 window, u32 count);
+int launch_mr_wide_setup(const u32 *d_wide_tab, u32 k, u32 *d_pcw, u32 *d_scr, const u32 *d_n, u32 count, u32 limbs,
+                         uint8_t *d_verdict, void *stream);
+size_t mr_wide_pcw_words(u32 k, u32 count);
+size_t mr_wide_scr_words(u32 k, u32 count);
 
 static const KernelSet &kernel_set_for(int k) {
     static std::vector<KernelSet> sets = {kernels_k1(),  kernels_k2(),  kernels_k3(),  kernels_k5(), kernels_k9(),
@@ -393,6 +401,16 @@ static std::vector<u32> build_wide_table(const Base &b) {
     for (int j = 0; j < k; j++)
         for (int l = 0; l <= k; l++) t[W.mpl + wch_at(j, l, k + 1)] = f[L.MpL + j * (k + 1) + l];
     for (int l = 0; l <= k; l++) t[W.nmp + l] = f[L.NMp + l];
+    // Miller-Rabin (per-candidate n): unmerged BE1, the per-k vectors the setup needs, M limbs, the image of 1
+    for (int i = 0; i < k; i++)
+        for (int j = 0; j < k; j++) t[W.a1w + wch_at(i, j, k)] = mulm(f[L.A1 + i * k + j], t[W.r32 + k + j], b.Bp[j]);
+    for (int j = 0; j < k; j++) {
+        t[W.lam + j] = b.lambda[j];
+        t[W.mu + j] = b.mu[j];
+    }
+    for (int i = 0; i < k; i++) t[W.mis + i] = b.Mi_self[i];
+    for (int l = 0; l <= k; l++) t[W.ml + l] = f[L.ML + l];
+    for (int c = 0; c < 2 * k + 1; c++) t[W.one + c] = f[L.ONE + c];
     return t;
 }
 static std::map<std::pair<int, int>, DevBase> g_devbases;
@@ -1482,7 +1500,7 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
             if (kmin < 0) return MR_ERR_ARG;
         }
         kk = auto_k(top, kmin);
-        if (kk < 0 || is_wide((u32)kk)) return MR_ERR_CAPACITY;   // Miller-Rabin: candidates up to 4096 bits
+        if (kk < 0) return MR_ERR_CAPACITY;
         if ((int)limbs > kk - 1) return MR_ERR_CAPACITY;
         int rc = ensure_device_base(kk, device, &d_pow, &d_be);
         if (rc != MR_OK) return rc;
@@ -1490,6 +1508,27 @@ int mr_internal_miller_rabin(const uint32_t *d_n, size_t limbs, size_t count, co
     }
     if (cudaSetDevice(device) != cudaSuccess) return MR_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
+    if (is_wide((u32)kk)) {   // 4,097 .. 16,128-bit candidates: channels-on-threads kernels (mr_wide.cu)
+        u32 *d_pcw = nullptr, *d_scr = nullptr, *d_wt = nullptr;
+        const u32 c = (u32)count, kw = (u32)kk;
+        if (cudaMallocAsync(&d_pcw, mr_wide_pcw_words(kw, c) * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+        if (cudaMallocAsync(&d_scr, mr_wide_scr_words(kw, c) * 4, st) != cudaSuccess ||
+            cudaMallocAsync(&d_wt, mr_wide_table_words(kw, (u32)window, c) * 4, st) != cudaSuccess) {
+            cudaFreeAsync(d_pcw, st);
+            if (d_scr) cudaFreeAsync(d_scr, st);
+            return MR_ERR_NOMEM;
+        }
+        int rc = timed_launch(2, st, [&] {
+                     return launch_mr_wide(db.d_wide, kw, d_pcw, d_scr, d_n, d_bases, c, (u32)limbs, (u32)rounds,
+                                           (u32)window, (u32)forced, d_wt, d_verdict, d_witness_round, d_status, stream);
+                 }) == 0
+                     ? MR_OK
+                     : MR_ERR_CUDA;
+        cudaFreeAsync(d_pcw, st);
+        cudaFreeAsync(d_scr, st);
+        cudaFreeAsync(d_wt, st);
+        return rc;
+    }
     const size_t nch = 2 * (size_t)kk + 1;
     const KernelSet &ks = kernel_set_for(kk);
     const bool tc = db.d_tcb1u && ks.launch_modexp_tc && ks.mr_tiles > 0 && tensor_path_enabled();
@@ -1610,6 +1649,27 @@ int mr_internal_tcw_image(int k, int e, const uint32_t *modulus, size_t limbs, u
     }
     if (out) memcpy(out, img.data(), std::min(cap, img.size()));
     return (int)img.size();
+}
+
+// test hook: the wide Miller-Rabin setup alone (k = 257 / 505): per-candidate rows wmr_* into d_pcw
+// (DEVICE, mr_wide_pcw_words), for checking σ, c2, R^2, s, d against their definitions
+int mr_internal_mr_wide_setup(const uint32_t *d_n, size_t limbs, size_t count, int k, uint32_t *d_pcw, uint8_t *d_verdict,
+                              int device) {
+    if (!is_wide((u32)k) || !d_n || !d_pcw || !d_verdict) return MR_ERR_ARG;
+    const u32 *d_pow = nullptr, *d_be = nullptr;
+    DevBase db;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int rc = ensure_device_base(k, device, &d_pow, &d_be);
+        if (rc != MR_OK) return rc;
+        db = g_devbases[std::make_pair(device, k)];
+    }
+    u32 *d_scr = nullptr;
+    if (cudaMalloc(&d_scr, mr_wide_scr_words((u32)k, (u32)count) * 4) != cudaSuccess) return MR_ERR_NOMEM;
+    const int rc = launch_mr_wide_setup(db.d_wide, (u32)k, d_pcw, d_scr, d_n, (u32)count, (u32)limbs, d_verdict, nullptr);
+    cudaDeviceSynchronize();
+    cudaFree(d_scr);
+    return rc == 0 ? MR_OK : MR_ERR_CUDA;
 }
 
 // test hook: the tensor-core wide kernel for k = 97 / 129 (§4k): 1 = on (default), 0 = the IMAD wide kernel,

@@ -160,6 +160,11 @@ struct WideLayout {
     u32 pow;                  // chunked [k][2k] |2^(32 l) 2^32|_{m_c} (B' × λ_j)
     u32 mpl;                  // chunked [k][k+1] M'_j limbs
     u32 nmp;                  // [k+1] 2^(32(k+1)) - M' limbs
+    // Miller-Rabin (per-candidate moduli, unmerged BE1; mr_wide.cu k_mr_*_wide):
+    u32 a1w;                  // chunked [k][k] row i, column j: |M_i|_{m'_j} 2^32 mod m'_j
+    u32 lam, mu, mis;         // [k] λ_j = |M'_j^-1|_{m'_j}, μ_j = |M^-1|_{m'_j}, |M_i|_{m_i}
+    u32 ml;                   // [k+1] M limbs
+    u32 one;                  // [2k+1] RNS image of 1 (B' in ξ-form)
     u32 words;
 };
 __host__ __device__ constexpr WideLayout wide_layout(u32 k) {
@@ -176,7 +181,13 @@ __host__ __device__ constexpr WideLayout wide_layout(u32 k) {
     w.pow = w.a2w + wch_words(k, k);
     w.mpl = w.pow + wch_words(k, 2 * k);
     w.nmp = w.mpl + wch_words(k, k + 1);
-    w.words = w.nmp + k + 1;
+    w.a1w = (w.nmp + k + 1 + 3) & ~3u;
+    w.lam = w.a1w + wch_words(k, k);
+    w.mu = w.lam + k;
+    w.mis = w.mu + k;
+    w.ml = w.mis + k;
+    w.one = w.ml + k + 1;
+    w.words = w.one + 2 * k + 1;
     return w;
 }
 // per-context wide section, after the cx block: σ_i 2^64 mod m_i [k], then A1'[i][j] 2^32 mod m'_j chunked
@@ -185,6 +196,17 @@ __host__ __device__ constexpr u32 wide_cx_sig(u32 k) { return 0; }
 __host__ __device__ constexpr u32 wide_cx_a1(u32 k) { return (k + 3) & ~3u; }
 __host__ __device__ constexpr u32 wide_cx_words(u32 k) { return wide_cx_a1(k) + wch_words(k, k); }
 __host__ __device__ constexpr bool is_wide(u32 k) { return k > 129; }
+// Per-candidate rows of the wide Miller-Rabin kernels (row r of candidate i at pcw[r * count + i]):
+__host__ __device__ constexpr u32 wmr_sig(u32 k) { return 0; }            // [k]    σ_i 2^64 mod m_i
+__host__ __device__ constexpr u32 wmr_c2(u32 k) { return k; }             // [k]    |n M^-1 λ_j| 2^32 mod m'_j
+__host__ __device__ constexpr u32 wmr_r2(u32 k) { return 2 * k; }         // [2k+1] RNS image of M^2 mod n
+__host__ __device__ constexpr u32 wmr_nminv(u32 k) { return 4 * k + 1; }  // [1]    n M^-1 mod 2^32
+__host__ __device__ constexpr u32 wmr_s(u32 k) { return 4 * k + 2; }      // [1]    s with n - 1 = 2^s d
+__host__ __device__ constexpr u32 wmr_live(u32 k) { return 4 * k + 3; }   // [1]    1 = run the rounds
+__host__ __device__ constexpr u32 wmr_d(u32 k) { return 4 * k + 4; }      // [k]    d limbs
+__host__ __device__ constexpr u32 wmr_n(u32 k) { return 5 * k + 4; }      // [k+1]  n limbs (0 above the input's)
+__host__ __device__ constexpr u32 wmr_scr(u32 k) { return 6 * k + 5; }    // [2k+4] setup scratch (positional M^2 mod n)
+__host__ __device__ constexpr u32 wmr_words(u32 k) { return 8 * k + 9; }
 
 // ---------------------------------------------------------------------------------------------
 // Tensor-core wide kernel (mr_tcw.cuh, k = 97 and 129: 3072- / 4096-bit moduli and the CRT halves of

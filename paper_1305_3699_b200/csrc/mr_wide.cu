@@ -171,6 +171,16 @@ __device__ __forceinline__ void dot_mb_warp(const u32 *__restrict__ mat, u32 nco
 
 
 
+// Miller-Rabin: per-candidate constants of the CTA's MB candidates (k_mr_rounds_wide)
+struct MrCand {
+    const u32 *pcw;                    // per-candidate rows (mr_internal.h wmr_*), row r of candidate i at pcw[r cnt + i]
+    size_t cnt;
+    const u32 *cand;                   // [MB] candidate index of message q (shared memory)
+    const u32 *const *mp;              // [MB] multiplicand of message q: channel ch at mp[q][ch mstr] (shared memory)
+    u32 mstr;
+    __device__ u32 row(u32 r, int q) const { return __ldcg(pcw + (size_t)r * cnt + cand[q]); }
+};
+
 template <bool PP>   // PP: dot_mb with ping-pong coefficient groups (faster at k >= 257, slower at 129)
 struct Wide {
     const WideArgs &W;
@@ -183,23 +193,29 @@ struct Wide {
     __device__ const u32 *T(u32 off) const { return W.tab + off; }
 
     // st <- st · b · M^-1 (mod N) for the CTA's MB messages; b at bp[ch * bstride + msg * mstride]
-    template <bool COOP>   // COOP: the CTA has fewer threads than k + 1 outputs (leftovers by whole warps)
-    __device__ void mont_mul(const u32 *bp, size_t bstride, u32 mstride, bool sq) {
+    // MRC (Miller-Rabin): every message q has its own modulus n_q; σ, c2, n M^-1 come from mc, b from mc->mp[q], and
+    // BE1 is the unmerged per-k contraction (a1w) followed by × c2_j per candidate (6.4)
+    template <bool COOP, bool MRC = false>   // COOP: the CTA has fewer threads than k + 1 outputs (leftovers by warps)
+    __device__ void mont_mul(const u32 *bp, size_t bstride, u32 mstride, bool sq, const MrCand *mc = nullptr) {
         const WideLayout L = wide_layout(k);
         const u32 tid = threadIdx.x, nt = blockDim.x;
-        const u32 *sigw = cx + W.cxw + wide_cx_sig(k);
+        const u32 *sigw = MRC ? nullptr : cx + W.cxw + wide_cx_sig(k);
+        auto mul_b = [&](u32 ch, int q) -> u32 {
+            if constexpr (MRC) return __ldcg(mc->mp[q] + (size_t)ch * mc->mstr);
+            else return __ldcg(bp + ch * bstride + (size_t)q * mstride);
+        };
         // ---- channel products: B: ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i;  B': t*_j = a* b* 2^-32
         for (u32 ch = tid; ch < 2 * k; ch += nt) {
             const u32 m = __ldg(T(L.mm) + ch), mi = __ldg(T(L.minv) + ch);
-            const u32 s = ch < k ? __ldg(sigw + ch) : 0u;
+            const u32 s = (!MRC && ch < k) ? __ldg(sigw + ch) : 0u;
 #pragma unroll 4
             for (int q = 0; q < MB; q++) {
                 const u32 a = ST(st, ch, q);
-                const u32 b = sq ? a : __ldcg(bp + ch * bstride + (size_t)q * mstride);
+                const u32 b = sq ? a : mul_b(ch, q);
                 const u64 pr = (u64)a * b;
                 u32 t = mont_red((u32)pr, (u32)(pr >> 32), m, mi);
                 if (ch < k) {
-                    const u64 ps = (u64)t * s;
+                    const u64 ps = (u64)t * (MRC ? mc->row(wmr_sig(k) + ch, q) : s);
                     t = mont_red((u32)ps, (u32)(ps >> 32), m, mi);
                 }
                 ST(st, ch, q) = t;
@@ -207,12 +223,12 @@ struct Wide {
         }
         if (tid < MB) {   // m_r: t_r = a_r b_r mod 2^32
             const u32 a = ST(st, 2 * k, tid);
-            const u32 b = sq ? a : __ldcg(bp + (2 * k) * bstride + (size_t)tid * mstride);
+            const u32 b = sq ? a : mul_b(2 * k, (int)tid);
             aux[0 * MB + tid] = a * b;
         }
         __syncthreads();
         // ---- BE1 (approximate, merged with 6.4): thread per output j of B' ∪ {m_r}
-        const u32 *A1w = cx + W.cxw + wide_cx_a1(k);
+        const u32 *A1w = MRC ? T(L.a1w) : cx + W.cxw + wide_cx_a1(k);
         u32 part[MB];
 #pragma unroll
         for (int q = 0; q < MB; q++) part[q] = 0;
@@ -232,7 +248,11 @@ struct Wide {
 #pragma unroll
                 for (int q = 0; q < MB; q++) {
                     if (coop && lane != (u32)q) continue;                              // lane q finishes message q
-                    const u32 v = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);        // Σ ξ A1'  (mod m'_j)
+                    u32 v = red96_mont(hi[q], mi[q], lo[q], m, mv, r32);              // Σ ξ A1'  (mod m'_j)
+                    if constexpr (MRC) {                                                // unmerged: × |n M^-1 λ_j| 2^32
+                        const u64 pv = (u64)v * mc->row(wmr_c2(k) + j, q);
+                        v = mont_red((u32)pv, (u32)(pv >> 32), m, mv);
+                    }
                     const u64 p = (u64)ST(st, ch, q) * X;                              // t* C1 2^64
                     const u32 xp = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);
                     ST(st, ch, q) = xp;                                                // ξ'_j (lazy)
@@ -253,10 +273,11 @@ struct Wide {
 #pragma unroll
                         for (int o = 16; o > 0; o >>= 1) qr[q] += __shfl_xor_sync(0xFFFFFFFFu, qr[q], o);
                 }
-                const u32 minv32 = __ldg(T(L.misc) + 0), nminv = cx[CX_NMINV_R];
+                const u32 minv32 = __ldg(T(L.misc) + 0), nminv = MRC ? 0u : cx[CX_NMINV_R];
                 if (!coop || lane == 0) {
 #pragma unroll
-                    for (int q = 0; q < MB; q++) aux[1 * MB + q] = aux[0 * MB + q] * minv32 + qr[q] * nminv;
+                    for (int q = 0; q < MB; q++)
+                        aux[1 * MB + q] = aux[0 * MB + q] * minv32 + qr[q] * (MRC ? mc->row(wmr_nminv(k), q) : nminv);
                 }
             }
         };
@@ -642,5 +663,425 @@ int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratc
                ? 0
                : 6;
 }
+
+}  // namespace mr
+
+// ------------------------------------------------------------------ Miller-Rabin on wide candidates (k = 257, 505)
+// P:50 §3.2 ("Miller-Rabin tests ... in the Montgomery domain"), HAC 4.24, for candidates of 4,097 .. 16,128 bits
+// (keys up to 16,128 bits).  Every candidate has its own modulus n, so the 6.4 step cannot be merged into a
+// per-context BE1 matrix as in the modexp kernel: BE1 contracts with the per-k |M_i|_{m'_j} 2^32 (wide table a1w) and
+// the epilogue multiplies by the candidate's c2_j = |n M^-1 λ_j| 2^32; σ_i, c2_j, n M^-1 mod 2^32, the RNS image of
+// M^2 mod n, s and d come from a per-candidate setup kernel (rows wmr_* of mr_internal.h).  Same channels-on-threads
+// mapping as k_modexp_wide: MB = 16 candidates per CTA, one thread per output channel.
+namespace mr {
+namespace {
+
+__host__ __device__ constexpr u32 wmr_scr_words(u32 k) { return 3 * k + 4; }
+
+struct WmrArgs {
+    const u32 *tab;          // wide table (wide_layout)
+    u32 k, nt;
+    u32 *pcw;                // [wmr_words(k)][count] per-candidate rows
+    u32 *scr;                // [count][wmr_scr_words(k)] setup scratch (positional M^2 mod n)
+    const u32 *n;            // [count][limbs]
+    const u32 *bases;        // [count][rounds][limbs]
+    u32 count, limbs, rounds, window, forced;
+    u32 *table;              // [E + 3 slots][2k + 1][count]: window table, stash, exit column scratch (2 slots)
+    uint8_t *verdict;
+    int16_t *witness;
+    int32_t *status;
+};
+
+__device__ __forceinline__ u32 wmr_mulm(u32 a, u32 b, u32 m) { return (u32)((u64)a * b % m); }
+__device__ u32 wmr_powm(u32 a, u32 e, u32 m) {
+    u32 r = 1;
+    while (e) {
+        if (e & 1) r = wmr_mulm(r, a, m);
+        a = wmr_mulm(a, a, m);
+        e >>= 1;
+    }
+    return r;
+}
+
+// per-candidate constants (thread per candidate): input rules, residues of n (factor test, reading R14), σ, c2,
+// n M^-1 mod 2^32, s and d (n - 1 = 2^s d), and the RNS image of R^2 mod n (R = M) by Knuth remainders
+__global__ void k_mr_setup_wide(const WmrArgs A) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.count) return;
+    const u32 k = A.k, L = A.limbs;
+    const size_t cnt = A.count;
+    const WideLayout W = wide_layout(k);
+    u32 *pc = A.pcw + i;
+    auto row = [&](u32 r) -> u32 & { return pc[(size_t)r * cnt]; };
+    const u32 *nrow = A.n + (size_t)i * L;
+    for (u32 l = 0; l <= k; l++) row(wmr_n(k) + l) = l < L ? nrow[l] : 0u;
+    u32 nz = 0;
+    for (u32 l = 1; l < L; l++) nz |= nrow[l];
+    const bool small = nz == 0;
+    int32_t status = 0;
+    u32 live = 1, verdict = 0 /* composite */;
+    if (!(nrow[0] & 1u) || (small && nrow[0] < 5u)) { status = 5; live = 0; }
+    if (live) {
+        // residues of n in every channel: Horner over the limbs (one 64-bit remainder per limb and channel)
+        bool factor = false;
+        for (u32 c = 0; c < 2 * k && !factor; c++) {
+            const u32 m = __ldg(A.tab + W.mm + c);
+            u32 r = 0;
+            for (int l = (int)L - 1; l >= 0; l--) r = (u32)((((u64)r << 32) | nrow[l]) % m);
+            if (r == 0) { factor = true; break; }
+            const u32 r32 = __ldg(A.tab + W.r32 + c);
+            if (c < k) {   // σ_i = -(n M_i)^-1 mod m_i, stored × 2^64
+                const u32 x = wmr_mulm(r, __ldg(A.tab + W.mis + c), m);
+                const u32 sg = (m - wmr_powm(x, m - 2, m)) % m;
+                row(wmr_sig(k) + c) = wmr_mulm(wmr_mulm(sg, r32, m), r32, m);
+            } else {       // c2_j = |n M^-1 λ_j|, stored × 2^32
+                const u32 j = c - k;
+                const u32 c2 = wmr_mulm(wmr_mulm(r, __ldg(A.tab + W.lam + j), m), __ldg(A.tab + W.mu + j), m);
+                row(wmr_c2(k) + j) = wmr_mulm(c2, r32, m);
+            }
+        }
+        if (factor) {
+            live = 0;
+            if (small) { status = 3; verdict = 1; }   // n is itself a base prime (MR_ERR_NOT_COPRIME)
+            else verdict = 2;                          // MR_FACTOR (reading R14)
+        }
+    }
+    if (live) {
+        row(wmr_nminv(k)) = nrow[0] * __ldg(A.tab + W.misc + 0);
+        u32 l0 = 0, w0 = nrow[0] & ~1u;
+        while (w0 == 0 && l0 + 1 < L) w0 = nrow[++l0];
+        const u32 s = 32 * l0 + __ffs(w0) - 1, ls = s / 32, bs = s % 32;
+        for (u32 l = 0; l < k; l++) {
+            const u32 a0 = l + ls < L ? nrow[l + ls] : 0u, a1 = l + ls + 1 < L ? nrow[l + ls + 1] : 0u;
+            row(wmr_d(k) + l) = __funnelshift_r(l + ls == 0 ? (a0 & ~1u) : a0, a1, bs);
+        }
+        row(wmr_s(k)) = s;
+        // R^2 mod n, positional: rho = M mod n, then rho^2 mod n (Knuth Algorithm D remainders)
+        u32 Ln = L;
+        while (Ln > 1 && nrow[Ln - 1] == 0) Ln--;
+        u32 *u = A.scr + (size_t)i * wmr_scr_words(k);    // [2k + 2] remainders, then [k] rho
+        for (u32 l = 0; l <= k; l++) u[l] = __ldg(A.tab + W.ml + l);
+        rem_knuth_row(u, k + 1, nrow, Ln);
+        u32 *t = u + 2 * k + 2;
+        for (u32 l = 0; l < Ln; l++) t[l] = u[l];          // rho (Ln <= k - 1 words)
+        for (u32 l = 0; l < 2 * Ln + 1; l++) u[l] = 0;
+        for (u32 a = 0; a < Ln; a++) {
+            u64 c = 0;
+            for (u32 b = 0; b < Ln; b++) {
+                const u64 v = (u64)t[a] * t[b] + u[a + b] + c;
+                u[a + b] = (u32)v;
+                c = v >> 32;
+            }
+            u[a + Ln] = (u32)c;
+        }
+        rem_knuth_row(u, 2 * Ln, nrow, Ln);
+        // RNS image: B plain, B' in ξ-form (× λ_j), m_r = low limb
+        for (u32 c = 0; c < 2 * k; c++) {
+            const u32 m = __ldg(A.tab + W.mm + c);
+            u32 r = 0;
+            for (int l = (int)Ln - 1; l >= 0; l--) r = (u32)((((u64)r << 32) | u[l]) % m);
+            row(wmr_r2(k) + c) = c < k ? r : wmr_mulm(r, __ldg(A.tab + W.lam + (c - k)), m);
+        }
+        row(wmr_r2(k) + 2 * k) = u[0];
+    }
+    row(wmr_live(k)) = live;
+    A.verdict[i] = (uint8_t)verdict;
+    if (A.witness) A.witness[i] = -1;
+    if (A.status) A.status[i] = status;
+}
+
+// exit of the CTA's MB candidates (as wide_exit, with the candidate's own n): X mod n_q in st rows 0..k
+template <bool COOP, bool PP>
+__device__ void wmr_exit(Wide<PP> &w, const MrCand &mc, u32 *scratch, size_t sstride, const u32 *sslot) {
+    const u32 k = w.k, tid = threadIdx.x, nt = blockDim.x;
+    const WideLayout L = wide_layout(k);
+    u32 part[MB];
+#pragma unroll
+    for (int q = 0; q < MB; q++) part[q] = 0;
+    for (u32 j = tid; j < k; j += nt) {
+        const u32 a2r = __ldg(w.T(L.a2r) + j);
+#pragma unroll
+        for (int q = 0; q < MB; q++) part[q] += ST(w.st, k + j, q) * a2r;
+    }
+    block_partials(part, w.red);
+    __syncthreads();
+    if (tid < MB) {
+        u32 sr = 0;
+        for (u32 v = 0; v < w.nw; v++) sr += w.red[v * MB + tid];
+        w.aux[2 * MB + tid] = (sr - ST(w.st, 2 * k, tid)) * __ldg(w.T(L.misc) + 1);
+    }
+    __syncthreads();
+    const u32 lane = tid & 31, warp = tid >> 5;
+    auto column = [&](u32 l, bool coop) {
+        u32 lo[MB], mi[MB], hi[MB];
+        const u32 nmp = __ldg(w.T(L.nmp) + l);
+#pragma unroll
+        for (int q = 0; q < MB; q++) {
+            const u64 p = (COOP && coop) ? 0ull : (u64)w.aux[2 * MB + q] * nmp;
+            lo[q] = (u32)p;
+            mi[q] = (u32)(p >> 32);
+            hi[q] = 0;
+        }
+        if (COOP && coop) dot_mb_warp(w.T(L.mpl), k + 1, l, w.st + k * MB, k, lo, mi, hi);
+        else dot_mb<PP>(w.T(L.mpl), k + 1, l, w.st + k * MB, k, lo, mi, hi);
+#pragma unroll
+        for (int q = 0; q < MB; q++) {
+            if (coop && lane != (u32)q) continue;
+            if (COOP && coop) mac96(lo[q], mi[q], hi[q], w.aux[2 * MB + q], nmp);
+            u32 *col = scratch + (size_t)(3 * l) * sstride + sslot[q];
+            col[0] = lo[q];
+            col[sstride] = mi[q];
+            col[2 * sstride] = hi[q];
+        }
+    };
+    for (u32 l = tid; l <= k && l < nt; l += nt) column(l, false);
+    if constexpr (COOP)
+        if (k + 1 > nt && nt + warp <= k) column(nt + warp, true);
+    __threadfence_block();
+    __syncthreads();
+    if (tid < MB) {
+        const u32 q = tid;
+        u64 carry = 0;
+        for (u32 l = 0; l <= k; l++) {
+            const u32 *col = scratch + (size_t)(3 * l) * sstride + sslot[q];
+            const u64 s = (u64)col[0] + (u32)carry;
+            ST(w.st, l, q) = (u32)s;
+            carry = (carry >> 32) + col[sstride] + ((u64)col[2 * sstride] << 32) + (s >> 32);
+        }
+        const int smax = (int)(32 - __clz(k + 2)) - 1;
+        for (int s = smax; s >= 0; s--) {
+            for (int pass = 0; pass < 2; pass++) {
+                u32 br = 0;
+                for (u32 l = 0; l <= k; l++) {
+                    const u32 nlo = l ? mc.row(wmr_n(k) + l - 1, q) : 0u, nhi = mc.row(wmr_n(k) + l, q);
+                    const u32 nsh = s ? __funnelshift_l(nlo, nhi, s) : nhi;
+                    const u64 t = (u64)ST(w.st, l, q) - nsh - br;
+                    if (pass) ST(w.st, l, q) = (u32)t;
+                    br = (u32)(t >> 63);
+                }
+                if (br) break;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// HAC 4.24 for MB candidates per CTA, every round r with the caller's base a_{i,r}: fixed-window a^d (window w, the
+// table T[e] = a^e R for e < 2^w per candidate), then up to s - 1 squarings looking for n - 1; the CTA skips a round
+// when none of its candidates is pending (early exit; forced: every live candidate runs every round).
+template <int NTB, int MINB, bool COOP, bool PP>
+__global__ void __launch_bounds__(NTB, MINB) k_mr_rounds_wide(const WmrArgs A) {
+    extern __shared__ __align__(16) u32 smem[];
+    const u32 k = A.k, nch = 2 * k + 1, nw = blockDim.x / 32, tid = threadIdx.x, L = A.limbs;
+    u32 *st = smem;
+    u32 *xs = st + nch * MB;
+    u32 *red = xs + k * MB;
+    u32 *aux = red + 16 * MB;
+    __shared__ u32 cand[MB], sslot[MB], dig[MB];
+    __shared__ const u32 *mp[MB];
+    __shared__ u32 live_s[MB], pend[MB], need[MB], pass_s[MB], jj_s[MB], verd[MB], anyf;
+    __shared__ int wit[MB];
+    const size_t cnt = A.count, tstride = A.count, entry = (size_t)nch * tstride;
+    const u32 j0 = blockIdx.x * MB;
+    const u32 E = 1u << A.window, ndig = (32 * L + A.window - 1) / A.window;
+    WideArgs WA{A.tab, k, blockDim.x, 0};
+    Wide<PP> w{WA, nullptr, st, red, aux, k, nch, nw};
+    MrCand mc{A.pcw, cnt, cand, mp, 0};
+    if (tid < MB) {
+        const u32 i = j0 + tid < A.count ? j0 + tid : A.count - 1;   // tail lanes shadow the last candidate
+        cand[tid] = i;
+        sslot[tid] = i;
+        live_s[tid] = j0 + tid < A.count ? A.pcw[(size_t)wmr_live(k) * cnt + i] : 0u;
+        verd[tid] = 1;
+        wit[tid] = -1;
+        if (live_s[tid]) {   // base rule for every round first (HAC 4.24 input): 2 <= a <= n - 2
+            const u32 *nrow = A.n + (size_t)i * L;
+            bool bad = false;
+            for (u32 r = 0; r < A.rounds && !bad; r++) {
+                const u32 *a = A.bases + ((size_t)i * A.rounds + r) * L;
+                u32 br = 0, dhi = 0, ahi = 0, d0 = 0;
+                for (u32 l = 0; l < L; l++) {
+                    const u64 t = (u64)nrow[l] - a[l] - br;
+                    br = (u32)(t >> 63);
+                    if (l) { dhi |= (u32)t; ahi |= a[l]; } else d0 = (u32)t;
+                }
+                bad = !(ahi || a[0] >= 2u) || !(!br && (dhi || d0 >= 2u));
+            }
+            if (bad) {
+                if (A.status) A.status[i] = 5;
+                verd[tid] = 0;          // composite, no witness round (as k_mr_rounds)
+                live_s[tid] = 0;
+            }
+        }
+        pend[tid] = live_s[tid];
+    }
+    __syncthreads();
+    const u32 *tab0 = A.table;
+#pragma unroll 1
+    for (u32 r = 0; r < A.rounds; r++) {
+        if (tid == 0) {
+            u32 a = 0;
+            for (int q = 0; q < MB; q++) a |= pend[q] | (A.forced ? live_s[q] : 0u);
+            anyf = a;
+        }
+        __syncthreads();
+        if (!anyf) break;
+        // uniform part: T0 = mm(R^2, 1) = R, T1 = mm(a, R^2) = a R, T[e] = T[e-1] T1; the ladder starts at T0
+        for (u32 u = 0; u < E + ndig * (A.window + 1); u++) {
+            bool sq = false;
+            if (u == 0) {
+                for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                    const u32 ch = e / MB, q = e % MB;
+                    st[e] = A.pcw[(size_t)(wmr_r2(k) + ch) * cnt + cand[q]];
+                }
+                if (tid < MB) mp[tid] = A.tab + wide_layout(k).one;
+                mc.mstr = 1;
+            } else if (u == 1) {
+                for (u32 e = tid; e < L * MB; e += blockDim.x) {
+                    const u32 l = e / MB, q = e % MB;
+                    xs[l * MB + q] = A.bases[((size_t)cand[q] * A.rounds + r) * L + l];
+                }
+                __syncthreads();
+                w.to_rns(xs, L);
+                if (tid < MB) mp[tid] = A.pcw + (size_t)wmr_r2(k) * cnt + cand[tid];
+                mc.mstr = (u32)cnt;
+            } else if (u < E) {
+                if (tid < MB) mp[tid] = tab0 + entry + cand[tid];
+                mc.mstr = (u32)tstride;
+            } else {
+                const u32 qq = u - E, dg = ndig - 1 - qq / (A.window + 1), sub = qq % (A.window + 1);
+                if (qq == 0) {
+                    for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                        const u32 ch = e / MB, q = e % MB;
+                        st[e] = tab0[ch * tstride + cand[q]];
+                    }
+                }
+                if (sub < A.window) {
+                    sq = true;
+                } else {
+                    if (tid < MB) {
+                        const u32 b0 = dg * A.window, lw = b0 / 32, bw = b0 % 32;
+                        const u32 *dl = A.pcw + (size_t)wmr_d(k) * cnt + cand[tid];
+                        const u32 lo = lw < k ? dl[(size_t)lw * cnt] : 0u, hi = lw + 1 < k ? dl[(size_t)(lw + 1) * cnt] : 0u;
+                        mp[tid] = tab0 + (size_t)(__funnelshift_r(lo, hi, bw) & (E - 1)) * entry + cand[tid];
+                    }
+                    mc.mstr = (u32)tstride;
+                }
+            }
+            __syncthreads();
+            w.template mont_mul<COOP, true>(nullptr, 0, 0, sq, &mc);
+
+            if (u < E) {
+                for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                    const u32 ch = e / MB, q = e % MB;
+                    A.table[u * entry + ch * tstride + cand[q]] = st[e];
+                }
+                __syncthreads();
+            }
+        }
+        // checks: even steps leave the Montgomery domain (× 1) and compare with 1 and n - 1, odd steps square
+        if (tid < MB) {
+            need[tid] = pend[tid] | (A.forced ? live_s[tid] : 0u);
+            pass_s[tid] = 0;
+            jj_s[tid] = 0;
+        }
+        __syncthreads();
+        u32 *stash = A.table + (size_t)E * entry;
+        for (u32 v = 0;; v++) {
+            const bool check = (v % 2) == 0;
+            if (check) {
+                for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                    const u32 ch = e / MB, q = e % MB;
+                    stash[ch * tstride + cand[q]] = st[e];
+                }
+                if (tid < MB) mp[tid] = A.tab + wide_layout(k).one;
+                mc.mstr = 1;
+            }
+            __syncthreads();
+            w.template mont_mul<COOP, true>(nullptr, 0, 0, !check, &mc);
+            if (check) {
+                wmr_exit<COOP, PP>(w, mc, A.table + (size_t)(E + 1) * entry, tstride, sslot);
+                if (tid < MB) {
+                    const u32 q = tid;
+                    u32 one = ST(st, 0, q) ^ 1u, nm1 = ST(st, 0, q) ^ (mc.row(wmr_n(k), q) - 1u);
+                    for (u32 l = 1; l <= k; l++) {
+                        one |= ST(st, l, q);
+                        nm1 |= ST(st, l, q) ^ mc.row(wmr_n(k) + l, q);
+                    }
+                    if (need[q]) {
+                        const u32 s = mc.row(wmr_s(k), q);
+                        if (nm1 == 0) { pass_s[q] = 1; need[q] = 0; }
+                        else if (one == 0) { pass_s[q] = jj_s[q] == 0; need[q] = 0; }
+                        else if (jj_s[q] + 1 >= s) need[q] = 0;
+                    }
+                    jj_s[q]++;
+                }
+                __syncthreads();   // the comparisons read st rows 0..k: restore the state only after them
+                for (u32 e = tid; e < nch * MB; e += blockDim.x) {
+                    const u32 ch = e / MB, q = e % MB;
+                    st[e] = stash[ch * tstride + cand[q]];
+                }
+                if (tid == 0) {
+                    u32 a = 0;
+                    for (int q = 0; q < MB; q++) a |= need[q];
+                    anyf = a;
+                }
+                __syncthreads();
+                if (!anyf) break;
+            }
+        }
+        if (tid < MB) {
+            const u32 q = tid;
+            if (pend[q] && !pass_s[q]) {
+                if (verd[q] == 1) { verd[q] = 0; wit[q] = (int)r; }
+                if (!A.forced) pend[q] = 0;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < MB && j0 + tid < A.count && A.pcw[(size_t)wmr_live(k) * cnt + cand[tid]]) {
+        const u32 i = cand[tid];
+        A.verdict[i] = (uint8_t)verd[tid];
+        if (A.witness) A.witness[i] = (int16_t)wit[tid];
+    }
+}
+
+}  // namespace
+
+// Miller-Rabin for wide candidates (k = 257, 505): setup (thread per candidate), then the rounds (16 per CTA)
+int launch_mr_wide(const u32 *d_wide_tab, u32 k, u32 *d_pcw, u32 *d_scr, const u32 *d_n, const u32 *d_bases, u32 count,
+                   u32 limbs, u32 rounds, u32 window, u32 forced, u32 *d_table, uint8_t *d_verdict, int16_t *d_witness,
+                   int32_t *d_status, void *stream) {
+    WmrArgs A{d_wide_tab, k, 0, d_pcw, d_scr, d_n, d_bases, count, limbs, rounds, window, forced, d_table, d_verdict,
+              d_witness, d_status};
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        void *args[] = {&A};
+        if (cudaLaunchKernel((const void *)k_mr_setup_wide, dim3((count + 63) / 64), dim3(64), args, 0, st) != cudaSuccess)
+            return 6;
+    }
+    const u32 up = 32 * ((k + 1 + 31) / 32), down = 32 * ((k + 1) / 32);
+    const u32 nt32 = (k + 1) - down <= 4 && down >= 64 ? down : up, nt = nt32 < (u32)NTMAX ? nt32 : (u32)NTMAX;
+    A.nt = nt;
+    const size_t smem = wide_smem_bytes(k);
+    const void *kern = nt > 256 ? (const void *)k_mr_rounds_wide<NTMAX, 1, false, true>
+                                : (const void *)k_mr_rounds_wide<256, 2, true, true>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 6;
+    void *args[] = {&A};
+    return cudaLaunchKernel(kern, dim3((count + MB - 1) / MB), dim3(nt), args, smem, st) == cudaSuccess ? 0 : 6;
+}
+// test hook: the per-candidate setup alone (rows wmr_* into d_pcw)
+int launch_mr_wide_setup(const u32 *d_wide_tab, u32 k, u32 *d_pcw, u32 *d_scr, const u32 *d_n, u32 count, u32 limbs,
+                         uint8_t *d_verdict, void *stream) {
+    WmrArgs A{d_wide_tab, k, 0, d_pcw, d_scr, d_n, nullptr, count, limbs, 0, 1, 0, nullptr, d_verdict, nullptr, nullptr};
+    void *args[] = {&A};
+    return cudaLaunchKernel((const void *)k_mr_setup_wide, dim3((count + 63) / 64), dim3(64), args, 0,
+                            (cudaStream_t)stream) == cudaSuccess
+               ? 0
+               : 6;
+}
+size_t mr_wide_table_words(u32 k, u32 window, u32 count) { return (size_t)((1u << window) + 3) * (2 * k + 1) * count; }
+size_t mr_wide_pcw_words(u32 k, u32 count) { return (size_t)wmr_words(k) * count; }
+size_t mr_wide_scr_words(u32 k, u32 count) { return (size_t)wmr_scr_words(k) * count; }
 
 }  // namespace mr

@@ -270,7 +270,13 @@ def _wide_layout(k):
     o["pow"] = o["a2w"] + _wch_rows(k) * k
     o["mpl"] = o["pow"] + _wch_rows(k) * 2 * k
     o["nmp"] = o["mpl"] + _wch_rows(k) * (k + 1)
-    o["words"] = o["nmp"] + k + 1
+    o["a1w"] = (o["nmp"] + k + 1 + 3) & ~3
+    o["lam"] = o["a1w"] + _wch_rows(k) * k
+    o["mu"] = o["lam"] + k
+    o["mis"] = o["mu"] + k
+    o["ml"] = o["mis"] + k
+    o["one"] = o["ml"] + k + 1
+    o["words"] = o["one"] + 2 * k + 1
     return o
 
 
@@ -330,6 +336,17 @@ def test_wide_table_identities():
     for j in [0, k - 1] + [int(v) for v in rng.integers(0, k, 4)]:   # M'_j positional limbs
         m = Bp[j]
         assert sum(t[o["mpl"] + _wch_at(j, l, k + 1)] << (32 * l) for l in range(k + 1)) == Mp // m
+    # Miller-Rabin section: unmerged BE1 A1_ij 2^32 mod m'_j, λ_j, μ_j, |M_i|_{m_i}, M limbs, the image of 1
+    for j in [0, k - 1] + [int(v) for v in rng.integers(0, k, 3)]:
+        m = Bp[j]
+        assert t[o["lam"] + j] == pow(Mp // m, -1, m) and t[o["mu"] + j] == pow(M, -1, m)
+        for i in [0, k - 1] + [int(v) for v in rng.integers(0, k, 3)]:
+            assert t[o["a1w"] + _wch_at(i, j, k)] == (M // B[i]) % m * W % m
+    for i in [0, k - 1]:
+        assert t[o["mis"] + i] == (M // B[i]) % B[i]
+    assert sum(t[o["ml"] + l] << (32 * l) for l in range(k + 1)) == M
+    assert [t[o["one"] + c] for c in (0, k - 1, 2 * k)] == [1, 1, 1]
+    assert t[o["one"] + k] == pow(Mp // Bp[0], -1, Bp[0])
     pad = [t[o["a2w"] + _wch_at(i, j, k)] for i in range(k, _wch_rows(k)) for j in (0, k - 1)]
     assert not any(pad)                                                # zero rows up to the group size
     assert L.mr_internal_wide_table(65, None, 0) < 0 and L.mr_internal_wide_table(129, None, 0) > 0

@@ -195,3 +195,33 @@ def test_small_candidate_equal_to_base_prime(torch_cuda, mr, orc):
     assert s[3] == 0 and v[3] == mr.MR_PROBABLY_PRIME
     ov, _ = orc.miller_rabin(ns[4], [2, 3, 5], fp)
     assert s[4] == 0 and v[4] == ov
+
+
+@pytest.mark.parametrize("bits, k, primes", [(4423, 257, [4253, 4423]), (11213, 505, [9689, 11213])])
+def test_wide_candidates_vs_oracle(torch_cuda, mr, orc, bits, k, primes):
+    """Miller-Rabin above 4,096 bits (k = 257 / 505, channels-on-threads kernels with a per-candidate setup,
+    DESIGN.md §4l; keys up to 16,128 bits): Mersenne primes 2^p - 1 (known primes: every round passes), random
+    odd composites, a FACTOR candidate (divisible by a base prime, reading R14) and a candidate with a base outside
+    [2, n-2] (status MR_ERR_RANGE); verdict and first witnessing round vs the oracle with the same explicit bases.
+    20 candidates = two 16-candidate CTAs (the second ragged)."""
+    import random
+    rng = random.Random(bits)
+    L = (bits + 31) // 32
+    fp = orc.base_primes(2 * k)
+    ns = [(1 << e) - 1 for e in primes]
+    while len(ns) < 17:
+        ns.append(rng.getrandbits(bits) | (1 << (bits - 1)) | 1)
+    nf = fp[3] * (rng.getrandbits(bits - 40) | (1 << (bits - 41)) | 1)
+    ns.append(nf)                                                   # FACTOR
+    ns.append(rng.getrandbits(bits) | (1 << (bits - 1)) | 1)        # bad base below
+    ns.append((1 << primes[0]) - 1)
+    R = 3
+    bases = [[rng.randrange(2, n - 1) for _ in range(R)] for n in ns]
+    bases[18][1] = 1                                                # outside [2, n-2]
+    v, w, s, limbs = gpu_mr(torch_cuda, mr, ns, bases, limbs=L)
+    assert v[0] == v[1] == v[19] == mr.MR_PROBABLY_PRIME and w[0] == w[1] == -1
+    assert v[17] == mr.MR_FACTOR and s[18] == mr.MR_ERR_RANGE and v[18] == mr.MR_COMPOSITE
+    for i in list(range(17)) + [17, 19]:
+        ov, ow = orc.miller_rabin(ns[i], bases[i], fp)
+        assert (v[i], w[i]) == (ov, ow), i
+        assert s[i] == 0
