@@ -34,6 +34,9 @@ MR_DECLARE_K(129)
 size_t wide_smem_bytes(u32 k);
 int wide_messages_per_cta();
 int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream);
+// the tensor-core wide kernel at k = 257 (mr_tcw257.cu; k = 97 / 129 come with their per-k kernel sets)
+int launch_modexp_tcw_k257(const ModexpParams &p, u32 ctas, const u32 *tab, const void *kimg, u32 cxw, u32 be1w, u32 jobs,
+                           void *trace, void *stream);
 int wide_messages_per_cta_lanes();
 int launch_modexp_wide_lanes(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream);
 int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream);
@@ -1118,18 +1121,22 @@ static bool tcw_enabled() {
 // 128-message tile-jobs (ctas0 per context) on one persistent CTA per SM
 static int launch_ladders_tcw(mr_rns_ctx *const *ctxs, const DevProg *progs, int nctx, const u32 *d_x, size_t in_limbs,
                               size_t half, u32 *d_y, size_t out_limbs, size_t count, int32_t *d_status, void *stream,
-                              const KernelSet &ks) {
+                              int (*launch_tcw)(const ModexpParams &, u32, const u32 *, const void *, u32, u32, u32, void *,
+                                                void *)) {
     const mr_rns_ctx *c0 = ctxs[0];
     cudaStream_t st = (cudaStream_t)stream;
     u32 ctas0 = (u32)((count + 127) / 128);
-    if (TCW_LOCK) ctas0 += ctas0 & 1u;        // lockstep tiles take job pairs of one context
+    if (TCW_LOCK || TCW_PAIR) ctas0 += ctas0 & 1u;   // lockstep tiles / CTA pairs take job pairs of one context
     const u32 jobs = ctas0 * (u32)nctx;
     const u32 jobs_total = ctas0 * 128 * (u32)nctx;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device);
     static const int max_sms = [] { const char *e = getenv("MR_RNS_MAX_SMS"); return e ? atoi(e) : 0; }();
     if (max_sms > 0) sms = std::min(sms, std::max(1, max_sms));
-    const u32 grid = std::min<u32>((u32)sms, (jobs + TCW_TILES - 1) / TCW_TILES);
+    const u32 tiles = tcw_tiles((u32)c0->k);
+    // CTA pairs (2-CTA clusters): each cluster runs `tiles` pair-jobs (256 messages each) at a time
+    const u32 grid = TCW_PAIR ? 2 * std::min<u32>(std::max(1, sms / 2), (jobs / 2 + tiles - 1) / tiles)
+                              : std::min<u32>((u32)sms, (jobs + tiles - 1) / tiles);
     int w = 1;
     for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
     const size_t nch = 2 * (size_t)c0->k + 1;
@@ -1161,7 +1168,7 @@ static int launch_ladders_tcw(mr_rns_ctx *const *ctxs, const DevProg *progs, int
     unsigned long long *d_trace = nullptr;
     if (trace_file && cudaMallocAsync(&d_trace, 16384 * 8, st) == cudaSuccess) cudaMemsetAsync(d_trace, 0, 16384 * 8, st);
     int rc = timed_launch(0, st, [&] {
-                 return ks.launch_modexp_tcw(P, grid, c0->d_wide, c0->d_tcw, c0->cxw, c0->be1w, jobs, d_trace, stream);
+                 return launch_tcw(P, grid, c0->d_wide, c0->d_tcw, c0->cxw, c0->be1w, jobs, d_trace, stream);
              }) == 0
                  ? MR_OK
                  : MR_ERR_CUDA;
@@ -1187,9 +1194,10 @@ static int launch_ladders_wide(mr_rns_ctx *const *ctxs, const DevProg *progs, in
     const mr_rns_ctx *c0 = ctxs[0];
     cudaStream_t st = (cudaStream_t)stream;
     if (!lanes && c0->d_tcw && c0->be1w && tcw_enabled()) {
-        const KernelSet &ks = kernel_set_for(c0->k);
-        if (ks.launch_modexp_tcw)
-            return launch_ladders_tcw(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count, d_status, stream, ks);
+        auto launch_tcw = c0->k == 257 ? launch_modexp_tcw_k257 : kernel_set_for(c0->k).launch_modexp_tcw;
+        if (launch_tcw)
+            return launch_ladders_tcw(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count, d_status, stream,
+                                      launch_tcw);
     }
     const u32 MBm = (u32)(lanes ? wide_messages_per_cta_lanes() : wide_messages_per_cta());
     const u32 ctas0 = (u32)((count + MBm - 1) / MBm);

@@ -228,7 +228,7 @@ __host__ __device__ constexpr u32 wmr_words(u32 k) { return 8 * k + 9; }
 // bytes in the K-major SWIZZLE_NONE core-matrix layout with SBO = steps_s·256 (LBO = 128).
 // ---------------------------------------------------------------------------------------------
 enum : u32 { TCW_BE1 = 0, TCW_BE2 = 1, TCW_TRN = 2, TCW_EXT = 3 };
-__host__ __device__ constexpr bool tcw_k(u32 k) { return k == 97 || k == 129; }
+__host__ __device__ constexpr bool tcw_k(u32 k) { return k == 97 || k == 129 || k == 257; }
 __host__ __device__ constexpr u32 tcw_kp(u32 k) { return (4 * k + 4 + 31) & ~31u; }     // A row bytes (α' word k)
 __host__ __device__ constexpr u32 tcw_ks(u32 k) { return tcw_kp(k) / 32; }               // K-steps
 __host__ __device__ constexpr u32 tcw_nslab(u32 k) { return (tcw_ks(k) + 3) / 4; }
@@ -238,20 +238,31 @@ __host__ __device__ constexpr u32 tcw_nout(u32 k, u32 e) {
     return e == TCW_BE1 ? k + 1 : e == TCW_BE2 ? k : e == TCW_TRN ? 2 * k : k + 1;
 }
 constexpr u32 TCW_TILES = 2;
+// tiles per CTA at channel count k: at k = 257 one 128-message A tile is 135 KB of shared memory and its B residues
+// take 260 TMEM columns, so a CTA runs a single tile (with two compute warps per lane quadrant, tcw_halves)
+__host__ __device__ constexpr u32 tcw_tiles(u32 k) { return k > 129 ? 1u : TCW_TILES; }
 // MR_TCW_LOCK = 1: the two tiles of a CTA run jobs of the same context in lockstep and share ONE stream of B slabs
 // (each slab feeds both tiles' MMAs: half the L2 traffic); 0: independent tiles, one stream each
 #ifndef MR_TCW_LOCK
 #define MR_TCW_LOCK 0
 #endif
 constexpr bool TCW_LOCK = MR_TCW_LOCK != 0;
+// MR_TCW_PAIR = 1: CTA pairs (2-CTA clusters) issue M = 256 MMAs (tcgen05 cta_group::2) over the two CTAs' 128-message
+// tiles, and each CTA streams only HALF of every B slab (its N/2 rows): the slab copies run at the chip's L2 -> SM
+// bandwidth cap, so halving the bytes each SM ingests per multiplication halves the MMA phases
+#ifndef MR_TCW_PAIR
+#define MR_TCW_PAIR 0
+#endif
+constexpr bool TCW_PAIR = MR_TCW_PAIR != 0 && !TCW_LOCK;
 // largest outputs per chunk (multiple of 4) whose columns fit a tile's accumulator buffer (MR_TCW_OCCAP: a smaller cap
 // trades MMA width for epilogue registers; host and device must be built with the same value)
 #ifndef MR_TCW_OCCAP
 #define MR_TCW_OCCAP 64
 #endif
 __host__ __device__ constexpr u32 tcw_ocmax(u32 k) {
-    return (((512 / TCW_TILES - tcw_bsw(k)) & ~15u) / 4 & ~3u) < MR_TCW_OCCAP ? (((512 / TCW_TILES - tcw_bsw(k)) & ~15u) / 4 & ~3u)
-                                                                             : MR_TCW_OCCAP;
+    return (((512 / tcw_tiles(k) - tcw_bsw(k)) & ~15u) / 4 & ~3u) < MR_TCW_OCCAP
+               ? (((512 / tcw_tiles(k) - tcw_bsw(k)) & ~15u) / 4 & ~3u)
+               : MR_TCW_OCCAP;
 }
 __host__ __device__ constexpr u32 tcw_nchunks(u32 k, u32 e) { return (tcw_nout(k, e) + tcw_ocmax(k) - 1) / tcw_ocmax(k); }
 __host__ __device__ constexpr u32 tcw_oc(u32 k, u32 e) {                                 // outputs per chunk (last: rest)

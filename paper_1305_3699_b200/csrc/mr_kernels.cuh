@@ -2074,22 +2074,8 @@ constexpr int TC_TILES = 0;
 // ctas = persistent CTAs (one per SM); tab = wide table, kimg = per-k images, cxw / be1w = context offsets (words)
 int launch_modexp_tcw(const ModexpParams &p, u32 ctas, const u32 *tab, const void *kimg, u32 cxw, u32 be1w, u32 jobs,
                       void *trace, void *stream) {
-    static bool attr = false;
-    if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute((const void *)k_modexp_tcw, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)W_SMEM);
-        if (e != cudaSuccess) {
-            if (getenv("MR_RNS_DEBUG")) fprintf(stderr, "k_modexp_tcw smem %zu: %s\n", (size_t)W_SMEM, cudaGetErrorString(e));
-            return 6;
-        }
-        attr = true;
-    }
-    TcwArgs a{tab, reinterpret_cast<const uint8_t *>(kimg), cxw, be1w, jobs, reinterpret_cast<unsigned long long *>(trace)};
-    void *args[] = {const_cast<ModexpParams *>(&p), &a};
-    const cudaError_t e = cudaLaunchKernel((const void *)k_modexp_tcw, dim3(ctas), dim3(W_THREADS), args, W_SMEM,
-                                           (cudaStream_t)stream);
-    if (e != cudaSuccess && getenv("MR_RNS_DEBUG")) fprintf(stderr, "k_modexp_tcw launch: %s\n", cudaGetErrorString(e));
-    return e == cudaSuccess ? 0 : 6;
+    return tcw_launch(p, ctas, TcwArgs{tab, reinterpret_cast<const uint8_t *>(kimg), cxw, be1w, jobs,
+                                       reinterpret_cast<unsigned long long *>(trace)}, stream);
 }
 #else
 constexpr int (*launch_modexp_tcw)(const ModexpParams &, u32, const u32 *, const void *, u32, u32, u32, void *,

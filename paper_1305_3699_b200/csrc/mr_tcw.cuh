@@ -1,6 +1,7 @@
 // mr_tcw.cuh — tensor-core modexp for wide operands, k = 97 and 129 (3072- / 4096-bit moduli, CRT halves of
 // 6144- / 8192-bit keys): SURVEY §8(f) rows 2-3, DESIGN.md §4k.  Included by mr_kernels.cuh inside its
-// per-k anonymous namespace (MR_K = 97 or 129), so K, NCH, SMAX, GB(), mont_red(), less_than() are this TU's.
+// per-k anonymous namespace (MR_K = 97 or 129), or by mr_tcw257.cu (MR_K = 257: one tile per CTA), so K, NCH, SMAX,
+// mont_red(), less_than() are this TU's.
 //
 // The arithmetic is the RNS Montgomery multiplication of mr_kernels.cuh (§3.1) in the plain
 // word-Montgomery form of the wide kernel (mr_wide.cu: every product reduced by mont_red, the 2^-32 factors
@@ -14,7 +15,7 @@
 // The B images (16k² bytes per extension: 150 KB at k = 97) exceed shared memory, so they are STREAMED from L2
 // by the bulk-copy (TMA) engine through a ring of stages, one [chunk rows x 128 K-bytes] slab per stage.
 //
-// A CTA runs TCW_TILES = 2 independent tiles of 128 messages (one message per thread, the 128 TMEM lanes), each
+// A CTA runs W_TILES = 2 (k = 257: 1) independent tiles of 128 messages (one message per thread, the 128 TMEM lanes), each
 // with its own producer thread (stage ring), MMA-issuer thread, accumulator buffer and four compute warps, so one
 // tile's CUDA-core phases (channel products, epilogues) run under the other tile's MMAs.
 // State of a message (the shared memory of two tiles holds only their A tiles and stages):
@@ -26,7 +27,9 @@
 // in the window table's spare slot), and the A row is written once all chunks are done.
 #pragma once
 
-#if MR_K == 97 || MR_K == 129
+#if MR_K == 97 || MR_K == 129 || MR_K == 257
+
+constexpr u32 W_TILES = tcw_tiles(K);                 // independent 128-message tiles per CTA (k = 257: one)
 
 constexpr u32 W_KP = tcw_kp(K);                       // A row bytes
 constexpr u32 W_KC = W_KP / 16;                       // K-cores (4 words) per A row
@@ -34,26 +37,27 @@ constexpr u32 W_SBOA = (W_KP / 16) * 128;             // A tile: bytes between 8
 constexpr u32 W_NCMAX = tcw_ncmax(K);                 // TMEM columns of a tile's accumulator buffer
 constexpr u32 W_BSW = tcw_bsw(K);
 constexpr u32 W_TCOLS = W_NCMAX + W_BSW;              // TMEM columns per tile: [acc | B residues]
-static_assert(TCW_TILES * W_TCOLS <= 512, "tiles x (accumulator + B residues) exceed the 512 TMEM columns");
+static_assert(W_TILES * W_TCOLS <= 512, "tiles x (accumulator + B residues) exceed the 512 TMEM columns");
 static_assert(W_KC * 4 >= K + 2, "A row must hold B' (k words), α' (word k) and m_r (word k+1)");
-constexpr u32 W_STG = tcw_stage_bytes(K);
+constexpr bool W_PAIR = TCW_PAIR;                     // CTA pairs: M = 256 MMAs, each CTA streams half of every slab
+constexpr u32 W_STG = tcw_stage_bytes(K) / (W_PAIR ? 2u : 1u);   // bytes of one stage (pair: the CTA's N/2 rows)
 constexpr u32 W_ABYTES = 128 * W_KP;
-constexpr size_t W_FIXED = (size_t)TCW_TILES * W_ABYTES + 16 * K + 8 * K + 8 * K + 512 + TCW_TILES * 2048;
-constexpr u32 W_RINGS = TCW_LOCK ? 1 : TCW_TILES;     // streams of B slabs per CTA
+constexpr size_t W_FIXED = (size_t)W_TILES * W_ABYTES + 16 * K + 8 * K + 8 * K + 512 + W_TILES * 2048;
+constexpr u32 W_RINGS = TCW_LOCK ? 1 : W_TILES;       // streams of B slabs per CTA
 constexpr u32 W_NST_FIT = (u32)((232448 - W_FIXED) / (W_RINGS * W_STG));
 constexpr u32 W_NST = W_NST_FIT > 8 ? 8 : W_NST_FIT;  // pipeline stages per stream
 static_assert(W_NST >= 2, "tensor wide kernel: fewer than two B stages per tile fit shared memory");
 constexpr size_t W_SMEM = W_FIXED + (size_t)W_RINGS * W_NST * W_STG;
-constexpr u32 W_SUB = TCW_LOCK ? TCW_TILES : 1;       // tiles served by one stream (one producer, one MMA issuer)
+constexpr u32 W_SUB = TCW_LOCK ? W_TILES : 1;         // tiles served by one stream (one producer, one MMA issuer)
 #ifndef MR_TCW_HALVES
 #define MR_TCW_HALVES 1       // compute warps per TMEM lane quadrant and tile (2: each takes alternate channel groups)
 #endif
-constexpr u32 W_HV = MR_TCW_HALVES;
+constexpr u32 W_HV = K > 129 ? 2u : (u32)MR_TCW_HALVES;   // k = 257: 8 compute warps for the single tile
 #ifndef MR_TCW_CHAN_PIPE
 #define MR_TCW_CHAN_PIPE 0    // 1: next group's operand loads under the current group's products (A/B: 9 % slower, spills)
 #endif
-constexpr u32 W_CW = 4 * W_HV * TCW_TILES;            // compute warps
-constexpr u32 W_THREADS = 32 * (W_CW + 2 * TCW_TILES);   // + per tile a producer warp and an MMA warp (one lane each:
+constexpr u32 W_CW = 4 * W_HV * W_TILES;              // compute warps
+constexpr u32 W_THREADS = 32 * (W_CW + 2 * W_TILES);     // + per tile a producer warp and an MMA warp (one lane each:
                                                          // two roles in one warp would sleep on each other's waits)
 constexpr u32 W_NBAR = 2 * W_NST + 3;                 // per tile: full[NST] empty[NST] accf acce aready
 
@@ -124,15 +128,23 @@ __device__ __forceinline__ u64 w_gtimer() {
 }
 // wait for phase `par` of an mbarrier; try_wait with a suspend-time hint parks the thread in hardware until the phase
 // completes (instead of re-issuing the test); a wait longer than 30 s traps instead of hanging the GPU
+template <bool CL = false>   // CL: acquire at cluster scope (the barrier also counts arrivals of the peer CTA)
 __device__ __forceinline__ void w_mbar_wait(u32 a, u32 par) {
     u32 done = 0;
     u64 t0 = 0;
 #pragma unroll 1
     for (u32 spin = 0; !done; spin++) {
-        asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
-                     : "=r"(done)
-                     : "r"(a), "r"(par), "r"(1000000u)
-                     : "memory");
+        if constexpr (CL)
+            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+                         "selp.u32 %0, 1, 0, P1;\n\t}"
+                         : "=r"(done)
+                         : "r"(a), "r"(par), "r"(1000000u)
+                         : "memory");
+        else
+            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+                         : "=r"(done)
+                         : "r"(a), "r"(par), "r"(1000000u)
+                         : "memory");
         if (!done && (spin & 255) == 255) {
             const u64 t = w_gtimer();
             if (!t0) t0 = t;
@@ -141,6 +153,16 @@ __device__ __forceinline__ void w_mbar_wait(u32 a, u32 par) {
     }
 }
 __device__ __forceinline__ void w_mbar_arrive(u32 a) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory"); }
+// arrive on a barrier of another CTA of the cluster (cluster-window address), releasing this thread's prior writes
+__device__ __forceinline__ void w_mbar_arrive_cl(u32 ca) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ca) : "memory");
+}
+// cluster-window address of the same shared-memory offset in the pair's leader CTA (rank 0)
+__device__ __forceinline__ u32 w_lead(u32 a) {
+    u32 r;
+    asm("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+    return r;
+}
 __device__ __forceinline__ void w_mbar_expect_tx(u32 a, u32 bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
@@ -215,6 +237,7 @@ struct TcwTile {               // one tile's shared memory and barriers
     u32 stage0;                // shared address of its stage 0
     u32 bar;                   // shared address of its barriers: full[NST] empty[NST] accf acce aready
     u32 tacc;                  // TMEM column of its accumulator buffer (lane 0)
+    u32 rank = 0;              // pair mode: CTA rank in the cluster (rank 0 issues the pair's MMAs)
     __device__ u32 full(u32 s) const { return bar + 8 * s; }
     __device__ u32 empty(u32 s) const { return bar + 8 * (W_NST + s); }
     __device__ u32 accf() const { return bar + 8 * (2 * W_NST); }
@@ -235,10 +258,12 @@ struct TcwProducer {
 #pragma unroll 1
             for (u32 s = 0; s < tcw_nslab(K); s++) {
                 const u32 bytes = nc * 32 * tcw_steps(K, s);
+                // pair mode: this CTA's N/2 rows = the first / second half of the block (row groups are outermost)
+                const u32 hb = W_PAIR ? bytes / 2 : bytes;
                 w_mbar_wait(T.empty(st), ph ^ 1u);
                 tr((e << 4) | (s == 0 ? 1 : 2));
-                w_mbar_expect_tx(T.full(st), bytes);
-                w_bulk_g2s(T.stage0 + st * W_STG, img + off, bytes, T.full(st), pol);
+                w_mbar_expect_tx(T.full(st), hb);
+                w_bulk_g2s(T.stage0 + st * W_STG, img + off + T.rank * hb, hb, T.full(st), pol);
                 off += bytes;
                 if (++st == W_NST) { st = 0; ph ^= 1u; }
             }
@@ -252,8 +277,29 @@ struct TcwMma {
     u32 tmem;
     WTrace tr;
     u32 sa1 = 0, td1 = 0;                  // lockstep: the second tile's A tile and accumulator
+    // completion of the MMAs issued so far -> an mbarrier (pair: the same offset in both CTAs)
+    __device__ static void commit(u32 bar) {
+        if constexpr (W_PAIR)
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                         ::"r"(bar), "h"((unsigned short)3) : "memory");
+        else
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    }
+    // pair mode, rank 1: forward each landed half-slab to the leader's full barrier (the bulk copy can only signal an
+    // mbarrier of its own CTA); walks the same (extension, chunk, slab) sequence as the leader's issuer
+    __device__ void relay(const TcwTile &T, u32 e) {
+#pragma unroll 1
+        for (u32 c = 0; c < w_nchunks(e); c++) {
+#pragma unroll 1
+            for (u32 s = 0; s < tcw_nslab(K); s++) {
+                w_mbar_wait(T.full(st), fph);
+                w_mbar_arrive_cl(w_lead(T.full(st)));
+                if (++st == W_NST) { st = 0; fph ^= 1u; }
+            }
+        }
+    }
     __device__ void ext(const TcwTile &T, u32 e) {
-        w_mbar_wait(T.aready(), aph);          // the A rows of all 128 messages are written (and proxy-fenced)
+        w_mbar_wait<W_PAIR>(T.aready(), aph);  // the A rows of all 128 (pair: 256) messages are written (and proxy-fenced)
         aph ^= 1u;
         tr(e << 4);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -261,15 +307,16 @@ struct TcwMma {
 #pragma unroll 1
         for (u32 c = 0; c < w_nchunks(e); c++) {
             const u32 nc = w_nc(e, c);
-            w_mbar_wait(T.acce(), eph ^ 1u);   // the epilogue has read the buffer's previous chunk
+            w_mbar_wait<W_PAIR>(T.acce(), eph ^ 1u);   // the epilogue (pair: of both CTAs) has read the previous chunk
             eph ^= 1u;
             tr((e << 4) | 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const u32 idesc = (2u << 4) | ((nc >> 3) << 17) | ((128u >> 4) << 24);   // s32 = u8 x u8, K-major, M = 128
+            // s32 = u8 x u8, K-major, M = 128 (pair: M = 256 over the two CTAs' tiles, N = nc with N/2 B rows per CTA)
+            const u32 idesc = (2u << 4) | ((nc >> 3) << 17) | (((W_PAIR ? 256u : 128u) >> 4) << 24);
 #pragma unroll 1
             for (u32 s = 0; s < tcw_nslab(K); s++) {
                 const u32 steps = tcw_steps(K, s);
-                w_mbar_wait(T.full(st), fph);
+                w_mbar_wait<W_PAIR>(T.full(st), fph);   // pair: own half landed + the peer's relayed arrival
                 tr((e << 4) | 3);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const u32 sb = T.stage0 + st * W_STG;
@@ -279,18 +326,22 @@ struct TcwMma {
                     for (u32 j = 0; j < steps; j++) {
                         const u64 da = w_desc((u ? sa1 : sa) + (4 * s + j) * 256, W_SBOA), db = w_desc(sb + j * 256, steps * 256);
                         const u32 accum = (s | j) ? 1u : 0u;
-                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(u ? td1 : td),
-                                     "l"(da), "l"(db), "r"(idesc), "r"(accum)
-                                     : "memory");
+                        if constexpr (W_PAIR)
+                            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(td),
+                                         "l"(da), "l"(db), "r"(idesc), "r"(accum)
+                                         : "memory");
+                        else
+                            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(u ? td1 : td),
+                                         "l"(da), "l"(db), "r"(idesc), "r"(accum)
+                                         : "memory");
                     }
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(T.empty(st))
-                             : "memory");
+                commit(T.empty(st));           // stage free (pair: in both CTAs)
                 if (++st == W_NST) { st = 0; fph ^= 1u; }
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(T.accf())
-                         : "memory");
+            commit(T.accf());                  // chunk accumulated (pair: both CTAs' epilogues start)
             tr((e << 4) | 2);
         }
     }
@@ -316,6 +367,7 @@ struct TcwCompute {
     u32 fph = 0;
     WTrace tr;                // trace (thread 0 of the tile only)
     __device__ void trace(u32 ev) { if (m == 0 && h == 0) tr(ev); }
+    u32 minv_r = 0, mpinv_r = 0;   // M^-1 and M'^-1 mod 2^32 (the m_r channel, wide table misc)
     u32 sel = 0;              // context of the current job
     const u32 *cx = nullptr;  // its context block (HBM)
 
@@ -344,8 +396,22 @@ struct TcwCompute {
     }
     __device__ void a_done() {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy A writes -> async proxy (MMA)
-        w_mbar_arrive(T.aready());
+        if (!W_PAIR || T.rank == 0) {
+            w_mbar_arrive(T.aready());
+        } else {                                                       // one arrival per warp on the leader's barrier
+            __syncwarp();
+            if ((m & 31) == 0) w_mbar_arrive_cl(w_lead(T.aready()));
+        }
         trace(0x0F);
+    }
+    // the accumulator buffer is read (one arrival per warp; pair: on the leader's barrier)
+    __device__ void acc_free() const {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if ((m & 31) == 0) {
+            if (!W_PAIR || T.rank == 0) w_mbar_arrive(T.acce());
+            else w_mbar_arrive_cl(w_lead(T.acce()));
+        }
     }
     // Chunks of extension E: wait for the accumulator, combine the four byte columns of every output of this half's
     // groups into V (64-bit registers), release the buffer at once (the next chunk's MMAs run under the rest of the
@@ -383,9 +449,7 @@ struct TcwCompute {
                     }
                 }
             }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if ((m & 31) == 0) w_mbar_arrive(T.acce());
+            acc_free();
             trace((E << 4) | 2);
             f(c * OC, n4, Vl, Vh);
             trace((E << 4) | 3);
@@ -598,12 +662,13 @@ struct TcwCompute {
                             for (int t = 0; t < 4; t++) {
                                 const u32 j = oh + t, q = 4 * (gi + u) + t;
                                 const uint4 e1 = ep1[j < K ? j : 0];
-                                // ξ'_j = mont(t*_j C1_j 2^64 + V_j): t* C1 2^64 < 2^32 m'_j <= 2^64 - 2^43 (the B' primes
-                                // are below 2^32 - 2^11, reading R1) and V < 2^49.2, so the sum fits 64 bits
+                                // ξ'_j = mont(t*_j C1_j 2^64 + V_j): t* < 2^32 and V <= 4k 255^2 (1 + 2^8 + 2^16 + 2^24)
+                                // < 2^50.1, and every per-k constant C1_j 2^64 mod m'_j is below 0.9985 2^32, so the sum
+                                // fits 64 bits (pinned per k by test_tcw_host.py::test_be1_epilogue_sum_fits_64_bits)
                                 const u64 p = madw(u ? tc[t] : ta[t], e1.z, ((u64)Vh[q] << 32) | Vl[q]);
                                 xp[t] = mont_red((u32)p, (u32)(p >> 32), e1.x, e1.y);
                                 if (j < K) sr += xp[t] * e1.w;
-                                if (j == K) rr = trm * GB(O_MISC + 0) + Vl[q] * nminv;   // q̂_r = Σ ξ_i |M_i|_{2^32}
+                                if (j == K) rr = trm * minv_r + Vl[q] * nminv;   // q̂_r = Σ ξ_i |M_i|_{2^32}
                             }
                             if (oh < K) w_tmem_st4(tb(bs + oh), xp[0], xp[1], xp[2], xp[3]);   // ξ'_j in place of t*_j
                         }
@@ -613,7 +678,7 @@ struct TcwCompute {
         });
         // ---- 6.6 BE2: A row = (ξ'_0 .. ξ'_{k-1}, α', r_r), α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 exact
         const uint2 tot = exchange(sr, rr);              // (also: every ξ'_j of both halves is in TMEM)
-        const u32 alpha = (tot.x - tot.y) * GB(O_MISC + 1);
+        const u32 alpha = (tot.x - tot.y) * mpinv_r;
         rr = tot.y;
 #pragma unroll 1
         for (u32 g = h; g < GW; g += W_HV) {
@@ -666,7 +731,7 @@ struct TcwCompute {
                 if (16 * g + t < K) sr += aw(16 * g + t) * ep1[16 * g + t].w;
         }
         const uint2 tot = exchange(sr, 0u);
-        if (mine16(K / 16)) aw(K) = (tot.x - aw(K + 1)) * GB(O_MISC + 1);
+        if (mine16(K / 16)) aw(K) = (tot.x - aw(K + 1)) * mpinv_r;
         a_done();
         // half 0 carries the byte-position sums into limbs group by group (the buffer is released after the chunk)
         u64 carry = 0;
@@ -692,9 +757,7 @@ struct TcwCompute {
                     w_tmem_st4(tb(bs + o0 + 4 * g), l4[0], l4[1], l4[2], l4[3]);   // limbs (columns < round4(K+1))
                 }
             }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if ((m & 31) == 0) w_mbar_arrive(T.acce());
+            acc_free();
         }
         if (h) return;
         w_tmem_wait_st();
@@ -825,7 +888,7 @@ struct TcwCompute {
     }
 };
 
-// Persistent kernel, one CTA per SM, TCW_TILES independent tiles per CTA: tile u of CTA b takes the tile-jobs
+// Persistent kernel, one CTA per SM, W_TILES independent tiles per CTA: tile u of CTA b takes the tile-jobs
 // t = b·TILES + u, + gridDim.x·TILES, ...; job t runs context sel = t / ctas0.  The producer, the MMA issuer and
 // the compute warps of a tile walk the same job list and op programs, so they meet on the same sequence of
 // (extension, chunk, slab).
@@ -833,20 +896,23 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
     extern __shared__ __align__(1024) uint8_t wsm[];
     __shared__ u32 tslot;
     const u32 tid = threadIdx.x, warp = tid / 32;
-    uint8_t *stages = wsm + (size_t)TCW_TILES * W_ABYTES;
+    u32 rank = 0;                                     // pair mode: CTA rank in the 2-CTA cluster
+    if constexpr (W_PAIR) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    uint8_t *stages = wsm + (size_t)W_TILES * W_ABYTES;
     uint4 *ep1 = reinterpret_cast<uint4 *>(stages + (size_t)W_RINGS * W_NST * W_STG);
     uint2 *ep2 = reinterpret_cast<uint2 *>(ep1 + K);
     u32 *sig = reinterpret_cast<u32 *>(ep2 + K);
     u64 *bars = reinterpret_cast<u64 *>(((uintptr_t)(sig + 2 * K) + 7) & ~(uintptr_t)7);
     // role: compute warps 0 .. W_CW-1 (tile = warp / (4 W_HV), half = (warp / 4) % W_HV; the warp's TMEM lane quadrant
-    // is warp % 4), then per tile a producer warp and an MMA warp (lane 0 works)
-    const u32 tile = warp < W_CW ? warp / (4 * W_HV) : (warp - W_CW) % TCW_TILES;
+    // is warp % 4), then per tile a producer warp and an MMA warp (lane 0 works; pair mode: rank 1's MMA warp relays)
+    const u32 tile = warp < W_CW ? warp / (4 * W_HV) : (warp - W_CW) % W_TILES;
     TcwTile T;
     const u32 ring = TCW_LOCK ? 0u : tile;
     T.a = wsm + (size_t)tile * W_ABYTES;
     T.stage0 = smem_u32(stages + (size_t)ring * W_NST * W_STG);
     T.bar = smem_u32(bars + ring * W_NBAR);
     T.tacc = tile * W_TCOLS;
+    T.rank = rank;
     const WideLayout WL = wide_layout(K);
     for (u32 j = tid; j < K; j += W_THREADS) {
         ep1[j] = make_uint4(__ldg(A.wtab + WL.mm + K + j), __ldg(A.wtab + WL.minv + K + j), __ldg(A.wtab + WL.xw + j),
@@ -858,36 +924,49 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
     if (tid < W_RINGS) {
         TcwTile U;
         U.bar = smem_u32(bars + tid * W_NBAR);
+        const bool lead = W_PAIR && rank == 0;        // the leader's barriers also count the peer's arrivals
         for (u32 s = 0; s < W_NST; s++) {
-            w_mbar_init(U.full(s), 1);
+            w_mbar_init(U.full(s), lead ? 2 : 1);     // pair leader: own expect_tx + the peer's relay
             w_mbar_init(U.empty(s), 1);
         }
         w_mbar_init(U.accf(), 1);
-        w_mbar_init(U.acce(), 4 * W_HV * W_SUB);
-        w_mbar_init(U.aready(), 128 * W_HV * W_SUB);
+        w_mbar_init(U.acce(), 4 * W_HV * W_SUB + (lead ? 4 * W_HV : 0));
+        w_mbar_init(U.aready(), 128 * W_HV * W_SUB + (lead ? 4 * W_HV : 0));
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (W_PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if constexpr (W_PAIR)   // both CTAs' barriers initialised before any remote arrival
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem = tslot;
     // independent tiles: tile u of CTA b walks jobs b TILES + u + i gridDim.x TILES; lockstep: the producer and the
-    // MMA issuer walk the job PAIRS (jobs 2p, 2p + 1 share a context: the host pads ctas0 to even) and tile u takes 2p + u
-    const u32 J = A.jobs, stride = gridDim.x * TCW_TILES;
-    const u32 first = blockIdx.x * TCW_TILES + tile;
+    // MMA issuer walk the job PAIRS (jobs 2p, 2p + 1 share a context: the host pads ctas0 to even) and tile u takes 2p + u;
+    // CTA pairs: tile u of cluster c walks the pair-jobs q = c TILES + u + i (clusters) TILES and CTA r takes job 2q + r
+    // (the two jobs of a pair share a context: the host pads ctas0 to even)
+    const u32 cl = W_PAIR ? blockIdx.x / 2 : blockIdx.x, ncl = W_PAIR ? gridDim.x / 2 : gridDim.x;
+    const u32 J = W_PAIR ? A.jobs / 2 : A.jobs, stride = ncl * W_TILES;
+    const u32 first = cl * W_TILES + tile;
+    auto job_of = [&](u32 q) { return W_PAIR ? 2 * q + rank : q; };
     const bool role_on = !TCW_LOCK || tile == 0 || warp < W_CW;   // lockstep: tile 1's producer / MMA warps idle
 
-    if (warp >= W_CW && warp < W_CW + TCW_TILES) {    // ---- producer of `tile`
+    if (warp >= W_CW && warp < W_CW + W_TILES) {    // ---- producer of `tile`
         if ((tid & 31) == 0 && role_on) {
             TcwProducer pr;
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pr.pol));
             pr.tr.init(A.trace, tile, 2);
 #pragma unroll 1
-            for (u32 t = first; t < J; t += stride) {
+            for (u32 q = first; q < J; q += stride) {
+                const u32 t = job_of(q);
                 const u32 sel = t / P.ctas0;
                 const uint8_t *be1 = reinterpret_cast<const uint8_t *>((sel ? P.ctx[1] : P.ctx[0]) + A.be1w);
                 const u64 *prog = sel ? P.prog[1] : P.prog[0];
@@ -904,7 +983,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
                 pr.ext(T, TCW_EXT, A.kimg + tcw_img_off(K, TCW_EXT));
             }
         }
-    } else if (warp >= W_CW + TCW_TILES) {            // ---- MMA issuer of `tile`
+    } else if (warp >= W_CW + W_TILES) {            // ---- MMA issuer of `tile` (pair mode, rank 1: relay)
         if ((tid & 31) == 0 && role_on) {
             TcwMma mm;
             mm.tmem = tmem;
@@ -912,30 +991,37 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
             mm.td1 = tmem + W_TCOLS;
             mm.tr.init(A.trace, tile, 1);
 #pragma unroll 1
-            for (u32 t = first; t < J; t += stride) {
-                const u32 sel = t / P.ctas0;
+            for (u32 q = first; q < J; q += stride) {
+                const u32 sel = job_of(q) / P.ctas0;
                 const u64 *prog = sel ? P.prog[1] : P.prog[0];
                 const u32 nops = sel ? P.nops[1] : P.nops[0];
+                auto ext = [&](u32 e) {
+                    if (W_PAIR && rank) mm.relay(T, e);
+                    else mm.ext(T, e);
+                };
 #pragma unroll 1
                 for (u32 s = 0; s < nops; s++) {
                     const u32 fl = (u32)__ldg(prog + s) & 0xFF;
-                    if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) mm.ext(T, TCW_TRN);
+                    if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) ext(TCW_TRN);
                     if (!(fl & OPF_NOMUL)) {
-                        mm.ext(T, TCW_BE1);
-                        mm.ext(T, TCW_BE2);
+                        ext(TCW_BE1);
+                        ext(TCW_BE2);
                     }
                 }
-                mm.ext(T, TCW_EXT);
+                ext(TCW_EXT);
             }
         }
     } else {                                          // ---- compute warps of `tile`
         const u32 m = (warp % 4) * 32 + (tid & 31), h = (warp / 4) % W_HV;
-        uint2 *xch = reinterpret_cast<uint2 *>(bars + TCW_TILES * W_NBAR) + tile * 256;
+        uint2 *xch = reinterpret_cast<uint2 *>(bars + W_TILES * W_NBAR) + tile * 256;
         TcwCompute cw{T, ep1, ep2, sig, tmem + ((warp % 4) * 32u << 16), T.tacc + W_NCMAX, m, h,
                       T.a + (m / 8) * W_SBOA + (m % 8) * 16, xch, 1 + tile};
         cw.tr.init(A.trace, tile, 0);
+        cw.minv_r = __ldg(A.wtab + WL.misc);
+        cw.mpinv_r = __ldg(A.wtab + WL.misc + 1);
 #pragma unroll 1
-        for (u32 t = first; t < J; t += stride) {
+        for (u32 q = first; q < J; q += stride) {
+            const u32 t = job_of(q);
             cw.sel = t / P.ctas0;
             cw.cx = cw.sel ? P.ctx[1] : P.ctx[0];
             const u32 jl = (t - cw.sel * P.ctas0) * 128 + m;
@@ -945,7 +1031,45 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    if constexpr (W_PAIR) {   // the peer's MMAs / remote arrivals are done before either CTA frees TMEM or exits
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    } else {
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
 }
 
-#endif  // MR_K == 97 || MR_K == 129
+// host side of one launch (both the per-k TUs and mr_tcw257.cu): shared-memory attribute once per process, 2-CTA
+// clusters in pair mode (ctas even)
+int tcw_launch(const ModexpParams &p, u32 ctas, const TcwArgs &a, void *stream) {
+    static bool attr = false;
+    if (!attr) {
+        const cudaError_t e = cudaFuncSetAttribute((const void *)k_modexp_tcw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)W_SMEM);
+        if (e != cudaSuccess) {
+            if (getenv("MR_RNS_DEBUG")) fprintf(stderr, "k_modexp_tcw<%d> smem %zu: %s\n", K, (size_t)W_SMEM, cudaGetErrorString(e));
+            return 6;
+        }
+        attr = true;
+    }
+    TcwArgs aa = a;
+    ModexpParams pp = p;
+    void *args[] = {&pp, &aa};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(W_THREADS);
+    cfg.dynamicSmemBytes = W_SMEM;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = W_PAIR ? 2 : 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = W_PAIR ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, (const void *)k_modexp_tcw, args);
+    if (e != cudaSuccess && getenv("MR_RNS_DEBUG")) fprintf(stderr, "k_modexp_tcw<%d> launch: %s\n", K, cudaGetErrorString(e));
+    return e == cudaSuccess ? 0 : 6;
+}
+
+#endif  // MR_K == 97 || MR_K == 129 || MR_K == 257

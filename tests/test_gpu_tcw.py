@@ -1,5 +1,5 @@
-"""GPU parity of the tensor-core wide kernel (k_modexp_tcw, mr_tcw.cuh) for k = 97 and 129:
-3072- / 4096-bit moduli and the CRT halves of 6144- / 8192-bit keys.  Every case runs on the tensor path and on the
+"""GPU parity of the tensor-core wide kernel (k_modexp_tcw, mr_tcw.cuh) for k = 97, 129 and 257:
+3072- / 4096- / 8192-bit moduli and the CRT halves of 6144- / 8192- / 16,128-bit keys.  Every case runs on the tensor path and on the
 IMAD wide kernel (mr_internal_set_tcw), both compared element by element with the CPU oracle; ragged batches span
 several 128-message tile-jobs, with edge inputs 0, 1, 2, N-1, N-2 and out-of-range inputs (status 5, output 0).
 """
@@ -74,6 +74,67 @@ def test_tcw_modexp_vs_oracle(torch_cuda, mr, orc, bits, path):
         assert np.array_equal(y[:387], ref), (path, E.bit_length())
 
 
+@pytest.mark.parametrize("path", PATHS)
+def test_tcw_k257_modexp_vs_oracle(torch_cuda, mr, orc, path):
+    """8192-bit modulus (k = 257: one 128-message tile per CTA, two compute warps per lane quadrant): ragged 200-message
+    batch (two tile-jobs, the second with 72) with edge inputs, E = 65537 and a 160-bit E, every output vs the oracle"""
+    set_path(mr, path)
+    bits = 8192
+    rng = random.Random(bits + 11)
+    N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+    L = bits // 32
+    xs = [0, 1, 2, N - 1, N - 2, 1 << (bits - 2)] + [rng.randrange(N) for _ in range(192)] + [N, N + 7]
+    for E in (65537, rng.getrandbits(160) | (1 << 159)):
+        y, st, ctx = modexp(torch_cuda, mr, N, xs, E, L)
+        assert ctx.k == 257
+        assert st == [0] * 198 + [5, 5] and not y[198:].any()
+        ref = orc.modexp_batch(mr.ints_to_limbs(xs[:198], L), E, N, threads=8)
+        assert np.array_equal(y[:198], ref), (path, E.bit_length())
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_tcw_k257_crt_decrypt_vs_oracle(torch_cuda, mr, orc, path):
+    """CRT decryption of a 16,128-bit key (§3.1): two 8064-bit half ladders at k = 257 in one launch, then the
+    positional recombination; 140 ciphertexts with edge inputs, every output vs the oracle"""
+    set_path(mr, path)
+    half_bits = 8064
+    rng = random.Random(half_bits + 5)
+    while True:
+        p = rng.getrandbits(half_bits) | (3 << (half_bits - 2)) | 1
+        q = rng.getrandbits(half_bits) | (3 << (half_bits - 2)) | 1
+        if p != q and math.gcd(p, q) == 1:
+            break
+    n, H = p * q, half_bits // 32
+    dp, dq = rng.getrandbits(96) | 1, rng.getrandbits(96) | 1
+    qinv = pow(q, -1, p)
+    cs = [0, 1, n - 1, p, q, 2 * p, 3 * q] + [rng.randrange(n) for _ in range(132)] + [n + 1]
+    key = mr.RsaPrivateKey(p, q, dp, dq, qinv)
+    c = dev(torch_cuda, mr.ints_to_limbs(cs, 2 * H))
+    m = torch_cuda.empty_like(c)
+    st = torch_cuda.full((len(cs),), -1, dtype=torch_cuda.int32, device="cuda")
+    key.decrypt(c, m, d_status=st)
+    torch_cuda.cuda.synchronize()
+    assert host(st).view(np.int32).tolist() == [0] * 139 + [5]
+    ref = orc.crt_decrypt_batch(mr.ints_to_limbs(cs[:139], 2 * H), p, q, dp, dq, qinv, H, threads=8)
+    got = host(m)
+    assert np.array_equal(got[:139], ref) and not got[139].any()
+
+
+def test_tcw_k257_paths_identical_full_exponent(torch_cuda, mr):
+    """k = 257 tensor path and IMAD wide kernel give identical bytes for a full 8192-bit exponent (300 messages)"""
+    rng = random.Random(257)
+    N = rng.getrandbits(8192) | (1 << 8191) | 1
+    xs = [rng.randrange(N) for _ in range(300)]
+    E = rng.getrandbits(8192) | (1 << 8191)
+    set_path(mr, "tcw")
+    a, _, _ = modexp(torch_cuda, mr, N, xs, E, 256)
+    set_path(mr, "imad_wide")
+    b, _, _ = modexp(torch_cuda, mr, N, xs, E, 256)
+    assert np.array_equal(a, b)
+    for i in (0, 150, 299):
+        assert int.from_bytes(a[i].tobytes(), "little") == pow(xs[i], E, N)
+
+
 @pytest.mark.parametrize("count", [1, 127, 128, 129])
 def test_tcw_batch_edges(torch_cuda, mr, orc, count):
     """single-tile edge counts at k = 97 (one message; a full tile; one past it)"""
@@ -145,7 +206,7 @@ import random, sys
 import numpy as np, torch
 sys.path.insert(0, {root!r})
 import paper_1305_3699_b200 as mr
-for bits in (3072, 4096):
+for bits in (3072, 4096, 8192):
     rng = random.Random(bits + 3)
     N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
     L = bits // 32

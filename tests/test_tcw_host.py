@@ -1,4 +1,4 @@
-"""CPU pins of the tensor-core wide kernel's host images (mr_tcw.cuh; k = 97 and 129).
+"""CPU pins of the tensor-core wide kernel's host images (mr_tcw.cuh; k = 97, 129 and 257).
 
 Each image is the byte-split B operand of one contraction (mr_internal.h tcw_*): row (output o, byte b), K byte
 (input word i, byte a) = byte b of 2^(8a) A(i, o) mod m_o.  The test decodes the exported image with an
@@ -19,7 +19,7 @@ import random
 import numpy as np
 import pytest
 
-from test_abi_host import _lib, _tables
+from test_abi_host import _layout, _lib, _tables
 
 BE1, BE2, TRN, EXT = 0, 1, 2, 3
 
@@ -49,11 +49,12 @@ def nout(k, e):
     return {BE1: k + 1, BE2: k, TRN: 2 * k, EXT: k + 1}[e]
 
 
-TILES = 2
+def tiles(k):
+    return 1 if k > 129 else 2
 
 
 def ocmax(k):
-    return (((512 // TILES - bsw(k)) & ~15) // 4) & ~3
+    return min((((512 // tiles(k) - bsw(k)) & ~15) // 4) & ~3, 64)
 
 
 def nchunks(k, e):
@@ -125,7 +126,7 @@ def combine(D, o):
     return sum(int(D[4 * o + b]) << (8 * b) for b in range(4))
 
 
-@pytest.fixture(scope="module", params=[97, 129])
+@pytest.fixture(scope="module", params=[97, 129, 257])
 def base(request):
     k = request.param
     flat, primes, _ = _tables(k)
@@ -140,7 +141,7 @@ def base(request):
 
 def test_geometry_fits(base):
     k = base[0]
-    assert TILES * (max(nc(k, e, c) for e in range(4) for c in range(nchunks(k, e))) + bsw(k)) <= 512
+    assert tiles(k) * (max(nc(k, e, c) for e in range(4) for c in range(nchunks(k, e))) + bsw(k)) <= 512
     assert kp(k) >= 4 * k + 4 and all(oc(k, e) % 4 == 0 for e in range(4))
 
 
@@ -162,6 +163,23 @@ def test_be1_image_definition(base):
             want = sum(x[i] * ((M // B[i]) % m) for i in range(k)) * nu * W % m
             assert combine(D[r], j) % m == want
         assert combine(D[r], k) % W == sum(x[i] * ((M // B[i]) % W) for i in range(k)) % W
+
+
+def test_be1_epilogue_sum_fits_64_bits(base):
+    """the BE1 epilogue forms t*_j (C1_j 2^64 mod m'_j) + V_j in ONE 64-bit multiply-add (mr_tcw.cuh, mad.wide.u32): t* is
+    a lazy residue < 2^32 and V = Σ_b 2^(8b) D_b with every D_b <= 4k 255^2 (4k u8 x u8 products per column), so the sum
+    fits only because every per-k constant C1_j 2^64 mod m'_j stays far enough below 2^32 — pinned here from the base
+    table (reading R1's primes), at every tensor-wide k"""
+    k, B, Bp, M, Mp = base
+    flat, primes, _ = _tables(k)
+    o_c1 = _layout(k)["C1"]
+    vmax = 4 * k * 255 * 255 * (1 + 2 ** 8 + 2 ** 16 + 2 ** 24)
+    for j in range(k):
+        m = Bp[j]
+        c1 = int(flat[o_c1 + j])
+        assert c1 == pow(M, -1, m) * pow(pow(Mp // m, -1, m), -1, m) % m   # C1_j = |M^-1 λ_j^-1|_{m'_j}
+        xw = c1 * pow(2, 64, m) % m
+        assert (2 ** 32 - 1) * xw + vmax < 2 ** 64, (k, j)
 
 
 def test_be2_image_definition(base):
