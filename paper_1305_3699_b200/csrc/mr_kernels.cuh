@@ -89,6 +89,17 @@ __constant__ u32 g_base[BASE_WORDS];
 #ifndef MR_MR_EPI_UNROLL
 #define MR_MR_EPI_UNROLL 0  // 1: Miller-Rabin tensor epilogues unrolled with constant-bank operands (A/B: 5 % slower, spills)
 #endif
+#ifndef MR_FRAC_ALPHA
+// 1: the tensor kernels take the BE2 / exit overflow count α' = floor(Σ_j ξ'_j / m'_j) from the top bits of the ξ'_j
+// (Kawamura's fractional base extension: the value r being extended is < (2k+3)N, so r / M' < 0.11 and the sum is
+// within 2^-13.9 below an integer plus r / M'), instead of through the extra modulus m_r = 2^32, which then needs no
+// upkeep at all (no m_r product, no Σ ξ_i |M_i|_{2^32} and Σ ξ'_j |M'_j|_{2^32} IMAD chains).  DESIGN.md §4e, reading R5.
+#define MR_FRAC_ALPHA 1
+#endif
+// α' = floor(Σ_j ξ'_j / m'_j) from s = Σ_j (ξ'_j >> 8): ξ'_j / m'_j exceeds ξ'_j / 2^32 by < c'_j / m'_j <= 2^-20 and the
+// shift drops < 2^-24, so s / 2^24 is below the sum by < k (2^-20 + 2^-24) <= 2^-13.9 (k <= 65); adding 2^-10 and
+// truncating gives α' exactly while r / M' + 2^-10 < 1
+__device__ __forceinline__ u32 frac_alpha(u32 s) { return (s + (1u << 14)) >> 24; }
 #ifndef MR_SIG_PF
 #define MR_SIG_PF 8         // Miller-Rabin: per-candidate σ_i / c2_j loaded this many channels / outputs ahead
 #endif
@@ -393,10 +404,16 @@ __device__ __forceinline__ void from_rns(STT st, const CS &cs, const u32 *__rest
     u32 x[K];
 #pragma unroll
     for (int j = 0; j < K; j++) x[j] = S(st, K + j);
-    u32 sr = 0;
+    u32 sr = 0, alpha;
+    if constexpr (MR_FRAC_ALPHA && CS::kMont) {   // tensor kernels: no m_r channel (frac_alpha; z / M' < 0.11)
 #pragma unroll
-    for (int j = 0; j < K; j++) sr += x[j] * GB(O_A2R + j);
-    const u32 alpha = (sr - S(st, 2 * K)) * GB(O_MISC + 1);
+        for (int j = 0; j < K; j++) sr += x[j] >> 8;
+        alpha = frac_alpha(sr);
+    } else {
+#pragma unroll
+        for (int j = 0; j < K; j++) sr += x[j] * GB(O_A2R + j);
+        alpha = (sr - S(st, 2 * K)) * GB(O_MISC + 1);
+    }
     u32 clo = 0, cmi = 0;
 #pragma unroll 1
     for (int l = 0; l <= K; l++) {
@@ -888,7 +905,7 @@ struct MulTc {
                         const u64 pr = (u64)a * b;
                         xi = mont_red((u32)pr, (u32)(pr >> 32), GB(O_MM + i), GB(O_MINV + i));
                         const uint2 ax = cs.a1x(i);
-                        qr += xi * ax.x;
+                        if (!MR_FRAC_ALPHA) qr += xi * ax.x;
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, ax.y);
                     } else if constexpr (CS::kMont) {   // ξ_i = mont(mont(a b) σ_i 2^64) = a b σ_i
                         const u64 pr = (u64)a * b;
@@ -902,7 +919,7 @@ struct MulTc {
                         }
                         const u64 ps = (u64)t * sg;
                         xi = mont_red((u32)ps, (u32)(ps >> 32), GB(O_MM + i), GB(O_MINV + i));   // lazy digit < 2^32
-                        qr += xi * GB(O_A1R + i);
+                        if (!MR_FRAC_ALPHA) qr += xi * GB(O_A1R + i);
                         if (TCNC) mac96(c1lo, c1mi, c1hi, xi, s_a1c[i]);
                     } else {
                         xi = mulmod(mulmod(a, b, cc), cs.sigma(i), cc);
@@ -956,6 +973,7 @@ struct MulTc {
 #if MR_BP_LATE
         return 0;
 #else
+        if constexpr (MR_FRAC_ALPHA && CS::kMont) return 0u;   // no m_r channel
         const u32 ar = S(st, 2 * K);
         return ar * (SQ || sq ? ar : mulop_ld<CS>(bq));
 #endif
@@ -977,6 +995,7 @@ struct MulTc {
                 S(st, K + j) = mulmod(a, b, GB(O_C + K + j));
             }
         }
+        if constexpr (MR_FRAC_ALPHA && CS::kMont) return 0u;
         const u32 ar = S(st, 2 * K);
         return ar * (SQ || sq ? ar : mulop_ld<CS>(bp + (size_t)(2 * K) * bs));
     }
@@ -985,6 +1004,7 @@ struct MulTc {
     __device__ __forceinline__ void operator()(const StTile &st, const u32 *bp, u32 bs, bool sq, const CS &cs) {
         constexpr bool MERGED = CS::kMerged;      // false: per-thread modulus (Miller-Rabin), unmerged BE1
         constexpr u32 ONECOL = CS::kScaled ? 0x100u : 0u;   // byte 1 of A word K: the BE1 offset column
+        constexpr bool FRAC = MR_FRAC_ALPHA && CS::kMont;   // α' from the top bits of ξ' (no m_r channel)
         const u32 lane_base = (u32)(t.m & ~31u) << 16;
         uint8_t *arow = st.arow;
         // ---- 6.1/6.2: q-digits ξ_i overwrite a_i in place in the A tile (4 channels per 16-byte chunk);
@@ -992,7 +1012,7 @@ struct MulTc {
         u32 qr = 0, tr;
         u32 c1lo = 0, c1mi = 0, c1hi = 0;
         if constexpr (CS::kScaled) {      // constant offsets of the sign-folded digits
-            qr = cs.qr_off();
+            if (!FRAC) qr = cs.qr_off();
             if (TCNC) c1lo = cs.c1_off();
         }
 #if MR_SQ_SPLIT
@@ -1006,9 +1026,9 @@ struct MulTc {
         //      channel products and the m_r product run while the MMA does
         tc_issue(t, t.b1);
         tr = sq ? chan_bp<true, CS>(st, bp, bs) : chan_bp<false, CS>(st, bp, bs);
-        const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
+        const u32 rr = FRAC ? 0u : tr * GB(O_MISC + 0) + qr * cs.nminv();
 #else
-        const u32 rr = tr * GB(O_MISC + 0) + qr * cs.nminv();
+        const u32 rr = FRAC ? 0u : tr * GB(O_MISC + 0) + qr * cs.nminv();
         // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij)
         tc_issue(t, t.b1);
 #endif
@@ -1073,7 +1093,7 @@ struct MulTc {
                         const u64 p = (u64)S(st, K + j) * e.z + (((u64)c33 << 32) | w33);
                         xp = mont_red((u32)p, (u32)(p >> 32), e.x, e.y);
                         S(st, K + j) = xp;
-                        sr += xp * e.w;
+                        sr += FRAC ? xp >> 8 : xp * e.w;
                         if (TCNC) mac96(c2lo, c2mi, c2hi, xp, GB(O_A2C + j));   // unscaled column, × ρ at the end
                         w[o] = xp;
                         continue;
@@ -1097,7 +1117,7 @@ struct MulTc {
                         xp = red96(h2, m2, l2, c, 0);
                     }
                     S(st, K + j) = xp;
-                    sr += xp * ((MR_MR_EPI_UNROLL && CS::kMont) ? GB(O_A2R + j) : s_be[bev_A2r(K) + j]);
+                    sr += FRAC ? xp >> 8 : xp * ((MR_MR_EPI_UNROLL && CS::kMont) ? GB(O_A2R + j) : s_be[bev_A2r(K) + j]);
                     if (TCNC) mac96(c2lo, c2mi, c2hi, xp, s_a2c[j]);
                     w[o] = xp;
                 }
@@ -1118,19 +1138,19 @@ struct MulTc {
         if constexpr (TCNC != 0) {   // CUDA-core output of BE1 completes the BE2 operand and its own BE2 term
             const int j = TCNT;
             S(st, K + j) = xp_c;
-            sr += xp_c * s_be[bev_A2r(K) + j];
+            sr += FRAC ? xp_c >> 8 : xp_c * s_be[bev_A2r(K) + j];
             if constexpr (CS::kScaled) mac96(c2lo, c2mi, c2hi, xp_c, GB(O_A2C + j));
             else mac96(c2lo, c2mi, c2hi, xp_c, s_a2c[j]);
-            alpha = (sr - rr) * GB(O_MISC + 1);
+            alpha = FRAC ? frac_alpha(sr) : (sr - rr) * GB(O_MISC + 1);
             *reinterpret_cast<uint4 *>(arow + (j / 4) * 128) = make_uint4(xp_c, alpha | ONECOL, 0u, 0u);
         } else {
-            alpha = (sr - rr) * GB(O_MISC + 1);
+            alpha = FRAC ? frac_alpha(sr) : (sr - rr) * GB(O_MISC + 1);
             *reinterpret_cast<u32 *>(arow + (K / 4) * 128 + 4 * (K % 4)) = alpha | ONECOL;
         }
         // ---- 6.6 BE2 on the tensor core; r_i back into the A tile
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // TMEM reads done before reuse
         tc_issue(t, t.b2);
-        S(st, 2 * K) = rr;
+        if (!FRAC) S(st, 2 * K) = rr;
         u32 r_c = 0;
         if (TCNC) {
             const int i = TCNT;
