@@ -4,6 +4,7 @@ identities of DESIGN.md §3 (checked with independent CPython arithmetic, no ora
 needed: these are definitions of the tables, not results of the method)."""
 import ctypes
 import os
+import random
 import re
 
 import numpy as np
@@ -394,3 +395,38 @@ def test_binding_validates_device_buffers():
         assert e.value.code == mr.MR_ERR_ARG, why
     with pytest.raises(mr.MrError):
         mr.mr_modexp_batch(ctypes.c_void_p(12345), ok, ok, 10, 3)        # handle not created here
+
+
+@pytest.mark.parametrize("k", [17, 33, 49, 65])
+def test_fractional_alpha_bound(k):
+    """reading R2b: the tensor kernels take α' = floor(Σ_j ξ'_j / m'_j) as (Σ_j (ξ'_j >> 8) + 2^14) >> 24.  Exact iff
+    (1) the approximation error stays below the 2^-10 offset: Σ_j ξ'_j/m'_j - Σ_j (ξ'_j >> 8)/2^24 < k (max c'_j/m'_j
+    + 2^-24) for lazy ξ'_j < 2^32, and (2) r/M' + 2^-10 < 1 for every value r < (2k+3)N that is extended, with N the
+    largest modulus ctx_create admits ((k+2)^2 N < M, (k+2) N < M').  Checked from the base primes, plus brute force of
+    the formula on random residue vectors of values r near the bound (exact rational arithmetic)."""
+    from fractions import Fraction
+    _, primes, _ = _tables(k)
+    B, Bp = primes[:k], primes[k:]
+    M, Mp = 1, 1
+    for m in B:
+        M *= m
+    for m in Bp:
+        Mp *= m
+    err = sum(Fraction((1 << 32) - m, m) + Fraction(1, 1 << 24) for m in Bp)
+    assert err < Fraction(1, 1 << 10)
+    nmax = min((M - 1) // (k + 2) ** 2, (Mp - 1) // (k + 2))
+    assert Fraction((2 * k + 3) * nmax, Mp) + Fraction(1, 1 << 10) < 1
+    rng = random.Random(k)
+    for _ in range(200):
+        r = rng.randrange((2 * k + 3) * nmax)
+        # lazy ξ'_j: the canonical value or + m'_j when that still fits 32 bits
+        xs = []
+        for m in Bp:
+            Mj = Mp // m
+            x = r * pow(Mj, -1, m) % m
+            if x + m < (1 << 32) and rng.random() < 0.5:
+                x += m
+            xs.append(x)
+        alpha = (sum(x >> 8 for x in xs) + (1 << 14)) >> 24
+        exact = sum(x * (Mp // m) for x, m in zip(xs, Bp)) - r
+        assert exact % Mp == 0 and exact // Mp == alpha
