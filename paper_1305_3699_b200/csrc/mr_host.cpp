@@ -287,8 +287,8 @@ static const Base &base_for(int k) {
         const u32 m = b.Bp[j], c = 0u - m;
         f[L.XW + j] = mulm(mulm(f[L.C1 + j], c, m), c, m);
     }
-    if (tc_nt(k) < (u32)k)
-        for (int j = 0; j < k; j++) f[L.A2C + j] = f[L.A2 + j * k + tc_nt(k)];   // |M'_j|_{m_TCNT}
+    if (tc_nt_mr(k) < (u32)k)   // the CUDA-core output column of the Miller-Rabin kernel's BE2
+        for (int j = 0; j < k; j++) f[L.A2C + j] = f[L.A2 + j * k + tc_nt_mr(k)];   // |M'_j|_{m_TCNT}
     b.pow.assign((size_t)k * 2 * k, 0);
     for (int l = 0; l < k; l++) {
         Big p2 = pow2(32 * l);
@@ -340,11 +340,11 @@ static void to_rns_host(const Base &b, const Big &x, u32 *out) {
 // path); the kernel puts α' (< 2^7) in that A column, so the MMA adds the Shenoy-Kumaresan term.
 // col1 (scaled BE1): k byte 4k + 1 holds byte b of col1[j], the constant offset of the sign-folded digits;
 // the kernel keeps a 1 in that A column.
-static void fill_tc_image(int k, const u32 *A /* [k][k], row i, column j */, const std::vector<u32> &mods,
+static void fill_tc_image(int k, int nt, const u32 *A /* [k][k], row i, column j */, const std::vector<u32> &mods,
                           uint8_t *out, const u32 *col0 = nullptr, const u32 *col1 = nullptr) {
     static_assert(tc_kp(33) >= 4 * 33 + 4 && tc_kp(65) >= 4 * 65 + 4, "a spare K byte column for α'");
-    memset(out, 0, tc_bbytes(k));
-    for (int j = 0; j < (int)tc_nt(k); j++) {
+    memset(out, 0, (size_t)tc_np_of((u32)nt) * tc_kp(k));
+    for (int j = 0; j < nt; j++) {
         for (int i = 0; i < k; i++)
             for (int a = 0; a < 4; a++) {
                 const u32 v = (u32)(((u64)A[i * k + j] << (8 * a)) % mods[j]);
@@ -496,12 +496,12 @@ static int ensure_device_base(int k, int device, const u32 **d_pow, const u32 **
         return MR_ERR_CUDA;
     if (tc_ok(k)) {   // tensor BE2 image of A2 as [input j][output i]
         const u32 *A2 = b.flat.data() + base_layout(k).A2;   // row j, column i
-        std::vector<uint8_t> img(tc_bbytes(k));
+        std::vector<uint8_t> img(tc_bbytes_mr(k));   // the per-k images serve the Miller-Rabin kernel
         if (4 * k + 4 > (int)tc_kp(k)) return MR_ERR_ARG;   // no spare K column for α' (not a supported k)
-        fill_tc_image(k, A2, b.B, img.data(), b.flat.data() + base_layout(k).pin);
+        fill_tc_image(k, (int)tc_nt_mr(k), A2, b.B, img.data(), b.flat.data() + base_layout(k).pin);
         if (cudaMalloc(&db.d_tcb2, img.size()) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_tcb2, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
-        fill_tc_image(k, b.flat.data() + base_layout(k).A1, b.Bp, img.data());
+        fill_tc_image(k, (int)tc_nt_mr(k), b.flat.data() + base_layout(k).A1, b.Bp, img.data());
         if (cudaMalloc(&db.d_tcb1u, img.size()) != cudaSuccess) return MR_ERR_NOMEM;
         if (cudaMemcpy(db.d_tcb1u, img.data(), img.size(), cudaMemcpyHostToDevice) != cudaSuccess) return MR_ERR_CUDA;
     }
@@ -700,14 +700,14 @@ static bool fill_tc_scaled(const Base &b, u32 *x) {
         for (int i = 0; i < k; i++) A1t[(size_t)i * k + j] = mulm(A1s[(size_t)i * k + j], cj, mj);
         offt[j] = mulm(off[j], cj, mj);
     }
-    fill_tc_image(k, A1t.data(), b.Bp, img1, nullptr, offt.data());
+    fill_tc_image(k, nt, A1t.data(), b.Bp, img1, nullptr, offt.data());
     // BE2: |M'_j|_{m_i} ρ_i c_i (row j, column i) and the α' column (m_i - |M'|_{m_i}) ρ_i c_i
     std::vector<u32> A2s((size_t)k * k), pins(k);
     for (int j = 0; j < k; j++)
         for (int i = 0; i < k; i++)
             A2s[(size_t)j * k + i] = mulm(mulm(A2[j * k + i], rho[i], b.B[i]), 0u - b.B[i], b.B[i]);
     for (int i = 0; i < k; i++) pins[i] = mulm(mulm(pin[i], rho[i], b.B[i]), 0u - b.B[i], b.B[i]);
-    fill_tc_image(k, A2s.data(), b.B, reinterpret_cast<uint8_t *>(x + cx_words(k) + be_half_words(k) + tcw),
+    fill_tc_image(k, nt, A2s.data(), b.B, reinterpret_cast<uint8_t *>(x + cx_words(k) + be_half_words(k) + tcw),
                   pins.data());
     return true;
 }

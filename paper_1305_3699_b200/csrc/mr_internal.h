@@ -120,13 +120,24 @@ __host__ __device__ constexpr u32 tc_kp(u32 k) { return (4 * k + 31) & ~31u; }  
 // outputs of each base extension computed on the tensor core; for k = 33 the 33rd output runs on the
 // CUDA cores so that N = 128 columns and four 128-message tiles fit the 512 TMEM columns of an SM;
 // for k = 65 the 65th, so that N = 256 (the largest MMA N) covers the other 64
+// k = 33, modexp kernel: all 33 outputs on the tensor core (N = 144; four tiles share three TMEM accumulator slots,
+// mr_kernels.cuh MR_TC_SLOTS) — 32 is the A/B alternative with the 33rd output on the CUDA cores (N = 128, a fixed
+// accumulator per tile).  The Miller-Rabin kernel keeps 32 (MR_TC_NT33_MR): with per-candidate constants its 4-tile
+// build spills heavily at N = 144 and 3 tiles are 36 % slower (profiles/r2r/ab.log).
 #ifndef MR_TC_NT33
-#define MR_TC_NT33 32       // A/B hook: 33 puts every k = 33 output on the tensor core (N = 144, 3 tiles per SM)
+#define MR_TC_NT33 33
 #endif
-__host__ __device__ constexpr u32 tc_nt(u32 k) {
-    return (4 * k > 128 && 4 * k <= 136) ? MR_TC_NT33 : ((4 * k > 256 && 4 * k <= 264) ? 64 : k);
+#ifndef MR_TC_NT33_MR
+#define MR_TC_NT33_MR 32
+#endif
+__host__ __device__ constexpr u32 tc_nt_for(u32 k, u32 nt33) {
+    return (4 * k > 128 && 4 * k <= 136) ? nt33 : ((4 * k > 256 && 4 * k <= 264) ? 64 : k);
 }
-__host__ __device__ constexpr u32 tc_np(u32 k) { return (4 * tc_nt(k) + 15) & ~15u; }  // N rows, multiple of 16
+__host__ __device__ constexpr u32 tc_nt(u32 k) { return tc_nt_for(k, MR_TC_NT33); }         // modexp kernel
+__host__ __device__ constexpr u32 tc_nt_mr(u32 k) { return tc_nt_for(k, MR_TC_NT33_MR); }   // Miller-Rabin kernel
+__host__ __device__ constexpr u32 tc_np_of(u32 nt) { return (4 * nt + 15) & ~15u; }          // N rows, multiple of 16
+__host__ __device__ constexpr u32 tc_np(u32 k) { return tc_np_of(tc_nt(k)); }
+__host__ __device__ constexpr u32 tc_np_mr(u32 k) { return tc_np_of(tc_nt_mr(k)); }
 // CTA-pair mode: the two B images of k = 65 (2 x 72 KB) do not fit one CTA next to two
 // tiles, so a 2-CTA cluster runs M = 256 MMAs (tcgen05 cta_group::2) and each CTA holds half of the
 // B rows (N/2 = 128 of the (j, b) columns); each CTA's TMEM still receives all N columns of its rows.
@@ -137,6 +148,7 @@ __host__ __device__ constexpr u32 tc_off(u32 k, u32 r, u32 kb) {
     return (r / 8) * tc_sbo(k) + (kb / 16) * 128 + (r % 8) * 16 + kb % 16;
 }
 __host__ __device__ constexpr u32 tc_bbytes(u32 k) { return tc_np(k) * tc_kp(k); }   // one B image
+__host__ __device__ constexpr u32 tc_bbytes_mr(u32 k) { return tc_np_mr(k) * tc_kp(k); }   // ... of the Miller-Rabin kernel
 __host__ __device__ constexpr u32 tc_abytes(u32 k) { return 128 * tc_kp(k); }        // one A tile
 
 // ---------------------------------------------------------------------------------------------

@@ -602,6 +602,10 @@ constexpr int TCNC = K - TCNT;                                  // outputs on th
 static_assert(TCNC <= 1, "at most one CUDA-core output per base extension");
 static_assert(TCNC == 0 || (TCNT + 1 == K && TCNT % 4 == 0), "α' word K sits right after the CUDA-core output");
 static_assert(TCNT % 4 == 0 || TCNC == 0, "tensor outputs must fill whole 16-column groups when split");
+// the Miller-Rabin kernel's split (mr_internal.h tc_nt_mr)
+constexpr int TCNT_MR = tc_nt_mr(K), TCNC_MR = K - TCNT_MR;
+constexpr u32 TCNP_MR = tc_np_mr(K);
+static_assert(TCNC_MR <= 1 && (TCNC_MR == 0 || (TCNT_MR + 1 == K && TCNT_MR % 4 == 0)), "Miller-Rabin output split");
 constexpr u32 BEV_ = BEW - bev_c(K);
 constexpr u32 TC_ROWS = (K + 1) * 128;                          // B' and m_r rows of a tile (words)
 constexpr u32 TC_CVEC = 2 * pad4(K);                            // CUDA-core output columns: A1' col, A2 col
@@ -609,14 +613,24 @@ constexpr size_t tc_smem_for(int tiles) {
     return 4 * (size_t)(tiles * TC_ROWS + BEV_ + CXW + TC_CVEC) + (size_t)tiles * tc_abytes(K) +
            2 * (size_t)TC_BB + 128;
 }
-constexpr bool tc_fits(int tiles) { return tc_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
+#ifndef MR_TC_SLOTS
+// 1: when the tiles' accumulators exceed the 512 TMEM columns (k = 33 with all 33 outputs on the tensor core: 4 x 144),
+// the tiles of a CTA share 512 / NP accumulator slots, each taken from BE1's MMA issue to the end of BE2's epilogue
+// (the channel products, a third of a multiplication, need none), so all four tiles still fit
+#define MR_TC_SLOTS 1
+#endif
+constexpr bool tc_fits(int tiles) {
+    return tc_smem_for(tiles) <= 232448 && ((u32)tiles * TCNP <= 512 || (MR_TC_SLOTS && !PAIR && tiles <= 4));
+}
 // tiles per CTA: as many as fit the 227 KB of shared memory and the 512 TMEM columns (at most 4)
 constexpr int TCT = tc_fits(4) ? 4 : (tc_fits(3) ? 3 : (tc_fits(2) ? 2 : 1));
 static_assert(tc_smem_for(TCT) <= 232448, "tensor-core tile does not fit shared memory");
 constexpr u32 TC_M = PAIR ? 256u : 128u;
 constexpr u32 TC_IDESC = (2u << 4) | ((TCNP >> 3) << 17) | ((TC_M >> 4) << 24);  // s32 = u8 x u8, K-major
 constexpr u32 tmem_cols_for(u32 n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
-constexpr u32 TC_TMEM_COLS = tmem_cols_for(TCT * TCNP);   // power of two >= 32
+// shared accumulator slots per CTA (0: every tile owns its accumulator)
+constexpr u32 TC_NSLOT = (u32)TCT * TCNP <= 512 ? 0u : 512u / TCNP;
+constexpr u32 TC_TMEM_COLS = tmem_cols_for(TC_NSLOT ? TC_NSLOT * TCNP : TCT * TCNP);   // power of two >= 32
 constexpr u32 BEV = BEV_;                                      // the per-channel vectors of the BE image
 constexpr size_t TC_SMEM = tc_smem_for(TCT);
 
@@ -652,9 +666,48 @@ struct TcTile {
     u32 rbar;                         // cluster-window address of rank 0's ready mbarrier for this tile
     u32 rphase;                       // its phase parity (rank 0 leader)
     bool issuer;                      // leader && (rank 0 || !PAIR)
+    // shared accumulator slots (TC_NSLOT / TC_MR_NSLOT != 0): free-slot mask of the CTA, this tile's slot word
+    u32 *pool = nullptr;
+    u32 *myslot = nullptr;
+    u32 tbase = 0;                    // TMEM base of the CTA's allocation
+    u32 idesc = TC_IDESC;             // MMA instruction descriptor (N of this kernel's images)
 };
 
+// Shared accumulator slots: the tile leader takes a free slot before BE1's MMA issue (the tile barrier inside tc_issue
+// then publishes it to the tile), the tile gives it back once every thread's TMEM reads of BE2 are done.  A tile holds
+// at most one slot and never waits while holding one, so the pool cannot deadlock.
+__device__ __forceinline__ void acc_acquire(TcTile &t, u32 np) {
+    if (!t.pool || !t.leader) return;
+    u32 sl = 0;
+#pragma unroll 1
+    for (u32 spin = 0;; spin++) {
+        const u32 f = *reinterpret_cast<volatile u32 *>(t.pool);
+        if (f) {
+            sl = __ffs(f) - 1;
+            if (atomicAnd(t.pool, ~(1u << sl)) & (1u << sl)) break;
+        } else {
+            __nanosleep(32);
+        }
+        if (spin > (1u << 28)) __trap();
+    }
+    __threadfence_block();
+    *reinterpret_cast<volatile u32 *>(t.myslot) = sl;
+    t.tmem = t.tbase + sl * np;
+}
+__device__ __forceinline__ void acc_bind(TcTile &t, u32 np) {   // after tc_issue's tile barrier
+    if (t.pool && !t.leader) t.tmem = t.tbase + *reinterpret_cast<volatile u32 *>(t.myslot) * np;
+}
+__device__ __forceinline__ void acc_release(TcTile &t, u32 np);
+
 __device__ __forceinline__ void tile_sync(const TcTile &t) { asm volatile("bar.sync %0, 128;" ::"r"(t.bar) : "memory"); }
+__device__ __forceinline__ void acc_release(TcTile &t, u32 np) {   // after tcgen05.fence::before_thread_sync
+    if (!t.pool) return;
+    tile_sync(t);
+    if (t.leader) {
+        __threadfence_block();
+        atomicOr(t.pool, 1u << ((t.tmem - t.tbase) / np));
+    }
+}
 
 // issue the K-steps of one base extension (tile leader) after the A tile is complete
 __device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
@@ -690,12 +743,12 @@ __device__ __forceinline__ void tc_issue(TcTile &t, const uint8_t *bimg) {
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t.tmem),
-                    "l"(da), "l"(db), "r"(TC_IDESC), "r"(ks) : "memory");
+                    "l"(da), "l"(db), "r"(t.idesc), "r"(ks) : "memory");
             else
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(t.tmem),
-                    "l"(da), "l"(db), "r"(TC_IDESC), "r"(ks) : "memory");
+                    "l"(da), "l"(db), "r"(t.idesc), "r"(ks) : "memory");
         }
         if (PAIR)           // completion to the same mbarrier offset in both CTAs
             asm volatile(
@@ -863,7 +916,13 @@ __device__ __forceinline__ u32 mulop_ld(const u32 *p) {
     else return *p;
 }
 
-struct MulTc {
+// NT_ = outputs of each base extension on the tensor core (the rest, at most one, on the CUDA cores); the member
+// constants below shadow the modexp kernel's namespace-level ones inside the body
+template <int NT_>
+struct MulTcT {
+    static constexpr int TCNT = NT_;
+    static constexpr int TCNC = K - NT_;
+    static constexpr u32 TCNP = tc_np_of(NT_);
     const u32 *s_be;
     const u32 *s_a1c;                 // CUDA-core output column of BE1: A1'[i][TCNT] (this context)
     const u32 *s_a2c;                 // CUDA-core output column of BE2: A2[j][TCNT]
@@ -1030,7 +1089,9 @@ struct MulTc {
 #else
         const u32 rr = FRAC ? 0u : tr * GB(O_MISC + 0) + qr * cs.nminv();
         // ---- 6.3-6.5 BE1 on the tensor core (merged image: ξ'_j = t*_j C1_j + Σ_i ξ_i A1'_ij)
+        acc_acquire(t, TCNP);
         tc_issue(t, t.b1);
+        acc_bind(t, TCNP);
 #endif
         u32 xp_c = 0;
         if (TCNC) {   // the CUDA-core output overlaps the MMA
@@ -1200,8 +1261,11 @@ struct MulTc {
         }
         if (TCNC) *reinterpret_cast<uint4 *>(arow + (TCNT / 4) * 128) = make_uint4(r_c, 0u, 0u, 0u);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        acc_release(t, TCNP);
     }
 };
+using MulTc = MulTcT<TCNT>;        // modexp kernel
+using MulTcMr = MulTcT<TCNT_MR>;   // Miller-Rabin kernel
 
 __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P) {
     extern __shared__ __align__(1024) u32 smem[];
@@ -1251,6 +1315,8 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
         reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(g_b1 + w);
         reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(g_b2 + w);
     }
+    __shared__ u32 s_pool, s_myslot[TCT];            // shared accumulator slots (TC_NSLOT != 0)
+    if (tid == 0) s_pool = (1u << TC_NSLOT) - 1u;
     if (tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
     if (PAIR && tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(mbar + TCT + tid)));
     if (tid < 32) {
@@ -1277,7 +1343,8 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     // CUDA-core output columns of the scaled path come from the context block (cx_a1x via CtxTc, cx_a2s)
     MulTc mm{s_be, s_a1c, s_cx + cx_a2s(K), TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
                                                  smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, rbar, 0u,
-                                                 m == 0 && rank == 0}};
+                                                 m == 0 && rank == 0, TC_NSLOT ? &s_pool : nullptr,
+                                                 s_myslot + tile, tmem_base}};
     // per-message state: B channels in the A tile row, B' and m_r in the tile's rows
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
@@ -1798,18 +1865,21 @@ __device__ __forceinline__ bool x_is_nm1_t(const StTile &st, const CtxMr &cs) {
 
 constexpr size_t tc_mr_smem_for(int tiles) {
     return 4 * (size_t)(tiles * TC_ROWS + BEV + pad4(NCH) + 3 * pad4(K)) +
-           (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes(K) + 64;
+           (size_t)tiles * tc_abytes(K) + 2 * (size_t)tc_bbytes_mr(K) + 64;
 }
-constexpr bool tc_mr_fits(int tiles) { return tc_mr_smem_for(tiles) <= 232448 && (u32)tiles * TCNP <= 512; }
+constexpr bool tc_mr_fits(int tiles) {
+    return tc_mr_smem_for(tiles) <= 232448 && ((u32)tiles * TCNP_MR <= 512 || (MR_TC_SLOTS && !PAIR && tiles <= 4));
+}
 constexpr int TCM = tc_mr_fits(4) ? 4 : (tc_mr_fits(3) ? 3 : (tc_mr_fits(2) ? 2 : 1));   // MR tiles per CTA
-constexpr u32 TC_MR_TMEM = tmem_cols_for(TCM * TCNP);
+constexpr u32 TC_MR_NSLOT = (u32)TCM * TCNP_MR <= 512 ? 0u : 512u / TCNP_MR;   // shared accumulator slots (0: per tile)
+constexpr u32 TC_MR_TMEM = tmem_cols_for(TC_MR_NSLOT ? TC_MR_NSLOT * TCNP_MR : TCM * TCNP_MR);
 
 __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P) {
     extern __shared__ __align__(1024) u32 smem[];
     // layout: [B1 (unmerged, per k) | B2 | A tiles | state rows | vectors | ONE | a1c | a2c | mbar]
     uint8_t *s_b1 = reinterpret_cast<uint8_t *>(smem);
-    uint8_t *s_b2 = s_b1 + tc_bbytes(K);
-    uint8_t *s_a = s_b2 + tc_bbytes(K);
+    uint8_t *s_b2 = s_b1 + tc_bbytes_mr(K);
+    uint8_t *s_a = s_b2 + tc_bbytes_mr(K);
     u32 *st_all = reinterpret_cast<u32 *>(s_a + TCM * tc_abytes(K));
     u32 *s_vec = st_all + TCM * TC_ROWS;
     u32 *s_be = s_vec - bev_c(K);
@@ -1827,15 +1897,17 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
         const u32 c = s_be[bev_c(K) + K + j];
         s_c1c[j] = canon(mulmod(s_be[bev_C1(K) + j], c, c), c);
     }
-    if (TCNC)
+    if (TCNC_MR)
         for (u32 i = tid; i < (u32)K; i += blockDim.x) {
-            s_a1c[i] = __ldg(P.be_tab + be_img_index(i, TCNT));
-            s_a2c[i] = __ldg(P.be_tab + BEH + be_img_index(i, TCNT));
+            s_a1c[i] = __ldg(P.be_tab + be_img_index(i, TCNT_MR));
+            s_a2c[i] = __ldg(P.be_tab + BEH + be_img_index(i, TCNT_MR));
         }
-    for (u32 w = tid; w < tc_bbytes(K) / 16; w += blockDim.x) {
+    for (u32 w = tid; w < tc_bbytes_mr(K) / 16; w += blockDim.x) {
         reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b1) + w);
         reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b2) + w);
     }
+    __shared__ u32 s_pool, s_myslot[TCM];            // shared accumulator slots (TC_MR_NSLOT != 0)
+    if (tid == 0) s_pool = (1u << TC_MR_NSLOT) - 1u;
     if (tid < (u32)TCM) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
     if (tid < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -1848,8 +1920,10 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem_base = *tslot;
 
-    MulTc mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
-                                        smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, 0u, 0u, m == 0}};
+    MulTcMr mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP_MR,
+                                        smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, 0u, 0u, m == 0,
+                                        TC_MR_NSLOT ? &s_pool : nullptr, s_myslot + tile, tmem_base,
+                                        (2u << 4) | ((TCNP_MR >> 3) << 17) | ((128u >> 4) << 24)}};
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
     const size_t cnt = P.count;
