@@ -671,6 +671,7 @@ struct TcTile {
     u32 *myslot = nullptr;
     u32 tbase = 0;                    // TMEM base of the CTA's allocation
     u32 idesc = TC_IDESC;             // MMA instruction descriptor (N of this kernel's images)
+    u32 *relcnt = nullptr;            // warps of the tile done with the slot (MR_TC_RELWARP)
 };
 
 // Shared accumulator slots: the tile leader takes a free slot before BE1's MMA issue (the tile barrier inside tc_issue
@@ -700,12 +701,28 @@ __device__ __forceinline__ void acc_bind(TcTile &t, u32 np) {   // after tc_issu
 __device__ __forceinline__ void acc_release(TcTile &t, u32 np);
 
 __device__ __forceinline__ void tile_sync(const TcTile &t) { asm volatile("bar.sync %0, 128;" ::"r"(t.bar) : "memory"); }
+#ifndef MR_TC_RELWARP
+#define MR_TC_RELWARP 0     // 1: each warp counts itself out of the slot, the last one frees it, no tile barrier (A/B: 1 % slower on C2)
+#endif
 __device__ __forceinline__ void acc_release(TcTile &t, u32 np) {   // after tcgen05.fence::before_thread_sync
     if (!t.pool) return;
+    const u32 bit = 1u << (((t.tmem & 0xFFFFu) - (t.tbase & 0xFFFFu)) / np);
+    if (MR_TC_RELWARP && t.relcnt) {
+        __syncwarp();
+        if ((t.m & 31) == 0) {
+            __threadfence_block();
+            if (atomicAdd(t.relcnt, 1u) == 3u) {   // the tile's fourth warp: every TMEM read of the slot is done
+                *reinterpret_cast<volatile u32 *>(t.relcnt) = 0u;
+                __threadfence_block();
+                atomicOr(t.pool, bit);
+            }
+        }
+        return;
+    }
     tile_sync(t);
     if (t.leader) {
         __threadfence_block();
-        atomicOr(t.pool, 1u << ((t.tmem - t.tbase) / np));
+        atomicOr(t.pool, bit);
     }
 }
 
@@ -1315,8 +1332,9 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
         reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(g_b1 + w);
         reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(g_b2 + w);
     }
-    __shared__ u32 s_pool, s_myslot[TCT];            // shared accumulator slots (TC_NSLOT != 0)
+    __shared__ u32 s_pool, s_myslot[TCT], s_relcnt[TCT];   // shared accumulator slots (TC_NSLOT != 0)
     if (tid == 0) s_pool = (1u << TC_NSLOT) - 1u;
+    if (tid < (u32)TCT) s_relcnt[tid] = 0u;
     if (tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
     if (PAIR && tid < (u32)TCT) asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(mbar + TCT + tid)));
     if (tid < 32) {
@@ -1344,7 +1362,7 @@ __global__ void __launch_bounds__(TCT * 128, 1) k_modexp_tc(const ModexpParams P
     MulTc mm{s_be, s_a1c, s_cx + cx_a2s(K), TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP,
                                                  smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, rbar, 0u,
                                                  m == 0 && rank == 0, TC_NSLOT ? &s_pool : nullptr,
-                                                 s_myslot + tile, tmem_base}};
+                                                 s_myslot + tile, tmem_base, TC_IDESC, s_relcnt + tile}};
     // per-message state: B channels in the A tile row, B' and m_r in the tile's rows
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
@@ -1906,8 +1924,9 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
         reinterpret_cast<uint4 *>(s_b1)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b1) + w);
         reinterpret_cast<uint4 *>(s_b2)[w] = __ldg(reinterpret_cast<const uint4 *>(P.tc_b2) + w);
     }
-    __shared__ u32 s_pool, s_myslot[TCM];            // shared accumulator slots (TC_MR_NSLOT != 0)
+    __shared__ u32 s_pool, s_myslot[TCM], s_relcnt[TCM];   // shared accumulator slots (TC_MR_NSLOT != 0)
     if (tid == 0) s_pool = (1u << TC_MR_NSLOT) - 1u;
+    if (tid < (u32)TCM) s_relcnt[tid] = 0u;
     if (tid < (u32)TCM) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + tid)));
     if (tid < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -1923,7 +1942,7 @@ __global__ void __launch_bounds__(TCM * 128, 1) k_mr_rounds_tc(const MrParams P)
     MulTcMr mm{s_be, s_a1c, s_a2c, TcTile{s_a + tile * tc_abytes(K), s_b1, s_b2, tmem_base + tile * TCNP_MR,
                                         smem_u32(mbar + tile), 0u, 1 + (int)tile, m == 0, m, 0u, 0u, m == 0,
                                         TC_MR_NSLOT ? &s_pool : nullptr, s_myslot + tile, tmem_base,
-                                        (2u << 4) | ((TCNP_MR >> 3) << 17) | ((128u >> 4) << 24)}};
+                                        (2u << 4) | ((TCNP_MR >> 3) << 17) | ((128u >> 4) << 24), s_relcnt + tile}};
     uint8_t *tile_a = s_a + tile * tc_abytes(K);
     const StTile st{tile_a + (m / 8) * TCSBO + (m % 8) * 16, st_all + tile * TC_ROWS + m};
     const size_t cnt = P.count;

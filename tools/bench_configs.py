@@ -84,7 +84,8 @@ def c3(torch, mr, orc, quick):
     n = k["n"]
     ctx = mr.RnsContext(n, 96)
     priv = mr.RsaPrivateKey(k["p"], k["q"], k["dp"], k["dq"], k["qinv"])
-    sizes = [1024, 4096, 16384] if quick else [1024, 4096, 16384, 65536]
+    # BASELINE configs[2]: the 1K-1M sweep (one GPU here; bench.py --total T --gpus N shards it)
+    sizes = [1024, 4096, 16384] if quick else [1024, 4096, 16384, 65536, 262144, 1048576]
     for cnt in sizes:
         msgs = synth.messages(n, cnt, 0x5EEDC003, 96, edge=synth.edge_values(n, k["p"], k["q"]))
         x = torch.from_numpy(msgs.view(np.int32)).cuda()
