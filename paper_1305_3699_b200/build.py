@@ -58,7 +58,7 @@ def build(force: bool = False, jobs: int | None = None) -> str:
         objs.append(obj)
         if force or _stale(obj, [src] + deps):
             steps.append(([NVCC] + NVFLAGS + ["-c", src, "-o", obj], obj + ".log"))
-    for cu in ("mr_keygen", "mr_wide", "mr_lanes", "mr_drbg", "mr_tcw257"):
+    for cu in ("mr_keygen", "mr_wide", "mr_lanes", "mr_drbg", "mr_tcw257", "mr_tcw505"):
         src = os.path.join(CSRC, cu + ".cu")
         obj = os.path.join(OBJ, cu + ".o")
         objs.append(obj)

@@ -37,6 +37,8 @@ int launch_modexp_wide(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u
 // the tensor-core wide kernel at k = 257 (mr_tcw257.cu; k = 97 / 129 come with their per-k kernel sets)
 int launch_modexp_tcw_k257(const ModexpParams &p, u32 ctas, const u32 *tab, const void *kimg, u32 cxw, u32 be1w, u32 jobs,
                            void *trace, void *stream);
+int launch_modexp_tcw_k505(const ModexpParams &p, u32 ctas, const u32 *tab, const void *kimg, u32 cxw, u32 be1w, u32 jobs,
+                           void *trace, void *stream);
 int wide_messages_per_cta_lanes();
 int launch_modexp_wide_lanes(const ModexpParams &p, u32 ctas, const u32 *d_wide_tab, u32 k, u32 cxw, void *stream);
 int launch_combine_wide(const CombineParams &p, const u32 *d_qinv, u32 *d_scratch, u32 k, void *stream);
@@ -1125,24 +1127,26 @@ static int launch_ladders_tcw(mr_rns_ctx *const *ctxs, const DevProg *progs, int
                                                 void *)) {
     const mr_rns_ctx *c0 = ctxs[0];
     cudaStream_t st = (cudaStream_t)stream;
-    u32 ctas0 = (u32)((count + 127) / 128);
-    if (TCW_LOCK || TCW_PAIR) ctas0 += ctas0 & 1u;   // lockstep tiles / CTA pairs take job pairs of one context
+    const u32 tm = tcw_m((u32)c0->k);                // messages per tile-job (k = 505: 64)
+    u32 ctas0 = (u32)((count + tm - 1) / tm);
+    if (TCW_LOCK || (TCW_PAIR && tm == 128)) ctas0 += ctas0 & 1u;   // lockstep tiles / CTA pairs: job pairs of one context
     const u32 jobs = ctas0 * (u32)nctx;
-    const u32 jobs_total = ctas0 * 128 * (u32)nctx;
+    const u32 jobs_total = ctas0 * tm * (u32)nctx;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c0->device);
     static const int max_sms = [] { const char *e = getenv("MR_RNS_MAX_SMS"); return e ? atoi(e) : 0; }();
     if (max_sms > 0) sms = std::min(sms, std::max(1, max_sms));
     const u32 tiles = tcw_tiles((u32)c0->k);
     // CTA pairs (2-CTA clusters): each cluster runs `tiles` pair-jobs (256 messages each) at a time
-    const u32 grid = TCW_PAIR ? 2 * std::min<u32>(std::max(1, sms / 2), (jobs / 2 + tiles - 1) / tiles)
+    const u32 grid = (TCW_PAIR && tm == 128) ? 2 * std::min<u32>(std::max(1, sms / 2), (jobs / 2 + tiles - 1) / tiles)
                               : std::min<u32>((u32)sms, (jobs + tiles - 1) / tiles);
     int w = 1;
     for (int i = 0; i < nctx; i++) w = std::max(w, progs[i].w);
     const size_t nch = 2 * (size_t)c0->k + 1;
     u32 *d_table = nullptr;
-    // window table + one spare slot (to_rns parks its B' outputs there, mr_tcw.cuh)
-    if (cudaMallocAsync(&d_table, (size_t)(table_slots(w) + 1) * nch * jobs_total * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
+    // window table + one spare slot (to_rns parks its B' outputs there, mr_tcw.cuh) [+ the B-residue slot, k = 505]
+    const size_t slots = (size_t)table_slots(w) + 1 + (tcw_bres_tmem((u32)c0->k) ? 0 : 1);
+    if (cudaMallocAsync(&d_table, slots * nch * jobs_total * 4, st) != cudaSuccess) return MR_ERR_NOMEM;
     ModexpParams P;
     memset(&P, 0, sizeof P);
     for (int i = 0; i < 2; i++) {
@@ -1194,7 +1198,9 @@ static int launch_ladders_wide(mr_rns_ctx *const *ctxs, const DevProg *progs, in
     const mr_rns_ctx *c0 = ctxs[0];
     cudaStream_t st = (cudaStream_t)stream;
     if (!lanes && c0->d_tcw && c0->be1w && tcw_enabled()) {
-        auto launch_tcw = c0->k == 257 ? launch_modexp_tcw_k257 : kernel_set_for(c0->k).launch_modexp_tcw;
+        auto launch_tcw = c0->k == 505   ? launch_modexp_tcw_k505
+                          : c0->k == 257 ? launch_modexp_tcw_k257
+                                         : kernel_set_for(c0->k).launch_modexp_tcw;
         if (launch_tcw)
             return launch_ladders_tcw(ctxs, progs, nctx, d_x, in_limbs, half, d_y, out_limbs, count, d_status, stream,
                                       launch_tcw);

@@ -240,12 +240,17 @@ __host__ __device__ constexpr u32 wmr_words(u32 k) { return 8 * k + 9; }
 // bytes in the K-major SWIZZLE_NONE core-matrix layout with SBO = steps_s·256 (LBO = 128).
 // ---------------------------------------------------------------------------------------------
 enum : u32 { TCW_BE1 = 0, TCW_BE2 = 1, TCW_TRN = 2, TCW_EXT = 3 };
-__host__ __device__ constexpr bool tcw_k(u32 k) { return k == 97 || k == 129 || k == 257; }
+__host__ __device__ constexpr bool tcw_k(u32 k) { return k == 97 || k == 129 || k == 257 || k == 505; }
+// messages per tile: at k = 505 a 128-row A tile (2,048-byte rows) would be 256 KB, so the tile is 64 messages and the
+// MMAs are M = 64 (the accumulator then sits in TMEM lanes 16q .. 16q + 15 of each lane quadrant q)
+__host__ __device__ constexpr u32 tcw_m(u32 k) { return k > 257 ? 64u : 128u; }
+// B residues in TMEM (k <= 257) or in an L2-resident global scratch slot (k = 505: they would take 508 columns)
+__host__ __device__ constexpr bool tcw_bres_tmem(u32 k) { return k <= 257; }
 __host__ __device__ constexpr u32 tcw_kp(u32 k) { return (4 * k + 4 + 31) & ~31u; }     // A row bytes (α' word k)
 __host__ __device__ constexpr u32 tcw_ks(u32 k) { return tcw_kp(k) / 32; }               // K-steps
 __host__ __device__ constexpr u32 tcw_nslab(u32 k) { return (tcw_ks(k) + 3) / 4; }
 __host__ __device__ constexpr u32 tcw_steps(u32 k, u32 s) { return s + 1 < tcw_nslab(k) ? 4u : tcw_ks(k) - 4 * s; }
-__host__ __device__ constexpr u32 tcw_bsw(u32 k) { return (k + 3) & ~3u; }              // TMEM columns of B residues
+__host__ __device__ constexpr u32 tcw_bsw(u32 k) { return tcw_bres_tmem(k) ? (k + 3) & ~3u : 0u; }   // TMEM columns of B residues
 __host__ __device__ constexpr u32 tcw_nout(u32 k, u32 e) {
     return e == TCW_BE1 ? k + 1 : e == TCW_BE2 ? k : e == TCW_TRN ? 2 * k : k + 1;
 }

@@ -27,10 +27,12 @@
 // in the window table's spare slot), and the A row is written once all chunks are done.
 #pragma once
 
-#if MR_K == 97 || MR_K == 129 || MR_K == 257
+#if MR_K == 97 || MR_K == 129 || MR_K == 257 || MR_K == 505
 
 constexpr u32 W_TILES = tcw_tiles(K);                 // independent 128-message tiles per CTA (k = 257: one)
 
+constexpr u32 W_M = tcw_m(K);                         // messages per tile (k = 505: 64, M = 64 MMAs)
+constexpr bool W_BT = tcw_bres_tmem(K);               // B residues in TMEM (else the global scratch slot)
 constexpr u32 W_KP = tcw_kp(K);                       // A row bytes
 constexpr u32 W_KC = W_KP / 16;                       // K-cores (4 words) per A row
 constexpr u32 W_SBOA = (W_KP / 16) * 128;             // A tile: bytes between 8-row groups
@@ -39,9 +41,9 @@ constexpr u32 W_BSW = tcw_bsw(K);
 constexpr u32 W_TCOLS = W_NCMAX + W_BSW;              // TMEM columns per tile: [acc | B residues]
 static_assert(W_TILES * W_TCOLS <= 512, "tiles x (accumulator + B residues) exceed the 512 TMEM columns");
 static_assert(W_KC * 4 >= K + 2, "A row must hold B' (k words), α' (word k) and m_r (word k+1)");
-constexpr bool W_PAIR = TCW_PAIR;                     // CTA pairs: M = 256 MMAs, each CTA streams half of every slab
+constexpr bool W_PAIR = TCW_PAIR && W_M == 128;                     // CTA pairs: M = 256 MMAs, each CTA streams half of every slab
 constexpr u32 W_STG = tcw_stage_bytes(K) / (W_PAIR ? 2u : 1u);   // bytes of one stage (pair: the CTA's N/2 rows)
-constexpr u32 W_ABYTES = 128 * W_KP;
+constexpr u32 W_ABYTES = W_M * W_KP;
 constexpr size_t W_FIXED = (size_t)W_TILES * W_ABYTES + 16 * K + 8 * K + 8 * K + 512 + W_TILES * 2048;
 constexpr u32 W_RINGS = TCW_LOCK ? 1 : W_TILES;       // streams of B slabs per CTA
 constexpr u32 W_NST_FIT = (u32)((232448 - W_FIXED) / (W_RINGS * W_STG));
@@ -312,7 +314,7 @@ struct TcwMma {
             tr((e << 4) | 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             // s32 = u8 x u8, K-major, M = 128 (pair: M = 256 over the two CTAs' tiles, N = nc with N/2 B rows per CTA)
-            const u32 idesc = (2u << 4) | ((nc >> 3) << 17) | (((W_PAIR ? 256u : 128u) >> 4) << 24);
+            const u32 idesc = (2u << 4) | ((nc >> 3) << 17) | (((W_PAIR ? 256u : W_M) >> 4) << 24);
 #pragma unroll 1
             for (u32 s = 0; s < tcw_nslab(K); s++) {
                 const u32 steps = tcw_steps(K, s);
@@ -374,6 +376,46 @@ struct TcwCompute {
     __device__ u32 &aw(u32 i) const { return *reinterpret_cast<u32 *>(arow + (i >> 2) * 128 + 4 * (i & 3)); }
     __device__ uint4 &ac(u32 c) const { return *reinterpret_cast<uint4 *>(arow + c * 128); }   // K-core c: words 4c..4c+3
     __device__ u32 tb(u32 col) const { return tmem + col; }
+    // lane 0 of the warp (M = 64: m no longer tells, lanes 16..31 shadow 0..15)
+    __device__ bool lane0() const { return (W_M == 128 ? (m & 31) : (threadIdx.x & 31)) == 0; }
+    // B residues / parked values: TMEM columns bs + c of this message's lane (k <= 257), or rows c of the job's global
+    // scratch slot (k = 505, bres / bstr set per job); bld issues, bwait completes (TMEM loads are asynchronous)
+    u32 *bres = nullptr;
+    size_t bstr = 0;
+    template <int N>
+    __device__ __forceinline__ void bld(u32 c, u32 (&v)[N]) const {
+        if constexpr (W_BT) {
+            if constexpr (N == 16) w_tmem_ld16(tb(bs + c), v);
+            else if constexpr (N == 8) w_tmem_ld8(tb(bs + c), v);
+            else w_tmem_ld4(tb(bs + c), v);
+        } else {
+#pragma unroll
+            for (int i = 0; i < N; i++) v[i] = bres[(size_t)(c + i) * bstr];
+        }
+    }
+    template <int N>
+    __device__ __forceinline__ void bwait(u32 (&v)[N]) const {
+        if constexpr (W_BT) w_tmem_wait(v);
+    }
+    __device__ __forceinline__ void bst4(u32 c, u32 a, u32 b, u32 d, u32 e) const {
+        if constexpr (W_BT) {
+            w_tmem_st4(tb(bs + c), a, b, d, e);
+        } else {
+            bres[(size_t)c * bstr] = a;
+            bres[(size_t)(c + 1) * bstr] = b;
+            bres[(size_t)(c + 2) * bstr] = d;
+            bres[(size_t)(c + 3) * bstr] = e;
+        }
+    }
+    // M = 64 tiles: the accumulator rows of message m sit in lane 32q + (m % 16) of quadrant q, so the upper 16 lanes of a
+    // warp load nothing useful; they take their partner's values and shadow its work (identical stores, no divergence)
+    template <int N>
+    __device__ __forceinline__ void dshare(u32 (&v)[N]) const {
+        if constexpr (W_M == 64) {
+#pragma unroll
+            for (int i = 0; i < N; i++) v[i] = __shfl_sync(0xFFFFFFFFu, v[i], threadIdx.x & 15);
+        }
+    }
     __device__ bool mine16(u32 g) const { return W_HV == 1 || (g & 1u) == h; }   // 16-word / 16-channel group g
     static constexpr u32 GW = (K + 16) / 16;                               // 16-word groups covering words 0 .. K+1
     // both halves of the tile: TMEM stores done, shared / global writes visible
@@ -386,6 +428,11 @@ struct TcwCompute {
     }
     // 16 B columns 16g.. of the tile (the last group stops at W_BSW: the next columns are the other tile's)
     __device__ void st_b16(u32 g, const u32 (&v)[16]) const {
+        if constexpr (!W_BT) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) bst4(16 * g + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            return;
+        }
         if (16 * g + 16 <= W_BSW) {
             w_tmem_st16(tb(bs + 16 * g), v);
         } else {
@@ -400,7 +447,7 @@ struct TcwCompute {
             w_mbar_arrive(T.aready());
         } else {                                                       // one arrival per warp on the leader's barrier
             __syncwarp();
-            if ((m & 31) == 0) w_mbar_arrive_cl(w_lead(T.aready()));
+            if (lane0()) w_mbar_arrive_cl(w_lead(T.aready()));
         }
         trace(0x0F);
     }
@@ -408,7 +455,7 @@ struct TcwCompute {
     __device__ void acc_free() const {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if ((m & 31) == 0) {
+        if (lane0()) {
             if (!W_PAIR || T.rank == 0) w_mbar_arrive(T.acce());
             else w_mbar_arrive_cl(w_lead(T.acce()));
         }
@@ -440,6 +487,8 @@ struct TcwCompute {
                         if (gi + 1 < LG && g1 < n4) w_tmem_ld16(tb(T.tacc + 16 * g1), w);
                         w_tmem_wait(v);
                         if (gi + 1 < LG && g1 < n4) w_tmem_wait(w);
+                        dshare(v);
+                        if (gi + 1 < LG && g1 < n4) dshare(w);
 #pragma unroll
                         for (int t = 0; t < 4; t++) {
                             tc_split(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3], Vl[4 * gi + t], Vh[4 * gi + t]);
@@ -485,7 +534,7 @@ struct TcwCompute {
                         r[t] = mont_red(Vl[4 * gi + t], Vh[4 * gi + t], mm.x, mm.y);
                         if (ch >= K && ch < 2 * K) park[(size_t)(ch - K) * tstride] = r[t];
                     }
-                    if (o < K) w_tmem_st4(tb(bs + o), r[0], r[1], r[2], r[3]);   // straddling group: B' lanes -> padding
+                    if (o < K) bst4(o, r[0], r[1], r[2], r[3]);   // straddling group: B' lanes -> padding
                 }
             }
         });
@@ -513,8 +562,7 @@ struct TcwCompute {
         const uint4 *e1 = ep1 + c0;
         const u32 *sgg = sg + c0;
         u32 r[NW], xa[NW], b1[N], b2[N];
-        if constexpr (NW == 16) w_tmem_ld16(tb(bs + c0), r);
-        else w_tmem_ld8(tb(bs + c0), r);
+        bld(c0, r);
 #pragma unroll
         for (u32 q = 0; q < (N + 3) / 4; q++) {
             const uint4 v = ac(c0 / 4 + q);
@@ -528,7 +576,7 @@ struct TcwCompute {
                 b2[t] = __ldcg(b + (size_t)(K + t) * bs_);
             }
         }
-        w_tmem_wait(r);
+        bwait(r);
         u32 xi[NW], ts[NW];
 #pragma unroll
         for (u32 t = 0; t < NW; t++) xi[t] = ts[t] = 0u;
@@ -544,7 +592,7 @@ struct TcwCompute {
             ts[t] = mont_red((u32)pp, (u32)(pp >> 32), c1.x, c1.y);
         }
 #pragma unroll
-        for (u32 q = 0; q < (N + 3) / 4; q++) w_tmem_st4(tb(bs + c0 + 4 * q), ts[4 * q], ts[4 * q + 1], ts[4 * q + 2], ts[4 * q + 3]);
+        for (u32 q = 0; q < (N + 3) / 4; q++) bst4(c0 + 4 * q, ts[4 * q], ts[4 * q + 1], ts[4 * q + 2], ts[4 * q + 3]);
 #pragma unroll
         for (u32 q = 0; q < (N + 3) / 4; q++) ac(c0 / 4 + q) = make_uint4(xi[4 * q], xi[4 * q + 1], xi[4 * q + 2], xi[4 * q + 3]);
     }
@@ -633,10 +681,11 @@ struct TcwCompute {
                 }
             }
         }
-        static_assert(K % 16 <= 8, "tail channels fit one 8-channel group");
+        static_assert(K % 16 <= 8 || !W_BT, "tail channels fit one 8-channel group (TMEM columns of the tile)");
         if (K % 16 && mine16(K / 16)) chan_group<SQ, K % 16>(16 * (K / 16), bp, bs_, sg);
         const u32 trm = ar * (SQ ? ar : br);
         w_tmem_wait_st();
+        if constexpr (!W_BT) sync();   // t*_j (global) of both halves written before either half's BE1 epilogue
         a_done();
         // ---- 6.3-6.5 BE1 epilogue: ξ'_j = mont(t*_j C1_j 2^64 + D_j) over t*_j in TMEM; m_r column -> r_r
         u32 sr = 0, rr = 0;
@@ -649,10 +698,10 @@ struct TcwCompute {
                 if (g0 < n4) {
                     const u32 oa = o0 + 4 * g0, ob = o0 + 4 * g1;
                     u32 ta[4], tc[4];
-                    w_tmem_ld4(tb(bs + (oa < K ? oa : 0)), ta);
-                    if (gi + 1 < LG1 && g1 < n4) w_tmem_ld4(tb(bs + (ob < K ? ob : 0)), tc);
-                    w_tmem_wait(ta);
-                    if (gi + 1 < LG1 && g1 < n4) w_tmem_wait(tc);
+                    bld(oa < K ? oa : 0, ta);
+                    if (gi + 1 < LG1 && g1 < n4) bld(ob < K ? ob : 0, tc);
+                    bwait(ta);
+                    if (gi + 1 < LG1 && g1 < n4) bwait(tc);
 #pragma unroll
                     for (u32 u = 0; u < 2; u++) {
                         if (gi + u < LG1 && (u == 0 || g1 < n4)) {
@@ -670,7 +719,7 @@ struct TcwCompute {
                                 if (j < K) sr += xp[t] * e1.w;
                                 if (j == K) rr = trm * minv_r + Vl[q] * nminv;   // q̂_r = Σ ξ_i |M_i|_{2^32}
                             }
-                            if (oh < K) w_tmem_st4(tb(bs + oh), xp[0], xp[1], xp[2], xp[3]);   // ξ'_j in place of t*_j
+                            if (oh < K) bst4(oh, xp[0], xp[1], xp[2], xp[3]);   // ξ'_j in place of t*_j
                         }
                     }
                 }
@@ -683,8 +732,8 @@ struct TcwCompute {
 #pragma unroll 1
         for (u32 g = h; g < GW; g += W_HV) {
             u32 v[16];
-            w_tmem_ld16(tb(bs + 16 * g), v);
-            w_tmem_wait(v);
+            bld(16 * g, v);
+            bwait(v);
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 if (4 * g + q < W_KC) {
@@ -712,7 +761,7 @@ struct TcwCompute {
                         const uint2 mm = ep2[o + t < K ? o + t : K - 1];
                         r[t] = mont_red(Vl[4 * gi + t], Vh[4 * gi + t], mm.x, mm.y);
                     }
-                    w_tmem_st4(tb(bs + o), r[0], r[1], r[2], r[3]);
+                    bst4(o, r[0], r[1], r[2], r[3]);
                 }
             }
         });
@@ -747,6 +796,7 @@ struct TcwCompute {
                     u32 v[16];
                     w_tmem_ld16(tb(T.tacc + 16 * g), v);
                     w_tmem_wait(v);
+                    dshare(v);
                     u32 l4[4];
 #pragma unroll
                     for (int t = 0; t < 4; t++) {
@@ -754,7 +804,7 @@ struct TcwCompute {
                         l4[t] = (u32)s;
                         carry = s >> 32;
                     }
-                    w_tmem_st4(tb(bs + o0 + 4 * g), l4[0], l4[1], l4[2], l4[3]);   // limbs (columns < round4(K+1))
+                    bst4(o0 + 4 * g, l4[0], l4[1], l4[2], l4[3]);   // limbs (columns < round4(K+1))
                 }
             }
             acc_free();
@@ -764,8 +814,8 @@ struct TcwCompute {
 #pragma unroll 1
         for (u32 g = 0; g < GW; g++) {
             u32 v[16];
-            w_tmem_ld16(tb(bs + 16 * g), v);
-            w_tmem_wait(v);
+            bld(16 * g, v);
+            bwait(v);
 #pragma unroll
             for (int q = 0; q < 4; q++)
                 if (4 * g + q < W_KC) ac(4 * g + q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -794,7 +844,11 @@ struct TcwCompute {
         const bool ok = valid && less_than(xrow, cx + cx_inb(K), P.in_limbs);
         if (valid && h == 0 && sel == 0 && P.status) P.status[jl] = ok ? 0 : 5 /* MR_ERR_RANGE */;
         const size_t tstride = P.jobs_total, entry = (size_t)NCH * tstride;
-        const u32 col = sel * P.ctas0 * 128 + jl;     // window-table column (tail lanes too: jl < ctas0 * 128)
+        const u32 col = sel * P.ctas0 * W_M + jl;     // window-table column (tail lanes too: jl < ctas0 * W_M)
+        if constexpr (!W_BT) {                         // B residues: the slot after to_rns's parking slot
+            bres = P.table + (size_t)(P.hslot + 1) * entry + col;
+            bstr = tstride;
+        }
         const u64 *prog = sel ? P.prog[1] : P.prog[0];
         const u32 nops = sel ? P.nops[1] : P.nops[0];
         u64 nop = __ldg(prog);
@@ -819,11 +873,11 @@ struct TcwCompute {
 #pragma unroll
                     for (u32 q = 0; q < 4; q++) {
                         const u32 w = 4 * g + q;
-                        if (w < W_BSW / 4) {
+                        if (w < (W_BT ? W_BSW : (K + 3) & ~3u) / 4) {   // B residues: TMEM columns / global rows
                             u32 b4[4];
 #pragma unroll
                             for (int t = 0; t < 4; t++) b4[t] = 4 * w + t < K ? src[(4 * w + t) * str] : 0u;
-                            w_tmem_st4(tb(bs + 4 * w), b4[0], b4[1], b4[2], b4[3]);
+                            bst4(4 * w, b4[0], b4[1], b4[2], b4[3]);
                         }
                         if (w < W_KC) {
                             u32 a4[4];
@@ -848,8 +902,8 @@ struct TcwCompute {
 #pragma unroll 1
                 for (u32 g = h; g < GW; g += W_HV) {
                     u32 a[16];
-                    w_tmem_ld16(tb(bs + 16 * g), a);
-                    w_tmem_wait(a);
+                    bld(16 * g, a);
+                    bwait(a);
 #pragma unroll
                     for (int t = 0; t < 16; t++) {
                         const u32 i = 16 * g + t;
@@ -866,8 +920,8 @@ struct TcwCompute {
 #pragma unroll 1
                 for (u32 g = h; g < GW; g += W_HV) {
                     u32 a[16];
-                    w_tmem_ld16(tb(bs + 16 * g), a);
-                    w_tmem_wait(a);
+                    bld(16 * g, a);
+                    bwait(a);
 #pragma unroll
                     for (int t = 0; t < 16; t++) {
                         const u32 i = 16 * g + t;
@@ -1012,7 +1066,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
             }
         }
     } else {                                          // ---- compute warps of `tile`
-        const u32 m = (warp % 4) * 32 + (tid & 31), h = (warp / 4) % W_HV;
+        const u32 m = (warp % 4) * (W_M / 4) + (tid & 31) % (W_M / 4), h = (warp / 4) % W_HV;   // M = 64: lanes 16..31
+                                                                                               // shadow lanes 0..15
         uint2 *xch = reinterpret_cast<uint2 *>(bars + W_TILES * W_NBAR) + tile * 256;
         TcwCompute cw{T, ep1, ep2, sig, tmem + ((warp % 4) * 32u << 16), T.tacc + W_NCMAX, m, h,
                       T.a + (m / 8) * W_SBOA + (m % 8) * 16, xch, 1 + tile};
@@ -1024,7 +1079,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
             const u32 t = job_of(q);
             cw.sel = t / P.ctas0;
             cw.cx = cw.sel ? P.ctx[1] : P.ctx[0];
-            const u32 jl = (t - cw.sel * P.ctas0) * 128 + m;
+            const u32 jl = (t - cw.sel * P.ctas0) * W_M + m;
             cw.job(P, jl, jl < P.count);
         }
     }
@@ -1072,4 +1127,4 @@ int tcw_launch(const ModexpParams &p, u32 ctas, const TcwArgs &a, void *stream) 
     return e == cudaSuccess ? 0 : 6;
 }
 
-#endif  // MR_K == 97 || MR_K == 129 || MR_K == 257
+#endif  // MR_K == 97 || MR_K == 129 || MR_K == 257 || MR_K == 505

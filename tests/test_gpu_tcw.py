@@ -1,5 +1,5 @@
-"""GPU parity of the tensor-core wide kernel (k_modexp_tcw, mr_tcw.cuh) for k = 97, 129 and 257:
-3072- / 4096- / 8192-bit moduli and the CRT halves of 6144- / 8192- / 16,128-bit keys.  Every case runs on the tensor path and on the
+"""GPU parity of the tensor-core wide kernel (k_modexp_tcw, mr_tcw.cuh) for k = 97, 129, 257 and 505:
+3072- / 4096- / 8192- / 16,128-bit moduli and the CRT halves of 6144- / 8192- / 16,128-bit keys.  Every case runs on the tensor path and on the
 IMAD wide kernel (mr_internal_set_tcw), both compared element by element with the CPU oracle; ragged batches span
 several 128-message tile-jobs, with edge inputs 0, 1, 2, N-1, N-2 and out-of-range inputs (status 5, output 0).
 """
@@ -135,6 +135,38 @@ def test_tcw_k257_paths_identical_full_exponent(torch_cuda, mr):
         assert int.from_bytes(a[i].tobytes(), "little") == pow(xs[i], E, N)
 
 
+@pytest.mark.parametrize("path", PATHS)
+def test_tcw_k505_modexp_vs_oracle(torch_cuda, mr, orc, path):
+    """16,128-bit modulus (k = 505: 64-message tiles, M = 64 MMAs, B residues in the global scratch slot): ragged
+    100-message batch (two tile-jobs, the second with 36) with edge inputs, E = 65537 and a 96-bit E, vs the oracle"""
+    set_path(mr, path)
+    bits = 16128
+    rng = random.Random(bits + 11)
+    N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+    L = bits // 32
+    xs = [0, 1, 2, N - 1, N - 2, 1 << (bits - 2)] + [rng.randrange(N) for _ in range(92)] + [N, N + 7]
+    for E in (65537, rng.getrandbits(96) | (1 << 95)):
+        y, st, ctx = modexp(torch_cuda, mr, N, xs, E, L)
+        assert ctx.k == 505
+        assert st == [0] * 98 + [5, 5] and not y[98:].any()
+        ref = orc.modexp_batch(mr.ints_to_limbs(xs[:98], L), E, N, threads=8)
+        assert np.array_equal(y[:98], ref), (path, E.bit_length())
+
+
+def test_tcw_k505_paths_identical_full_exponent(torch_cuda, mr):
+    """k = 505 tensor path and IMAD wide kernel give identical bytes for a full 16,128-bit exponent (70 messages)"""
+    rng = random.Random(505)
+    N = rng.getrandbits(16128) | (1 << 16127) | 1
+    xs = [rng.randrange(N) for _ in range(70)]
+    E = rng.getrandbits(16128) | (1 << 16127)
+    set_path(mr, "tcw")
+    a, _, _ = modexp(torch_cuda, mr, N, xs, E, 504)
+    set_path(mr, "imad_wide")
+    b, _, _ = modexp(torch_cuda, mr, N, xs, E, 504)
+    assert np.array_equal(a, b)
+    assert int.from_bytes(a[69].tobytes(), "little") == pow(xs[69], E, N)
+
+
 @pytest.mark.parametrize("count", [1, 127, 128, 129])
 def test_tcw_batch_edges(torch_cuda, mr, orc, count):
     """single-tile edge counts at k = 97 (one message; a full tile; one past it)"""
@@ -206,7 +238,7 @@ import random, sys
 import numpy as np, torch
 sys.path.insert(0, {root!r})
 import paper_1305_3699_b200 as mr
-for bits in (3072, 4096, 8192):
+for bits in (3072, 4096, 8192, 16128):
     rng = random.Random(bits + 3)
     N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
     L = bits // 32

@@ -1,4 +1,4 @@
-"""CPU pins of the tensor-core wide kernel's host images (mr_tcw.cuh; k = 97, 129 and 257).
+"""CPU pins of the tensor-core wide kernel's host images (mr_tcw.cuh; k = 97, 129, 257 and 505).
 
 Each image is the byte-split B operand of one contraction (mr_internal.h tcw_*): row (output o, byte b), K byte
 (input word i, byte a) = byte b of 2^(8a) A(i, o) mod m_o.  The test decodes the exported image with an
@@ -42,7 +42,7 @@ def steps(k, s):
 
 
 def bsw(k):
-    return (k + 3) & ~3
+    return (k + 3) & ~3 if k <= 257 else 0   # k = 505: B residues in a global scratch slot, not in TMEM
 
 
 def nout(k, e):
@@ -126,7 +126,7 @@ def combine(D, o):
     return sum(int(D[4 * o + b]) << (8 * b) for b in range(4))
 
 
-@pytest.fixture(scope="module", params=[97, 129, 257])
+@pytest.fixture(scope="module", params=[97, 129, 257, 505])
 def base(request):
     k = request.param
     flat, primes, _ = _tables(k)

@@ -129,10 +129,9 @@ def wide(torch, mr, orc, quick):
         ctx = mr.RnsContext(N, limbs)
         for ell in (17, bits):
             E = 65537 if ell == 17 else rng.getrandbits(bits) | (1 << (bits - 1))
-            # k = 129 / 257: tensor-core wide kernel, 128-message tile-jobs (2 / 1 per SM: 37,888 / 18,944 = one per
-            # tile); k = 505: IMAD wide kernel, CTAs of 16 messages (1 per SM)
-            cnt = 65536 if bits == 4096 and ell == 17 else 37888 if bits == 4096 else \
-                18944 if bits == 8192 else 4736 if ell == 17 else 2368
+            # tensor-core wide kernel: k = 129 / 257 128-message tile-jobs (2 / 1 per SM: 37,888 / 18,944 = one per
+            # tile), k = 505 64-message tile-jobs (9,472 = one per SM)
+            cnt = 65536 if bits == 4096 and ell == 17 else 37888 if bits == 4096 else 9472 if bits == 16128 else 18944
             xs = synth.messages(N, cnt, 0x5EEDC0DE, limbs)
             x = torch.from_numpy(xs.view(np.int32)).cuda()
             y = torch.empty_like(x)

@@ -25,7 +25,7 @@ def run(N, L, xs, E):
 
 
 ok_all = True
-for bits in (3072, 4096, 8192):
+for bits in (3072, 4096, 8192, 16128):
     rng = random.Random(bits)
     N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
     L = bits // 32
@@ -40,12 +40,12 @@ for bits in (3072, 4096, 8192):
         print(f"bits={bits} k={ctx.k} E.bits={E.bit_length()} ok={ok} bad={len(bad)} first_bad={bad[:5]} st_last={st[-1]} ({time.time()-t0:.1f}s)", flush=True)
 if len(sys.argv) > 1 and sys.argv[1] == "quick":
     sys.exit(0 if ok_all else 1)
-for bits, E in ((3072, 65537), (4096, 65537), (8192, 65537), (3072, None), (4096, None), (8192, None)):
+for bits, E in ((3072, 65537), (4096, 65537), (8192, 65537), (16128, 65537), (3072, None), (4096, None), (8192, None), (16128, None)):
     rng = random.Random(bits + 7)
     N = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
     L = bits // 32
     E = E or (rng.getrandbits(bits) | (1 << (bits - 1)))
-    count = 18944 if bits == 8192 else 65536 if E == 65537 else 37888   # 8192: one 128-message job per SM
+    count = 9472 if bits == 16128 else 18944 if bits == 8192 else 65536 if E == 65537 else 37888   # 8192 / 16128: one job per SM
     xs = np.ascontiguousarray(mr.ints_to_limbs([rng.randrange(N) for _ in range(256)], L))
     xs = np.tile(xs, (count // 256, 1))
     ctx = mr.RnsContext(N, L)
