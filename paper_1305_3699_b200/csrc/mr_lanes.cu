@@ -67,6 +67,15 @@ __device__ __forceinline__ void quad_sum(u32 &lo, u32 &mi, u32 &hi) {
     }
 }
 
+#ifndef MR_LANES_FRAC
+// 1: α' of BE2 and of the exit from the top bits of the ξ'_j (reading R2b, as the tensor kernels), so the
+// m_r = 2^32 channel needs no upkeep: no m_r column in BE1 (a divergent branch of one output group), no
+// Σ ξ'_j |M'_j|_{2^32} products, no r_r round trip through shared memory
+#define MR_LANES_FRAC 1
+#endif
+// α' = floor(Σ_j ξ'_j / m'_j) from s = Σ_j (ξ'_j >> 8) (exact for k <= 65 and r / M' < 0.11: reading R2b)
+__device__ __forceinline__ u32 frac_alpha(u32 s) { return (s + (1u << 14)) >> 24; }
+
 template <int K>
 struct LaneCfg {
     static constexpr int NCH = 2 * K + 1;
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                 t = mont_red((u32)ps, (u32)(ps >> 32), m, mi);
             }
             st[tid] = t;
-        } else if (tid == (u32)(2 * K)) {
+        } else if (!MR_LANES_FRAC && tid == (u32)(2 * K)) {
             const u32 a = st[tid];
             st[tid] = a * (sq ? a : __ldcg(bp + tid * bstride));
         }
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                     }
                 }
                 add96(lo, mi, hi, l1, m1, h1);
-            } else if (o == (u32)K) {
+            } else if (!MR_LANES_FRAC && o == (u32)K) {
 #pragma unroll
                 for (int t = 0; t < C::Q; t++) {
                     const u32 i = sub + 4 * t;
@@ -186,14 +195,16 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                 }
             }
             quad_sum(lo, mi, hi);
-            qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 1);
-            qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 2);
+            if (!MR_LANES_FRAC) {
+                qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 1);
+                qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 2);
+            }
             if (sub == 0 && o < (u32)K) {
                 const u32 ch = K + o, m = sm[S::mm + ch], mv = sm[S::minv + ch], r32 = sm[S::r32 + ch];
                 const u32 v = red96_mont(hi, mi, lo, m, mv, r32);          // Σ ξ A1'  (mod m'_j)
                 const u64 p = (u64)st[ch] * sm[S::xw + o];                 // t* C1 2^64
                 st[ch] = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);   // ξ'_j (lazy)
-            } else if (sub == 0 && o == (u32)K) {
+            } else if (!MR_LANES_FRAC && sub == 0 && o == (u32)K) {
                 sm[S::aux + 0] = st[2 * K] * minv32 + qr * nminv;          // r_r = (t_r + q̂_r N) M^-1
             }
         }
@@ -202,7 +213,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
         // Σ_j ξ'_j |M'_j|_{2^32} over the same j, so each group forms α' = (that sum - r_r) M'^-1 mod 2^32
         // (exact: Shenoy-Kumaresan through m_r) itself — no block reduction and no extra barrier — and adds
         // α' (m_i - |M'|_{m_i}) after the contraction.
-        const u32 rr = sm[S::aux + 0];
+        const u32 rr = MR_LANES_FRAC ? 0u : sm[S::aux + 0];
         {
             u32 lo = 0, mi = 0, hi = 0, l1 = 0, m1 = 0, h1 = 0, sa = 0;
             if (o < (u32)K) {
@@ -213,7 +224,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                         const u32 x = st[K + j];
                         if (t & 1) mac96(l1, m1, h1, x, a2row[j]);
                         else mac96(lo, mi, hi, x, a2row[j]);
-                        sa += x * sm[S::a2r + j];
+                        sa += MR_LANES_FRAC ? x >> 8 : x * sm[S::a2r + j];
                     }
                 }
                 add96(lo, mi, hi, l1, m1, h1);
@@ -222,12 +233,12 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             sa += __shfl_xor_sync(0xFFFFFFFFu, sa, 1);
             sa += __shfl_xor_sync(0xFFFFFFFFu, sa, 2);
             if (sub == 0 && o < (u32)K) {
-                const u32 alpha = (sa - rr) * minvp;
+                const u32 alpha = MR_LANES_FRAC ? frac_alpha(sa) : (sa - rr) * minvp;
                 mac96(lo, mi, hi, alpha, sm[S::pinw + o]);
                 st[o] = red96_mont(hi, mi, lo, sm[S::mm + o], sm[S::minv + o], sm[S::r32 + o]);
             }
         }
-        if (tid == 0) st[2 * K] = rr;
+        if (!MR_LANES_FRAC && tid == 0) st[2 * K] = rr;
         __syncthreads();
     };
 
@@ -280,7 +291,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
     // ---- exit (a7): X = Σ_j ξ'_j M'_j + α'(2^(32(k+1)) - M') (column sums), then X mod N
     {
         u32 part = 0;
-        if (tid < (u32)K) part = st[K + tid] * sm[S::a2r + tid];
+        if (tid < (u32)K) part = MR_LANES_FRAC ? st[K + tid] >> 8 : st[K + tid] * sm[S::a2r + tid];
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, s);
         if (lane == 0) sm[S::red + warp] = part;
@@ -288,7 +299,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
         u32 sr = 0;
 #pragma unroll
         for (int w = 0; w < C::W; w++) sr += sm[S::red + w];
-        const u32 alpha = (sr - st[2 * K]) * minvp;
+        const u32 alpha = MR_LANES_FRAC ? frac_alpha(sr) : (sr - st[2 * K]) * minvp;
         if (tid <= (u32)K) {   // column l = tid
             const u32 l = tid;
             u32 lo = 0, mi = 0, hi = 0;
