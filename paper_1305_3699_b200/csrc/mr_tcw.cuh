@@ -61,7 +61,18 @@ constexpr u32 W_HV = K > 129 ? 2u : (u32)MR_TCW_HALVES;   // k = 257: 8 compute 
 constexpr u32 W_CW = 4 * W_HV * W_TILES;              // compute warps
 constexpr u32 W_THREADS = 32 * (W_CW + 2 * W_TILES);     // + per tile a producer warp and an MMA warp (one lane each:
                                                          // two roles in one warp would sleep on each other's waits)
-constexpr u32 W_NBAR = 2 * W_NST + 3;                 // per tile: full[NST] empty[NST] accf acce aready
+constexpr u32 W_NBAR = 2 * W_NST + 3;
+#ifndef MR_TCW_FRAC
+#define MR_TCW_FRAC 1   // α' from the top bits of the ξ'_j (reading R2b) instead of the m_r channel
+#endif
+// s = Σ_j (ξ'_j >> W_FSH) stays below 2^32 (k < 2^W_FSH) and α' = (s + 2^(26 - W_FSH)) >> (32 - W_FSH): the shift drops
+// < k 2^(W_FSH - 32) and ξ'_j / 2^32 undercuts ξ'_j / m'_j by < k max c'_j / m'_j, together < 2^-6 for every tensor-wide
+// k (2^-9.5 at k = 505), while r / M' < 2^-20; pinned by tests/test_abi_host.py::test_fractional_alpha_bound_wide
+constexpr u32 W_FSH = K <= 129 ? 8u : (K <= 257 ? 9u : 10u);
+// with the m_r channel (MR_TCW_FRAC = 0) the thread that forms r_r reads A-row word k+1, which at k = 505 the other half
+// of the tile writes (16-word group 31) with no barrier in between: that variant is only valid up to k = 257
+static_assert(MR_TCW_FRAC || K <= 257, "k = 505 needs the fractional α' (MR_TCW_FRAC = 1)");
+__device__ __forceinline__ u32 w_frac_alpha(u32 s) { return (s + (1u << (26 - W_FSH))) >> (32 - W_FSH); }                 // per tile: full[NST] empty[NST] accf acce aready
 
 struct TcwArgs {
     const u32 *wtab;          // per-k wide table (mr_internal.h wide_layout): m, -m^-1, C1 2^64, |M'_j|_{2^32}
@@ -716,8 +727,8 @@ struct TcwCompute {
                                 // fits 64 bits (pinned per k by test_tcw_host.py::test_be1_epilogue_sum_fits_64_bits)
                                 const u64 p = madw(u ? tc[t] : ta[t], e1.z, ((u64)Vh[q] << 32) | Vl[q]);
                                 xp[t] = mont_red((u32)p, (u32)(p >> 32), e1.x, e1.y);
-                                if (j < K) sr += xp[t] * e1.w;
-                                if (j == K) rr = trm * minv_r + Vl[q] * nminv;   // q̂_r = Σ ξ_i |M_i|_{2^32}
+                                if (j < K) sr += MR_TCW_FRAC ? xp[t] >> W_FSH : xp[t] * e1.w;
+                                if (!MR_TCW_FRAC && j == K) rr = trm * minv_r + Vl[q] * nminv;   // q̂_r = Σ ξ_i |M_i|_{2^32}
                             }
                             if (oh < K) bst4(oh, xp[0], xp[1], xp[2], xp[3]);   // ξ'_j in place of t*_j
                         }
@@ -727,7 +738,7 @@ struct TcwCompute {
         });
         // ---- 6.6 BE2: A row = (ξ'_0 .. ξ'_{k-1}, α', r_r), α' = (Σ ξ'_j |M'_j|_{2^32} - r_r) M'^-1 exact
         const uint2 tot = exchange(sr, rr);              // (also: every ξ'_j of both halves is in TMEM)
-        const u32 alpha = (tot.x - tot.y) * mpinv_r;
+        const u32 alpha = MR_TCW_FRAC ? w_frac_alpha(tot.x) : (tot.x - tot.y) * mpinv_r;
         rr = tot.y;
 #pragma unroll 1
         for (u32 g = h; g < GW; g += W_HV) {
@@ -777,10 +788,10 @@ struct TcwCompute {
         for (u32 g = h; g < GW; g += W_HV) {
 #pragma unroll
             for (u32 t = 0; t < 16; t++)
-                if (16 * g + t < K) sr += aw(16 * g + t) * ep1[16 * g + t].w;
+                if (16 * g + t < K) sr += MR_TCW_FRAC ? aw(16 * g + t) >> W_FSH : aw(16 * g + t) * ep1[16 * g + t].w;
         }
         const uint2 tot = exchange(sr, 0u);
-        if (mine16(K / 16)) aw(K) = (tot.x - aw(K + 1)) * mpinv_r;
+        if (mine16(K / 16)) aw(K) = MR_TCW_FRAC ? w_frac_alpha(tot.x) : (tot.x - aw(K + 1)) * mpinv_r;
         a_done();
         // half 0 carries the byte-position sums into limbs group by group (the buffer is released after the chunk)
         u64 carry = 0;

@@ -430,3 +430,39 @@ def test_fractional_alpha_bound(k):
         alpha = (sum(x >> 8 for x in xs) + (1 << 14)) >> 24
         exact = sum(x * (Mp // m) for x, m in zip(xs, Bp)) - r
         assert exact % Mp == 0 and exact // Mp == alpha
+
+
+@pytest.mark.parametrize("k", [97, 129, 257, 505])
+def test_fractional_alpha_bound_wide(k):
+    """reading R2b in the tensor-core wide kernel (mr_tcw.cuh W_FSH): α' = (Σ_j (ξ'_j >> sh) + 2^(26 - sh)) >> (32 - sh)
+    with sh = 8 / 9 / 10 for k <= 129 / 257 / 505.  Exact iff the sum fits 32 bits (k < 2^sh), the approximation error
+    k (max c'_j / m'_j + 2^(sh - 32)) stays below the 2^-6 offset, and r / M' + 2^-6 < 1 for the extended values r <
+    (k+3) N of every admitted modulus; plus brute force on lazy residue vectors near the bound (exact arithmetic)."""
+    from fractions import Fraction
+    sh = 8 if k <= 129 else (9 if k <= 257 else 10)
+    assert k < (1 << sh)
+    _, primes, _ = _tables(k)
+    B, Bp = primes[:k], primes[k:]
+    M, Mp = 1, 1
+    for m in B:
+        M *= m
+    for m in Bp:
+        Mp *= m
+    err = sum(Fraction((1 << 32) - m, m) + Fraction(1, 1 << (32 - sh)) for m in Bp)
+    assert err < Fraction(1, 64)
+    nmax = min((M - 1) // (k + 2) ** 2, (Mp - 1) // (k + 2))
+    assert Fraction((k + 3) * nmax, Mp) + Fraction(1, 64) < 1
+    rng = random.Random(k)
+    for _ in range(40):
+        r = rng.randrange((k + 3) * nmax)
+        xs = []
+        for m in Bp:
+            x = r * pow(Mp // m, -1, m) % m
+            if x + m < (1 << 32) and rng.random() < 0.5:
+                x += m
+            xs.append(x)
+        s = sum(x >> sh for x in xs)
+        assert s < (1 << 32)
+        alpha = (s + (1 << (26 - sh))) >> (32 - sh)
+        exact = sum(x * (Mp // m) for x, m in zip(xs, Bp)) - r
+        assert exact % Mp == 0 and exact // Mp == alpha
