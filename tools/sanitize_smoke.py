@@ -12,6 +12,9 @@ Cases (each checks its outputs against Python's pow / the property it computes):
   imad33    RSA-1024 modexp on the IMAD-path kernel (MR_RNS_IMAD_ONLY=1), 200 messages
   drbg      Hash_DRBG generate + FIPS 140-2 health kernel
   keygen    mr_rsa_keygen_batch_drbg, 2 RSA-1024 keys
+  tcw257    8192-bit modexp on the tensor-core wide kernel (k = 257, one tile per CTA), 20 messages, 24-bit E
+  tcw505    16,128-bit modexp on the tensor-core wide kernel (k = 505, 64-message tiles), 10 messages, 24-bit E
+  lanes33   RSA-1024 modexp on the small-batch lanes kernel (k = 33, one message per CTA), 40 messages, 200-bit E
 """
 import os
 import random
@@ -83,12 +86,12 @@ elif CASE == "mr33":
     torch.cuda.synchronize()
     vv = v.cpu().tolist()
     assert all((vv[i] == mr.MR_PROBABLY_PRIME) == sympy.isprime(c) for i, c in enumerate(cands) if vv[i] != mr.MR_FACTOR)
-elif CASE == "wide97" or CASE == "imad33":
-    bits = 3072 if CASE == "wide97" else 1024
+elif CASE in ("wide97", "imad33", "tcw257", "tcw505", "lanes33"):
+    bits = {"wide97": 3072, "imad33": 1024, "tcw257": 8192, "tcw505": 16128, "lanes33": 1024}[CASE]
     n = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
-    cnt = 40 if CASE == "wide97" else 200
+    cnt = {"wide97": 40, "imad33": 200, "tcw257": 20, "tcw505": 10, "lanes33": 40}[CASE]
     xs = [rng.randrange(n) for _ in range(cnt)]
-    E = 65537 if CASE == "wide97" else rng.getrandbits(200) | 1
+    E = 65537 if CASE == "wide97" else (0xB5A3F1 if CASE.startswith("tcw") else rng.getrandbits(200) | 1)
     ctx = mr.RnsContext(n)
     x = dev(mr.ints_to_limbs(xs, bits // 32))
     y = torch.empty_like(x)
