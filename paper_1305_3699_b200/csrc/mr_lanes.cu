@@ -73,9 +73,6 @@ __device__ __forceinline__ void quad_sum(u32 &lo, u32 &mi, u32 &hi) {
 // Σ ξ'_j |M'_j|_{2^32} products, no r_r round trip through shared memory
 #define MR_LANES_FRAC 1
 #endif
-#ifndef MR_LANES_PF
-#define MR_LANES_PF 1       // 1: the next op's window-table multiplicand is loaded one op ahead
-#endif
 // α' = floor(Σ_j ξ'_j / m'_j) from s = Σ_j (ξ'_j >> 8) (exact for k <= 65 and r / M' < 0.11: reading R2b)
 __device__ __forceinline__ u32 frac_alpha(u32 s) { return (s + (1u << 14)) >> 24; }
 
@@ -158,11 +155,10 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
     const u32 *a1row = sm + S::a1 + o * K, *a2row = sm + S::a2 + o * K;
 
     // st <- st · b · M^-1 (mod N); b at bp[ch * bstride] or the state itself (sq)
-    // bpre: the channel's multiplicand when it was loaded ahead (hasb), else it is read here
-    auto mont_mul = [&](const u32 *bp, size_t bstride, bool sq, u32 bpre = 0u, bool hasb = false) {
+    auto mont_mul = [&](const u32 *bp, size_t bstride, bool sq) {
         // channel products: B: ξ_i = mont(mont(a b) σ_i 2^64); B': t*_j = mont(a* b*); m_r: a_r b_r
         if (tid < (u32)(2 * K)) {
-            const u32 a = st[tid], b = sq ? a : (hasb ? bpre : __ldcg(bp + tid * bstride));
+            const u32 a = st[tid], b = sq ? a : __ldcg(bp + tid * bstride);
             const u32 m = sm[S::mm + tid], mi = sm[S::minv + tid];
             const u64 pr = (u64)a * b;
             u32 t = mont_red((u32)pr, (u32)(pr >> 32), m, mi);
@@ -251,25 +247,10 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
     const size_t tstride = P.jobs_total, entry = (size_t)NCH * tstride;
     const u32 slot0 = sel * P.ctas0 + jl;
     u32 *xs = sm + S::xs;
-    // the next op is read one op ahead, and so is the window-table multiplicand of the next op's multiplication (unless
-    // this op stores into that slot): both L2 latencies run under this op's multiplication (MR_LANES_PF)
-    u64 nop = nops ? __ldg(prog) : 0ull;
-    u32 bcur = 0u;
-    bool hcur = false;
     for (u32 s = 0; s < nops; s++) {
-        const u64 op = nop;
-        if (s + 1 < nops) nop = __ldg(prog + s + 1);
+        const u64 op = __ldg(prog + s);
         const u32 fl = (u32)op & 0xFF, opnd = (u32)(op >> 8) & 0xFF, ld = (u32)(op >> 16) & 0xFF;
         const u32 ad = (u32)(op >> 24) & 0xFF, sto = (u32)(op >> 32) & 0xFF;
-        u32 bnext = 0u;
-        bool hnext = false;
-        if (MR_LANES_PF && s + 1 < nops) {
-            const u32 fl2 = (u32)nop & 0xFF, opnd2 = (u32)(nop >> 8) & 0xFF;
-            if (!(fl2 & OPF_NOMUL) && opnd2 < 0xF0 && !((fl & OPF_STORE) && sto == opnd2)) {
-                if (tid < (u32)(2 * K)) bnext = __ldcg(P.table + opnd2 * entry + tid * tstride + slot0);
-                hnext = true;
-            }
-        }
         if (fl & (OPF_TORNS_ALL | OPF_TORNS_LO | OPF_TORNS_HI)) {   // positional -> RNS (a2)
             const u32 off = (fl & OPF_TORNS_HI) ? P.half : 0u;
             const u32 nl = (fl & OPF_TORNS_ALL) ? P.in_limbs : P.half;
@@ -292,7 +273,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
         if (!(fl & OPF_NOMUL)) {
             if (opnd == OPND_SQ) mont_mul(nullptr, 0, true);
             else if (opnd >= 0xF0) mont_mul(cx + cx_r2(K) + (opnd - 0xF0) * NCH, 1, false);
-            else mont_mul(P.table + opnd * entry + slot0, tstride, false, bcur, hcur);
+            else mont_mul(P.table + opnd * entry + slot0, tstride, false);
         }
         if (fl & OPF_ADD) {   // channel-wise lazy modular addition (CRT entry)
             if (tid < (u32)NCH) {
@@ -305,8 +286,6 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             if (tid < (u32)NCH) P.table[sto * entry + tid * tstride + slot0] = st[tid];
             __syncthreads();
         }
-        bcur = bnext;
-        hcur = hnext;
     }
 
     // ---- exit (a7): X = Σ_j ξ'_j M'_j + α'(2^(32(k+1)) - M') (column sums), then X mod N
