@@ -466,3 +466,20 @@ def test_fractional_alpha_bound_wide(k):
         alpha = (s + (1 << (26 - sh))) >> (32 - sh)
         exact = sum(x * (Mp // m) for x, m in zip(xs, Bp)) - r
         assert exact % Mp == 0 and exact // Mp == alpha
+
+
+@pytest.mark.parametrize("k", [17, 33, 49, 65])
+def test_scaled_be1_epilogue_sum_fits_64_bits(k):
+    """the ρ-scaled BE1 epilogue (mr_kernels.cuh, MR_EPI_NOFOLD) forms t*_j (C1 c'^2)_j + V_j in one 64-bit multiply-add
+    with the byte-column sum V unfolded: t* < 2^32 (lazy), V <= (4k 255^2 + 128 255)(1 + 2^8 + 2^16 + 2^24) (the 4k
+    digit bytes plus the offset and α' columns), so the sum fits only because every per-k constant (C1 c'^2)_j =
+    C1_j 2^64 mod m'_j is far enough below 2^32 — pinned here from the base table"""
+    flat, primes, _ = _tables(k)
+    L = _layout(k)
+    Bp = primes[k:]
+    vmax = (4 * k * 255 * 255 + 128 * 255) * (1 + 2 ** 8 + 2 ** 16 + 2 ** 24)
+    for j in range(k):
+        m = Bp[j]
+        xw = int(flat[L["XW"] + j])
+        assert xw == int(flat[L["C1"] + j]) * pow(2, 64, m) % m
+        assert (2 ** 32 - 1) * xw + vmax < 2 ** 64, (k, j)
