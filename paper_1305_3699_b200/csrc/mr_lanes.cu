@@ -67,6 +67,9 @@ __device__ __forceinline__ void quad_sum(u32 &lo, u32 &mi, u32 &hi) {
     }
 }
 
+#ifndef MR_LANES_CREG
+#define MR_LANES_CREG 1     // 1: each lane keeps its 2 x ceil(k/4) base-extension coefficients in registers
+#endif
 #ifndef MR_LANES_FRAC
 // 1: α' of BE2 and of the exit from the top bits of the ξ'_j (reading R2b, as the tensor kernels), so the
 // m_r = 2^32 channel needs no upkeep: no m_r column in BE1 (a divergent branch of one output group), no
@@ -153,6 +156,16 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
     const u32 minv32 = __ldg(tab + L.misc + 0), minvp = __ldg(tab + L.misc + 1), nminv = cx[CX_NMINV_R];
     const u32 g = lane >> 2, sub = lane & 3, o = warp * 8 + g;   // this lane's output and quarter
     const u32 *a1row = sm + S::a1 + o * K, *a2row = sm + S::a2 + o * K;
+    // this lane's base-extension coefficients (inputs sub + 4 t of its output) in registers for the whole ladder
+    // (MR_LANES_CREG): the multiply-accumulate loops then read only the state from shared memory
+    u32 c1r[C::Q], c2r[C::Q];
+#pragma unroll
+    for (int t = 0; t < C::Q; t++) {
+        const u32 i = sub + 4 * t;
+        const bool in = MR_LANES_CREG && o < (u32)K && i < (u32)K;
+        c1r[t] = in ? a1row[i] : 0u;
+        c2r[t] = in ? a2row[i] : 0u;
+    }
 
     // st <- st · b · M^-1 (mod N); b at bp[ch * bstride] or the state itself (sq)
     auto mont_mul = [&](const u32 *bp, size_t bstride, bool sq) {
@@ -182,8 +195,9 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                 for (int t = 0; t < C::Q; t++) {
                     const u32 i = sub + 4 * t;
                     if (4 * t + 3 < K || i < (u32)K) {
-                        if (t & 1) mac96(l1, m1, h1, st[i], a1row[i]);
-                        else mac96(lo, mi, hi, st[i], a1row[i]);
+                        const u32 cf = MR_LANES_CREG ? c1r[t] : a1row[i];
+                        if (t & 1) mac96(l1, m1, h1, st[i], cf);
+                        else mac96(lo, mi, hi, st[i], cf);
                     }
                 }
                 add96(lo, mi, hi, l1, m1, h1);
@@ -222,8 +236,9 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                     const u32 j = sub + 4 * t;
                     if (4 * t + 3 < K || j < (u32)K) {
                         const u32 x = st[K + j];
-                        if (t & 1) mac96(l1, m1, h1, x, a2row[j]);
-                        else mac96(lo, mi, hi, x, a2row[j]);
+                        const u32 cf = MR_LANES_CREG ? c2r[t] : a2row[j];
+                        if (t & 1) mac96(l1, m1, h1, x, cf);
+                        else mac96(lo, mi, hi, x, cf);
                         sa += MR_LANES_FRAC ? x >> 8 : x * sm[S::a2r + j];
                     }
                 }
