@@ -166,17 +166,23 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
         c1r[t] = in ? a1row[i] : 0u;
         c2r[t] = in ? a2row[i] : 0u;
     }
+    // ... and the per-channel / per-output moduli and constants (shared-memory reads otherwise, every multiplication)
+    const u32 chm = tid < (u32)(2 * K) ? sm[S::mm + tid] : 1u, chmi = tid < (u32)(2 * K) ? sm[S::minv + tid] : 0u;
+    const u32 chsig = tid < (u32)K ? sm[S::sig + tid] : 0u;
+    const u32 oc = o < (u32)K ? o : 0u;
+    const u32 e1m = sm[S::mm + K + oc], e1mv = sm[S::minv + K + oc], e1r = sm[S::r32 + K + oc], e1xw = sm[S::xw + oc];
+    const u32 e2m = sm[S::mm + oc], e2mv = sm[S::minv + oc], e2r = sm[S::r32 + oc], e2pin = sm[S::pinw + oc];
 
     // st <- st · b · M^-1 (mod N); b at bp[ch * bstride] or the state itself (sq)
     auto mont_mul = [&](const u32 *bp, size_t bstride, bool sq) {
         // channel products: B: ξ_i = mont(mont(a b) σ_i 2^64); B': t*_j = mont(a* b*); m_r: a_r b_r
         if (tid < (u32)(2 * K)) {
             const u32 a = st[tid], b = sq ? a : __ldcg(bp + tid * bstride);
-            const u32 m = sm[S::mm + tid], mi = sm[S::minv + tid];
+            const u32 m = MR_LANES_CREG ? chm : sm[S::mm + tid], mi = MR_LANES_CREG ? chmi : sm[S::minv + tid];
             const u64 pr = (u64)a * b;
             u32 t = mont_red((u32)pr, (u32)(pr >> 32), m, mi);
             if (tid < (u32)K) {
-                const u64 ps = (u64)t * sm[S::sig + tid];
+                const u64 ps = (u64)t * (MR_LANES_CREG ? chsig : sm[S::sig + tid]);
                 t = mont_red((u32)ps, (u32)(ps >> 32), m, mi);
             }
             st[tid] = t;
@@ -214,9 +220,11 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                 qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 2);
             }
             if (sub == 0 && o < (u32)K) {
-                const u32 ch = K + o, m = sm[S::mm + ch], mv = sm[S::minv + ch], r32 = sm[S::r32 + ch];
+                const u32 ch = K + o;
+                const u32 m = MR_LANES_CREG ? e1m : sm[S::mm + ch], mv = MR_LANES_CREG ? e1mv : sm[S::minv + ch];
+                const u32 r32 = MR_LANES_CREG ? e1r : sm[S::r32 + ch];
                 const u32 v = red96_mont(hi, mi, lo, m, mv, r32);          // Σ ξ A1'  (mod m'_j)
-                const u64 p = (u64)st[ch] * sm[S::xw + o];                 // t* C1 2^64
+                const u64 p = (u64)st[ch] * (MR_LANES_CREG ? e1xw : sm[S::xw + o]);   // t* C1 2^64
                 st[ch] = addmod_lazy(mont_red((u32)p, (u32)(p >> 32), m, mv), v, r32);   // ξ'_j (lazy)
             } else if (!MR_LANES_FRAC && sub == 0 && o == (u32)K) {
                 sm[S::aux + 0] = st[2 * K] * minv32 + qr * nminv;          // r_r = (t_r + q̂_r N) M^-1
@@ -249,8 +257,9 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             sa += __shfl_xor_sync(0xFFFFFFFFu, sa, 2);
             if (sub == 0 && o < (u32)K) {
                 const u32 alpha = MR_LANES_FRAC ? frac_alpha(sa) : (sa - rr) * minvp;
-                mac96(lo, mi, hi, alpha, sm[S::pinw + o]);
-                st[o] = red96_mont(hi, mi, lo, sm[S::mm + o], sm[S::minv + o], sm[S::r32 + o]);
+                mac96(lo, mi, hi, alpha, MR_LANES_CREG ? e2pin : sm[S::pinw + o]);
+                st[o] = MR_LANES_CREG ? red96_mont(hi, mi, lo, e2m, e2mv, e2r)
+                                      : red96_mont(hi, mi, lo, sm[S::mm + o], sm[S::minv + o], sm[S::r32 + o]);
             }
         }
         if (!MR_LANES_FRAC && tid == 0) st[2 * K] = rr;
