@@ -4,7 +4,7 @@
 // each tile then runs at the latency of one Montgomery multiplication chain (~3.3 µs per multiplication).
 // This kernel maps ONE message to a CTA and its RNS channels to threads — the paper's own mapping ("channels
 // are directly mapped onto threads", §3.1) — so a 256-message batch occupies 256 CTAs, and splits every
-// base-extension output over FOUR lanes (each lane sums every fourth input, two 96-bit shuffle adds combine
+// base-extension output over MR_LANES_LPO = 4 lanes (each lane sums every LPO-th input, log2(LPO) 96-bit shuffle adds combine
 // them), so the critical path of a multiplication is ~k/4 multiply-accumulates instead of k:
 //   channel products   thread per channel (2k+1 <= threads)
 //   BE1 (6.3-6.5)      output j in B' ∪ {m_r}: lanes 4j..4j+3 of the CTA, Σ_i ξ_i A1'[j][i]
@@ -57,10 +57,13 @@ __device__ __forceinline__ u32 red96_mont(u32 hi, u32 mid, u32 lo, u32 m, u32 mi
     const u32 s = r + t;
     return s < r ? s + r32 : s;
 }
-// 96-bit sum over the 4 lanes of an output group (lanes 4g .. 4g+3 of a warp)
+#ifndef MR_LANES_LPO
+#define MR_LANES_LPO 4      // lanes per base-extension output (4 or 8; A/B: 8 is 15 % slower on C1, profiles/r2aj)
+#endif
+// 96-bit sum over the MR_LANES_LPO lanes of an output group (lanes LPO g .. LPO g + LPO - 1 of a warp)
 __device__ __forceinline__ void quad_sum(u32 &lo, u32 &mi, u32 &hi) {
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
+    for (int o = 1; o < MR_LANES_LPO; o <<= 1) {
         const u32 l2 = __shfl_xor_sync(0xFFFFFFFFu, lo, o), m2 = __shfl_xor_sync(0xFFFFFFFFu, mi, o);
         const u32 h2 = __shfl_xor_sync(0xFFFFFFFFu, hi, o);
         add96(lo, mi, hi, l2, m2, h2);
@@ -82,9 +85,11 @@ __device__ __forceinline__ u32 frac_alpha(u32 s) { return (s + (1u << 14)) >> 24
 template <int K>
 struct LaneCfg {
     static constexpr int NCH = 2 * K + 1;
-    static constexpr int W = (K + 1 + 7) / 8;       // warps: 8 outputs of 4 lanes each
+    static constexpr int LPO = MR_LANES_LPO;          // lanes per output
+    static constexpr int OPW = 32 / LPO;              // outputs per warp
+    static constexpr int W = (K + 1 + OPW - 1) / OPW; // warps
     static constexpr int NT = 32 * W;
-    static constexpr int Q = (K + 3) / 4;           // inputs per lane (the last lanes may have one fewer)
+    static constexpr int Q = (K + LPO - 1) / LPO;     // inputs per lane (the last lanes may have one fewer)
     static_assert(NT >= NCH, "one thread per channel");
 };
 
@@ -102,7 +107,7 @@ struct LaneSmem {
     static constexpr u32 a2r = xw + K;                       // [k]  |M'_j|_{2^32}
     static constexpr u32 pinw = a2r + K;                     // [k]  (m_i - |M'|_{m_i}) 2^32
     static constexpr u32 red = pinw + K;                     // [W]  warp partials
-    static constexpr u32 aux = red + 16;                     // [4]  r_r, α', misc
+    static constexpr u32 aux = red + 32;                     // [4]  r_r, α', misc
     static constexpr u32 xs = aux + 4;                       // [2k+2] staged input limbs / exit scratch
     static constexpr u32 words = xs + 3 * (K + 1) + 4;       // exit: 3 words per column
 };
@@ -154,14 +159,14 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
     __syncthreads();
     const bool ok = ok_s;
     const u32 minv32 = __ldg(tab + L.misc + 0), minvp = __ldg(tab + L.misc + 1), nminv = cx[CX_NMINV_R];
-    const u32 g = lane >> 2, sub = lane & 3, o = warp * 8 + g;   // this lane's output and quarter
+    const u32 g = lane / C::LPO, sub = lane % C::LPO, o = warp * C::OPW + g;   // this lane's output and share
     const u32 *a1row = sm + S::a1 + o * K, *a2row = sm + S::a2 + o * K;
-    // this lane's base-extension coefficients (inputs sub + 4 t of its output) in registers for the whole ladder
+    // this lane's base-extension coefficients (inputs sub + LPO t of its output) in registers for the whole ladder
     // (MR_LANES_CREG): the multiply-accumulate loops then read only the state from shared memory
     u32 c1r[C::Q], c2r[C::Q];
 #pragma unroll
     for (int t = 0; t < C::Q; t++) {
-        const u32 i = sub + 4 * t;
+        const u32 i = sub + C::LPO * t;
         const bool in = MR_LANES_CREG && o < (u32)K && i < (u32)K;
         c1r[t] = in ? a1row[i] : 0u;
         c2r[t] = in ? a2row[i] : 0u;
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             st[tid] = a * (sq ? a : __ldcg(bp + tid * bstride));
         }
         __syncthreads();
-        // BE1: output o (o < K: B' channel; o = K: the m_r column), lanes split the inputs i = sub + 4 t over two
+        // BE1: output o (o < K: B' channel; o = K: the m_r column), lanes split the inputs i = sub + LPO t over two
         // accumulator chains.  The shuffles run on every lane (groups past the last output sum zeros), so they
         // stay convergent.
         {
@@ -199,8 +204,8 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             if (o < (u32)K) {
 #pragma unroll
                 for (int t = 0; t < C::Q; t++) {
-                    const u32 i = sub + 4 * t;
-                    if (4 * t + 3 < K || i < (u32)K) {
+                    const u32 i = sub + C::LPO * t;
+                    if (C::LPO * t + C::LPO - 1 < K || i < (u32)K) {
                         const u32 cf = MR_LANES_CREG ? c1r[t] : a1row[i];
                         if (t & 1) mac96(l1, m1, h1, st[i], cf);
                         else mac96(lo, mi, hi, st[i], cf);
@@ -210,14 +215,14 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             } else if (!MR_LANES_FRAC && o == (u32)K) {
 #pragma unroll
                 for (int t = 0; t < C::Q; t++) {
-                    const u32 i = sub + 4 * t;
-                    if (4 * t + 3 < K || i < (u32)K) qr += st[i] * a1row[i];
+                    const u32 i = sub + C::LPO * t;
+                    if (C::LPO * t + C::LPO - 1 < K || i < (u32)K) qr += st[i] * a1row[i];
                 }
             }
             quad_sum(lo, mi, hi);
             if (!MR_LANES_FRAC) {
-                qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 1);
-                qr += __shfl_xor_sync(0xFFFFFFFFu, qr, 2);
+#pragma unroll
+                for (int sh = 1; sh < C::LPO; sh <<= 1) qr += __shfl_xor_sync(0xFFFFFFFFu, qr, sh);
             }
             if (sub == 0 && o < (u32)K) {
                 const u32 ch = K + o;
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             }
         }
         __syncthreads();
-        // BE2: output o < K of B, lanes split the inputs j = sub + 4 t.  Every group also sums its share of
+        // BE2: output o < K of B, lanes split the inputs j = sub + LPO t.  Every group also sums its share of
         // Σ_j ξ'_j |M'_j|_{2^32} over the same j, so each group forms α' = (that sum - r_r) M'^-1 mod 2^32
         // (exact: Shenoy-Kumaresan through m_r) itself — no block reduction and no extra barrier — and adds
         // α' (m_i - |M'|_{m_i}) after the contraction.
@@ -241,8 +246,8 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             if (o < (u32)K) {
 #pragma unroll
                 for (int t = 0; t < C::Q; t++) {
-                    const u32 j = sub + 4 * t;
-                    if (4 * t + 3 < K || j < (u32)K) {
+                    const u32 j = sub + C::LPO * t;
+                    if (C::LPO * t + C::LPO - 1 < K || j < (u32)K) {
                         const u32 x = st[K + j];
                         const u32 cf = MR_LANES_CREG ? c2r[t] : a2row[j];
                         if (t & 1) mac96(l1, m1, h1, x, cf);
@@ -253,8 +258,8 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
                 add96(lo, mi, hi, l1, m1, h1);
             }
             quad_sum(lo, mi, hi);
-            sa += __shfl_xor_sync(0xFFFFFFFFu, sa, 1);
-            sa += __shfl_xor_sync(0xFFFFFFFFu, sa, 2);
+#pragma unroll
+            for (int sh = 1; sh < C::LPO; sh <<= 1) sa += __shfl_xor_sync(0xFFFFFFFFu, sa, sh);
             if (sub == 0 && o < (u32)K) {
                 const u32 alpha = MR_LANES_FRAC ? frac_alpha(sa) : (sa - rr) * minvp;
                 mac96(lo, mi, hi, alpha, MR_LANES_CREG ? e2pin : sm[S::pinw + o]);
