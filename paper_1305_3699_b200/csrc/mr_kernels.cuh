@@ -626,7 +626,10 @@ constexpr bool tc_fits(int tiles) {
     return tc_smem_for(tiles) <= 232448 && ((u32)tiles * TCNP <= 512 || (MR_TC_SLOTS && !PAIR && tiles <= 4));
 }
 // tiles per CTA: as many as fit the 227 KB of shared memory and the 512 TMEM columns (at most 4)
-constexpr int TCT = tc_fits(4) ? 4 : (tc_fits(3) ? 3 : (tc_fits(2) ? 2 : 1));
+#ifndef MR_TCT_MAX
+#define MR_TCT_MAX 4        // A/B hook: cap on the tiles per CTA of the modexp tensor kernel
+#endif
+constexpr int TCT = (MR_TCT_MAX >= 4 && tc_fits(4)) ? 4 : ((MR_TCT_MAX >= 3 && tc_fits(3)) ? 3 : (tc_fits(2) ? 2 : 1));
 static_assert(tc_smem_for(TCT) <= 232448, "tensor-core tile does not fit shared memory");
 constexpr u32 TC_M = PAIR ? 256u : 128u;
 constexpr u32 TC_IDESC = (2u << 4) | ((TCNP >> 3) << 17) | ((TC_M >> 4) << 24);  // s32 = u8 x u8, K-major
