@@ -1108,15 +1108,17 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_modexp_tcw(const ModexpParams 
 // host side of one launch (both the per-k TUs and mr_tcw257.cu): shared-memory attribute once per process, 2-CTA
 // clusters in pair mode (ctas even)
 int tcw_launch(const ModexpParams &p, u32 ctas, const TcwArgs &a, void *stream) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};                        // the attribute is per device: set once on each
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 6;
+    if (!attr[dev]) {
         const cudaError_t e = cudaFuncSetAttribute((const void *)k_modexp_tcw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)W_SMEM);
         if (e != cudaSuccess) {
             if (getenv("MR_RNS_DEBUG")) fprintf(stderr, "k_modexp_tcw<%d> smem %zu: %s\n", K, (size_t)W_SMEM, cudaGetErrorString(e));
             return 6;
         }
-        attr = true;
+        attr[dev] = true;
     }
     TcwArgs aa = a;
     ModexpParams pp = p;
