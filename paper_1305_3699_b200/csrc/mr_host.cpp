@@ -958,7 +958,9 @@ static int table_cost(int w) { return w > 1 ? (1 << (w - 1)) : 0; }
 
 static int best_window(const Big &E) {
     int best = 1, bestc = 1 << 30;
-    for (int w = 1; w <= 7; w++) {
+    // MR_RNS_WMAX=w: cap the sliding window (A/B hook: a smaller window table stays in L2 longer)
+    static const int wmax = [] { const char *e = getenv("MR_RNS_WMAX"); const int v = e ? atoi(e) : 7; return v < 1 ? 1 : (v > 7 ? 7 : v); }();
+    for (int w = 1; w <= wmax; w++) {
         int c = table_cost(w) + sliding_ops(E, w, nullptr);
         if (c < bestc) bestc = c, best = w;
     }
