@@ -62,6 +62,12 @@ constexpr u32 W_CW = 4 * W_HV * W_TILES;              // compute warps
 constexpr u32 W_THREADS = 32 * (W_CW + 2 * W_TILES);     // + per tile a producer warp and an MMA warp (one lane each:
                                                          // two roles in one warp would sleep on each other's waits)
 constexpr u32 W_NBAR = 2 * W_NST + 3;
+#ifndef MR_TCW_CMPTOP
+#define MR_TCW_CMPTOP 1 // exit: compare X with N 2^s from the top limb (usually one limb) before a full subtraction pass
+#endif
+#ifndef MR_TCW_VEC
+#define MR_TCW_VEC 1    // 16-byte loads of the input rows in to_rns and 16-byte stores of the output rows
+#endif
 #ifndef MR_TCW_FRAC
 #define MR_TCW_FRAC 1   // α' from the top bits of the ξ'_j (reading R2b) instead of the m_r channel
 #endif
@@ -519,9 +525,14 @@ struct TcwCompute {
     // a2: positional -> RNS of nl limbs at x (masked to zero when !ok); B -> TMEM, B' -> the A row (parked in the
     // window table's spare slot `park` while the chunks still read the limbs), m_r = x_0 -> word k+1
     __device__ void to_rns(const u32 *x, u32 nl, bool ok, u32 *park, size_t tstride) {
+        const bool vec = (nl & 3u) == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0;   // row of whole uint4 groups
 #pragma unroll 1
         for (u32 w = 0; w < W_KC; w++) {
             if (!mine16(w / 4)) continue;
+            if (MR_TCW_VEC && vec) {                  // whole 16-byte limb groups: one vector load each
+                ac(w) = (ok && 4 * w < nl) ? __ldg(reinterpret_cast<const uint4 *>(x) + w) : make_uint4(0u, 0u, 0u, 0u);
+                continue;
+            }
             u32 q[4];
 #pragma unroll
             for (int t = 0; t < 4; t++) q[t] = (ok && 4 * w + t < nl) ? __ldg(x + 4 * w + t) : 0u;
@@ -834,6 +845,24 @@ struct TcwCompute {
         const u32 *nl = cx + cx_n(K);
 #pragma unroll 1
         for (int s = SMAX; s >= 0; s--) {
+            if (MR_TCW_CMPTOP) {   // X >= N 2^s ? from the most significant limb down: the first difference decides
+                int cmp = 0;
+#pragma unroll 1
+                for (int l = K; l >= 0 && cmp == 0; l--) {
+                    const u32 nsh = __funnelshift_l(l ? __ldg(nl + l - 1) : 0u, __ldg(nl + l), s), xv = aw(l);
+                    cmp = xv > nsh ? 1 : (xv < nsh ? -1 : 0);
+                }
+                if (cmp < 0) continue;
+                u32 brw = 0;
+#pragma unroll 4
+                for (u32 l = 0; l <= K; l++) {
+                    const u32 nsh = __funnelshift_l(l ? __ldg(nl + l - 1) : 0u, __ldg(nl + l), s);
+                    const u64 t = (u64)aw(l) - nsh - brw;
+                    aw(l) = (u32)t;
+                    brw = (u32)(t >> 63);
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int pass = 0; pass < 2; pass++) {   // pass 0: borrow of X - N 2^s; pass 1: subtract
                 u32 brw = 0;
@@ -947,7 +976,13 @@ struct TcwCompute {
         if (valid && h == 0) {
             u32 *yrow = P.y + sel * P.out_stride + (size_t)jl * P.out_limbs;
 #pragma unroll 1
-            for (u32 l = 0; l < P.out_limbs; l++) yrow[l] = ok ? aw(l) : 0u;
+            if (MR_TCW_VEC && (P.out_limbs & 3u) == 0 && (reinterpret_cast<uintptr_t>(yrow) & 15u) == 0) {
+#pragma unroll 1
+                for (u32 w = 0; w < P.out_limbs / 4; w++)   // the A row's K-core w holds limbs 4w .. 4w+3
+                    reinterpret_cast<uint4 *>(yrow)[w] = ok ? ac(w) : make_uint4(0u, 0u, 0u, 0u);
+            } else {
+                for (u32 l = 0; l < P.out_limbs; l++) yrow[l] = ok ? aw(l) : 0u;
+            }
         }
         sync();                                           // the A row is free for the next job
     }
