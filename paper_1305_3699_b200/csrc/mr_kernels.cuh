@@ -430,17 +430,22 @@ __device__ __forceinline__ void from_rns(STT st, const CS &cs, const u32 *__rest
     }
 #pragma unroll 1
     for (int s = SMAX; s >= 0; s--) {
+        // X >= N·2^s ?  compared from the most significant limb down (the first difference decides, usually at
+        // once), then one subtraction pass; same decisions as a full borrow pass
+        int cmp = 0;
 #pragma unroll 1
-        for (int pass = 0; pass < 2; pass++) {   // pass 0: borrow of X - N·2^s; pass 1: subtract
-            u32 br = 0;
+        for (int l = K; l >= 0 && cmp == 0; l--) {
+            const u32 nsh = __funnelshift_l(l ? cs.nlimb(l - 1) : 0u, cs.nlimb(l), s), xv = S(st, l);
+            cmp = xv > nsh ? 1 : (xv < nsh ? -1 : 0);
+        }
+        if (cmp < 0) continue;
+        u32 br = 0;
 #pragma unroll 1
-            for (int l = 0; l <= K; l++) {
-                const u32 nsh = __funnelshift_l(l ? cs.nlimb(l - 1) : 0u, cs.nlimb(l), s);
-                const u64 t = (u64)S(st, l) - nsh - br;
-                if (pass) S(st, l) = (u32)t;
-                br = (u32)(t >> 63);
-            }
-            if (br) break;
+        for (int l = 0; l <= K; l++) {
+            const u32 nsh = __funnelshift_l(l ? cs.nlimb(l - 1) : 0u, cs.nlimb(l), s);
+            const u64 t = (u64)S(st, l) - nsh - br;
+            S(st, l) = (u32)t;
+            br = (u32)(t >> 63);
         }
     }
 }

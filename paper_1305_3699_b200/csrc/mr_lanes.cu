@@ -350,16 +350,20 @@ __global__ void __launch_bounds__(LaneCfg<K>::NT) k_modexp_lane(const ModexpPara
             const u32 *nl = cx + cx_n(K);
             const int smax = (int)(32 - __clz(K + 2)) - 1;   // X < (k+3) N <= 2^(smax+1) N
             for (int s = smax; s >= 0; s--) {
-                for (int pass = 0; pass < 2; pass++) {
-                    u32 br = 0;
-                    for (u32 l = 0; l <= (u32)K; l++) {
-                        const u32 nlo = l ? nl[l - 1] : 0u, nhi = l < (u32)K ? nl[l] : 0u;
-                        const u32 nsh = s ? __funnelshift_l(nlo, nhi, s) : nhi;
-                        const u64 t = (u64)X[l] - nsh - br;
-                        if (pass) X[l] = (u32)t;
-                        br = (u32)(t >> 63);
-                    }
-                    if (br) break;
+                int cmp = 0;   // X >= N 2^s ? from the top limb down, then one subtraction pass
+                for (int l = K; l >= 0 && cmp == 0; l--) {
+                    const u32 nlo = l ? nl[l - 1] : 0u, nhi = l < K ? nl[l] : 0u;
+                    const u32 nsh = s ? __funnelshift_l(nlo, nhi, s) : nhi;
+                    cmp = X[l] > nsh ? 1 : (X[l] < nsh ? -1 : 0);
+                }
+                if (cmp < 0) continue;
+                u32 br = 0;
+                for (u32 l = 0; l <= (u32)K; l++) {
+                    const u32 nlo = l ? nl[l - 1] : 0u, nhi = l < (u32)K ? nl[l] : 0u;
+                    const u32 nsh = s ? __funnelshift_l(nlo, nhi, s) : nhi;
+                    const u64 t = (u64)X[l] - nsh - br;
+                    X[l] = (u32)t;
+                    br = (u32)(t >> 63);
                 }
             }
         }
